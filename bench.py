@@ -1,0 +1,465 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark of the B200 par_loop hot path.
+
+Workload (BASELINE.json configs[1], the metric's config): P1 Laplace stiffness
+matrix assembly into CSR on the unit square 1024^2 mesh (2,097,152 cells,
+1,050,625 vertices, jitter 0.2h seed 2, cell permutation seed 3).  A step is
+one par_loop execute(stiffness_p1_tri; Mat INC (cell_vertex, cell_vertex),
+coordinates READ) into a freshly zero-initialised Mat whose sparsity was built
+once beforehand (assemble_matrix without its build_sparsity: the
+sparsity build is reported separately).  Inputs are resident in HBM; L2 is
+flushed (a 512 MiB write) before every timed step.  Each step is timed with
+CUDA events on the launching stream; N>1 runs N independent replicas (one
+rank per GPU, weak scaling) and takes the max over ranks.
+
+  value      assembled cells/s (whole job)
+  e2e        same metric through loam_gpu_execute_host (the reference calling
+             convention, host buffers): H2D of maps/pattern/coordinates and
+             D2H of the values inside the timed region
+  roofline   minimal algorithmic bytes (map int32 + coords fp64 + values fp64
+             written once) / kernel time vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the reference's own par_loop (oracle/_ref: loam::execute with
+             the reference's optimised AST kernel, all host threads) on a
+             bounded sample of the same workload (256^2 mesh, same generator)
+
+--impl reference runs only the reference CPU arm (rank 0) and prints its line.
+--all-configs (developer) prints one line per config/strategy for profiles/.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "assembled cells/s + achieved HBM GB/s vs peak for P1/P2 residual & CSR matrix"
+UNIT = "cells/s"
+WORKLOAD = "C2: P1 Laplace stiffness CSR assembly, unit square 1024x1024 (2,097,152 cells)"
+REF_SAMPLE_N = 256  # reference CPU arm: 131,072-cell mesh of the same generator
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(tag):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(tag, {}).get("dram_bytes")
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML while the GPU works."""
+
+    REASONS = {
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
+    }
+
+    def __init__(self, index=0, period=0.005):
+        self.samples, self.reasons, self.period = [], set(), period
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                util = nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                if util > 0:
+                    self.samples.append(mhz)
+                    for bit, name in self.REASONS.items():
+                        if r & bit:
+                            self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples_under_load": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- helpers
+def algorithmic_bytes(w):
+    """Minimal bytes: every map entry once (int32), unique inputs once
+    and outputs written once (fp64)."""
+    m = w.inputs
+    cfg = w.cfg
+    if cfg == 1:
+        return m.ncells * 3 * 4 + m.nv * 2 * 8 + m.nv * 8 + m.nv * 8
+    if cfg == 2:
+        return m.ncells * 3 * 4 + m.nv * 2 * 8 + w.outputs[0].sparsity.nnz * 8
+    if cfg == 3:
+        nn = m.extra["nn"]
+        b = m.ncells * 10 * 4 + m.nv * 3 * 8
+        if w.part == "residual":
+            return b + 2 * nn * 8
+        return b + w.outputs[0].sparsity.nnz * 8
+    if cfg == 4:
+        return m.ncells * 4 * 4 + m.nv * 3 * 8 + w.outputs[0].sparsity.nnz * 8
+    if cfg == 5:
+        return m.ncells * (6 + 3) * 4 + m.nv * 2 * 8 + sum(o.sparsity.nnz for o in w.outputs) * 8
+    raise ValueError(cfg)
+
+
+class Flusher:
+    def __init__(self, torch):
+        self.buf = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+        self.v = 0
+
+    def __call__(self):
+        self.v = (self.v + 1) & 0xFF
+        self.buf.fill_(self.v)
+
+
+def time_steps(torch, w, steps, flush, stream):
+    """Per-step device time (ms) with L2 flushed before each step."""
+    times = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(steps):
+        w.reset()
+        flush()
+        e0.record(stream)
+        w.run()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    return times
+
+
+def e2e_host(torch, w, steps, warmup):
+    """The same assembly through loam_gpu_execute_host with pinned host buffers."""
+    from paper_1501_01809_b200 import capi
+    from paper_1501_01809_b200 import loam as L
+    lib = capi.lib()
+    loops = w.loops
+    pinned = {}
+
+    def pin(arr):
+        t = torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
+        pinned[id(t)] = t
+        return t
+
+    h2d = d2h = 0
+    host_loops = []
+    seen = set()
+    for lp in loops:
+        kd, descs, keep = L._build(lp)
+        hdescs = (capi.ArgDesc * len(lp.args))()
+        mkeep = []
+        for k, a in enumerate(lp.args):
+            d = capi.ArgDesc()
+            C.memmove(C.byref(d), C.byref(descs[k]), C.sizeof(d))
+            if a.dat is not None:
+                t = pin(a.dat.view())
+                d.data = t.data_ptr()
+                if a.access != L.READ:
+                    d.flags = capi.ARG_ZERO if a.access == L.INC else 0  # fresh assemble_vector output
+                    d2h += t.numel() * 8
+                else:
+                    h2d += t.numel() * 8
+            elif a.mat is not None:
+                t = pin(np.zeros(a.mat.sparsity.nnz))
+                d.data = t.data_ptr()
+                d.flags = capi.ARG_ZERO
+                d2h += t.numel() * 8
+                sp = capi.SparsityDesc()
+                C.memmove(C.byref(sp), C.byref(a.mat.sparsity.desc()), C.sizeof(sp))
+                rp, ci = a.mat.sparsity.host()
+                trp, tci = pin(rp), pin(ci)
+                sp.row_ptr, sp.col_idx = trp.data_ptr(), tci.data_ptr()
+                if ("sp", a.mat.sparsity.id) not in seen:
+                    h2d += trp.numel() * 8 + tci.numel() * 4
+                    seen.add(("sp", a.mat.sparsity.id))
+                mkeep.append(sp)
+                d.sparsity = C.pointer(sp)
+            for fld, mp in (("map", a.maps[0] if a.maps else None), ("col_map", a.maps[1] if len(a.maps) > 1 else None)):
+                if mp is None:
+                    continue
+                md = capi.MapDesc()
+                C.memmove(C.byref(md), C.byref(mp.desc()), C.sizeof(md))
+                tv = pin(mp.values)
+                md.values = tv.data_ptr()
+                if ("map", mp.id) not in seen:
+                    h2d += tv.numel() * 4
+                    seen.add(("map", mp.id))
+                if mp.node_map is not None:
+                    tn = pin(mp.node_map.values)
+                    md.node_values = tn.data_ptr()
+                    if ("map", mp.node_map.id) not in seen:
+                        h2d += tn.numel() * 4
+                        seen.add(("map", mp.node_map.id))
+                mkeep.append(md)
+                setattr(d, fld, C.pointer(md))
+            hdescs[k] = d
+        host_loops.append((kd, hdescs, keep, mkeep, lp))
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    def run():
+        for kd, hd, _, _, lp in host_loops:
+            capi.check(lib.loam_gpu_execute_host(C.byref(kd), lp.iterset.size, lp.iterset.id, hd, len(lp.args), sh))
+
+    for _ in range(warmup):
+        run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for _ in range(steps):
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    return times, h2d, d2h
+
+
+def reference_sample(threads, warmup, steps, n=REF_SAMPLE_N):
+    """The reference's own par_loop on the host cores (oracle/_ref)."""
+    import oracle as O
+    from paper_1501_01809_b200 import configs
+    m = configs.config_inputs(2, n)
+    times = O.ref_time_execute(O.STIFFNESS, 1, 2, m.cv, m.coords, as_shipped=True, threads=threads,
+                               warmup=warmup, steps=steps)
+    return m.ncells, times
+
+
+# --------------------------------------------------------------------------- arms
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    steps = max(1, min(args.steps, 3))
+    ncells, times = reference_sample(threads, min(args.warmup, 1), steps)
+    value = ncells / min(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * float(np.mean(times)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "sample_cells": ncells},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"loam::execute(optimised AST stiffness_p1_tri) on the {REF_SAMPLE_N}^2 "
+                                   f"mesh ({ncells} cells) of the same generator, min of {steps}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def gpu_arm(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    from paper_1501_01809_b200 import capi, configs
+    lib = capi.lib()
+    assert lib.loam_gpu_device_ok() == 1, "no sm_100 device"
+    capi.set_strategy(args.strategy)
+
+    w = configs.Workload(2, None)
+    stream = torch.cuda.current_stream()
+    flush = Flusher(torch)
+    # plan build (colour/pair/slot plans are cached like the reference's colouring)
+    t0 = time.perf_counter()
+    w.reset()
+    w.run()
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - t0
+    clocks = ClockSampler(local)
+    with clocks:
+        for _ in range(max(args.warmup, 3)):
+            w.reset()
+            flush()
+            w.run()
+        soak_end = time.perf_counter() + 0.3  # keep the GPU busy so NVML sees load
+        while time.perf_counter() < soak_end:
+            w.reset()
+            w.run()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        l0 = capi.launch_count()
+        times = time_steps(torch, w, args.steps, flush, stream)
+        launches = capi.launch_count() - l0
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+    ms = float(np.mean(times))
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    cells = w.inputs.ncells
+    value = world * cells / (ms * 1e-3)
+    abytes = algorithmic_bytes(w)
+    peak, peak_kind = peaks()
+    kernel_ms = float(np.median(times))
+    achieved = abytes / (kernel_ms * 1e-3) / 1e9
+    # end to end through the C ABI with host buffers
+    e2e_times, h2d, d2h = e2e_host(torch, w, max(2, min(args.steps, 5)), 1)
+    e2e_ms = float(np.mean(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    # correctness spot check of this very run against the reference pattern size
+    line = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            try:
+                threads = os.cpu_count() or 1
+                ncells_s, ct = reference_sample(threads, 1, 2)
+                cpu = {"value": ncells_s / min(ct), "unit": UNIT, "cores": threads, "kind": "reference",
+                       "sample": f"oracle/_ref loam::execute (optimised AST stiffness_p1_tri) on the "
+                                 f"{REF_SAMPLE_N}^2 mesh of the same generator ({ncells_s} cells), min of 2"}
+            except Exception as exc:  # noqa: BLE001
+                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                       "sample": f"unavailable: {exc}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "cells": cells, "vertices": w.inputs.nv,
+                       "nnz": w.outputs[0].sparsity.nnz, "l2": "flushed (512 MiB write) before every step",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "strategy": args.strategy, "plan_build_s": round(plan_s, 4)},
+            "e2e": {"value": world * cells / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic("c2_matrix"),
+                         "algorithmic_bytes": abytes, "kernel_ms": kernel_ms, "peak_kind": peak_kind},
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def all_configs(args):
+    """Developer table: every config x strategy (not the contract line)."""
+    import torch
+    torch.cuda.set_device(0)
+    from paper_1501_01809_b200 import capi, configs
+    peak, _ = peaks()
+    flush = Flusher(torch)
+    stream = torch.cuda.current_stream()
+    rows = []
+    cases = [(1, None), (2, None), (3, "residual"), (3, "matrix"), (4, None), (5, None)]
+    if args.configs:
+        want = set(args.configs.split(","))
+        cases = [c for c in cases if f"{c[0]}{'' if c[1] is None else c[1][0]}" in want or str(c[0]) in want]
+    for cfg, part in cases:
+        w = configs.Workload(cfg, args.size, part)
+        for strat in args.strategies.split(","):
+            capi.set_strategy(strat)
+            try:
+                t0 = time.perf_counter()
+                w.reset()
+                w.run()
+                torch.cuda.synchronize()
+                plan = time.perf_counter() - t0
+                for _ in range(3):
+                    w.reset()
+                    flush()
+                    w.run()
+                l0 = capi.launch_count()
+                times = time_steps(torch, w, args.steps, flush, stream)
+                launches = (capi.launch_count() - l0) / args.steps
+                ms = float(np.median(times))
+                ab = algorithmic_bytes(w)
+                rows.append({"config": cfg, "part": part, "strategy": strat, "cells": w.inputs.ncells,
+                             "ms": ms, "cells_per_s": w.inputs.ncells / (ms * 1e-3),
+                             "algorithmic_MB": ab / 1e6, "GB_s": ab / (ms * 1e-3) / 1e9,
+                             "frac_of_measured_peak": ab / (ms * 1e-3) / 1e9 / peak,
+                             "launches_per_step": launches, "first_call_s": plan})
+            except Exception as exc:  # noqa: BLE001
+                rows.append({"config": cfg, "part": part, "strategy": strat, "error": str(exc)})
+            print(json.dumps(rows[-1]), flush=True)
+        del w
+        torch.cuda.empty_cache()
+    capi.set_strategy("auto")
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="loam_gpu", choices=["loam_gpu", "reference"])
+    ap.add_argument("--strategy", default="auto", choices=["auto", "owner", "atomic", "color"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--all-configs", action="store_true")
+    ap.add_argument("--configs", default="")
+    ap.add_argument("--strategies", default="owner,atomic,color")
+    ap.add_argument("--size", type=int, default=None)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    if args.all_configs:
+        return all_configs(args)
+    return gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

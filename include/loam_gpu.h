@@ -1,0 +1,209 @@
+/*
+ * loam_gpu.h -- C ABI of the B200-native par_loop engine (drop-in boundary).
+ *
+ * The reference (`loam`, C++20 header-only, /root/reference/proj/include/loam)
+ * has no FFI; its operator surface is the C++ API
+ *     void loam::execute(const Parloop&, int threads)          parloop.hpp:191
+ *     SparsityPtr loam::build_sparsity(row, col, rdim, cdim)   data.hpp:149
+ *     Coloring loam::color_iteration(iter, conflict_maps)      topology.hpp:86
+ *     void loam::validate(const Parloop&)                      parloop.hpp:89
+ * over Set/Map/Dat/Mat/Global/Arg objects (topology.hpp:15-74,
+ * data.hpp:15-234, parloop.hpp:17-59).  This header is exactly what an FFI
+ * binding of those entry points needs: plain descriptors (POD, device
+ * pointers, sizes, identities) and int error codes.  The C++ facade
+ * paper_1501_01809_b200/csrc/loam_gpu.hpp restores the reference's class API
+ * on top of it; INTEGRATION.md shows the ctypes and C++ bindings.
+ *
+ * Conventions
+ *   - Every function returns 0 on success or LOAM_ERR(kind) = 1 + the
+ *     loam::ErrorKind value (common.hpp:10-33); LOAM_GPU_ERR_CUDA reports a
+ *     CUDA runtime failure.  loam_gpu_last_error() returns a thread-local
+ *     message (the reference's Error::what()).
+ *   - Pointers in descriptors are DEVICE pointers borrowed for the call
+ *     ("execute borrows everything for its duration"); the
+ *     library never frees caller memory.  The *_host variants take host
+ *     pointers and stage the copies themselves.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *     stream-ordered; loam_gpu_execute returns after enqueueing unless the
+ *     kernel reports a device-side error (OutsideSparsity), which needs a
+ *     sync: see LOAM_OPT_CHECK_SPARSITY.
+ *   - No CPU fallback: without a usable sm_100 device every compute entry
+ *     point fails with LOAM_GPU_ERR_NO_DEVICE.
+ */
+#ifndef LOAM_GPU_H
+#define LOAM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* loam::ErrorKind (common.hpp:10-33), same order. */
+enum loam_error_kind {
+  LOAM_KIND_IndexOutOfRange = 0,
+  LOAM_KIND_ArityMismatch,
+  LOAM_KIND_SourceMismatch,
+  LOAM_KIND_AsymmetricAdjacency,
+  LOAM_KIND_IllegalAccess,
+  LOAM_KIND_MapSourceMismatch,
+  LOAM_KIND_ShapeMismatch,
+  LOAM_KIND_UnboundIdentifier,
+  LOAM_KIND_NonDividingFactor,
+  LOAM_KIND_OutsideSparsity,
+  LOAM_KIND_EmptyPartials,
+  LOAM_KIND_DimensionMismatch,
+  LOAM_KIND_InvalidSubdivision,
+  LOAM_KIND_ParseError,
+  LOAM_KIND_NonManifold,
+  LOAM_KIND_CellMismatch,
+  LOAM_KIND_UnsupportedForm,
+  LOAM_KIND_MissingDiagonal,
+  LOAM_KIND_SpaceMismatch,
+  LOAM_KIND_IndefiniteBreakdown,
+  LOAM_KIND_InstabilityDetected,
+  LOAM_KIND_InvalidArgument
+};
+#define LOAM_ERR(kind) (1 + LOAM_KIND_##kind)
+#define LOAM_GPU_ERR_CUDA 100      /* CUDA runtime error (message has details) */
+#define LOAM_GPU_ERR_NO_DEVICE 101 /* no usable sm_100 device: no CPU fallback */
+
+/* loam::Access (data.hpp:17), same order. */
+enum loam_access { LOAM_READ = 0, LOAM_WRITE, LOAM_RW, LOAM_INC, LOAM_SUM, LOAM_MIN, LOAM_MAX };
+
+enum loam_arg_kind { LOAM_ARG_DAT = 0, LOAM_ARG_MAT = 1, LOAM_ARG_GLOBAL = 2 };
+
+/* loam::Map (topology.hpp:36-66): int32 row-major [source_size x arity].
+ * `id` identifies the map object (the reference compares MapPtr identity);
+ * plans (colourings, inverse maps, slot ranks) are cached per id exactly like
+ * the reference's colouring cache (parloop.hpp:153-168).  id 0 = uncached.
+ * A dof-expanded map (entries dim*n+d, what a vector Mat needs)
+ * may declare its node map in `node_values`/`node_arity`/`node_target_size`
+ * with `expand_dim` = dim so the device reads the 1/dim-size node map. */
+typedef struct loam_map_desc {
+  const int32_t* values;
+  int32_t source_size, target_size, arity;
+  uint64_t source_id, target_id, id;
+  int32_t expand_dim; /* 0 or 1: plain map */
+  const int32_t* node_values;
+  int32_t node_arity, node_target_size;
+} loam_map_desc;
+
+/* loam::Sparsity (data.hpp:116-142): CSR, int64 row offsets, int32 columns. */
+typedef struct loam_sparsity_desc {
+  const int64_t* row_ptr; /* [nrows+1] */
+  const int32_t* col_idx; /* [nnz]     */
+  int32_t nrows, ncols;
+  int64_t nnz;
+  int32_t row_dim, col_dim; /* dof expansion the pattern was built with (>=1) */
+  uint64_t id;
+} loam_sparsity_desc;
+
+/* loam::Arg (parloop.hpp:17-52) over a Dat, Mat or Global. */
+typedef struct loam_arg_desc {
+  int32_t kind;   /* loam_arg_kind */
+  int32_t access; /* loam_access   */
+  double* data;   /* Dat [set_size*dim] | Global [dim] | Mat values [nnz] */
+  int32_t dim;    /* Dat / Global dim (Mat: ignored) */
+  int32_t set_size;
+  uint64_t set_id;  /* Dat's Set identity (direct args must match the iteration set) */
+  uint64_t obj_id;  /* object identity for the written-alias check (parloop.hpp:131-137) */
+  const loam_map_desc* map;     /* Dat: indirection or NULL (direct); Mat: row map */
+  const loam_map_desc* col_map; /* Mat column map */
+  const loam_sparsity_desc* sparsity; /* Mat pattern */
+  int32_t flags;  /* LOAM_ARG_ZERO: treat the target as freshly zero-initialised
+                     (make_dat/make_mat zero-fill, data.hpp:37-39,185-187, or
+                     zero()); its current contents are ignored.  The library
+                     zero-fills it only when the chosen path needs zeros (atomic /
+                     colour scatter); owner-computes writes every entry once. */
+} loam_arg_desc;
+#define LOAM_ARG_ZERO 1
+
+/* loam::ir::Kernel (kernel.hpp:504-511) as a registry key.  The reference
+ * bakes literals (helmholtz kappa, ...) into the kernel AST; here they are
+ * `params`.  An unregistered name is an error: there is no CPU fallback. */
+typedef struct loam_kernel_desc {
+  const char* name;
+  const double* params;
+  int32_t nparams;
+} loam_kernel_desc;
+
+/* ---- library ------------------------------------------------------------- */
+const char* loam_gpu_last_error(void);
+const char* loam_gpu_version(void);
+int loam_gpu_device_ok(void); /* 1 when an sm_100 device is usable */
+
+/* Tunables.  LOAM_OPT_INC_STRATEGY selects the indirect INC scatter:
+ *   0 auto (owner-computes), 1 fp64 atomics, 2 owner-computes row gather,
+ *   3 colouring (colour-major launches, plain read-modify-write).
+ * LOAM_OPT_CHECK_SPARSITY: 1 (default) = a Mat INC/WRITE synchronises once to
+ *   report OutsideSparsity like Mat::addto (data.hpp:214-216); 0 = the check
+ *   is done only when the slot plan is built (plans prove the pattern).
+ * LOAM_OPT_LOCALITY: 1 (default) = renumber cells internally for locality. */
+enum loam_option { LOAM_OPT_INC_STRATEGY = 0, LOAM_OPT_CHECK_SPARSITY = 1, LOAM_OPT_LOCALITY = 2 };
+int loam_gpu_set_option(int option, int value);
+int loam_gpu_get_option(int option);
+int loam_gpu_plan_cache_clear(void);
+/* Number of kernels this library launched since load (bench gpu_launches). */
+int64_t loam_gpu_launch_count(void);
+
+/* ---- kernel registry ----------------------------------------------------- */
+/* Staged parameter extents of a registered kernel (kernel.hpp:176-186 Param),
+ * flattened: for each param, rank then extents.  Returns the param count or
+ * -error.  `buf` holds at most `cap` ints. */
+int loam_gpu_kernel_signature(const char* name, int32_t* buf, int cap);
+/* Newline-separated registered kernel names (static storage). */
+const char* loam_gpu_kernel_names(void);
+
+/* ---- the operator -------------------------------------------------------- */
+/* loam::validate (parloop.hpp:89-146): checks descriptors only. */
+int loam_gpu_validate(const loam_kernel_desc* kernel, int32_t iterset_size, uint64_t iterset_id,
+                      const loam_arg_desc* args, int nargs);
+/* loam::execute (parloop.hpp:191-384) on device data. */
+int loam_gpu_execute(const loam_kernel_desc* kernel, int32_t iterset_size, uint64_t iterset_id,
+                     const loam_arg_desc* args, int nargs, void* stream);
+/* loam::execute on HOST data (every pointer in args/maps/sparsity is host
+ * memory, ideally pinned): uploads what the loop reads, runs, downloads what
+ * it writes, synchronously -- the reference's host-memory calling convention. */
+int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t iterset_size,
+                          uint64_t iterset_id, const loam_arg_desc* args, int nargs,
+                          void* stream);
+
+/* ---- topology / data services ------------------------------------------- */
+/* Map construction check (topology.hpp:45-48): every entry in [0, target). */
+int loam_gpu_map_check(const loam_map_desc* map, void* stream);
+/* loam::build_sparsity (data.hpp:149-179), bit-exact.  Allocates device
+ * arrays *row_ptr ([rows+1] int64) and *col_idx ([nnz] int32), released with
+ * loam_gpu_free. */
+int loam_gpu_build_sparsity(const loam_map_desc* row_map, const loam_map_desc* col_map,
+                            int row_dim, int col_dim, int64_t** row_ptr, int32_t** col_idx,
+                            int64_t* nnz, void* stream);
+/* loam::color_iteration (topology.hpp:86-125), bit-exact greedy colouring
+ * computed on the device (Jones-Plassmann with ascending-index priority).
+ * colors: device [n]. */
+int loam_gpu_color_iteration(int32_t n, uint64_t iterset_id, const loam_map_desc* maps,
+                             int nmaps, int32_t* colors, int32_t* num_colors, void* stream);
+
+/* ---- device memory helpers (for FFI callers without a CUDA binding) ------ */
+int loam_gpu_malloc(void** ptr, size_t bytes);
+int loam_gpu_free(void* ptr);
+int loam_gpu_host_alloc(void** ptr, size_t bytes); /* pinned */
+int loam_gpu_host_free(void* ptr);
+int loam_gpu_memcpy(void* dst, const void* src, size_t bytes, void* stream); /* any direction */
+int loam_gpu_memset(void* dst, int value, size_t bytes, void* stream);
+int loam_gpu_stream_sync(void* stream);
+
+/* ---- seeded synthetic inputs (host; csrc/meshgen.cpp) --------- */
+int loam_gpu_unit_square_mesh(int n, double* coords, int32_t* cv);  /* mesh.hpp:96-143 */
+int loam_gpu_unit_cube_mesh(int n, double* coords, int32_t* cv);    /* mesh.hpp:148-214 */
+int loam_gpu_jitter(int gdim, int n, double amp, uint64_t seed, double* coords);
+int loam_gpu_permute_cells(int ncells, int arity, uint64_t seed, int32_t* cv);
+int loam_gpu_uniform(int64_t count, uint64_t seed, double lo, double hi, double* out);
+int loam_gpu_p2_cell_node_map(int ncells, int nv, int gdim, const int32_t* cv, int32_t* cn);
+int loam_gpu_expand_map(int nsrc, int arity, const int32_t* map, int dim, int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOAM_GPU_H */

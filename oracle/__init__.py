@@ -1,0 +1,289 @@
+"""Oracle package -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this package, and only as the checker or the
+timed CPU baseline.  The product (paper_1501_01809_b200/) never imports it.
+
+  orc()  -> liborc.so            : C restatement of the reference algorithm
+  ref()  -> _ref/libloam_ref.so  : the unmodified reference headers compiled
+                                   by oracle/Makefile (extern "C" shim)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORC_PATH = os.path.join(HERE, "liborc.so")
+REF_PATH = os.path.join(HERE, "_ref", "libloam_ref.so")
+
+# orc_form numbering (loam_oracle.h)
+MASS, STIFFNESS, HELMHOLTZ, MASS_ACTION, STIFFNESS_ACTION, HELMHOLTZ_ACTION = range(6)
+ELASTICITY, STOKES_A, STOKES_B, STOKES_BT = 6, 7, 8, 9
+
+_orc = _ref = None
+IP, DP = C.POINTER(C.c_int32), C.POINTER(C.c_double)
+I64P = C.POINTER(C.c_int64)
+
+
+def ip(a):
+    return a.ctypes.data_as(IP)
+
+
+def dp(a):
+    return None if a is None else a.ctypes.data_as(DP)
+
+
+def orc():
+    global _orc
+    if _orc is None:
+        L = C.CDLL(ORC_PATH)
+        L.orc_color_iteration.argtypes = [C.c_int, C.c_int, C.POINTER(IP), IP, IP, IP]
+        L.orc_build_sparsity.restype = C.c_int64
+        L.orc_build_sparsity.argtypes = [C.c_int, IP, C.c_int, C.c_int, IP, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, C.POINTER(I64P), C.POINTER(IP)]
+        L.orc_free.argtypes = [C.c_void_p]
+        L.orc_p2_cell_node_map.argtypes = [C.c_int, C.c_int, C.c_int, IP, IP]
+        L.orc_element.argtypes = [C.c_int, C.c_int, C.c_int, DP, DP, DP, DP]
+        L.orc_element_shape.argtypes = [C.c_int, C.c_int, C.c_int, IP, IP]
+        L.orc_assemble_vector.argtypes = [C.c_int, C.c_int, C.c_int, DP, C.c_int, IP, C.c_int, IP, DP,
+                                          IP, C.c_int, DP, C.c_int, DP]
+        L.orc_assemble_matrix.argtypes = [C.c_int, C.c_int, C.c_int, DP, C.c_int, IP, C.c_int, IP,
+                                          C.c_int, IP, DP, C.c_int, I64P, IP, DP]
+        _orc = L
+    return _orc
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        L = C.CDLL(REF_PATH)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_free.argtypes = [C.c_void_p]
+        L.ref_unit_square_mesh.argtypes = [C.c_int, DP, IP]
+        L.ref_unit_cube_mesh.argtypes = [C.c_int, DP, IP]
+        L.ref_color_iteration.argtypes = [C.c_int, C.c_int, C.POINTER(IP), IP, IP, IP]
+        L.ref_build_sparsity.restype = C.c_int64
+        L.ref_build_sparsity.argtypes = [C.c_int, IP, C.c_int, C.c_int, IP, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, C.POINTER(I64P), C.POINTER(IP)]
+        L.ref_p2_tri_map.argtypes = [C.c_int, C.c_int, IP, DP, IP]
+        L.ref_local_kernel.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, DP, DP, DP]
+        L.ref_assemble_vector.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, IP, DP,
+                                          DP, C.c_int, DP, IP]
+        L.ref_assemble_matrix.restype = C.c_int64
+        L.ref_assemble_matrix.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, IP, DP,
+                                          C.c_int, IP, C.POINTER(I64P), C.POINTER(IP), C.POINTER(DP)]
+        L.ref_engine_matrix.restype = C.c_int64
+        L.ref_engine_matrix.argtypes = [C.c_int, C.c_int, C.c_int, DP, C.c_int, IP, C.c_int, C.c_int, IP,
+                                        C.c_int, C.c_int, IP, C.c_int, DP, C.c_int, C.POINTER(I64P),
+                                        C.POINTER(IP), C.POINTER(DP)]
+        L.ref_engine_vector.argtypes = [C.c_int, C.c_int, C.c_int, DP, C.c_int, IP, C.c_int, C.c_int, IP,
+                                        C.c_int, DP, DP, C.c_int, DP]
+        L.ref_time_execute.argtypes = [C.c_int, C.c_int, C.c_int, DP, C.c_int, C.c_int, IP, DP, DP,
+                                       C.c_int, C.c_int, C.c_int, C.c_int, DP]
+        _ref = L
+    return _ref
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _check(code, lib=None):
+    if code != 0:
+        msg = lib.ref_last_error().decode() if lib is not None else ""
+        raise OracleError(f"oracle error {code}: {msg}")
+
+
+def _params(params):
+    p = np.zeros(4)
+    p[: len(params)] = params
+    return p
+
+
+# ---------------------------------------------------------------- C restatement wrappers
+def color_iteration(n, maps, arities, targets, lib="orc"):
+    maps = [np.ascontiguousarray(m, dtype=np.int32) for m in maps]
+    arr = (IP * max(len(maps), 1))(*[ip(m) for m in maps])
+    ar = np.asarray(arities, dtype=np.int32)
+    tg = np.asarray(targets, dtype=np.int32)
+    colors = np.empty(max(n, 1), dtype=np.int32)
+    if lib == "orc":
+        nc = orc().orc_color_iteration(n, len(maps), arr, ip(ar), ip(tg), ip(colors))
+    else:
+        nc = ref().ref_color_iteration(n, len(maps), arr, ip(ar), ip(tg), ip(colors))
+    if nc < 0:
+        raise OracleError(f"colouring failed ({-nc})")
+    return colors[:n], nc
+
+
+def build_sparsity(nsrc, row_map, ar_r, nrt, col_map, ar_c, nct, row_dim=1, col_dim=1, lib="orc"):
+    rm = np.ascontiguousarray(row_map, dtype=np.int32)
+    cm = np.ascontiguousarray(col_map, dtype=np.int32)
+    rp, ci = I64P(), IP()
+    L = orc() if lib == "orc" else ref()
+    fn = L.orc_build_sparsity if lib == "orc" else L.ref_build_sparsity
+    nnz = fn(nsrc, ip(rm), ar_r, nrt, ip(cm), ar_c, nct, row_dim, col_dim, C.byref(rp), C.byref(ci))
+    if nnz < 0:
+        raise OracleError(f"build_sparsity failed ({-nnz})")
+    nrows = nrt * row_dim
+    row_ptr = np.ctypeslib.as_array(rp, shape=(nrows + 1,)).copy()
+    col_idx = np.ctypeslib.as_array(ci, shape=(max(nnz, 1),))[:nnz].copy()
+    free = L.orc_free if lib == "orc" else L.ref_free
+    free(C.cast(rp, C.c_void_p))
+    free(C.cast(ci, C.c_void_p))
+    return row_ptr, col_idx
+
+
+def p2_cell_node_map(cv, nv, gdim):
+    cv = np.ascontiguousarray(cv, dtype=np.int32)
+    nc = cv.size // (gdim + 1)
+    cn = np.empty(nc * (6 if gdim == 2 else 10), dtype=np.int32)
+    nn = orc().orc_p2_cell_node_map(nc, nv, gdim, ip(cv), ip(cn))
+    return cn, nn
+
+
+def element(form, degree, gdim, X, C_=None, params=()):
+    r, c = C.c_int32(), C.c_int32()
+    _check(orc().orc_element_shape(form, degree, gdim, C.byref(r), C.byref(c)))
+    out = np.zeros(r.value * c.value)
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    Cc = None if C_ is None else np.ascontiguousarray(C_, dtype=np.float64)
+    _check(orc().orc_element(form, degree, gdim, dp(_params(params)), dp(X), dp(Cc), dp(out)))
+    return out.reshape(r.value, c.value)
+
+
+def assemble_vector(form, degree, gdim, ncells, test_map, ar_t, coord_map, coords, coeff_map, ar_c,
+                    coeff, nout, params=()):
+    out = np.zeros(nout)
+    tm = np.ascontiguousarray(test_map, dtype=np.int32)
+    xm = np.ascontiguousarray(coord_map, dtype=np.int32)
+    cm = np.ascontiguousarray(coeff_map, dtype=np.int32)
+    _check(orc().orc_assemble_vector(form, degree, gdim, dp(_params(params)), ncells, ip(tm), ar_t,
+                                     ip(xm), dp(np.ascontiguousarray(coords)), ip(cm), ar_c,
+                                     dp(np.ascontiguousarray(coeff)), nout, dp(out)))
+    return out
+
+
+def assemble_matrix(form, degree, gdim, ncells, row_map, ar_r, col_map, ar_c, coord_map, coords,
+                    row_ptr, col_idx, params=()):
+    nrows = row_ptr.size - 1
+    vals = np.zeros(max(int(row_ptr[-1]), 1))
+    rm = np.ascontiguousarray(row_map, dtype=np.int32)
+    cm = np.ascontiguousarray(col_map, dtype=np.int32)
+    xm = np.ascontiguousarray(coord_map, dtype=np.int32)
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    code = orc().orc_assemble_matrix(form, degree, gdim, dp(_params(params)), ncells, ip(rm), ar_r, ip(cm),
+                                     ar_c, ip(xm), dp(np.ascontiguousarray(coords)), nrows,
+                                     rp.ctypes.data_as(I64P), ip(ci), dp(vals))
+    _check(code)
+    return vals[: int(row_ptr[-1])]
+
+
+# ---------------------------------------------------------------- reference (compiled) wrappers
+def ref_unit_mesh(gdim, n):
+    if gdim == 2:
+        coords, cv = np.empty((n + 1) ** 2 * 2), np.empty(2 * n * n * 3, dtype=np.int32)
+        _check(ref().ref_unit_square_mesh(n, dp(coords), ip(cv)), ref())
+    else:
+        coords, cv = np.empty((n + 1) ** 3 * 3), np.empty(6 * n ** 3 * 4, dtype=np.int32)
+        _check(ref().ref_unit_cube_mesh(n, dp(coords), ip(cv)), ref())
+    return coords, cv
+
+
+def ref_p2_tri_map(cv, coords):
+    cv = np.ascontiguousarray(cv, dtype=np.int32)
+    nc, nv = cv.size // 3, coords.size // 2
+    cn = np.empty(nc * 6, dtype=np.int32)
+    nn = ref().ref_p2_tri_map(nc, nv, ip(cv), dp(np.ascontiguousarray(coords)), ip(cn))
+    if nn < 0:
+        raise OracleError(ref().ref_last_error().decode())
+    return cn, nn
+
+
+def ref_local_kernel(kind, degree, gdim, X, C_=None, kappa=0.0):
+    nb = (gdim + 1) if degree == 1 else (6 if gdim == 2 else 10)
+    bil = kind in (MASS, STIFFNESS, HELMHOLTZ)
+    out = np.zeros(nb * nb if bil else nb)
+    Cc = np.zeros(nb) if C_ is None else np.ascontiguousarray(C_, dtype=np.float64)
+    _check(ref().ref_local_kernel(kind, degree, gdim, kappa, dp(np.ascontiguousarray(X, dtype=np.float64)),
+                                  dp(Cc), dp(out)), ref())
+    return out.reshape(nb, nb) if bil else out
+
+
+def ref_assemble_vector(kind, degree, gdim, cv, coords, coeff, kappa=1.0, threads=1):
+    cv = np.ascontiguousarray(cv, dtype=np.int32)
+    nc, nv = cv.size // (gdim + 1), coords.size // gdim
+    out = np.zeros(max(coeff.size, nv))
+    nout = C.c_int32()
+    _check(ref().ref_assemble_vector(kind, degree, gdim, kappa, nc, nv, ip(cv), dp(np.ascontiguousarray(coords)),
+                                     dp(np.ascontiguousarray(coeff)), threads, dp(out), C.byref(nout)), ref())
+    return out[: nout.value]
+
+
+def ref_assemble_matrix(kind, degree, gdim, cv, coords, kappa=1.0, threads=1):
+    cv = np.ascontiguousarray(cv, dtype=np.int32)
+    nc, nv = cv.size // (gdim + 1), coords.size // gdim
+    nrows = C.c_int32()
+    rp, ci, vals = I64P(), IP(), DP()
+    nnz = ref().ref_assemble_matrix(kind, degree, gdim, kappa, nc, nv, ip(cv), dp(np.ascontiguousarray(coords)),
+                                    threads, C.byref(nrows), C.byref(rp), C.byref(ci), C.byref(vals))
+    if nnz < 0:
+        raise OracleError(ref().ref_last_error().decode())
+    out = (np.ctypeslib.as_array(rp, shape=(nrows.value + 1,)).copy(),
+           np.ctypeslib.as_array(ci, shape=(max(nnz, 1),))[:nnz].copy(),
+           np.ctypeslib.as_array(vals, shape=(max(nnz, 1),))[:nnz].copy())
+    for p in (rp, ci, vals):
+        ref().ref_free(C.cast(p, C.c_void_p))
+    return out
+
+
+def ref_engine_matrix(form, degree, gdim, ncells, row_map, ar_r, nrt, col_map, ar_c, nct, coord_map,
+                      coords, params=(), threads=1):
+    rm = np.ascontiguousarray(row_map, dtype=np.int32)
+    cm = rm if col_map is row_map else np.ascontiguousarray(col_map, dtype=np.int32)
+    xm = np.ascontiguousarray(coord_map, dtype=np.int32)
+    nv = coords.size // gdim
+    rp, ci, vals = I64P(), IP(), DP()
+    nnz = ref().ref_engine_matrix(form, degree, gdim, dp(_params(params)), ncells, ip(rm), ar_r, nrt, ip(cm),
+                                  ar_c, nct, ip(xm), nv, dp(np.ascontiguousarray(coords)), threads,
+                                  C.byref(rp), C.byref(ci), C.byref(vals))
+    if nnz < 0:
+        raise OracleError(ref().ref_last_error().decode())
+    nrows = nrt
+    out = (np.ctypeslib.as_array(rp, shape=(nrows + 1,)).copy(),
+           np.ctypeslib.as_array(ci, shape=(max(nnz, 1),))[:nnz].copy(),
+           np.ctypeslib.as_array(vals, shape=(max(nnz, 1),))[:nnz].copy())
+    for p in (rp, ci, vals):
+        ref().ref_free(C.cast(p, C.c_void_p))
+    return out
+
+
+def ref_engine_vector(form, degree, gdim, ncells, test_map, ar_t, nt, coord_map, coords, coeff,
+                      params=(), threads=1):
+    tm = np.ascontiguousarray(test_map, dtype=np.int32)
+    xm = np.ascontiguousarray(coord_map, dtype=np.int32)
+    out = np.zeros(nt)
+    _check(ref().ref_engine_vector(form, degree, gdim, dp(_params(params)), ncells, ip(tm), ar_t, nt, ip(xm),
+                                   coords.size // gdim, dp(np.ascontiguousarray(coords)),
+                                   dp(np.ascontiguousarray(coeff)), threads, dp(out)), ref())
+    return out
+
+
+def ref_time_execute(form, degree, gdim, cv, coords, coeff=None, params=(), as_shipped=True, threads=1,
+                     warmup=1, steps=3):
+    cv = np.ascontiguousarray(cv, dtype=np.int32)
+    nc, nv = cv.size // (gdim + 1), coords.size // gdim
+    times = np.zeros(steps)
+    _check(ref().ref_time_execute(form, degree, gdim, dp(_params(params)), nc, nv, ip(cv),
+                                  dp(np.ascontiguousarray(coords)),
+                                  None if coeff is None else dp(np.ascontiguousarray(coeff)),
+                                  int(as_shipped), threads, warmup, steps, dp(times)), ref())
+    return times

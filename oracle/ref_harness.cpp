@@ -1,0 +1,400 @@
+// ref_harness.cpp -- extern "C" shim over the UNMODIFIED reference headers.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile against the headers
+// where they lie (-I/root/reference/proj/include) into oracle/_ref/libloam_ref.so.
+// Nothing from the reference is copied into this repository.  Used by
+//   * tests/ to pin the C restatement (oracle/loam_oracle.c) and the CUDA path,
+//   * tools/make_golden.py to write tests/golden/*.npz,
+//   * bench.py --impl reference / cpu_baseline to time the reference par_loop.
+//
+// For configs 3-5 the reference has no element kernel (fem/element.hpp:179-180,
+// fem/form.hpp:30-45); there the reference ENGINE (build_sparsity, execute,
+// Mat::addto) runs a host kernel (kernel.hpp:523-529) whose body is the C
+// restatement orc_element (oracle/loam_oracle.c), linked into this library.
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "loam/loam.hpp"
+#include "loam_oracle.h"
+
+using namespace loam;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail_code(const Error& e) {
+  g_error = e.what();
+  return 1 + static_cast<int>(e.kind());
+}
+
+MeshPtr mesh_from_arrays(int gdim, int ncells, int nv, const int32_t* cv, const double* coords,
+                         bool facets) {
+  auto mesh = std::make_shared<Mesh>();
+  mesh->dim = gdim;
+  mesh->cells = make_set(ncells, "cells");
+  mesh->vertices = make_set(nv, "vertices");
+  std::vector<int> table(cv, cv + static_cast<size_t>(ncells) * (gdim + 1));
+  mesh->cell_vertex_map = make_map(mesh->cells, mesh->vertices, gdim + 1, std::move(table),
+                                   "cell_vertex");
+  mesh->coordinates = make_dat(mesh->vertices, gdim, "coordinates");
+  auto x = mesh->coordinates->mutable_view();
+  std::memcpy(x.data(), coords, sizeof(double) * static_cast<size_t>(nv) * gdim);
+  if (facets) loam::detail::derive_exterior_facets(*mesh, nullptr);
+  return mesh;
+}
+
+template <class T>
+T* copy_out(const std::vector<T>& v) {
+  T* p = static_cast<T*>(std::malloc(sizeof(T) * (v.size() ? v.size() : 1)));
+  std::memcpy(p, v.data(), sizeof(T) * v.size());
+  return p;
+}
+
+double now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+// Catalogue form for (kind, degree) on V.  kind uses the orc_form numbering.
+fem::Form catalogue_form(int kind, const fem::FunctionSpacePtr& V, const fem::FunctionPtr& u,
+                         double kappa) {
+  switch (kind) {
+  case ORC_MASS: return fem::mass(V, V);
+  case ORC_STIFFNESS: return fem::stiffness(V, V);
+  case ORC_HELMHOLTZ: return fem::helmholtz(V, V, kappa);
+  case ORC_MASS_ACTION: return fem::mass_action(V, u);
+  case ORC_STIFFNESS_ACTION: return fem::stiffness_action(V, u);
+  default: fail(ErrorKind::UnsupportedForm, "not a reference catalogue form");
+  }
+}
+
+} // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_error.c_str(); }
+void ref_free(void* p) { std::free(p); }
+
+// mesh.hpp:96-143
+int ref_unit_square_mesh(int n, double* coords, int32_t* cv) {
+  try {
+    auto m = unit_square_mesh(n);
+    auto x = m->coordinates->view();
+    std::memcpy(coords, x.data(), sizeof(double) * x.size());
+    const auto& v = m->cell_vertex_map->values();
+    std::memcpy(cv, v.data(), sizeof(int32_t) * v.size());
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
+// mesh.hpp:148-214
+int ref_unit_cube_mesh(int n, double* coords, int32_t* cv) {
+  try {
+    auto m = unit_cube_mesh(n);
+    auto x = m->coordinates->view();
+    std::memcpy(coords, x.data(), sizeof(double) * x.size());
+    const auto& v = m->cell_vertex_map->values();
+    std::memcpy(cv, v.data(), sizeof(int32_t) * v.size());
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
+// topology.hpp:86-125 (through the cached conflict_coloring entry point is not
+// needed: the cache returns the same colouring).  Returns num_colors or -err.
+int ref_color_iteration(int n, int nmaps, const int32_t* const* maps, const int32_t* arity,
+                        const int32_t* target, int32_t* colors) {
+  try {
+    auto iter = make_set(n, "iter");
+    std::vector<MapPtr> ms;
+    for (int m = 0; m < nmaps; ++m) {
+      auto t = make_set(target[m], "target");
+      std::vector<int> vals(maps[m], maps[m] + static_cast<size_t>(n) * arity[m]);
+      ms.push_back(make_map(iter, t, arity[m], std::move(vals)));
+    }
+    auto c = color_iteration(iter, ms);
+    std::memcpy(colors, c.colors.data(), sizeof(int32_t) * c.colors.size());
+    return c.num_colors;
+  } catch (const Error& e) {
+    return -fail_code(e);
+  }
+}
+
+// data.hpp:149-179.  Returns nnz or -err; arrays via ref_free.
+int64_t ref_build_sparsity(int nsrc, const int32_t* row_map, int ar_r, int nrt,
+                           const int32_t* col_map, int ar_c, int nct, int row_dim, int col_dim,
+                           int64_t** rp, int32_t** ci) {
+  try {
+    auto src = make_set(nsrc);
+    auto rt = make_set(nrt);
+    auto ct = make_set(nct);
+    auto rm = make_map(src, rt, ar_r,
+                       std::vector<int>(row_map, row_map + static_cast<size_t>(nsrc) * ar_r));
+    auto cm = make_map(src, ct, ar_c,
+                       std::vector<int>(col_map, col_map + static_cast<size_t>(nsrc) * ar_c));
+    auto sp = build_sparsity(rm, cm, row_dim, col_dim);
+    std::vector<int64_t> offs(sp->row_offsets().begin(), sp->row_offsets().end());
+    *rp = copy_out(offs);
+    *ci = copy_out(sp->col_indices());
+    return sp->nnz();
+  } catch (const Error& e) {
+    return -fail_code(e);
+  }
+}
+
+// space.hpp:30-82 for triangles (degree 2).  Returns node count or -err.
+int ref_p2_tri_map(int ncells, int nv, const int32_t* cv, const double* coords, int32_t* cn) {
+  try {
+    auto mesh = mesh_from_arrays(2, ncells, nv, cv, coords, true);
+    auto V = fem::make_function_space(mesh, 2);
+    const auto& v = V->cell_node_map->values();
+    std::memcpy(cn, v.data(), sizeof(int32_t) * v.size());
+    return V->node_set->size();
+  } catch (const Error& e) {
+    return -fail_code(e);
+  }
+}
+
+// Local element tensor of a catalogue form through the reference kernel
+// pipeline: compile_local_kernel -> hoist_invariants -> fold_constants ->
+// interpret (assemble.hpp:16-19, kernel.hpp:482-495).
+int ref_local_kernel(int kind, int degree, int gdim, double kappa, const double* X,
+                     const double* C, double* out) {
+  try {
+    auto mesh = gdim == 2 ? unit_square_mesh(1) : unit_cube_mesh(1);
+    auto V = fem::make_function_space(mesh, degree);
+    auto u = fem::make_function(V);
+    auto form = catalogue_form(kind, V, u, kappa);
+    auto kernel = fem::detail::optimized_kernel(form);
+    const auto& params = kernel->params();
+    std::vector<std::vector<Real>> bufs;
+    for (const auto& p : params) bufs.emplace_back(p.size(), 0.0);
+    std::memcpy(bufs[1].data(), X, sizeof(double) * bufs[1].size());
+    if (bufs.size() > 2) std::memcpy(bufs[2].data(), C, sizeof(double) * bufs[2].size());
+    std::vector<Real*> ptrs;
+    for (auto& b : bufs) ptrs.push_back(b.data());
+    ir::invoke(*kernel, {ptrs.data(), ptrs.size()});
+    std::memcpy(out, bufs[0].data(), sizeof(double) * bufs[0].size());
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
+// fem::assemble_vector (assemble.hpp:108-135) of a catalogue linear form on
+// the given mesh; kind ORC_HELMHOLTZ_ACTION = stiffness_action + kappa *
+// mass_action as two reference loops (no single catalogue form).
+// coeff lives on the degree-`degree` node set the reference builds.
+int ref_assemble_vector(int kind, int degree, int gdim, double kappa, int ncells, int nv,
+                        const int32_t* cv, const double* coords, const double* coeff,
+                        int threads, double* out, int* nout) {
+  try {
+    auto mesh = mesh_from_arrays(gdim, ncells, nv, cv, coords, degree == 2);
+    auto V = fem::make_function_space(mesh, degree);
+    auto u = fem::make_function(V);
+    auto w = u->dat->mutable_view();
+    std::memcpy(w.data(), coeff, sizeof(double) * w.size());
+    *nout = V->node_set->size();
+    if (kind == ORC_HELMHOLTZ_ACTION) {
+      auto a = fem::assemble_vector(fem::stiffness_action(V, u), {}, threads);
+      auto b = fem::assemble_vector(fem::mass_action(V, u), {}, threads);
+      auto av = a->view();
+      auto bv = b->view();
+      for (size_t i = 0; i < av.size(); ++i) out[i] = av[i] + kappa * bv[i];
+    } else {
+      auto a = fem::assemble_vector(catalogue_form(kind, V, u, kappa), {}, threads);
+      auto av = a->view();
+      std::memcpy(out, av.data(), sizeof(double) * av.size());
+    }
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
+// fem::assemble_matrix (assemble.hpp:85-104) of a catalogue bilinear form.
+// Returns nnz or -err; rp/ci/vals via ref_free.
+int64_t ref_assemble_matrix(int kind, int degree, int gdim, double kappa, int ncells, int nv,
+                            const int32_t* cv, const double* coords, int threads, int* nrows,
+                            int64_t** rp, int32_t** ci, double** vals) {
+  try {
+    auto mesh = mesh_from_arrays(gdim, ncells, nv, cv, coords, degree == 2);
+    auto V = fem::make_function_space(mesh, degree);
+    auto mat = fem::assemble_matrix(catalogue_form(kind, V, nullptr, kappa), {}, threads);
+    const auto& sp = *mat->sparsity();
+    *nrows = sp.nrows();
+    std::vector<int64_t> offs(sp.row_offsets().begin(), sp.row_offsets().end());
+    *rp = copy_out(offs);
+    *ci = copy_out(sp.col_indices());
+    *vals = copy_out(mat->values());
+    return sp.nnz();
+  } catch (const Error& e) {
+    return -fail_code(e);
+  }
+}
+
+// The reference ENGINE with a restated host kernel: build_sparsity +
+// Mat + execute (parloop.hpp:191-384) for forms the reference catalogue
+// lacks (P2 tet, elasticity, Stokes blocks).  Maps are dof-expanded where the
+// Mat is vector valued.  Returns nnz or -err.
+int64_t ref_engine_matrix(int form, int degree, int gdim, const double* params, int ncells,
+                          const int32_t* row_map, int ar_r, int nrt, const int32_t* col_map,
+                          int ar_c, int nct, const int32_t* coord_map, int nv,
+                          const double* coords, int threads, int64_t** rp, int32_t** ci,
+                          double** vals) {
+  try {
+    auto cells = make_set(ncells, "cells");
+    auto rt = make_set(nrt, "rows");
+    auto ct = nct == nrt && col_map == row_map ? rt : make_set(nct, "cols");
+    auto verts = make_set(nv, "vertices");
+    auto rm = make_map(cells, rt, ar_r,
+                       std::vector<int>(row_map, row_map + static_cast<size_t>(ncells) * ar_r));
+    auto cm = col_map == row_map
+                  ? rm
+                  : make_map(cells, ct, ar_c,
+                             std::vector<int>(col_map, col_map + static_cast<size_t>(ncells) * ar_c));
+    auto xm = make_map(cells, verts, gdim + 1,
+                       std::vector<int>(coord_map, coord_map + static_cast<size_t>(ncells) * (gdim + 1)));
+    auto X = make_dat(verts, gdim, "coordinates");
+    std::memcpy(X->mutable_view().data(), coords, sizeof(double) * static_cast<size_t>(nv) * gdim);
+    auto mat = make_mat(build_sparsity(rm, cm), "assembled");
+    std::vector<double> p(params, params + 4);
+    auto kernel = ir::make_host_kernel(
+        "host_form_" + std::to_string(form), {{"A", {ar_r, ar_c}}, {"X", {gdim + 1, gdim}}},
+        [=](Real* const* a) { orc_element(form, degree, gdim, p.data(), a[1], nullptr, a[0]); });
+    Parloop loop{kernel, cells, {arg(mat, Access::INC, rm, cm), arg(X, Access::READ, xm)}};
+    execute(loop, threads);
+    const auto& sp = *mat->sparsity();
+    std::vector<int64_t> offs(sp.row_offsets().begin(), sp.row_offsets().end());
+    *rp = copy_out(offs);
+    *ci = copy_out(sp.col_indices());
+    *vals = copy_out(mat->values());
+    return sp.nnz();
+  } catch (const Error& e) {
+    return -fail_code(e);
+  }
+}
+
+// Same engine for a residual with a restated host kernel (P2 tet action).
+int ref_engine_vector(int form, int degree, int gdim, const double* params, int ncells,
+                      const int32_t* test_map, int ar_t, int nt, const int32_t* coord_map,
+                      int nv, const double* coords, const double* coeff, int threads,
+                      double* out) {
+  try {
+    auto cells = make_set(ncells, "cells");
+    auto nodes = make_set(nt, "nodes");
+    auto verts = make_set(nv, "vertices");
+    auto tm = make_map(cells, nodes, ar_t,
+                       std::vector<int>(test_map, test_map + static_cast<size_t>(ncells) * ar_t));
+    auto xm = make_map(cells, verts, gdim + 1,
+                       std::vector<int>(coord_map, coord_map + static_cast<size_t>(ncells) * (gdim + 1)));
+    auto X = make_dat(verts, gdim, "coordinates");
+    std::memcpy(X->mutable_view().data(), coords, sizeof(double) * static_cast<size_t>(nv) * gdim);
+    auto u = make_dat(nodes, 1, "u");
+    std::memcpy(u->mutable_view().data(), coeff, sizeof(double) * static_cast<size_t>(nt));
+    auto b = make_dat(nodes, 1, "assembled");
+    std::vector<double> p(params, params + 4);
+    auto kernel = ir::make_host_kernel(
+        "host_form_" + std::to_string(form),
+        {{"A", {ar_t}}, {"X", {gdim + 1, gdim}}, {"C", {ar_t}}},
+        [=](Real* const* a) { orc_element(form, degree, gdim, p.data(), a[1], a[2], a[0]); });
+    Parloop loop{kernel, cells, {arg(b, Access::INC, tm), arg(X, Access::READ, xm), arg(u, Access::READ, tm)}};
+    execute(loop, threads);
+    auto bv = b->view();
+    std::memcpy(out, bv.data(), sizeof(double) * bv.size());
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Timing entry for bench.py (--impl reference and the cpu_baseline leg).
+// Builds the reference objects once, runs `warmup` untimed executes, then
+// times `steps` calls of loam::execute (the reference par_loop, parloop.hpp:191)
+// with `threads` workers, each preceded by Mat::zero()/Dat reset as
+// assemble_matrix/assemble_vector's fresh allocation would do.  The element
+// kernel is the reference's own optimised AST kernel (assemble.hpp:16-19)
+// when `as_shipped` is nonzero, else a compiled host kernel (orc_element).
+// Writes per-step seconds into times[steps].  Returns 0 or err.
+int ref_time_execute(int form, int degree, int gdim, const double* params, int ncells, int nv,
+                     const int32_t* cv, const double* coords, const double* coeff,
+                     int as_shipped, int threads, int warmup, int steps, double* times) {
+  try {
+    auto mesh = mesh_from_arrays(gdim, ncells, nv, cv, coords, degree == 2);
+    auto V = fem::make_function_space(mesh, degree);
+    auto u = fem::make_function(V);
+    if (coeff) std::memcpy(u->dat->mutable_view().data(), coeff,
+                           sizeof(double) * static_cast<size_t>(V->node_set->size()));
+    const bool bilinear = form == ORC_MASS || form == ORC_STIFFNESS || form == ORC_HELMHOLTZ;
+    std::vector<Parloop> loops;
+    MatPtr mat;
+    DatPtr vec;
+    const double kappa = params[0];
+    std::vector<double> p(params, params + 4);
+    if (bilinear) {
+      mat = make_mat(build_sparsity(V->cell_node_map, V->cell_node_map), "assembled");
+      ir::KernelPtr kernel;
+      if (as_shipped) {
+        kernel = fem::detail::optimized_kernel(catalogue_form(form, V, u, kappa));
+      } else {
+        const int m = V->element.node_count;
+        kernel = ir::make_host_kernel(
+            "host_form", {{"A", {m, m}}, {"X", {gdim + 1, gdim}}},
+            [=](Real* const* a) { orc_element(form, degree, gdim, p.data(), a[1], nullptr, a[0]); });
+      }
+      loops.push_back({kernel, mesh->cells,
+                       {arg(mat, Access::INC, V->cell_node_map, V->cell_node_map),
+                        arg(mesh->coordinates, Access::READ, mesh->cell_vertex_map)}});
+    } else {
+      vec = make_dat(V->node_set, 1, "assembled");
+      std::vector<ir::KernelPtr> kernels;
+      if (as_shipped) {
+        if (form == ORC_HELMHOLTZ_ACTION) { // two catalogue loops
+          kernels.push_back(fem::detail::optimized_kernel(fem::stiffness_action(V, u)));
+          kernels.push_back(fem::detail::optimized_kernel(fem::mass_action(V, u)));
+        } else {
+          kernels.push_back(fem::detail::optimized_kernel(catalogue_form(form, V, u, kappa)));
+        }
+      } else {
+        const int m = V->element.node_count;
+        kernels.push_back(ir::make_host_kernel(
+            "host_form", {{"A", {m}}, {"X", {gdim + 1, gdim}}, {"C", {m}}},
+            [=](Real* const* a) { orc_element(form, degree, gdim, p.data(), a[1], a[2], a[0]); }));
+      }
+      for (auto& k : kernels)
+        loops.push_back({k, mesh->cells,
+                         {arg(vec, Access::INC, V->cell_node_map),
+                          arg(mesh->coordinates, Access::READ, mesh->cell_vertex_map),
+                          arg(u->dat, Access::READ, V->cell_node_map)}});
+    }
+    auto run = [&]() {
+      if (mat) mat->zero();
+      if (vec) {
+        auto w = vec->mutable_view();
+        std::fill(w.begin(), w.end(), 0.0);
+      }
+      for (auto& l : loops) execute(l, threads);
+    };
+    for (int i = 0; i < warmup; ++i) run();
+    for (int i = 0; i < steps; ++i) {
+      double t0 = now();
+      run();
+      times[i] = now() - t0;
+    }
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
+} // extern "C"

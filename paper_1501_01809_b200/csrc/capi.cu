@@ -1,0 +1,260 @@
+// capi.cu -- extern "C" boundary (include/loam_gpu.h) over the engine.
+//
+// Error convention: loam::Error (common.hpp:36-49) -> int code 1 + ErrorKind
+// with a thread-local message; CUDA failures -> LOAM_GPU_ERR_CUDA.  No CPU
+// fallback: compute entry points fail with LOAM_GPU_ERR_NO_DEVICE when no
+// sm_100 device is usable.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+#include "plan.cuh"
+
+using namespace loam_gpu;
+
+namespace {
+
+thread_local std::string g_msg;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_msg.clear();
+    return 0;
+  } catch (const Error& e) {
+    g_msg = e.what();
+    return e.code();
+  } catch (const std::exception& e) {
+    g_msg = e.what();
+    return LOAM_ERR(InvalidArgument);
+  }
+}
+
+bool device_ok() {
+  static const bool ok = [] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      return false;
+    }
+    int dev = 0, major = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    return major == 10;
+  }();
+  return ok;
+}
+
+void require_device() {
+  require(device_ok(), LOAM_GPU_ERR_NO_DEVICE,
+          "no usable sm_100 (B200) device: the loam_gpu engine has no CPU fallback");
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+} // namespace
+
+extern "C" {
+
+const char* loam_gpu_last_error(void) { return g_msg.c_str(); }
+const char* loam_gpu_version(void) { return "loam_gpu 0.1 (sm_100a)"; }
+int loam_gpu_device_ok(void) { return device_ok() ? 1 : 0; }
+
+int loam_gpu_set_option(int option, int value) {
+  return guarded([&] {
+    switch (option) {
+    case LOAM_OPT_INC_STRATEGY:
+      require(value >= 0 && value <= 3, LOAM_ERR(InvalidArgument), "strategy must be 0..3");
+      options().inc_strategy = value;
+      break;
+    case LOAM_OPT_CHECK_SPARSITY: options().check_sparsity = value ? 1 : 0; break;
+    case LOAM_OPT_LOCALITY: options().locality = value ? 1 : 0; break;
+    default: fail(LOAM_ERR(InvalidArgument), "unknown option");
+    }
+  });
+}
+
+int loam_gpu_get_option(int option) {
+  switch (option) {
+  case LOAM_OPT_INC_STRATEGY: return options().inc_strategy;
+  case LOAM_OPT_CHECK_SPARSITY: return options().check_sparsity;
+  case LOAM_OPT_LOCALITY: return options().locality;
+  default: return -1;
+  }
+}
+
+int loam_gpu_plan_cache_clear(void) {
+  return guarded([] { plan_cache_clear(); });
+}
+
+int64_t loam_gpu_launch_count(void) { return g_launches.load(); }
+
+int loam_gpu_kernel_signature(const char* name, int32_t* buf, int cap) {
+  const KernelInfo* k = name ? find_kernel(name) : nullptr;
+  if (!k) {
+    g_msg = std::string("kernel ") + (name ? name : "(null)") + " is not registered";
+    return -LOAM_ERR(InvalidArgument);
+  }
+  int w = 0;
+  for (const auto& ext : k->extents) {
+    if (w < cap) buf[w] = (int32_t)ext.size();
+    ++w;
+    for (int x : ext) {
+      if (w < cap) buf[w] = x;
+      ++w;
+    }
+  }
+  return (int)k->extents.size();
+}
+
+const char* loam_gpu_kernel_names(void) { return kernel_names().c_str(); }
+
+int loam_gpu_validate(const loam_kernel_desc* kernel, int32_t n, uint64_t iter, const loam_arg_desc* args,
+                      int nargs) {
+  return guarded([&] { validate(kernel, n, iter, args, nargs); });
+}
+
+int loam_gpu_execute(const loam_kernel_desc* kernel, int32_t n, uint64_t iter, const loam_arg_desc* args,
+                     int nargs, void* stream) {
+  return guarded([&] {
+    require_device();
+    execute(kernel, n, iter, args, nargs, as_stream(stream));
+  });
+}
+
+// Host-memory calling convention of the reference: every pointer is host
+// memory.  Uploads maps, patterns and the data the loop reads, runs, downloads
+// every written object, and returns with the results visible on the host.
+int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t n, uint64_t iter,
+                          const loam_arg_desc* args, int nargs, void* stream) {
+  return guarded([&] {
+    require_device();
+    validate(kernel, n, iter, args, nargs); // nothing is copied for an illegal loop
+    cudaStream_t s = as_stream(stream);
+    std::vector<DevBuf<char>> bufs;
+    std::vector<std::pair<const void*, void*>> uploaded; // one copy per host array
+    auto up = [&](const void* host, size_t bytes) -> void* {
+      for (auto& [h, d] : uploaded)
+        if (h == host) return d;
+      bufs.emplace_back(bytes ? bytes : 1, s);
+      if (bytes) LG_CUDA(cudaMemcpyAsync(bufs.back().get(), host, bytes, cudaMemcpyHostToDevice, s));
+      uploaded.emplace_back(host, bufs.back().get());
+      return bufs.back().get();
+    };
+    auto alloc = [&](size_t bytes) -> void* {
+      bufs.emplace_back(bytes ? bytes : 1, s);
+      return bufs.back().get();
+    };
+    std::vector<loam_arg_desc> dargs(args, args + nargs);
+    std::vector<loam_map_desc> dmaps(2 * nargs);
+    std::vector<loam_sparsity_desc> dsp(nargs);
+    auto map_up = [&](const loam_map_desc* m, loam_map_desc& d) {
+      d = *m;
+      d.values = static_cast<const int32_t*>(up(m->values, sizeof(int32_t) * (size_t)m->source_size * m->arity));
+      if (m->expand_dim > 1 && m->node_values)
+        d.node_values = static_cast<const int32_t*>(
+            up(m->node_values, sizeof(int32_t) * (size_t)m->source_size * m->node_arity));
+    };
+    for (int q = 0; q < nargs; ++q) {
+      const loam_arg_desc& a = args[q];
+      loam_arg_desc& d = dargs[q];
+      if (a.map) { map_up(a.map, dmaps[2 * q]); d.map = &dmaps[2 * q]; }
+      if (a.col_map) { map_up(a.col_map, dmaps[2 * q + 1]); d.col_map = &dmaps[2 * q + 1]; }
+      size_t count;
+      if (a.kind == LOAM_ARG_MAT) {
+        const loam_sparsity_desc* sp = a.sparsity;
+        dsp[q] = *sp;
+        dsp[q].row_ptr = static_cast<const int64_t*>(up(sp->row_ptr, sizeof(int64_t) * ((size_t)sp->nrows + 1)));
+        dsp[q].col_idx = static_cast<const int32_t*>(up(sp->col_idx, sizeof(int32_t) * (size_t)sp->nnz));
+        d.sparsity = &dsp[q];
+        count = (size_t)sp->nnz;
+      } else if (a.kind == LOAM_ARG_DAT) {
+        count = (size_t)a.set_size * a.dim;
+      } else {
+        count = (size_t)a.dim;
+      }
+      const bool needs_old = a.access == LOAM_READ || a.access == LOAM_RW ||
+                             (a.access == LOAM_INC && !(a.flags & LOAM_ARG_ZERO)) ||
+                             (a.kind != LOAM_ARG_DAT && a.access == LOAM_WRITE);
+      d.data = static_cast<double*>(needs_old ? up(a.data, sizeof(double) * count) : alloc(sizeof(double) * count));
+      if (!needs_old && a.kind == LOAM_ARG_DAT && a.access == LOAM_WRITE && a.map) {
+        // indirect WRITE leaves untouched entries as they were (test_parloop.cpp:182-200)
+        LG_CUDA(cudaMemcpyAsync(d.data, a.data, sizeof(double) * count, cudaMemcpyHostToDevice, s));
+      }
+    }
+    execute(kernel, n, iter, dargs.data(), nargs, s);
+    for (int q = 0; q < nargs; ++q) {
+      const loam_arg_desc& a = args[q];
+      if (a.access == LOAM_READ) continue;
+      size_t count = a.kind == LOAM_ARG_MAT ? (size_t)a.sparsity->nnz
+                     : a.kind == LOAM_ARG_DAT ? (size_t)a.set_size * a.dim : (size_t)a.dim;
+      if (count) LG_CUDA(cudaMemcpyAsync(a.data, dargs[q].data, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+    }
+    LG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int loam_gpu_map_check(const loam_map_desc* map, void* stream) {
+  return guarded([&] {
+    require_device();
+    map_check(map, as_stream(stream));
+  });
+}
+
+int loam_gpu_build_sparsity(const loam_map_desc* row_map, const loam_map_desc* col_map, int row_dim,
+                            int col_dim, int64_t** row_ptr, int32_t** col_idx, int64_t* nnz, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(row_dim >= 1 && col_dim >= 1, LOAM_ERR(InvalidArgument), "dims must be positive");
+    require(row_map->source_size == col_map->source_size &&
+                (row_map->source_id == 0 || col_map->source_id == 0 || row_map->source_id == col_map->source_id),
+            LOAM_ERR(SourceMismatch), "row and column maps must share their source set");
+    MapView r{row_map->values, row_map->source_size, row_map->arity, row_map->target_size};
+    MapView c{col_map->values, col_map->source_size, col_map->arity, col_map->target_size};
+    build_sparsity_dev(r, c, row_dim, col_dim, row_ptr, col_idx, nnz, as_stream(stream));
+    LG_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  });
+}
+
+int loam_gpu_color_iteration(int32_t n, uint64_t iter, const loam_map_desc* maps, int nmaps, int32_t* colors,
+                             int32_t* num_colors, void* stream) {
+  return guarded([&] {
+    require_device();
+    for (int i = 0; i < nmaps; ++i)
+      require(maps[i].source_id == 0 || iter == 0 || maps[i].source_id == iter, LOAM_ERR(SourceMismatch),
+              "conflict map source differs from iteration set");
+    color_iteration(n, maps, nmaps, colors, num_colors, as_stream(stream));
+  });
+}
+
+int loam_gpu_malloc(void** ptr, size_t bytes) {
+  return guarded([&] {
+    require_device();
+    LG_CUDA(cudaMalloc(ptr, bytes ? bytes : 1));
+  });
+}
+int loam_gpu_free(void* ptr) {
+  return guarded([&] { LG_CUDA(cudaFree(ptr)); });
+}
+int loam_gpu_host_alloc(void** ptr, size_t bytes) {
+  return guarded([&] {
+    require_device();
+    LG_CUDA(cudaMallocHost(ptr, bytes ? bytes : 1));
+  });
+}
+int loam_gpu_host_free(void* ptr) {
+  return guarded([&] { LG_CUDA(cudaFreeHost(ptr)); });
+}
+int loam_gpu_memcpy(void* dst, const void* src, size_t bytes, void* stream) {
+  return guarded([&] { LG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream))); });
+}
+int loam_gpu_memset(void* dst, int value, size_t bytes, void* stream) {
+  return guarded([&] { LG_CUDA(cudaMemsetAsync(dst, value, bytes, as_stream(stream))); });
+}
+int loam_gpu_stream_sync(void* stream) {
+  return guarded([&] { LG_CUDA(cudaStreamSynchronize(as_stream(stream))); });
+}
+
+} // extern "C"

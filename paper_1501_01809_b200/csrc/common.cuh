@@ -1,0 +1,91 @@
+// common.cuh -- error convention, CUDA helpers and device buffers.
+//
+// Errors follow the reference: loam::Error(kind, message) (common.hpp:36-49)
+// becomes an int code 1 + kind with a thread-local message.  Internally the
+// engine throws loam_gpu::Error and the C ABI (capi.cu) converts.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "loam_gpu.h"
+
+namespace loam_gpu {
+
+class Error : public std::runtime_error {
+public:
+  Error(int code, const std::string& what) : std::runtime_error(what), code_(code) {}
+  int code() const { return code_; }
+
+private:
+  int code_;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+inline void require(bool cond, int code, const std::string& msg) {
+  if (!cond) fail(code, msg);
+}
+
+#define LG_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t err_ = (call);                                                           \
+    if (err_ != cudaSuccess)                                                             \
+      ::loam_gpu::fail(LOAM_GPU_ERR_CUDA, std::string(#call) + ": " +                    \
+                                              cudaGetErrorString(err_) + " (" __FILE__ ":" + \
+                                              std::to_string(__LINE__) + ")");           \
+  } while (0)
+
+// Number of kernels launched by this library (bench gpu_launches).
+extern std::atomic<int64_t> g_launches;
+inline void count_launch(int64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+#define LG_LAUNCH_CHECK() LG_CUDA(cudaGetLastError())
+
+// Owned device buffer (stream-ordered allocation from the default mempool).
+template <class T>
+class DevBuf {
+public:
+  DevBuf() = default;
+  DevBuf(size_t n, cudaStream_t s) { alloc(n, s); }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) { o.p_ = nullptr; o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_; n_ = o.n_; s_ = o.s_;
+      o.p_ = nullptr; o.n_ = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t n, cudaStream_t s) {
+    release();
+    s_ = s;
+    n_ = n;
+    if (n) LG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+  }
+  void release() {
+    if (p_) cudaFreeAsync(p_, s_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  size_t bytes() const { return n_ * sizeof(T); }
+
+private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+  cudaStream_t s_ = nullptr;
+};
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+constexpr int kNumSMs = 148; // B200
+
+} // namespace loam_gpu

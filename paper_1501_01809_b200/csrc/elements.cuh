@@ -1,0 +1,450 @@
+// elements.cuh -- element kernels of the form catalogue, B200 (sm_100a) device code.
+//
+// The reference generates one quadrature-loop AST per form and interprets it
+// (fem/form.hpp:201-320 -> kernel.hpp:482-495).  For affine simplices every
+// catalogue integrand is a polynomial in the barycentric coordinates lambda_k
+// whose gradients g_k = grad(lambda_k) are constant per cell, so each local
+// entry is an exact closed form in
+//     V = |detJ| * |reference cell|      (form.hpp:157, quadrature weights sum to |ref|)
+//     g_k (physical barycentric gradients; g_k[a] = K_{a,k-1}, K = J^{-T}, form.hpp:139-178)
+// and a few rational integrals int(lambda^alpha) = V d! alpha! / (|alpha|+d)!.
+// The results equal the reference's quadrature sums up to rounding (the rules
+// are exact for these degrees, element.hpp:31-33); parity is checked at 1e-12.
+//
+// Every form exposes a ROW functor -- local row i of the element tensor,
+// i possibly thread-dependent -- used by the owner-computes gather
+// (engine.cu), and the full tensor is the row functor unrolled over i.
+#pragma once
+#include <cstdint>
+
+namespace loam_gpu {
+
+// Catalogue forms; numbering shared with oracle/loam_oracle.h (orc_form).
+enum FormId : int {
+  F_MASS = 0,
+  F_STIFFNESS = 1,
+  F_HELMHOLTZ = 2,
+  F_MASS_ACTION = 3,
+  F_STIFFNESS_ACTION = 4,
+  F_HELMHOLTZ_ACTION = 5,
+  F_ELASTICITY = 6,
+  F_STOKES_A = 7,
+  F_STOKES_B = 8,
+  F_STOKES_BT = 9,
+};
+
+// Rational barycentric integrals divided by V (d = spatial dimension):
+//   qint(x,y) = int l_x l_y / V          (1+delta)/((d+1)(d+2))
+//   eint(a,x) = int (4 l_a - 1) l_x / V
+// (int l^alpha = V d! alpha! / (|alpha|+d)!), plus the P2 mass constants below.
+template <int D>
+struct Simplex;
+
+template <>
+struct Simplex<2> {
+  // q: 2/4! *2 = 1/6 ; 1/12 ; e_same = 4/6 - 1/3 ; e_diff = 4/12 - 1/3
+  static constexpr double q_same = 1.0 / 6, q_diff = 1.0 / 12;
+  static constexpr double l1 = 1.0 / 3;
+  static constexpr double ref_measure = 0.5;
+  static constexpr int NV = 3, NE = 3;
+  // local edge k of the P2 row -> vertex pair (space.hpp:66-71): (1,2),(0,2),(0,1)
+  __host__ __device__ static constexpr int edge_a(int k) { return k == 0 ? 1 : 0; }
+  __host__ __device__ static constexpr int edge_b(int k) { return k == 2 ? 1 : 2; }
+};
+
+template <>
+struct Simplex<3> {
+  static constexpr double q_same = 1.0 / 10, q_diff = 1.0 / 20;
+  static constexpr double l1 = 1.0 / 4;
+  static constexpr double ref_measure = 1.0 / 6;
+  static constexpr int NV = 4, NE = 6;
+  // extension: (2,3),(1,3),(1,2),(0,3),(0,2),(0,1) -- UFC order; restricted to
+  // the face opposite vertex 3 it reproduces the triangle order above.
+  __host__ __device__ static constexpr int edge_a(int k) {
+    return k == 0 ? 2 : (k == 1 || k == 2) ? 1 : 0;
+  }
+  __host__ __device__ static constexpr int edge_b(int k) {
+    return (k == 0 || k == 1 || k == 3) ? 3 : (k == 2 || k == 4) ? 2 : 1;
+  }
+};
+
+// int l_x l_y / V
+template <int D>
+__host__ __device__ __forceinline__ double qint(int x, int y) {
+  return x == y ? Simplex<D>::q_same : Simplex<D>::q_diff;
+}
+// int (4 l_a - 1) l_x / V
+template <int D>
+__host__ __device__ __forceinline__ double eint(int a, int x) {
+  return 4.0 * qint<D>(a, x) - Simplex<D>::l1;
+}
+
+// ---------------------------------------------------------------------------
+// Geometry: J_ab = X[b+1][a] - X[0][a] (form.hpp:143-146), K = J^{-T}
+// (form.hpp:160-177), V = |detJ| * |ref| (form.hpp:157).
+
+template <int D>
+struct Geom {
+  double g[D + 1][D]; // physical barycentric gradients
+  double V;
+};
+
+template <int D>
+__device__ __forceinline__ void geometry(const double (&X)[D + 1][D], Geom<D>& G) {
+  if constexpr (D == 2) {
+    const double J00 = X[1][0] - X[0][0], J01 = X[2][0] - X[0][0];
+    const double J10 = X[1][1] - X[0][1], J11 = X[2][1] - X[0][1];
+    const double det = J00 * J11 - J01 * J10;
+    const double r = 1.0 / det;
+    // K = [[J11, -J10], [-J01, J00]] / det ; g_k[a] = K[a][k-1]
+    G.g[1][0] = J11 * r;
+    G.g[1][1] = -J01 * r;
+    G.g[2][0] = -J10 * r;
+    G.g[2][1] = J00 * r;
+    G.g[0][0] = -(G.g[1][0] + G.g[2][0]);
+    G.g[0][1] = -(G.g[1][1] + G.g[2][1]);
+    G.V = fabs(det) * 0.5;
+  } else {
+    double J[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) J[a][b] = X[b + 1][a] - X[0][a];
+    const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const double c01 = -(J[1][0] * J[2][2] - J[1][2] * J[2][0]);
+    const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    const double c10 = -(J[0][1] * J[2][2] - J[0][2] * J[2][1]);
+    const double c11 = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    const double c12 = -(J[0][0] * J[2][1] - J[0][1] * J[2][0]);
+    const double c20 = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    const double c21 = -(J[0][0] * J[1][2] - J[0][2] * J[1][0]);
+    const double c22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double r = 1.0 / det;
+    // g_k[a] = K[a][k-1] = c[a][k-1] / det
+    G.g[1][0] = c00 * r; G.g[1][1] = c10 * r; G.g[1][2] = c20 * r;
+    G.g[2][0] = c01 * r; G.g[2][1] = c11 * r; G.g[2][2] = c21 * r;
+    G.g[3][0] = c02 * r; G.g[3][1] = c12 * r; G.g[3][2] = c22 * r;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) G.g[0][a] = -(G.g[1][a] + G.g[2][a] + G.g[3][a]);
+    G.V = fabs(det) * (1.0 / 6.0);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ double dot(const double* a, const double* b) {
+  double s = a[0] * b[0];
+#pragma unroll
+  for (int k = 1; k < D; ++k) s = fma(a[k], b[k], s);
+  return s;
+}
+
+// Select vector k of g with a runtime k without dynamic register indexing.
+template <int D>
+__device__ __forceinline__ void sel(const Geom<D>& G, int k, double (&out)[D]) {
+#pragma unroll
+  for (int a = 0; a < D; ++a) out[a] = G.g[0][a];
+#pragma unroll
+  for (int m = 1; m <= D; ++m)
+    if (k == m)
+#pragma unroll
+      for (int a = 0; a < D; ++a) out[a] = G.g[m][a];
+}
+
+// ---------------------------------------------------------------------------
+// Scalar Lagrange P1 / P2: entries of stiffness (grad.grad) and mass.
+
+// P1: int grad l_i . grad l_j = V g_i.g_j ; int l_i l_j = V qint(i,j)
+
+// P2 basis: node n < NV is vertex n with phi = l_n(2 l_n - 1), grad = (4 l_n - 1) g_n;
+// node NV+k is edge (a,b) with phi = 4 l_a l_b, grad = 4 (l_b g_a + l_a g_b).
+// int grad phi_i . grad phi_j / V is a combination of D_kl = g_k.g_l with
+// rational weights.  Row state: the i-dependent vectors, selected once per row.
+template <int D>
+struct P2Row {
+  int i, a, b;        // vertex row: a = i; edge row: (a, b)
+  bool vertex;
+  double ga[D], gb[D];
+  __device__ __forceinline__ P2Row(const Geom<D>& G, int i_) : i(i_) {
+    constexpr int NV = Simplex<D>::NV;
+    vertex = i < NV;
+    a = vertex ? i : Simplex<D>::edge_a(i - NV);
+    b = vertex ? i : Simplex<D>::edge_b(i - NV);
+    sel<D>(G, a, ga);
+    sel<D>(G, b, gb);
+  }
+  // stiffness entry (i, j) for a compile-time j, times 1/V
+  __device__ __forceinline__ double stiff(const Geom<D>& G, int j) const {
+    constexpr int NV = Simplex<D>::NV;
+    if (vertex) {
+      if (j < NV) {
+        const double c = i == j ? 16.0 * Simplex<D>::q_same - 8.0 * Simplex<D>::l1 + 1.0
+                                : 16.0 * Simplex<D>::q_diff - 8.0 * Simplex<D>::l1 + 1.0;
+        return c * dot<D>(ga, G.g[j]);
+      }
+      const int c = Simplex<D>::edge_a(j - NV), d = Simplex<D>::edge_b(j - NV);
+      return 4.0 * (eint<D>(a, d) * dot<D>(ga, G.g[c]) + eint<D>(a, c) * dot<D>(ga, G.g[d]));
+    }
+    if (j < NV)
+      return 4.0 * (eint<D>(j, b) * dot<D>(ga, G.g[j]) + eint<D>(j, a) * dot<D>(gb, G.g[j]));
+    const int c = Simplex<D>::edge_a(j - NV), d = Simplex<D>::edge_b(j - NV);
+    return 16.0 * (qint<D>(b, d) * dot<D>(ga, G.g[c]) + qint<D>(b, c) * dot<D>(ga, G.g[d]) +
+                   qint<D>(a, d) * dot<D>(gb, G.g[c]) + qint<D>(a, c) * dot<D>(gb, G.g[d]));
+  }
+};
+
+
+// int phi_i phi_j / V for P2 (exact rationals, classified by index coincidence).
+template <int D>
+__host__ __device__ constexpr double p2_mass_const(int kind);
+// kinds: 0 vv diag, 1 vv off, 2 ve vertex-in-edge, 3 ve vertex-not-in-edge,
+//        4 ee same, 5 ee sharing one vertex, 6 ee disjoint
+template <>
+__host__ __device__ constexpr double p2_mass_const<2>(int kind) {
+  // triangle: diag 6/180, off -1/180, ve in 0, ve out -4/180, ee same 32/180, share 16/180
+  return kind == 0 ? 6.0 / 180 : kind == 1 ? -1.0 / 180 : kind == 2 ? 0.0 : kind == 3 ? -4.0 / 180
+       : kind == 4 ? 32.0 / 180 : kind == 5 ? 16.0 / 180 : 0.0;
+}
+template <>
+__host__ __device__ constexpr double p2_mass_const<3>(int kind) {
+  // tetrahedron (x 1/420): diag 6, off 1, ve in -4, ve out -6, ee same 32, share 16, disjoint 8
+  return kind == 0 ? 6.0 / 420 : kind == 1 ? 1.0 / 420 : kind == 2 ? -4.0 / 420 : kind == 3 ? -6.0 / 420
+       : kind == 4 ? 32.0 / 420 : kind == 5 ? 16.0 / 420 : 8.0 / 420;
+}
+
+template <int D>
+__host__ __device__ __forceinline__ int p2_mass_kind(int i, int j) {
+  constexpr int NV = Simplex<D>::NV;
+  if (i < NV && j < NV) return i == j ? 0 : 1;
+  if (i < NV || j < NV) {
+    const int v = i < NV ? i : j, e = (i < NV ? j : i) - NV;
+    return (Simplex<D>::edge_a(e) == v || Simplex<D>::edge_b(e) == v) ? 2 : 3;
+  }
+  const int a = Simplex<D>::edge_a(i - NV), b = Simplex<D>::edge_b(i - NV);
+  const int c = Simplex<D>::edge_a(j - NV), d = Simplex<D>::edge_b(j - NV);
+  const int shared = (a == c) + (a == d) + (b == c) + (b == d);
+  return i == j ? 4 : shared == 1 ? 5 : 6;
+}
+
+template <int D, int P>
+struct Lagrange {
+  static constexpr int N = P == 1 ? D + 1 : (D == 2 ? 6 : 10);
+};
+
+// ---------------------------------------------------------------------------
+// Form traits.  For each form:
+//   NR, NC       local row / column count of the staged tensor (A extents)
+//   NRN, NCN     node arity of the row / column maps (NR = NRN*RD)
+//   RD, CD       dof expansion of rows / columns (vector spaces)
+//   HAS_COEFF    linear (action) forms read a coefficient through the test map
+//   row(i, G, C, prm, out)   out[0..NC) = row i of the tensor (RD=CD=1 scalar case)
+// Vector forms produce the node-row block: rows (i, 0..RD), cols NC.
+
+struct FormParams {
+  double p[4];
+};
+
+template <int FORM, int D, int P>
+struct FormT;
+
+// Bilinear scalar forms: mass / stiffness / helmholtz (form.hpp:263-283)
+template <int FORM, int D, int P>
+struct ScalarBilinear {
+  static constexpr int N = Lagrange<D, P>::N;
+  static constexpr int NR = N, NC = N, NRN = N, NCN = N, RD = 1, CD = 1, GD = D;
+  static constexpr bool HAS_COEFF = false, BILINEAR = true;
+  static constexpr int NCOEFF = 0;
+  __device__ __forceinline__ static void row(int i, const Geom<D>& G, const double*,
+                                             const FormParams& prm, double* out) {
+    if constexpr (P == 1) {
+      double gi[D];
+      sel<D>(G, i, gi);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const double k = dot<D>(gi, G.g[j]), m = qint<D>(i, j);
+        double v;
+        if constexpr (FORM == F_MASS) v = m;
+        else if constexpr (FORM == F_STIFFNESS) v = k;
+        else v = fma(prm.p[0], m, k);
+        out[j] = G.V * v;
+      }
+    } else {
+      const P2Row<D> R(G, i);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double v;
+        if constexpr (FORM == F_MASS) v = p2_mass_const<D>(p2_mass_kind<D>(i, j));
+        else if constexpr (FORM == F_STIFFNESS) v = R.stiff(G, j);
+        else v = fma(prm.p[0], p2_mass_const<D>(p2_mass_kind<D>(i, j)), R.stiff(G, j));
+        out[j] = G.V * v;
+      }
+    }
+  }
+};
+template <int D, int P> struct FormT<F_MASS, D, P> : ScalarBilinear<F_MASS, D, P> {};
+template <int D, int P> struct FormT<F_STIFFNESS, D, P> : ScalarBilinear<F_STIFFNESS, D, P> {};
+template <int D, int P> struct FormT<F_HELMHOLTZ, D, P> : ScalarBilinear<F_HELMHOLTZ, D, P> {};
+
+// Linear action forms: b_i = sum_j A_ij C_j (form.hpp:288-312); helmholtz
+// action = stiffness action + kappa * mass action in one loop.
+template <int FORM, int D, int P>
+struct ScalarAction {
+  static constexpr int N = Lagrange<D, P>::N;
+  static constexpr int NR = N, NC = 1, NRN = N, NCN = 0, RD = 1, CD = 1, GD = D;
+  static constexpr bool HAS_COEFF = true, BILINEAR = false;
+  static constexpr int NCOEFF = N;
+  __device__ __forceinline__ static void row(int i, const Geom<D>& G, const double* C,
+                                             const FormParams& prm, double* out) {
+    if constexpr (P == 1) {
+      double gi[D], gu[D];
+      sel<D>(G, i, gi);
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        double s = C[0] * G.g[0][a];
+#pragma unroll
+        for (int k = 1; k < N; ++k) s = fma(C[k], G.g[k][a], s);
+        gu[a] = s;
+      }
+      double b = 0.0;
+      if constexpr (FORM != F_MASS_ACTION) b = G.V * dot<D>(gi, gu);
+      if constexpr (FORM != F_STIFFNESS_ACTION) {
+        double sum = C[0], ci = C[0];
+#pragma unroll
+        for (int k = 1; k < N; ++k) {
+          sum += C[k];
+          if (k == i) ci = C[k];
+        }
+        // int l_i sum_k C_k l_k = V (q_diff sum_k C_k + (q_same - q_diff) C_i)
+        const double m = G.V * fma(Simplex<D>::q_same - Simplex<D>::q_diff, ci, Simplex<D>::q_diff * sum);
+        b = FORM == F_MASS_ACTION ? m : fma(prm.p[0], m, b);
+      }
+      out[0] = b;
+    } else {
+      const P2Row<D> R(G, i);
+      double b = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double a;
+        if constexpr (FORM == F_MASS_ACTION) a = p2_mass_const<D>(p2_mass_kind<D>(i, j));
+        else if constexpr (FORM == F_STIFFNESS_ACTION) a = R.stiff(G, j);
+        else a = fma(prm.p[0], p2_mass_const<D>(p2_mass_kind<D>(i, j)), R.stiff(G, j));
+        b = fma(a, C[j], b);
+      }
+      out[0] = G.V * b;
+    }
+  }
+};
+template <int D, int P> struct FormT<F_MASS_ACTION, D, P> : ScalarAction<F_MASS_ACTION, D, P> {};
+template <int D, int P> struct FormT<F_STIFFNESS_ACTION, D, P> : ScalarAction<F_STIFFNESS_ACTION, D, P> {};
+template <int D, int P> struct FormT<F_HELMHOLTZ_ACTION, D, P> : ScalarAction<F_HELMHOLTZ_ACTION, D, P> {};
+
+// Linear elasticity, vector P1 tet (config 4): a(u,v) = int 2 mu eps(u):eps(v)
+// + lambda div u div v.  Local dof (a,d) = a*3+d.  Entry
+//   V [ mu d_de (g_a.g_b) + mu g_a[e] g_b[d] + lambda g_a[d] g_b[e] ].
+template <>
+struct FormT<F_ELASTICITY, 3, 1> {
+  static constexpr int NR = 12, NC = 12, NRN = 4, NCN = 4, RD = 3, CD = 3, GD = 3;
+  static constexpr bool HAS_COEFF = false, BILINEAR = true;
+  static constexpr int NCOEFF = 0;
+  // out: RD x NC block for node row a
+  __device__ __forceinline__ static void row(int a, const Geom<3>& G, const double*,
+                                             const FormParams& prm, double* out) {
+    const double lam = prm.p[0], mu = prm.p[1];
+    double ga[3];
+    sel<3>(G, a, ga);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const double gg = mu * dot<3>(ga, G.g[b]);
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          double v = fma(mu * ga[e], G.g[b][d], lam * ga[d] * G.g[b][e]);
+          if (d == e) v += gg;
+          out[d * 12 + b * 3 + e] = G.V * v;
+        }
+    }
+  }
+};
+
+// Taylor-Hood Stokes blocks (config 5), velocity vector P2 tri (dof (b,e) = b*2+e),
+// pressure P1 tri.
+//   A  = nu int grad u : grad v      (component-diagonal)           12 x 12
+//   B  = - int q div u               pressure rows, velocity cols   3 x 12
+//   BT = B^T                         velocity rows, pressure cols   12 x 3
+template <>
+struct FormT<F_STOKES_A, 2, 2> {
+  static constexpr int NR = 12, NC = 12, NRN = 6, NCN = 6, RD = 2, CD = 2, GD = 2;
+  static constexpr bool HAS_COEFF = false, BILINEAR = true;
+  static constexpr int NCOEFF = 0;
+  __device__ __forceinline__ static void row(int a, const Geom<2>& G, const double*,
+                                             const FormParams& prm, double* out) {
+    const P2Row<2> R(G, a);
+    const double scale = prm.p[0] * G.V;
+#pragma unroll
+    for (int b = 0; b < 6; ++b) {
+      const double s = scale * R.stiff(G, b);
+      out[0 * 12 + b * 2 + 0] = s;
+      out[0 * 12 + b * 2 + 1] = 0.0;
+      out[1 * 12 + b * 2 + 0] = 0.0;
+      out[1 * 12 + b * 2 + 1] = s;
+    }
+  }
+};
+
+// int l_p d_e phi_b / V for pressure basis p (P1) and velocity node b (P2):
+//   vertex b: (4 l_b - 1) g_b[e] -> eint(b,p) g_b[e]
+//   edge (x,y): 4 (l_y g_x[e] + l_x g_y[e]) -> 4 (q(p,y) g_x[e] + q(p,x) g_y[e])
+template <>
+struct FormT<F_STOKES_B, 2, 2> {
+  static constexpr int NR = 3, NC = 12, NRN = 3, NCN = 6, RD = 1, CD = 2, GD = 2;
+  static constexpr bool HAS_COEFF = false, BILINEAR = true;
+  static constexpr int NCOEFF = 0;
+  __device__ __forceinline__ static void row(int p, const Geom<2>& G, const double*,
+                                             const FormParams&, double* out) {
+#pragma unroll
+    for (int b = 0; b < 6; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double v;
+        if (b < 3) {
+          v = eint<2>(b, p) * G.g[b][e];
+        } else {
+          const int x = Simplex<2>::edge_a(b - 3), y = Simplex<2>::edge_b(b - 3);
+          v = 4.0 * (qint<2>(p, y) * G.g[x][e] + qint<2>(p, x) * G.g[y][e]);
+        }
+        out[b * 2 + e] = -G.V * v;
+      }
+  }
+};
+
+template <>
+struct FormT<F_STOKES_BT, 2, 2> {
+  static constexpr int NR = 12, NC = 3, NRN = 6, NCN = 3, RD = 2, CD = 1, GD = 2;
+  static constexpr bool HAS_COEFF = false, BILINEAR = true;
+  static constexpr int NCOEFF = 0;
+  __device__ __forceinline__ static void row(int b, const Geom<2>& G, const double*,
+                                             const FormParams&, double* out) {
+    const P2Row<2> R(G, b); // vertex: ga = g_b ; edge (x,y): ga = g_x, gb = g_y
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const double v = R.vertex ? eint<2>(b, p) * R.ga[e]
+                                  : 4.0 * (qint<2>(p, R.b) * R.ga[e] + qint<2>(p, R.a) * R.gb[e]);
+        out[e * 3 + p] = -G.V * v;
+      }
+  }
+};
+
+// Full local tensor (NR x NC, row-major, the staged layout of staged_extents,
+// parloop.hpp:63-70): unrolled row functor.  For vector forms node row a
+// covers tensor rows a*RD .. a*RD+RD-1.
+template <class F>
+__device__ __forceinline__ void element_tensor(const Geom<F::GD>& G, const double* C,
+                                               const FormParams& prm, double* A) {
+#pragma unroll
+  for (int a = 0; a < F::NRN; ++a) F::row(a, G, C, prm, A + a * F::RD * F::NC);
+}
+
+} // namespace loam_gpu

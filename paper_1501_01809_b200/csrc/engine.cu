@@ -1,0 +1,973 @@
+// engine.cu -- the B200 par_loop engine: registry, validate, execute.
+//
+// Replaces loam::execute (parloop.hpp:191-384).  Two device paths:
+//
+//  * OWNER-COMPUTES (default for catalogue forms with the assemble_* argument
+//    pattern, assemble.hpp:91-99,123-129): one thread owns one row node and
+//    gathers every (cell, local index) pair incident to it (plan.cuh), computes
+//    its element rows in registers and writes each output entry exactly once
+//    -- no atomics, no zero-fill pass, deterministic sums.  Mats accumulate a
+//    warp's contiguous CSR segment in shared memory and store it coalesced.
+//  * CELL-MAJOR generic staging engine for any registered kernel and any
+//    access mix (the reference's stage-in / kernel / stage-out, parloop.hpp:
+//    253-320): indirect INC through fp64 atomics, or -- when a loop writes
+//    indirectly with WRITE/RW, or the colouring strategy is selected -- one
+//    launch per colour of the bit-exact greedy colouring with plain stores.
+//    Global reductions go through per-entity slots and a fixed-shape tree.
+//
+// There is no CPU fallback: an unregistered kernel is an error.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <unordered_map>
+
+#include "elements.cuh"
+#include "engine.cuh"
+#include "plan.cuh"
+#include "test_kernels.cuh"
+
+namespace loam_gpu {
+
+std::atomic<int64_t> g_launches{0};
+
+Options& options() {
+  static Options o;
+  return o;
+}
+
+namespace {
+
+constexpr int kMaxArgs = 8;
+constexpr int kTPB = 256;
+
+// ===========================================================================
+// Generic cell-major staging engine
+// ===========================================================================
+
+struct GArg {
+  int kind, access, dim;
+  double* data;
+  const int32_t* map;
+  int arity;
+  const int32_t* map2;
+  int arity2;
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  int nrows;
+  int off, size;   // staging slot
+  int slot_off;    // Global reduction slot offset within an entity's slots
+};
+
+struct GLaunch {
+  int nargs;
+  GArg a[kMaxArgs];
+  const int32_t* order; // entity list (nullptr: identity)
+  int count;
+  int plain;            // entities of one launch are conflict-free: plain RMW
+  int slot_stride;
+  double* slots;        // [n * slot_stride] Global contributions
+  FormParams prm;
+  unsigned long long* err;
+};
+
+__device__ __forceinline__ double red_identity(int access) {
+  return access == LOAM_SUM ? 0.0 : (access == LOAM_MIN ? __longlong_as_double(0x7ff0000000000000ll)
+                                                        : __longlong_as_double(0xfff0000000000000ll));
+}
+
+__device__ __forceinline__ int64_t csr_find(const int64_t* rp, const int32_t* ci, int nrows, int row,
+                                            int col) {
+  if (row < 0 || row >= nrows) return -1;
+  int64_t lo = rp[row], hi = rp[row + 1];
+  const int64_t end = hi;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (ci[mid] < col) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo == end || ci[lo] != col) ? -1 : lo;
+}
+
+template <class K>
+__global__ void k_generic(const __grid_constant__ GLaunch L) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= L.count) return;
+  const int e = L.order ? L.order[t] : t;
+  double stage[K::STAGE];
+  double* ptrs[kMaxArgs];
+  // ---- stage in (parloop.hpp:254-283)
+  for (int k = 0; k < L.nargs; ++k) {
+    const GArg& a = L.a[k];
+    double* st = stage + a.off;
+    ptrs[k] = st;
+    if (a.kind == LOAM_ARG_DAT) {
+      if (a.access == LOAM_WRITE || a.access == LOAM_INC) {
+        for (int x = 0; x < a.size; ++x) st[x] = 0.0;
+      } else if (!a.map) {
+        for (int d = 0; d < a.dim; ++d) st[d] = a.data[(int64_t)e * a.dim + d];
+      } else {
+        for (int q = 0; q < a.arity; ++q) {
+          const int64_t base = (int64_t)a.map[(int64_t)e * a.arity + q] * a.dim;
+          for (int d = 0; d < a.dim; ++d) st[q * a.dim + d] = a.data[base + d];
+        }
+      }
+    } else if (a.kind == LOAM_ARG_MAT) {
+      for (int x = 0; x < a.size; ++x) st[x] = 0.0;
+    } else {
+      if (a.access == LOAM_READ)
+        for (int d = 0; d < a.dim; ++d) st[d] = a.data[d];
+      else
+        for (int d = 0; d < a.dim; ++d) st[d] = red_identity(a.access);
+    }
+  }
+  K::run(ptrs, L.prm);
+  // ---- stage out (parloop.hpp:287-319)
+  for (int k = 0; k < L.nargs; ++k) {
+    const GArg& a = L.a[k];
+    const double* st = stage + a.off;
+    if (a.kind == LOAM_ARG_DAT) {
+      if (a.access == LOAM_READ) continue;
+      if (!a.map) {
+        double* dst = a.data + (int64_t)e * a.dim;
+        for (int d = 0; d < a.dim; ++d) dst[d] = a.access == LOAM_INC ? dst[d] + st[d] : st[d];
+      } else {
+        for (int q = 0; q < a.arity; ++q) {
+          double* dst = a.data + (int64_t)a.map[(int64_t)e * a.arity + q] * a.dim;
+          for (int d = 0; d < a.dim; ++d) {
+            const double v = st[q * a.dim + d];
+            if (a.access != LOAM_INC) dst[d] = v; // WRITE/RW: coloured launches only
+            else if (L.plain) dst[d] += v;
+            else atomicAdd(dst + d, v);
+          }
+        }
+      }
+    } else if (a.kind == LOAM_ARG_MAT) {
+      // Mat::addto (data.hpp:205-222)
+      for (int i = 0; i < a.arity; ++i) {
+        const int row = a.map[(int64_t)e * a.arity + i];
+        for (int j = 0; j < a.arity2; ++j) {
+          const int col = a.map2[(int64_t)e * a.arity2 + j];
+          const int64_t pos = csr_find(a.row_ptr, a.col_idx, a.nrows, row, col);
+          if (pos < 0) {
+            atomicCAS(L.err, 0ull, (1ull << 63) | ((unsigned long long)(uint32_t)row << 32) | (uint32_t)col);
+            continue;
+          }
+          const double v = st[i * a.arity2 + j];
+          if (a.access == LOAM_WRITE) a.data[pos] = v;
+          else if (L.plain) a.data[pos] += v;
+          else atomicAdd(a.data + pos, v);
+        }
+      }
+    } else if (a.access != LOAM_READ) {
+      double* slot = L.slots + (int64_t)e * L.slot_stride + a.slot_off;
+      for (int d = 0; d < a.dim; ++d) slot[d] = st[d];
+    }
+  }
+}
+
+// Fixed-shape tree reduction of Global slots over entities 0..n-1 into dst.
+__global__ void k_global_reduce(const double* __restrict__ slots, int n, int stride, int off,
+                                int access, double* dst) {
+  __shared__ double sh[kTPB];
+  const int d = blockIdx.x;
+  double acc = red_identity(access);
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const double v = slots[(int64_t)e * stride + off + d];
+    acc = access == LOAM_SUM ? acc + v : (access == LOAM_MIN ? fmin(acc, v) : fmax(acc, v));
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double a = sh[threadIdx.x], b = sh[threadIdx.x + w];
+      sh[threadIdx.x] = access == LOAM_SUM ? a + b : (access == LOAM_MIN ? fmin(a, b) : fmax(a, b));
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) dst[d] = sh[0];
+}
+
+__global__ void k_fill_identity(double* dst, int dim, int access) {
+  if (threadIdx.x < dim) dst[threadIdx.x] = red_identity(access);
+}
+
+// Catalogue form as a staged kernel: A = element tensor(X, C)  (form.hpp:201-320).
+template <class F>
+struct FormKernel {
+  static constexpr int STAGE = F::NR * F::NC + (F::GD + 1) * F::GD + (F::HAS_COEFF ? F::NCOEFF : 0);
+  __device__ static void run(double* const* p, const FormParams& prm) {
+    double X[F::GD + 1][F::GD];
+#pragma unroll
+    for (int v = 0; v <= F::GD; ++v)
+#pragma unroll
+      for (int d = 0; d < F::GD; ++d) X[v][d] = p[1][v * F::GD + d];
+    Geom<F::GD> G;
+    geometry<F::GD>(X, G);
+    element_tensor<F>(G, F::HAS_COEFF ? p[2] : nullptr, prm, p[0]);
+  }
+};
+
+// ===========================================================================
+// Owner-computes kernels
+// ===========================================================================
+
+struct OwnerArgs {
+  const int32_t* ptr;
+  const int32_t* pairs;
+  const uint8_t* ranks;
+  const int32_t* xmap;
+  int xstride;
+  const double* coords;
+  const int32_t* cmap;
+  int cstride;
+  const double* coeff;
+  FormParams prm;
+  double* out;
+  const int64_t* row_ptr;
+  const int32_t* chunk_row;
+  int nchunks, seg_max, nrows_node, accumulate;
+};
+
+template <class F>
+__device__ __forceinline__ void gather_geom(const OwnerArgs& a, int s, Geom<F::GD>& G) {
+  constexpr int GD = F::GD;
+  double X[GD + 1][GD];
+  const int32_t* xr = a.xmap + (int64_t)s * a.xstride;
+#pragma unroll
+  for (int v = 0; v <= GD; ++v) {
+    const int vid = __ldg(xr + v);
+    if constexpr (GD == 2) {
+      const double2 c = __ldg(reinterpret_cast<const double2*>(a.coords) + vid);
+      X[v][0] = c.x;
+      X[v][1] = c.y;
+    } else {
+#pragma unroll
+      for (int d = 0; d < GD; ++d) X[v][d] = __ldg(a.coords + (int64_t)vid * GD + d);
+    }
+  }
+  geometry<GD>(X, G);
+}
+
+// Residual (Dat INC, dim 1): out[r] (+)= sum over pairs of row i of the action.
+template <class F>
+__global__ void __launch_bounds__(kTPB) k_owner_vec(const __grid_constant__ OwnerArgs a) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.nrows_node) return;
+  double acc = 0.0;
+  const int p1 = __ldg(a.ptr + r + 1);
+  for (int p = __ldg(a.ptr + r); p < p1; ++p) {
+    const int k = __ldg(a.pairs + p);
+    const int s = k / F::NRN, i = k - s * F::NRN;
+    Geom<F::GD> G;
+    gather_geom<F>(a, s, G);
+    double C[F::HAS_COEFF ? F::NCOEFF : 1];
+    if constexpr (F::HAS_COEFF) {
+      const int32_t* cr = a.cmap + (int64_t)s * a.cstride;
+#pragma unroll
+      for (int q = 0; q < F::NCOEFF; ++q) C[q] = __ldg(a.coeff + __ldg(cr + q));
+    }
+    double v;
+    F::row(i, G, C, a.prm, &v);
+    acc += v;
+  }
+  a.out[r] = a.accumulate ? a.out[r] + acc : acc;
+}
+
+// Matrix (Mat INC): one warp per chunk of consecutive row nodes, one lane per
+// row node; the chunk's CSR value segment lives in shared memory.
+template <class F>
+__global__ void __launch_bounds__(128) k_owner_mat(const __grid_constant__ OwnerArgs a) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int chunk = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (chunk >= a.nchunks) return;
+  double* seg = smem + (threadIdx.x >> 5) * a.seg_max;
+  const int r0 = __ldg(a.chunk_row + chunk), r1 = __ldg(a.chunk_row + chunk + 1);
+  const int64_t base = __ldg(a.row_ptr + (int64_t)r0 * F::RD);
+  const int len = (int)(__ldg(a.row_ptr + (int64_t)r1 * F::RD) - base);
+  if (a.accumulate)
+    for (int t = lane; t < len; t += 32) seg[t] = a.out[base + t];
+  else
+    for (int t = lane; t < len; t += 32) seg[t] = 0.0;
+  __syncwarp();
+  const int r = r0 + lane;
+  if (r < r1) {
+    const int64_t rs = __ldg(a.row_ptr + (int64_t)r * F::RD);
+    const int rstart = (int)(rs - base);
+    const int nlen = (int)((__ldg(a.row_ptr + (int64_t)r * F::RD + 1) - rs) / F::CD); // column nodes
+    const int p1 = __ldg(a.ptr + r + 1);
+    for (int p = __ldg(a.ptr + r); p < p1; ++p) {
+      const int k = __ldg(a.pairs + p);
+      const int s = k / F::NRN, i = k - s * F::NRN;
+      Geom<F::GD> G;
+      gather_geom<F>(a, s, G);
+      double blk[F::RD * F::NC];
+      F::row(i, G, nullptr, a.prm, blk);
+      const uint8_t* rk = a.ranks + (int64_t)p * F::NCN;
+#pragma unroll
+      for (int j = 0; j < F::NCN; ++j) {
+        const int pos = rstart + __ldg(rk + j) * F::CD;
+#pragma unroll
+        for (int d = 0; d < F::RD; ++d)
+#pragma unroll
+          for (int c = 0; c < F::CD; ++c) seg[pos + d * nlen * F::CD + c] += blk[d * F::NC + j * F::CD + c];
+      }
+    }
+  }
+  __syncwarp();
+  for (int t = lane; t < len; t += 32) a.out[base + t] = seg[t];
+}
+
+// ===========================================================================
+// Registry
+// ===========================================================================
+
+using GenericFn = void (*)(const GLaunch&, cudaStream_t);
+using OwnerFn = void (*)(const OwnerArgs&, int grid, size_t smem, cudaStream_t);
+
+struct Entry {
+  KernelInfo info;
+  GenericFn generic = nullptr;
+  int stage = 0;
+  // catalogue form traits (form < 0: plain staged kernel)
+  int form = -1, gd = 0, nrn = 0, ncn = 0, rd = 1, cd = 1, ncoeff = 0;
+  bool bilinear = false, has_coeff = false;
+  OwnerFn owner = nullptr;
+};
+
+template <class K>
+void launch_generic(const GLaunch& L, cudaStream_t s) {
+  if (L.count == 0) return;
+  k_generic<K><<<ceil_div(L.count, kTPB), kTPB, 0, s>>>(L);
+  count_launch();
+  LG_LAUNCH_CHECK();
+}
+
+template <class F>
+void launch_owner(const OwnerArgs& a, int grid, size_t smem, cudaStream_t s) {
+  if (grid == 0) return;
+  if constexpr (F::BILINEAR) {
+    static bool attr = [] {
+      cudaFuncSetAttribute(k_owner_mat<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      return true;
+    }();
+    (void)attr;
+    k_owner_mat<F><<<grid, 128, smem, s>>>(a);
+  } else {
+    k_owner_vec<F><<<grid, kTPB, 0, s>>>(a);
+  }
+  count_launch();
+  LG_LAUNCH_CHECK();
+}
+
+template <class K>
+Entry plain_entry(const char* name, std::vector<std::string> names, std::vector<std::vector<int>> ext) {
+  Entry e;
+  e.info = KernelInfo{name, std::move(names), std::move(ext)};
+  e.generic = &launch_generic<K>;
+  e.stage = K::STAGE;
+  return e;
+}
+
+template <int FORM, int D, int P>
+Entry form_entry(const std::string& name) {
+  using F = FormT<FORM, D, P>;
+  Entry e;
+  e.info.name = name;
+  e.info.param_names = {"A", "X"};
+  if (F::BILINEAR) e.info.extents = {{F::NR, F::NC}, {D + 1, D}};
+  else e.info.extents = {{F::NR}, {D + 1, D}};
+  if (F::HAS_COEFF) {
+    e.info.param_names.push_back("C");
+    e.info.extents.push_back({F::NCOEFF});
+  }
+  e.generic = &launch_generic<FormKernel<F>>;
+  e.stage = FormKernel<F>::STAGE;
+  e.form = FORM;
+  e.gd = D;
+  e.nrn = F::NRN;
+  e.ncn = F::NCN;
+  e.rd = F::RD;
+  e.cd = F::CD;
+  e.ncoeff = F::NCOEFF;
+  e.bilinear = F::BILINEAR;
+  e.has_coeff = F::HAS_COEFF;
+  e.owner = &launch_owner<F>;
+  return e;
+}
+
+template <int D, int P>
+void add_scalar_forms(std::map<std::string, Entry>& r) {
+  const std::string sfx = std::string("_p") + std::to_string(P) + (D == 2 ? "_tri" : "_tet");
+  // names as compile_cell_kernel builds them (form.hpp:214-222)
+  r["mass" + sfx] = form_entry<F_MASS, D, P>("mass" + sfx);
+  r["stiffness" + sfx] = form_entry<F_STIFFNESS, D, P>("stiffness" + sfx);
+  r["helmholtz" + sfx] = form_entry<F_HELMHOLTZ, D, P>("helmholtz" + sfx);
+  r["mass_action" + sfx] = form_entry<F_MASS_ACTION, D, P>("mass_action" + sfx);
+  r["source" + sfx] = form_entry<F_MASS_ACTION, D, P>("source" + sfx); // interpolated density
+  r["stiffness_action" + sfx] = form_entry<F_STIFFNESS_ACTION, D, P>("stiffness_action" + sfx);
+  r["helmholtz_action" + sfx] = form_entry<F_HELMHOLTZ_ACTION, D, P>("helmholtz_action" + sfx);
+}
+
+const std::map<std::string, Entry>& registry() {
+  static const std::map<std::string, Entry> r = [] {
+    std::map<std::string, Entry> m;
+    add_scalar_forms<2, 1>(m);
+    add_scalar_forms<2, 2>(m);
+    add_scalar_forms<3, 1>(m);
+    add_scalar_forms<3, 2>(m);
+    m["elasticity_p1_tet"] = form_entry<F_ELASTICITY, 3, 1>("elasticity_p1_tet");
+    m["stokes_a_p2_tri"] = form_entry<F_STOKES_A, 2, 2>("stokes_a_p2_tri");
+    m["stokes_b_p2_tri"] = form_entry<F_STOKES_B, 2, 2>("stokes_b_p2_tri");
+    m["stokes_bt_p2_tri"] = form_entry<F_STOKES_BT, 2, 2>("stokes_bt_p2_tri");
+    using namespace testk;
+    m["double_direct"] = plain_entry<DoubleDirect>("double_direct", {"A", "B"}, {{1}, {1}});
+    m["add_one"] = plain_entry<AddOne>("add_one", {"V"}, {{3}});
+    m["ones_block"] = plain_entry<OnesBlock>("ones_block", {"A"}, {{3, 3}});
+    m["weighted_scatter"] = plain_entry<WeightedScatter>("weighted_scatter", {"V", "X"}, {{3}, {1}});
+    m["bump"] = plain_entry<Bump>("bump", {"V"}, {{3}});
+    m["fill"] = plain_entry<Fill>("fill", {"V"}, {{2}});
+    m["sum"] = plain_entry<Sum>("sum", {"G", "X"}, {{1}, {1}});
+    m["maxval"] = plain_entry<MaxVal>("maxval", {"G", "X"}, {{1}, {1}});
+    m["sumcells"] = plain_entry<SumCells>("sumcells", {"G", "X"}, {{1}, {1}});
+    m["dw"] = plain_entry<Dw>("dw", {"A", "B"}, {{1}, {1}});
+    m["drw"] = plain_entry<Drw>("drw", {"A", "B"}, {{1}, {1}});
+    m["dinc"] = plain_entry<Dinc>("dinc", {"A", "B"}, {{1}, {1}});
+    m["gw"] = plain_entry<Gw>("gw", {"A", "V"}, {{1}, {3}});
+    m["iinc"] = plain_entry<WeightedScatter>("iinc", {"V", "C"}, {{3}, {1}});
+    m["iincv"] = plain_entry<Iincv>("iincv", {"V", "C"}, {{3, 2}, {1}});
+    m["gsum"] = plain_entry<Gsum>("gsum", {"G", "B", "S"}, {{1}, {1}, {1}});
+    m["gmm"] = plain_entry<Gmm>("gmm", {"LO", "HI", "B"}, {{1}, {1}, {1}});
+    return m;
+  }();
+  return r;
+}
+
+const Entry& lookup(const char* name) {
+  require(name != nullptr, LOAM_ERR(InvalidArgument), "parloop without kernel");
+  auto it = registry().find(name);
+  require(it != registry().end(), LOAM_ERR(InvalidArgument),
+          std::string("kernel ") + name + " has no device implementation (no CPU fallback)");
+  return it->second;
+}
+
+// ===========================================================================
+// Validation (parloop.hpp:89-146)
+// ===========================================================================
+
+const char* access_name(int a) {
+  static const char* n[] = {"READ", "WRITE", "RW", "INC", "SUM", "MIN", "MAX"};
+  return a >= 0 && a < 7 ? n[a] : "?";
+}
+
+bool same_id(uint64_t a, uint64_t b) { return a == 0 || b == 0 || a == b; }
+bool writes(int access) { return access != LOAM_READ; }
+
+std::vector<int> staged_extents(const loam_arg_desc& a) { // parloop.hpp:63-70
+  if (a.kind == LOAM_ARG_GLOBAL) return {a.dim};
+  if (a.kind == LOAM_ARG_MAT) return {a.map->arity, a.col_map->arity};
+  if (!a.map) return {a.dim};
+  if (a.dim == 1) return {a.map->arity};
+  return {a.map->arity, a.dim};
+}
+
+void validate_args(const Entry& k, int n, uint64_t iter, const loam_arg_desc* args, int nargs) {
+  require(n >= 0, LOAM_ERR(InvalidArgument), "iteration set size must be non-negative");
+  require(nargs >= 0 && nargs <= kMaxArgs, LOAM_ERR(InvalidArgument), "too many arguments");
+  for (int q = 0; q < nargs; ++q) {
+    const loam_arg_desc& a = args[q];
+    require(a.kind >= 0 && a.kind <= 2, LOAM_ERR(InvalidArgument), "argument must target exactly one object");
+    if (a.kind == LOAM_ARG_DAT) {
+      require(a.access == LOAM_READ || a.access == LOAM_WRITE || a.access == LOAM_RW || a.access == LOAM_INC,
+              LOAM_ERR(IllegalAccess), std::string("access ") + access_name(a.access) + " not legal for Dats");
+      require(a.col_map == nullptr, LOAM_ERR(InvalidArgument), "Dat argument with several maps");
+      require(a.dim > 0, LOAM_ERR(InvalidArgument), "Dat dim must be positive");
+      if (!a.map) {
+        require(a.set_size == n && same_id(a.set_id, iter), LOAM_ERR(MapSourceMismatch),
+                "direct argument not defined on the iteration set");
+      } else {
+        require(a.map->source_size == n && same_id(a.map->source_id, iter), LOAM_ERR(MapSourceMismatch),
+                "map source differs from iteration set");
+        require(a.map->target_size == a.set_size && same_id(a.map->target_id, a.set_id),
+                LOAM_ERR(MapSourceMismatch), "map target differs from set of dat");
+      }
+    } else if (a.kind == LOAM_ARG_MAT) {
+      require(a.access == LOAM_WRITE || a.access == LOAM_INC, LOAM_ERR(IllegalAccess),
+              "Mats are write-only: only WRITE and INC are permitted");
+      require(a.map && a.col_map && a.sparsity, LOAM_ERR(InvalidArgument),
+              "Mat argument requires row and column maps");
+      require(a.map->source_size == n && same_id(a.map->source_id, iter) && a.col_map->source_size == n &&
+                  same_id(a.col_map->source_id, iter),
+              LOAM_ERR(MapSourceMismatch), "map source differs from iteration set");
+      require(a.map->target_size == a.sparsity->nrows && a.col_map->target_size == a.sparsity->ncols,
+              LOAM_ERR(ShapeMismatch), "matrix shape does not match its maps");
+    } else {
+      require(a.access == LOAM_READ || a.access == LOAM_SUM || a.access == LOAM_MIN || a.access == LOAM_MAX,
+              LOAM_ERR(IllegalAccess), std::string("access ") + access_name(a.access) + " not legal for Globals");
+      require(!a.map && !a.col_map, LOAM_ERR(InvalidArgument), "Global argument cannot carry a map");
+      require(a.dim > 0, LOAM_ERR(InvalidArgument), "Global dim must be positive");
+    }
+  }
+  for (int i = 0; i < nargs; ++i) // written-alias rejection (parloop.hpp:131-137)
+    for (int j = i + 1; j < nargs; ++j) {
+      const bool same = (args[i].obj_id && args[i].obj_id == args[j].obj_id) ||
+                        (!args[i].obj_id && args[i].data && args[i].data == args[j].data);
+      if (same)
+        require(!writes(args[i].access) && !writes(args[j].access), LOAM_ERR(IllegalAccess),
+                "aliased argument is written by this parloop");
+    }
+  const auto& ext = k.info.extents;
+  require((int)ext.size() == nargs, LOAM_ERR(ShapeMismatch),
+          "kernel parameter count does not match argument count");
+  for (int q = 0; q < nargs; ++q)
+    require(ext[q] == staged_extents(args[q]), LOAM_ERR(ShapeMismatch),
+            "staged shape of argument " + std::to_string(q) + " does not match kernel parameter " +
+                k.info.param_names[q]);
+}
+
+// ===========================================================================
+// Plans and their cache (the reference caches colourings, parloop.hpp:153-168)
+// ===========================================================================
+
+struct NodeMap { // node-level view of a map (undoing a declared dof expansion)
+  MapView v;
+  int dim = 1;
+  uint64_t id = 0;
+};
+
+NodeMap node_view(const loam_map_desc* m) {
+  NodeMap r;
+  r.id = m->id;
+  if (m->expand_dim > 1 && m->node_values) {
+    r.v = MapView{m->node_values, m->source_size, m->node_arity, m->node_target_size};
+    r.dim = m->expand_dim;
+  } else {
+    r.v = MapView{m->values, m->source_size, m->arity, m->target_size};
+  }
+  return r;
+}
+
+struct FastPlan {
+  LocalityPlan loc;
+  SortedMap xmap, cmap;
+  const int32_t* xptr = nullptr;
+  const int32_t* cptr = nullptr;
+  int xstride = 0, cstride = 0;
+  PairPlan pp;
+};
+
+struct ColorCacheEntry {
+  ColorPlan cp;
+};
+
+std::mutex g_cache_mutex;
+std::map<std::vector<uint64_t>, std::shared_ptr<FastPlan>> g_fast_cache;
+std::map<std::vector<uint64_t>, std::shared_ptr<ColorCacheEntry>> g_color_cache;
+
+__global__ void k_prefix_equal(const int32_t* __restrict__ a, int sa, const int32_t* __restrict__ b,
+                               int sb, int ncols, int n, int* bad) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  for (int c = 0; c < ncols; ++c)
+    if (a[(int64_t)e * sa + c] != b[(int64_t)e * sb + c]) { *bad = 1; return; }
+}
+
+bool prefix_equal(const int32_t* a, int sa, const int32_t* b, int sb, int ncols, int n, cudaStream_t s) {
+  if (n == 0) return true;
+  DevBuf<int> bad(1, s);
+  LG_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+  k_prefix_equal<<<ceil_div(n, kTPB), kTPB, 0, s>>>(a, sa, b, sb, ncols, n, bad.get());
+  count_launch();
+  LG_LAUNCH_CHECK();
+  int h = 0;
+  LG_CUDA(cudaMemcpyAsync(&h, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  return h == 0;
+}
+
+constexpr int kSegMax = 2048; // doubles of shared memory per warp (16 KB)
+
+std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_desc* args,
+                                          cudaStream_t s) {
+  auto P = std::make_shared<FastPlan>();
+  const NodeMap R = node_view(args[0].map);
+  const loam_map_desc* X = args[1].map;
+  const loam_map_desc* Cm = k.has_coeff ? args[2].map : nullptr;
+  // locality order of the cells, by their smallest row node
+  if (options().locality) {
+    build_locality(R.v, P->loc, s);
+  } else {
+    P->loc.n = n;
+    P->loc.perm.alloc(n, s);
+    std::vector<int32_t> id(n);
+    for (int e = 0; e < n; ++e) id[e] = e;
+    LG_CUDA(cudaMemcpyAsync(P->loc.perm.get(), id.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    LG_CUDA(cudaStreamSynchronize(s));
+  }
+  const int32_t* perm = P->loc.perm.get();
+  SortedMap srows;
+  gather_rows(R.v, perm, srows, s);
+  build_pairs(srows.v.get(), n, R.v.arity, R.v.target, P->pp, s);
+  if (k.bilinear) {
+    const NodeMap Cn = node_view(args[0].col_map);
+    SortedMap scols;
+    const int32_t* sc = srows.v.get();
+    if (!(Cn.v.v == R.v.v && Cn.v.arity == R.v.arity)) {
+      gather_rows(Cn.v, perm, scols, s);
+      sc = scols.v.get();
+    }
+    const loam_sparsity_desc* sp = args[0].sparsity;
+    CsrView csr{sp->row_ptr, sp->col_idx, sp->nrows, sp->ncols, sp->nnz, R.dim, Cn.dim};
+    build_ranks(P->pp, srows.v.get(), sc, Cn.v.arity, csr, s);
+    build_chunks(P->pp, csr, kSegMax, s);
+  }
+  // sorted coordinate / coefficient maps; share storage where maps coincide
+  const MapView xv{X->values, n, X->arity, X->target_size};
+  if (Cm) {
+    const MapView cv{Cm->values, n, Cm->arity, Cm->target_size};
+    if (Cm->values == R.v.v && Cm->arity == R.v.arity) {
+      P->cmap = std::move(srows);
+    } else {
+      gather_rows(cv, perm, P->cmap, s);
+    }
+    P->cptr = P->cmap.v.get();
+    P->cstride = Cm->arity;
+    // vertex ids are the first gdim+1 entries of the coefficient map (P1, and P2 vertices first)
+    if (prefix_equal(Cm->values, Cm->arity, X->values, X->arity, X->arity, n, s)) {
+      P->xptr = P->cptr;
+      P->xstride = P->cstride;
+    }
+  }
+  if (!P->xptr) {
+    if (X->values == R.v.v && X->arity == R.v.arity && srows.v.get()) {
+      P->xmap = std::move(srows);
+    } else {
+      gather_rows(xv, perm, P->xmap, s);
+    }
+    P->xptr = P->xmap.v.get();
+    P->xstride = X->arity;
+  }
+  return P;
+}
+
+// The argument pattern of assemble_matrix / assemble_vector
+// (assemble.hpp:91-99, 123-129) that the owner-computes path serves.
+bool fast_pattern(const Entry& k, const loam_arg_desc* args, int nargs) {
+  if (k.form < 0 || !k.owner) return false;
+  if (nargs != 2 + (k.has_coeff ? 1 : 0)) return false;
+  const loam_arg_desc& A = args[0];
+  if (A.access != LOAM_INC) return false;
+  if (k.bilinear) {
+    if (A.kind != LOAM_ARG_MAT) return false;
+    const NodeMap R = node_view(A.map), C = node_view(A.col_map);
+    if (R.v.arity != k.nrn || R.dim != k.rd || C.v.arity != k.ncn || C.dim != k.cd) return false;
+  } else {
+    if (A.kind != LOAM_ARG_DAT || !A.map || A.dim != 1 || A.map->arity != k.nrn) return false;
+  }
+  const loam_arg_desc& X = args[1];
+  if (X.kind != LOAM_ARG_DAT || X.access != LOAM_READ || !X.map || X.dim != k.gd ||
+      X.map->arity != k.gd + 1)
+    return false;
+  if (k.has_coeff) {
+    const loam_arg_desc& C = args[2];
+    if (C.kind != LOAM_ARG_DAT || C.access != LOAM_READ || !C.map || C.dim != 1 ||
+        C.map->arity != k.ncoeff)
+      return false;
+  }
+  return true;
+}
+
+void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const FormParams& prm,
+              cudaStream_t s) {
+  std::vector<uint64_t> key{(uint64_t)k.form, (uint64_t)k.gd, (uint64_t)k.nrn, (uint64_t)k.ncn,
+                            (uint64_t)options().locality};
+  bool cacheable = true;
+  for (int q = 0; q < nargs; ++q) {
+    const loam_arg_desc& a = args[q];
+    for (const loam_map_desc* m : {a.map, a.col_map})
+      if (m) {
+        key.push_back(m->id);
+        cacheable &= m->id != 0;
+      }
+    if (a.kind == LOAM_ARG_MAT) {
+      key.push_back(a.sparsity->id);
+      cacheable &= a.sparsity->id != 0;
+    }
+  }
+  std::shared_ptr<FastPlan> P;
+  if (cacheable) {
+    std::lock_guard<std::mutex> g(g_cache_mutex);
+    auto it = g_fast_cache.find(key);
+    if (it != g_fast_cache.end()) P = it->second;
+  }
+  if (!P) {
+    P = build_fast_plan(k, n, args, s);
+    if (cacheable) {
+      std::lock_guard<std::mutex> g(g_cache_mutex);
+      g_fast_cache[key] = P;
+    }
+  }
+  OwnerArgs a{};
+  a.ptr = P->pp.ptr.get();
+  a.pairs = P->pp.pairs.get();
+  a.ranks = P->pp.ranks.get();
+  a.xmap = P->xptr;
+  a.xstride = P->xstride;
+  a.coords = args[1].data;
+  a.cmap = P->cptr;
+  a.cstride = P->cstride;
+  a.coeff = k.has_coeff ? args[2].data : nullptr;
+  a.prm = prm;
+  a.out = args[0].data;
+  a.nrows_node = P->pp.nrows_node;
+  a.accumulate = (args[0].flags & LOAM_ARG_ZERO) ? 0 : 1;
+  if (k.bilinear) {
+    a.row_ptr = args[0].sparsity->row_ptr;
+    a.chunk_row = P->pp.chunk_row.get();
+    a.nchunks = P->pp.nchunks;
+    a.seg_max = P->pp.seg_max;
+    const int warps = 4;
+    k.owner(a, ceil_div(a.nchunks, warps), (size_t)warps * a.seg_max * sizeof(double), s);
+  } else {
+    k.owner(a, ceil_div(a.nrows_node, kTPB), 0, s);
+  }
+}
+
+// --- generic path ----------------------------------------------------------
+
+std::shared_ptr<ColorCacheEntry> get_coloring(int n, uint64_t iter, const std::vector<const loam_map_desc*>& maps,
+                                              cudaStream_t s) {
+  std::vector<uint64_t> key{iter, (uint64_t)n};
+  bool cacheable = iter != 0;
+  std::vector<const loam_map_desc*> uniq;
+  for (auto* m : maps) {
+    bool dup = false;
+    for (auto* u : uniq) dup |= (u == m) || (m->id && u->id == m->id);
+    if (!dup) uniq.push_back(m);
+  }
+  std::sort(uniq.begin(), uniq.end(), [](auto* a, auto* b) { return a->id < b->id; });
+  for (auto* m : uniq) {
+    key.push_back(m->id);
+    cacheable &= m->id != 0;
+  }
+  if (cacheable) {
+    std::lock_guard<std::mutex> g(g_cache_mutex);
+    auto it = g_color_cache.find(key);
+    if (it != g_color_cache.end()) return it->second;
+  }
+  auto c = std::make_shared<ColorCacheEntry>();
+  std::vector<MapView> mv;
+  for (auto* m : uniq) mv.push_back(MapView{m->values, m->source_size, m->arity, m->target_size});
+  color_dev(n, mv, c->cp, s);
+  if (cacheable) {
+    std::lock_guard<std::mutex> g(g_cache_mutex);
+    g_color_cache[key] = c;
+  }
+  return c;
+}
+
+void run_generic(const Entry& k, int n, uint64_t iter, const loam_arg_desc* args, int nargs,
+                 const FormParams& prm, cudaStream_t s) {
+  GLaunch L{};
+  L.nargs = nargs;
+  L.prm = prm;
+  int off = 0, slot_stride = 0;
+  bool need_color = options().inc_strategy == 3;
+  std::vector<const loam_map_desc*> conflict;
+  for (int q = 0; q < nargs; ++q) {
+    const loam_arg_desc& a = args[q];
+    GArg& g = L.a[q];
+    g.kind = a.kind;
+    g.access = a.access;
+    g.dim = a.dim;
+    g.data = a.data;
+    std::vector<int> ext = staged_extents(a);
+    g.size = 1;
+    for (int x : ext) g.size *= x;
+    g.off = off;
+    off += g.size;
+    if (a.map) {
+      g.map = a.map->values;
+      g.arity = a.map->arity;
+    }
+    if (a.kind == LOAM_ARG_MAT) {
+      g.map2 = a.col_map->values;
+      g.arity2 = a.col_map->arity;
+      g.row_ptr = a.sparsity->row_ptr;
+      g.col_idx = a.sparsity->col_idx;
+      g.nrows = a.sparsity->nrows;
+      conflict.push_back(a.map);
+      conflict.push_back(a.col_map);
+      if (a.access == LOAM_WRITE) need_color = true;
+    } else if (a.kind == LOAM_ARG_DAT && a.map && writes(a.access)) { // parloop.hpp:212-215
+      conflict.push_back(a.map);
+      if (a.access != LOAM_INC) need_color = true;
+    } else if (a.kind == LOAM_ARG_GLOBAL && a.access != LOAM_READ) {
+      g.slot_off = slot_stride;
+      slot_stride += a.dim;
+    }
+  }
+  require(off == k.stage, LOAM_ERR(ShapeMismatch), "staged size mismatch");
+  // lazily zero-initialised targets (LOAM_ARG_ZERO): this path accumulates
+  for (int q = 0; q < nargs; ++q) {
+    const loam_arg_desc& a = args[q];
+    if (!(a.flags & LOAM_ARG_ZERO) || a.access == LOAM_READ || a.kind == LOAM_ARG_GLOBAL) continue;
+    const size_t count = a.kind == LOAM_ARG_MAT ? (size_t)a.sparsity->nnz : (size_t)a.set_size * a.dim;
+    if (count) {
+      LG_CUDA(cudaMemsetAsync(a.data, 0, sizeof(double) * count, s));
+      count_launch();
+    }
+  }
+  L.slot_stride = slot_stride;
+  DevBuf<double> slots;
+  if (slot_stride) {
+    slots.alloc((size_t)std::max(n, 1) * slot_stride, s);
+    L.slots = slots.get();
+  }
+  DevBuf<unsigned long long> err(1, s);
+  LG_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(unsigned long long), s));
+  L.err = err.get();
+  if (need_color && !conflict.empty() && n > 0) {
+    auto c = get_coloring(n, iter, conflict, s);
+    L.plain = 1;
+    for (int col = 0; col < c->cp.ncolors; ++col) {
+      L.order = c->cp.order.get() + c->cp.offsets[col];
+      L.count = c->cp.offsets[col + 1] - c->cp.offsets[col];
+      k.generic(L, s);
+    }
+  } else {
+    L.order = nullptr;
+    L.count = n;
+    L.plain = 0;
+    k.generic(L, s);
+  }
+  // Global reductions, then overwrite (parloop.hpp:354-383)
+  for (int q = 0; q < nargs; ++q) {
+    const loam_arg_desc& a = args[q];
+    if (a.kind != LOAM_ARG_GLOBAL || a.access == LOAM_READ) continue;
+    if (n == 0) {
+      k_fill_identity<<<1, 32, 0, s>>>(a.data, a.dim, a.access);
+    } else {
+      k_global_reduce<<<a.dim, kTPB, 0, s>>>(L.slots, n, slot_stride, L.a[q].slot_off, a.access, a.data);
+    }
+    count_launch();
+    LG_LAUNCH_CHECK();
+  }
+  if (options().check_sparsity) {
+    bool has_mat = false;
+    for (int q = 0; q < nargs; ++q) has_mat |= args[q].kind == LOAM_ARG_MAT;
+    if (has_mat) {
+      unsigned long long h = 0;
+      LG_CUDA(cudaMemcpyAsync(&h, err.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+      LG_CUDA(cudaStreamSynchronize(s));
+      if (h >> 63)
+        fail(LOAM_ERR(OutsideSparsity), "mat: entry (" + std::to_string((int)((h >> 32) & 0x7fffffff)) +
+                                            ", " + std::to_string((int)(uint32_t)h) + ") outside sparsity");
+    }
+  }
+}
+
+} // namespace
+
+// ===========================================================================
+// Public engine API
+// ===========================================================================
+
+const KernelInfo* find_kernel(const std::string& name) {
+  auto it = registry().find(name);
+  return it == registry().end() ? nullptr : &it->second.info;
+}
+
+const std::string& kernel_names() {
+  static const std::string s = [] {
+    std::string r;
+    for (auto& [name, e] : registry()) r += name + "\n";
+    return r;
+  }();
+  return s;
+}
+
+void validate(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_desc* args, int nargs) {
+  require(kd != nullptr, LOAM_ERR(InvalidArgument), "parloop without kernel");
+  validate_args(lookup(kd->name), n, iter, args, nargs);
+}
+
+void execute(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_desc* args, int nargs,
+             cudaStream_t s) {
+  require(kd != nullptr, LOAM_ERR(InvalidArgument), "parloop without kernel");
+  const Entry& k = lookup(kd->name);
+  validate_args(k, n, iter, args, nargs); // before any mutation (parloop.hpp:193)
+  FormParams prm{{0, 0, 0, 0}};
+  for (int i = 0; i < kd->nparams && i < 4; ++i) prm.p[i] = kd->params[i];
+  const int strat = options().inc_strategy;
+  if (n > 0 && (strat == 0 || strat == 2) && fast_pattern(k, args, nargs)) {
+    try {
+      run_fast(k, n, args, nargs, prm, s);
+      return;
+    } catch (const Error& e) {
+      // a pattern that is not blocked by the maps' dof expansion is served by
+      // the generic path; every other failure propagates
+      if (e.code() != LOAM_ERR(ShapeMismatch)) throw;
+    }
+  }
+  run_generic(k, n, iter, args, nargs, prm, s);
+}
+
+void plan_cache_clear() {
+  std::lock_guard<std::mutex> g(g_cache_mutex);
+  g_fast_cache.clear();
+  g_color_cache.clear();
+}
+
+namespace {
+__global__ void k_map_check(const int32_t* __restrict__ v, int64_t n, int target, unsigned long long* bad) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int x = v[t];
+  if (x < 0 || x >= target) atomicCAS(bad, 0ull, (1ull << 63) | (uint32_t)x);
+}
+} // namespace
+
+void map_check(const loam_map_desc* m, cudaStream_t s) { // topology.hpp:45-48
+  require(m->arity > 0, LOAM_ERR(InvalidArgument), "Map arity must be positive");
+  const int64_t total = (int64_t)m->source_size * m->arity;
+  DevBuf<unsigned long long> bad(1, s);
+  LG_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned long long), s));
+  if (total) {
+    k_map_check<<<ceil_div(total, kTPB), kTPB, 0, s>>>(m->values, total, m->target_size, bad.get());
+    count_launch();
+    LG_LAUNCH_CHECK();
+  }
+  unsigned long long h = 0;
+  LG_CUDA(cudaMemcpyAsync(&h, bad.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  if (h >> 63)
+    fail(LOAM_ERR(IndexOutOfRange), "map: map entry " + std::to_string((int)(uint32_t)h) +
+                                        " outside target set of size " + std::to_string(m->target_size));
+}
+
+void color_iteration(int n, const loam_map_desc* maps, int nmaps, int32_t* colors, int32_t* ncolors,
+                     cudaStream_t s) {
+  std::vector<MapView> mv;
+  for (int i = 0; i < nmaps; ++i) {
+    require(maps[i].source_size == n, LOAM_ERR(SourceMismatch),
+            "conflict map source differs from iteration set");
+    bool dup = false;
+    for (int j = 0; j < i; ++j) dup |= maps[j].values == maps[i].values && maps[j].arity == maps[i].arity;
+    if (!dup) mv.push_back(MapView{maps[i].values, n, maps[i].arity, maps[i].target_size});
+  }
+  ColorPlan cp;
+  if (mv.empty()) { // direct loop: everything colour 0 (test_topology.cpp:64-67)
+    LG_CUDA(cudaMemsetAsync(colors, 0, sizeof(int32_t) * n, s));
+    *ncolors = n > 0 ? 1 : 0;
+    return;
+  }
+  color_dev(n, mv, cp, s);
+  if (n) LG_CUDA(cudaMemcpyAsync(colors, cp.colors.get(), sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  *ncolors = cp.ncolors;
+}
+
+} // namespace loam_gpu

@@ -1,0 +1,36 @@
+// engine.cuh -- host interface of the par_loop engine (engine.cu).
+#pragma once
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace loam_gpu {
+
+struct Options {
+  int inc_strategy = 0;   // 0 auto, 1 atomics, 2 owner-computes, 3 colouring
+  int check_sparsity = 1;
+  int locality = 1;
+};
+Options& options();
+
+struct KernelInfo {
+  std::string name;
+  std::vector<std::string> param_names;
+  std::vector<std::vector<int>> extents;
+};
+const KernelInfo* find_kernel(const std::string& name);
+const std::string& kernel_names();
+
+void validate(const loam_kernel_desc* k, int n, uint64_t iter_id, const loam_arg_desc* args,
+              int nargs);
+void execute(const loam_kernel_desc* k, int n, uint64_t iter_id, const loam_arg_desc* args,
+             int nargs, cudaStream_t s);
+void plan_cache_clear();
+
+// Services.
+void map_check(const loam_map_desc* m, cudaStream_t s);
+void color_iteration(int n, const loam_map_desc* maps, int nmaps, int32_t* colors,
+                     int32_t* ncolors, cudaStream_t s);
+
+} // namespace loam_gpu

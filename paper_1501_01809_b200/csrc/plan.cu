@@ -1,0 +1,433 @@
+// plan.cu -- device-side plan construction (see plan.cuh).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "plan.cuh"
+
+namespace loam_gpu {
+
+namespace {
+
+constexpr int kTPB = 256;
+
+template <class F>
+void cub_call(F f, cudaStream_t s) {
+  size_t bytes = 0;
+  LG_CUDA(f(nullptr, bytes));
+  DevBuf<uint8_t> tmp(bytes ? bytes : 1, s);
+  LG_CUDA(f(tmp.get(), bytes));
+}
+
+int bits_for(int64_t maxval) {
+  int b = 1;
+  while (b < 63 && (int64_t(1) << b) <= maxval) ++b;
+  return b;
+}
+
+__global__ void k_min_key(const int32_t* __restrict__ m, int n, int arity, int32_t* keys,
+                          int32_t* iota) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  int k = m[(int64_t)e * arity];
+  for (int a = 1; a < arity; ++a) k = min(k, m[(int64_t)e * arity + a]);
+  keys[e] = k;
+  iota[e] = e;
+}
+
+__global__ void k_gather_rows(const int32_t* __restrict__ m, const int32_t* __restrict__ perm,
+                              int n, int arity, int32_t* out) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * arity) return;
+  int64_t p = t / arity;
+  int a = (int)(t - p * arity);
+  out[t] = m[(int64_t)perm[p] * arity + a];
+}
+
+__global__ void k_iota(int32_t* v, int64_t n) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) v[t] = (int32_t)t;
+}
+
+__global__ void k_count(const int32_t* __restrict__ keys, int64_t n, int32_t* counts) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) atomicAdd(counts + keys[t], 1);
+}
+
+// Blockedness of a dof-expanded pattern: for node row r, rows r*rd+d have the
+// same length L = cd * Ln and col_idx[start + t*cd + c] = node_t*cd + c.
+__global__ void k_check_blocked(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                int nrows_node, int rd, int cd, int* bad) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrows_node) return;
+  const int64_t s0 = rp[(int64_t)r * rd], l0 = rp[(int64_t)r * rd + 1] - s0;
+  if (l0 % cd) { *bad = 1; return; }
+  for (int d = 0; d < rd; ++d) {
+    const int64_t s = rp[(int64_t)r * rd + d], l = rp[(int64_t)r * rd + d + 1] - s;
+    if (l != l0) { *bad = 1; return; }
+    for (int64_t t = 0; t < l; t += cd) {
+      const int node = ci[s + t] / cd;
+      if (ci[s + t] != node * cd) { *bad = 1; return; }
+      for (int c = 1; c < cd; ++c)
+        if (ci[s + t + c] != node * cd + c) { *bad = 1; return; }
+    }
+  }
+}
+
+__global__ void k_ranks(const int32_t* __restrict__ pairs, int64_t npairs, int nrn, int ncn,
+                        const int32_t* __restrict__ srows, const int32_t* __restrict__ scols,
+                        const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int rd,
+                        int cd, uint8_t* ranks, unsigned long long* err) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= npairs) return;
+  const int32_t k = pairs[p];
+  const int s = k / nrn;
+  const int r = srows[k];
+  const int64_t start = rp[(int64_t)r * rd];
+  const int len = (int)((rp[(int64_t)r * rd + 1] - start) / cd);
+  for (int j = 0; j < ncn; ++j) {
+    const int c = scols[(int64_t)s * ncn + j];
+    int lo = 0, hi = len;
+    while (lo < hi) { // lower_bound over node columns (data.hpp:129-136)
+      int mid = (lo + hi) >> 1;
+      if (ci[start + (int64_t)mid * cd] / cd < c) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo == len || ci[start + (int64_t)lo * cd] / cd != c) {
+      // first offender: (dof row, dof col) as Mat::addto reports it
+      atomicCAS(err, 0ull, (1ull << 63) | ((unsigned long long)(r * rd) << 32) | (unsigned)(c * cd));
+      return;
+    }
+    if (lo > 255) {
+      atomicCAS(err, 0ull, (1ull << 62));
+      return;
+    }
+    ranks[p * ncn + j] = (uint8_t)lo;
+  }
+}
+
+__global__ void k_node_starts(const int64_t* __restrict__ rp, int nrows_node, int rd, int64_t* out) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r <= nrows_node) out[r] = rp[(int64_t)r * rd];
+}
+
+// ---- sparsity
+__global__ void k_emit_keys(const int32_t* __restrict__ rm, int ar_r, const int32_t* __restrict__ cm,
+                            int ar_c, int n, unsigned long long* keys) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)ar_r * ar_c;
+  if (t >= (int64_t)n * per) return;
+  const int64_t e = t / per;
+  const int rem = (int)(t - e * per);
+  const int a = rem / ar_c, b = rem - a * ar_c;
+  keys[t] = ((unsigned long long)(uint32_t)rm[e * ar_r + a] << 32) | (uint32_t)cm[e * ar_c + b];
+}
+
+__global__ void k_key_rows(const unsigned long long* __restrict__ keys, int64_t n, int32_t* counts) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) atomicAdd(counts + (int)(keys[t] >> 32), 1);
+}
+
+__global__ void k_expand_rowptr(const int64_t* __restrict__ node_off, int nrows_node, int rd, int cd,
+                                int64_t* rp) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > (int64_t)nrows_node * rd) return;
+  if (t == (int64_t)nrows_node * rd) { rp[t] = node_off[nrows_node] * rd * cd; return; }
+  const int r = (int)(t / rd), d = (int)(t - (int64_t)r * rd);
+  const int64_t len = node_off[r + 1] - node_off[r];
+  rp[t] = node_off[r] * rd * cd + d * len * cd;
+}
+
+__global__ void k_fill_cols(const unsigned long long* __restrict__ ukeys, int64_t nu,
+                            const int64_t* __restrict__ node_off, const int64_t* __restrict__ rp,
+                            int rd, int cd, int32_t* ci) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nu) return;
+  const unsigned long long k = ukeys[t];
+  const int r = (int)(k >> 32), c = (int)(uint32_t)k;
+  const int64_t pos = t - node_off[r];
+  for (int d = 0; d < rd; ++d) {
+    const int64_t base = rp[(int64_t)r * rd + d] + pos * cd;
+    for (int x = 0; x < cd; ++x) ci[base + x] = c * cd + x;
+  }
+}
+
+// ---- colouring (Jones-Plassmann, priority = ascending index == greedy order)
+struct InvMap {
+  const int32_t* ptr;  // [target+1]
+  const int32_t* ent;  // pair codes f*arity+k incident to target, ascending f
+  const int32_t* map;
+  int arity;
+};
+
+constexpr int kMaxColorWords = 4; // 256 colours
+
+template <int NM>
+__global__ void k_jp_round(int n, InvMap m0, InvMap m1, InvMap m2, InvMap m3, int32_t* colors,
+                           int* remaining, int* overflow) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  volatile int32_t* col = colors;
+  if (col[e] >= 0) return;
+  unsigned long long mask[kMaxColorWords] = {0, 0, 0, 0};
+  const InvMap ms[4] = {m0, m1, m2, m3};
+#pragma unroll
+  for (int mi = 0; mi < NM; ++mi) {
+    const InvMap& m = ms[mi];
+    for (int k = 0; k < m.arity; ++k) {
+      const int t = m.map[(int64_t)e * m.arity + k];
+      for (int q = m.ptr[t]; q < m.ptr[t + 1]; ++q) {
+        const int f = m.ent[q] / m.arity;
+        if (f >= e) break; // only earlier entities constrain e (topology.hpp:152-159)
+        const int c = col[f];
+        if (c < 0) { atomicAdd(remaining, 1); return; } // not decided yet: next round
+        mask[c >> 6] |= 1ull << (c & 63);
+      }
+    }
+  }
+  int c = 0;
+  while (c < 64 * kMaxColorWords && (mask[c >> 6] >> (c & 63) & 1ull)) ++c;
+  if (c >= 64 * kMaxColorWords) { *overflow = 1; return; }
+  col[e] = c;
+}
+
+} // namespace
+
+void build_locality(const MapView& key, LocalityPlan& out, cudaStream_t s) {
+  const int n = key.n;
+  out.n = n;
+  DevBuf<int32_t> keys(n, s), iota(n, s), keys_out(n, s);
+  out.perm.alloc(n, s);
+  if (n == 0) return;
+  k_min_key<<<ceil_div(n, kTPB), kTPB, 0, s>>>(key.v, n, key.arity, keys.get(), iota.get());
+  count_launch();
+  LG_LAUNCH_CHECK();
+  const int endbit = bits_for(key.target);
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, keys.get(), keys_out.get(), iota.get(),
+                                           out.perm.get(), n, 0, endbit, s);
+  }, s);
+}
+
+void gather_rows(const MapView& m, const int32_t* perm, SortedMap& out, cudaStream_t s) {
+  out.arity = m.arity;
+  out.target = m.target;
+  const int64_t total = (int64_t)m.n * m.arity;
+  out.v.alloc(total, s);
+  if (!total) return;
+  k_gather_rows<<<ceil_div(total, kTPB), kTPB, 0, s>>>(m.v, perm, m.n, m.arity, out.v.get());
+  count_launch();
+  LG_LAUNCH_CHECK();
+}
+
+void build_pairs(const int32_t* sorted_rows, int ncells, int nrn, int nrows_node, PairPlan& out,
+                 cudaStream_t s) {
+  const int64_t np = (int64_t)ncells * nrn;
+  require(np < (int64_t(1) << 31), LOAM_ERR(InvalidArgument), "pair list exceeds 2^31 entries");
+  out.nrows_node = nrows_node;
+  out.nrn = nrn;
+  out.npairs = np;
+  out.ptr.alloc(nrows_node + 1, s);
+  out.pairs.alloc(np, s);
+  DevBuf<int32_t> iota(np, s), keys_out(np, s), counts(nrows_node + 1, s);
+  LG_CUDA(cudaMemsetAsync(counts.get(), 0, sizeof(int32_t) * (nrows_node + 1), s));
+  if (np) {
+    k_iota<<<ceil_div(np, kTPB), kTPB, 0, s>>>(iota.get(), np);
+    k_count<<<ceil_div(np, kTPB), kTPB, 0, s>>>(sorted_rows, np, counts.get());
+    count_launch(2);
+    LG_LAUNCH_CHECK();
+    const int endbit = bits_for(nrows_node);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, sorted_rows, keys_out.get(), iota.get(),
+                                             out.pairs.get(), (int)np, 0, endbit, s);
+    }, s);
+  }
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, counts.get(), out.ptr.get(), nrows_node + 1, s);
+  }, s);
+}
+
+void build_ranks(PairPlan& pp, const int32_t* sorted_rows, const int32_t* sorted_cols, int ncn,
+                 const CsrView& csr, cudaStream_t s) {
+  pp.ncn = ncn;
+  DevBuf<int> bad(1, s);
+  LG_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+  if (csr.rd > 1 || csr.cd > 1) {
+    k_check_blocked<<<ceil_div(pp.nrows_node, kTPB), kTPB, 0, s>>>(
+        csr.row_ptr, csr.col_idx, pp.nrows_node, csr.rd, csr.cd, bad.get());
+    count_launch();
+    LG_LAUNCH_CHECK();
+  }
+  int hbad = 0;
+  LG_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  require(!hbad, LOAM_ERR(ShapeMismatch), "sparsity is not blocked by the maps' dof expansion");
+  pp.ranks.alloc(pp.npairs * ncn, s);
+  DevBuf<unsigned long long> err(1, s);
+  LG_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(unsigned long long), s));
+  if (pp.npairs) {
+    k_ranks<<<ceil_div(pp.npairs, kTPB), kTPB, 0, s>>>(pp.pairs.get(), pp.npairs, pp.nrn, ncn,
+                                                       sorted_rows, sorted_cols, csr.row_ptr,
+                                                       csr.col_idx, csr.rd, csr.cd,
+                                                       pp.ranks.get(), err.get());
+    count_launch();
+    LG_LAUNCH_CHECK();
+  }
+  unsigned long long herr = 0;
+  LG_CUDA(cudaMemcpyAsync(&herr, err.get(), sizeof(herr), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  if (herr >> 63) {
+    const int row = (int)((herr >> 32) & 0x7fffffff), col = (int)(uint32_t)herr;
+    fail(LOAM_ERR(OutsideSparsity), "mat: entry (" + std::to_string(row) + ", " +
+                                        std::to_string(col) + ") outside sparsity");
+  }
+  require(!(herr >> 62), LOAM_ERR(InvalidArgument), "row with more than 256 column nodes");
+}
+
+void build_chunks(PairPlan& pp, const CsrView& csr, int smax, cudaStream_t s) {
+  const int nr = pp.nrows_node;
+  DevBuf<int64_t> starts(nr + 1, s);
+  k_node_starts<<<ceil_div(nr + 1, kTPB), kTPB, 0, s>>>(csr.row_ptr, nr, csr.rd, starts.get());
+  count_launch();
+  LG_LAUNCH_CHECK();
+  std::vector<int64_t> h(nr + 1);
+  LG_CUDA(cudaMemcpyAsync(h.data(), starts.get(), sizeof(int64_t) * (nr + 1),
+                          cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int32_t> chunks{0};
+  int seg_max = 0;
+  int r0 = 0;
+  while (r0 < nr) {
+    int r1 = r0 + 1;
+    require(h[r1] - h[r0] <= smax, LOAM_ERR(InvalidArgument), "row segment exceeds shared memory");
+    while (r1 < nr && r1 - r0 < 32 && h[r1 + 1] - h[r0] <= smax) ++r1;
+    seg_max = std::max<int>(seg_max, (int)(h[r1] - h[r0]));
+    chunks.push_back(r1);
+    r0 = r1;
+  }
+  pp.nchunks = (int)chunks.size() - 1;
+  pp.seg_max = seg_max;
+  pp.chunk_row.alloc(chunks.size(), s);
+  LG_CUDA(cudaMemcpyAsync(pp.chunk_row.get(), chunks.data(), sizeof(int32_t) * chunks.size(),
+                          cudaMemcpyHostToDevice, s));
+  LG_CUDA(cudaStreamSynchronize(s)); // host vector goes out of scope
+}
+
+void build_sparsity_dev(const MapView& rows, const MapView& cols, int rd, int cd,
+                        int64_t** row_ptr, int32_t** col_idx, int64_t* nnz, cudaStream_t s) {
+  require(rows.n == cols.n, LOAM_ERR(SourceMismatch),
+          "row and column maps must share their source set");
+  const int n = rows.n;
+  const int64_t nk = (int64_t)n * rows.arity * cols.arity;
+  require(nk < (int64_t(1) << 31), LOAM_ERR(InvalidArgument), "sparsity key count exceeds 2^31");
+  DevBuf<unsigned long long> keys(nk, s), sorted(nk, s);
+  if (nk) {
+    k_emit_keys<<<ceil_div(nk, kTPB), kTPB, 0, s>>>(rows.v, rows.arity, cols.v, cols.arity, n,
+                                                    keys.get());
+    count_launch();
+    LG_LAUNCH_CHECK();
+    const int endbit = 32 + bits_for(rows.target);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, keys.get(), sorted.get(), (int)nk, 0, endbit, s);
+    }, s);
+  }
+  DevBuf<int> nsel(1, s);
+  LG_CUDA(cudaMemsetAsync(nsel.get(), 0, sizeof(int), s));
+  if (nk)
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceSelect::Unique(t, b, sorted.get(), keys.get(), nsel.get(), (int)nk, s);
+    }, s);
+  int nu = 0;
+  LG_CUDA(cudaMemcpyAsync(&nu, nsel.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  const int nr = rows.target;
+  DevBuf<int32_t> counts(nr + 1, s);
+  DevBuf<int64_t> node_off(nr + 1, s);
+  LG_CUDA(cudaMemsetAsync(counts.get(), 0, sizeof(int32_t) * (nr + 1), s));
+  if (nu) {
+    k_key_rows<<<ceil_div(nu, kTPB), kTPB, 0, s>>>(keys.get(), nu, counts.get());
+    count_launch();
+    LG_LAUNCH_CHECK();
+  }
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, counts.get(), node_off.get(), nr + 1, s);
+  }, s);
+  const int64_t nrows = (int64_t)nr * rd;
+  const int64_t total = (int64_t)nu * rd * cd;
+  require(total < (int64_t(1) << 40), LOAM_ERR(InvalidArgument), "sparsity too large");
+  LG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(row_ptr), sizeof(int64_t) * (nrows + 1), s));
+  LG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(col_idx), sizeof(int32_t) * (total ? total : 1), s));
+  k_expand_rowptr<<<ceil_div(nrows + 1, kTPB), kTPB, 0, s>>>(node_off.get(), nr, rd, cd, *row_ptr);
+  count_launch();
+  if (nu) {
+    k_fill_cols<<<ceil_div(nu, kTPB), kTPB, 0, s>>>(keys.get(), nu, node_off.get(), *row_ptr, rd, cd,
+                                                    *col_idx);
+    count_launch();
+  }
+  LG_LAUNCH_CHECK();
+  *nnz = total;
+}
+
+void color_dev(int n, const std::vector<MapView>& maps, ColorPlan& out, cudaStream_t s) {
+  require(maps.size() <= 4, LOAM_ERR(InvalidArgument), "at most 4 distinct conflict maps");
+  out.colors.alloc(n, s);
+  if (n == 0) { out.ncolors = 0; out.offsets = {0}; return; }
+  LG_CUDA(cudaMemsetAsync(out.colors.get(), 0xff, sizeof(int32_t) * n, s));
+  // inverse maps (target -> ascending entities)
+  std::vector<DevBuf<int32_t>> ptrs(maps.size()), ents(maps.size());
+  InvMap inv[4] = {};
+  for (size_t mi = 0; mi < maps.size(); ++mi) {
+    const MapView& m = maps[mi];
+    PairPlan pp; // target -> pair codes e*arity+k, ascending e within a target
+    build_pairs(m.v, m.n, m.arity, m.target, pp, s);
+    ptrs[mi] = std::move(pp.ptr);
+    ents[mi] = std::move(pp.pairs);
+    inv[mi] = InvMap{ptrs[mi].get(), ents[mi].get(), m.v, m.arity};
+  }
+  DevBuf<int> remaining(1, s), overflow(1, s);
+  LG_CUDA(cudaMemsetAsync(overflow.get(), 0, sizeof(int), s));
+  int rounds = 0;
+  for (;;) {
+    LG_CUDA(cudaMemsetAsync(remaining.get(), 0, sizeof(int), s));
+    const int g = ceil_div(n, kTPB);
+    switch (maps.size()) {
+    case 0: k_jp_round<0><<<g, kTPB, 0, s>>>(n, inv[0], inv[1], inv[2], inv[3], out.colors.get(), remaining.get(), overflow.get()); break;
+    case 1: k_jp_round<1><<<g, kTPB, 0, s>>>(n, inv[0], inv[1], inv[2], inv[3], out.colors.get(), remaining.get(), overflow.get()); break;
+    case 2: k_jp_round<2><<<g, kTPB, 0, s>>>(n, inv[0], inv[1], inv[2], inv[3], out.colors.get(), remaining.get(), overflow.get()); break;
+    case 3: k_jp_round<3><<<g, kTPB, 0, s>>>(n, inv[0], inv[1], inv[2], inv[3], out.colors.get(), remaining.get(), overflow.get()); break;
+    default: k_jp_round<4><<<g, kTPB, 0, s>>>(n, inv[0], inv[1], inv[2], inv[3], out.colors.get(), remaining.get(), overflow.get()); break;
+    }
+    count_launch();
+    LG_LAUNCH_CHECK();
+    ++rounds;
+    int hrem = 0, hov = 0;
+    LG_CUDA(cudaMemcpyAsync(&hrem, remaining.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    LG_CUDA(cudaMemcpyAsync(&hov, overflow.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    LG_CUDA(cudaStreamSynchronize(s));
+    require(!hov, LOAM_ERR(InvalidArgument), "more than 256 colours");
+    if (hrem == 0) break;
+  }
+  // entities sorted by (colour, index) and colour offsets
+  DevBuf<int32_t> iota(n, s), ckeys(n, s), counts(257, s);
+  out.order.alloc(n, s);
+  k_iota<<<ceil_div(n, kTPB), kTPB, 0, s>>>(iota.get(), n);
+  LG_CUDA(cudaMemsetAsync(counts.get(), 0, sizeof(int32_t) * 257, s));
+  k_count<<<ceil_div(n, kTPB), kTPB, 0, s>>>(out.colors.get(), n, counts.get());
+  count_launch(2);
+  LG_LAUNCH_CHECK();
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, out.colors.get(), ckeys.get(), iota.get(),
+                                           out.order.get(), n, 0, 9, s);
+  }, s);
+  std::vector<int32_t> hc(257);
+  LG_CUDA(cudaMemcpyAsync(hc.data(), counts.get(), sizeof(int32_t) * 257, cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  out.ncolors = 0;
+  for (int c = 0; c < 256; ++c)
+    if (hc[c]) out.ncolors = c + 1;
+  out.offsets.assign(out.ncolors + 1, 0);
+  for (int c = 0; c < out.ncolors; ++c) out.offsets[c + 1] = out.offsets[c] + hc[c];
+}
+
+} // namespace loam_gpu

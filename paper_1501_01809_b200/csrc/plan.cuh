@@ -1,0 +1,84 @@
+// plan.cuh -- execution plans for the par_loop engine (built on the device, cached).
+//
+// The reference caches one thing per (iteration set, conflict maps): the greedy
+// colouring (parloop.hpp:153-168).  The B200 engine caches, per loop shape,
+//   * a cell LOCALITY order (cells sorted by their smallest row node) and the
+//     maps re-laid in that order, so every gather is coalesced/L2-resident;
+//   * the owner-computes PAIR list: for each row node, the (cell, local index)
+//     pairs incident to it (the node->cell inverse of the row map);
+//   * for Mats, the per-pair SLOT RANKS: the in-row position of each column
+//     node -- the "precomputed per-cell slot offsets into col_idx" of the
+//     north star, compressed to one byte per entry -- and the warp chunking
+//     of rows into shared-memory segments;
+//   * the bit-exact greedy COLOURING (topology.hpp:86-125), when a loop or a
+//     strategy needs it.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace loam_gpu {
+
+struct MapView {         // device map, row-major [n x arity]
+  const int32_t* v = nullptr;
+  int n = 0, arity = 0, target = 0;
+};
+
+struct CsrView {         // device CSR (data.hpp:116-142) with its dof expansion
+  const int64_t* row_ptr = nullptr;
+  const int32_t* col_idx = nullptr;
+  int nrows = 0, ncols = 0;
+  int64_t nnz = 0;
+  int rd = 1, cd = 1;
+};
+
+struct LocalityPlan {
+  DevBuf<int32_t> perm; // sorted position -> user cell
+  int n = 0;
+};
+
+struct SortedMap {
+  DevBuf<int32_t> v;    // rows of a map in locality order
+  int arity = 0, target = 0;
+};
+
+struct PairPlan {
+  int nrows_node = 0, nrn = 0, ncn = 0;
+  int64_t npairs = 0;
+  DevBuf<int32_t> ptr;   // [nrows_node + 1]
+  DevBuf<int32_t> pairs; // sorted_cell * nrn + i, grouped by row node
+  DevBuf<uint8_t> ranks; // [npairs * ncn] in-row node rank of each column node
+  // warp chunks of consecutive row nodes whose value segment fits in smem
+  DevBuf<int32_t> chunk_row; // [nchunks + 1]
+  int nchunks = 0, seg_max = 0;
+};
+
+struct ColorPlan {
+  DevBuf<int32_t> colors; // per user entity (bit-exact with the reference)
+  DevBuf<int32_t> order;  // entities sorted by (colour, index)
+  std::vector<int> offsets; // host: colour c is order[offsets[c] .. offsets[c+1])
+  int ncolors = 0;
+};
+
+// Locality order: cells sorted (stably) by the smallest node of `key`.
+void build_locality(const MapView& key, LocalityPlan& out, cudaStream_t s);
+// out[p] = m[perm[p]] row by row.
+void gather_rows(const MapView& m, const int32_t* perm, SortedMap& out, cudaStream_t s);
+// Pair list of a (sorted) node-level row map.
+void build_pairs(const int32_t* sorted_rows, int ncells, int nrn, int nrows_node, PairPlan& out,
+                 cudaStream_t s);
+// Slot ranks of the column nodes of each pair in its row (throws OutsideSparsity);
+// verifies the pattern is blocked by (rd, cd) first.
+void build_ranks(PairPlan& pp, const int32_t* sorted_rows, const int32_t* sorted_cols, int ncn,
+                 const CsrView& csr, cudaStream_t s);
+// Warp chunking of row nodes (<= 32 rows, segment <= smax doubles).
+void build_chunks(PairPlan& pp, const CsrView& csr, int smax, cudaStream_t s);
+
+// build_sparsity (data.hpp:149-179) on the device, bit-exact.
+void build_sparsity_dev(const MapView& rows, const MapView& cols, int rd, int cd,
+                        int64_t** row_ptr, int32_t** col_idx, int64_t* nnz, cudaStream_t s);
+// color_iteration (topology.hpp:86-125) on the device, bit-exact.
+void color_dev(int n, const std::vector<MapView>& maps, ColorPlan& out, cudaStream_t s);
+
+} // namespace loam_gpu

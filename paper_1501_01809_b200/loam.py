@@ -1,0 +1,418 @@
+"""Python mirror of the reference operator surface over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(/root/reference/proj/include/loam): Set/Map (topology.hpp:15-74),
+Dat/Global/Sparsity/Mat/build_sparsity (data.hpp:15-234), Arg/arg/Parloop/
+validate/execute (parloop.hpp:17-384), color_iteration (topology.hpp:86-125).
+Objects are DEVICE-resident (torch CUDA tensors are only the allocator);
+every compute call goes through libloam_gpu.so -- there is no CPU path.
+Errors raise capi.LoamError whose `.kind` is the reference ErrorKind name.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import itertools
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import capi
+from .capi import INC, MAX, MIN, READ, RW, SUM, WRITE, LoamError
+
+_ids = itertools.count(1)
+
+
+def _fail(kind: str, msg: str):
+    raise LoamError(1 + capi.ERROR_KINDS.index(kind), msg)
+
+
+def _require(cond: bool, kind: str, msg: str) -> None:
+    if not cond:
+        _fail(kind, msg)
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+class Access:
+    READ, WRITE, RW, INC, SUM, MIN, MAX = READ, WRITE, RW, INC, SUM, MIN, MAX
+
+
+# --------------------------------------------------------------------------- topology
+
+
+class Set:
+    """topology.hpp:15-26: a count only."""
+
+    def __init__(self, size: int, name: str = "set"):
+        _require(size >= 0, "InvalidArgument", "Set size must be non-negative")
+        self.size = int(size)
+        self.name = name
+        self.id = next(_ids)
+
+
+def make_set(size: int, name: str = "set") -> Set:
+    return Set(size, name)
+
+
+class Map:
+    """topology.hpp:36-66: int32 row-major [source.size x arity], validated on construction.
+
+    `node_map`/`expand_dim` (extension): a dof-expanded map (entries dim*n+d,
+    SURVEY A6) can declare the node map it expands so the device reads the
+    smaller node map; see expanded_map().
+    """
+
+    def __init__(self, source: Set, target: Set, arity: int, values, name: str = "map",
+                 node_map: "Map | None" = None, expand_dim: int = 0):
+        _require(arity > 0, "InvalidArgument", "Map arity must be positive")
+        vals = np.ascontiguousarray(np.asarray(values, dtype=np.int32).reshape(-1))
+        _require(vals.size == source.size * arity, "ArityMismatch",
+                 f"{name}: value table length != source size * arity")
+        if vals.size:
+            lo, hi = int(vals.min()), int(vals.max())
+            bad = lo if lo < 0 else hi
+            _require(lo >= 0 and hi < target.size, "IndexOutOfRange",
+                     f"{name}: map entry {bad} outside target set of size {target.size}")
+        self.source, self.target, self.arity, self.name = source, target, int(arity), name
+        self.values = vals
+        self.dev = torch.from_numpy(vals).cuda() if vals.size else torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.id = next(_ids)
+        self.node_map = node_map
+        self.expand_dim = expand_dim
+        self._desc = None
+
+    def row(self, e: int) -> np.ndarray:
+        return self.values[e * self.arity:(e + 1) * self.arity]
+
+    def desc(self) -> capi.MapDesc:
+        if self._desc is None:
+            d = capi.MapDesc()
+            d.values = self.dev.data_ptr()
+            d.source_size, d.target_size, d.arity = self.source.size, self.target.size, self.arity
+            d.source_id, d.target_id, d.id = self.source.id, self.target.id, self.id
+            if self.node_map is not None:
+                d.expand_dim = self.expand_dim
+                d.node_values = self.node_map.dev.data_ptr()
+                d.node_arity = self.node_map.arity
+                d.node_target_size = self.node_map.target.size
+            self._desc = d
+        return self._desc
+
+
+def make_map(source: Set, target: Set, arity: int, values, name: str = "map") -> Map:
+    return Map(source, target, arity, values, name)
+
+
+def expanded_map(node_map: Map, dim: int, target: Set | None = None, name: str = "dof_map") -> Map:
+    """The dof-expanded Map a vector-valued Mat needs (entries dim*n+d)."""
+    if target is None:
+        target = Set(node_map.target.size * dim, name + "_dofs")
+    v = node_map.values.reshape(-1, node_map.arity).astype(np.int64)
+    exp = (v[:, :, None] * dim + np.arange(dim)[None, None, :]).reshape(-1).astype(np.int32)
+    return Map(node_map.source, target, node_map.arity * dim, exp, name, node_map=node_map, expand_dim=dim)
+
+
+def color_iteration(iterset: Set, conflict_maps: Sequence[Map]):
+    """topology.hpp:86-125 on the device: returns (colors ndarray, num_colors)."""
+    for m in conflict_maps:
+        _require(m.source is iterset, "SourceMismatch",
+                 f"conflict map {m.name} source differs from iteration set")
+    n = iterset.size
+    colors = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    descs = (capi.MapDesc * max(len(conflict_maps), 1))(*[m.desc() for m in conflict_maps])
+    nc = C.c_int32(0)
+    capi.check(capi.lib().loam_gpu_color_iteration(n, iterset.id, descs, len(conflict_maps),
+                                                    colors.data_ptr(), C.byref(nc), _stream()))
+    return colors[:n].cpu().numpy(), int(nc.value)
+
+
+# --------------------------------------------------------------------------- data
+
+
+class Dat:
+    """data.hpp:35-60: fp64 AoS [set.size x dim] with a version counter."""
+
+    def __init__(self, set_: Set, dim: int, name: str = "dat"):
+        _require(dim > 0, "InvalidArgument", "Dat dim must be positive")
+        self.set, self.dim, self.name = set_, int(dim), name
+        self.data = torch.zeros(max(set_.size * dim, 1), dtype=torch.float64, device="cuda")
+        self.version = 0
+        self.id = next(_ids)
+        self._zero = True    # logically zero-initialised (make_dat, data.hpp:37-39)
+        self._stale = False  # zero() deferred: memory not cleared yet
+
+    def _materialize(self) -> None:
+        if self._stale:
+            self.data.zero_()
+            self._stale = False
+
+    def view(self) -> np.ndarray:
+        self._materialize()
+        return self.data[: self.set.size * self.dim].cpu().numpy()
+
+    def set_values(self, values) -> None:
+        """mutable_view() + assignment: bumps the version (data.hpp:49-52)."""
+        v = torch.as_tensor(np.asarray(values, dtype=np.float64).reshape(-1))
+        _require(v.numel() == self.set.size * self.dim, "DimensionMismatch", "value count mismatch")
+        self.version += 1
+        self.data[: v.numel()].copy_(v.cuda())
+        self._zero = self._stale = False
+
+    def zero(self) -> None:
+        """Lazy: the next INC through the device treats the Dat as zeros
+        (LOAM_ARG_ZERO); the memory is cleared only if something reads it."""
+        self.version += 1
+        self._zero = self._stale = True
+
+
+def make_dat(set_: Set, dim: int, name: str = "dat") -> Dat:
+    return Dat(set_, dim, name)
+
+
+class Global:
+    """data.hpp:69-87."""
+
+    def __init__(self, dim: int = 1, name: str = "global", init=None):
+        if init is not None:
+            init = list(init)
+            dim = len(init)
+        _require(dim > 0, "InvalidArgument", "Global dim must be positive")
+        self.dim, self.name = int(dim), name
+        self.data = torch.zeros(self.dim, dtype=torch.float64, device="cuda")
+        if init is not None:
+            self.data.copy_(torch.tensor(init, dtype=torch.float64))
+        self.id = next(_ids)
+
+    def view(self) -> np.ndarray:
+        return self.data.cpu().numpy()
+
+    def set_values(self, values) -> None:
+        self.data.copy_(torch.as_tensor(np.asarray(values, dtype=np.float64)))
+
+
+def make_global(dim: int = 1, name: str = "global") -> Global:
+    return Global(dim, name)
+
+
+class Sparsity:
+    """data.hpp:116-142: CSR with int64 row offsets and int32 columns (device)."""
+
+    def __init__(self, nrows: int, ncols: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
+                 row_dim: int = 1, col_dim: int = 1):
+        self.nrows, self.ncols = int(nrows), int(ncols)
+        self.row_ptr, self.col_idx = row_ptr, col_idx
+        self.row_dim, self.col_dim = row_dim, col_dim
+        self.id = next(_ids)
+        self._host = None
+        self._desc = None
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[self.nrows].item())
+
+    def host(self):
+        if self._host is None:
+            self._host = (self.row_ptr.cpu().numpy(), self.col_idx[: max(self.nnz, 0)].cpu().numpy())
+        return self._host
+
+    def find(self, row: int, col: int) -> int:
+        """Position of (row, col) in the values array or -1 (data.hpp:129-136)."""
+        if row < 0 or row >= self.nrows:
+            return -1
+        rp, ci = self.host()
+        lo, hi = int(rp[row]), int(rp[row + 1])
+        k = lo + int(np.searchsorted(ci[lo:hi], col))
+        return k if k < hi and ci[k] == col else -1
+
+    def desc(self) -> capi.SparsityDesc:
+        if self._desc is None:
+            d = capi.SparsityDesc()
+            d.row_ptr, d.col_idx = self.row_ptr.data_ptr(), self.col_idx.data_ptr()
+            d.nrows, d.ncols, d.nnz = self.nrows, self.ncols, self.nnz
+            d.row_dim, d.col_dim, d.id = self.row_dim, self.col_dim, self.id
+            self._desc = d
+        return self._desc
+
+
+def build_sparsity(row_map: Map, col_map: Map, row_dim: int = 1, col_dim: int = 1) -> Sparsity:
+    """data.hpp:149-179 on the device (bit-exact)."""
+    rp, ci, nnz = C.c_void_p(), C.c_void_p(), C.c_int64()
+    capi.check(capi.lib().loam_gpu_build_sparsity(row_map.desc(), col_map.desc(), row_dim, col_dim,
+                                                   C.byref(rp), C.byref(ci), C.byref(nnz), _stream()))
+    nrows = row_map.target.size * row_dim
+    ncols = col_map.target.size * col_dim
+    try:  # copy into torch-owned storage, release the library allocation
+        row_ptr = torch.empty(nrows + 1, dtype=torch.int64, device="cuda")
+        col_idx = torch.empty(max(nnz.value, 1), dtype=torch.int32, device="cuda")
+        capi.check(capi.lib().loam_gpu_memcpy(row_ptr.data_ptr(), rp, 8 * (nrows + 1), _stream()))
+        capi.check(capi.lib().loam_gpu_memcpy(col_idx.data_ptr(), ci, 4 * nnz.value, _stream()))
+        capi.check(capi.lib().loam_gpu_stream_sync(_stream()))
+    finally:
+        capi.lib().loam_gpu_free(rp)
+        capi.lib().loam_gpu_free(ci)
+    return Sparsity(nrows, ncols, row_ptr, col_idx, row_dim, col_dim)
+
+
+class Mat:
+    """data.hpp:183-228: fp64 values over a fixed sparsity, zero-initialised."""
+
+    def __init__(self, sparsity: Sparsity, name: str = "mat"):
+        self.sparsity, self.name = sparsity, name
+        self.values = torch.zeros(max(sparsity.nnz, 1), dtype=torch.float64, device="cuda")
+        self.id = next(_ids)
+        self._zero = True    # make_mat zero-fills (data.hpp:185-187)
+        self._stale = False
+
+    def _materialize(self) -> None:
+        if self._stale:
+            self.values.zero_()
+            self._stale = False
+
+    @property
+    def nrows(self):
+        return self.sparsity.nrows
+
+    @property
+    def ncols(self):
+        return self.sparsity.ncols
+
+    def host_values(self) -> np.ndarray:
+        self._materialize()
+        return self.values[: self.sparsity.nnz].cpu().numpy()
+
+    def at(self, row: int, col: int) -> float:
+        self._materialize()
+        pos = self.sparsity.find(row, col)
+        return 0.0 if pos < 0 else float(self.values[pos].item())
+
+    def zero(self) -> None:
+        """Lazy Mat::zero (data.hpp:201): the next INC treats the values as zeros."""
+        self._zero = self._stale = True
+
+
+def make_mat(sparsity: Sparsity, name: str = "mat") -> Mat:
+    return Mat(sparsity, name)
+
+
+# --------------------------------------------------------------------------- par_loop
+
+
+@dataclass
+class Arg:
+    """parloop.hpp:17-28."""
+    dat: Optional[Dat] = None
+    mat: Optional[Mat] = None
+    glob: Optional[Global] = None
+    access: int = READ
+    maps: list = field(default_factory=list)
+
+
+def arg(obj, access: int, map1: Map | None = None, map2: Map | None = None) -> Arg:
+    """arg(dat, access, map=None) | arg(mat, access, row_map, col_map) | arg(global, access)."""
+    if isinstance(obj, Dat):
+        return Arg(dat=obj, access=access, maps=[map1] if map1 is not None else [])
+    if isinstance(obj, Mat):
+        return Arg(mat=obj, access=access, maps=[map1, map2])
+    if isinstance(obj, Global):
+        return Arg(glob=obj, access=access)
+    raise TypeError("arg() expects a Dat, Mat or Global")
+
+
+@dataclass
+class Kernel:
+    """ir::Kernel (kernel.hpp:504-511) as a registry key plus its baked literals."""
+    name: str
+    params: tuple = ()
+
+    def signature(self):
+        buf = (C.c_int32 * 64)()
+        n = capi.lib().loam_gpu_kernel_signature(self.name.encode(), buf, 64)
+        if n < 0:
+            raise LoamError(-n, capi.lib().loam_gpu_last_error().decode())
+        out, w = [], 0
+        for _ in range(n):
+            rank = buf[w]
+            out.append(list(buf[w + 1:w + 1 + rank]))
+            w += 1 + rank
+        return out
+
+
+def kernel(name: str, *params: float) -> Kernel:
+    return Kernel(name, tuple(float(p) for p in params))
+
+
+@dataclass
+class Parloop:
+    """parloop.hpp:55-59."""
+    kernel: Kernel
+    iterset: Set
+    args: list
+
+
+def _build(loop: Parloop):
+    keep = []
+    descs = (capi.ArgDesc * max(len(loop.args), 1))()
+    for k, a in enumerate(loop.args):
+        d = descs[k]
+        d.access = a.access
+        if a.dat is not None:
+            d.kind, d.data, d.dim = capi.ARG_DAT, a.dat.data.data_ptr(), a.dat.dim
+            d.set_size, d.set_id, d.obj_id = a.dat.set.size, a.dat.set.id, a.dat.id
+            if a.access == INC and a.dat._zero:
+                d.flags = capi.ARG_ZERO  # the device zero-fills only if its path needs it
+            else:
+                a.dat._materialize()
+            _require(len(a.maps) <= 1, "InvalidArgument", "Dat argument with several maps")
+            if a.maps:
+                md = a.maps[0].desc()
+                keep.append(md)
+                d.map = C.pointer(md)
+        elif a.mat is not None:
+            d.kind, d.data, d.obj_id = capi.ARG_MAT, a.mat.values.data_ptr(), a.mat.id
+            if a.mat._zero:
+                d.flags = capi.ARG_ZERO
+            else:
+                a.mat._materialize()
+            _require(len(a.maps) == 2 and all(m is not None for m in a.maps), "InvalidArgument",
+                     "Mat argument requires row and column maps")
+            r, c, s = a.maps[0].desc(), a.maps[1].desc(), a.mat.sparsity.desc()
+            keep += [r, c, s]
+            d.map, d.col_map, d.sparsity = C.pointer(r), C.pointer(c), C.pointer(s)
+        elif a.glob is not None:
+            d.kind, d.data, d.dim, d.obj_id = capi.ARG_GLOBAL, a.glob.data.data_ptr(), a.glob.dim, a.glob.id
+        else:
+            _fail("InvalidArgument", "argument must target exactly one object")
+    params = (C.c_double * max(len(loop.kernel.params), 1))(*loop.kernel.params)
+    kd = capi.KernelDesc(loop.kernel.name.encode(), params, len(loop.kernel.params))
+    keep += [params, kd]
+    return kd, descs, keep
+
+
+def validate(loop: Parloop) -> None:
+    """parloop.hpp:89-146: descriptor checks only, no state change."""
+    kd, descs, keep = _build(loop)
+    capi.check(capi.lib().loam_gpu_validate(C.byref(kd), loop.iterset.size, loop.iterset.id, descs,
+                                            len(loop.args)))
+
+
+def execute(loop: Parloop, threads: int = 1) -> None:
+    """parloop.hpp:191: `threads` is accepted for drop-in compatibility (the device decides)."""
+    _require(threads >= 1, "InvalidArgument", "thread count must be positive")
+    kd, descs, keep = _build(loop)
+    capi.check(capi.lib().loam_gpu_execute(C.byref(kd), loop.iterset.size, loop.iterset.id, descs,
+                                           len(loop.args), _stream()))
+    for a in loop.args:  # written objects: version bump (data.hpp:49-52), no longer known zero
+        if a.access != READ:
+            if a.dat is not None:
+                a.dat.version += 1
+                a.dat._zero = a.dat._stale = False
+            if a.mat is not None:
+                a.mat._zero = a.mat._stale = False
