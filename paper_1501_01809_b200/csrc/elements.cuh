@@ -89,13 +89,24 @@ struct Geom {
   double V;
 };
 
+// 1/x to within an ulp without the IEEE-division slow path (x is a nonzero,
+// finite Jacobian determinant): hardware seed + two Newton steps.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 template <int D>
 __device__ __forceinline__ void geometry(const double (&X)[D + 1][D], Geom<D>& G) {
   if constexpr (D == 2) {
     const double J00 = X[1][0] - X[0][0], J01 = X[2][0] - X[0][0];
     const double J10 = X[1][1] - X[0][1], J11 = X[2][1] - X[0][1];
     const double det = J00 * J11 - J01 * J10;
-    const double r = 1.0 / det;
+    const double r = fast_rcp(det);
     // K = [[J11, -J10], [-J01, J00]] / det ; g_k[a] = K[a][k-1]
     G.g[1][0] = J11 * r;
     G.g[1][1] = -J01 * r;
@@ -120,7 +131,7 @@ __device__ __forceinline__ void geometry(const double (&X)[D + 1][D], Geom<D>& G
     const double c20 = J[0][1] * J[1][2] - J[0][2] * J[1][1];
     const double c21 = -(J[0][0] * J[1][2] - J[0][2] * J[1][0]);
     const double c22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-    const double r = 1.0 / det;
+    const double r = fast_rcp(det);
     // g_k[a] = K[a][k-1] = c[a][k-1] / det
     G.g[1][0] = c00 * r; G.g[1][1] = c10 * r; G.g[1][2] = c20 * r;
     G.g[2][0] = c01 * r; G.g[2][1] = c11 * r; G.g[2][2] = c21 * r;
@@ -365,6 +376,29 @@ struct FormT<F_ELASTICITY, 3, 1> {
         }
     }
   }
+  // tensor row (a, d) only: used when one lane owns one dof row
+  __device__ __forceinline__ static void subrow(int a, int d, const Geom<3>& G, const double*,
+                                                const FormParams& prm, double* out) {
+    const double lam = prm.p[0], mu = prm.p[1];
+    double ga[3];
+    sel<3>(G, a, ga);
+    const double gad = d == 0 ? ga[0] : (d == 1 ? ga[1] : ga[2]);
+    double mga[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mga[k] = mu * ga[k] * G.V;
+    const double lgad = lam * gad * G.V;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const double gbd = d == 0 ? G.g[b][0] : (d == 1 ? G.g[b][1] : G.g[b][2]);
+      const double gg = dot<3>(mga, G.g[b]);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        double v = fma(mga[e], gbd, lgad * G.g[b][e]);
+        if (d == e) v += gg;
+        out[b * 3 + e] = v;
+      }
+    }
+  }
 };
 
 // Taylor-Hood Stokes blocks (config 5), velocity vector P2 tri (dof (b,e) = b*2+e),
@@ -388,6 +422,17 @@ struct FormT<F_STOKES_A, 2, 2> {
       out[0 * 12 + b * 2 + 1] = 0.0;
       out[1 * 12 + b * 2 + 0] = 0.0;
       out[1 * 12 + b * 2 + 1] = s;
+    }
+  }
+  __device__ __forceinline__ static void subrow(int a, int d, const Geom<2>& G, const double*,
+                                                const FormParams& prm, double* out) {
+    const P2Row<2> R(G, a);
+    const double scale = prm.p[0] * G.V;
+#pragma unroll
+    for (int b = 0; b < 6; ++b) {
+      const double s = scale * R.stiff(G, b);
+      out[b * 2 + 0] = d == 0 ? s : 0.0;
+      out[b * 2 + 1] = d == 1 ? s : 0.0;
     }
   }
 };
@@ -435,7 +480,26 @@ struct FormT<F_STOKES_BT, 2, 2> {
         out[e * 3 + p] = -G.V * v;
       }
   }
+  __device__ __forceinline__ static void subrow(int b, int e, const Geom<2>& G, const double*,
+                                                const FormParams&, double* out) {
+    const P2Row<2> R(G, b);
+    const double gae = e == 0 ? R.ga[0] : R.ga[1], gbe = e == 0 ? R.gb[0] : R.gb[1];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      const double v = R.vertex ? eint<2>(b, p) * gae
+                                : 4.0 * (qint<2>(p, R.b) * gae + qint<2>(p, R.a) * gbe);
+      out[p] = -G.V * v;
+    }
+  }
 };
+
+// Row d of node row i's RD x NC block (the whole row for scalar rows).
+template <class F>
+__device__ __forceinline__ void form_subrow(int i, int d, const Geom<F::GD>& G, const double* C,
+                                            const FormParams& prm, double* out) {
+  if constexpr (F::RD == 1) F::row(i, G, C, prm, out);
+  else F::subrow(i, d, G, C, prm, out);
+}
 
 // Full local tensor (NR x NC, row-major, the staged layout of staged_extents,
 // parloop.hpp:63-70): unrolled row functor.  For vector forms node row a

@@ -17,12 +17,14 @@
 //
 // There is no CPU fallback: an unregistered kernel is an error.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
 #include <unordered_map>
 
+#include "async.cuh"
 #include "elements.cuh"
 #include "engine.cuh"
 #include "plan.cuh"
@@ -230,55 +232,121 @@ struct OwnerArgs {
   int nchunks, seg_max, nrows_node, accumulate;
 };
 
-template <class F>
-__device__ __forceinline__ void gather_geom(const OwnerArgs& a, int s, Geom<F::GD>& G) {
-  constexpr int GD = F::GD;
-  double X[GD + 1][GD];
-  const int32_t* xr = a.xmap + (int64_t)s * a.xstride;
+// Batched gather: the loads of U pairs are issued before any use so U
+// independent pair -> cell-map -> coordinate chains are in flight per lane
+// (the single-pair loop was latency bound: long-scoreboard stalls ~80%).
+template <class F, int U>
+struct PairBatch {
+  static constexpr int GD = F::GD;
+  int code[U];
+  bool valid[U];
+  double X[U][GD + 1][GD];
+  double C[U][F::HAS_COEFF ? F::NCOEFF : 1];
+
+  __device__ __forceinline__ void load(const OwnerArgs& a, int p, int p1) {
+    int vid[U][GD + 1];
 #pragma unroll
-  for (int v = 0; v <= GD; ++v) {
-    const int vid = __ldg(xr + v);
-    if constexpr (GD == 2) {
-      const double2 c = __ldg(reinterpret_cast<const double2*>(a.coords) + vid);
-      X[v][0] = c.x;
-      X[v][1] = c.y;
-    } else {
-#pragma unroll
-      for (int d = 0; d < GD; ++d) X[v][d] = __ldg(a.coords + (int64_t)vid * GD + d);
+    for (int u = 0; u < U; ++u) {
+      valid[u] = p + u < p1;
+      code[u] = __ldg(a.pairs + (valid[u] ? p + u : p));
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int s = code[u] / F::NRN;
+      const int32_t* xr = a.xmap + (int64_t)s * a.xstride;
+#pragma unroll
+      for (int v = 0; v <= GD; ++v) vid[u][v] = __ldg(xr + v);
+    }
+    if constexpr (F::HAS_COEFF) {
+      int cid[U][F::NCOEFF];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int32_t* cr = a.cmap + (int64_t)(code[u] / F::NRN) * a.cstride;
+#pragma unroll
+        for (int q = 0; q < F::NCOEFF; ++q) cid[u][q] = __ldg(cr + q);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < F::NCOEFF; ++q) C[u][q] = __ldg(a.coeff + cid[u][q]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v <= GD; ++v) {
+        if constexpr (GD == 2) {
+          const double2 c = __ldg(reinterpret_cast<const double2*>(a.coords) + vid[u][v]);
+          X[u][v][0] = c.x;
+          X[u][v][1] = c.y;
+        } else {
+#pragma unroll
+          for (int d = 0; d < GD; ++d) X[u][v][d] = __ldg(a.coords + (int64_t)vid[u][v] * GD + d);
+        }
+      }
   }
-  geometry<GD>(X, G);
+};
+
+// In-row ranks of the NCN column nodes of pair p, with the widest aligned loads.
+template <int NCN>
+__device__ __forceinline__ void load_ranks(const uint8_t* ranks, int64_t p, int (&rk)[NCN]) {
+  const uint8_t* b = ranks + p * NCN;
+  if constexpr (NCN % 4 == 0) {
+#pragma unroll
+    for (int w = 0; w < NCN / 4; ++w) {
+      const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(b) + w);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) rk[4 * w + k] = (x >> (8 * k)) & 0xff;
+    }
+  } else if constexpr (NCN % 2 == 0) {
+#pragma unroll
+    for (int w = 0; w < NCN / 2; ++w) {
+      const uint32_t x = __ldg(reinterpret_cast<const uint16_t*>(b) + w);
+      rk[2 * w] = x & 0xff;
+      rk[2 * w + 1] = x >> 8;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < NCN; ++k) rk[k] = __ldg(b + k);
+  }
+}
+
+template <class F>
+constexpr int batch_of() {
+  return F::GD == 2 ? 4 : 2;
 }
 
 // Residual (Dat INC, dim 1): out[r] (+)= sum over pairs of row i of the action.
 template <class F>
 __global__ void __launch_bounds__(kTPB) k_owner_vec(const __grid_constant__ OwnerArgs a) {
+  constexpr int U = batch_of<F>();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= a.nrows_node) return;
   double acc = 0.0;
   const int p1 = __ldg(a.ptr + r + 1);
-  for (int p = __ldg(a.ptr + r); p < p1; ++p) {
-    const int k = __ldg(a.pairs + p);
-    const int s = k / F::NRN, i = k - s * F::NRN;
-    Geom<F::GD> G;
-    gather_geom<F>(a, s, G);
-    double C[F::HAS_COEFF ? F::NCOEFF : 1];
-    if constexpr (F::HAS_COEFF) {
-      const int32_t* cr = a.cmap + (int64_t)s * a.cstride;
+  for (int p = __ldg(a.ptr + r); p < p1; p += U) {
+    PairBatch<F, U> B;
+    B.load(a, p, p1);
 #pragma unroll
-      for (int q = 0; q < F::NCOEFF; ++q) C[q] = __ldg(a.coeff + __ldg(cr + q));
+    for (int u = 0; u < U; ++u) {
+      if (!B.valid[u]) continue;
+      const int i = B.code[u] % F::NRN;
+      Geom<F::GD> G;
+      geometry<F::GD>(B.X[u], G);
+      double v;
+      F::row(i, G, B.C[u], a.prm, &v);
+      acc += v;
     }
-    double v;
-    F::row(i, G, C, a.prm, &v);
-    acc += v;
   }
   a.out[r] = a.accumulate ? a.out[r] + acc : acc;
 }
 
-// Matrix (Mat INC): one warp per chunk of consecutive row nodes, one lane per
-// row node; the chunk's CSR value segment lives in shared memory.
+// Matrix (Mat INC): one warp per chunk of consecutive row nodes; one lane per
+// DOF row (node row x component); the chunk's contiguous CSR value segment
+// is accumulated in shared memory (single owner per row: plain adds) and
+// stored coalesced.
 template <class F>
 __global__ void __launch_bounds__(128) k_owner_mat(const __grid_constant__ OwnerArgs a) {
+  constexpr int U = batch_of<F>();
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const int chunk = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -292,32 +360,291 @@ __global__ void __launch_bounds__(128) k_owner_mat(const __grid_constant__ Owner
   else
     for (int t = lane; t < len; t += 32) seg[t] = 0.0;
   __syncwarp();
-  const int r = r0 + lane;
-  if (r < r1) {
+  const int node = lane / F::RD, d = lane - node * F::RD;
+  const int r = r0 + node;
+  if (node < 32 / F::RD && r < r1) {
     const int64_t rs = __ldg(a.row_ptr + (int64_t)r * F::RD);
-    const int rstart = (int)(rs - base);
     const int nlen = (int)((__ldg(a.row_ptr + (int64_t)r * F::RD + 1) - rs) / F::CD); // column nodes
+    const int rstart = (int)(rs - base) + d * nlen * F::CD;
     const int p1 = __ldg(a.ptr + r + 1);
-    for (int p = __ldg(a.ptr + r); p < p1; ++p) {
-      const int k = __ldg(a.pairs + p);
-      const int s = k / F::NRN, i = k - s * F::NRN;
-      Geom<F::GD> G;
-      gather_geom<F>(a, s, G);
-      double blk[F::RD * F::NC];
-      F::row(i, G, nullptr, a.prm, blk);
-      const uint8_t* rk = a.ranks + (int64_t)p * F::NCN;
+    for (int p = __ldg(a.ptr + r); p < p1; p += U) {
+      PairBatch<F, U> B;
+      B.load(a, p, p1);
+      int rk[U][F::NCN];
 #pragma unroll
-      for (int j = 0; j < F::NCN; ++j) {
-        const int pos = rstart + __ldg(rk + j) * F::CD;
+      for (int u = 0; u < U; ++u) load_ranks<F::NCN>(a.ranks, B.valid[u] ? p + u : p, rk[u]);
 #pragma unroll
-        for (int d = 0; d < F::RD; ++d)
+      for (int u = 0; u < U; ++u) {
+        if (!B.valid[u]) continue;
+        const int i = B.code[u] % F::NRN;
+        Geom<F::GD> G;
+        geometry<F::GD>(B.X[u], G);
+        double blk[F::NC];
+        form_subrow<F>(i, d, G, nullptr, a.prm, blk);
 #pragma unroll
-          for (int c = 0; c < F::CD; ++c) seg[pos + d * nlen * F::CD + c] += blk[d * F::NC + j * F::CD + c];
+        for (int j = 0; j < F::NCN; ++j) {
+          const int pos = rstart + rk[u][j] * F::CD;
+#pragma unroll
+          for (int c = 0; c < F::CD; ++c) seg[pos + c] += blk[j * F::CD + c];
+        }
       }
     }
   }
   __syncwarp();
   for (int t = lane; t < len; t += 32) a.out[base + t] = seg[t];
+}
+
+// ---------------------------------------------------------------------------
+// Neighbour-list tile kernel (plan.cuh NbrPlan): P1 forms whose row, column
+// and coordinate maps are one node map.  Persistent CTAs walk tiles of
+// consecutive rows through a 3-deep ring of shared-memory stages.  For tile
+// k+2, thread 0 issues TMA bulk copies (cp.async.bulk + mbarrier tx count) of
+//   * the tile's contiguous plan ranges: row offsets, pair offsets, pair
+//     records (in-row ranks), window slots of the pattern entries, own ranks;
+//   * the tile's VERTEX WINDOW: the few contiguous runs of coordinates (and
+//     coefficients) the tile references -- no per-entry gathers at all;
+// then every thread computes tile k from shared memory: one thread per dof
+// row walks its pair records, reads the cell's vertices as
+// window[widx[rank]], computes its element row (cells are pre-rotated so the
+// row is local vertex 0) and accumulates it -- in registers with
+// compile-time slots when rows are short (LMAX), else in a shared segment --
+// writing every output value exactly once.
+
+struct TileArgs {
+  const int32_t* tiles;
+  int ntiles;
+  const int32_t* nptr;
+  const int32_t* pptr;
+  const uint8_t* recs;
+  const uint16_t* widx;
+  const uint8_t* selfr;
+  const int32_t* runs;
+  const double* coords;
+  const double* coeff;
+  FormParams prm;
+  double* out;
+  int accumulate, bits, max_len;
+  long long* timing; // unused (kept for ABI of the phase-timing tool)
+  // dynamic shared memory layout (bytes)
+  int off_seg, off_buf, buf_bytes;
+  int b_nptr, b_pptr, b_recs, b_widx, b_selfr, b_win, b_winc; // inside one ring stage
+};
+
+__device__ __forceinline__ int skew_of(int lo, int es) { return ((lo * es) & 15) / es; }
+
+constexpr int kTileThreads = 256;
+
+template <class F, class Rec, int LMAX>
+__global__ void __launch_bounds__(kTileThreads, 3) k_tile(const __grid_constant__ TileArgs a) {
+  constexpr int GD = F::GD, W = F::RD * F::CD;
+  constexpr int ES = sizeof(Rec);
+  constexpr bool REG = F::BILINEAR && LMAX > 0;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int b = 0; b < 3; ++b) mbar_init(&full[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int K = a.ntiles > (int)blockIdx.x ? (a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto tile_meta = [&](int k, int (&m)[8]) {
+    const int4* t = reinterpret_cast<const int4*>(a.tiles + 8 * (blockIdx.x + k * gridDim.x));
+    const int4 x = __ldg(t), y = __ldg(t + 1);
+    m[0] = x.x; m[1] = x.y; m[2] = x.z; m[3] = x.w; m[4] = y.x; m[5] = y.y; m[6] = y.z; m[7] = y.w;
+  };
+  auto ring = [&](int k) { return sm + a.off_buf + (k % 3) * a.buf_bytes; };
+  auto issue = [&](int k) { // thread 0
+    int m[8];
+    tile_meta(k, m);
+    unsigned char* buf = ring(k);
+    uint64_t* bar = &full[k % 3];
+    uint32_t tx = 0;
+    auto range = [&](unsigned char* dst, const void* src, int lo, int hi, int es) {
+      const int64_t s0 = ((int64_t)lo * es) & ~int64_t(15), s1 = ((int64_t)hi * es + 15) & ~int64_t(15);
+      const uint32_t n = (uint32_t)(s1 - s0);
+      if (n) bulk_g2s(dst, reinterpret_cast<const unsigned char*>(src) + s0, n, bar);
+    };
+    auto range_bytes = [](int lo, int hi, int es) {
+      const int64_t s0 = ((int64_t)lo * es) & ~int64_t(15), s1 = ((int64_t)hi * es + 15) & ~int64_t(15);
+      return (uint32_t)(s1 - s0);
+    };
+    tx += 2 * range_bytes(m[0], m[1] + 1, 4) + range_bytes(m[4], m[5], ES) + range_bytes(m[2], m[3], 2) +
+          range_bytes(m[0], m[1], 1);
+    // vertex window runs: 16-byte multiples by TMA, an 8-byte tail by hand
+    double* win = reinterpret_cast<double*>(buf + a.b_win);
+    double* winc = reinterpret_cast<double*>(buf + a.b_winc);
+    int slot = 0;
+    for (int r = 0; r < m[7]; ++r) {
+      const int lo = __ldg(a.runs + 2 * (m[6] + r)), hi = __ldg(a.runs + 2 * (m[6] + r) + 1);
+      const uint32_t nb = (uint32_t)(hi - lo) * GD * 8;
+      tx += nb & ~15u;
+      if (nb & 15) { // odd vertex count at the end of the array (GD odd): copy the last 8 bytes
+        const int64_t e = (int64_t)hi * GD - 1;
+        win[(int64_t)(slot + hi - lo) * GD - 1] = a.coords[e];
+      }
+      if constexpr (F::HAS_COEFF) {
+        const uint32_t nc = (uint32_t)(hi - lo) * 8;
+        tx += nc & ~15u;
+        if (nc & 15) winc[slot + hi - lo - 1] = a.coeff[hi - 1];
+      }
+      slot += hi - lo;
+    }
+    fence_async_shared();
+    mbar_arrive_expect_tx(bar, tx);
+    range(buf + a.b_nptr, a.nptr, m[0], m[1] + 1, 4);
+    range(buf + a.b_pptr, a.pptr, m[0], m[1] + 1, 4);
+    range(buf + a.b_recs, a.recs, m[4], m[5], ES);
+    range(buf + a.b_widx, a.widx, m[2], m[3], 2);
+    range(buf + a.b_selfr, a.selfr, m[0], m[1], 1);
+    slot = 0;
+    for (int r = 0; r < m[7]; ++r) {
+      const int lo = __ldg(a.runs + 2 * (m[6] + r)), hi = __ldg(a.runs + 2 * (m[6] + r) + 1);
+      const uint32_t nb = ((uint32_t)(hi - lo) * GD * 8) & ~15u;
+      if (nb) bulk_g2s(win + (int64_t)slot * GD, a.coords + (int64_t)lo * GD, nb, bar);
+      if constexpr (F::HAS_COEFF) {
+        const uint32_t nc = ((uint32_t)(hi - lo) * 8) & ~15u;
+        if (nc) bulk_g2s(winc + slot, a.coeff + lo, nc, bar);
+      }
+      slot += hi - lo;
+    }
+  };
+
+  if (tid == 0) {
+    if (K > 0) issue(0);
+    if (K > 1) issue(1);
+  }
+  double* seg = reinterpret_cast<double*>(sm + a.off_seg);
+  const uint32_t mask = (1u << a.bits) - 1;
+  for (int k = 0; k < K; ++k) {
+    if (tid == 0 && k + 2 < K) issue(k + 2); // its ring stage was released by the barrier ending tile k-1
+    int m[8];
+    tile_meta(k, m);
+    const int R0 = m[0], nrows = m[1] - m[0], A0 = m[2], nA = m[3] - m[2], P0 = m[4];
+    const int64_t E0 = (int64_t)A0 * W;
+    if constexpr (F::BILINEAR && !REG) {
+      const int len = nA * W;
+      if (a.accumulate)
+        for (int t = tid; t < len; t += kTileThreads) seg[t] = a.out[E0 + t];
+      else
+        for (int t = tid; t < len; t += kTileThreads) seg[t] = 0.0;
+      __syncthreads();
+    }
+    mbar_wait(&full[k % 3], (k / 3) & 1);
+    const unsigned char* buf = ring(k);
+    const int32_t* nptr_s = reinterpret_cast<const int32_t*>(buf + a.b_nptr) + skew_of(R0, 4);
+    const int32_t* pptr_s = reinterpret_cast<const int32_t*>(buf + a.b_pptr) + skew_of(R0, 4);
+    const Rec* recs_s = reinterpret_cast<const Rec*>(buf + a.b_recs) + skew_of(P0, ES);
+    const uint16_t* widx_s = reinterpret_cast<const uint16_t*>(buf + a.b_widx) + skew_of(A0, 2);
+    const uint8_t* selfr_s = buf + a.b_selfr + skew_of(R0, 1);
+    const double* win = reinterpret_cast<const double*>(buf + a.b_win);
+    const double* winc = reinterpret_cast<const double*>(buf + a.b_winc);
+    const int node = tid / F::RD, d = tid - node * F::RD;
+    if (node < nrows) {
+      const int a0 = nptr_s[node] - A0;
+      const int L = nptr_s[node + 1] - A0 - a0;
+      const int rstart = a0 * W + d * L * F::CD - a0 * F::CD;
+      const int p1 = pptr_s[node + 1] - P0;
+      const int self = a0 + selfr_s[node];
+      double racc[REG ? LMAX : 1];
+      double diag = 0.0, acc = 0.0;
+      if constexpr (REG)
+#pragma unroll
+        for (int q = 0; q < LMAX; ++q) racc[q] = 0.0;
+      auto vertex = [&](int rank, double (&x)[GD]) {
+        const int wv = widx_s[rank];
+        if constexpr (GD == 2) {
+          const double2 c2 = reinterpret_cast<const double2*>(win)[wv];
+          x[0] = c2.x;
+          x[1] = c2.y;
+        } else {
+#pragma unroll
+          for (int c = 0; c < GD; ++c) x[c] = win[wv * GD + c];
+        }
+      };
+      double X0[GD];
+      vertex(self, X0);
+      for (int p = pptr_s[node] - P0; p < p1; p += 2) { // two pairs per iteration (ILP)
+        constexpr int N = F::NRN;
+        const bool two = p + 1 < p1;
+        const uint32_t rec[2] = {(uint32_t)recs_s[p], (uint32_t)recs_s[two ? p + 1 : p]};
+        int rr[2][N];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          rr[u][0] = self;
+#pragma unroll
+          for (int j = 1; j < N; ++j) rr[u][j] = a0 + ((rec[u] >> ((j - 1) * a.bits)) & mask);
+        }
+        double X[2][GD + 1][GD];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+#pragma unroll
+          for (int c = 0; c < GD; ++c) X[u][0][c] = X0[c];
+#pragma unroll
+          for (int v = 1; v <= GD; ++v) vertex(rr[u][v], X[u][v]);
+        }
+        Geom<GD> G[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) geometry<GD>(X[u], G[u]);
+        if constexpr (F::BILINEAR) {
+          double blk[2][F::NC];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) form_subrow<F>(0, d, G[u], nullptr, a.prm, blk[u]);
+          if constexpr (REG) { // rotated local vertex 0 is the row node: blk[0] is diagonal
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const double wgt = (u == 0 || two) ? 1.0 : 0.0;
+              diag = fma(wgt, blk[u][0], diag);
+#pragma unroll
+              for (int j = 1; j < F::NCN; ++j) {
+                const int sl = rr[u][j] - a0;
+                const double v = wgt * blk[u][j];
+#pragma unroll
+                for (int q = 0; q < LMAX; ++q)
+                  if (sl == q) racc[q] += v;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              if (u == 1 && !two) break;
+#pragma unroll
+              for (int j = 0; j < F::NCN; ++j)
+#pragma unroll
+                for (int c = 0; c < F::CD; ++c) seg[rstart + rr[u][j] * F::CD + c] += blk[u][j * F::CD + c];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            double C[F::HAS_COEFF ? F::NCOEFF : 1];
+            if constexpr (F::HAS_COEFF)
+#pragma unroll
+              for (int q = 0; q < F::NCOEFF; ++q) C[q] = winc[widx_s[rr[u][q]]];
+            double v;
+            F::row(0, G[u], C, a.prm, &v);
+            if (u == 0 || two) acc += v;
+          }
+        }
+      }
+      if constexpr (!F::BILINEAR) a.out[R0 + node] = a.accumulate ? a.out[R0 + node] + acc : acc;
+      if constexpr (REG) { // the row straight from registers (scalar rows: W == 1)
+        double* o = a.out + E0 + a0;
+#pragma unroll
+        for (int q = 0; q < LMAX; ++q)
+          if (q < L) {
+            const double v = racc[q] + (q == self - a0 ? diag : 0.0);
+            o[q] = a.accumulate ? o[q] + v : v;
+          }
+      }
+    }
+    __syncthreads(); // tile k consumed: ring stage k%3 may be refilled
+    if constexpr (F::BILINEAR && !REG) {
+      const int len = nA * W;
+      for (int t = tid; t < len; t += kTileThreads) a.out[E0 + t] = seg[t];
+      __syncthreads();
+    }
+  }
 }
 
 // ===========================================================================
@@ -326,6 +653,7 @@ __global__ void __launch_bounds__(128) k_owner_mat(const __grid_constant__ Owner
 
 using GenericFn = void (*)(const GLaunch&, cudaStream_t);
 using OwnerFn = void (*)(const OwnerArgs&, int grid, size_t smem, cudaStream_t);
+using NbrFn = void (*)(const TileArgs&, int rec_bytes, size_t smem, cudaStream_t);
 
 struct Entry {
   KernelInfo info;
@@ -335,6 +663,7 @@ struct Entry {
   int form = -1, gd = 0, nrn = 0, ncn = 0, rd = 1, cd = 1, ncoeff = 0;
   bool bilinear = false, has_coeff = false;
   OwnerFn owner = nullptr;
+  NbrFn nbr = nullptr; // P1 forms only
 };
 
 template <class K>
@@ -358,6 +687,40 @@ void launch_owner(const OwnerArgs& a, int grid, size_t smem, cudaStream_t s) {
   } else {
     k_owner_vec<F><<<grid, kTPB, 0, s>>>(a);
   }
+  count_launch();
+  LG_LAUNCH_CHECK();
+}
+
+template <class F>
+void launch_nbr(const TileArgs& a, int rec_bytes, size_t smem, cudaStream_t s) {
+  if (a.ntiles == 0) return;
+  auto go = [&](auto kern) {
+    static int per_sm = -1;
+    static size_t attr_smem = 0;
+    if (attr_smem < smem) {
+      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_smem = smem;
+      per_sm = -1;
+    }
+    int blocks = 1;
+    LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kTileThreads, smem));
+    per_sm = blocks > 0 ? blocks : 1;
+    const int grid = std::min(a.ntiles, per_sm * kNumSMs);
+    kern<<<grid, kTileThreads, smem, s>>>(a);
+  };
+  if constexpr (F::BILINEAR && F::RD == 1 && F::CD == 1) {
+    if (a.max_len <= 8) {
+      if (rec_bytes == 1) go(k_tile<F, uint8_t, 8>);
+      else if (rec_bytes == 2) go(k_tile<F, uint16_t, 8>);
+      else go(k_tile<F, uint32_t, 8>);
+      count_launch();
+      LG_LAUNCH_CHECK();
+      return;
+    }
+  }
+  if (rec_bytes == 1) go(k_tile<F, uint8_t, 0>);
+  else if (rec_bytes == 2) go(k_tile<F, uint16_t, 0>);
+  else go(k_tile<F, uint32_t, 0>);
   count_launch();
   LG_LAUNCH_CHECK();
 }
@@ -395,6 +758,7 @@ Entry form_entry(const std::string& name) {
   e.bilinear = F::BILINEAR;
   e.has_coeff = F::HAS_COEFF;
   e.owner = &launch_owner<F>;
+  if constexpr (P == 1 && F::NRN == D + 1 && (!F::BILINEAR || F::NCN == F::NRN)) e.nbr = &launch_nbr<F>;
   return e;
 }
 
@@ -550,6 +914,8 @@ NodeMap node_view(const loam_map_desc* m) {
 }
 
 struct FastPlan {
+  bool use_nbr = false;
+  NbrPlan nb;
   LocalityPlan loc;
   SortedMap xmap, cmap;
   const int32_t* xptr = nullptr;
@@ -587,7 +953,10 @@ bool prefix_equal(const int32_t* a, int sa, const int32_t* b, int sb, int ncols,
   return h == 0;
 }
 
-constexpr int kSegMax = 2048; // doubles of shared memory per warp (16 KB)
+constexpr int kSegMax = 2048;  // doubles of shared memory per warp (16 KB), pair-list kernels
+constexpr int kTileSeg = 4096;   // matrix values per neighbour-list tile (32 KB)
+constexpr int kTileSlots = 1024; // vertices in a tile's window
+constexpr int kTileRuns = 32;    // contiguous runs per window
 
 std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_desc* args,
                                           cudaStream_t s) {
@@ -609,6 +978,39 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
   const int32_t* perm = P->loc.perm.get();
   SortedMap srows;
   gather_rows(R.v, perm, srows, s);
+  // Neighbour-list plan when row, column, coordinate (and coefficient) maps
+  // are one node map (P1 forms): no per-pair cell ids or map rows at all.
+  const int strat = options().inc_strategy;
+  if (k.nbr && (strat == 0 || strat == 4)) {
+    auto same = [&](const MapView& m) {
+      return m.arity == R.v.arity && (m.v == R.v.v || prefix_equal(m.v, m.arity, R.v.v, R.v.arity, m.arity, n, s));
+    };
+    bool ok = R.dim == 1 || k.bilinear;
+    ok = ok && same(MapView{X->values, n, X->arity, X->target_size}) && X->target_size == R.v.target;
+    if (Cm) ok = ok && same(MapView{Cm->values, n, Cm->arity, Cm->target_size});
+    CsrView csr{};
+    if (k.bilinear) {
+      const NodeMap Cn = node_view(args[0].col_map);
+      ok = ok && same(Cn.v) && Cn.v.target == R.v.target;
+      const loam_sparsity_desc* sp = args[0].sparsity;
+      csr = CsrView{sp->row_ptr, sp->col_idx, sp->nrows, sp->ncols, sp->nnz, R.dim, Cn.dim};
+      if (ok && (R.dim > 1 || Cn.dim > 1)) { // blockedness of the pattern
+        DevBuf<int> dummy;
+        PairPlan probe;
+        probe.nrows_node = R.v.target;
+        probe.npairs = 0;
+        build_ranks(probe, srows.v.get(), srows.v.get(), 0, csr, s); // throws ShapeMismatch if not blocked
+      }
+    }
+    // the window TMA needs 16-byte aligned coordinate / coefficient arrays
+    ok = ok && (reinterpret_cast<uintptr_t>(args[1].data) & 15) == 0 &&
+         (!Cm || (reinterpret_cast<uintptr_t>(args[2].data) & 15) == 0);
+    if (ok && build_nbr(P->nb, srows.v.get(), n, R.v.arity, R.v.target, csr, kTileThreads / R.dim,
+                        k.bilinear ? kTileSeg : (1 << 30), kTileSlots, kTileRuns, s)) {
+      P->use_nbr = true;
+      return P;
+    }
+  }
   build_pairs(srows.v.get(), n, R.v.arity, R.v.target, P->pp, s);
   if (k.bilinear) {
     const NodeMap Cn = node_view(args[0].col_map);
@@ -621,7 +1023,7 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     const loam_sparsity_desc* sp = args[0].sparsity;
     CsrView csr{sp->row_ptr, sp->col_idx, sp->nrows, sp->ncols, sp->nnz, R.dim, Cn.dim};
     build_ranks(P->pp, srows.v.get(), sc, Cn.v.arity, csr, s);
-    build_chunks(P->pp, csr, kSegMax, s);
+    build_chunks(P->pp, csr, kSegMax, 32 / R.dim, s);
   }
   // sorted coordinate / coefficient maps; share storage where maps coincide
   const MapView xv{X->values, n, X->arity, X->target_size};
@@ -682,7 +1084,7 @@ bool fast_pattern(const Entry& k, const loam_arg_desc* args, int nargs) {
 void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const FormParams& prm,
               cudaStream_t s) {
   std::vector<uint64_t> key{(uint64_t)k.form, (uint64_t)k.gd, (uint64_t)k.nrn, (uint64_t)k.ncn,
-                            (uint64_t)options().locality};
+                            (uint64_t)options().locality, (uint64_t)options().inc_strategy};
   bool cacheable = true;
   for (int q = 0; q < nargs; ++q) {
     const loam_arg_desc& a = args[q];
@@ -708,6 +1110,50 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
       std::lock_guard<std::mutex> g(g_cache_mutex);
       g_fast_cache[key] = P;
     }
+  }
+  if (P->use_nbr) {
+    const NbrPlan& nb = P->nb;
+    TileArgs t{};
+    t.tiles = nb.tiles.get();
+    t.ntiles = nb.ntiles;
+    t.nptr = nb.nptr.get();
+    t.pptr = nb.pptr.get();
+    t.recs = nb.recs.get();
+    t.widx = nb.widx.get();
+    t.selfr = nb.selfr.get();
+    t.runs = nb.runs.get();
+    t.coords = args[1].data;
+    t.coeff = k.has_coeff ? args[2].data : nullptr;
+    t.prm = prm;
+    t.out = args[0].data;
+    t.accumulate = (args[0].flags & LOAM_ARG_ZERO) ? 0 : 1;
+    t.bits = nb.bits;
+    t.max_len = nb.max_len;
+    auto up16 = [](int x) { return (x + 15) & ~15; };
+    int off = 64; // 3 mbarriers
+    t.off_seg = off;
+    const bool reg = k.bilinear && k.rd == 1 && k.cd == 1 && nb.max_len <= 8;
+    off += up16(k.bilinear && !reg ? nb.max_seg * 8 : 0);
+    t.off_buf = off;
+    int b = 0;
+    t.b_nptr = b;
+    b += up16((nb.max_rows + 1) * 4 + 32);
+    t.b_pptr = b;
+    b += up16((nb.max_rows + 1) * 4 + 32);
+    t.b_recs = b;
+    b += up16(nb.max_pairs * nb.rec_bytes + 32);
+    t.b_widx = b;
+    b += up16(nb.max_adj * 2 + 32);
+    t.b_selfr = b;
+    b += up16(nb.max_rows + 32);
+    t.b_win = b;
+    b += up16(nb.max_slots * k.gd * 8);
+    t.b_winc = b;
+    b += up16(k.has_coeff ? nb.max_slots * 8 : 0);
+    t.buf_bytes = b;
+    off += 3 * b;
+    k.nbr(t, nb.rec_bytes, (size_t)off, s);
+    return;
   }
   OwnerArgs a{};
   a.ptr = P->pp.ptr.get();
@@ -902,7 +1348,7 @@ void execute(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_de
   FormParams prm{{0, 0, 0, 0}};
   for (int i = 0; i < kd->nparams && i < 4; ++i) prm.p[i] = kd->params[i];
   const int strat = options().inc_strategy;
-  if (n > 0 && (strat == 0 || strat == 2) && fast_pattern(k, args, nargs)) {
+  if (n > 0 && (strat == 0 || strat == 2 || strat == 4) && fast_pattern(k, args, nargs)) {
     try {
       run_fast(k, n, args, nargs, prm, s);
       return;

@@ -192,7 +192,230 @@ __global__ void k_jp_round(int n, InvMap m0, InvMap m1, InvMap m2, InvMap m3, in
   col[e] = c;
 }
 
+__global__ void k_node_pattern(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int nrows_node,
+                               int rd, int cd, int64_t* nptr, int32_t* nadj) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > nrows_node) return;
+  const int64_t s0 = rp[(int64_t)r * rd];
+  nptr[r] = s0 / ((int64_t)rd * cd);
+  if (r == nrows_node) return;
+  const int64_t len = (rp[(int64_t)r * rd + 1] - s0) / cd;
+  const int64_t o = s0 / ((int64_t)rd * cd);
+  for (int64_t k = 0; k < len; ++k) nadj[o + k] = ci[s0 + k * cd] / cd;
+}
+
+// Records of the neighbour-list plan (P1 forms): the cell is rotated so the
+// owning row is local vertex 0, and the record packs the in-row ranks of the
+// other vertices (i+1)%N .. (i+N-1)%N, `bits` each from bit 0.  The row's own
+// rank is a per-row constant recomputed by the kernel.
+template <class Rec>
+__global__ void k_records(const int32_t* __restrict__ pairs, int64_t npairs, int nrn,
+                          const int32_t* __restrict__ srows, const int32_t* __restrict__ pptr, int nrows_node,
+                          const int64_t* __restrict__ nptr, const int32_t* __restrict__ nadj, int bits, Rec* recs,
+                          unsigned long long* err) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrows_node) return;
+  const int64_t a0 = nptr[r];
+  const int len = (int)(nptr[r + 1] - a0);
+  if (len > (1 << bits)) { atomicCAS(err, 0ull, 1ull << 62); return; }
+  for (int p = pptr[r]; p < pptr[r + 1]; ++p) {
+    const int k = pairs[p];
+    const int s = k / nrn, i = k - s * nrn;
+    uint32_t rec = 0;
+    for (int j = 0; j < nrn; ++j) {
+      const int c = srows[(int64_t)s * nrn + (i + j) % nrn];
+      int lo = 0, hi = len;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (nadj[a0 + mid] < c) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo == len || nadj[a0 + lo] != c) {
+        atomicCAS(err, 0ull, (1ull << 63) | ((unsigned long long)(uint32_t)r << 32) | (uint32_t)c);
+        return;
+      }
+      if (j > 0) rec |= (uint32_t)lo << ((j - 1) * bits);
+    }
+    recs[p] = (Rec)rec;
+  }
+}
+
 } // namespace
+
+__global__ void k_i64_to_i32(const int64_t* __restrict__ a, int64_t n, int32_t* b) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) b[t] = (int32_t)a[t];
+}
+
+bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int nrows_node,
+               const CsrView& csr, int tile_rows, int tile_seg, int tile_slots, int tile_runs,
+               cudaStream_t s) {
+  np.nrows_node = nrows_node;
+  np.nrn = nrn;
+  // ---- node-level pattern, as plan-owned int32 arrays padded by 16 bytes
+  CsrView node = csr;
+  int64_t* built_rp = nullptr;
+  int32_t* built_ci = nullptr;
+  if (!csr.row_ptr) { // Dat INC: the pattern of (map, map)
+    MapView m{sorted_rows, ncells, nrn, nrows_node};
+    int64_t nnz = 0;
+    build_sparsity_dev(m, m, 1, 1, &built_rp, &built_ci, &nnz, s);
+    node = CsrView{built_rp, built_ci, nrows_node, nrows_node, nnz, 1, 1};
+  }
+  np.rd = node.rd;
+  np.cd = node.cd;
+  const int64_t nn = node.nnz / ((int64_t)node.rd * node.cd);
+  require(nn < (int64_t(1) << 31), LOAM_ERR(InvalidArgument), "node pattern exceeds 2^31 entries");
+  np.nptr.alloc(nrows_node + 1 + 4, s);
+  DevBuf<int32_t> nadj(nn + 4, s);
+  LG_CUDA(cudaMemsetAsync(np.nptr.get(), 0, np.nptr.bytes(), s));
+  LG_CUDA(cudaMemsetAsync(nadj.get(), 0, nadj.bytes(), s));
+  if (node.rd == 1 && node.cd == 1) {
+    k_i64_to_i32<<<ceil_div(nrows_node + 1, kTPB), kTPB, 0, s>>>(node.row_ptr, nrows_node + 1, np.nptr.get());
+    count_launch();
+    if (nn) LG_CUDA(cudaMemcpyAsync(nadj.get(), node.col_idx, sizeof(int32_t) * nn, cudaMemcpyDeviceToDevice, s));
+  } else {
+    DevBuf<int64_t> tmp(nrows_node + 1, s);
+    k_node_pattern<<<ceil_div(nrows_node + 1, kTPB), kTPB, 0, s>>>(node.row_ptr, node.col_idx, nrows_node, node.rd,
+                                                                   node.cd, tmp.get(), nadj.get());
+    k_i64_to_i32<<<ceil_div(nrows_node + 1, kTPB), kTPB, 0, s>>>(tmp.get(), nrows_node + 1, np.nptr.get());
+    count_launch(2);
+  }
+  LG_LAUNCH_CHECK();
+  if (built_rp) {
+    LG_CUDA(cudaFreeAsync(built_rp, s));
+    LG_CUDA(cudaFreeAsync(built_ci, s));
+  }
+  // ---- pairs grouped by row, packed records
+  PairPlan pp;
+  build_pairs(sorted_rows, ncells, nrn, nrows_node, pp, s);
+  std::vector<int32_t> h(nrows_node + 1), hp(nrows_node + 1);
+  LG_CUDA(cudaMemcpyAsync(h.data(), np.nptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hp.data(), pp.ptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  int64_t maxlen = 1;
+  for (int r = 0; r < nrows_node; ++r) maxlen = std::max<int64_t>(maxlen, h[r + 1] - h[r]);
+  np.bits = bits_for(maxlen - 1);
+  np.max_len = (int)maxlen;
+  const int rbits = (nrn - 1) * np.bits;
+  if (rbits > 32) return false;
+  np.rec_bytes = rbits <= 8 ? 1 : (rbits <= 16 ? 2 : 4);
+  np.recs.alloc(pp.npairs * np.rec_bytes + 16, s);
+  LG_CUDA(cudaMemsetAsync(np.recs.get(), 0, np.recs.bytes(), s));
+  DevBuf<unsigned long long> err(1, s);
+  LG_CUDA(cudaMemsetAsync(err.get(), 0, sizeof(unsigned long long), s));
+  DevBuf<int64_t> nptr64(nrows_node + 1, s);
+  {
+    std::vector<int64_t> h64(h.begin(), h.end());
+    LG_CUDA(cudaMemcpyAsync(nptr64.get(), h64.data(), sizeof(int64_t) * (nrows_node + 1), cudaMemcpyHostToDevice, s));
+    if (pp.npairs) {
+      if (np.rec_bytes == 1)
+        k_records<uint8_t><<<ceil_div(nrows_node, kTPB), kTPB, 0, s>>>(
+            pp.pairs.get(), pp.npairs, nrn, sorted_rows, pp.ptr.get(), nrows_node, nptr64.get(), nadj.get(),
+            np.bits, reinterpret_cast<uint8_t*>(np.recs.get()), err.get());
+      else if (np.rec_bytes == 2)
+        k_records<uint16_t><<<ceil_div(nrows_node, kTPB), kTPB, 0, s>>>(
+            pp.pairs.get(), pp.npairs, nrn, sorted_rows, pp.ptr.get(), nrows_node, nptr64.get(), nadj.get(),
+            np.bits, reinterpret_cast<uint16_t*>(np.recs.get()), err.get());
+      else
+        k_records<uint32_t><<<ceil_div(nrows_node, kTPB), kTPB, 0, s>>>(
+            pp.pairs.get(), pp.npairs, nrn, sorted_rows, pp.ptr.get(), nrows_node, nptr64.get(), nadj.get(),
+            np.bits, reinterpret_cast<uint32_t*>(np.recs.get()), err.get());
+      count_launch();
+      LG_LAUNCH_CHECK();
+    }
+    unsigned long long herr = 0;
+    LG_CUDA(cudaMemcpyAsync(&herr, err.get(), sizeof(herr), cudaMemcpyDeviceToHost, s));
+    LG_CUDA(cudaStreamSynchronize(s));
+    if (herr >> 63) {
+      const int row = (int)((herr >> 32) & 0x7fffffff), col = (int)(uint32_t)herr;
+      fail(LOAM_ERR(OutsideSparsity), "mat: entry (" + std::to_string(row * node.rd) + ", " +
+                                          std::to_string(col * node.cd) + ") outside sparsity");
+    }
+    if (herr >> 62) return false;
+  }
+  np.pptr.alloc(nrows_node + 1 + 4, s);
+  LG_CUDA(cudaMemsetAsync(np.pptr.get(), 0, np.pptr.bytes(), s));
+  LG_CUDA(cudaMemcpyAsync(np.pptr.get(), pp.ptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToDevice, s));
+  // ---- CTA tiles with contiguous vertex windows
+  std::vector<int32_t> hadj(nn);
+  if (nn) LG_CUDA(cudaMemcpyAsync(hadj.data(), nadj.get(), sizeof(int32_t) * nn, cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  const int64_t w = (int64_t)node.rd * node.cd;
+  const int nv = nrows_node; // P1: row nodes are the coordinate vertices
+  constexpr int kGap = 8;    // merge runs separated by <= kGap unused vertices
+  std::vector<int32_t> tiles, runs;
+  std::vector<uint16_t> hw(nn + 8, 0);
+  std::vector<uint8_t> hs(nrows_node + 16, 0);
+  std::vector<int32_t> verts;
+  std::vector<std::pair<int, int>> rr;
+  auto make_runs = [&](int r0, int r1) { // runs of the tile's vertices; returns slot count
+    verts.assign(hadj.begin() + h[r0], hadj.begin() + h[r1]);
+    std::sort(verts.begin(), verts.end());
+    verts.erase(std::unique(verts.begin(), verts.end()), verts.end());
+    rr.clear();
+    int slots = 0;
+    for (int v : verts) {
+      const int lo = v & ~1, hi = std::min(nv, (v + 2) & ~1);
+      if (!rr.empty() && lo <= rr.back().second + kGap) rr.back().second = std::max(rr.back().second, hi);
+      else rr.emplace_back(lo, hi);
+    }
+    for (auto& x : rr) slots += x.second - x.first;
+    return slots;
+  };
+  int r0 = 0;
+  while (r0 < nrows_node) {
+    int r1 = std::min(nrows_node, r0 + tile_rows);
+    while (r1 > r0 + 1 && (int64_t)(h[r1] - h[r0]) * w > tile_seg) --r1;
+    int slots = make_runs(r0, r1);
+    while (r1 > r0 + 1 && (slots > tile_slots || (int)rr.size() > tile_runs)) {
+      r1 = r0 + (r1 - r0) / 2;
+      slots = make_runs(r0, r1);
+    }
+    if (slots > tile_slots || (int)rr.size() > tile_runs || (int64_t)(h[r1] - h[r0]) * w > tile_seg)
+      return false; // a single row does not fit: use the pair-list path
+    // window slots: run k occupies [base_k, base_k + hi - lo)
+    std::vector<int> base(rr.size());
+    int acc = 0;
+    for (size_t k = 0; k < rr.size(); ++k) {
+      base[k] = acc;
+      acc += rr[k].second - rr[k].first;
+    }
+    for (int64_t a = h[r0]; a < h[r1]; ++a) {
+      const int v = hadj[a];
+      size_t k = std::upper_bound(rr.begin(), rr.end(), std::make_pair(v, INT32_MAX)) - rr.begin() - 1;
+      hw[a] = (uint16_t)(base[k] + v - rr[k].first);
+    }
+    for (int r = r0; r < r1; ++r) {
+      int q = 0;
+      while (h[r] + q < h[r + 1] && hadj[h[r] + q] != r) ++q;
+      require(h[r] + q < h[r + 1], LOAM_ERR(InvalidArgument), "row node missing from its own pattern row");
+      hs[r] = (uint8_t)q;
+    }
+    tiles.insert(tiles.end(), {r0, r1, h[r0], h[r1], hp[r0], hp[r1], (int)runs.size() / 2, (int)rr.size()});
+    for (auto& x : rr) runs.insert(runs.end(), {x.first, x.second});
+    np.max_rows = std::max(np.max_rows, r1 - r0);
+    np.max_adj = std::max(np.max_adj, h[r1] - h[r0]);
+    np.max_pairs = std::max(np.max_pairs, hp[r1] - hp[r0]);
+    np.max_seg = std::max<int>(np.max_seg, (int)((h[r1] - h[r0]) * w));
+    np.max_slots = std::max(np.max_slots, slots);
+    np.max_runs = std::max(np.max_runs, (int)rr.size());
+    r0 = r1;
+  }
+  np.ntiles = (int)tiles.size() / 8;
+  np.tiles.alloc(tiles.size() ? tiles.size() : 8, s);
+  np.runs.alloc(runs.size() ? runs.size() : 2, s);
+  np.widx.alloc(hw.size(), s);
+  np.selfr.alloc(hs.size(), s);
+  if (!tiles.empty())
+    LG_CUDA(cudaMemcpyAsync(np.tiles.get(), tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice, s));
+  if (!runs.empty())
+    LG_CUDA(cudaMemcpyAsync(np.runs.get(), runs.data(), sizeof(int32_t) * runs.size(), cudaMemcpyHostToDevice, s));
+  LG_CUDA(cudaMemcpyAsync(np.widx.get(), hw.data(), sizeof(uint16_t) * hw.size(), cudaMemcpyHostToDevice, s));
+  LG_CUDA(cudaMemcpyAsync(np.selfr.get(), hs.data(), hs.size(), cudaMemcpyHostToDevice, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  return true;
+}
 
 void build_locality(const MapView& key, LocalityPlan& out, cudaStream_t s) {
   const int n = key.n;
@@ -285,7 +508,7 @@ void build_ranks(PairPlan& pp, const int32_t* sorted_rows, const int32_t* sorted
   require(!(herr >> 62), LOAM_ERR(InvalidArgument), "row with more than 256 column nodes");
 }
 
-void build_chunks(PairPlan& pp, const CsrView& csr, int smax, cudaStream_t s) {
+void build_chunks(PairPlan& pp, const CsrView& csr, int smax, int max_rows, cudaStream_t s) {
   const int nr = pp.nrows_node;
   DevBuf<int64_t> starts(nr + 1, s);
   k_node_starts<<<ceil_div(nr + 1, kTPB), kTPB, 0, s>>>(csr.row_ptr, nr, csr.rd, starts.get());
@@ -301,7 +524,7 @@ void build_chunks(PairPlan& pp, const CsrView& csr, int smax, cudaStream_t s) {
   while (r0 < nr) {
     int r1 = r0 + 1;
     require(h[r1] - h[r0] <= smax, LOAM_ERR(InvalidArgument), "row segment exceeds shared memory");
-    while (r1 < nr && r1 - r0 < 32 && h[r1 + 1] - h[r0] <= smax) ++r1;
+    while (r1 < nr && r1 - r0 < max_rows && h[r1 + 1] - h[r0] <= smax) ++r1;
     seg_max = std::max<int>(seg_max, (int)(h[r1] - h[r0]));
     chunks.push_back(r1);
     r0 = r1;

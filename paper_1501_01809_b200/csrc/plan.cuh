@@ -72,8 +72,38 @@ void build_pairs(const int32_t* sorted_rows, int ncells, int nrn, int nrows_node
 // verifies the pattern is blocked by (rd, cd) first.
 void build_ranks(PairPlan& pp, const int32_t* sorted_rows, const int32_t* sorted_cols, int ncn,
                  const CsrView& csr, cudaStream_t s);
-// Warp chunking of row nodes (<= 32 rows, segment <= smax doubles).
-void build_chunks(PairPlan& pp, const CsrView& csr, int smax, cudaStream_t s);
+// Warp chunking of row nodes (<= max_rows nodes, segment <= smax doubles).
+void build_chunks(PairPlan& pp, const CsrView& csr, int smax, int max_rows, cudaStream_t s);
+
+// Neighbour-list plan (P1 forms whose row, column and coordinate maps are the
+// same node map): the node-level pattern N(r) of every row is the list of
+// cell-neighbour nodes, so a pair needs only (local index | in-row ranks of the
+// cell's nodes) -- a 16/32-bit record -- and the kernel gathers each chunk's
+// neighbour coordinates once instead of per pair.
+struct NbrPlan {
+  int nrows_node = 0, nrn = 0, bits = 0, rec_bytes = 4, rd = 1, cd = 1;
+  // plan-owned, 16-byte padded arrays; the tile kernel TMA-loads tile ranges of them
+  DevBuf<int32_t> nptr;  // node-level pattern offsets [nrows_node + 1]
+  DevBuf<int32_t> pptr;  // pair offsets per row [nrows_node + 1]
+  DevBuf<uint8_t> recs;  // npairs records: in-row ranks of the cell's other vertices
+  DevBuf<uint16_t> widx; // per pattern entry: slot of its node in the tile's vertex window
+  DevBuf<uint8_t> selfr; // per row: rank of the row node in its own pattern row
+  DevBuf<int32_t> runs;  // per tile: contiguous vertex runs [lo, hi) (lo, hi even or hi = nv)
+  // CTA tiles of consecutive rows: {R0, R1, A0, A1, P0, P1, run_off, run_cnt}
+  DevBuf<int32_t> tiles;
+  int ntiles = 0;
+  int max_rows = 0, max_adj = 0, max_pairs = 0, max_seg = 0, max_slots = 0, max_runs = 0; // per tile
+  int max_len = 0; // longest node row
+};
+// Build from a (sorted) node-level map and a node-level pattern.  For Mats the
+// pattern is the Mat's sparsity (csr, possibly blocked by rd/cd); for Dats
+// csr.row_ptr == nullptr and the pattern of (map, map) is built here.
+// Returns false when a row is too long for the packed record.
+// Tiles hold <= tile_rows row nodes, <= tile_seg matrix values and a vertex
+// window of <= tile_slots vertices in <= tile_runs contiguous runs.
+bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int nrows_node,
+               const CsrView& csr, int tile_rows, int tile_seg, int tile_slots, int tile_runs,
+               cudaStream_t s);
 
 // build_sparsity (data.hpp:149-179) on the device, bit-exact.
 void build_sparsity_dev(const MapView& rows, const MapView& cols, int rd, int cd,

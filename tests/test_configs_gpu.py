@@ -14,7 +14,7 @@ from paper_1501_01809_b200 import capi, configs
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
-STRATS = ["owner", "atomic", "color"]
+STRATS = ["auto", "owner", "atomic", "color"]
 
 
 def rel(a, b):
@@ -123,13 +123,16 @@ def test_strategies_agree_and_owner_is_deterministic():
     assert rel(c, a) <= TOL
 
 
-def test_inc_accumulates_into_existing_values():
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+@pytest.mark.parametrize("strat", STRATS)
+def test_inc_accumulates_into_existing_values(cfg, strat):
     """execute INC adds to what is there (parloop.hpp:301-305), not only into zeros."""
-    capi.set_strategy("owner")
-    w = configs.Workload(2, 12)
+    capi.set_strategy(strat)
+    w = configs.Workload(cfg, 6 if cfg != 4 else 3)
     w.reset()
     w.run()
-    once = w.outputs[0].host_values()
+    get = (lambda o: o.view()) if cfg == 1 else (lambda o: o.host_values())
+    once = get(w.outputs[0])
     w.run()  # second INC without reset: doubles every entry
-    twice = w.outputs[0].host_values()
+    twice = get(w.outputs[0])
     assert rel(twice, 2 * once) <= TOL
