@@ -432,18 +432,23 @@ struct TileArgs {
 
 __device__ __forceinline__ int skew_of(int lo, int es) { return ((lo * es) & 15) / es; }
 
-constexpr int kTileThreads = 256;
+constexpr int kTileThreads = 256;                 // consumer threads (8 warps)
+constexpr int kTileBlock = kTileThreads + 32;     // + one TMA producer warp
 
 template <class F, class Rec, int LMAX>
-__global__ void __launch_bounds__(kTileThreads, 3) k_tile(const __grid_constant__ TileArgs a) {
+__global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ TileArgs a) {
   constexpr int GD = F::GD, W = F::RD * F::CD;
   constexpr int ES = sizeof(Rec);
   constexpr bool REG = F::BILINEAR && LMAX > 0;
   extern __shared__ __align__(128) unsigned char sm[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);  // [3] stage landed (tx bytes)
+  uint64_t* empty = full + 3;                          // [3] stage released by the 8 consumer warps
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int b = 0; b < 3; ++b) mbar_init(&full[b], 1);
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kTileThreads / 32);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -510,14 +515,18 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_tile(const __grid_constant_
     }
   };
 
-  if (tid == 0) {
-    if (K > 0) issue(0);
-    if (K > 1) issue(1);
+  if (tid >= kTileThreads) { // ---- producer warp: TMA issue only, up to 3 tiles ahead
+    if (tid == kTileThreads)
+      for (int k = 0; k < K; ++k) {
+        if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
+        issue(k);
+      }
+    return;
   }
+  // ---- consumer warps
   double* seg = reinterpret_cast<double*>(sm + a.off_seg);
   const uint32_t mask = (1u << a.bits) - 1;
   for (int k = 0; k < K; ++k) {
-    if (tid == 0 && k + 2 < K) issue(k + 2); // its ring stage was released by the barrier ending tile k-1
     int m[8];
     tile_meta(k, m);
     const int R0 = m[0], nrows = m[1] - m[0], A0 = m[2], nA = m[3] - m[2], P0 = m[4];
@@ -528,7 +537,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_tile(const __grid_constant_
         for (int t = tid; t < len; t += kTileThreads) seg[t] = a.out[E0 + t];
       else
         for (int t = tid; t < len; t += kTileThreads) seg[t] = 0.0;
-      __syncthreads();
+      named_bar(1, kTileThreads);
     }
     mbar_wait(&full[k % 3], (k / 3) & 1);
     const unsigned char* buf = ring(k);
@@ -638,11 +647,13 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_tile(const __grid_constant_
           }
       }
     }
-    __syncthreads(); // tile k consumed: ring stage k%3 may be refilled
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[k % 3]); // this warp is done with stage k%3
     if constexpr (F::BILINEAR && !REG) {
+      named_bar(1, kTileThreads); // segment complete
       const int len = nA * W;
       for (int t = tid; t < len; t += kTileThreads) a.out[E0 + t] = seg[t];
-      __syncthreads();
+      named_bar(1, kTileThreads); // segment drained before the next tile reuses it
     }
   }
 }
@@ -703,10 +714,10 @@ void launch_nbr(const TileArgs& a, int rec_bytes, size_t smem, cudaStream_t s) {
       per_sm = -1;
     }
     int blocks = 1;
-    LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kTileThreads, smem));
+    LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kTileBlock, smem));
     per_sm = blocks > 0 ? blocks : 1;
     const int grid = std::min(a.ntiles, per_sm * kNumSMs);
-    kern<<<grid, kTileThreads, smem, s>>>(a);
+    kern<<<grid, kTileBlock, smem, s>>>(a);
   };
   if constexpr (F::BILINEAR && F::RD == 1 && F::CD == 1) {
     if (a.max_len <= 8) {
@@ -1130,7 +1141,7 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     t.bits = nb.bits;
     t.max_len = nb.max_len;
     auto up16 = [](int x) { return (x + 15) & ~15; };
-    int off = 64; // 3 mbarriers
+    int off = 64; // 6 mbarriers
     t.off_seg = off;
     const bool reg = k.bilinear && k.rd == 1 && k.cd == 1 && nb.max_len <= 8;
     off += up16(k.bilinear && !reg ? nb.max_seg * 8 : 0);
