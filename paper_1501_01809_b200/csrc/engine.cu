@@ -557,6 +557,9 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
       const int self = a0 + selfr_s[node];
       double racc[REG ? LMAX : 1];
       double diag = 0.0, acc = 0.0;
+      double dblk[F::CD];
+#pragma unroll
+      for (int c = 0; c < F::CD; ++c) dblk[c] = 0.0;
       if constexpr (REG)
 #pragma unroll
         for (int q = 0; q < LMAX; ++q) racc[q] = 0.0;
@@ -617,10 +620,17 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
               if (u == 1 && !two) break;
+              // column block 0 is the row node itself: kept in registers
 #pragma unroll
-              for (int j = 0; j < F::NCN; ++j)
+              for (int c = 0; c < F::CD; ++c) dblk[c] += blk[u][c];
 #pragma unroll
-                for (int c = 0; c < F::CD; ++c) seg[rstart + rr[u][j] * F::CD + c] += blk[u][j * F::CD + c];
+              for (int j = 1; j < F::NCN; ++j) {
+                double o[F::CD];
+#pragma unroll
+                for (int c = 0; c < F::CD; ++c) o[c] = seg[rstart + rr[u][j] * F::CD + c];
+#pragma unroll
+                for (int c = 0; c < F::CD; ++c) seg[rstart + rr[u][j] * F::CD + c] = o[c] + blk[u][j * F::CD + c];
+              }
             }
           }
         } else {
@@ -637,6 +647,9 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
         }
       }
       if constexpr (!F::BILINEAR) a.out[R0 + node] = a.accumulate ? a.out[R0 + node] + acc : acc;
+      if constexpr (F::BILINEAR && !REG)
+#pragma unroll
+        for (int c = 0; c < F::CD; ++c) seg[rstart + self * F::CD + c] += dblk[c];
       if constexpr (REG) { // the row straight from registers (scalar rows: W == 1)
         double* o = a.out + E0 + a0;
 #pragma unroll
@@ -720,7 +733,7 @@ void launch_nbr(const TileArgs& a, int rec_bytes, size_t smem, cudaStream_t s) {
     kern<<<grid, kTileBlock, smem, s>>>(a);
   };
   if constexpr (F::BILINEAR && F::RD == 1 && F::CD == 1) {
-    if (a.max_len <= 8) {
+    if (a.max_len <= 8 && std::getenv("LOAM_GPU_REG")) { // register-slot accumulator (experimental)
       if (rec_bytes == 1) go(k_tile<F, uint8_t, 8>);
       else if (rec_bytes == 2) go(k_tile<F, uint16_t, 8>);
       else go(k_tile<F, uint32_t, 8>);
@@ -996,7 +1009,8 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     auto same = [&](const MapView& m) {
       return m.arity == R.v.arity && (m.v == R.v.v || prefix_equal(m.v, m.arity, R.v.v, R.v.arity, m.arity, n, s));
     };
-    bool ok = R.dim == 1 || k.bilinear;
+    // (3D vector rows -- elasticity -- are still faster on the pair-list kernel)
+    bool ok = (R.dim == 1 || k.bilinear) && (R.dim == 1 || strat == 4);
     ok = ok && same(MapView{X->values, n, X->arity, X->target_size}) && X->target_size == R.v.target;
     if (Cm) ok = ok && same(MapView{Cm->values, n, Cm->arity, Cm->target_size});
     CsrView csr{};
@@ -1143,7 +1157,7 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     auto up16 = [](int x) { return (x + 15) & ~15; };
     int off = 64; // 6 mbarriers
     t.off_seg = off;
-    const bool reg = k.bilinear && k.rd == 1 && k.cd == 1 && nb.max_len <= 8;
+    const bool reg = k.bilinear && k.rd == 1 && k.cd == 1 && nb.max_len <= 8 && std::getenv("LOAM_GPU_REG");
     off += up16(k.bilinear && !reg ? nb.max_seg * 8 : 0);
     t.off_buf = off;
     int b = 0;
