@@ -1,0 +1,230 @@
+"""CPU: the oracle (C restatement, oracle/liborc.so) pinned to the reference.
+
+Pins, in order of strength:
+  1. known-answer tests copied (as numbers) from the reference's own tests:
+     test_topology.cpp:55-84, test_data.cpp:22-62, test_fem.cpp:141-161,226-250;
+  2. golden vectors produced by the UNMODIFIED reference (oracle/_ref, see
+     tools/make_golden.py) -- bit-exact for integer outputs, <= 1e-13 for values;
+  3. the reference's property checks (colouring validity by brute force,
+     sparsity vs a dense boolean pattern, oracles.hpp:17-48);
+  4. exact symbolic integration (tests/exact_fem.py) for what the reference
+     lacks: P2 tets, the 14-point rule, elasticity, Stokes -- "parity unpinned"
+     by reference tests, pinned here only against exact integrals.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from tests import exact_fem as EX
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+def rel(a, b):
+    return np.max(np.abs(np.asarray(a) - np.asarray(b))) / max(np.max(np.abs(b)), 1e-300)
+
+
+# ------------------------------------------------------------------ 1. KATs
+def test_colouring_kats():  # test_topology.cpp:55-84
+    c, n = O.color_iteration(2, [np.array([0, 1, 2, 1, 3, 2])], [3], [4])
+    assert list(c) == [0, 1] and n == 2
+    c, n = O.color_iteration(2, [], [], [])
+    assert list(c) == [0, 0] and n == 1
+    c, n = O.color_iteration(4, [np.array([0, 1, 2, 0, 3, 4, 0, 5, 6, 0, 7, 8])], [3], [9])
+    assert list(c) == [0, 1, 2, 3] and n == 4
+
+
+def test_sparsity_kats():  # test_data.cpp:22-62
+    rp, ci = O.build_sparsity(2, [0, 1, 2, 1, 3, 2], 3, 4, [0, 1, 2, 1, 3, 2], 3, 4)
+    assert rp[-1] == 14 and list(np.diff(rp)) == [3, 4, 4, 3]
+    rp, ci = O.build_sparsity(1, [0, 1, 2], 3, 3, [0, 1, 2], 3, 3)
+    assert rp[-1] == 9
+    rp, ci = O.build_sparsity(5, [0, 1, 2, 3, 4], 1, 5, [0, 1, 2, 3, 4], 1, 5)
+    assert rp[-1] == 5 and list(ci) == [0, 1, 2, 3, 4]
+
+
+def test_p2_numbering_kat():  # test_fem.cpp:226-250 on unit_square_mesh(1)
+    cv = np.array([0, 1, 3, 0, 3, 2], dtype=np.int32)  # mesh.hpp:119-124, n=1
+    cn, nn = O.p2_cell_node_map(cv, 4, 2)
+    assert nn == 9
+    edge = {(0, 1): 4, (0, 2): 5, (0, 3): 6, (1, 3): 7, (2, 3): 8}
+    assert list(cn[:6]) == [0, 1, 3, edge[(1, 3)], edge[(0, 3)], edge[(0, 1)]]
+
+
+def test_reference_triangle_kernels_kat():  # test_fem.cpp:141-161
+    X = np.array([0.0, 0.0, 1.0, 0.0, 0.0, 1.0])
+    K = O.element(O.STIFFNESS, 1, 2, X)
+    assert np.allclose(K, [[1.0, -0.5, -0.5], [-0.5, 0.5, 0.0], [-0.5, 0.0, 0.5]], atol=1e-15)
+    M = O.element(O.MASS, 1, 2, X)
+    assert np.allclose(M, (np.ones((3, 3)) + np.eye(3)) / 24.0, atol=1e-15)
+    b = O.element(O.MASS_ACTION, 1, 2, X, np.ones(3))  # source(V, 1.0) == mass action on ones
+    assert np.allclose(b.ravel(), 1.0 / 6, atol=1e-15)
+    H = O.element(O.HELMHOLTZ, 1, 2, X, params=(2.5,))
+    assert np.allclose(H, K + 2.5 * M, atol=1e-15)
+
+
+# ------------------------------------------------------------------ 2. golden vectors of the reference
+def test_golden_colourings_bit_exact():
+    g = gold("c1_n8.npz")
+    c, n = O.color_iteration(g["cv"].size // 3, [g["cv"]], [3], [g["coords"].size // 2])
+    assert np.array_equal(c, g["colors"]) and n == int(g["ncolors"])
+    g = gold("p1tet_n3.npz")
+    c, n = O.color_iteration(g["cv"].size // 4, [g["cv"]], [4], [g["coords"].size // 3])
+    assert np.array_equal(c, g["colors"]) and n == int(g["ncolors"])
+
+
+def test_golden_sparsities_bit_exact():
+    for name, ar, gd in (("c2_n8.npz", 3, 2), ("p1tet_n3.npz", 4, 3)):
+        g = gold(name)
+        nc, nv = g["cv"].size // ar, g["coords"].size // gd
+        rp, ci = O.build_sparsity(nc, g["cv"], ar, nv, g["cv"], ar, nv)
+        assert np.array_equal(rp, g["row_ptr"]) and np.array_equal(ci, g["col_idx"])
+    g = gold("sparsity_dims.npz")
+    rp, ci = O.build_sparsity(20, g["rv"], 3, 9, g["cv"], 2, 7, 2, 3)
+    assert np.array_equal(rp, g["row_ptr"]) and np.array_equal(ci, g["col_idx"])
+
+
+def test_golden_p2_triangle_numbering_bit_exact():
+    g = gold("p2tri_n4.npz")
+    cn, nn = O.p2_cell_node_map(g["cv"], g["coords"].size // 2, 2)
+    assert nn == int(g["nn"]) and np.array_equal(cn, g["cn"])
+
+
+def test_golden_assembled_values():
+    g = gold("c1_n8.npz")
+    nc, nv = g["cv"].size // 3, g["coords"].size // 2
+    b = O.assemble_vector(O.HELMHOLTZ_ACTION, 1, 2, nc, g["cv"], 3, g["cv"], g["coords"], g["cv"], 3, g["u"], nv,
+                          params=(1.0,))
+    assert rel(b, g["residual"]) <= 1e-13
+    g = gold("c2_n8.npz")
+    nc = g["cv"].size // 3
+    v = O.assemble_matrix(O.STIFFNESS, 1, 2, nc, g["cv"], 3, g["cv"], 3, g["cv"], g["coords"], g["row_ptr"], g["col_idx"])
+    assert rel(v, g["values"]) <= 1e-13
+    g = gold("p2tri_n4.npz")
+    nc = g["cv"].size // 3
+    v = O.assemble_matrix(O.HELMHOLTZ, 2, 2, nc, g["cn"], 6, g["cn"], 6, g["cv"], g["coords"], g["row_ptr"],
+                          g["col_idx"], params=(1.5,))
+    assert rel(v, g["values"]) <= 1e-13
+    g = gold("p1tet_n3.npz")
+    nc = g["cv"].size // 4
+    v = O.assemble_matrix(O.MASS, 1, 3, nc, g["cv"], 4, g["cv"], 4, g["cv"], g["coords"], g["row_ptr"], g["col_idx"])
+    assert rel(v, g["values"]) <= 1e-13
+
+
+def test_golden_local_kernels():
+    g = gold("local_kernels.npz")
+    for kind in (O.MASS, O.STIFFNESS, O.HELMHOLTZ, O.MASS_ACTION, O.STIFFNESS_ACTION):
+        for tag, deg, gd, X, C in (("tri_p1", 1, 2, g["X2"], g["C3"]), ("tri_p2", 2, 2, g["X2"], g["C6"]),
+                                   ("tet_p1", 1, 3, g["X3"], np.append(g["C3"], 0.4))):
+            out = O.element(kind, deg, gd, X, C if kind >= O.MASS_ACTION else None, params=(2.5,))
+            assert rel(out.ravel(), g[f"{tag}_{kind}"].ravel()) <= 1e-13, (tag, kind)
+
+
+# ------------------------------------------------------------------ 3. property checks (oracles.hpp)
+@pytest.mark.parametrize("trial", range(12))
+def test_colouring_valid_by_brute_force(trial):  # oracles.hpp:17-32
+    rng = np.random.default_rng(trial)
+    n, nv = int(rng.integers(1, 60)), int(rng.integers(3, 40))
+    t = rng.integers(0, nv, 3 * n).astype(np.int32)
+    c, nc = O.color_iteration(n, [t], [3], [nv])
+    T = t.reshape(n, 3)
+    for a in range(n):
+        for b in range(a + 1, n):
+            if c[a] == c[b]:
+                assert not set(T[a]) & set(T[b])
+    # greedy first-fit: every entity's colour is the smallest not used by earlier conflicting entities
+    for e in range(n):
+        used = {c[f] for f in range(e) if set(T[f]) & set(T[e])}
+        assert c[e] == min(set(range(nc + 1)) - used)
+
+
+@pytest.mark.parametrize("trial", range(8))
+def test_sparsity_matches_dense_pattern(trial):  # oracles.hpp:35-48
+    rng = np.random.default_rng(100 + trial)
+    n, nrt, nct = int(rng.integers(1, 40)), int(rng.integers(2, 12)), int(rng.integers(2, 12))
+    rd, cd = int(rng.integers(1, 3)), int(rng.integers(1, 4))
+    rv = rng.integers(0, nrt, 3 * n).astype(np.int32)
+    cv = rng.integers(0, nct, 2 * n).astype(np.int32)
+    rp, ci = O.build_sparsity(n, rv, 3, nrt, cv, 2, nct, rd, cd)
+    dense = np.zeros((nrt * rd, nct * cd), dtype=bool)
+    for e in range(n):
+        for a in rv[3 * e:3 * e + 3]:
+            for b in cv[2 * e:2 * e + 2]:
+                dense[a * rd:(a + 1) * rd, b * cd:(b + 1) * cd] = True
+    for r in range(nrt * rd):
+        assert list(ci[rp[r]:rp[r + 1]]) == list(np.nonzero(dense[r])[0])
+
+
+# ------------------------------------------------------------------ 4. exact integration (unpinned forms)
+@pytest.mark.parametrize("d,p", [(2, 1), (2, 2), (3, 1), (3, 2)])
+def test_lagrange_kernels_match_exact_integration(d, p):  # test_fem.cpp:163-202 extended to P2 tets
+    rng = np.random.default_rng(2024 + 10 * d + p)
+    for _ in range(5):
+        X = EX.random_simplex(d, rng)
+        M, K = EX.mass(X, d, p), EX.stiffness(X, d, p)
+        assert rel(O.element(O.MASS, p, d, X), M) <= 1e-12
+        assert rel(O.element(O.STIFFNESS, p, d, X), K) <= 1e-12
+        assert rel(O.element(O.HELMHOLTZ, p, d, X, params=(1.7,)), K + 1.7 * M) <= 1e-12
+        c = rng.uniform(-1, 1, M.shape[0])
+        assert rel(O.element(O.MASS_ACTION, p, d, X, c).ravel(), M @ c) <= 1e-12
+        assert rel(O.element(O.STIFFNESS_ACTION, p, d, X, c).ravel(), K @ c) <= 1e-12
+        assert rel(O.element(O.HELMHOLTZ_ACTION, p, d, X, c, params=(1.7,)).ravel(), (K + 1.7 * M) @ c) <= 1e-12
+
+
+def test_vector_forms_match_exact_integration():
+    rng = np.random.default_rng(77)
+    for _ in range(5):
+        X3 = EX.random_simplex(3, rng)
+        assert rel(O.element(O.ELASTICITY, 1, 3, X3, params=(1.0, 0.5)), EX.elasticity(X3, 1.0, 0.5)) <= 1e-12
+        X2 = EX.random_simplex(2, rng)
+        A, B = EX.stokes(X2, 1.0)
+        assert rel(O.element(O.STOKES_A, 2, 2, X2, params=(1.0,)), A) <= 1e-12
+        assert rel(O.element(O.STOKES_B, 2, 2, X2), B) <= 1e-12
+        assert rel(O.element(O.STOKES_BT, 2, 2, X2), B.T) <= 1e-12
+
+
+def test_elasticity_kernel_properties():
+    """Rigid motions are in the kernel; the matrix is symmetric."""
+    rng = np.random.default_rng(5)
+    X = EX.random_simplex(3, rng)
+    K = O.element(O.ELASTICITY, 1, 3, X, params=(1.0, 0.5))
+    assert rel(K, K.T) <= 1e-14
+    pts = X.reshape(4, 3)
+    for t in np.eye(3):  # translations
+        assert np.max(np.abs(K @ np.tile(t, 4))) <= 1e-12 * np.max(np.abs(K))
+    w = np.array([0.3, -0.2, 0.7])  # infinitesimal rotation u = w x x
+    u = np.concatenate([np.cross(w, x) for x in pts])
+    assert np.max(np.abs(K @ u)) <= 1e-11 * np.max(np.abs(K)) * np.max(np.abs(u))
+
+
+# ------------------------------------------------------------------ 5. compiled reference directly (build container only)
+needs_ref = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built (no /root/reference)")
+
+
+@needs_ref
+def test_reference_engine_agrees_with_restatement_on_p2_tets():
+    from paper_1501_01809_b200 import configs
+    m = configs.config_inputs(3, 3)
+    cn, nn = m.extra["p2"], m.extra["nn"]
+    rp, ci, rv = O.ref_engine_matrix(O.HELMHOLTZ, 2, 3, m.ncells, cn, 10, nn, cn, 10, nn, m.cv, m.coords, params=(1.0,))
+    ov = O.assemble_matrix(O.HELMHOLTZ, 2, 3, m.ncells, cn, 10, cn, 10, m.cv, m.coords, rp, ci, params=(1.0,))
+    assert rel(ov, rv) <= 1e-13
+    rb = O.ref_engine_vector(O.HELMHOLTZ_ACTION, 2, 3, m.ncells, cn, 10, nn, m.cv, m.coords, m.extra["u"], params=(1.0,))
+    ob = O.assemble_vector(O.HELMHOLTZ_ACTION, 2, 3, m.ncells, cn, 10, m.cv, m.coords, cn, 10, m.extra["u"], nn,
+                           params=(1.0,))
+    assert rel(ob, rb) <= 1e-13
+
+
+@needs_ref
+def test_reference_threads_bitwise_identical():  # test_parloop.cpp:273-315 on the compiled reference
+    from paper_1501_01809_b200 import configs
+    m = configs.config_inputs(2, 12)
+    a = O.ref_assemble_matrix(O.STIFFNESS, 1, 2, m.cv, m.coords, threads=1)[2]
+    b = O.ref_assemble_matrix(O.STIFFNESS, 1, 2, m.cv, m.coords, threads=4)[2]
+    assert np.array_equal(a, b)
