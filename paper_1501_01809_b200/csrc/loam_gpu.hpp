@@ -1,0 +1,509 @@
+// loam_gpu.hpp -- C++ drop-in facade of the reference operator surface.
+//
+// Mirrors /root/reference/proj/include/loam (C++20 header-only) for the
+// par_loop path, over the C ABI of include/loam_gpu.h:
+//   Set / Map / make_set / make_map                topology.hpp:15-74
+//   Coloring / color_iteration                     topology.hpp:76-125
+//   Access / Dat / Global / Sparsity / Mat         data.hpp:15-234
+//   build_sparsity                                 data.hpp:149-179
+//   Arg / arg() / Parloop / validate / execute     parloop.hpp:17-384
+//   Error / ErrorKind                              common.hpp:10-49
+// Porting code from the reference means replacing `loam::` by `loam_gpu::`
+// and the AST kernel by a registry kernel (kernel.hpp:504-511 -> Kernel{name,
+// params}); every call keeps its arguments, meaning and error kinds.  Objects
+// own DEVICE storage (cudaMalloc); view()/mutable_view() expose a host mirror
+// that is synchronised on demand, so the reference's host-side idioms work.
+#pragma once
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "loam_gpu.h"
+
+namespace loam_gpu {
+
+using Real = double;
+
+enum class ErrorKind {
+  IndexOutOfRange, ArityMismatch, SourceMismatch, AsymmetricAdjacency, IllegalAccess,
+  MapSourceMismatch, ShapeMismatch, UnboundIdentifier, NonDividingFactor, OutsideSparsity,
+  EmptyPartials, DimensionMismatch, InvalidSubdivision, ParseError, NonManifold, CellMismatch,
+  UnsupportedForm, MissingDiagonal, SpaceMismatch, IndefiniteBreakdown, InstabilityDetected,
+  InvalidArgument,
+  CudaError = 99, NoDevice = 100
+};
+
+class Error : public std::runtime_error {
+public:
+  Error(ErrorKind kind, const std::string& what) : std::runtime_error(what), kind_(kind) {}
+  ErrorKind kind() const { return kind_; }
+
+private:
+  ErrorKind kind_;
+};
+
+inline void check(int code) {
+  if (code == 0) return;
+  const ErrorKind k = code == LOAM_GPU_ERR_CUDA ? ErrorKind::CudaError
+                      : code == LOAM_GPU_ERR_NO_DEVICE ? ErrorKind::NoDevice
+                                                       : static_cast<ErrorKind>(code - 1);
+  throw Error(k, loam_gpu_last_error());
+}
+inline void require(bool c, ErrorKind k, const std::string& m) {
+  if (!c) throw Error(k, m);
+}
+
+namespace detail {
+inline uint64_t next_id() {
+  static std::atomic<uint64_t> id{1};
+  return id++;
+}
+template <class T>
+struct DeviceArray { // owned device buffer + lazily synchronised host mirror
+  T* dev = nullptr;
+  size_t n = 0;
+  mutable std::vector<T> host;
+  mutable bool host_valid = false, dev_stale = false;
+  explicit DeviceArray(size_t count, bool zero = true) : n(count) {
+    check(loam_gpu_malloc(reinterpret_cast<void**>(&dev), sizeof(T) * (n ? n : 1)));
+    if (zero) check(loam_gpu_memset(dev, 0, sizeof(T) * (n ? n : 1), nullptr));
+  }
+  ~DeviceArray() { loam_gpu_free(dev); }
+  DeviceArray(const DeviceArray&) = delete;
+  DeviceArray& operator=(const DeviceArray&) = delete;
+  void upload(const T* src) {
+    check(loam_gpu_memcpy(dev, src, sizeof(T) * n, nullptr));
+    check(loam_gpu_stream_sync(nullptr));
+    host_valid = false;
+  }
+  const std::vector<T>& download() const {
+    if (!host_valid) {
+      host.resize(n);
+      check(loam_gpu_memcpy(host.data(), dev, sizeof(T) * n, nullptr));
+      check(loam_gpu_stream_sync(nullptr));
+      host_valid = true;
+    }
+    return host;
+  }
+  T* device() { // push host edits (mutable_view) before device use
+    if (dev_stale) {
+      check(loam_gpu_memcpy(dev, host.data(), sizeof(T) * n, nullptr));
+      dev_stale = false;
+    }
+    return dev;
+  }
+};
+} // namespace detail
+
+// ---------------------------------------------------------------- topology
+class Set { // topology.hpp:15-26
+public:
+  explicit Set(int size, std::string name = "set") : size_(size), name_(std::move(name)) {
+    require(size >= 0, ErrorKind::InvalidArgument, "Set size must be non-negative");
+  }
+  int size() const { return size_; }
+  const std::string& name() const { return name_; }
+  uint64_t id() const { return id_; }
+
+private:
+  int size_;
+  std::string name_;
+  uint64_t id_ = detail::next_id();
+};
+using SetPtr = std::shared_ptr<const Set>;
+inline SetPtr make_set(int size, std::string name = "set") { return std::make_shared<const Set>(size, std::move(name)); }
+
+class Map { // topology.hpp:36-66 (validated on construction, on the device)
+public:
+  Map(SetPtr source, SetPtr target, int arity, std::vector<int> values, std::string name = "map")
+      : source_(std::move(source)), target_(std::move(target)), arity_(arity), values_(std::move(values)),
+        name_(std::move(name)), dev_(values_.size()) {
+    require(arity_ > 0, ErrorKind::InvalidArgument, "Map arity must be positive");
+    require((long)values_.size() == (long)source_->size() * arity_, ErrorKind::ArityMismatch,
+            name_ + ": value table length != source size * arity");
+    dev_.upload(values_.data());
+    loam_map_desc d = desc();
+    if (!values_.empty()) check(loam_gpu_map_check(&d, nullptr));
+  }
+  const SetPtr& source() const { return source_; }
+  const SetPtr& target() const { return target_; }
+  int arity() const { return arity_; }
+  const std::string& name() const { return name_; }
+  const int* row(int e) const { return values_.data() + static_cast<long>(e) * arity_; }
+  const std::vector<int>& values() const { return values_; }
+  loam_map_desc desc() const {
+    loam_map_desc d{};
+    d.values = dev_.dev;
+    d.source_size = source_->size();
+    d.target_size = target_->size();
+    d.arity = arity_;
+    d.source_id = source_->id();
+    d.target_id = target_->id();
+    d.id = id_;
+    return d;
+  }
+
+private:
+  SetPtr source_, target_;
+  int arity_;
+  std::vector<int> values_;
+  std::string name_;
+  detail::DeviceArray<int32_t> dev_;
+  uint64_t id_ = detail::next_id();
+};
+using MapPtr = std::shared_ptr<const Map>;
+inline MapPtr make_map(SetPtr source, SetPtr target, int arity, std::vector<int> values, std::string name = "map") {
+  return std::make_shared<const Map>(std::move(source), std::move(target), arity, std::move(values), std::move(name));
+}
+
+struct Coloring { // topology.hpp:78-81
+  std::vector<int> colors;
+  int num_colors = 0;
+};
+inline Coloring color_iteration(const SetPtr& iter, const std::vector<MapPtr>& conflict_maps) {
+  std::vector<loam_map_desc> d;
+  for (const auto& m : conflict_maps) {
+    require(m->source() == iter, ErrorKind::SourceMismatch,
+            "conflict map " + m->name() + " source differs from iteration set");
+    d.push_back(m->desc());
+  }
+  detail::DeviceArray<int32_t> colors(iter->size(), false);
+  int32_t nc = 0;
+  check(loam_gpu_color_iteration(iter->size(), iter->id(), d.data(), (int)d.size(), colors.dev, &nc, nullptr));
+  Coloring c;
+  const auto& h = colors.download();
+  c.colors.assign(h.begin(), h.end());
+  c.num_colors = nc;
+  return c;
+}
+
+// ---------------------------------------------------------------- data
+enum class Access { READ, WRITE, RW, INC, SUM, MIN, MAX }; // data.hpp:17
+
+class Dat { // data.hpp:35-60
+public:
+  Dat(SetPtr set, int dim, std::string name = "dat")
+      : set_(std::move(set)), dim_(dim), name_(std::move(name)), data_((size_t)set_->size() * dim) {
+    require(dim > 0, ErrorKind::InvalidArgument, "Dat dim must be positive");
+  }
+  const SetPtr& set() const { return set_; }
+  int dim() const { return dim_; }
+  const std::string& name() const { return name_; }
+  std::uint64_t version() const { return version_; }
+  std::span<const Real> view() const {
+    const auto& h = data_.download();
+    return {h.data(), h.size()};
+  }
+  std::span<Real> mutable_view() { // host edits are pushed before the next device use
+    ++version_;
+    data_.download();
+    data_.dev_stale = true;
+    zero_ = false;
+    return {data_.host.data(), data_.host.size()};
+  }
+  // device access for execute
+  double* device_data() { return data_.device(); }
+  void touched_by_device() {
+    ++version_;
+    data_.host_valid = false;
+    zero_ = false;
+  }
+  bool known_zero() const { return zero_; }
+  uint64_t id() const { return id_; }
+
+private:
+  SetPtr set_;
+  int dim_;
+  std::string name_;
+  detail::DeviceArray<double> data_;
+  std::uint64_t version_ = 0;
+  bool zero_ = true;
+  uint64_t id_ = detail::next_id();
+};
+using DatPtr = std::shared_ptr<Dat>;
+inline DatPtr make_dat(SetPtr set, int dim, std::string name = "dat") {
+  return std::make_shared<Dat>(std::move(set), dim, std::move(name));
+}
+
+class Global { // data.hpp:69-87
+public:
+  explicit Global(int dim, std::string name = "global") : dim_(dim), name_(std::move(name)), data_(dim) {
+    require(dim > 0, ErrorKind::InvalidArgument, "Global dim must be positive");
+  }
+  int dim() const { return dim_; }
+  std::span<const Real> view() const {
+    const auto& h = data_.download();
+    return {h.data(), h.size()};
+  }
+  std::span<Real> mutable_view() {
+    data_.download();
+    data_.dev_stale = true;
+    return {data_.host.data(), data_.host.size()};
+  }
+  double* device_data() { return data_.device(); }
+  void touched_by_device() { data_.host_valid = false; }
+  uint64_t id() const { return id_; }
+
+private:
+  int dim_;
+  std::string name_;
+  detail::DeviceArray<double> data_;
+  uint64_t id_ = detail::next_id();
+};
+using GlobalPtr = std::shared_ptr<Global>;
+inline GlobalPtr make_global(int dim, std::string name = "global") { return std::make_shared<Global>(dim, std::move(name)); }
+
+class Sparsity { // data.hpp:116-142 (device CSR)
+public:
+  Sparsity(int nrows, int ncols, int64_t* row_ptr, int32_t* col_idx, int64_t nnz, int rd, int cd)
+      : nrows_(nrows), ncols_(ncols), rp_(row_ptr), ci_(col_idx), nnz_(nnz), rd_(rd), cd_(cd) {}
+  ~Sparsity() {
+    loam_gpu_free(rp_);
+    loam_gpu_free(ci_);
+  }
+  Sparsity(const Sparsity&) = delete;
+  Sparsity& operator=(const Sparsity&) = delete;
+  int nrows() const { return nrows_; }
+  int ncols() const { return ncols_; }
+  long nnz() const { return (long)nnz_; }
+  const std::vector<long>& row_offsets() const {
+    sync();
+    return hrp_;
+  }
+  const std::vector<int>& col_indices() const {
+    sync();
+    return hci_;
+  }
+  long find(int row, int col) const { // data.hpp:129-136
+    if (row < 0 || row >= nrows_) return -1;
+    sync();
+    auto first = hci_.begin() + hrp_[row], last = hci_.begin() + hrp_[row + 1];
+    auto it = std::lower_bound(first, last, col);
+    return (it == last || *it != col) ? -1 : it - hci_.begin();
+  }
+  loam_sparsity_desc desc() const {
+    return loam_sparsity_desc{rp_, ci_, nrows_, ncols_, nnz_, rd_, cd_, id_};
+  }
+
+private:
+  void sync() const {
+    if (synced_) return;
+    std::vector<int64_t> r(nrows_ + 1);
+    hci_.resize(nnz_);
+    check(loam_gpu_memcpy(r.data(), rp_, sizeof(int64_t) * r.size(), nullptr));
+    if (nnz_) check(loam_gpu_memcpy(hci_.data(), ci_, sizeof(int32_t) * nnz_, nullptr));
+    check(loam_gpu_stream_sync(nullptr));
+    hrp_.assign(r.begin(), r.end());
+    synced_ = true;
+  }
+  int nrows_, ncols_;
+  int64_t* rp_;
+  int32_t* ci_;
+  int64_t nnz_;
+  int rd_, cd_;
+  uint64_t id_ = detail::next_id();
+  mutable bool synced_ = false;
+  mutable std::vector<long> hrp_;
+  mutable std::vector<int> hci_;
+};
+using SparsityPtr = std::shared_ptr<const Sparsity>;
+
+// data.hpp:149-179, built on the device (bit-exact).
+inline SparsityPtr build_sparsity(const MapPtr& row_map, const MapPtr& col_map, int row_dim = 1, int col_dim = 1) {
+  require(row_map->source() == col_map->source(), ErrorKind::SourceMismatch,
+          "row and column maps must share their source set");
+  loam_map_desc r = row_map->desc(), c = col_map->desc();
+  int64_t* rp = nullptr;
+  int32_t* ci = nullptr;
+  int64_t nnz = 0;
+  check(loam_gpu_build_sparsity(&r, &c, row_dim, col_dim, &rp, &ci, &nnz, nullptr));
+  return std::make_shared<const Sparsity>(row_map->target()->size() * row_dim, col_map->target()->size() * col_dim, rp,
+                                          ci, nnz, row_dim, col_dim);
+}
+
+class Mat { // data.hpp:183-228
+public:
+  explicit Mat(SparsityPtr sparsity, std::string name = "mat")
+      : sparsity_(std::move(sparsity)), name_(std::move(name)), values_(sparsity_->nnz(), false) {}
+  const SparsityPtr& sparsity() const { return sparsity_; }
+  int nrows() const { return sparsity_->nrows(); }
+  int ncols() const { return sparsity_->ncols(); }
+  const std::vector<Real>& values() const {
+    materialize();
+    return values_.download();
+  }
+  Real at(int row, int col) const {
+    const long pos = sparsity_->find(row, col);
+    return pos < 0 ? 0.0 : values()[pos];
+  }
+  void zero() { zero_ = stale_ = true; } // lazily: the next INC treats the values as zeros
+  double* device_data() {
+    materialize();
+    return values_.device();
+  }
+  double* device_data_for_zero_inc() { return values_.dev; } // contents ignored (LOAM_ARG_ZERO)
+  void touched_by_device() {
+    values_.host_valid = false;
+    zero_ = stale_ = false;
+  }
+  bool known_zero() const { return zero_; }
+  uint64_t id() const { return id_; }
+
+private:
+  void materialize() const {
+    if (stale_) {
+      check(loam_gpu_memset(values_.dev, 0, sizeof(double) * (values_.n ? values_.n : 1), nullptr));
+      values_.host_valid = false;
+      stale_ = false;
+    }
+  }
+  SparsityPtr sparsity_;
+  std::string name_;
+  mutable detail::DeviceArray<double> values_;
+  bool zero_ = true;
+  mutable bool stale_ = true; // make_mat: zero-filled on first materialisation
+  uint64_t id_ = detail::next_id();
+};
+using MatPtr = std::shared_ptr<Mat>;
+inline MatPtr make_mat(SparsityPtr sparsity, std::string name = "mat") {
+  return std::make_shared<Mat>(std::move(sparsity), std::move(name));
+}
+
+// ---------------------------------------------------------------- par_loop
+struct Kernel { // ir::Kernel (kernel.hpp:504-511) -> registry key + baked literals
+  std::string name;
+  std::vector<double> params;
+};
+using KernelPtr = std::shared_ptr<const Kernel>;
+inline KernelPtr kernel(std::string name, std::vector<double> params = {}) {
+  return std::make_shared<const Kernel>(Kernel{std::move(name), std::move(params)});
+}
+
+struct Arg { // parloop.hpp:17-28
+  DatPtr dat;
+  MatPtr mat;
+  GlobalPtr global;
+  Access access = Access::READ;
+  std::vector<MapPtr> maps;
+};
+inline Arg arg(DatPtr dat, Access access, MapPtr map = nullptr) {
+  Arg a;
+  a.dat = std::move(dat);
+  a.access = access;
+  if (map) a.maps.push_back(std::move(map));
+  return a;
+}
+inline Arg arg(MatPtr mat, Access access, MapPtr row_map, MapPtr col_map) {
+  Arg a;
+  a.mat = std::move(mat);
+  a.access = access;
+  a.maps = {std::move(row_map), std::move(col_map)};
+  return a;
+}
+inline Arg arg(GlobalPtr global, Access access) {
+  Arg a;
+  a.global = std::move(global);
+  a.access = access;
+  return a;
+}
+
+struct Parloop { // parloop.hpp:55-59
+  KernelPtr kernel;
+  SetPtr iterset;
+  std::vector<Arg> args;
+};
+
+namespace detail {
+struct Descs {
+  std::vector<loam_arg_desc> args;
+  std::vector<loam_map_desc> maps;
+  std::vector<loam_sparsity_desc> sps;
+  loam_kernel_desc kd{};
+};
+inline void build(const Parloop& loop, Descs& D, bool for_execute) {
+  require(loop.kernel != nullptr, ErrorKind::InvalidArgument, "parloop without kernel");
+  require(loop.iterset != nullptr, ErrorKind::InvalidArgument, "parloop without iteration set");
+  const size_t n = loop.args.size();
+  D.args.assign(n, loam_arg_desc{});
+  D.maps.assign(2 * n, loam_map_desc{});
+  D.sps.assign(n, loam_sparsity_desc{});
+  for (size_t k = 0; k < n; ++k) {
+    const Arg& a = loop.args[k];
+    loam_arg_desc& d = D.args[k];
+    d.access = static_cast<int32_t>(a.access);
+    const int kinds = int(a.dat != nullptr) + int(a.mat != nullptr) + int(a.global != nullptr);
+    require(kinds == 1, ErrorKind::InvalidArgument, "argument must target exactly one object");
+    if (a.dat) {
+      d.kind = LOAM_ARG_DAT;
+      d.dim = a.dat->dim();
+      d.set_size = a.dat->set()->size();
+      d.set_id = a.dat->set()->id();
+      d.obj_id = a.dat->id();
+      require(a.maps.size() <= 1, ErrorKind::InvalidArgument, "Dat argument with several maps");
+      if (for_execute) {
+        d.data = a.dat->device_data();
+        if (a.access == Access::INC && a.dat->known_zero()) d.flags = LOAM_ARG_ZERO;
+      }
+      if (!a.maps.empty()) {
+        D.maps[2 * k] = a.maps[0]->desc();
+        d.map = &D.maps[2 * k];
+      }
+    } else if (a.mat) {
+      d.kind = LOAM_ARG_MAT;
+      d.obj_id = a.mat->id();
+      require(a.maps.size() == 2, ErrorKind::InvalidArgument, "Mat argument requires row and column maps");
+      if (for_execute) {
+        if (a.mat->known_zero()) {
+          d.flags = LOAM_ARG_ZERO;
+          d.data = a.mat->device_data_for_zero_inc();
+        } else {
+          d.data = a.mat->device_data();
+        }
+      }
+      D.maps[2 * k] = a.maps[0]->desc();
+      D.maps[2 * k + 1] = a.maps[1]->desc();
+      D.sps[k] = a.mat->sparsity()->desc();
+      d.map = &D.maps[2 * k];
+      d.col_map = &D.maps[2 * k + 1];
+      d.sparsity = &D.sps[k];
+    } else {
+      d.kind = LOAM_ARG_GLOBAL;
+      d.dim = a.global->dim();
+      d.obj_id = a.global->id();
+      if (for_execute) d.data = a.global->device_data();
+    }
+  }
+  D.kd = loam_kernel_desc{loop.kernel->name.c_str(), loop.kernel->params.data(),
+                          (int32_t)loop.kernel->params.size()};
+}
+} // namespace detail
+
+// parloop.hpp:89-146
+inline void validate(const Parloop& loop) {
+  detail::Descs D;
+  detail::build(loop, D, false);
+  check(loam_gpu_validate(&D.kd, loop.iterset->size(), loop.iterset->id(), D.args.data(), (int)D.args.size()));
+}
+
+// parloop.hpp:191.  `threads` is accepted for drop-in compatibility; results are
+// visible on return, as in the reference (the call synchronises the stream).
+inline void execute(const Parloop& loop, int threads = 1) {
+  require(threads >= 1, ErrorKind::InvalidArgument, "thread count must be positive");
+  detail::Descs D;
+  detail::build(loop, D, true);
+  check(loam_gpu_execute(&D.kd, loop.iterset->size(), loop.iterset->id(), D.args.data(), (int)D.args.size(), nullptr));
+  check(loam_gpu_stream_sync(nullptr));
+  for (const Arg& a : loop.args) {
+    if (a.access == Access::READ) continue;
+    if (a.dat) a.dat->touched_by_device();
+    if (a.mat) a.mat->touched_by_device();
+    if (a.global) a.global->touched_by_device();
+  }
+}
+
+} // namespace loam_gpu
