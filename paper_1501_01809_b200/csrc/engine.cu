@@ -526,7 +526,9 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
   // ---- consumer warps
   double* seg = reinterpret_cast<double*>(sm + a.off_seg);
   const uint32_t mask = (1u << a.bits) - 1;
+  long long t_wait = 0, t_comp = 0;
   for (int k = 0; k < K; ++k) {
+    const long long c0 = a.timing ? clock64() : 0;
     int m[8];
     tile_meta(k, m);
     const int R0 = m[0], nrows = m[1] - m[0], A0 = m[2], nA = m[3] - m[2], P0 = m[4];
@@ -540,6 +542,7 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
       named_bar(1, kTileThreads);
     }
     mbar_wait(&full[k % 3], (k / 3) & 1);
+    const long long c1 = a.timing ? clock64() : 0;
     const unsigned char* buf = ring(k);
     const int32_t* nptr_s = reinterpret_cast<const int32_t*>(buf + a.b_nptr) + skew_of(R0, 4);
     const int32_t* pptr_s = reinterpret_cast<const int32_t*>(buf + a.b_pptr) + skew_of(R0, 4);
@@ -661,6 +664,10 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
       }
     }
     __syncwarp();
+    if (a.timing) {
+      t_wait += c1 - c0;
+      t_comp += clock64() - c1;
+    }
     if ((tid & 31) == 0) mbar_arrive(&empty[k % 3]); // this warp is done with stage k%3
     if constexpr (F::BILINEAR && !REG) {
       named_bar(1, kTileThreads); // segment complete
@@ -668,6 +675,210 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
       for (int t = tid; t < len; t += kTileThreads) a.out[E0 + t] = seg[t];
       named_bar(1, kTileThreads); // segment drained before the next tile reuses it
     }
+  }
+  if (a.timing && (tid & 31) == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.timing), (unsigned long long)t_wait);
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.timing) + 1, (unsigned long long)t_comp);
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.timing) + 2, (unsigned long long)K);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Ring kernel (NbrPlan ring mode: P1 triangles on a manifold mesh).  Same
+// producer/consumer TMA pipeline as k_tile, but each row's cells arrive in
+// ring / fan order as one 16-bit record per chain vertex (window slot << 3 |
+// in-row rank): a cell is (row vertex, previous chain vertex, new vertex), so
+// one vertex is fetched per cell, and every off-diagonal entry is complete
+// after two consecutive cells -- written once with a plain store.
+struct RingArgs {
+  const int32_t* tiles;
+  int ntiles;
+  const int32_t* nptr;
+  const int32_t* rptr;
+  const uint16_t* recs;
+  const uint32_t* rowinfo;
+  const int32_t* runs;
+  const double* coords;
+  const double* coeff;
+  FormParams prm;
+  double* out;
+  int accumulate;
+  int off_seg, off_buf, buf_bytes;
+  int b_nptr, b_rptr, b_recs, b_info, b_win, b_winc;
+};
+
+template <class F>
+__global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ RingArgs a) {
+  static_assert(F::GD == 2 && F::NRN == 3, "ring kernel: P1 triangles");
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + 3;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kTileThreads / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int K = a.ntiles > (int)blockIdx.x ? (a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto tile_meta = [&](int k, int (&m)[8]) {
+    const int4* t = reinterpret_cast<const int4*>(a.tiles + 8 * (blockIdx.x + k * gridDim.x));
+    const int4 x = __ldg(t), y = __ldg(t + 1);
+    m[0] = x.x; m[1] = x.y; m[2] = x.z; m[3] = x.w; m[4] = y.x; m[5] = y.y; m[6] = y.z; m[7] = y.w;
+  };
+  auto ring = [&](int k) { return sm + a.off_buf + (k % 3) * a.buf_bytes; };
+  if (tid >= kTileThreads) { // ---- producer warp
+    if (tid == kTileThreads)
+      for (int k = 0; k < K; ++k) {
+        if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
+        int m[8];
+        tile_meta(k, m);
+        unsigned char* buf = ring(k);
+        uint64_t* bar = &full[k % 3];
+        auto rb = [](int lo, int hi, int es, int64_t& s0) {
+          s0 = ((int64_t)lo * es) & ~int64_t(15);
+          return (uint32_t)((((int64_t)hi * es + 15) & ~int64_t(15)) - s0);
+        };
+        int64_t g0, g1, g2, g3;
+        const uint32_t n0 = F::BILINEAR ? rb(m[0], m[1] + 1, 4, g0) : (g0 = 0, 0u);
+        const uint32_t n1 = rb(m[0], m[1] + 1, 4, g1), n2 = rb(m[4], m[5], 2, g2), n3 = rb(m[0], m[1], 4, g3);
+        uint32_t tx = n0 + n1 + n2 + n3;
+        double* win = reinterpret_cast<double*>(buf + a.b_win);
+        double* winc = reinterpret_cast<double*>(buf + a.b_winc);
+        int slot = 0;
+        for (int r = 0; r < m[7]; ++r) {
+          const int lo = __ldg(a.runs + 2 * (m[6] + r)), hi = __ldg(a.runs + 2 * (m[6] + r) + 1);
+          tx += (uint32_t)(hi - lo) * 16;
+          if constexpr (F::HAS_COEFF) {
+            const uint32_t nc = (uint32_t)(hi - lo) * 8;
+            tx += nc & ~15u;
+            if (nc & 15) winc[slot + hi - lo - 1] = a.coeff[hi - 1];
+          }
+          slot += hi - lo;
+        }
+        fence_async_shared();
+        mbar_arrive_expect_tx(bar, tx);
+        if (n0) bulk_g2s(buf + a.b_nptr, reinterpret_cast<const unsigned char*>(a.nptr) + g0, n0, bar);
+        bulk_g2s(buf + a.b_rptr, reinterpret_cast<const unsigned char*>(a.rptr) + g1, n1, bar);
+        if (n2) bulk_g2s(buf + a.b_recs, reinterpret_cast<const unsigned char*>(a.recs) + g2, n2, bar);
+        if (n3) bulk_g2s(buf + a.b_info, reinterpret_cast<const unsigned char*>(a.rowinfo) + g3, n3, bar);
+        slot = 0;
+        for (int r = 0; r < m[7]; ++r) {
+          const int lo = __ldg(a.runs + 2 * (m[6] + r)), hi = __ldg(a.runs + 2 * (m[6] + r) + 1);
+          bulk_g2s(win + 2 * slot, a.coords + 2 * (int64_t)lo, (uint32_t)(hi - lo) * 16, bar);
+          if constexpr (F::HAS_COEFF) {
+            const uint32_t nc = ((uint32_t)(hi - lo) * 8) & ~15u;
+            if (nc) bulk_g2s(winc + slot, a.coeff + lo, nc, bar);
+          }
+          slot += hi - lo;
+        }
+      }
+    return;
+  }
+  // ---- consumers: one thread per row vertex
+  double* seg = reinterpret_cast<double*>(sm + a.off_seg);
+  for (int k = 0; k < K; ++k) {
+    int m[8];
+    tile_meta(k, m);
+    const int R0 = m[0], nrows = m[1] - m[0], A0 = m[2], nA = m[3] - m[2], P0 = m[4];
+    if constexpr (F::BILINEAR) {
+      if (a.accumulate) {
+        for (int t = tid; t < nA; t += kTileThreads) seg[t] = a.out[(int64_t)A0 + t];
+        named_bar(1, kTileThreads);
+      }
+    }
+    mbar_wait(&full[k % 3], (k / 3) & 1);
+    const unsigned char* buf = ring(k);
+    const int32_t* nptr_s = reinterpret_cast<const int32_t*>(buf + a.b_nptr) + skew_of(R0, 4);
+    const int32_t* rptr_s = reinterpret_cast<const int32_t*>(buf + a.b_rptr) + skew_of(R0, 4);
+    const uint16_t* rec_s = reinterpret_cast<const uint16_t*>(buf + a.b_recs) + skew_of(P0, 2);
+    const uint32_t* info_s = reinterpret_cast<const uint32_t*>(buf + a.b_info) + skew_of(R0, 4);
+    const double2* win = reinterpret_cast<const double2*>(buf + a.b_win);
+    const double* winc = reinterpret_cast<const double*>(buf + a.b_winc);
+    if (tid < nrows) {
+      const uint32_t info = info_s[tid];
+      const int self_slot = info & 0xffff, self_rank = (info >> 16) & 0xff;
+      const int a0 = F::BILINEAR ? nptr_s[tid] - A0 : 0;
+      const int q0 = rptr_s[tid] - P0, q1 = rptr_s[tid + 1] - P0;
+      const double2 xs = win[self_slot];
+      const double cs = F::HAS_COEFF ? winc[self_slot] : 0.0;
+      const uint32_t h = rec_s[q0];
+      const int rk0 = h & 7;
+      double2 xp = win[h >> 3];
+      double cp = F::HAS_COEFF ? winc[h >> 3] : 0.0;
+      int rkp = rk0;
+      double diag = 0.0, first = 0.0, carry = 0.0, acc = 0.0;
+      auto put = [&](int rank, double v) {
+        if (a.accumulate) seg[a0 + rank] += v;
+        else seg[a0 + rank] = v;
+      };
+#pragma unroll 2
+      for (int q = q0 + 1; q < q1; ++q) {
+        const uint32_t r = rec_s[q];
+        const double2 xn = win[r >> 3];
+        const double cn = F::HAS_COEFF ? winc[r >> 3] : 0.0;
+        const double X[3][2] = {{xs.x, xs.y}, {xp.x, xp.y}, {xn.x, xn.y}};
+        Geom<2> G;
+        geometry<2>(X, G);
+        if constexpr (F::BILINEAR) {
+          double blk[3];
+          F::row(0, G, nullptr, a.prm, blk);
+          diag += blk[0];
+          if (q == q0 + 1) first = blk[1];
+          else put(rkp, carry + blk[1]);
+          carry = blk[2];
+        } else {
+          const double C[3] = {cs, cp, cn};
+          double v;
+          F::row(0, G, C, a.prm, &v);
+          acc += v;
+        }
+        xp = xn;
+        cp = cn;
+        rkp = r & 7;
+      }
+      if constexpr (F::BILINEAR) {
+        if (q1 - q0 > 1) {
+          if (rkp == rk0) put(rk0, first + carry); // closed ring
+          else {
+            put(rk0, first);
+            put(rkp, carry);
+          }
+        }
+        put(self_rank, diag);
+      } else {
+        a.out[R0 + tid] = a.accumulate ? a.out[R0 + tid] + acc : acc;
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[k % 3]);
+    if constexpr (F::BILINEAR) {
+      named_bar(1, kTileThreads); // segment complete
+      for (int t = tid; t < nA; t += kTileThreads) a.out[(int64_t)A0 + t] = seg[t];
+      named_bar(1, kTileThreads);
+    }
+  }
+}
+
+template <class F>
+void launch_ring(const RingArgs& a, size_t smem, cudaStream_t s) {
+  if constexpr (F::GD == 2 && F::NRN == 3 && F::RD == 1 && F::CD == 1) {
+    if (a.ntiles == 0) return;
+    static size_t attr = 0;
+    if (attr < smem) {
+      LG_CUDA(cudaFuncSetAttribute(k_ring<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    int blocks = 1;
+    LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_ring<F>, kTileBlock, smem));
+    const int grid = std::min(a.ntiles, std::max(blocks, 1) * kNumSMs);
+    k_ring<F><<<grid, kTileBlock, smem, s>>>(a);
+    count_launch();
+    LG_LAUNCH_CHECK();
+  } else {
+    fail(LOAM_ERR(InvalidArgument), "ring kernel needs a scalar P1 triangle form");
   }
 }
 
@@ -678,6 +889,7 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
 using GenericFn = void (*)(const GLaunch&, cudaStream_t);
 using OwnerFn = void (*)(const OwnerArgs&, int grid, size_t smem, cudaStream_t);
 using NbrFn = void (*)(const TileArgs&, int rec_bytes, size_t smem, cudaStream_t);
+using RingFn = void (*)(const RingArgs&, size_t smem, cudaStream_t);
 
 struct Entry {
   KernelInfo info;
@@ -687,7 +899,8 @@ struct Entry {
   int form = -1, gd = 0, nrn = 0, ncn = 0, rd = 1, cd = 1, ncoeff = 0;
   bool bilinear = false, has_coeff = false;
   OwnerFn owner = nullptr;
-  NbrFn nbr = nullptr; // P1 forms only
+  NbrFn nbr = nullptr;   // P1 forms only
+  RingFn ring = nullptr; // scalar P1 triangle forms only
 };
 
 template <class K>
@@ -783,6 +996,7 @@ Entry form_entry(const std::string& name) {
   e.has_coeff = F::HAS_COEFF;
   e.owner = &launch_owner<F>;
   if constexpr (P == 1 && F::NRN == D + 1 && (!F::BILINEAR || F::NCN == F::NRN)) e.nbr = &launch_nbr<F>;
+  if constexpr (P == 1 && D == 2 && F::RD == 1 && F::CD == 1) e.ring = &launch_ring<F>;
   return e;
 }
 
@@ -1136,6 +1350,44 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
       g_fast_cache[key] = P;
     }
   }
+  if (P->use_nbr && P->nb.ring && k.ring && !std::getenv("LOAM_GPU_NO_RING")) {
+    const NbrPlan& nb = P->nb;
+    RingArgs t{};
+    t.tiles = nb.rtiles.get();
+    t.ntiles = nb.ntiles;
+    t.nptr = nb.nptr.get();
+    t.rptr = nb.rptr.get();
+    t.recs = nb.rrecs.get();
+    t.rowinfo = nb.rowinfo.get();
+    t.runs = nb.runs.get();
+    t.coords = args[1].data;
+    t.coeff = k.has_coeff ? args[2].data : nullptr;
+    t.prm = prm;
+    t.out = args[0].data;
+    t.accumulate = (args[0].flags & LOAM_ARG_ZERO) ? 0 : 1;
+    auto up16 = [](int x) { return (x + 15) & ~15; };
+    int off = 64;
+    t.off_seg = off;
+    off += up16(k.bilinear ? nb.max_seg * 8 : 0);
+    t.off_buf = off;
+    int b = 0;
+    t.b_nptr = b;
+    b += up16((nb.max_rows + 1) * 4 + 32);
+    t.b_rptr = b;
+    b += up16((nb.max_rows + 1) * 4 + 32);
+    t.b_recs = b;
+    b += up16(nb.max_pairs * 2 + 32);
+    t.b_info = b;
+    b += up16(nb.max_rows * 4 + 32);
+    t.b_win = b;
+    b += up16(nb.max_slots * 16);
+    t.b_winc = b;
+    b += up16(k.has_coeff ? nb.max_slots * 8 : 0);
+    t.buf_bytes = b;
+    off += 3 * b;
+    k.ring(t, (size_t)off, s);
+    return;
+  }
   if (P->use_nbr) {
     const NbrPlan& nb = P->nb;
     TileArgs t{};
@@ -1177,7 +1429,21 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     b += up16(k.has_coeff ? nb.max_slots * 8 : 0);
     t.buf_bytes = b;
     off += 3 * b;
+    static const bool timing = std::getenv("LOAM_GPU_PHASE_TIMING") != nullptr;
+    DevBuf<long long> tbuf;
+    if (timing) {
+      tbuf.alloc(4, s);
+      LG_CUDA(cudaMemsetAsync(tbuf.get(), 0, tbuf.bytes(), s));
+      t.timing = tbuf.get();
+    }
     k.nbr(t, nb.rec_bytes, (size_t)off, s);
+    if (timing) {
+      long long h[4];
+      LG_CUDA(cudaMemcpyAsync(h, tbuf.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+      LG_CUDA(cudaStreamSynchronize(s));
+      fprintf(stderr, "[phase timing] per warp-tile cycles: wait %.0f compute %.0f (tiles %d, smem %d B)\n",
+              (double)h[0] / std::max<long long>(h[2], 1), (double)h[1] / std::max<long long>(h[2], 1), nb.ntiles, off);
+    }
     return;
   }
   OwnerArgs a{};

@@ -349,6 +349,7 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
   std::vector<uint8_t> hs(nrows_node + 16, 0);
   std::vector<int32_t> verts;
   std::vector<std::pair<int, int>> rr;
+  std::vector<std::pair<int, int>> tile_of_rows;
   auto make_runs = [&](int r0, int r1) { // runs of the tile's vertices; returns slot count
     verts.assign(hadj.begin() + h[r0], hadj.begin() + h[r1]);
     std::sort(verts.begin(), verts.end());
@@ -386,6 +387,7 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
       size_t k = std::upper_bound(rr.begin(), rr.end(), std::make_pair(v, INT32_MAX)) - rr.begin() - 1;
       hw[a] = (uint16_t)(base[k] + v - rr[k].first);
     }
+    tile_of_rows.push_back({r0, r1});
     for (int r = r0; r < r1; ++r) {
       int q = 0;
       while (h[r] + q < h[r + 1] && hadj[h[r] + q] != r) ++q;
@@ -407,6 +409,95 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
   np.runs.alloc(runs.size() ? runs.size() : 2, s);
   np.widx.alloc(hw.size(), s);
   np.selfr.alloc(hs.size(), s);
+  // ---- ring mode for P1 triangles (nrn == 3): chain each row's cells along the
+  // vertex ring / fan so a kernel fetches one new vertex per cell and completes
+  // every off-diagonal entry after two consecutive cells (no read-modify-write)
+  np.ring = false;
+  if (nrn == 3 && maxlen <= 8 && np.max_slots <= 8191 && pp.npairs) {
+    std::vector<int32_t> hpairs(pp.npairs), hrows((size_t)ncells * nrn);
+    // pp.ptr was moved into np.pptr above; pair codes are still in pp.pairs
+    LG_CUDA(cudaMemcpyAsync(hpairs.data(), pp.pairs.get(), sizeof(int32_t) * pp.npairs, cudaMemcpyDeviceToHost, s));
+    LG_CUDA(cudaMemcpyAsync(hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size(), cudaMemcpyDeviceToHost, s));
+    LG_CUDA(cudaStreamSynchronize(s));
+    std::vector<int32_t> rptr(nrows_node + 1);
+    for (int r = 0; r <= nrows_node; ++r) rptr[r] = hp[r] + r;
+    std::vector<uint16_t> rrec((size_t)rptr[nrows_node] + 8, 0);
+    std::vector<uint32_t> rinfo(nrows_node + 4, 0);
+    bool ok = true;
+    std::vector<int> av, bv;
+    std::vector<char> used;
+    for (size_t t = 0; t < tile_of_rows.size() && ok; ++t) {
+      const int tr0 = tile_of_rows[t].first, tr1 = tile_of_rows[t].second;
+      for (int r = tr0; r < tr1 && ok; ++r) {
+        auto slot_of = [&](int v) { // window slot of vertex v in this row's tile
+          for (int64_t a = h[r]; a < h[r + 1]; ++a)
+            if (hadj[a] == v) return (int)hw[a];
+          return -1;
+        };
+        auto rank_of = [&](int v) {
+          for (int64_t a = h[r]; a < h[r + 1]; ++a)
+            if (hadj[a] == v) return (int)(a - h[r]);
+          return -1;
+        };
+        const int P = hp[r + 1] - hp[r];
+        av.resize(P);
+        bv.resize(P);
+        for (int q = 0; q < P; ++q) {
+          const int code = hpairs[hp[r] + q];
+          const int c = code / 3, i = code - 3 * c;
+          av[q] = hrows[(size_t)c * 3 + (i + 1) % 3];
+          bv[q] = hrows[(size_t)c * 3 + (i + 2) % 3];
+        }
+        const int self_slot = slot_of(r), self_rank = rank_of(r);
+        rinfo[r] = (uint32_t)self_slot | ((uint32_t)self_rank << 16);
+        if (P == 0) {
+          rrec[rptr[r]] = (uint16_t)((self_slot << 3) | self_rank);
+          continue;
+        }
+        // degree of every neighbour in the star; open fans start at a degree-1 vertex
+        int start = av[0], ones = 0;
+        for (int q = 0; q < P && ok; ++q)
+          for (int v : {av[q], bv[q]}) {
+            int deg = 0;
+            for (int u = 0; u < P; ++u) deg += (av[u] == v) + (bv[u] == v);
+            if (deg > 2 || v == r) ok = false;
+            if (deg == 1) { ++ones; start = v; }
+          }
+        if (!ok || (ones != 0 && ones != 2)) { ok = false; break; }
+        used.assign(P, 0);
+        int v = start;
+        rrec[rptr[r]] = (uint16_t)((slot_of(v) << 3) | rank_of(v));
+        for (int k = 0; k < P; ++k) {
+          int q = 0;
+          while (q < P && (used[q] || (av[q] != v && bv[q] != v))) ++q;
+          if (q == P) { ok = false; break; } // star is not a single fan / ring
+          used[q] = 1;
+          v = av[q] == v ? bv[q] : av[q];
+          rrec[rptr[r] + 1 + k] = (uint16_t)((slot_of(v) << 3) | rank_of(v));
+        }
+        if (ok && ones == 0 && v != start) ok = false; // a ring must close
+      }
+    }
+    if (ok) {
+      np.ring = true;
+      np.rptr.alloc(rptr.size() + 4, s);
+      np.rrecs.alloc(rrec.size(), s);
+      np.rowinfo.alloc(rinfo.size(), s);
+      LG_CUDA(cudaMemsetAsync(np.rptr.get(), 0, np.rptr.bytes(), s));
+      LG_CUDA(cudaMemcpyAsync(np.rptr.get(), rptr.data(), sizeof(int32_t) * rptr.size(), cudaMemcpyHostToDevice, s));
+      LG_CUDA(cudaMemcpyAsync(np.rrecs.get(), rrec.data(), sizeof(uint16_t) * rrec.size(), cudaMemcpyHostToDevice, s));
+      LG_CUDA(cudaMemcpyAsync(np.rowinfo.get(), rinfo.data(), sizeof(uint32_t) * rinfo.size(), cudaMemcpyHostToDevice, s));
+      std::vector<int32_t> rt(tiles);
+      for (size_t t = 0; t < rt.size() / 8; ++t) {
+        rt[8 * t + 4] = rptr[rt[8 * t + 0]];
+        rt[8 * t + 5] = rptr[rt[8 * t + 1]];
+      }
+      np.rtiles.alloc(rt.size() ? rt.size() : 8, s);
+      if (!rt.empty())
+        LG_CUDA(cudaMemcpyAsync(np.rtiles.get(), rt.data(), sizeof(int32_t) * rt.size(), cudaMemcpyHostToDevice, s));
+      np.max_pairs += np.max_rows; // ring records per tile: pairs + one head per row
+    }
+  }
   if (!tiles.empty())
     LG_CUDA(cudaMemcpyAsync(np.tiles.get(), tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice, s));
   if (!runs.empty())

@@ -94,6 +94,14 @@ struct NbrPlan {
   int ntiles = 0;
   int max_rows = 0, max_adj = 0, max_pairs = 0, max_seg = 0, max_slots = 0, max_runs = 0; // per tile
   int max_len = 0; // longest node row
+  // RING mode (P1 triangles on a manifold mesh): the cells around each row
+  // vertex ordered along their ring / fan, one 16-bit record per chain vertex
+  // (window slot << 3 | in-row rank), P+1 records per row (head first)
+  bool ring = false;
+  DevBuf<int32_t> rptr;      // [nrows_node + 1] record offsets (pptr[r] + r)
+  DevBuf<uint16_t> rrecs;    // chain records
+  DevBuf<uint32_t> rowinfo;  // self window slot | self rank << 16
+  DevBuf<int32_t> rtiles;    // tiles with P0/P1 in ring-record units
 };
 // Build from a (sorted) node-level map and a node-level pattern.  For Mats the
 // pattern is the Mat's sparsity (csr, possibly blocked by rd/cd); for Dats

@@ -136,3 +136,34 @@ def test_inc_accumulates_into_existing_values(cfg, strat):
     w.run()  # second INC without reset: doubles every entry
     twice = get(w.outputs[0])
     assert rel(twice, 2 * once) <= TOL
+
+
+@pytest.mark.parametrize("form,kind", [("stiffness_p1_tri", O.STIFFNESS), ("helmholtz_p1_tri", O.HELMHOLTZ)])
+def test_non_manifold_star_falls_back_correctly(form, kind):
+    """A duplicated cell makes vertex stars non-manifold: the ring plan must be
+    refused and the general neighbour-list path must still match the oracle."""
+    from paper_1501_01809_b200 import loam as L
+    m = configs.mesh(2, 9, 0.2, 11, 12)
+    cv = np.concatenate([m.cv, m.cv[:3 * 5]])  # cells 0..4 appear twice
+    nc = cv.size // 3
+    cells, verts = L.Set(nc), L.Set(m.nv)
+    cm = L.Map(cells, verts, 3, cv)
+    X = L.Dat(verts, 2)
+    X.set_values(m.coords)
+    A = L.Mat(L.build_sparsity(cm, cm))
+    L.execute(L.Parloop(L.kernel(form, 1.3), cells, [L.arg(A, L.INC, cm, cm), L.arg(X, L.READ, cm)]))
+    rp, ci = A.sparsity.host()
+    ref = O.assemble_matrix(kind, 1, 2, nc, cv, 3, cv, 3, cv, m.coords, rp, ci, params=(1.3,))
+    assert rel(A.host_values(), ref) <= TOL
+
+
+def test_ring_and_general_paths_agree():
+    import os
+    a = run_cfg(2, 20, "auto").outputs[0].host_values()
+    os.environ["LOAM_GPU_NO_RING"] = "1"
+    try:
+        capi.check(capi.lib().loam_gpu_plan_cache_clear())
+        b = run_cfg(2, 20, "auto").outputs[0].host_values()
+    finally:
+        del os.environ["LOAM_GPU_NO_RING"]
+    assert rel(a, b) <= TOL
