@@ -693,6 +693,8 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
 struct RingArgs {
   const int32_t* tiles;
   int ntiles;
+  int* next_tile;  // dynamic scheduler counter of this launch (zeroed by the previous launch)
+  int* reset_tile; // counter of the next launch: zeroed here
   const int32_t* nptr;
   const int32_t* rptr;
   const uint16_t* recs;
@@ -713,7 +715,9 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + 3;
+  int* slot_tile = reinterpret_cast<int*>(full + 6); // [3] tile id carried by each ring stage (-1: done)
   const int tid = threadIdx.x;
+  if (blockIdx.x == 0 && tid == 0) *a.reset_tile = 0;
   if (tid == 0) {
     for (int b = 0; b < 3; ++b) {
       mbar_init(&full[b], 1);
@@ -722,19 +726,25 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
     fence_mbar_init();
   }
   __syncthreads();
-  const int K = a.ntiles > (int)blockIdx.x ? (a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  auto tile_meta = [&](int k, int (&m)[8]) {
-    const int4* t = reinterpret_cast<const int4*>(a.tiles + 8 * (blockIdx.x + k * gridDim.x));
+  auto tile_meta = [&](int tile, int (&m)[8]) {
+    const int4* t = reinterpret_cast<const int4*>(a.tiles + 8 * tile);
     const int4 x = __ldg(t), y = __ldg(t + 1);
     m[0] = x.x; m[1] = x.y; m[2] = x.z; m[3] = x.w; m[4] = y.x; m[5] = y.y; m[6] = y.z; m[7] = y.w;
   };
   auto ring = [&](int k) { return sm + a.off_buf + (k % 3) * a.buf_bytes; };
-  if (tid >= kTileThreads) { // ---- producer warp
+  if (tid >= kTileThreads) { // ---- producer warp: grabs tiles dynamically
     if (tid == kTileThreads)
-      for (int k = 0; k < K; ++k) {
+      for (int k = 0;; ++k) {
         if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
+        const int tile = atomicAdd(a.next_tile, 1);
+        if (tile >= a.ntiles) { // publish "no more tiles" through the stage
+          slot_tile[k % 3] = -1;
+          mbar_arrive(&full[k % 3]);
+          break;
+        }
+        slot_tile[k % 3] = tile;
         int m[8];
-        tile_meta(k, m);
+        tile_meta(tile, m);
         unsigned char* buf = ring(k);
         uint64_t* bar = &full[k % 3];
         auto rb = [](int lo, int hi, int es, int64_t& s0) {
@@ -779,9 +789,12 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
   }
   // ---- consumers: one thread per row vertex
   double* seg = reinterpret_cast<double*>(sm + a.off_seg);
-  for (int k = 0; k < K; ++k) {
+  for (int k = 0;; ++k) {
+    mbar_wait(&full[k % 3], (k / 3) & 1);
+    const int tile = slot_tile[k % 3];
+    if (tile < 0) break;
     int m[8];
-    tile_meta(k, m);
+    tile_meta(tile, m);
     const int R0 = m[0], nrows = m[1] - m[0], A0 = m[2], nA = m[3] - m[2], P0 = m[4];
     if constexpr (F::BILINEAR) {
       if (a.accumulate) {
@@ -789,7 +802,6 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
         named_bar(1, kTileThreads);
       }
     }
-    mbar_wait(&full[k % 3], (k / 3) & 1);
     const unsigned char* buf = ring(k);
     const int32_t* nptr_s = reinterpret_cast<const int32_t*>(buf + a.b_nptr) + skew_of(R0, 4);
     const int32_t* rptr_s = reinterpret_cast<const int32_t*>(buf + a.b_rptr) + skew_of(R0, 4);
@@ -814,11 +826,20 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
         if (a.accumulate) seg[a0 + rank] += v;
         else seg[a0 + rank] = v;
       };
-#pragma unroll 2
+      // software pipeline: the record and vertex of cell q+1 are loaded before
+      // cell q is computed
+      uint32_t r_nx = rec_s[q0 + 1 < q1 ? q0 + 1 : q0];
+      double2 x_nx = win[r_nx >> 3];
+      double c_nx = F::HAS_COEFF ? winc[r_nx >> 3] : 0.0;
       for (int q = q0 + 1; q < q1; ++q) {
-        const uint32_t r = rec_s[q];
-        const double2 xn = win[r >> 3];
-        const double cn = F::HAS_COEFF ? winc[r >> 3] : 0.0;
+        const uint32_t r = r_nx;
+        const double2 xn = x_nx;
+        const double cn = c_nx;
+        if (q + 1 < q1) {
+          r_nx = rec_s[q + 1];
+          x_nx = win[r_nx >> 3];
+          if constexpr (F::HAS_COEFF) c_nx = winc[r_nx >> 3];
+        }
         const double X[3][2] = {{xs.x, xs.y}, {xp.x, xp.y}, {xn.x, xn.y}};
         Geom<2> G;
         geometry<2>(X, G);
@@ -1152,6 +1173,8 @@ NodeMap node_view(const loam_map_desc* m) {
 }
 
 struct FastPlan {
+  DevBuf<int> counter; // dynamic tile scheduler: two ping-pong counters
+  int parity = 0;
   bool use_nbr = false;
   NbrPlan nb;
   LocalityPlan loc;
@@ -1199,6 +1222,8 @@ constexpr int kTileRuns = 32;    // contiguous runs per window
 std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_desc* args,
                                           cudaStream_t s) {
   auto P = std::make_shared<FastPlan>();
+  P->counter.alloc(4, s);
+  LG_CUDA(cudaMemsetAsync(P->counter.get(), 0, 4 * sizeof(int), s));
   const NodeMap R = node_view(args[0].map);
   const loam_map_desc* X = args[1].map;
   const loam_map_desc* Cm = k.has_coeff ? args[2].map : nullptr;
@@ -1355,6 +1380,9 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     RingArgs t{};
     t.tiles = nb.rtiles.get();
     t.ntiles = nb.ntiles;
+    t.next_tile = P->counter.get() + P->parity;
+    t.reset_tile = P->counter.get() + (P->parity ^ 1);
+    P->parity ^= 1;
     t.nptr = nb.nptr.get();
     t.rptr = nb.rptr.get();
     t.recs = nb.rrecs.get();
@@ -1366,7 +1394,7 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     t.out = args[0].data;
     t.accumulate = (args[0].flags & LOAM_ARG_ZERO) ? 0 : 1;
     auto up16 = [](int x) { return (x + 15) & ~15; };
-    int off = 64;
+    int off = 128; // 6 mbarriers + 3 stage tile ids
     t.off_seg = off;
     off += up16(k.bilinear ? nb.max_seg * 8 : 0);
     t.off_buf = off;
