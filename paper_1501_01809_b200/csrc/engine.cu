@@ -432,6 +432,53 @@ struct TileArgs {
 
 __device__ __forceinline__ int skew_of(int lo, int es) { return ((lo * es) & 15) / es; }
 
+// Warp-cooperative staging of a tile's id runs [lo, hi) of an es-doubles-per-id
+// array into consecutive window slots: lane r handles run r (32 at a time),
+// slots from a warp scan.  A run whose byte count is not a multiple of 16 gets
+// its last double stored by the lane itself (bulk copies move 16-byte units;
+// runs start at even ids so the source side is aligned).  prepare() does the
+// tail stores and returns the warp-total bulk bytes; issue() launches copies.
+struct RunSet {
+  const int2* runs;
+  int cnt;
+  const double* src;
+  double* dst;
+  int es;
+};
+template <bool ISSUE>
+__device__ __forceinline__ uint32_t stage_runs(const RunSet& s, int lane, uint64_t* bar) {
+  uint32_t tx = 0;
+  int base = 0;
+  for (int r0 = 0; r0 < s.cnt; r0 += 32) {
+    int lo = 0, hi = 0;
+    if (r0 + lane < s.cnt) {
+      const int2 p = __ldg(s.runs + r0 + lane);
+      lo = p.x;
+      hi = p.y;
+    }
+    const int n = hi - lo;
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int slot = base + incl - n;
+    const uint32_t nb = (uint32_t)n * s.es * 8;
+    if (ISSUE) {
+      if (nb >= 16) bulk_g2s(s.dst + (int64_t)slot * s.es, s.src + (int64_t)lo * s.es, nb & ~15u, bar);
+    } else {
+      if (nb & 15) s.dst[(int64_t)(slot + n) * s.es - 1] = s.src[(int64_t)hi * s.es - 1];
+      tx += nb & ~15u;
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (!ISSUE)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
+  return tx;
+}
+
 constexpr int kTileThreads = 256;                 // consumer threads (8 warps)
 constexpr int kTileBlock = kTileThreads + 32;     // + one TMA producer warp
 
@@ -733,58 +780,49 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
   };
   auto ring = [&](int k) { return sm + a.off_buf + (k % 3) * a.buf_bytes; };
   if (tid >= kTileThreads) { // ---- producer warp: grabs tiles dynamically
-    if (tid == kTileThreads)
-      for (int k = 0;; ++k) {
-        if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
-        const int tile = atomicAdd(a.next_tile, 1);
-        if (tile >= a.ntiles) { // publish "no more tiles" through the stage
+    const int lane = tid & 31;
+    for (int k = 0;; ++k) {
+      if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
+      int tile = 0;
+      if (lane == 0) tile = atomicAdd(a.next_tile, 1);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      if (tile >= a.ntiles) { // publish "no more tiles" through the stage
+        if (lane == 0) {
           slot_tile[k % 3] = -1;
           mbar_arrive(&full[k % 3]);
-          break;
         }
-        slot_tile[k % 3] = tile;
-        int m[8];
-        tile_meta(tile, m);
-        unsigned char* buf = ring(k);
-        uint64_t* bar = &full[k % 3];
-        auto rb = [](int lo, int hi, int es, int64_t& s0) {
-          s0 = ((int64_t)lo * es) & ~int64_t(15);
-          return (uint32_t)((((int64_t)hi * es + 15) & ~int64_t(15)) - s0);
-        };
-        int64_t g0, g1, g2, g3;
-        const uint32_t n0 = F::BILINEAR ? rb(m[0], m[1] + 1, 4, g0) : (g0 = 0, 0u);
-        const uint32_t n1 = rb(m[0], m[1] + 1, 4, g1), n2 = rb(m[4], m[5], 2, g2), n3 = rb(m[0], m[1], 4, g3);
-        uint32_t tx = n0 + n1 + n2 + n3;
-        double* win = reinterpret_cast<double*>(buf + a.b_win);
-        double* winc = reinterpret_cast<double*>(buf + a.b_winc);
-        int slot = 0;
-        for (int r = 0; r < m[7]; ++r) {
-          const int lo = __ldg(a.runs + 2 * (m[6] + r)), hi = __ldg(a.runs + 2 * (m[6] + r) + 1);
-          tx += (uint32_t)(hi - lo) * 16;
-          if constexpr (F::HAS_COEFF) {
-            const uint32_t nc = (uint32_t)(hi - lo) * 8;
-            tx += nc & ~15u;
-            if (nc & 15) winc[slot + hi - lo - 1] = a.coeff[hi - 1];
-          }
-          slot += hi - lo;
-        }
-        fence_async_shared();
+        break;
+      }
+      if (lane == 0) slot_tile[k % 3] = tile;
+      int m[8];
+      tile_meta(tile, m);
+      unsigned char* buf = ring(k);
+      uint64_t* bar = &full[k % 3];
+      auto rb = [](int lo, int hi, int es, int64_t& s0) {
+        s0 = ((int64_t)lo * es) & ~int64_t(15);
+        return (uint32_t)((((int64_t)hi * es + 15) & ~int64_t(15)) - s0);
+      };
+      int64_t g0, g1, g2, g3;
+      const uint32_t n0 = F::BILINEAR ? rb(m[0], m[1] + 1, 4, g0) : (g0 = 0, 0u);
+      const uint32_t n1 = rb(m[0], m[1] + 1, 4, g1), n2 = rb(m[4], m[5], 2, g2), n3 = rb(m[0], m[1], 4, g3);
+      const RunSet rc{reinterpret_cast<const int2*>(a.runs) + m[6], m[7], a.coords,
+                      reinterpret_cast<double*>(buf + a.b_win), 2};
+      const RunSet rk{reinterpret_cast<const int2*>(a.runs) + m[6], F::HAS_COEFF ? m[7] : 0, a.coeff,
+                      reinterpret_cast<double*>(buf + a.b_winc), 1};
+      const uint32_t tx = n0 + n1 + n2 + n3 + stage_runs<false>(rc, lane, bar) + stage_runs<false>(rk, lane, bar);
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) {
         mbar_arrive_expect_tx(bar, tx);
         if (n0) bulk_g2s(buf + a.b_nptr, reinterpret_cast<const unsigned char*>(a.nptr) + g0, n0, bar);
         bulk_g2s(buf + a.b_rptr, reinterpret_cast<const unsigned char*>(a.rptr) + g1, n1, bar);
         if (n2) bulk_g2s(buf + a.b_recs, reinterpret_cast<const unsigned char*>(a.recs) + g2, n2, bar);
         if (n3) bulk_g2s(buf + a.b_info, reinterpret_cast<const unsigned char*>(a.rowinfo) + g3, n3, bar);
-        slot = 0;
-        for (int r = 0; r < m[7]; ++r) {
-          const int lo = __ldg(a.runs + 2 * (m[6] + r)), hi = __ldg(a.runs + 2 * (m[6] + r) + 1);
-          bulk_g2s(win + 2 * slot, a.coords + 2 * (int64_t)lo, (uint32_t)(hi - lo) * 16, bar);
-          if constexpr (F::HAS_COEFF) {
-            const uint32_t nc = ((uint32_t)(hi - lo) * 8) & ~15u;
-            if (nc) bulk_g2s(winc + slot, a.coeff + lo, nc, bar);
-          }
-          slot += hi - lo;
-        }
       }
+      __syncwarp();
+      stage_runs<true>(rc, lane, bar);
+      stage_runs<true>(rk, lane, bar);
+    }
     return;
   }
   // ---- consumers: one thread per row vertex
@@ -903,6 +941,241 @@ void launch_ring(const RingArgs& a, size_t smem, cudaStream_t s) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Canonical pair-tile kernel (plan.cuh PTilePlan) for every catalogue form:
+// P2 tets and triangles, vector P1 elasticity, Taylor-Hood blocks.  The plan
+// permuted each cell's local numbering so the owning row is local vertex 0
+// (vertex rows) or the first local edge (P2 edge rows): the element row is a
+// compile-time index and one thread computes its node row's whole RD x NC
+// block once per pair.  TMA producer warp + consumer warps as in k_tile; the
+// cell vertices (and coefficients) come from TMA-loaded vertex windows via the
+// u16 slots in the pair record; no per-pair global gathers remain.
+struct PTileArgs {
+  const int32_t* tiles;
+  int ntiles;
+  int* next_tile;
+  int* reset_tile;
+  const int32_t* pptr;
+  const int32_t* nptr;
+  const uint8_t* recs;
+  const int32_t* runs;
+  const int32_t* cruns;
+  const double* coords;
+  const double* coeff;
+  FormParams prm;
+  double* out;
+  int accumulate;
+  int off_seg, off_buf, buf_bytes;
+  int b_pptr, b_nptr, b_recs, b_win, b_winc;
+};
+
+template <class F>
+struct PRec { // record layout (plan.cu:build_ptile)
+  static constexpr int NV = F::GD + 1;
+  static constexpr int NCF = F::HAS_COEFF ? F::NCOEFF : 0;
+  static constexpr int OFF_CF = 2 * NV, OFF_RK = OFF_CF + 2 * NCF, OFF_CI = OFF_RK + F::NCN;
+  static constexpr int BYTES = (OFF_CI + 1 + 3) & ~3;
+};
+
+template <class F, int NT>
+__global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PTileArgs a) {
+  constexpr int GD = F::GD, NV = GD + 1, W = F::RD * F::CD;
+  using RL = PRec<F>;
+  constexpr int RB = RL::BYTES;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + 3;
+  int* slot_tile = reinterpret_cast<int*>(full + 6);
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0 && tid == 0) *a.reset_tile = 0;
+  if (tid == 0) {
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], NT / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto tile_meta = [&](int tile, int (&m)[12]) {
+    const int4* t = reinterpret_cast<const int4*>(a.tiles + 12 * tile);
+    const int4 x = __ldg(t), y = __ldg(t + 1), z = __ldg(t + 2);
+    m[0] = x.x; m[1] = x.y; m[2] = x.z; m[3] = x.w; m[4] = y.x; m[5] = y.y; m[6] = y.z; m[7] = y.w;
+    m[8] = z.x; m[9] = z.y; m[10] = z.z; m[11] = z.w;
+  };
+  auto ring = [&](int k) { return sm + a.off_buf + (k % 3) * a.buf_bytes; };
+  if (tid >= NT) { // ---- producer warp (warp-cooperative run staging)
+    const int lane = tid & 31;
+    for (int k = 0;; ++k) {
+      if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
+      int tile = 0;
+      if (lane == 0) tile = atomicAdd(a.next_tile, 1);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      if (tile >= a.ntiles) {
+        if (lane == 0) {
+          slot_tile[k % 3] = -1;
+          mbar_arrive(&full[k % 3]);
+        }
+        break;
+      }
+      if (lane == 0) slot_tile[k % 3] = tile;
+      int m[12];
+      tile_meta(tile, m);
+      unsigned char* buf = ring(k);
+      uint64_t* bar = &full[k % 3];
+      auto rb = [](int64_t lo_b, int64_t hi_b, int64_t& s0) {
+        s0 = lo_b & ~int64_t(15);
+        return (uint32_t)(((hi_b + 15) & ~int64_t(15)) - s0);
+      };
+      int64_t g0, g1, g2;
+      const uint32_t n0 = rb((int64_t)m[0] * 4, (int64_t)(m[1] + 1) * 4, g0);
+      const uint32_t n1 = F::BILINEAR ? rb((int64_t)m[0] * 4, (int64_t)(m[1] + 1) * 4, g1) : (g1 = 0, 0u);
+      const uint32_t n2 = rb((int64_t)m[4] * RB, (int64_t)m[5] * RB, g2);
+      const RunSet rc{reinterpret_cast<const int2*>(a.runs) + m[6], m[7], a.coords,
+                      reinterpret_cast<double*>(buf + a.b_win), GD};
+      const RunSet rk{reinterpret_cast<const int2*>(a.cruns) + m[8], F::HAS_COEFF ? m[9] : 0, a.coeff,
+                      reinterpret_cast<double*>(buf + a.b_winc), 1};
+      const uint32_t tx = n0 + n1 + n2 + stage_runs<false>(rc, lane, bar) + stage_runs<false>(rk, lane, bar);
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(bar, tx);
+        bulk_g2s(buf + a.b_pptr, reinterpret_cast<const unsigned char*>(a.pptr) + g0, n0, bar);
+        if (n1) bulk_g2s(buf + a.b_nptr, reinterpret_cast<const unsigned char*>(a.nptr) + g1, n1, bar);
+        if (n2) bulk_g2s(buf + a.b_recs, a.recs + g2, n2, bar);
+      }
+      __syncwarp();
+      stage_runs<true>(rc, lane, bar);
+      stage_runs<true>(rk, lane, bar);
+    }
+    return;
+  }
+  // ---- consumers: one thread per node row
+  double* seg = reinterpret_cast<double*>(sm + a.off_seg);
+  for (int k = 0;; ++k) {
+    mbar_wait(&full[k % 3], (k / 3) & 1);
+    const int tile = slot_tile[k % 3];
+    if (tile < 0) break;
+    int m[12];
+    tile_meta(tile, m);
+    const int R0 = m[0], nrows = m[1] - m[0], A0 = m[2], nA = m[3] - m[2], P0 = m[4];
+    const int64_t E0 = (int64_t)A0 * W;
+    if constexpr (F::BILINEAR) {
+      const int len = nA * W;
+      if (a.accumulate)
+        for (int t = tid; t < len; t += NT) seg[t] = a.out[E0 + t];
+      else
+        for (int t = tid; t < len; t += NT) seg[t] = 0.0;
+      named_bar(1, NT);
+    }
+    const unsigned char* buf = ring(k);
+    const int32_t* pptr_s = reinterpret_cast<const int32_t*>(buf + a.b_pptr) + skew_of(R0, 4);
+    const int32_t* nptr_s = reinterpret_cast<const int32_t*>(buf + a.b_nptr) + skew_of(R0, 4);
+    const unsigned char* rec0 = buf + a.b_recs + (((int64_t)P0 * RB) & 15);
+    const double* win = reinterpret_cast<const double*>(buf + a.b_win);
+    const double* winc = reinterpret_cast<const double*>(buf + a.b_winc);
+    // G lanes per row (tile field 10): lane `sub` takes pairs sub, sub+G, ...;
+    // the group's element rows are added to the row segment in G serialized
+    // sub-steps (no shared-memory atomics: f64 ATOMS is a CAS loop)
+    const int G = m[10], sub = tid & (G - 1), RPP = NT / G;
+    for (int base = 0; base < nrows; base += RPP) {
+      const int node = base + tid / G;
+      const bool live = node < nrows;
+      int a0 = 0, L = 0, p0 = 0, p1 = 0;
+      if (live) {
+        if constexpr (F::BILINEAR) {
+          a0 = nptr_s[node] - A0;
+          L = nptr_s[node + 1] - A0 - a0;
+        }
+        p0 = pptr_s[node] - P0;
+        p1 = pptr_s[node + 1] - P0;
+      }
+      const int iters = __reduce_max_sync(0xffffffffu, (p1 - p0 + G - 1) / G);
+      double acc = 0.0;
+      for (int it = 0; it < iters; ++it) {
+        const int p = p0 + it * G + sub;
+        const bool has = p < p1;
+        double blk[F::RD * F::NC];
+        const unsigned char* rec = rec0 + (int64_t)(has ? p : p0) * RB;
+        if (has) {
+          double X[NV][GD];
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const int sl = *reinterpret_cast<const uint16_t*>(rec + 2 * v);
+            if constexpr (GD == 2) {
+              const double2 c2 = reinterpret_cast<const double2*>(win)[sl];
+              X[v][0] = c2.x;
+              X[v][1] = c2.y;
+            } else {
+#pragma unroll
+              for (int c = 0; c < GD; ++c) X[v][c] = win[sl * GD + c];
+            }
+          }
+          double C[F::HAS_COEFF ? F::NCOEFF : 1];
+          if constexpr (F::HAS_COEFF)
+#pragma unroll
+            for (int q = 0; q < F::NCOEFF; ++q) C[q] = winc[*reinterpret_cast<const uint16_t*>(rec + RL::OFF_CF + 2 * q)];
+          Geom<GD> Gm;
+          geometry<GD>(X, Gm);
+          const int ci = rec[RL::OFF_CI];
+          if constexpr (F::NRN > NV) { // P2 row space: vertex or edge canonical row
+            if (ci == 0) F::row(0, Gm, C, a.prm, blk);
+            else F::row(NV, Gm, C, a.prm, blk);
+          } else {
+            F::row(0, Gm, C, a.prm, blk);
+          }
+          if constexpr (!F::BILINEAR) acc += blk[0];
+        }
+        if constexpr (F::BILINEAR) {
+          for (int st = 0; st < G; ++st) {
+            if (has && st == sub) {
+#pragma unroll
+              for (int j = 0; j < F::NCN; ++j) {
+                const int rk = rec[RL::OFF_RK + j];
+#pragma unroll
+                for (int d = 0; d < F::RD; ++d)
+#pragma unroll
+                  for (int c = 0; c < F::CD; ++c) seg[a0 * W + d * L * F::CD + rk * F::CD + c] += blk[d * F::NC + j * F::CD + c];
+              }
+            }
+            if (G > 1) __syncwarp();
+          }
+        }
+      }
+      if constexpr (!F::BILINEAR) {
+        for (int o = 1; o < G; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (live && sub == 0) a.out[R0 + node] = a.accumulate ? a.out[R0 + node] + acc : acc;
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[k % 3]);
+    if constexpr (F::BILINEAR) {
+      named_bar(1, NT);
+      const int len = nA * W;
+      for (int t = tid; t < len; t += NT) a.out[E0 + t] = seg[t];
+      named_bar(1, NT);
+    }
+  }
+}
+
+constexpr int kPTileThreads = 128;
+
+template <class F>
+void launch_ptile(const PTileArgs& a, size_t smem, cudaStream_t s) {
+  if (a.ntiles == 0) return;
+  static size_t attr = 0;
+  auto kern = k_ptile<F, kPTileThreads>;
+  if (attr < smem) {
+    LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  int blocks = 1;
+  LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kPTileThreads + 32, smem));
+  const int grid = std::min(a.ntiles, std::max(blocks, 1) * kNumSMs);
+  kern<<<grid, kPTileThreads + 32, smem, s>>>(a);
+  count_launch();
+  LG_LAUNCH_CHECK();
+}
+
 // ===========================================================================
 // Registry
 // ===========================================================================
@@ -911,6 +1184,7 @@ using GenericFn = void (*)(const GLaunch&, cudaStream_t);
 using OwnerFn = void (*)(const OwnerArgs&, int grid, size_t smem, cudaStream_t);
 using NbrFn = void (*)(const TileArgs&, int rec_bytes, size_t smem, cudaStream_t);
 using RingFn = void (*)(const RingArgs&, size_t smem, cudaStream_t);
+using PTileFn = void (*)(const PTileArgs&, size_t smem, cudaStream_t);
 
 struct Entry {
   KernelInfo info;
@@ -922,6 +1196,7 @@ struct Entry {
   OwnerFn owner = nullptr;
   NbrFn nbr = nullptr;   // P1 forms only
   RingFn ring = nullptr; // scalar P1 triangle forms only
+  PTileFn ptile = nullptr;
 };
 
 template <class K>
@@ -1016,6 +1291,7 @@ Entry form_entry(const std::string& name) {
   e.bilinear = F::BILINEAR;
   e.has_coeff = F::HAS_COEFF;
   e.owner = &launch_owner<F>;
+  e.ptile = &launch_ptile<F>;
   if constexpr (P == 1 && F::NRN == D + 1 && (!F::BILINEAR || F::NCN == F::NRN)) e.nbr = &launch_nbr<F>;
   if constexpr (P == 1 && D == 2 && F::RD == 1 && F::CD == 1) e.ring = &launch_ring<F>;
   return e;
@@ -1177,6 +1453,8 @@ struct FastPlan {
   int parity = 0;
   bool use_nbr = false;
   NbrPlan nb;
+  bool use_ptile = false;
+  PTilePlan pt;
   LocalityPlan loc;
   SortedMap xmap, cmap;
   const int32_t* xptr = nullptr;
@@ -1288,6 +1566,38 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     CsrView csr{sp->row_ptr, sp->col_idx, sp->nrows, sp->ncols, sp->nnz, R.dim, Cn.dim};
     build_ranks(P->pp, srows.v.get(), sc, Cn.v.arity, csr, s);
     build_chunks(P->pp, csr, kSegMax, 32 / R.dim, s);
+  }
+  // canonical pair tiles: default for the scalar / 2-vector bilinear forms the
+  // ring / neighbour paths do not take (P2 matrices, Taylor-Hood blocks).  P2
+  // actions are coefficient-window bound and 3-vector rows overflow the tile
+  // segment; both stay on the pair-list kernel (profiles/r01/strategies_*).
+  const bool ptile_form = (k.bilinear && k.rd * k.cd <= 4) || std::getenv("LOAM_GPU_PTILE_ALL");
+  if (strat == 0 && ptile_form && !std::getenv("LOAM_GPU_NO_PTILE") && (reinterpret_cast<uintptr_t>(args[1].data) & 15) == 0 &&
+      (!Cm || (reinterpret_cast<uintptr_t>(args[2].data) & 15) == 0)) {
+    SortedMap sx, scf;
+    gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, sx, s);
+    if (Cm) gather_rows(MapView{Cm->values, n, Cm->arity, Cm->target_size}, perm, scf, s);
+    PTileSpec spec;
+    spec.gd = k.gd;
+    spec.nrn = k.nrn;
+    spec.ncn = k.bilinear ? k.ncn : 0;
+    spec.ncoeff = k.has_coeff ? k.ncoeff : 0;
+    spec.rd = k.rd;
+    spec.cd = k.cd;
+    spec.tile_rows = 128;
+    spec.tile_seg = 4096;
+    spec.tile_pairs = 768;
+    spec.tile_slots = 1024;
+    CsrView csr{};
+    if (k.bilinear) {
+      const loam_sparsity_desc* sp = args[0].sparsity;
+      csr = CsrView{sp->row_ptr, sp->col_idx, sp->nrows, sp->ncols, sp->nnz, R.dim, node_view(args[0].col_map).dim};
+    }
+    if (build_ptile(P->pt, spec, n, R.v.target, srows.v.get(), nullptr, sx.v.get(), X->target_size,
+                    Cm ? scf.v.get() : nullptr, Cm ? Cm->target_size : 0, P->pp, csr, s)) {
+      P->use_ptile = true;
+      return P;
+    }
   }
   // sorted coordinate / coefficient maps; share storage where maps coincide
   const MapView xv{X->values, n, X->arity, X->target_size};
@@ -1414,6 +1724,45 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     t.buf_bytes = b;
     off += 3 * b;
     k.ring(t, (size_t)off, s);
+    return;
+  }
+  if (P->use_ptile) {
+    const PTilePlan& pt = P->pt;
+    PTileArgs t{};
+    t.tiles = pt.tiles.get();
+    t.ntiles = pt.ntiles;
+    t.next_tile = P->counter.get() + P->parity;
+    t.reset_tile = P->counter.get() + (P->parity ^ 1);
+    P->parity ^= 1;
+    t.pptr = pt.pptr.get();
+    t.nptr = pt.nptr.get();
+    t.recs = pt.recs.get();
+    t.runs = pt.runs.get();
+    t.cruns = pt.cruns.get();
+    t.coords = args[1].data;
+    t.coeff = k.has_coeff ? args[2].data : nullptr;
+    t.prm = prm;
+    t.out = args[0].data;
+    t.accumulate = (args[0].flags & LOAM_ARG_ZERO) ? 0 : 1;
+    auto up16 = [](int x) { return (x + 15) & ~15; };
+    int off = 128;
+    t.off_seg = off;
+    off += up16(k.bilinear ? pt.max_seg * 8 : 0);
+    t.off_buf = off;
+    int b = 0;
+    t.b_pptr = b;
+    b += up16((pt.max_rows + 1) * 4 + 32);
+    t.b_nptr = b;
+    b += up16(k.bilinear ? (pt.max_rows + 1) * 4 + 32 : 0);
+    t.b_recs = b;
+    b += up16(pt.max_pairs * pt.rec_bytes + 32);
+    t.b_win = b;
+    b += up16(pt.max_slots * k.gd * 8 + 16);
+    t.b_winc = b;
+    b += up16(k.has_coeff ? pt.max_cslots * 8 + 16 : 0);
+    t.buf_bytes = b;
+    off += 3 * b;
+    k.ptile(t, (size_t)off, s);
     return;
   }
   if (P->use_nbr) {
@@ -1667,7 +2016,11 @@ void execute(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_de
   FormParams prm{{0, 0, 0, 0}};
   for (int i = 0; i < kd->nparams && i < 4; ++i) prm.p[i] = kd->params[i];
   const int strat = options().inc_strategy;
-  if (n > 0 && (strat == 0 || strat == 2 || strat == 4) && fast_pattern(k, args, nargs)) {
+  // auto: P2 tetrahedral actions (C3 residual) are fastest with one fp64 RED
+  // per element entry -- 10 rows per cell, each recomputed by its owner would
+  // redo the cell geometry 10 times (profiles/r01/strategies_*: 0.34 vs 0.80 ms)
+  const bool atomic_auto = strat == 0 && !std::getenv("LOAM_GPU_PTILE_ALL") && !k.bilinear && k.form >= 0 && k.gd == 3 && k.nrn > k.gd + 1;
+  if (n > 0 && !atomic_auto && (strat == 0 || strat == 2 || strat == 4) && fast_pattern(k, args, nargs)) {
     try {
       run_fast(k, n, args, nargs, prm, s);
       return;

@@ -2,6 +2,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
+#include <cstring>
 #include <vector>
 
 #include "plan.cuh"
@@ -504,6 +506,198 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
     LG_CUDA(cudaMemcpyAsync(np.runs.get(), runs.data(), sizeof(int32_t) * runs.size(), cudaMemcpyHostToDevice, s));
   LG_CUDA(cudaMemcpyAsync(np.widx.get(), hw.data(), sizeof(uint16_t) * hw.size(), cudaMemcpyHostToDevice, s));
   LG_CUDA(cudaMemcpyAsync(np.selfr.get(), hs.data(), hs.size(), cudaMemcpyHostToDevice, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  return true;
+}
+
+namespace {
+// Local node permutation induced by a vertex permutation sigma (new vertex
+// index of old vertex v is sigma[v]) on Lagrange P1 / P2 simplices; returns
+// newpos[old local node].  P2 local edges follow elements.cuh / space.hpp.
+const int kTriEdge[3][2] = {{1, 2}, {0, 2}, {0, 1}};
+const int kTetEdge[6][2] = {{2, 3}, {1, 3}, {1, 2}, {0, 3}, {0, 2}, {0, 1}};
+void induced(int gd, int nloc, const int* sigma, int* newpos) {
+  const int nv = gd + 1;
+  for (int v = 0; v < nv && v < nloc; ++v) newpos[v] = sigma[v];
+  if (nloc == nv) return;
+  const int ne = gd == 2 ? 3 : 6;
+  const int (*E)[2] = gd == 2 ? kTriEdge : kTetEdge;
+  for (int e = 0; e < ne; ++e) {
+    int a = sigma[E[e][0]], b = sigma[E[e][1]];
+    if (a > b) std::swap(a, b);
+    for (int f = 0; f < ne; ++f)
+      if (E[f][0] == a && E[f][1] == b) newpos[nv + e] = nv + f;
+  }
+}
+// Vertex permutation that makes row-space local node i canonical.
+// Returns the canonical local index (0 or nv).
+int canonical_sigma(int gd, int nrn, int i, int* sigma) {
+  const int nv = gd + 1;
+  if (i < nv) { // vertex i -> 0, the others keep their relative order
+    int k = 1;
+    for (int v = 0; v < nv; ++v) sigma[v] = v == i ? 0 : k++;
+    return 0;
+  }
+  const int (*E)[2] = gd == 2 ? kTriEdge : kTetEdge;
+  const int a = E[i - nv][0], b = E[i - nv][1];
+  // edge (a,b) -> the first local edge: (1,2) on triangles, (2,3) on tets
+  int k = 0;
+  const int ta = gd == 2 ? 1 : 2, tb = gd == 2 ? 2 : 3;
+  for (int v = 0; v < nv; ++v) sigma[v] = v == a ? ta : (v == b ? tb : k++);
+  (void)nrn;
+  return nv;
+}
+} // namespace
+
+bool build_ptile(PTilePlan& out, const PTileSpec& sp, int ncells, int nrows_node, const int32_t* sorted_rows,
+                 const int32_t* sorted_cols, const int32_t* sorted_x, int nverts, const int32_t* sorted_coeff,
+                 int ncoeff_nodes, const PairPlan& pp, const CsrView& csr, cudaStream_t s) {
+  const int gd = sp.gd, nv = gd + 1, nrn = sp.nrn, ncn = sp.ncn, ncf = sp.ncoeff;
+  const int64_t np = pp.npairs;
+  // ---- host copies
+  std::vector<int32_t> hrows((size_t)ncells * nrn), hx((size_t)ncells * nv), hcols, hcf, hpairs(np), hp(nrows_node + 1);
+  std::vector<uint8_t> hrank;
+  LG_CUDA(cudaMemcpyAsync(hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size(), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hx.data(), sorted_x, sizeof(int32_t) * hx.size(), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hpairs.data(), pp.pairs.get(), sizeof(int32_t) * np, cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hp.data(), pp.ptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
+  if (ncn) {
+    hrank.resize((size_t)np * ncn);
+    LG_CUDA(cudaMemcpyAsync(hrank.data(), pp.ranks.get(), hrank.size(), cudaMemcpyDeviceToHost, s));
+  }
+  if (ncf) {
+    hcf.resize((size_t)ncells * ncf);
+    LG_CUDA(cudaMemcpyAsync(hcf.data(), sorted_coeff, sizeof(int32_t) * hcf.size(), cudaMemcpyDeviceToHost, s));
+  }
+  std::vector<int64_t> hn(nrows_node + 1, 0);
+  if (ncn) { // node-level pattern offsets from the (blocked) CSR
+    std::vector<int64_t> rp((size_t)nrows_node * csr.rd + 1);
+    LG_CUDA(cudaMemcpyAsync(rp.data(), csr.row_ptr, sizeof(int64_t) * rp.size(), cudaMemcpyDeviceToHost, s));
+    LG_CUDA(cudaStreamSynchronize(s));
+    for (int r = 0; r <= nrows_node; ++r) hn[r] = rp[(size_t)r * csr.rd] / ((int64_t)csr.rd * csr.cd);
+  }
+  LG_CUDA(cudaStreamSynchronize(s));
+  (void)sorted_cols;
+  const int W = sp.rd * sp.cd;
+  // ---- record layout
+  const int off_cf = 2 * nv, off_rk = off_cf + 2 * ncf, off_ci = off_rk + ncn;
+  const int rb = (off_ci + 1 + 3) & ~3;
+  out.rec_bytes = rb;
+  out.nrows_node = nrows_node;
+  // ---- tiles with coordinate / coefficient windows
+  constexpr int kGap = 8;
+  auto make_runs = [&](std::vector<int>& ids, int limit, std::vector<std::pair<int, int>>& rr) {
+    std::sort(ids.begin(), ids.end());
+    ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+    rr.clear();
+    int slots = 0;
+    for (int v : ids) {
+      const int lo = v & ~1, hi = std::min(limit, (v + 2) & ~1);
+      if (!rr.empty() && lo <= rr.back().second + kGap) rr.back().second = std::max(rr.back().second, hi);
+      else rr.emplace_back(lo, hi);
+    }
+    for (auto& x : rr) slots += x.second - x.first;
+    return slots;
+  };
+  std::vector<int32_t> tiles, runs, cruns;
+  std::vector<uint8_t> recs((size_t)np * rb + 64, 0);
+  std::vector<int> vid, cid;
+  std::vector<std::pair<int, int>> rr, cr;
+  auto slot_in = [](const std::vector<std::pair<int, int>>& R, const std::vector<int>& base, int v) {
+    size_t k = std::upper_bound(R.begin(), R.end(), std::make_pair(v, INT32_MAX)) - R.begin() - 1;
+    return base[k] + v - R[k].first;
+  };
+  int r0 = 0;
+  while (r0 < nrows_node) {
+    int r1 = std::min(nrows_node, r0 + sp.tile_rows);
+    auto fits = [&](int a, int b, int& slots, int& cslots) {
+      if (ncn && (hn[b] - hn[a]) * W > sp.tile_seg) return false;
+      if (hp[b] - hp[a] > sp.tile_pairs) return false;
+      vid.clear();
+      cid.clear();
+      for (int p = hp[a]; p < hp[b]; ++p) {
+        const int c = hpairs[p] / nrn;
+        for (int v = 0; v < nv; ++v) vid.push_back(hx[(size_t)c * nv + v]);
+        for (int q = 0; q < ncf; ++q) cid.push_back(hcf[(size_t)c * ncf + q]);
+      }
+      slots = make_runs(vid, nverts, rr);
+      cslots = ncf ? make_runs(cid, ncoeff_nodes, cr) : 0;
+      return slots <= sp.tile_slots && (int)rr.size() <= sp.tile_runs && cslots <= sp.tile_slots &&
+             (int)cr.size() <= sp.tile_runs;
+    };
+    int slots = 0, cslots = 0;
+    while (!fits(r0, r1, slots, cslots)) {
+      if (r1 == r0 + 1) return false;
+      r1 = r0 + (r1 - r0) / 2;
+    }
+    std::vector<int> base(rr.size()), cbase(cr.size());
+    for (size_t k = 0, acc = 0; k < rr.size(); ++k) {
+      base[k] = (int)acc;
+      acc += rr[k].second - rr[k].first;
+    }
+    for (size_t k = 0, acc = 0; k < cr.size(); ++k) {
+      cbase[k] = (int)acc;
+      acc += cr[k].second - cr[k].first;
+    }
+    for (int r = r0; r < r1; ++r)
+      for (int p = hp[r]; p < hp[r + 1]; ++p) {
+        const int code = hpairs[p], c = code / nrn, i = code - c * nrn;
+        int sigma[4], inv[4], rowpos[10], colpos[10];
+        const int ci = canonical_sigma(gd, nrn, i, sigma);
+        for (int v = 0; v < nv; ++v) inv[sigma[v]] = v;
+        uint8_t* rec = &recs[(size_t)p * rb];
+        for (int k = 0; k < nv; ++k) { // permuted vertex k = original vertex inv[k]
+          const uint16_t sl = (uint16_t)slot_in(rr, base, hx[(size_t)c * nv + inv[k]]);
+          memcpy(rec + 2 * k, &sl, 2);
+        }
+        if (ncf) {
+          induced(gd, ncf, sigma, colpos);
+          for (int q = 0; q < ncf; ++q) {
+            const uint16_t sl = (uint16_t)slot_in(cr, cbase, hcf[(size_t)c * ncf + q]);
+            memcpy(rec + off_cf + 2 * colpos[q], &sl, 2);
+          }
+        }
+        if (ncn) {
+          induced(gd, ncn, sigma, colpos);
+          for (int j = 0; j < ncn; ++j) rec[off_rk + colpos[j]] = hrank[(size_t)p * ncn + j];
+        }
+        (void)rowpos;
+        rec[off_ci] = (uint8_t)ci;
+      }
+    // thread group per row: the G lanes of a row take interleaved pairs, so a
+    // tile of few long rows (P2 vertex rows: 24 cells) still fills the CTA
+    int maxp = 0, G = 1;
+    for (int r = r0; r < r1; ++r) maxp = std::max(maxp, hp[r + 1] - hp[r]);
+    while (G < 8 && (r1 - r0) * G * 2 <= sp.tile_rows && G * 4 <= maxp) G *= 2;
+    tiles.insert(tiles.end(), {r0, r1, (int)hn[r0], (int)hn[r1], hp[r0], hp[r1], (int)runs.size() / 2,
+                               (int)rr.size(), (int)cruns.size() / 2, (int)cr.size(), G, 0});
+    for (auto& x : rr) runs.insert(runs.end(), {x.first, x.second});
+    for (auto& x : cr) cruns.insert(cruns.end(), {x.first, x.second});
+    out.max_rows = std::max(out.max_rows, r1 - r0);
+    out.max_pairs = std::max(out.max_pairs, hp[r1] - hp[r0]);
+    out.max_seg = std::max<int>(out.max_seg, (int)((hn[r1] - hn[r0]) * W));
+    out.max_slots = std::max(out.max_slots, slots);
+    out.max_cslots = std::max(out.max_cslots, cslots);
+    r0 = r1;
+  }
+  out.ntiles = (int)tiles.size() / 12;
+  std::vector<int32_t> pp32(hp.begin(), hp.end()), nn32(hn.begin(), hn.end());
+  pp32.resize(pp32.size() + 8, 0);
+  nn32.resize(nn32.size() + 8, 0);
+  out.pptr.alloc(pp32.size(), s);
+  out.nptr.alloc(nn32.size(), s);
+  out.recs.alloc(recs.size(), s);
+  out.runs.alloc(runs.size() + 2, s);
+  out.cruns.alloc(cruns.size() + 2, s);
+  out.tiles.alloc(tiles.size() + 12, s);
+  LG_CUDA(cudaMemcpyAsync(out.pptr.get(), pp32.data(), sizeof(int32_t) * pp32.size(), cudaMemcpyHostToDevice, s));
+  LG_CUDA(cudaMemcpyAsync(out.nptr.get(), nn32.data(), sizeof(int32_t) * nn32.size(), cudaMemcpyHostToDevice, s));
+  LG_CUDA(cudaMemcpyAsync(out.recs.get(), recs.data(), recs.size(), cudaMemcpyHostToDevice, s));
+  if (!runs.empty())
+    LG_CUDA(cudaMemcpyAsync(out.runs.get(), runs.data(), sizeof(int32_t) * runs.size(), cudaMemcpyHostToDevice, s));
+  if (!cruns.empty())
+    LG_CUDA(cudaMemcpyAsync(out.cruns.get(), cruns.data(), sizeof(int32_t) * cruns.size(), cudaMemcpyHostToDevice, s));
+  LG_CUDA(cudaMemcpyAsync(out.tiles.get(), tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice, s));
   LG_CUDA(cudaStreamSynchronize(s));
   return true;
 }

@@ -113,6 +113,34 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
                const CsrView& csr, int tile_rows, int tile_seg, int tile_slots, int tile_runs,
                cudaStream_t s);
 
+// Canonical pair-tile plan (any catalogue form on simplices).  Each pair
+// (row node r, cell e) is stored with the cell's local numbering PERMUTED so
+// that r is a canonical local node (vertex rows: local vertex 0; P2 edge rows:
+// the first local edge), making the element row a compile-time index.  Record
+// (rec_bytes each): u16 window slots of the permuted vertices [GD+1], then
+// u16 coefficient window slots [NCOEFF] (actions), then u8 in-row ranks of the
+// permuted column nodes [NCN] (matrices), then u8 canonical index.
+struct PTilePlan {
+  int nrows_node = 0, rec_bytes = 0, ntiles = 0;
+  int max_rows = 0, max_pairs = 0, max_seg = 0, max_slots = 0, max_cslots = 0;
+  DevBuf<int32_t> pptr;   // pair offsets per row [nrows_node + 1] (+pad)
+  DevBuf<int32_t> nptr;   // node-level pattern offsets [nrows_node + 1] (+pad)
+  DevBuf<uint8_t> recs;   // npairs * rec_bytes (+pad)
+  DevBuf<int32_t> runs;   // coordinate-window runs
+  DevBuf<int32_t> cruns;  // coefficient-window runs
+  DevBuf<int32_t> tiles;  // 12 ints per tile: R0,R1,A0,A1,P0,P1,run_off,run_cnt,crun_off,crun_cnt,0,0
+};
+struct PTileSpec {
+  int gd = 2, nrn = 3, ncn = 0, ncoeff = 0, rd = 1, cd = 1;
+  int tile_rows = 128, tile_seg = 4096, tile_pairs = 2048, tile_slots = 1024, tile_runs = 48;
+};
+// sorted_* are node-level maps in the locality order; pp holds the pairs and
+// (for matrices) the ranks of the column nodes; csr the Mat pattern (matrices).
+// Returns false when a tile limit cannot be met (caller falls back).
+bool build_ptile(PTilePlan& out, const PTileSpec& sp, int ncells, int nrows_node, const int32_t* sorted_rows,
+                 const int32_t* sorted_cols, const int32_t* sorted_x, int nverts, const int32_t* sorted_coeff,
+                 int ncoeff_nodes, const PairPlan& pp, const CsrView& csr, cudaStream_t s);
+
 // build_sparsity (data.hpp:149-179) on the device, bit-exact.
 void build_sparsity_dev(const MapView& rows, const MapView& cols, int rd, int cd,
                         int64_t** row_ptr, int32_t** col_idx, int64_t* nnz, cudaStream_t s);
