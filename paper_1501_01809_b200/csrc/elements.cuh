@@ -263,6 +263,7 @@ template <int FORM, int D, int P>
 struct ScalarBilinear {
   static constexpr int N = Lagrange<D, P>::N;
   static constexpr int NR = N, NC = N, NRN = N, NCN = N, RD = 1, CD = 1, GD = D;
+  static constexpr int ID = FORM, DEG = P;
   static constexpr bool HAS_COEFF = false, BILINEAR = true;
   static constexpr int NCOEFF = 0;
   __device__ __forceinline__ static void row(int i, const Geom<D>& G, const double*,
@@ -302,6 +303,7 @@ template <int FORM, int D, int P>
 struct ScalarAction {
   static constexpr int N = Lagrange<D, P>::N;
   static constexpr int NR = N, NC = 1, NRN = N, NCN = 0, RD = 1, CD = 1, GD = D;
+  static constexpr int ID = FORM, DEG = P;
   static constexpr bool HAS_COEFF = true, BILINEAR = false;
   static constexpr int NCOEFF = N;
   __device__ __forceinline__ static void row(int i, const Geom<D>& G, const double* C,

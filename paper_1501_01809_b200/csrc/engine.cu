@@ -445,14 +445,18 @@ struct RunSet {
   double* dst;
   int es;
 };
+// `first`: the lane's run of the first chunk, prefetched by the caller.
+__device__ __forceinline__ int2 first_run(const int2* runs, int cnt, int lane) {
+  return lane < cnt ? __ldg(runs + lane) : make_int2(0, 0);
+}
 template <bool ISSUE>
-__device__ __forceinline__ uint32_t stage_runs(const RunSet& s, int lane, uint64_t* bar) {
+__device__ __forceinline__ uint32_t stage_runs(const RunSet& s, int lane, uint64_t* bar, int2 first) {
   uint32_t tx = 0;
   int base = 0;
   for (int r0 = 0; r0 < s.cnt; r0 += 32) {
-    int lo = 0, hi = 0;
-    if (r0 + lane < s.cnt) {
-      const int2 p = __ldg(s.runs + r0 + lane);
+    int lo = first.x, hi = first.y;
+    if (r0 > 0) {
+      const int2 p = r0 + lane < s.cnt ? __ldg(s.runs + r0 + lane) : make_int2(0, 0);
       lo = p.x;
       hi = p.y;
     }
@@ -752,11 +756,62 @@ struct RingArgs {
   FormParams prm;
   double* out;
   int accumulate;
-  int off_seg, off_buf, buf_bytes;
+  int off_seg, seg_stride, off_buf, buf_bytes; // seg_stride: doubles in the segment buffer
   int b_nptr, b_rptr, b_recs, b_info, b_win, b_winc;
+  unsigned long long* timing; // LOAM_GPU_PHASE_TIMING: [first wait, waits, compute, tiles] in cycles
 };
 
+// One ring cell (s, p, n) of a P1 triangle form seen from the row vertex s,
+// in closed form from the edge vectors a = x_p - x_s, b = x_n - x_s
+// (aa = a.a, ab = a.b, bb = b.b, ad = |a x b| = 2 |T|):
+//   K_sp = (ab - bb) / (2 ad),  K_sn = (ab - aa) / (2 ad),  K_ss = -(K_sp + K_sn)
+//   M_ss = ad / 12,             M_sp = M_sn = ad / 24
+// -- the same entries elements.cuh's barycentric-gradient row produces
+// (cotangent form of grad l_i . grad l_j |T|; P1 mass |T|/12 (1 + delta_ij)),
+// at a third of the arithmetic: b.b of one cell is a.a of the next.
 template <class F>
+struct RingCell {
+  static constexpr int ID = F::ID;
+  static constexpr bool K = ID != F_MASS && ID != F_MASS_ACTION;
+  static constexpr bool M = ID != F_STIFFNESS && ID != F_STIFFNESS_ACTION;
+  // bilinear: the s-row entries for s, p, n
+  __device__ __forceinline__ static void entries(double aa, double ab, double bb, double ad, double kappa,
+                                                 double& vs, double& vp, double& vn) {
+    double kp = 0.0, kn = 0.0;
+    if constexpr (K) {
+      const double r = 0.5 * fast_rcp(ad);
+      kp = (ab - bb) * r;
+      kn = (ab - aa) * r;
+    }
+    if constexpr (!M) {
+      vp = kp;
+      vn = kn;
+      vs = -(kp + kn);
+    } else {
+      const double m = ad * (1.0 / 24.0);
+      const double km = K ? kappa * m : m;
+      vp = kp + km;
+      vn = kn + km;
+      vs = K ? fma(2.0, km, -(kp + kn)) : 2.0 * m;
+    }
+  }
+  // action: sum_j A_sj u_j
+  __device__ __forceinline__ static double action(double aa, double ab, double bb, double ad, double kappa,
+                                                  double us, double up, double un) {
+    double v = 0.0;
+    if constexpr (K) {
+      const double r = 0.5 * fast_rcp(ad);
+      v = ((ab - bb) * (up - us) + (ab - aa) * (un - us)) * r;
+    }
+    if constexpr (M) {
+      const double m = ad * (1.0 / 24.0) * (2.0 * us + up + un);
+      v = K ? fma(kappa, m, v) : m;
+    }
+    return v;
+  }
+};
+
+template <class F, bool ACC>
 __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ RingArgs a) {
   static_assert(F::GD == 2 && F::NRN == 3, "ring kernel: P1 triangles");
   extern __shared__ __align__(128) unsigned char sm[];
@@ -774,18 +829,42 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
   }
   __syncthreads();
   auto tile_meta = [&](int tile, int (&m)[8]) {
-    const int4* t = reinterpret_cast<const int4*>(a.tiles + 8 * tile);
+    const int4* t = reinterpret_cast<const int4*>(a.tiles + 16 * tile);
     const int4 x = __ldg(t), y = __ldg(t + 1);
     m[0] = x.x; m[1] = x.y; m[2] = x.z; m[3] = x.w; m[4] = y.x; m[5] = y.y; m[6] = y.z; m[7] = y.w;
   };
   auto ring = [&](int k) { return sm + a.off_buf + (k % 3) * a.buf_bytes; };
-  if (tid >= kTileThreads) { // ---- producer warp: grabs tiles dynamically
+  if (tid >= kTileThreads) { // ---- producer warp
+    // Tiles: the first three of each CTA are static (blockIdx + k * grid), the
+    // rest come from the dynamic counter.  A tile's meta and its first window
+    // runs share one 64-byte record (plan.cu, kRingInlineRuns), and the next
+    // tile is fetched while the current stage drains, so a freed stage waits
+    // only for its bulk copies.
     const int lane = tid & 31;
+    auto grab = [&](int k) {
+      if (k < 3) return (int)(blockIdx.x + k * gridDim.x);
+      int t = 0;
+      if (lane == 0) t = 3 * gridDim.x + atomicAdd(a.next_tile, 1);
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    auto fetch = [&](int tile, int (&mm)[8], int2& run) {
+      tile_meta(tile, mm);
+      int2 inl = make_int2(0, 0);
+      if (lane < kRingInlineRuns) inl = __ldg(reinterpret_cast<const int2*>(a.tiles + 16 * tile + 8) + lane);
+      const int cnt = mm[7];
+      run = lane < cnt ? (lane < kRingInlineRuns ? inl : __ldg(reinterpret_cast<const int2*>(a.runs) + mm[6] + lane))
+                       : make_int2(0, 0);
+    };
+    int nt = grab(0), nm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int2 nrun = make_int2(0, 0);
+    if (nt < a.ntiles) fetch(nt, nm, nrun);
     for (int k = 0;; ++k) {
+      const int tile = nt;
+      int m[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) m[q] = nm[q];
+      const int2 run0 = nrun;
       if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
-      int tile = 0;
-      if (lane == 0) tile = atomicAdd(a.next_tile, 1);
-      tile = __shfl_sync(0xffffffffu, tile, 0);
       if (tile >= a.ntiles) { // publish "no more tiles" through the stage
         if (lane == 0) {
           slot_tile[k % 3] = -1;
@@ -794,8 +873,6 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
         break;
       }
       if (lane == 0) slot_tile[k % 3] = tile;
-      int m[8];
-      tile_meta(tile, m);
       unsigned char* buf = ring(k);
       uint64_t* bar = &full[k % 3];
       auto rb = [](int lo, int hi, int es, int64_t& s0) {
@@ -809,7 +886,8 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
                       reinterpret_cast<double*>(buf + a.b_win), 2};
       const RunSet rk{reinterpret_cast<const int2*>(a.runs) + m[6], F::HAS_COEFF ? m[7] : 0, a.coeff,
                       reinterpret_cast<double*>(buf + a.b_winc), 1};
-      const uint32_t tx = n0 + n1 + n2 + n3 + stage_runs<false>(rc, lane, bar) + stage_runs<false>(rk, lane, bar);
+      const uint32_t tx = n0 + n1 + n2 + n3 + stage_runs<false>(rc, lane, bar, run0) +
+                          stage_runs<false>(rk, lane, bar, run0);
       fence_async_shared();
       __syncwarp();
       if (lane == 0) {
@@ -820,23 +898,41 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
         if (n3) bulk_g2s(buf + a.b_info, reinterpret_cast<const unsigned char*>(a.rowinfo) + g3, n3, bar);
       }
       __syncwarp();
-      stage_runs<true>(rc, lane, bar);
-      stage_runs<true>(rk, lane, bar);
+      stage_runs<true>(rc, lane, bar, run0);
+      stage_runs<true>(rk, lane, bar, run0);
+      nt = grab(k + 1);
+      if (nt < a.ntiles) fetch(nt, nm, nrun);
     }
     return;
   }
   // ---- consumers: one thread per row vertex
   double* seg = reinterpret_cast<double*>(sm + a.off_seg);
+  const double kappa = a.prm.p[0];
+  const long long t_start = clock64();
+  long long t_first = 0, t_wait = 0, t_comp = 0, t_n = 0, t_early = 0, t_last = 0;
   for (int k = 0;; ++k) {
+    const long long c0 = a.timing ? clock64() : 0;
     mbar_wait(&full[k % 3], (k / 3) & 1);
+    const long long c1 = a.timing ? clock64() : 0;
     const int tile = slot_tile[k % 3];
+    if (a.timing) {
+      if (k == 0) t_first += c1 - c0;
+      else if (tile < 0) t_last += c1 - c0;
+      else if (k < 3) t_early += c1 - c0;
+      else t_wait += c1 - c0;
+    }
     if (tile < 0) break;
     int m[8];
     tile_meta(tile, m);
     const int R0 = m[0], nrows = m[1] - m[0], A0 = m[2], nA = m[3] - m[2], P0 = m[4];
+    // the segment, skewed so segb[t] and out[A0 + t] agree mod 16 bytes; the
+    // previous tile's bulk store must have finished reading it
+    double* segb = seg + (A0 & 1);
     if constexpr (F::BILINEAR) {
-      if (a.accumulate) {
-        for (int t = tid; t < nA; t += kTileThreads) seg[t] = a.out[(int64_t)A0 + t];
+      if (tid == 0) bulk_wait_read<0>();
+      named_bar(1, kTileThreads);
+      if constexpr (ACC) {
+        for (int t = tid; t < nA; t += kTileThreads) segb[t] = a.out[(int64_t)A0 + t];
         named_bar(1, kTileThreads);
       }
     }
@@ -852,72 +948,101 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
       const int self_slot = info & 0xffff, self_rank = (info >> 16) & 0xff;
       const int a0 = F::BILINEAR ? nptr_s[tid] - A0 : 0;
       const int q0 = rptr_s[tid] - P0, q1 = rptr_s[tid + 1] - P0;
-      const double2 xs = win[self_slot];
-      const double cs = F::HAS_COEFF ? winc[self_slot] : 0.0;
-      const uint32_t h = rec_s[q0];
-      const int rk0 = h & 7;
-      double2 xp = win[h >> 3];
-      double cp = F::HAS_COEFF ? winc[h >> 3] : 0.0;
-      int rkp = rk0;
-      double diag = 0.0, first = 0.0, carry = 0.0, acc = 0.0;
+      double* row = segb + a0;
       auto put = [&](int rank, double v) {
-        if (a.accumulate) seg[a0 + rank] += v;
-        else seg[a0 + rank] = v;
+        if constexpr (ACC) row[rank] += v;
+        else row[rank] = v;
       };
-      // software pipeline: the record and vertex of cell q+1 are loaded before
-      // cell q is computed
-      uint32_t r_nx = rec_s[q0 + 1 < q1 ? q0 + 1 : q0];
-      double2 x_nx = win[r_nx >> 3];
-      double c_nx = F::HAS_COEFF ? winc[r_nx >> 3] : 0.0;
-      for (int q = q0 + 1; q < q1; ++q) {
-        const uint32_t r = r_nx;
-        const double2 xn = x_nx;
-        const double cn = c_nx;
-        if (q + 1 < q1) {
-          r_nx = rec_s[q + 1];
-          x_nx = win[r_nx >> 3];
-          if constexpr (F::HAS_COEFF) c_nx = winc[r_nx >> 3];
-        }
-        const double X[3][2] = {{xs.x, xs.y}, {xp.x, xp.y}, {xn.x, xn.y}};
-        Geom<2> G;
-        geometry<2>(X, G);
-        if constexpr (F::BILINEAR) {
-          double blk[3];
-          F::row(0, G, nullptr, a.prm, blk);
-          diag += blk[0];
-          if (q == q0 + 1) first = blk[1];
-          else put(rkp, carry + blk[1]);
-          carry = blk[2];
-        } else {
-          const double C[3] = {cs, cp, cn};
-          double v;
-          F::row(0, G, C, a.prm, &v);
-          acc += v;
-        }
-        xp = xn;
-        cp = cn;
-        rkp = r & 7;
+      const double2 xs = win[self_slot];
+      const double us = F::HAS_COEFF ? winc[self_slot] : 0.0;
+      // chain vertex 0 (a row with no cell has q1 == q0 + 1 and no pair)
+      const uint32_t h0 = rec_s[q0];
+      const int rk0 = h0 & 7;
+      double2 ea;
+      {
+        const double2 x = win[h0 >> 3];
+        ea = make_double2(x.x - xs.x, x.y - xs.y);
       }
-      if constexpr (F::BILINEAR) {
-        if (q1 - q0 > 1) {
+      double aa = ea.x * ea.x + ea.y * ea.y;
+      double up = F::HAS_COEFF ? winc[h0 >> 3] : 0.0;
+      double diag = 0.0, first = 0.0, carry = 0.0, acc = 0.0;
+      int rkp = rk0;
+      // one cell: (s, previous chain vertex, chain vertex q)
+      auto cell = [&](uint32_t r, double& vp, double& vn) {
+        const double2 x = win[r >> 3];
+        const double2 eb = make_double2(x.x - xs.x, x.y - xs.y);
+        const double bb = eb.x * eb.x + eb.y * eb.y;
+        const double ab = ea.x * eb.x + ea.y * eb.y;
+        const double ad = fabs(ea.x * eb.y - ea.y * eb.x);
+        if constexpr (F::BILINEAR) {
+          double vs;
+          RingCell<F>::entries(aa, ab, bb, ad, kappa, vs, vp, vn);
+          diag += vs;
+        } else {
+          const double un = winc[r >> 3];
+          acc += RingCell<F>::action(aa, ab, bb, ad, kappa, us, up, un);
+          up = un;
+        }
+        ea = eb;
+        aa = bb;
+      };
+      if (q1 - q0 > 1) {
+        double vp, vn;
+        uint32_t r = rec_s[q0 + 1];
+        cell(r, first, carry);
+        rkp = r & 7;
+#pragma unroll 2
+        for (int q = q0 + 2; q < q1; ++q) {
+          r = rec_s[q];
+          cell(r, vp, vn);
+          if constexpr (F::BILINEAR) put(rkp, carry + vp);
+          carry = vn;
+          rkp = r & 7;
+        }
+        if constexpr (F::BILINEAR) {
           if (rkp == rk0) put(rk0, first + carry); // closed ring
           else {
             put(rk0, first);
             put(rkp, carry);
           }
         }
-        put(self_rank, diag);
-      } else {
-        a.out[R0 + tid] = a.accumulate ? a.out[R0 + tid] + acc : acc;
       }
+      if constexpr (F::BILINEAR) put(self_rank, diag);
+      else a.out[R0 + tid] = ACC ? a.out[R0 + tid] + acc : acc;
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[k % 3]);
     if constexpr (F::BILINEAR) {
-      named_bar(1, kTileThreads); // segment complete
-      for (int t = tid; t < nA; t += kTileThreads) a.out[(int64_t)A0 + t] = seg[t];
+      // segment complete -> one bulk store (head / tail doubles off the
+      // 16-byte grid stored directly)
+      fence_async_shared();
       named_bar(1, kTileThreads);
+      if (tid == 0) {
+        double* dst = a.out + A0;
+        const int h = A0 & 1, t1 = nA - ((A0 + nA) & 1);
+        if (h && nA > 0) dst[0] = segb[0];
+        if (t1 > h) {
+          bulk_s2g(dst + h, segb + h, (uint32_t)(t1 - h) * 8);
+          bulk_commit();
+        }
+        if (t1 < nA && t1 >= h) dst[t1] = segb[t1];
+      }
     }
+    if (a.timing) {
+      t_comp += clock64() - c1;
+      ++t_n;
+    }
+  }
+  if (F::BILINEAR && tid == 0) bulk_wait<0>();
+  if (a.timing && (tid & 31) == 0) {
+    atomicAdd(a.timing, (unsigned long long)t_first);
+    atomicAdd(a.timing + 1, (unsigned long long)t_wait);
+    atomicAdd(a.timing + 2, (unsigned long long)t_comp);
+    atomicAdd(a.timing + 3, (unsigned long long)t_n);
+    atomicAdd(a.timing + 4, 1ull);
+    atomicAdd(a.timing + 5, (unsigned long long)t_early);
+    atomicAdd(a.timing + 6, (unsigned long long)t_last);
+    atomicAdd(a.timing + 7, (unsigned long long)(clock64() - t_start));
   }
 }
 
@@ -926,14 +1051,16 @@ void launch_ring(const RingArgs& a, size_t smem, cudaStream_t s) {
   if constexpr (F::GD == 2 && F::NRN == 3 && F::RD == 1 && F::CD == 1) {
     if (a.ntiles == 0) return;
     static size_t attr = 0;
+    auto kern = a.accumulate ? k_ring<F, true> : k_ring<F, false>;
     if (attr < smem) {
-      LG_CUDA(cudaFuncSetAttribute(k_ring<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      LG_CUDA(cudaFuncSetAttribute(k_ring<F, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      LG_CUDA(cudaFuncSetAttribute(k_ring<F, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr = smem;
     }
     int blocks = 1;
-    LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_ring<F>, kTileBlock, smem));
+    LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kTileBlock, smem));
     const int grid = std::min(a.ntiles, std::max(blocks, 1) * kNumSMs);
-    k_ring<F><<<grid, kTileBlock, smem, s>>>(a);
+    kern<<<grid, kTileBlock, smem, s>>>(a);
     count_launch();
     LG_LAUNCH_CHECK();
   } else {
@@ -1003,13 +1130,30 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
     m[8] = z.x; m[9] = z.y; m[10] = z.z; m[11] = z.w;
   };
   auto ring = [&](int k) { return sm + a.off_buf + (k % 3) * a.buf_bytes; };
-  if (tid >= NT) { // ---- producer warp (warp-cooperative run staging)
+  if (tid >= NT) { // ---- producer warp (software-pipelined as in k_ring)
     const int lane = tid & 31;
+    auto grab = [&]() {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(a.next_tile, 1);
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    int nt = grab(), nm[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int2 nrun = make_int2(0, 0), ncrun = make_int2(0, 0);
+    auto prefetch = [&]() {
+      if (nt < a.ntiles) {
+        tile_meta(nt, nm);
+        nrun = first_run(reinterpret_cast<const int2*>(a.runs) + nm[6], nm[7], lane);
+        if constexpr (F::HAS_COEFF) ncrun = first_run(reinterpret_cast<const int2*>(a.cruns) + nm[8], nm[9], lane);
+      }
+    };
+    prefetch();
     for (int k = 0;; ++k) {
+      const int tile = nt;
+      int m[12];
+#pragma unroll
+      for (int q = 0; q < 12; ++q) m[q] = nm[q];
+      const int2 run0 = nrun, crun0 = ncrun;
       if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
-      int tile = 0;
-      if (lane == 0) tile = atomicAdd(a.next_tile, 1);
-      tile = __shfl_sync(0xffffffffu, tile, 0);
       if (tile >= a.ntiles) {
         if (lane == 0) {
           slot_tile[k % 3] = -1;
@@ -1018,8 +1162,6 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
         break;
       }
       if (lane == 0) slot_tile[k % 3] = tile;
-      int m[12];
-      tile_meta(tile, m);
       unsigned char* buf = ring(k);
       uint64_t* bar = &full[k % 3];
       auto rb = [](int64_t lo_b, int64_t hi_b, int64_t& s0) {
@@ -1034,7 +1176,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
                       reinterpret_cast<double*>(buf + a.b_win), GD};
       const RunSet rk{reinterpret_cast<const int2*>(a.cruns) + m[8], F::HAS_COEFF ? m[9] : 0, a.coeff,
                       reinterpret_cast<double*>(buf + a.b_winc), 1};
-      const uint32_t tx = n0 + n1 + n2 + stage_runs<false>(rc, lane, bar) + stage_runs<false>(rk, lane, bar);
+      const uint32_t tx = n0 + n1 + n2 + stage_runs<false>(rc, lane, bar, run0) + stage_runs<false>(rk, lane, bar, crun0);
       fence_async_shared();
       __syncwarp();
       if (lane == 0) {
@@ -1044,8 +1186,10 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
         if (n2) bulk_g2s(buf + a.b_recs, a.recs + g2, n2, bar);
       }
       __syncwarp();
-      stage_runs<true>(rc, lane, bar);
-      stage_runs<true>(rk, lane, bar);
+      stage_runs<true>(rc, lane, bar, run0);
+      stage_runs<true>(rk, lane, bar, crun0);
+      nt = grab();
+      prefetch();
     }
     return;
   }
@@ -1706,7 +1850,8 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     auto up16 = [](int x) { return (x + 15) & ~15; };
     int off = 128; // 6 mbarriers + 3 stage tile ids
     t.off_seg = off;
-    off += up16(k.bilinear ? nb.max_seg * 8 : 0);
+    t.seg_stride = k.bilinear ? up16((nb.max_seg + 2) * 8) / 8 : 0;
+    off += t.seg_stride * 8;
     t.off_buf = off;
     int b = 0;
     t.b_nptr = b;
@@ -1723,7 +1868,23 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     b += up16(k.has_coeff ? nb.max_slots * 8 : 0);
     t.buf_bytes = b;
     off += 3 * b;
+    static const bool timing = std::getenv("LOAM_GPU_PHASE_TIMING") != nullptr;
+    DevBuf<unsigned long long> tbuf;
+    if (timing) {
+      tbuf.alloc(8, s);
+      LG_CUDA(cudaMemsetAsync(tbuf.get(), 0, tbuf.bytes(), s));
+      t.timing = tbuf.get();
+    }
     k.ring(t, (size_t)off, s);
+    if (timing) {
+      unsigned long long h[8];
+      LG_CUDA(cudaMemcpyAsync(h, tbuf.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+      LG_CUDA(cudaStreamSynchronize(s));
+      const double nw = std::max(1.0, (double)h[4]), nt = std::max(1.0, (double)h[3]);
+      fprintf(stderr, "[ring timing] cycles per consumer warp: total %.0f = first wait %.0f + stage 1-2 waits %.0f + "
+              "steady waits %.0f + final wait %.0f + compute %.0f (%.1f tiles/warp; tiles %d, warps %.0f, smem %d B)\n",
+              h[7] / nw, h[0] / nw, h[5] / nw, h[1] / nw, h[6] / nw, h[2] / nw, nt / nw, nb.ntiles, nw, off);
+    }
     return;
   }
   if (P->use_ptile) {

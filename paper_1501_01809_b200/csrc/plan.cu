@@ -489,12 +489,22 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
       LG_CUDA(cudaMemcpyAsync(np.rptr.get(), rptr.data(), sizeof(int32_t) * rptr.size(), cudaMemcpyHostToDevice, s));
       LG_CUDA(cudaMemcpyAsync(np.rrecs.get(), rrec.data(), sizeof(uint16_t) * rrec.size(), cudaMemcpyHostToDevice, s));
       LG_CUDA(cudaMemcpyAsync(np.rowinfo.get(), rinfo.data(), sizeof(uint32_t) * rinfo.size(), cudaMemcpyHostToDevice, s));
-      std::vector<int32_t> rt(tiles);
-      for (size_t t = 0; t < rt.size() / 8; ++t) {
-        rt[8 * t + 4] = rptr[rt[8 * t + 0]];
-        rt[8 * t + 5] = rptr[rt[8 * t + 1]];
+      // ring tiles: 16 ints -- the 8 tile fields (P0/P1 in ring-record units)
+      // followed by the first kRingInlineRuns window runs, so a producer gets a
+      // tile's meta and runs from one 64-byte line with no dependent load
+      const size_t nt = tiles.size() / 8;
+      std::vector<int32_t> rt(nt * 16, 0);
+      for (size_t t = 0; t < nt; ++t) {
+        for (int q = 0; q < 8; ++q) rt[16 * t + q] = tiles[8 * t + q];
+        rt[16 * t + 4] = rptr[tiles[8 * t + 0]];
+        rt[16 * t + 5] = rptr[tiles[8 * t + 1]];
+        const int ro = tiles[8 * t + 6], rc = tiles[8 * t + 7];
+        for (int q = 0; q < std::min(rc, kRingInlineRuns); ++q) {
+          rt[16 * t + 8 + 2 * q] = runs[2 * (ro + q)];
+          rt[16 * t + 9 + 2 * q] = runs[2 * (ro + q) + 1];
+        }
       }
-      np.rtiles.alloc(rt.size() ? rt.size() : 8, s);
+      np.rtiles.alloc(rt.size() ? rt.size() : 16, s);
       if (!rt.empty())
         LG_CUDA(cudaMemcpyAsync(np.rtiles.get(), rt.data(), sizeof(int32_t) * rt.size(), cudaMemcpyHostToDevice, s));
       np.max_pairs += np.max_rows; // ring records per tile: pairs + one head per row

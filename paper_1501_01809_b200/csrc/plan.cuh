@@ -80,6 +80,8 @@ void build_chunks(PairPlan& pp, const CsrView& csr, int smax, int max_rows, cuda
 // cell-neighbour nodes, so a pair needs only (local index | in-row ranks of the
 // cell's nodes) -- a 16/32-bit record -- and the kernel gathers each chunk's
 // neighbour coordinates once instead of per pair.
+constexpr int kRingInlineRuns = 4; // window runs stored inside a ring tile record
+
 struct NbrPlan {
   int nrows_node = 0, nrn = 0, bits = 0, rec_bytes = 4, rd = 1, cd = 1;
   // plan-owned, 16-byte padded arrays; the tile kernel TMA-loads tile ranges of them
@@ -101,7 +103,7 @@ struct NbrPlan {
   DevBuf<int32_t> rptr;      // [nrows_node + 1] record offsets (pptr[r] + r)
   DevBuf<uint16_t> rrecs;    // chain records
   DevBuf<uint32_t> rowinfo;  // self window slot | self rank << 16
-  DevBuf<int32_t> rtiles;    // tiles with P0/P1 in ring-record units
+  DevBuf<int32_t> rtiles;    // 16-int ring tiles: P0/P1 in ring-record units + inline runs
 };
 // Build from a (sorted) node-level map and a node-level pattern.  For Mats the
 // pattern is the Mat's sparsity (csr, possibly blocked by rd/cd); for Dats
