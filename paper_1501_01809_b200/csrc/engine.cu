@@ -936,6 +936,7 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
         named_bar(1, kTileThreads);
       }
     }
+    const long long c1b = a.timing ? clock64() : 0;
     const unsigned char* buf = ring(k);
     const int32_t* nptr_s = reinterpret_cast<const int32_t*>(buf + a.b_nptr) + skew_of(R0, 4);
     const int32_t* rptr_s = reinterpret_cast<const int32_t*>(buf + a.b_rptr) + skew_of(R0, 4);
@@ -1011,6 +1012,7 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
       else a.out[R0 + tid] = ACC ? a.out[R0 + tid] + acc : acc;
     }
     __syncwarp();
+    const long long c1c = a.timing ? clock64() : 0;
     if ((tid & 31) == 0) mbar_arrive(&empty[k % 3]);
     if constexpr (F::BILINEAR) {
       // segment complete -> one bulk store (head / tail doubles off the
@@ -1029,11 +1031,22 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
       }
     }
     if (a.timing) {
-      t_comp += clock64() - c1;
+      const long long c2 = clock64();
+      t_comp += c2 - c1;
       ++t_n;
+      if (tid == 0 && tile < 16384) { // per-tile record (warp 0): wait | start barrier, rows, end (16 bits each)
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.timing[16 + 4 * 2048 + 2 * tile] = (unsigned long long)(c1 - c0) | ((unsigned long long)blockIdx.x << 32) |
+                                            ((unsigned long long)smid << 48) | ((unsigned long long)(k & 15) << 60);
+        a.timing[17 + 4 * 2048 + 2 * tile] = (unsigned long long)(c1b - c1) | ((unsigned long long)(c1c - c1b) << 20) |
+                                            ((unsigned long long)(c2 - c1c) << 40);
+      }
     }
   }
-  if (F::BILINEAR && tid == 0) bulk_wait<0>();
+  // the segment must outlive its bulk store's shared-memory reads; the global
+  // writes themselves complete with the grid
+  if (F::BILINEAR && tid == 0) bulk_wait_read<0>();
   if (a.timing && (tid & 31) == 0) {
     atomicAdd(a.timing, (unsigned long long)t_first);
     atomicAdd(a.timing + 1, (unsigned long long)t_wait);
@@ -1043,6 +1056,24 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
     atomicAdd(a.timing + 5, (unsigned long long)t_early);
     atomicAdd(a.timing + 6, (unsigned long long)t_last);
     atomicAdd(a.timing + 7, (unsigned long long)(clock64() - t_start));
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    atomicMax(a.timing + 9, gt);
+  }
+  if (a.timing && tid == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    const unsigned long long st = gt - (unsigned long long)((clock64() - t_start) / 2); // ~start (ns, 2 GHz)
+    atomicMin(a.timing + 8, st);
+    atomicAdd(a.timing + 10, (unsigned long long)(clock64() - t_start));
+    atomicMax(a.timing + 11, st);
+    atomicMin(a.timing + 12, gt);
+    a.timing[16 + 4 * blockIdx.x] = st;
+    a.timing[17 + 4 * blockIdx.x] = gt;
+    a.timing[18 + 4 * blockIdx.x] = t_n;
+    unsigned sm_id;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
+    a.timing[19 + 4 * blockIdx.x] = sm_id;
   }
 }
 
@@ -1871,19 +1902,35 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     static const bool timing = std::getenv("LOAM_GPU_PHASE_TIMING") != nullptr;
     DevBuf<unsigned long long> tbuf;
     if (timing) {
-      tbuf.alloc(8, s);
+      tbuf.alloc(16 + 4 * 2048 + 2 * 16384, s);
       LG_CUDA(cudaMemsetAsync(tbuf.get(), 0, tbuf.bytes(), s));
+      LG_CUDA(cudaMemsetAsync(tbuf.get() + 8, 0xff, 8, s));
+      LG_CUDA(cudaMemsetAsync(tbuf.get() + 12, 0xff, 8, s));
       t.timing = tbuf.get();
     }
     k.ring(t, (size_t)off, s);
     if (timing) {
-      unsigned long long h[8];
-      LG_CUDA(cudaMemcpyAsync(h, tbuf.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+      std::vector<unsigned long long> hv(16 + 4 * 2048 + 2 * 16384);
+      unsigned long long* h = hv.data();
+      LG_CUDA(cudaMemcpyAsync(h, tbuf.get(), sizeof(unsigned long long) * hv.size(), cudaMemcpyDeviceToHost, s));
       LG_CUDA(cudaStreamSynchronize(s));
+      if (const char* dump = std::getenv("LOAM_GPU_PHASE_DUMP")) {
+        FILE* f = fopen(dump, "w");
+        for (int b = 0; b < 2048 && h[17 + 4 * b]; ++b)
+          fprintf(f, "%d %.3f %.3f %llu %llu\n", b, (h[16 + 4 * b] - h[8]) * 1e-3, (h[17 + 4 * b] - h[8]) * 1e-3,
+                  h[18 + 4 * b], h[19 + 4 * b]);
+        fclose(f);
+        f = fopen((std::string(dump) + ".tiles").c_str(), "w");
+        for (int t = 0; t < std::min(nb.ntiles, 16384); ++t)
+          fprintf(f, "%d %llu %llu\n", t, h[16 + 4 * 2048 + 2 * t], h[17 + 4 * 2048 + 2 * t]);
+        fclose(f);
+      }
       const double nw = std::max(1.0, (double)h[4]), nt = std::max(1.0, (double)h[3]);
       fprintf(stderr, "[ring timing] cycles per consumer warp: total %.0f = first wait %.0f + stage 1-2 waits %.0f + "
               "steady waits %.0f + final wait %.0f + compute %.0f (%.1f tiles/warp; tiles %d, warps %.0f, smem %d B)\n",
               h[7] / nw, h[0] / nw, h[5] / nw, h[1] / nw, h[6] / nw, h[2] / nw, nt / nw, nb.ntiles, nw, off);
+      fprintf(stderr, "[ring timing] CTA starts span %.2f us, CTA ends from %.2f to %.2f us after the first start\n",
+              (double)(h[11] - h[8]) * 1e-3, (double)(h[12] - h[8]) * 1e-3, (double)(h[9] - h[8]) * 1e-3);
     }
     return;
   }
