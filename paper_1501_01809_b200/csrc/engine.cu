@@ -340,6 +340,66 @@ __global__ void __launch_bounds__(kTPB) k_owner_vec(const __grid_constant__ Owne
   a.out[r] = a.accumulate ? a.out[r] + acc : acc;
 }
 
+// Cell-centric action (Dat INC, the atomic strategy for catalogue actions):
+// one thread per cell in locality order (sorted maps: coalesced map rows),
+// the element vector in registers with compile-time rows -- each cell's
+// geometry is computed once, not once per row as the owner kernels must --
+// and one fp64 RED per entry (form.hpp:288-312 actions; parloop.hpp:302-338
+// INC scatter).
+struct CellArgs {
+  int n;
+  const int32_t* rmap; // sorted row map, NRN per cell
+  const int32_t* xmap; // sorted coordinate map rows
+  int xstride;
+  const int32_t* cmap; // sorted coefficient map rows
+  int cstride;
+  const double* coords;
+  const double* coeff;
+  FormParams prm;
+  double* out;
+};
+
+template <class F>
+__global__ void __launch_bounds__(128) k_cell_vec(const __grid_constant__ CellArgs a) {
+  constexpr int GD = F::GD, NV = GD + 1;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.n) return;
+  int vid[NV], rows[F::NRN];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) vid[v] = __ldg(a.xmap + (int64_t)e * a.xstride + v);
+#pragma unroll
+  for (int i = 0; i < F::NRN; ++i) rows[i] = __ldg(a.rmap + (int64_t)e * F::NRN + i);
+  double C[F::HAS_COEFF ? F::NCOEFF : 1];
+  if constexpr (F::HAS_COEFF)
+#pragma unroll
+    for (int q = 0; q < F::NCOEFF; ++q) C[q] = __ldg(a.coeff + __ldg(a.cmap + (int64_t)e * a.cstride + q));
+  double X[NV][GD];
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int c = 0; c < GD; ++c) X[v][c] = __ldg(a.coords + (int64_t)vid[v] * GD + c);
+  Geom<GD> G;
+  geometry<GD>(X, G);
+#pragma unroll
+  for (int i = 0; i < F::NRN; ++i) {
+    double v;
+    F::row(i, G, C, a.prm, &v);
+    atomicAdd(a.out + rows[i], v);
+  }
+}
+
+template <class F>
+void launch_cell(const CellArgs& a, cudaStream_t s) {
+  if constexpr (!F::BILINEAR) {
+    if (a.n == 0) return;
+    k_cell_vec<F><<<ceil_div(a.n, 128), 128, 0, s>>>(a);
+    count_launch();
+    LG_LAUNCH_CHECK();
+  } else {
+    fail(LOAM_ERR(InvalidArgument), "cell kernel: actions only");
+  }
+}
+
 // Matrix (Mat INC): one warp per chunk of consecutive row nodes; one lane per
 // DOF row (node row x component); the chunk's contiguous CSR value segment
 // is accumulated in shared memory (single owner per row: plain adds) and
@@ -1360,6 +1420,7 @@ using OwnerFn = void (*)(const OwnerArgs&, int grid, size_t smem, cudaStream_t);
 using NbrFn = void (*)(const TileArgs&, int rec_bytes, size_t smem, cudaStream_t);
 using RingFn = void (*)(const RingArgs&, size_t smem, cudaStream_t);
 using PTileFn = void (*)(const PTileArgs&, size_t smem, cudaStream_t);
+using CellFn = void (*)(const CellArgs&, cudaStream_t);
 
 struct Entry {
   KernelInfo info;
@@ -1372,6 +1433,7 @@ struct Entry {
   NbrFn nbr = nullptr;   // P1 forms only
   RingFn ring = nullptr; // scalar P1 triangle forms only
   PTileFn ptile = nullptr;
+  CellFn cell = nullptr;   // actions only
 };
 
 template <class K>
@@ -1467,6 +1529,7 @@ Entry form_entry(const std::string& name) {
   e.has_coeff = F::HAS_COEFF;
   e.owner = &launch_owner<F>;
   e.ptile = &launch_ptile<F>;
+  if constexpr (!F::BILINEAR) e.cell = &launch_cell<F>;
   if constexpr (P == 1 && F::NRN == D + 1 && (!F::BILINEAR || F::NCN == F::NRN)) e.nbr = &launch_nbr<F>;
   if constexpr (P == 1 && D == 2 && F::RD == 1 && F::CD == 1) e.ring = &launch_ring<F>;
   return e;
@@ -1630,6 +1693,8 @@ struct FastPlan {
   NbrPlan nb;
   bool use_ptile = false;
   PTilePlan pt;
+  bool use_cell = false;   // cell-centric atomic action
+  SortedMap crows;         // (cell mode) sorted row map
   LocalityPlan loc;
   SortedMap xmap, cmap;
   const int32_t* xptr = nullptr;
@@ -1672,7 +1737,7 @@ constexpr int kTileSeg = 4096;   // matrix values per neighbour-list tile (32 KB
 constexpr int kTileSlots = 1024; // vertices in a tile's window
 constexpr int kTileRuns = 32;    // contiguous runs per window
 
-std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_desc* args,
+std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_desc* args, bool cell_mode,
                                           cudaStream_t s) {
   auto P = std::make_shared<FastPlan>();
   P->counter.alloc(4, s);
@@ -1694,6 +1759,23 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
   const int32_t* perm = P->loc.perm.get();
   SortedMap srows;
   gather_rows(R.v, perm, srows, s);
+  if (cell_mode) { // sorted row / coordinate / coefficient maps only
+    P->use_cell = true;
+    P->crows = std::move(srows);
+    gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, P->xmap, s);
+    P->xptr = P->xmap.v.get();
+    P->xstride = X->arity;
+    if (Cm) {
+      if (Cm->values == R.v.v && Cm->arity == R.v.arity) {
+        P->cptr = P->crows.v.get();
+      } else {
+        gather_rows(MapView{Cm->values, n, Cm->arity, Cm->target_size}, perm, P->cmap, s);
+        P->cptr = P->cmap.v.get();
+      }
+      P->cstride = Cm->arity;
+    }
+    return P;
+  }
   // Neighbour-list plan when row, column, coordinate (and coefficient) maps
   // are one node map (P1 forms): no per-pair cell ids or map rows at all.
   const int strat = options().inc_strategy;
@@ -1831,9 +1913,9 @@ bool fast_pattern(const Entry& k, const loam_arg_desc* args, int nargs) {
 }
 
 void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const FormParams& prm,
-              cudaStream_t s) {
+              cudaStream_t s, bool cell_mode = false) {
   std::vector<uint64_t> key{(uint64_t)k.form, (uint64_t)k.gd, (uint64_t)k.nrn, (uint64_t)k.ncn,
-                            (uint64_t)options().locality, (uint64_t)options().inc_strategy};
+                            (uint64_t)options().locality, (uint64_t)options().inc_strategy, (uint64_t)cell_mode};
   bool cacheable = true;
   for (int q = 0; q < nargs; ++q) {
     const loam_arg_desc& a = args[q];
@@ -1854,11 +1936,28 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     if (it != g_fast_cache.end()) P = it->second;
   }
   if (!P) {
-    P = build_fast_plan(k, n, args, s);
+    P = build_fast_plan(k, n, args, cell_mode, s);
     if (cacheable) {
       std::lock_guard<std::mutex> g(g_cache_mutex);
       g_fast_cache[key] = P;
     }
+  }
+  if (P->use_cell) {
+    CellArgs c{};
+    c.n = n;
+    c.rmap = P->crows.v.get();
+    c.xmap = P->xptr;
+    c.xstride = P->xstride;
+    c.cmap = P->cptr;
+    c.cstride = P->cstride;
+    c.coords = args[1].data;
+    c.coeff = k.has_coeff ? args[2].data : nullptr;
+    c.prm = prm;
+    c.out = args[0].data;
+    if (args[0].flags & LOAM_ARG_ZERO)
+      LG_CUDA(cudaMemsetAsync(args[0].data, 0, sizeof(double) * (size_t)args[0].set_size * args[0].dim, s));
+    k.cell(c, s);
+    return;
   }
   if (P->use_nbr && P->nb.ring && k.ring && !std::getenv("LOAM_GPU_NO_RING")) {
     const NbrPlan& nb = P->nb;
@@ -2228,6 +2327,11 @@ void execute(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_de
   // per element entry -- 10 rows per cell, each recomputed by its owner would
   // redo the cell geometry 10 times (profiles/r01/strategies_*: 0.34 vs 0.80 ms)
   const bool atomic_auto = strat == 0 && !std::getenv("LOAM_GPU_PTILE_ALL") && !k.bilinear && k.form >= 0 && k.gd == 3 && k.nrn > k.gd + 1;
+  // catalogue actions under the atomic strategy: the cell-centric kernel
+  if (n > 0 && k.cell && (atomic_auto || strat == 1) && fast_pattern(k, args, nargs)) {
+    run_fast(k, n, args, nargs, prm, s, true);
+    return;
+  }
   if (n > 0 && !atomic_auto && (strat == 0 || strat == 2 || strat == 4) && fast_pattern(k, args, nargs)) {
     try {
       run_fast(k, n, args, nargs, prm, s);
