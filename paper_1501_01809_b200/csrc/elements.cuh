@@ -15,11 +15,20 @@
 // i possibly thread-dependent -- used by the owner-computes gather
 // (engine.cu), and the full tensor is the row functor unrolled over i.
 #pragma once
+#include <type_traits>
 #include <cstdint>
 
 namespace loam_gpu {
 
 // Catalogue forms; numbering shared with oracle/loam_oracle.h (orc_form).
+// Forms whose RD x CD node blocks are structurally diagonal (component-wise
+// operators such as nu grad u : grad v) declare DIAG_BLOCK: a scatter may skip
+// the off-diagonal components (they are zero in every element row).
+template <class F, class = void>
+struct diag_block : std::false_type {};
+template <class F>
+struct diag_block<F, std::void_t<decltype(F::DIAG_BLOCK)>> : std::bool_constant<F::DIAG_BLOCK> {};
+
 enum FormId : int {
   F_MASS = 0,
   F_STIFFNESS = 1,
@@ -412,6 +421,7 @@ template <>
 struct FormT<F_STOKES_A, 2, 2> {
   static constexpr int NR = 12, NC = 12, NRN = 6, NCN = 6, RD = 2, CD = 2, GD = 2;
   static constexpr bool HAS_COEFF = false, BILINEAR = true;
+  static constexpr bool DIAG_BLOCK = true; // (d, c) blocks vanish for d != c
   static constexpr int NCOEFF = 0;
   __device__ __forceinline__ static void row(int a, const Geom<2>& G, const double*,
                                              const FormParams& prm, double* out) {

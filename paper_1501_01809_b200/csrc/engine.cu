@@ -1369,7 +1369,9 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
 #pragma unroll
                 for (int d = 0; d < F::RD; ++d)
 #pragma unroll
-                  for (int c = 0; c < F::CD; ++c) seg[a0 * W + d * L * F::CD + rk * F::CD + c] += blk[d * F::NC + j * F::CD + c];
+                  for (int c = 0; c < F::CD; ++c)
+                    if (!diag_block<F>::value || d == c)
+                      seg[a0 * W + d * L * F::CD + rk * F::CD + c] += blk[d * F::NC + j * F::CD + c];
               }
             }
             if (G > 1) __syncwarp();
@@ -1841,10 +1843,15 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     spec.ncoeff = k.has_coeff ? k.ncoeff : 0;
     spec.rd = k.rd;
     spec.cd = k.cd;
-    spec.tile_rows = 128;
-    spec.tile_seg = 4096;
-    spec.tile_pairs = 768;
-    spec.tile_slots = 1024;
+    auto env_int = [](const char* name, int dflt) {
+      const char* v = std::getenv(name);
+      return v ? std::atoi(v) : dflt;
+    };
+    spec.tile_rows = kPTileThreads;
+    spec.tile_seg = env_int("LOAM_GPU_PT_SEG", 4096);
+    spec.tile_pairs = env_int("LOAM_GPU_PT_PAIRS", 768);
+    spec.tile_slots = env_int("LOAM_GPU_PT_SLOTS", 1024);
+    spec.tile_runs = env_int("LOAM_GPU_PT_RUNS", 48);
     CsrView csr{};
     if (k.bilinear) {
       const loam_sparsity_desc* sp = args[0].sparsity;
