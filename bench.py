@@ -469,7 +469,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--all-configs", action="store_true")
     ap.add_argument("--configs", default="")
-    ap.add_argument("--strategies", default="auto,owner,atomic,color")
+    ap.add_argument("--strategies", default="auto,owner,atomic,warpagg,color")
     ap.add_argument("--size", type=int, default=None)
     args = ap.parse_args()
     if args.impl == "reference":

@@ -135,8 +135,14 @@ const char* loam_gpu_version(void);
 int loam_gpu_device_ok(void); /* 1 when an sm_100 device is usable */
 
 /* Tunables.  LOAM_OPT_INC_STRATEGY selects the indirect INC scatter:
- *   0 auto (owner-computes), 1 fp64 atomics, 2 owner-computes row gather,
- *   3 colouring (colour-major launches, plain read-modify-write).
+ *   0 auto (owner-computes; cell-centric atomics for P2-tet actions),
+ *   1 fp64 atomics (catalogue forms: one thread per cell, one RED per entry
+ *     at a precomputed slot; other kernels: the staging engine),
+ *   2 owner-computes row gather (pair lists),
+ *   3 colouring (colour-major launches, plain read-modify-write),
+ *   4 owner-computes neighbour-list tiles (P1 forms),
+ *   5 warp-aggregated fp64 atomics (as 1, lanes hitting one address combine
+ *     in the warp first).
  * LOAM_OPT_CHECK_SPARSITY: 1 (default) = a Mat INC/WRITE synchronises once to
  *   report OutsideSparsity like Mat::addto (data.hpp:214-216); 0 = the check
  *   is done only when the slot plan is built (plans prove the pattern).

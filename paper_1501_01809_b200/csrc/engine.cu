@@ -340,12 +340,16 @@ __global__ void __launch_bounds__(kTPB) k_owner_vec(const __grid_constant__ Owne
   a.out[r] = a.accumulate ? a.out[r] + acc : acc;
 }
 
-// Cell-centric action (Dat INC, the atomic strategy for catalogue actions):
-// one thread per cell in locality order (sorted maps: coalesced map rows),
-// the element vector in registers with compile-time rows -- each cell's
-// geometry is computed once, not once per row as the owner kernels must --
-// and one fp64 RED per entry (form.hpp:288-312 actions; parloop.hpp:302-338
-// INC scatter).
+// Cell-centric scatter (the fp64-atomic strategies for catalogue forms): one
+// thread per cell in locality order (sorted maps: coalesced map rows), the
+// element tensor in registers with compile-time rows -- each cell's geometry
+// is computed once, not once per row as the owner kernels must -- and one
+// fp64 RED per entry (parloop.hpp:302-313 INC scatter / Mat::addto).  Matrix
+// entries go to the precomputed per-cell slot: row_ptr[dof row] + in-row rank
+// (the pair plan's ranks scattered to cell-major order, plan.cu:build_ranks),
+// so no CSR search happens at assembly time.  AGG: lanes of a warp that hit
+// the same address first combine through __match_any_sync + shuffles and the
+// group leader issues one RED (the north star's warp-aggregated reduction).
 struct CellArgs {
   int n;
   const int32_t* rmap; // sorted row map, NRN per cell
@@ -355,49 +359,115 @@ struct CellArgs {
   int cstride;
   const double* coords;
   const double* coeff;
+  const uint8_t* cranks;  // (matrices) [n x NRN x NCN] in-row rank per entry
+  const int64_t* row_ptr; // (matrices) CSR dof-row offsets
   FormParams prm;
   double* out;
 };
 
-template <class F>
-__global__ void __launch_bounds__(128) k_cell_vec(const __grid_constant__ CellArgs a) {
-  constexpr int GD = F::GD, NV = GD + 1;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= a.n) return;
-  int vid[NV], rows[F::NRN];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) vid[v] = __ldg(a.xmap + (int64_t)e * a.xstride + v);
-#pragma unroll
-  for (int i = 0; i < F::NRN; ++i) rows[i] = __ldg(a.rmap + (int64_t)e * F::NRN + i);
-  double C[F::HAS_COEFF ? F::NCOEFF : 1];
-  if constexpr (F::HAS_COEFF)
-#pragma unroll
-    for (int q = 0; q < F::NCOEFF; ++q) C[q] = __ldg(a.coeff + __ldg(a.cmap + (int64_t)e * a.cstride + q));
-  double X[NV][GD];
-#pragma unroll
-  for (int v = 0; v < NV; ++v)
-#pragma unroll
-    for (int c = 0; c < GD; ++c) X[v][c] = __ldg(a.coords + (int64_t)vid[v] * GD + c);
-  Geom<GD> G;
-  geometry<GD>(X, G);
-#pragma unroll
-  for (int i = 0; i < F::NRN; ++i) {
-    double v;
-    F::row(i, G, C, a.prm, &v);
-    atomicAdd(a.out + rows[i], v);
+template <bool AGG>
+__device__ __forceinline__ void red_add(double* base, int64_t pos, double v, bool valid) {
+  if constexpr (!AGG) {
+    if (valid) atomicAdd(base + pos, v);
+  } else {
+    const int lane = threadIdx.x & 31;
+    const int64_t key = valid ? pos : -1 - (int64_t)lane; // invalid lanes: unique keys
+    const unsigned peers = __match_any_sync(0xffffffffu, (unsigned long long)key);
+    const int leader = __ffs(peers) - 1;
+    unsigned m = lane == leader ? peers & (peers - 1) : 0u; // the leader collects its peers
+    double sum = v;
+    while (__any_sync(0xffffffffu, m != 0)) {
+      const int src = m ? __ffs(m) - 1 : lane;
+      const double x = __shfl_sync(0xffffffffu, v, src);
+      if (m) {
+        sum += x;
+        m &= m - 1;
+      }
+    }
+    if (valid && lane == leader) atomicAdd(base + pos, sum);
   }
 }
 
 template <class F>
-void launch_cell(const CellArgs& a, cudaStream_t s) {
-  if constexpr (!F::BILINEAR) {
-    if (a.n == 0) return;
-    k_cell_vec<F><<<ceil_div(a.n, 128), 128, 0, s>>>(a);
-    count_launch();
-    LG_LAUNCH_CHECK();
-  } else {
-    fail(LOAM_ERR(InvalidArgument), "cell kernel: actions only");
+__device__ __forceinline__ void cell_gather(const CellArgs& a, int e, double (&X)[F::GD + 1][F::GD],
+                                            double (&C)[F::HAS_COEFF ? F::NCOEFF : 1], int (&rows)[F::NRN]) {
+  constexpr int GD = F::GD, NV = GD + 1;
+  int vid[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) vid[v] = __ldg(a.xmap + (int64_t)e * a.xstride + v);
+#pragma unroll
+  for (int i = 0; i < F::NRN; ++i) rows[i] = __ldg(a.rmap + (int64_t)e * F::NRN + i);
+  if constexpr (F::HAS_COEFF)
+#pragma unroll
+    for (int q = 0; q < F::NCOEFF; ++q) C[q] = __ldg(a.coeff + __ldg(a.cmap + (int64_t)e * a.cstride + q));
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int c = 0; c < GD; ++c) X[v][c] = __ldg(a.coords + (int64_t)vid[v] * GD + c);
+}
+
+template <class F, bool AGG>
+__global__ void __launch_bounds__(128) k_cell_vec(const __grid_constant__ CellArgs a) {
+  const int e0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e0 < a.n;
+  if (!AGG && !valid) return;
+  const int e = valid ? e0 : 0;
+  double X[F::GD + 1][F::GD], C[F::HAS_COEFF ? F::NCOEFF : 1];
+  int rows[F::NRN];
+  cell_gather<F>(a, e, X, C, rows);
+  Geom<F::GD> G;
+  geometry<F::GD>(X, G);
+#pragma unroll
+  for (int i = 0; i < F::NRN; ++i) {
+    double v;
+    F::row(i, G, C, a.prm, &v);
+    red_add<AGG>(a.out, rows[i], v, valid);
   }
+}
+
+template <class F, bool AGG>
+__global__ void __launch_bounds__(128) k_cell_mat(const __grid_constant__ CellArgs a) {
+  const int e0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = e0 < a.n;
+  if (!AGG && !valid) return;
+  const int e = valid ? e0 : 0;
+  double X[F::GD + 1][F::GD], C[1];
+  int rows[F::NRN];
+  cell_gather<F>(a, e, X, C, rows);
+  Geom<F::GD> G;
+  geometry<F::GD>(X, G);
+#pragma unroll
+  for (int i = 0; i < F::NRN; ++i) {
+    int rk[F::NCN];
+    load_ranks<F::NCN>(a.cranks, (int64_t)e * F::NRN + i, rk);
+    double blk[F::RD * F::NC];
+    F::row(i, G, C, a.prm, blk);
+#pragma unroll
+    for (int d = 0; d < F::RD; ++d) {
+      const int64_t base = __ldg(a.row_ptr + (int64_t)rows[i] * F::RD + d);
+#pragma unroll
+      for (int j = 0; j < F::NCN; ++j)
+#pragma unroll
+        for (int c = 0; c < F::CD; ++c)
+          if (!diag_block<F>::value || d == c)
+            red_add<AGG>(a.out, base + rk[j] * F::CD + c, blk[d * F::NC + j * F::CD + c], valid);
+    }
+  }
+}
+
+template <class F>
+void launch_cell(const CellArgs& a, bool agg, cudaStream_t s) {
+  if (a.n == 0) return;
+  const int grid = ceil_div(a.n, 128);
+  if constexpr (F::BILINEAR) {
+    if (agg) k_cell_mat<F, true><<<grid, 128, 0, s>>>(a);
+    else k_cell_mat<F, false><<<grid, 128, 0, s>>>(a);
+  } else {
+    if (agg) k_cell_vec<F, true><<<grid, 128, 0, s>>>(a);
+    else k_cell_vec<F, false><<<grid, 128, 0, s>>>(a);
+  }
+  count_launch();
+  LG_LAUNCH_CHECK();
 }
 
 // Matrix (Mat INC): one warp per chunk of consecutive row nodes; one lane per
@@ -1422,7 +1492,7 @@ using OwnerFn = void (*)(const OwnerArgs&, int grid, size_t smem, cudaStream_t);
 using NbrFn = void (*)(const TileArgs&, int rec_bytes, size_t smem, cudaStream_t);
 using RingFn = void (*)(const RingArgs&, size_t smem, cudaStream_t);
 using PTileFn = void (*)(const PTileArgs&, size_t smem, cudaStream_t);
-using CellFn = void (*)(const CellArgs&, cudaStream_t);
+using CellFn = void (*)(const CellArgs&, bool agg, cudaStream_t);
 
 struct Entry {
   KernelInfo info;
@@ -1435,7 +1505,7 @@ struct Entry {
   NbrFn nbr = nullptr;   // P1 forms only
   RingFn ring = nullptr; // scalar P1 triangle forms only
   PTileFn ptile = nullptr;
-  CellFn cell = nullptr;   // actions only
+  CellFn cell = nullptr;
 };
 
 template <class K>
@@ -1531,7 +1601,7 @@ Entry form_entry(const std::string& name) {
   e.has_coeff = F::HAS_COEFF;
   e.owner = &launch_owner<F>;
   e.ptile = &launch_ptile<F>;
-  if constexpr (!F::BILINEAR) e.cell = &launch_cell<F>;
+  e.cell = &launch_cell<F>;
   if constexpr (P == 1 && F::NRN == D + 1 && (!F::BILINEAR || F::NCN == F::NRN)) e.nbr = &launch_nbr<F>;
   if constexpr (P == 1 && D == 2 && F::RD == 1 && F::CD == 1) e.ring = &launch_ring<F>;
   return e;
@@ -1695,8 +1765,9 @@ struct FastPlan {
   NbrPlan nb;
   bool use_ptile = false;
   PTilePlan pt;
-  bool use_cell = false;   // cell-centric atomic action
+  bool use_cell = false;   // cell-centric atomic scatter
   SortedMap crows;         // (cell mode) sorted row map
+  DevBuf<uint8_t> cranks;  // (cell mode, matrices) per-cell in-row ranks
   LocalityPlan loc;
   SortedMap xmap, cmap;
   const int32_t* xptr = nullptr;
@@ -1761,8 +1832,23 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
   const int32_t* perm = P->loc.perm.get();
   SortedMap srows;
   gather_rows(R.v, perm, srows, s);
-  if (cell_mode) { // sorted row / coordinate / coefficient maps only
+  if (cell_mode) { // sorted row / coordinate / coefficient maps (+ per-cell slot ranks)
     P->use_cell = true;
+    if (k.bilinear) {
+      const NodeMap Cn = node_view(args[0].col_map);
+      SortedMap scols;
+      const int32_t* sc = srows.v.get();
+      if (!(Cn.v.v == R.v.v && Cn.v.arity == R.v.arity)) {
+        gather_rows(Cn.v, perm, scols, s);
+        sc = scols.v.get();
+      }
+      const loam_sparsity_desc* sp = args[0].sparsity;
+      CsrView csr{sp->row_ptr, sp->col_idx, sp->nrows, sp->ncols, sp->nnz, R.dim, Cn.dim};
+      PairPlan pp;
+      build_pairs(srows.v.get(), n, R.v.arity, R.v.target, pp, s);
+      build_ranks(pp, srows.v.get(), sc, Cn.v.arity, csr, s); // OutsideSparsity / ShapeMismatch here
+      cell_major_ranks(pp, P->cranks, s);
+    }
     P->crows = std::move(srows);
     gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, P->xmap, s);
     P->xptr = P->xmap.v.get();
@@ -1951,6 +2037,8 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
   }
   if (P->use_cell) {
     CellArgs c{};
+    c.cranks = P->cranks.get();
+    c.row_ptr = k.bilinear ? args[0].sparsity->row_ptr : nullptr;
     c.n = n;
     c.rmap = P->crows.v.get();
     c.xmap = P->xptr;
@@ -1961,9 +2049,11 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     c.coeff = k.has_coeff ? args[2].data : nullptr;
     c.prm = prm;
     c.out = args[0].data;
-    if (args[0].flags & LOAM_ARG_ZERO)
-      LG_CUDA(cudaMemsetAsync(args[0].data, 0, sizeof(double) * (size_t)args[0].set_size * args[0].dim, s));
-    k.cell(c, s);
+    if (args[0].flags & LOAM_ARG_ZERO) {
+      const size_t len = k.bilinear ? (size_t)args[0].sparsity->nnz : (size_t)args[0].set_size * args[0].dim;
+      LG_CUDA(cudaMemsetAsync(args[0].data, 0, sizeof(double) * len, s));
+    }
+    k.cell(c, options().inc_strategy == 5, s);
     return;
   }
   if (P->use_nbr && P->nb.ring && k.ring && !std::getenv("LOAM_GPU_NO_RING")) {
@@ -2334,10 +2424,15 @@ void execute(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_de
   // per element entry -- 10 rows per cell, each recomputed by its owner would
   // redo the cell geometry 10 times (profiles/r01/strategies_*: 0.34 vs 0.80 ms)
   const bool atomic_auto = strat == 0 && !std::getenv("LOAM_GPU_PTILE_ALL") && !k.bilinear && k.form >= 0 && k.gd == 3 && k.nrn > k.gd + 1;
-  // catalogue actions under the atomic strategy: the cell-centric kernel
-  if (n > 0 && k.cell && (atomic_auto || strat == 1) && fast_pattern(k, args, nargs)) {
-    run_fast(k, n, args, nargs, prm, s, true);
-    return;
+  // catalogue forms under the atomic strategies (and P2-tet actions under
+  // auto): the cell-centric kernel, plain or warp-aggregated REDs
+  if (n > 0 && k.cell && (atomic_auto || strat == 1 || strat == 5) && fast_pattern(k, args, nargs)) {
+    try {
+      run_fast(k, n, args, nargs, prm, s, true);
+      return;
+    } catch (const Error& e) {
+      if (e.code() != LOAM_ERR(ShapeMismatch)) throw; // unblocked pattern: generic engine
+    }
   }
   if (n > 0 && !atomic_auto && (strat == 0 || strat == 2 || strat == 4) && fast_pattern(k, args, nargs)) {
     try {

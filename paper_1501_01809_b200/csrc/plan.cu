@@ -766,6 +766,22 @@ void build_pairs(const int32_t* sorted_rows, int ncells, int nrn, int nrows_node
   }, s);
 }
 
+__global__ void k_cell_major_ranks(const int32_t* pairs, int64_t np, int ncn, const uint8_t* ranks, uint8_t* out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  const int64_t code = pairs[p];
+  for (int j = 0; j < ncn; ++j) out[code * ncn + j] = ranks[p * ncn + j];
+}
+
+void cell_major_ranks(const PairPlan& pp, DevBuf<uint8_t>& out, cudaStream_t s) {
+  out.alloc((size_t)pp.npairs * pp.ncn + 16, s);
+  if (!pp.npairs) return;
+  k_cell_major_ranks<<<ceil_div(pp.npairs, kTPB), kTPB, 0, s>>>(pp.pairs.get(), pp.npairs, pp.ncn, pp.ranks.get(),
+                                                                  out.get());
+  count_launch();
+  LG_LAUNCH_CHECK();
+}
+
 void build_ranks(PairPlan& pp, const int32_t* sorted_rows, const int32_t* sorted_cols, int ncn,
                  const CsrView& csr, cudaStream_t s) {
   pp.ncn = ncn;

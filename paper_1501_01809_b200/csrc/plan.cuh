@@ -70,6 +70,9 @@ void build_pairs(const int32_t* sorted_rows, int ncells, int nrn, int nrows_node
                  cudaStream_t s);
 // Slot ranks of the column nodes of each pair in its row (throws OutsideSparsity);
 // verifies the pattern is blocked by (rd, cd) first.
+// Scatter the pair plan's ranks (pair order) to cell-major order:
+// out[(cell * nrn + i) * ncn + j] = pp.ranks[p * ncn + j] for pair p = (cell, i).
+void cell_major_ranks(const PairPlan& pp, DevBuf<uint8_t>& out, cudaStream_t s);
 void build_ranks(PairPlan& pp, const int32_t* sorted_rows, const int32_t* sorted_cols, int ncn,
                  const CsrView& csr, cudaStream_t s);
 // Warp chunking of row nodes (<= max_rows nodes, segment <= smax doubles).
