@@ -180,77 +180,22 @@ def time_steps(torch, w, steps, flush, stream):
 
 
 def e2e_host(torch, w, steps, warmup):
-    """The same assembly through loam_gpu_execute_host with pinned host buffers."""
-    from paper_1501_01809_b200 import capi
+    """The same assembly through loam_gpu_execute_host (loam.HostLoop) with
+    pinned host buffers: every step copies the Dats the loop reads host->device
+    and the values it writes device->host inside the timed region.  Maps and
+    the Sparsity are immutable, id'd objects the library keeps resident after
+    the first (warm-up) call, so they are not per-step transfers."""
     from paper_1501_01809_b200 import loam as L
-    lib = capi.lib()
-    loops = w.loops
-    pinned = {}
-
-    def pin(arr):
-        t = torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
-        pinned[id(t)] = t
-        return t
-
-    h2d = d2h = 0
-    host_loops = []
-    seen = set()
-    for lp in loops:
-        kd, descs, keep = L._build(lp)
-        hdescs = (capi.ArgDesc * len(lp.args))()
-        mkeep = []
-        for k, a in enumerate(lp.args):
-            d = capi.ArgDesc()
-            C.memmove(C.byref(d), C.byref(descs[k]), C.sizeof(d))
-            if a.dat is not None:
-                t = pin(a.dat.view())
-                d.data = t.data_ptr()
-                if a.access != L.READ:
-                    d.flags = capi.ARG_ZERO if a.access == L.INC else 0  # fresh assemble_vector output
-                    d2h += t.numel() * 8
-                else:
-                    h2d += t.numel() * 8
-            elif a.mat is not None:
-                t = pin(np.zeros(a.mat.sparsity.nnz))
-                d.data = t.data_ptr()
-                d.flags = capi.ARG_ZERO
-                d2h += t.numel() * 8
-                sp = capi.SparsityDesc()
-                C.memmove(C.byref(sp), C.byref(a.mat.sparsity.desc()), C.sizeof(sp))
-                rp, ci = a.mat.sparsity.host()
-                trp, tci = pin(rp), pin(ci)
-                sp.row_ptr, sp.col_idx = trp.data_ptr(), tci.data_ptr()
-                if ("sp", a.mat.sparsity.id) not in seen:
-                    h2d += trp.numel() * 8 + tci.numel() * 4
-                    seen.add(("sp", a.mat.sparsity.id))
-                mkeep.append(sp)
-                d.sparsity = C.pointer(sp)
-            for fld, mp in (("map", a.maps[0] if a.maps else None), ("col_map", a.maps[1] if len(a.maps) > 1 else None)):
-                if mp is None:
-                    continue
-                md = capi.MapDesc()
-                C.memmove(C.byref(md), C.byref(mp.desc()), C.sizeof(md))
-                tv = pin(mp.values)
-                md.values = tv.data_ptr()
-                if ("map", mp.id) not in seen:
-                    h2d += tv.numel() * 4
-                    seen.add(("map", mp.id))
-                if mp.node_map is not None:
-                    tn = pin(mp.node_map.values)
-                    md.node_values = tn.data_ptr()
-                    if ("map", mp.node_map.id) not in seen:
-                        h2d += tn.numel() * 4
-                        seen.add(("map", mp.node_map.id))
-                mkeep.append(md)
-                setattr(d, fld, C.pointer(md))
-            hdescs[k] = d
-        host_loops.append((kd, hdescs, keep, mkeep, lp))
+    w.reset()
+    host_loops = [L.HostLoop(lp) for lp in w.loops]
+    h2d = sum(h.h2d_bytes for h in host_loops)
+    d2h = sum(h.d2h_bytes for h in host_loops)
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
     def run():
-        for kd, hd, _, _, lp in host_loops:
-            capi.check(lib.loam_gpu_execute_host(C.byref(kd), lp.iterset.size, lp.iterset.id, hd, len(lp.args), sh))
+        for h in host_loops:
+            h.run(sh)
 
     for _ in range(warmup):
         run()
@@ -373,7 +318,9 @@ def gpu_arm(args):
     kernel_ms = float(np.median(times))
     achieved = abytes / (kernel_ms * 1e-3) / 1e9
     # end to end through the C ABI with host buffers
-    e2e_times, h2d, d2h = e2e_host(torch, w, max(2, min(args.steps, 5)), 1)
+    e2e_times, h2d, d2h = e2e_host(torch, w, max(3, min(args.steps, 10)), 2)
+    if os.environ.get("LOAM_BENCH_DEBUG"):
+        print("e2e step ms:", [round(t, 3) for t in e2e_times], file=sys.stderr)
     e2e_ms = max_over_ranks(float(np.mean(e2e_times)), "cuda")
     # correctness spot check of this very run against the reference pattern size
     line = None

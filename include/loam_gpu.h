@@ -171,7 +171,12 @@ int loam_gpu_execute(const loam_kernel_desc* kernel, int32_t iterset_size, uint6
                      const loam_arg_desc* args, int nargs, void* stream);
 /* loam::execute on HOST data (every pointer in args/maps/sparsity is host
  * memory, ideally pinned): uploads what the loop reads, runs, downloads what
- * it writes, synchronously -- the reference's host-memory calling convention. */
+ * it writes, synchronously -- the reference's host-memory calling convention.
+ * Maps and Sparsities are immutable in the reference (shared_ptr<const Map>,
+ * a Sparsity is never modified after build_sparsity): those with a nonzero
+ * id are uploaded once per (id, host pointer, size) and kept resident;
+ * Dats are copied on every call.  loam_gpu_plan_cache_clear() drops the
+ * resident copies. */
 int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t iterset_size,
                           uint64_t iterset_id, const loam_arg_desc* args, int nargs,
                           void* stream);

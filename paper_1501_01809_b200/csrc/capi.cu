@@ -4,6 +4,8 @@
 // with a thread-local message; CUDA failures -> LOAM_GPU_ERR_CUDA.  No CPU
 // fallback: compute entry points fail with LOAM_GPU_ERR_NO_DEVICE when no
 // sm_100 device is usable.
+#include <map>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -42,6 +44,17 @@ bool device_ok() {
     int dev = 0, major = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (major == 10) {
+      // plan and staging buffers come from the stream-ordered pool: keep freed
+      // blocks cached instead of returning them to the driver at every
+      // synchronisation (the host calling convention synchronises per call)
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      cudaGetLastError();
+    }
     return major == 10;
   }();
   return ok;
@@ -53,6 +66,44 @@ void require_device() {
 }
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Device copies of the immutable objects of the host calling convention.  In
+// the reference a Map is a shared_ptr<const Map> (topology.hpp:68) and a
+// Sparsity is never modified after build_sparsity (data.hpp:116-179), so an
+// object id names its content: execute_host uploads a Map / Sparsity once per
+// (id, host pointer, size) and keeps it resident, like the C++ facade's
+// Map/Sparsity objects do.  Dats (mutable, data.hpp:49-52) are copied every
+// call.  loam_gpu_plan_cache_clear() drops these copies too.
+struct Resident {
+  const void* host = nullptr;
+  size_t bytes = 0;
+  void* dev = nullptr;
+};
+std::mutex g_res_mutex;
+std::map<std::pair<int, uint64_t>, Resident> g_resident;
+
+void* resident_copy(int kind, uint64_t id, const void* host, size_t bytes, cudaStream_t s) {
+  std::lock_guard<std::mutex> g(g_res_mutex);
+  Resident& r = g_resident[{kind, id}];
+  if (r.dev && r.host == host && r.bytes == bytes) return r.dev;
+  if (r.dev) {
+    LG_CUDA(cudaStreamSynchronize(s));
+    LG_CUDA(cudaFree(r.dev));
+    r.dev = nullptr;
+  }
+  LG_CUDA(cudaMalloc(&r.dev, bytes ? bytes : 1));
+  if (bytes) LG_CUDA(cudaMemcpyAsync(r.dev, host, bytes, cudaMemcpyHostToDevice, s));
+  r.host = host;
+  r.bytes = bytes;
+  return r.dev;
+}
+
+void resident_clear() {
+  std::lock_guard<std::mutex> g(g_res_mutex);
+  for (auto& [k, r] : g_resident)
+    if (r.dev) cudaFree(r.dev);
+  g_resident.clear();
+}
 
 } // namespace
 
@@ -86,7 +137,10 @@ int loam_gpu_get_option(int option) {
 }
 
 int loam_gpu_plan_cache_clear(void) {
-  return guarded([] { plan_cache_clear(); });
+  return guarded([] {
+    plan_cache_clear();
+    resident_clear();
+  });
 }
 
 int64_t loam_gpu_launch_count(void) { return g_launches.load(); }
@@ -150,12 +204,17 @@ int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t n, uint64_t it
     std::vector<loam_arg_desc> dargs(args, args + nargs);
     std::vector<loam_map_desc> dmaps(2 * nargs);
     std::vector<loam_sparsity_desc> dsp(nargs);
+    // immutable objects with an id stay resident; anonymous ones (id 0) are copied per call
+    auto keep = [&](int kind, uint64_t id, const void* host, size_t bytes) -> void* {
+      return id ? resident_copy(kind, id, host, bytes, s) : up(host, bytes);
+    };
     auto map_up = [&](const loam_map_desc* m, loam_map_desc& d) {
       d = *m;
-      d.values = static_cast<const int32_t*>(up(m->values, sizeof(int32_t) * (size_t)m->source_size * m->arity));
+      d.values = static_cast<const int32_t*>(
+          keep(0, m->id, m->values, sizeof(int32_t) * (size_t)m->source_size * m->arity));
       if (m->expand_dim > 1 && m->node_values)
         d.node_values = static_cast<const int32_t*>(
-            up(m->node_values, sizeof(int32_t) * (size_t)m->source_size * m->node_arity));
+            keep(1, m->id, m->node_values, sizeof(int32_t) * (size_t)m->source_size * m->node_arity));
     };
     for (int q = 0; q < nargs; ++q) {
       const loam_arg_desc& a = args[q];
@@ -166,8 +225,9 @@ int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t n, uint64_t it
       if (a.kind == LOAM_ARG_MAT) {
         const loam_sparsity_desc* sp = a.sparsity;
         dsp[q] = *sp;
-        dsp[q].row_ptr = static_cast<const int64_t*>(up(sp->row_ptr, sizeof(int64_t) * ((size_t)sp->nrows + 1)));
-        dsp[q].col_idx = static_cast<const int32_t*>(up(sp->col_idx, sizeof(int32_t) * (size_t)sp->nnz));
+        dsp[q].row_ptr = static_cast<const int64_t*>(
+            keep(2, sp->id, sp->row_ptr, sizeof(int64_t) * ((size_t)sp->nrows + 1)));
+        dsp[q].col_idx = static_cast<const int32_t*>(keep(3, sp->id, sp->col_idx, sizeof(int32_t) * (size_t)sp->nnz));
         d.sparsity = &dsp[q];
         count = (size_t)sp->nnz;
       } else if (a.kind == LOAM_ARG_DAT) {

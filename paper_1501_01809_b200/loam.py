@@ -396,6 +396,99 @@ def _build(loop: Parloop):
     return kd, descs, keep
 
 
+class HostLoop:
+    """A par_loop over HOST memory through loam_gpu_execute_host -- the
+    reference's calling convention (execute reads and writes host buffers,
+    parloop.hpp:191).  Every object's data is mirrored into (pinned) host
+    arrays; Maps and the Sparsity keep their ids, so the library uploads them
+    once and keeps them resident (they are immutable in the reference); Dats
+    are copied on every call.  ``outputs`` holds the host arrays the loop
+    writes; ``h2d_bytes`` / ``d2h_bytes`` count the per-call Dat transfers.
+    """
+
+    def __init__(self, loop: Parloop, pin: bool = True):
+        self.loop = loop
+        self._keep, self.outputs = [], []
+        self.h2d_bytes = self.d2h_bytes = 0
+        kd, dev_descs, keep = _build(loop)
+        self._keep += [kd, keep]
+        self.kd = kd
+        self.descs = (capi.ArgDesc * max(len(loop.args), 1))()
+
+        mirrors = {}  # one host mirror per object: an id must name one host buffer
+
+        def host(t) -> torch.Tensor:
+            key = (id(t), t.data_ptr() if isinstance(t, torch.Tensor) else t.ctypes.data)
+            if key in mirrors:
+                return mirrors[key]
+            mirrors[key] = h = host_copy(t)
+            return h
+
+        def host_copy(t) -> torch.Tensor:
+            if isinstance(t, np.ndarray):
+                h = torch.from_numpy(np.ascontiguousarray(t))
+            else:
+                h = t.detach().cpu().contiguous()
+            h = h.pin_memory() if pin else h
+            self._keep.append(h)
+            return h
+
+        maps = {}
+
+        def host_map(m: Map) -> capi.MapDesc:
+            if m.id in maps:
+                return maps[m.id]
+            md = capi.MapDesc()
+            C.memmove(C.byref(md), C.byref(m.desc()), C.sizeof(md))
+            md.values = host(m.values).data_ptr()
+            if m.node_map is not None:
+                md.node_values = host(m.node_map.values).data_ptr()
+            self._keep.append(md)
+            maps[m.id] = md
+            return md
+
+        for k, a in enumerate(loop.args):
+            d = capi.ArgDesc()
+            C.memmove(C.byref(d), C.byref(dev_descs[k]), C.sizeof(d))
+            if a.dat is not None:
+                h = host(a.dat.data)
+                d.data = h.data_ptr()
+                if a.maps:
+                    d.map = C.pointer(host_map(a.maps[0]))
+                if a.access != READ:
+                    self.outputs.append(h)
+                    self.d2h_bytes += h.numel() * 8
+                if a.access != WRITE and not (d.flags & capi.ARG_ZERO):
+                    self.h2d_bytes += h.numel() * 8
+            elif a.mat is not None:
+                h = host(a.mat.values[: max(a.mat.sparsity.nnz, 1)])
+                d.data = h.data_ptr()
+                sp = capi.SparsityDesc()
+                C.memmove(C.byref(sp), C.byref(a.mat.sparsity.desc()), C.sizeof(sp))
+                sp.row_ptr = host(a.mat.sparsity.row_ptr).data_ptr()
+                sp.col_idx = host(a.mat.sparsity.col_idx).data_ptr()
+                self._keep.append(sp)
+                d.sparsity = C.pointer(sp)
+                d.map, d.col_map = C.pointer(host_map(a.maps[0])), C.pointer(host_map(a.maps[1]))
+                self.outputs.append(h)
+                self.d2h_bytes += a.mat.sparsity.nnz * 8
+                if not (d.flags & capi.ARG_ZERO):
+                    self.h2d_bytes += a.mat.sparsity.nnz * 8
+            else:
+                h = host(a.glob.data)
+                d.data = h.data_ptr()
+                self.h2d_bytes += h.numel() * 8
+                if a.access != READ:
+                    self.outputs.append(h)
+                    self.d2h_bytes += h.numel() * 8
+            self.descs[k] = d
+
+    def run(self, stream: Optional[int] = None) -> None:
+        capi.check(capi.lib().loam_gpu_execute_host(C.byref(self.kd), self.loop.iterset.size,
+                                                    self.loop.iterset.id, self.descs, len(self.loop.args),
+                                                    _stream() if stream is None else stream))
+
+
 def validate(loop: Parloop) -> None:
     """parloop.hpp:89-146: descriptor checks only, no state change."""
     kd, descs, keep = _build(loop)
