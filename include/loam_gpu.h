@@ -181,6 +181,51 @@ int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t iterset_size,
                           uint64_t iterset_id, const loam_arg_desc* args, int nargs,
                           void* stream);
 
+/* ---- consumers of the assembled matrix --------------------- */
+/* y = A x by CSR traversal (data.hpp:236-250 mat_spmv): rows ascending, each
+ * row folded in column order with a separate multiply and add -- bitwise
+ * equal to the reference.  x_len must equal the column count
+ * (DimensionMismatch otherwise); y has nrows entries.  Device pointers. */
+int loam_gpu_spmv(const loam_sparsity_desc* sparsity, const double* values, const double* x,
+                  int64_t x_len, double* y, void* stream);
+
+/* 2x2 nested operator (solver.hpp:21-28 BlockMat): a null sparsity is a zero
+ * block; block (i, j) is row_sizes[i] x col_sizes[j]. */
+typedef struct loam_block_mat {
+  const loam_sparsity_desc* sparsity[2][2];
+  const double* values[2][2];
+  int32_t row_sizes[2];
+  int32_t col_sizes[2];
+} loam_block_mat;
+
+/* y_i = sum_j A_ij x_j on the flattened numbering (solver.hpp:33-58
+ * block_spmv): each row folds its block-0 entries, then block 1 -- bitwise
+ * equal to the reference. */
+int loam_gpu_block_spmv(const loam_block_mat* op, const double* x, int64_t x_len, double* y,
+                        void* stream);
+
+/* solver.hpp:13-18 SolveReport; reason 0 rtol, 1 atol, 2 maxit. */
+typedef struct loam_solve_report {
+  int32_t iterations;
+  double final_residual_norm;
+  int32_t converged;
+  int32_t reason;
+} loam_solve_report;
+
+/* Preconditioned CG (solver.hpp:80-207 cg_solve): x holds x0 on entry (zeros
+ * are the reference default) and the iterate on return; stopping test
+ * max(rtol ||b||, atol) on the recurrence, re-verified with the true
+ * residual; IndefiniteBreakdown when p'Ap <= 0 or (jacobi != 0) a diagonal
+ * entry is not positive; maxit returns the last iterate unconverged.  The
+ * iteration runs on the device (flag-gated kernels, no per-iteration host
+ * synchronisation); dot products are deterministic two-pass reductions. */
+int loam_gpu_cg_solve(const loam_sparsity_desc* sparsity, const double* values, const double* b,
+                      int64_t b_len, double* x, double rtol, double atol, int32_t maxit,
+                      int32_t jacobi, loam_solve_report* report, void* stream);
+int loam_gpu_cg_solve_block(const loam_block_mat* op, const double* b, int64_t b_len, double* x,
+                            double rtol, double atol, int32_t maxit, int32_t jacobi,
+                            loam_solve_report* report, void* stream);
+
 /* ---- topology / data services ------------------------------------------- */
 /* Map construction check (topology.hpp:45-48): every entry in [0, target). */
 int loam_gpu_map_check(const loam_map_desc* map, void* stream);

@@ -52,6 +52,10 @@ def orc():
                                           IP, C.c_int, DP, C.c_int, DP]
         L.orc_assemble_matrix.argtypes = [C.c_int, C.c_int, C.c_int, DP, C.c_int, IP, C.c_int, IP,
                                           C.c_int, IP, DP, C.c_int, I64P, IP, DP]
+        VPP = C.POINTER(C.c_void_p)
+        L.orc_block_spmv.argtypes = [IP, IP, VPP, VPP, VPP, DP, DP]
+        L.orc_cg.argtypes = [IP, IP, VPP, VPP, VPP, C.c_int, DP, DP, C.c_double, C.c_double, C.c_int, C.c_int,
+                             IP, DP, IP]
         _orc = L
     return _orc
 
@@ -87,6 +91,11 @@ def ref():
                                         C.c_int, DP, DP, C.c_int, DP]
         L.ref_time_execute.argtypes = [C.c_int, C.c_int, C.c_int, DP, C.c_int, C.c_int, IP, DP, DP,
                                        C.c_int, C.c_int, C.c_int, C.c_int, DP]
+        VPP = C.POINTER(C.c_void_p)
+        L.ref_spmv.argtypes = [C.c_int, C.c_int, I64P, IP, DP, DP, C.c_int64, DP]
+        L.ref_block_spmv.argtypes = [IP, IP, VPP, VPP, VPP, DP, C.c_int64, DP]
+        L.ref_cg_solve.argtypes = [C.c_int, IP, IP, VPP, VPP, VPP, DP, C.c_int64, DP, C.c_int64, C.c_double,
+                                   C.c_double, C.c_int, C.c_int, IP, DP]
         _ref = L
     return _ref
 
@@ -287,3 +296,120 @@ def ref_time_execute(form, degree, gdim, cv, coords, coeff=None, params=(), as_s
                                   None if coeff is None else dp(np.ascontiguousarray(coeff)),
                                   int(as_shipped), threads, warmup, steps, dp(times)), ref())
     return times
+
+
+# ------------------------------------------- consumers of the assembled matrix
+# A CSR operand is (nrows, ncols, row_ptr int64, col_idx int32, values f64); a
+# nested operator is a 2x2 list of CSR operands or None (zero block) with
+# row_sizes / col_sizes (solver.hpp:21-28).
+KINDS = ["IndexOutOfRange", "ArityMismatch", "SourceMismatch", "AsymmetricAdjacency", "IllegalAccess",
+         "MapSourceMismatch", "ShapeMismatch", "UnboundIdentifier", "NonDividingFactor", "OutsideSparsity",
+         "EmptyPartials", "DimensionMismatch", "InvalidSubdivision", "ParseError", "NonManifold", "CellMismatch",
+         "UnsupportedForm", "MissingDiagonal", "SpaceMismatch", "IndefiniteBreakdown", "InstabilityDetected",
+         "InvalidArgument"]
+
+
+class KindError(OracleError):
+    def __init__(self, code, msg=""):
+        self.kind = KINDS[code - 1] if 1 <= code <= len(KINDS) else str(code)
+        super().__init__(f"{self.kind}: {msg}")
+
+
+def _blocks(blocks, row_sizes, col_sizes):
+    keep = []
+    rp, ci, v = (C.c_void_p * 4)(), (C.c_void_p * 4)(), (C.c_void_p * 4)()
+    for i in range(2):
+        for j in range(2):
+            b = blocks[i][j]
+            if b is None:
+                continue
+            _, _, r, c, vals = b
+            r, c, vals = (np.ascontiguousarray(r, np.int64), np.ascontiguousarray(c, np.int32),
+                          np.ascontiguousarray(vals, np.float64))
+            keep += [r, c, vals]
+            rp[2 * i + j], ci[2 * i + j], v[2 * i + j] = r.ctypes.data, c.ctypes.data, vals.ctypes.data
+    rs = np.array(row_sizes, np.int32)
+    cs = np.array(col_sizes, np.int32)
+    keep += [rs, cs]
+    return rs, cs, rp, ci, v, keep
+
+
+def _plain(csr):
+    return [[csr, None], [None, None]], (csr[0], 0), (csr[1], 0)
+
+
+def block_spmv(blocks, row_sizes, col_sizes, x):
+    """orc_block_spmv (data.hpp:236-250, solver.hpp:33-58)."""
+    rs, cs, rp, ci, v, keep = _blocks(blocks, row_sizes, col_sizes)
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.zeros(int(rs.sum()))
+    orc().orc_block_spmv(ip(rs), ip(cs), rp, ci, v, dp(x), dp(y))
+    return y
+
+
+def spmv(csr, x):
+    return block_spmv(*_plain(csr), x)
+
+
+def cg(op, b, x0=None, rtol=1e-8, atol=1e-14, maxit=1000, jacobi=False, nested=None):
+    """orc_cg (solver.hpp:80-207).  op: CSR operand or (blocks, row_sizes, col_sizes)."""
+    if nested is None:
+        nested = isinstance(op, tuple) and len(op) == 3
+    blocks, rsz, csz = op if nested else _plain(op)
+    rs, cs, rp, ci, v, keep = _blocks(blocks, rsz, csz)
+    b = np.ascontiguousarray(b, np.float64)
+    x = np.zeros(len(b)) if x0 is None else np.array(x0, np.float64)
+    rep = np.zeros(3, np.int32)
+    rn = np.zeros(1)
+    fail = np.zeros(1, np.int32)
+    L = orc()
+    rc = L.orc_cg(ip(rs), ip(cs), rp, ci, v, int(nested), dp(b), dp(x), C.c_double(rtol), C.c_double(atol),
+                  int(maxit), int(jacobi), ip(rep), dp(rn), ip(fail))
+    if rc:
+        raise KindError(rc, f"fail={int(fail[0])}")
+    return x, {"iterations": int(rep[0]), "converged": bool(rep[1]), "reason": ("rtol", "atol", "maxit")[rep[2]],
+               "final_residual_norm": float(rn[0])}
+
+
+def ref_block_spmv(blocks, row_sizes, col_sizes, x):
+    """The compiled reference's block_spmv (solver.hpp:33-58)."""
+    rs, cs, rp, ci, v, keep = _blocks(blocks, row_sizes, col_sizes)
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.zeros(max(int(rs.sum()), 1))
+    L = ref()
+    rc = L.ref_block_spmv(ip(rs), ip(cs), rp, ci, v, dp(x), C.c_int64(len(x)), dp(y))
+    if rc:
+        raise KindError(rc, L.ref_last_error().decode())
+    return y[: int(rs.sum())]
+
+
+def ref_spmv(csr, x):
+    """The compiled reference's mat_spmv (data.hpp:236-250)."""
+    n, m, r, c, vals = csr
+    r, c, vals = np.ascontiguousarray(r, np.int64), np.ascontiguousarray(c, np.int32), np.ascontiguousarray(vals)
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.zeros(max(n, 1))
+    L = ref()
+    rc = L.ref_spmv(int(n), int(m), r.ctypes.data_as(I64P), ip(c), dp(vals), dp(x), C.c_int64(len(x)), dp(y))
+    if rc:
+        raise KindError(rc, L.ref_last_error().decode())
+    return y[:n]
+
+
+def ref_cg(op, b, x0=None, rtol=1e-8, atol=1e-14, maxit=1000, jacobi=False, nested=None):
+    """The compiled reference's cg_solve (solver.hpp:170-207)."""
+    if nested is None:
+        nested = isinstance(op, tuple) and len(op) == 3
+    blocks, rsz, csz = op if nested else _plain(op)
+    rs, cs, rp, ci, v, keep = _blocks(blocks, rsz, csz)
+    b = np.ascontiguousarray(b, np.float64)
+    x = np.zeros(len(b)) if x0 is None else np.array(x0, np.float64)
+    oi = np.zeros(3, np.int32)
+    od = np.zeros(1)
+    L = ref()
+    rc = L.ref_cg_solve(int(nested), ip(rs), ip(cs), rp, ci, v, dp(b), C.c_int64(len(b)), dp(x),
+                        C.c_int64(len(x)), C.c_double(rtol), C.c_double(atol), int(maxit), int(jacobi), ip(oi), dp(od))
+    if rc:
+        raise KindError(rc, L.ref_last_error().decode())
+    return x, {"iterations": int(oi[0]), "converged": bool(oi[1]), "reason": ("rtol", "atol", "maxit")[oi[2]],
+               "final_residual_norm": float(od[0])}

@@ -631,3 +631,124 @@ int orc_assemble_matrix_colored(int form, int degree, int gdim, const double* pa
     }
   return 0;
 }
+
+
+/* ---- consumers of the assembled matrix ------------------- */
+
+/* data.hpp:236-250 mat_spmv / solver.hpp:33-58 block_spmv */
+void orc_block_spmv(const int32_t* rs, const int32_t* cs, const int64_t* const* rp, const int32_t* const* ci,
+                    const double* const* v, const double* x, double* y) {
+  int out = 0;
+  for (int bi = 0; bi < 2; ++bi)
+    for (int r = 0; r < rs[bi]; ++r) {
+      double acc = 0.0;
+      int col_off = 0;
+      for (int bj = 0; bj < 2; ++bj) {
+        const int k = 2 * bi + bj;
+        if (rp[k])
+          for (int64_t e = rp[k][r]; e < rp[k][r + 1]; ++e) {
+            const double prod = v[k][e] * x[col_off + ci[k][e]];
+            acc = acc + prod;
+          }
+        col_off += cs[bj];
+      }
+      y[out++] = acc;
+    }
+}
+
+static double orc_dot(const double* a, const double* c, int n) { /* solver.hpp:93-97 */
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i) acc += a[i] * c[i];
+  return acc;
+}
+
+/* solver.hpp:64-76: 1 / A(r, r), Mat::at = 0 outside the pattern */
+static int orc_inv_diag(int n, const int64_t* rp, const int32_t* ci, const double* v, double* inv) {
+  for (int r = 0; r < n; ++r) {
+    double d = 0.0;
+    for (int64_t e = rp[r]; e < rp[r + 1]; ++e)
+      if (ci[e] == r) d = v[e];
+    if (!(d > 0.0)) return r;
+    inv[r] = 1.0 / d;
+  }
+  return -1;
+}
+
+int orc_cg(const int32_t* rs, const int32_t* cs, const int64_t* const* rp, const int32_t* const* ci,
+           const double* const* v, int nested, const double* b, double* x, double rtol, double atol, int maxit,
+           int jacobi, int32_t* report, double* rnorm_out, int32_t* fail) {
+  const int n = rs[0] + rs[1];
+  double *inv = NULL, *r = malloc(sizeof(double) * (n + 1)), *z = malloc(sizeof(double) * (n + 1)),
+         *p = malloc(sizeof(double) * (n + 1)), *q = malloc(sizeof(double) * (n + 1));
+  int rc = 0;
+  report[0] = 0;
+  report[1] = 0;
+  report[2] = 2;
+  if (jacobi) { /* solver.hpp:180-201 */
+    inv = malloc(sizeof(double) * (n + 1));
+    int off = 0;
+    for (int i = 0; i < (nested ? 2 : 1); ++i) {
+      const int k = 3 * i; /* diagonal block (i, i) */
+      int bad = rp[k] ? orc_inv_diag(rs[i], rp[k], ci[k], v[k], inv + off) : 0;
+      if (bad >= 0) {
+        *fail = bad;
+        rc = ORC_ERR_INDEFINITE;
+        goto done;
+      }
+      off += rs[i];
+    }
+  }
+  { /* cg_iterate, solver.hpp:88-167 */
+    const double target = fmax(rtol * sqrt(orc_dot(b, b, n)), atol);
+    orc_block_spmv(rs, cs, rp, ci, v, x, q);
+    for (int i = 0; i < n; ++i) r[i] = b[i] - q[i];
+    double rnorm = sqrt(orc_dot(r, r, n));
+    if (rnorm <= target) {
+      report[1] = 1;
+      report[2] = rnorm <= atol ? 1 : 0;
+      *rnorm_out = rnorm;
+      goto done;
+    }
+    for (int i = 0; i < n; ++i) z[i] = inv ? inv[i] * r[i] : r[i];
+    for (int i = 0; i < n; ++i) p[i] = z[i];
+    double rz = orc_dot(r, z, n);
+    for (int it = 1; it <= maxit; ++it) {
+      orc_block_spmv(rs, cs, rp, ci, v, p, q);
+      const double pq = orc_dot(p, q, n);
+      if (!(pq > 0.0)) {
+        *fail = it;
+        rc = ORC_ERR_INDEFINITE;
+        goto done;
+      }
+      const double alpha = rz / pq;
+      for (int i = 0; i < n; ++i) x[i] += alpha * p[i];
+      for (int i = 0; i < n; ++i) r[i] -= alpha * q[i];
+      report[0] = it;
+      rnorm = sqrt(orc_dot(r, r, n));
+      if (rnorm <= target) {
+        orc_block_spmv(rs, cs, rp, ci, v, x, q);
+        for (int i = 0; i < n; ++i) r[i] = b[i] - q[i];
+        rnorm = sqrt(orc_dot(r, r, n));
+        if (rnorm <= target) {
+          report[1] = 1;
+          report[2] = rnorm <= atol ? 1 : 0;
+          *rnorm_out = rnorm;
+          goto done;
+        }
+      }
+      for (int i = 0; i < n; ++i) z[i] = inv ? inv[i] * r[i] : r[i];
+      const double rz_next = orc_dot(r, z, n);
+      const double beta = rz_next / rz;
+      rz = rz_next;
+      for (int i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+    }
+    *rnorm_out = rnorm;
+  }
+done:
+  free(inv);
+  free(r);
+  free(z);
+  free(p);
+  free(q);
+  return rc;
+}

@@ -118,6 +118,26 @@ int orc_assemble_matrix_colored(int form, int degree, int gdim, const double* pa
                                 int nrows, const int64_t* row_ptr, const int32_t* col_idx,
                                 const int32_t* colors, int ncolors, double* values);
 
+/* ---- consumers of the assembled matrix ---------------------
+ * A nested operator is 2x2 blocks given as arrays of 4 row-major (i, j)
+ * pointers; a null row_ptr is a zero block (solver.hpp:21-28).  A plain Mat
+ * is block (0, 0) with row_sizes = {nrows, 0}, col_sizes = {ncols, 0}. */
+
+/* y = A x: rows ascending, entries folded in column order, acc += v * x with a
+ * separate multiply and add (data.hpp:236-250; solver.hpp:33-58 for nested). */
+void orc_block_spmv(const int32_t* row_sizes, const int32_t* col_sizes, const int64_t* const* row_ptr,
+                    const int32_t* const* col_idx, const double* const* values, const double* x, double* y);
+
+/* cg_iterate (solver.hpp:80-168) with cg_solve's Jacobi set-up
+ * (solver.hpp:64-76, 180-201).  x: x0 in, iterate out.  Returns 0, or
+ * ORC_ERR_INDEFINITE (non-positive Jacobi diagonal: *fail = row; p'Ap <= 0:
+ * *fail = iteration).  report: iterations, converged, reason (0 rtol, 1 atol,
+ * 2 maxit); *rnorm = final residual norm. */
+#define ORC_ERR_INDEFINITE 20
+int orc_cg(const int32_t* row_sizes, const int32_t* col_sizes, const int64_t* const* row_ptr,
+           const int32_t* const* col_idx, const double* const* values, int nested, const double* b, double* x,
+           double rtol, double atol, int maxit, int jacobi, int32_t* report, double* rnorm, int32_t* fail);
+
 #ifdef __cplusplus
 }
 #endif

@@ -397,4 +397,87 @@ int ref_time_execute(int form, int degree, int gdim, const double* params, int n
   }
 }
 
+// ---- consumers of the assembled matrix (data.hpp:236-250, solver.hpp) ----
+// A block is given as (nrows, ncols, row_offsets, col_indices, values); a null
+// row_offsets pointer is a zero block.
+
+}  // extern "C" (helpers below are C++)
+
+namespace {
+MatPtr mat_from_csr(int nrows, int ncols, const int64_t* rp, const int32_t* ci, const double* v) {
+  std::vector<long> offs(rp, rp + nrows + 1);
+  std::vector<int> cols(ci, ci + rp[nrows]);
+  auto sp = std::make_shared<const Sparsity>(nrows, ncols, std::move(offs), std::move(cols));
+  auto m = make_mat(sp);
+  std::memcpy(m->values().data(), v, sizeof(double) * static_cast<size_t>(rp[nrows]));
+  return m;
+}
+
+BlockMat block_from_csr(const int32_t* rs, const int32_t* cs, const int64_t* const* rp, const int32_t* const* ci,
+                        const double* const* v) {
+  BlockMat op;
+  for (int i = 0; i < 2; ++i) {
+    op.row_sizes[i] = rs[i];
+    op.col_sizes[i] = cs[i];
+    for (int j = 0; j < 2; ++j)
+      if (rp[2 * i + j]) op.blocks[i][j] = mat_from_csr(rs[i], cs[j], rp[2 * i + j], ci[2 * i + j], v[2 * i + j]);
+  }
+  return op;
+}
+
+void report_out(const SolveReport& r, int32_t* out_i, double* out_d) {
+  out_i[0] = r.iterations;
+  out_i[1] = r.converged ? 1 : 0;
+  out_i[2] = r.reason == SolveReport::Reason::rtol ? 0 : (r.reason == SolveReport::Reason::atol ? 1 : 2);
+  out_d[0] = r.final_residual_norm;
+}
+} // namespace
+
+extern "C" {
+
+// data.hpp:236-250
+int ref_spmv(int nrows, int ncols, const int64_t* rp, const int32_t* ci, const double* v, const double* x,
+             int64_t xlen, double* y) {
+  try {
+    auto m = mat_from_csr(nrows, ncols, rp, ci, v);
+    auto out = mat_spmv(*m, std::span<const Real>(x, static_cast<size_t>(xlen)));
+    std::memcpy(y, out.data(), sizeof(double) * out.size());
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
+// solver.hpp:33-58; rp/ci/v: 4 block pointers in row-major (i, j) order
+int ref_block_spmv(const int32_t* rs, const int32_t* cs, const int64_t* const* rp, const int32_t* const* ci,
+                   const double* const* v, const double* x, int64_t xlen, double* y) {
+  try {
+    auto op = block_from_csr(rs, cs, rp, ci, v);
+    auto out = block_spmv(op, std::span<const Real>(x, static_cast<size_t>(xlen)));
+    std::memcpy(y, out.data(), sizeof(double) * out.size());
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
+// solver.hpp:170-207 (nested = 0: block (0, 0) as a plain Mat); x: x0 in, iterate out
+int ref_cg_solve(int nested, const int32_t* rs, const int32_t* cs, const int64_t* const* rp,
+                 const int32_t* const* ci, const double* const* v, const double* b, int64_t blen, double* x,
+                 int64_t xlen, double rtol, double atol, int maxit, int jacobi, int32_t* out_i, double* out_d) {
+  try {
+    std::vector<Real> x0(x, x + xlen);
+    const auto pc = jacobi ? Preconditioner::Jacobi : Preconditioner::None;
+    std::span<const Real> bs(b, static_cast<size_t>(blen));
+    std::pair<std::vector<Real>, SolveReport> res;
+    if (nested) res = cg_solve(block_from_csr(rs, cs, rp, ci, v), bs, x0, rtol, atol, maxit, pc);
+    else res = cg_solve(*mat_from_csr(rs[0], cs[0], rp[0], ci[0], v[0]), bs, x0, rtol, atol, maxit, pc);
+    std::memcpy(x, res.first.data(), sizeof(double) * res.first.size());
+    report_out(res.second, out_i, out_d);
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
 } // extern "C"

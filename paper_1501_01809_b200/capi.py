@@ -79,6 +79,16 @@ class KernelDesc(C.Structure):
     _fields_ = [("name", C.c_char_p), ("params", C.POINTER(C.c_double)), ("nparams", C.c_int32)]
 
 
+class BlockMatDesc(C.Structure):  # loam_block_mat (solver.hpp:21-28 BlockMat)
+    _fields_ = [("sparsity", (C.POINTER(SparsityDesc) * 2) * 2), ("values", (C.c_void_p * 2) * 2),
+                ("row_sizes", C.c_int32 * 2), ("col_sizes", C.c_int32 * 2)]
+
+
+class SolveReportDesc(C.Structure):  # loam_solve_report (solver.hpp:13-18)
+    _fields_ = [("iterations", C.c_int32), ("final_residual_norm", C.c_double), ("converged", C.c_int32),
+                ("reason", C.c_int32)]
+
+
 _lib = None
 
 
@@ -122,6 +132,12 @@ def lib() -> C.CDLL:
             "loam_gpu_uniform": (C.c_int, [i64, u64, C.c_double, C.c_double, dp]),
             "loam_gpu_p2_cell_node_map": (C.c_int, [C.c_int, C.c_int, C.c_int, ip, ip]),
             "loam_gpu_expand_map": (C.c_int, [C.c_int, C.c_int, ip, C.c_int, ip]),
+            "loam_gpu_spmv": (C.c_int, [C.POINTER(SparsityDesc), vp, vp, i64, vp, vp]),
+            "loam_gpu_block_spmv": (C.c_int, [C.POINTER(BlockMatDesc), vp, i64, vp, vp]),
+            "loam_gpu_cg_solve": (C.c_int, [C.POINTER(SparsityDesc), vp, vp, i64, vp, C.c_double, C.c_double,
+                                            i32, i32, C.POINTER(SolveReportDesc), vp]),
+            "loam_gpu_cg_solve_block": (C.c_int, [C.POINTER(BlockMatDesc), vp, i64, vp, C.c_double, C.c_double,
+                                                  i32, i32, C.POINTER(SolveReportDesc), vp]),
         }
         for name, (res, args) in proto.items():
             fn = getattr(L, name)
@@ -141,7 +157,8 @@ EXPORTED = [
     "loam_gpu_host_free", "loam_gpu_memcpy", "loam_gpu_memset", "loam_gpu_stream_sync",
     "loam_gpu_unit_square_mesh", "loam_gpu_unit_cube_mesh", "loam_gpu_jitter",
     "loam_gpu_permute_cells", "loam_gpu_uniform", "loam_gpu_p2_cell_node_map",
-    "loam_gpu_expand_map",
+    "loam_gpu_expand_map", "loam_gpu_spmv", "loam_gpu_block_spmv", "loam_gpu_cg_solve",
+    "loam_gpu_cg_solve_block",
 ]
 
 

@@ -12,6 +12,7 @@
 
 #include "engine.cuh"
 #include "plan.cuh"
+#include "solver.cuh"
 
 using namespace loam_gpu;
 
@@ -253,6 +254,58 @@ int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t n, uint64_t it
       if (count) LG_CUDA(cudaMemcpyAsync(a.data, dargs[q].data, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
     }
     LG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int loam_gpu_spmv(const loam_sparsity_desc* sparsity, const double* values, const double* x, int64_t x_len,
+                  double* y, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(sparsity != nullptr, LOAM_ERR(InvalidArgument), "spmv without a sparsity");
+    spmv(single_block(sparsity, values), x, x_len, y, false, as_stream(stream));
+  });
+}
+
+namespace {
+BlockOperator block_op(const loam_block_mat* op) {
+  require(op != nullptr, LOAM_ERR(InvalidArgument), "null block operator");
+  BlockOperator B;
+  for (int i = 0; i < 2; ++i) {
+    B.row_sizes[i] = op->row_sizes[i];
+    B.col_sizes[i] = op->col_sizes[i];
+    for (int j = 0; j < 2; ++j) {
+      B.sparsity[i][j] = op->sparsity[i][j];
+      B.values[i][j] = op->values[i][j];
+    }
+  }
+  return B;
+}
+} // namespace
+
+int loam_gpu_block_spmv(const loam_block_mat* op, const double* x, int64_t x_len, double* y, void* stream) {
+  return guarded([&] {
+    require_device();
+    spmv(block_op(op), x, x_len, y, true, as_stream(stream));
+  });
+}
+
+int loam_gpu_cg_solve(const loam_sparsity_desc* sparsity, const double* values, const double* b, int64_t b_len,
+                      double* x, double rtol, double atol, int32_t maxit, int32_t jacobi, loam_solve_report* report,
+                      void* stream) {
+  return guarded([&] {
+    require_device();
+    require(sparsity != nullptr && report != nullptr, LOAM_ERR(InvalidArgument), "cg without matrix or report");
+    *report = cg_solve(single_block(sparsity, values), b, b_len, x, rtol, atol, maxit, jacobi != 0, false,
+                       as_stream(stream));
+  });
+}
+
+int loam_gpu_cg_solve_block(const loam_block_mat* op, const double* b, int64_t b_len, double* x, double rtol,
+                            double atol, int32_t maxit, int32_t jacobi, loam_solve_report* report, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(report != nullptr, LOAM_ERR(InvalidArgument), "cg without a report");
+    *report = cg_solve(block_op(op), b, b_len, x, rtol, atol, maxit, jacobi != 0, true, as_stream(stream));
   });
 }
 

@@ -509,3 +509,98 @@ def execute(loop: Parloop, threads: int = 1) -> None:
                 a.dat._zero = a.dat._stale = False
             if a.mat is not None:
                 a.mat._zero = a.mat._stale = False
+
+
+# --------------------------------------------------------------------------
+# Consumers of the assembled matrix: data.hpp:236-250,
+# solver.hpp:13-207, on the device through the C ABI.
+
+def mat_spmv(mat: Mat, x) -> torch.Tensor:
+    """y = A x (data.hpp:236-250), bitwise equal to the reference's CSR fold."""
+    mat._materialize()
+    xt = torch.as_tensor(np.asarray(x, dtype=np.float64) if not isinstance(x, torch.Tensor) else x,
+                         dtype=torch.float64).to("cuda").contiguous()
+    y = torch.empty(max(mat.nrows, 1), dtype=torch.float64, device="cuda")
+    capi.check(capi.lib().loam_gpu_spmv(mat.sparsity.desc(), mat.values.data_ptr(), xt.data_ptr(), xt.numel(),
+                                        y.data_ptr(), _stream()))
+    return y[: mat.nrows]
+
+
+class BlockMat:
+    """solver.hpp:21-28: 2x2 table of blocks; None is a zero block."""
+
+    def __init__(self, blocks=None, row_sizes=(0, 0), col_sizes=(0, 0)):
+        self.blocks = [[None, None], [None, None]] if blocks is None else [list(r) for r in blocks]
+        self.row_sizes, self.col_sizes = list(row_sizes), list(col_sizes)
+
+    @property
+    def nrows(self):
+        return sum(self.row_sizes)
+
+    @property
+    def ncols(self):
+        return sum(self.col_sizes)
+
+    def desc(self):
+        d = capi.BlockMatDesc()
+        keep = []
+        for i in range(2):
+            d.row_sizes[i], d.col_sizes[i] = self.row_sizes[i], self.col_sizes[i]
+            for j in range(2):
+                m = self.blocks[i][j]
+                if m is not None:
+                    m._materialize()
+                    sd = m.sparsity.desc()
+                    keep.append(sd)
+                    d.sparsity[i][j] = C.pointer(sd)
+                    d.values[i][j] = m.values.data_ptr()
+        return d, keep
+
+
+def _vec(x, n=None) -> torch.Tensor:
+    t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x, dtype=np.float64))
+    return t.to(device="cuda", dtype=torch.float64).contiguous()
+
+
+def block_spmv(op: BlockMat, x) -> torch.Tensor:
+    """solver.hpp:33-58, bitwise equal to the reference's nested fold."""
+    xt = _vec(x)
+    y = torch.empty(max(op.nrows, 1), dtype=torch.float64, device="cuda")
+    d, keep = op.desc()
+    capi.check(capi.lib().loam_gpu_block_spmv(C.byref(d), xt.data_ptr(), xt.numel(), y.data_ptr(), _stream()))
+    return y[: op.nrows]
+
+
+class SolveReport:
+    """solver.hpp:13-18."""
+    REASONS = ("rtol", "atol", "maxit")
+
+    def __init__(self, r: capi.SolveReportDesc):
+        self.iterations = int(r.iterations)
+        self.final_residual_norm = float(r.final_residual_norm)
+        self.converged = bool(r.converged)
+        self.reason = self.REASONS[int(r.reason)]
+
+
+class Preconditioner:
+    NONE, JACOBI = 0, 1
+
+
+def cg_solve(op, b, x0=None, rtol: float = 1e-8, atol: float = 1e-14, maxit: int = 1000,
+             precond: int = Preconditioner.NONE):
+    """solver.hpp:170-207 (Mat or BlockMat): returns (x, SolveReport)."""
+    bt = _vec(b)
+    n = bt.numel()
+    if x0 is not None and len(x0) != 0:
+        _require(len(x0) == n, "DimensionMismatch", "x0 length != rhs length")  # solver.hpp:90
+    x = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda") if x0 is None or len(x0) == 0 else _vec(x0).clone()
+    rep = capi.SolveReportDesc()
+    if isinstance(op, BlockMat):
+        d, keep = op.desc()
+        capi.check(capi.lib().loam_gpu_cg_solve_block(C.byref(d), bt.data_ptr(), n, x.data_ptr(), rtol, atol,
+                                                      maxit, precond, C.byref(rep), _stream()))
+    else:
+        op._materialize()
+        capi.check(capi.lib().loam_gpu_cg_solve(op.sparsity.desc(), op.values.data_ptr(), bt.data_ptr(), n,
+                                                x.data_ptr(), rtol, atol, maxit, precond, C.byref(rep), _stream()))
+    return x[:n], SolveReport(rep)
