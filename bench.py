@@ -406,6 +406,81 @@ def all_configs(args):
     return 0
 
 
+def solver_bench(args):
+    """Developer lines for SURVEY 8f-1: device SpMV on assembled config
+    matrices against the HBM roofline, and CG time per iteration on the C2-size
+    P1 Helmholtz matrix next to the reference's cg_solve on the host."""
+    import torch
+    from paper_1501_01809_b200 import configs
+    from paper_1501_01809_b200 import loam as L
+    torch.cuda.set_device(0)
+    peak, peak_kind = peaks()
+    flush = Flusher(torch)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for cfg in [int(c) for c in (args.configs or "2,4,5").split(",")]:
+        w = configs.Workload(cfg, args.size)
+        w.reset()
+        w.run()
+        mats = [o for o in w.outputs if isinstance(o, L.Mat)]
+        if cfg == 5:
+            Am, BTm, Bm = mats
+            op = L.BlockMat([[Am, BTm], [Bm, None]], (Am.nrows, Bm.nrows), (Am.ncols, BTm.ncols))
+            run = lambda x: L.block_spmv(op, x)
+            nnz = sum(m.sparsity.nnz for m in mats)
+            nrows, ncols = op.nrows, op.ncols
+            rp_bytes = 8 * sum(m.nrows + 1 for m in mats)
+        else:
+            A = mats[0]
+            run = lambda x: L.mat_spmv(A, x)
+            nnz, nrows, ncols = A.sparsity.nnz, A.nrows, A.ncols
+            rp_bytes = 8 * (nrows + 1)
+        x = torch.rand(ncols, dtype=torch.float64, device="cuda")
+        for _ in range(3):
+            run(x)
+        times = []
+        for _ in range(args.steps):
+            flush()
+            e0.record(stream)
+            run(x)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = float(np.median(times))
+        abytes = nnz * 12 + rp_bytes + ncols * 8 + nrows * 8
+        achieved = abytes / (ms * 1e-3) / 1e9
+        print(json.dumps({"solver": "spmv", "config": cfg, "nnz": nnz, "rows": nrows, "ms": ms,
+                          "algorithmic_MB": abytes / 1e6, "GB_s": achieved, "frac": achieved / peak,
+                          "peak_kind": peak_kind, "bitwise": "reference mat_spmv / block_spmv"}), flush=True)
+    # CG per iteration: P1 Helmholtz (SPD) on the C2 mesh, fixed iteration count
+    import oracle as O
+    for n, on_ref in ((1024, False), (256, True)):
+        m = configs.config_inputs(2, n)
+        cells, verts = L.Set(m.ncells), L.Set(m.nv)
+        cv = L.Map(cells, verts, 3, m.cv)
+        X = L.Dat(verts, 2)
+        X.set_values(m.coords)
+        A = L.Mat(L.build_sparsity(cv, cv))
+        L.execute(L.Parloop(L.kernel("helmholtz_p1_tri", 1.0), cells, [L.arg(A, L.INC, cv, cv), L.arg(X, L.READ, cv)]))
+        b = np.random.default_rng(1).uniform(-1, 1, m.nv)
+        its = 200
+        L.cg_solve(A, b, rtol=1e-30, atol=0.0, maxit=5)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x, rep = L.cg_solve(A, b, rtol=1e-30, atol=0.0, maxit=its)
+        torch.cuda.synchronize()
+        gpu_ms = (time.perf_counter() - t0) * 1e3 / rep.iterations
+        line = {"solver": "cg", "mesh": f"{n}^2 P1 Helmholtz", "rows": m.nv, "nnz": A.sparsity.nnz,
+                "iterations": rep.iterations, "gpu_ms_per_iteration": gpu_ms}
+        if on_ref and O.ref_available():
+            rp, ci = A.sparsity.host()
+            t0 = time.perf_counter()
+            xr, rr = O.ref_cg((m.nv, m.nv, rp, ci, A.host_values()), b, rtol=1e-30, atol=0.0, maxit=its)
+            line["reference_cpu_ms_per_iteration"] = (time.perf_counter() - t0) * 1e3 / rr["iterations"]
+            line["reference_iterations"] = rr["iterations"]
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -418,7 +493,10 @@ def main():
     ap.add_argument("--configs", default="")
     ap.add_argument("--strategies", default="auto,owner,atomic,warpagg,color")
     ap.add_argument("--size", type=int, default=None)
+    ap.add_argument("--solver", action="store_true", help="developer: SpMV roofline and CG per-iteration lines")
     args = ap.parse_args()
+    if args.solver:
+        return solver_bench(args)
     if args.impl == "reference":
         return reference_arm(args)
     if args.all_configs:

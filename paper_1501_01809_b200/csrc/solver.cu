@@ -101,6 +101,43 @@ __global__ void __launch_bounds__(kThreads) k_spmv(const __grid_constant__ Op op
   }
 }
 
+// Plain CSR with long rows (C4: 45 entries per dof row): the CTA's 256 rows
+// own one contiguous entry range, which is staged through shared memory in
+// coalesced chunks; each thread still folds its own row sequentially in
+// column order, so y stays bitwise equal to the reference.
+constexpr int kChunk = 2048; // entries per staged chunk (24 KB)
+__global__ void __launch_bounds__(kThreads) k_spmv_staged(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                          const double* __restrict__ v, int n,
+                                                          const double* __restrict__ x, double* __restrict__ y,
+                                                          const double* __restrict__ w, double* partials,
+                                                          const CgState* st, int gate) {
+  if (gated_off(st, gate)) return;
+  __shared__ double sv[kChunk];
+  __shared__ int32_t sc[kChunk];
+  const int r0 = blockIdx.x * blockDim.x, row = r0 + threadIdx.x;
+  const int r1 = min(n, r0 + (int)blockDim.x);
+  const int64_t e0 = __ldg(rp + r0), e1 = __ldg(rp + r1);
+  int64_t k = row < n ? __ldg(rp + row) : e1;
+  const int64_t kend = row < n ? __ldg(rp + row + 1) : e1;
+  double acc = 0.0;
+  for (int64_t c0 = e0; c0 < e1; c0 += kChunk) {
+    const int len = (int)(e1 - c0 < kChunk ? e1 - c0 : kChunk);
+    __syncthreads();
+    for (int t = threadIdx.x; t < len; t += blockDim.x) {
+      sv[t] = __ldg(v + c0 + t);
+      sc[t] = __ldg(ci + c0 + t);
+    }
+    __syncthreads();
+    const int64_t stop = kend < c0 + len ? kend : c0 + len;
+    for (; k < stop; ++k) acc = __dadd_rn(acc, __dmul_rn(sv[k - c0], __ldg(x + sc[k - c0])));
+  }
+  if (row < n) y[row] = acc;
+  if (partials) {
+    const double s = block_sum(row < n ? __dmul_rn(w[row], acc) : 0.0);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_dot(const double* __restrict__ a, const double* __restrict__ b,
                                                   int64_t n, double* partials) {
   double s = 0.0;
@@ -254,10 +291,15 @@ Op make_op(const BlockOperator& B) {
 }
 
 void launch_spmv(const Op& op, const double* x, double* y, const double* w, double* partials, const CgState* st,
-                 int gate, cudaStream_t s) {
+                 int gate, cudaStream_t s, int64_t nnz_hint = 0) {
   const int n = op.rs[0] + op.rs[1];
   if (n == 0) return;
-  k_spmv<<<ceil_div(n, kThreads), kThreads, 0, s>>>(op, x, y, w, partials, st, gate);
+  const bool plain = op.rs[1] == 0 && !op.rp[0][1] && !op.rp[1][0] && !op.rp[1][1];
+  if (plain && nnz_hint > (int64_t)16 * n) // long rows: coalesced staging
+    k_spmv_staged<<<ceil_div(n, kThreads), kThreads, 0, s>>>(op.rp[0][0], op.ci[0][0], op.v[0][0], n, x, y, w,
+                                                               partials, st, gate);
+  else
+    k_spmv<<<ceil_div(n, kThreads), kThreads, 0, s>>>(op, x, y, w, partials, st, gate);
   count_launch();
   LG_LAUNCH_CHECK();
 }
@@ -268,6 +310,14 @@ void check_layout(const BlockOperator& B) {
       if (const loam_sparsity_desc* sp = B.sparsity[i][j])
         require(sp->nrows == B.row_sizes[i] && sp->ncols == B.col_sizes[j], LOAM_ERR(DimensionMismatch),
                 "block shape inconsistent with layout");
+}
+
+int64_t nnz_of(const BlockOperator& B) {
+  int64_t z = 0;
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j)
+      if (B.sparsity[i][j]) z += B.sparsity[i][j]->nnz;
+  return z;
 }
 
 } // namespace
@@ -289,11 +339,40 @@ void spmv(const BlockOperator& B, const double* x, int64_t x_len, double* y, boo
   } else {
     require(x_len == B.col_sizes[0], LOAM_ERR(DimensionMismatch), "spmv operand length != matrix column count");
   }
-  launch_spmv(make_op(B), x, y, nullptr, nullptr, nullptr, kAlways, s);
+  launch_spmv(make_op(B), x, y, nullptr, nullptr, nullptr, kAlways, s, nnz_of(B));
 }
 
+namespace {
+// CG runs on a private non-blocking stream (graph capture is not allowed on
+// the legacy default stream), ordered after / before the caller's stream.
+cudaStream_t solver_stream() {
+  static cudaStream_t cs = [] {
+    cudaStream_t t;
+    LG_CUDA(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+    return t;
+  }();
+  return cs;
+}
+struct StreamJoin {
+  cudaStream_t user, own;
+  cudaEvent_t ev;
+  StreamJoin(cudaStream_t u) : user(u), own(solver_stream()) {
+    LG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    LG_CUDA(cudaEventRecord(ev, user));
+    LG_CUDA(cudaStreamWaitEvent(own, ev, 0));
+  }
+  ~StreamJoin() {
+    cudaEventRecord(ev, own);
+    cudaStreamWaitEvent(user, ev, 0);
+    cudaEventDestroy(ev);
+  }
+};
+} // namespace
+
 loam_solve_report cg_solve(const BlockOperator& B, const double* b, int64_t b_len, double* x, double rtol,
-                           double atol, int maxit, bool jacobi, bool nested, cudaStream_t s) {
+                           double atol, int maxit, bool jacobi, bool nested, cudaStream_t user_stream) {
+  StreamJoin join(user_stream);
+  const cudaStream_t s = join.own;
   const int64_t n = (int64_t)B.row_sizes[0] + B.row_sizes[1];
   if (nested) {
     require(n == (int64_t)B.col_sizes[0] + B.col_sizes[1], LOAM_ERR(DimensionMismatch), "cg needs a square operator");
@@ -342,7 +421,8 @@ loam_solve_report cg_solve(const BlockOperator& B, const double* b, int64_t b_le
     LG_LAUNCH_CHECK();
   };
   // prologue (solver.hpp:101-132): r = b - A x0, target, early exit, z, p, rz
-  launch_spmv(op, x, q.get(), nullptr, nullptr, nullptr, kAlways, s);
+  const int64_t nnz = nnz_of(B);
+  launch_spmv(op, x, q.get(), nullptr, nullptr, nullptr, kAlways, s, nnz);
   k_residual<<<vb, kThreads, 0, s>>>(r.get(), b, q.get(), n, nullptr, kAlways, partials.get());
   count_launch();
   dot_finish(vb, kInitRn, kAlways);
@@ -361,18 +441,18 @@ loam_solve_report cg_solve(const BlockOperator& B, const double* b, int64_t b_le
   k_precond<<<vb, kThreads, 0, s>>>(z.get(), r.get(), invp, p.get(), n, nullptr, kAlways, partials.get());
   count_launch();
   dot_finish(vb, kInitRz, kAlways);
-  // iterations (solver.hpp:134-167) in batches; every kernel is gated
-  constexpr int kBatch = 16;
-  int launched = 0;
-  while (launched < maxit) {
-    const int nb = std::min(kBatch, maxit - launched);
-    for (int t = 0; t < nb; ++t) {
-      launch_spmv(op, p.get(), q.get(), p.get(), partials.get(), st.get(), kNotDone, s);
+  // iterations (solver.hpp:134-167) in batches; every kernel is gated, so a
+  // batch may run past convergence / breakdown without effect.  A full batch
+  // is captured once into a CUDA graph and replayed (10 launches per
+  // iteration would otherwise be launch-bound on small systems).
+  auto enqueue = [&](int iters) {
+    for (int t = 0; t < iters; ++t) {
+      launch_spmv(op, p.get(), q.get(), p.get(), partials.get(), st.get(), kNotDone, s, nnz);
       dot_finish(sb, kPq, kNotDone);
       k_axpy2<<<vb, kThreads, 0, s>>>(x, r.get(), p.get(), q.get(), n, st.get(), partials.get());
       count_launch();
       dot_finish(vb, kRn, kNotDone);
-      launch_spmv(op, x, q.get(), nullptr, nullptr, st.get(), kRecheck, s);
+      launch_spmv(op, x, q.get(), nullptr, nullptr, st.get(), kRecheck, s, nnz);
       k_residual<<<vb, kThreads, 0, s>>>(r.get(), b, q.get(), n, st.get(), kRecheck, partials.get());
       count_launch();
       dot_finish(vb, kTrue, kRecheck);
@@ -383,11 +463,31 @@ loam_solve_report cg_solve(const BlockOperator& B, const double* b, int64_t b_le
       count_launch();
       LG_LAUNCH_CHECK();
     }
+  };
+  constexpr int kBatch = 16;
+  cudaGraphExec_t exec = nullptr;
+  int launched = 0;
+  while (launched < maxit) {
+    const int nb = std::min(kBatch, maxit - launched);
+    if (nb == kBatch && maxit >= 2 * kBatch) {
+      if (!exec) {
+        cudaGraph_t g;
+        LG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        enqueue(kBatch);
+        LG_CUDA(cudaStreamEndCapture(s, &g));
+        LG_CUDA(cudaGraphInstantiate(&exec, g, 0));
+        LG_CUDA(cudaGraphDestroy(g));
+      }
+      LG_CUDA(cudaGraphLaunch(exec, s));
+    } else {
+      enqueue(nb);
+    }
     launched += nb;
     LG_CUDA(cudaMemcpyAsync(&h, st.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
     LG_CUDA(cudaStreamSynchronize(s));
     if (h.done) break;
   }
+  if (exec) cudaGraphExecDestroy(exec);
   require(h.status == 0, LOAM_ERR(IndefiniteBreakdown),
           "p'Ap <= 0 after " + std::to_string(h.fail_it) + " iterations; matrix is not SPD");
   rep.iterations = h.it;
