@@ -15,6 +15,7 @@
 // that is synchronised on demand, so the reference's host-side idioms work.
 #pragma once
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cstdint>
 #include <memory>
@@ -353,6 +354,33 @@ public:
   }
   bool known_zero() const { return zero_; }
   uint64_t id() const { return id_; }
+  const double* device_values() const { // current values on the device (for spmv / cg)
+    materialize();
+    return values_.device();
+  }
+
+  /// data.hpp:205-222: add (INC) or overwrite (WRITE) a dense local block at
+  /// rows x cols -- the reference's host-side setter; every (row, col) pair
+  /// must lie inside the sparsity.
+  void addto(std::span<const int> rows, std::span<const int> cols, std::span<const Real> block,
+             Access mode = Access::INC) {
+    require(mode == Access::INC || mode == Access::WRITE, ErrorKind::IllegalAccess,
+            "Mats are write-only: only WRITE and INC are permitted");
+    require(block.size() == rows.size() * cols.size(), ErrorKind::ShapeMismatch,
+            "block shape does not match rows x cols");
+    materialize();
+    values_.download();
+    for (size_t i = 0; i < rows.size(); ++i)
+      for (size_t j = 0; j < cols.size(); ++j) {
+        const long pos = sparsity_->find(rows[i], cols[j]);
+        require(pos >= 0, ErrorKind::OutsideSparsity,
+                name_ + ": entry (" + std::to_string(rows[i]) + ", " + std::to_string(cols[j]) + ") outside sparsity");
+        if (mode == Access::INC) values_.host[pos] += block[i * cols.size() + j];
+        else values_.host[pos] = block[i * cols.size() + j];
+      }
+    values_.dev_stale = true;
+    zero_ = false;
+  }
 
 private:
   void materialize() const {
@@ -504,6 +532,127 @@ inline void execute(const Parloop& loop, int threads = 1) {
     if (a.mat) a.mat->touched_by_device();
     if (a.global) a.global->touched_by_device();
   }
+}
+
+// ---------------------------------------------------------------- matrix consumers
+namespace detail {
+inline DeviceArray<double>* to_device(std::span<const Real> v, std::unique_ptr<DeviceArray<double>>& keep) {
+  keep = std::make_unique<DeviceArray<double>>(v.size(), false);
+  if (!v.empty()) keep->upload(v.data());
+  return keep.get();
+}
+inline std::vector<Real> to_host(const DeviceArray<double>& d, size_t n) {
+  const auto& h = d.download();
+  return std::vector<Real>(h.begin(), h.begin() + n);
+}
+} // namespace detail
+
+/// y = A x by CSR traversal (data.hpp:236-250), bitwise equal to the reference.
+inline std::vector<Real> mat_spmv(const Mat& mat, std::span<const Real> x) {
+  std::unique_ptr<detail::DeviceArray<double>> dx;
+  detail::to_device(x, dx);
+  detail::DeviceArray<double> y(mat.nrows(), false);
+  const loam_sparsity_desc sp = mat.sparsity()->desc();
+  check(loam_gpu_spmv(&sp, mat.device_values(), dx->dev, (int64_t)x.size(), y.dev, nullptr));
+  check(loam_gpu_stream_sync(nullptr));
+  return detail::to_host(y, mat.nrows());
+}
+
+/// solver.hpp:21-28: 2x2 table of blocks; missing entries are zero blocks.
+struct BlockMat {
+  std::array<std::array<MatPtr, 2>, 2> blocks{};
+  std::array<int, 2> row_sizes{};
+  std::array<int, 2> col_sizes{};
+  int nrows() const { return row_sizes[0] + row_sizes[1]; }
+  int ncols() const { return col_sizes[0] + col_sizes[1]; }
+};
+
+namespace detail {
+struct BlockDesc {
+  loam_block_mat op{};
+  loam_sparsity_desc sp[2][2]{};
+  explicit BlockDesc(const BlockMat& B) {
+    for (int i = 0; i < 2; ++i) {
+      op.row_sizes[i] = B.row_sizes[i];
+      op.col_sizes[i] = B.col_sizes[i];
+      for (int j = 0; j < 2; ++j)
+        if (const MatPtr& m = B.blocks[i][j]) {
+          sp[i][j] = m->sparsity()->desc();
+          op.sparsity[i][j] = &sp[i][j];
+          op.values[i][j] = m->device_values();
+        }
+    }
+  }
+};
+} // namespace detail
+
+/// solver.hpp:33-58, bitwise equal to the reference.
+inline std::vector<Real> block_spmv(const BlockMat& op, std::span<const Real> x) {
+  detail::BlockDesc D(op);
+  std::unique_ptr<detail::DeviceArray<double>> dx;
+  detail::to_device(x, dx);
+  detail::DeviceArray<double> y(op.nrows(), false);
+  check(loam_gpu_block_spmv(&D.op, dx->dev, (int64_t)x.size(), y.dev, nullptr));
+  check(loam_gpu_stream_sync(nullptr));
+  return detail::to_host(y, op.nrows());
+}
+
+struct SolveReport { // solver.hpp:13-18
+  int iterations = 0;
+  Real final_residual_norm = 0.0;
+  bool converged = false;
+  enum class Reason { rtol, atol, maxit } reason = Reason::maxit;
+};
+
+enum class Preconditioner { None, Jacobi };
+
+namespace detail {
+inline SolveReport report_of(const loam_solve_report& r) {
+  SolveReport s;
+  s.iterations = r.iterations;
+  s.final_residual_norm = r.final_residual_norm;
+  s.converged = r.converged != 0;
+  s.reason = r.reason == 0 ? SolveReport::Reason::rtol
+                           : (r.reason == 1 ? SolveReport::Reason::atol : SolveReport::Reason::maxit);
+  return s;
+}
+template <class Call>
+std::pair<std::vector<Real>, SolveReport> cg_run(std::span<const Real> b, std::vector<Real> x0, Call&& call) {
+  if (x0.empty()) x0.assign(b.size(), 0.0);
+  require(x0.size() == b.size(), ErrorKind::DimensionMismatch, "x0 length != rhs length");
+  std::unique_ptr<DeviceArray<double>> db, dx;
+  to_device(b, db);
+  to_device(std::span<const Real>(x0.data(), x0.size()), dx);
+  loam_solve_report rep{};
+  check(call(db->dev, dx->dev, &rep));
+  check(loam_gpu_stream_sync(nullptr));
+  dx->host_valid = false;
+  return {to_host(*dx, b.size()), report_of(rep)};
+}
+} // namespace detail
+
+/// Preconditioned CG (solver.hpp:170-188), the iteration on the device.
+inline std::pair<std::vector<Real>, SolveReport> cg_solve(const Mat& mat, std::span<const Real> b,
+                                                          std::vector<Real> x0 = {}, Real rtol = 1e-8,
+                                                          Real atol = 1e-14, int maxit = 1000,
+                                                          Preconditioner precond = Preconditioner::None) {
+  const loam_sparsity_desc sp = mat.sparsity()->desc();
+  return detail::cg_run(b, std::move(x0), [&](const double* db, double* dx, loam_solve_report* rep) {
+    return loam_gpu_cg_solve(&sp, mat.device_values(), db, (int64_t)b.size(), dx, rtol, atol, maxit,
+                             precond == Preconditioner::Jacobi ? 1 : 0, rep, nullptr);
+  });
+}
+
+/// CG on a nested block operator over the flattened numbering (solver.hpp:190-207).
+inline std::pair<std::vector<Real>, SolveReport> cg_solve(const BlockMat& op, std::span<const Real> b,
+                                                          std::vector<Real> x0 = {}, Real rtol = 1e-8,
+                                                          Real atol = 1e-14, int maxit = 1000,
+                                                          Preconditioner precond = Preconditioner::None) {
+  detail::BlockDesc D(op);
+  return detail::cg_run(b, std::move(x0), [&](const double* db, double* dx, loam_solve_report* rep) {
+    return loam_gpu_cg_solve_block(&D.op, db, (int64_t)b.size(), dx, rtol, atol, maxit,
+                                   precond == Preconditioner::Jacobi ? 1 : 0, rep, nullptr);
+  });
 }
 
 } // namespace loam_gpu

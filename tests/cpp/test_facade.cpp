@@ -215,6 +215,100 @@ static void test_stiffness_reference_triangle() { // test_fem.cpp:141-161 throug
   }, "no CPU fallback");
 }
 
+// ---- matrix consumers ----------------------------------------
+static MatPtr dense_mat(const std::vector<Real>& entries, int n) { // test_solver.cpp:10-20
+  auto nodes = make_set(n);
+  auto one = make_set(1);
+  std::vector<int> all(n);
+  for (int i = 0; i < n; ++i) all[i] = i;
+  auto map = make_map(one, nodes, n, all);
+  auto mat = make_mat(build_sparsity(map, map));
+  mat->addto(all, all, entries, Access::WRITE);
+  return mat;
+}
+
+static void test_spmv() { // test_data.cpp:175-205
+  auto diag = dense_mat({2, 0, 0, 3}, 2);
+  std::vector<Real> x{1.0, 1.0};
+  CHECK(mat_spmv(*diag, x) == (std::vector<Real>{2.0, 3.0}));
+  auto full = dense_mat({4, 1, 1, 3}, 2);
+  std::vector<Real> x2{1.0, 2.0};
+  CHECK(mat_spmv(*full, x2) == (std::vector<Real>{6.0, 7.0}));
+  std::vector<Real> bad{1.0, 2.0, 3.0};
+  expect_error(ErrorKind::DimensionMismatch, [&] { mat_spmv(*full, bad); });
+}
+
+static void test_block_spmv() { // test_solver.cpp:171-206
+  auto A = dense_mat({2, 1, 1, 2}, 2), B = dense_mat({0, 1, 2, 0}, 2), C = dense_mat({1, 1, 0, 1}, 2);
+  BlockMat diag;
+  diag.blocks[0][0] = A;
+  diag.blocks[1][1] = A;
+  diag.row_sizes = {2, 2};
+  diag.col_sizes = {2, 2};
+  std::vector<Real> x{1, 2, 3, 4};
+  auto y = block_spmv(diag, x);
+  auto Au = mat_spmv(*A, {x.data(), 2}), Av = mat_spmv(*A, {x.data() + 2, 2});
+  CHECK(std::vector<Real>(y.begin(), y.begin() + 2) == Au);
+  CHECK(std::vector<Real>(y.begin() + 2, y.end()) == Av);
+  BlockMat anti;
+  anti.blocks[0][1] = B;
+  anti.blocks[1][0] = C;
+  anti.row_sizes = {2, 2};
+  anti.col_sizes = {2, 2};
+  auto z = block_spmv(anti, x);
+  CHECK(std::vector<Real>(z.begin(), z.begin() + 2) == mat_spmv(*B, {x.data() + 2, 2}));
+  CHECK(std::vector<Real>(z.begin() + 2, z.end()) == mat_spmv(*C, {x.data(), 2}));
+  std::vector<Real> bad{1, 2, 3};
+  expect_error(ErrorKind::DimensionMismatch, [&] { block_spmv(diag, bad); });
+}
+
+static void test_cg() { // test_solver.cpp:24-123
+  std::vector<Real> e(25, 0.0);
+  for (int i = 0; i < 5; ++i) e[i * 5 + i] = 1.0;
+  std::vector<Real> b{0.3, 0.1, 0.7, 0.2, 0.9};
+  auto [x, rep] = cg_solve(*dense_mat(e, 5), b);
+  CHECK(rep.converged && rep.iterations == 1);
+  for (int i = 0; i < 5; ++i) CHECK(std::abs(x[i] - b[i]) <= 1e-14);
+  auto [x2, rep2] = cg_solve(*dense_mat({4, 1, 1, 3}, 2), std::vector<Real>{1, 2}, {}, 1e-12, 1e-16, 10);
+  CHECK(rep2.converged && std::abs(x2[0] - 1.0 / 11) <= 1e-12 && std::abs(x2[1] - 7.0 / 11) <= 1e-12);
+  expect_error(ErrorKind::IndefiniteBreakdown, [&] {
+    cg_solve(*dense_mat({0, 1, 1, 3}, 2), std::vector<Real>{1, 2}, {}, 1e-10, 1e-15, 10, Preconditioner::Jacobi);
+  });
+  expect_error(ErrorKind::IndefiniteBreakdown, [&] {
+    cg_solve(*dense_mat({1, 0, 0, -1}, 2), std::vector<Real>{1, 1}, {}, 1e-10, 1e-15, 10);
+  }, "after 1 iterations");
+  // maxit returns the iterate unconverged: B^T B + I, n = 30
+  const int n = 30;
+  std::vector<Real> Bm(n * n), A(n * n, 0.0), rhs(n);
+  unsigned s = 47;
+  auto u = [&] { s = s * 1103515245u + 12345u; return (s >> 8) / 16777216.0; };
+  for (auto& v : Bm) v = u();
+  for (auto& v : rhs) v = u();
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      for (int k = 0; k < n; ++k) A[i * n + j] += Bm[k * n + i] * Bm[k * n + j];
+      if (i == j) A[i * n + j] += 1.0;
+    }
+  auto [x3, rep3] = cg_solve(*dense_mat(A, n), rhs, {}, 1e-14, 0.0, 2);
+  CHECK(!rep3.converged && rep3.reason == SolveReport::Reason::maxit && rep3.iterations == 2);
+  // block operator [[A, 0], [0, A]] equals two independent solves
+  BlockMat op;
+  auto Am = dense_mat(A, n);
+  op.blocks[0][0] = op.blocks[1][1] = Am;
+  op.row_sizes = op.col_sizes = {n, n};
+  std::vector<Real> bb(rhs);
+  bb.insert(bb.end(), rhs.begin(), rhs.end());
+  auto [xb, repb] = cg_solve(op, bb, {}, 1e-10, 1e-16, 200, Preconditioner::Jacobi);
+  CHECK(repb.converged);
+  auto r = block_spmv(op, xb);
+  Real rn = 0.0, bn = 0.0;
+  for (size_t i = 0; i < bb.size(); ++i) {
+    rn += (bb[i] - r[i]) * (bb[i] - r[i]);
+    bn += bb[i] * bb[i];
+  }
+  CHECK(std::sqrt(rn) <= 1e-10 * std::sqrt(bn) + 1e-12);
+}
+
 int main() {
   const std::vector<std::pair<const char*, void (*)()>> cases = {
       {"direct loop doubles a field", test_direct_loop},
@@ -228,6 +322,9 @@ int main() {
       {"sparsity and colouring KATs", test_sparsity_and_colouring},
       {"OutsideSparsity / map range", test_outside_sparsity_and_map_range},
       {"stiffness on the reference triangle", test_stiffness_reference_triangle},
+      {"spmv by CSR traversal", test_spmv},
+      {"block spmv skips zero blocks and swaps components", test_block_spmv},
+      {"cg known answers, breakdown, maxit, block operator", test_cg},
   };
   for (auto& [name, fn] : cases) {
     const int before = g_fail;
