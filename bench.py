@@ -487,11 +487,11 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="loam_gpu", choices=["loam_gpu", "reference"])
-    ap.add_argument("--strategy", default="auto", choices=["auto", "owner", "atomic", "color", "nbr"])
+    ap.add_argument("--strategy", default="auto", choices=["auto", "owner", "atomic", "color", "nbr", "warpagg", "patch"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--all-configs", action="store_true")
     ap.add_argument("--configs", default="")
-    ap.add_argument("--strategies", default="auto,owner,atomic,warpagg,color")
+    ap.add_argument("--strategies", default="auto,owner,atomic,warpagg,color,patch")
     ap.add_argument("--size", type=int, default=None)
     ap.add_argument("--solver", action="store_true", help="developer: SpMV roofline and CG per-iteration lines")
     args = ap.parse_args()

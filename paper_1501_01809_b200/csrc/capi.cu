@@ -118,7 +118,7 @@ int loam_gpu_set_option(int option, int value) {
   return guarded([&] {
     switch (option) {
     case LOAM_OPT_INC_STRATEGY:
-      require(value >= 0 && value <= 5, LOAM_ERR(InvalidArgument), "strategy must be 0..5");
+      require(value >= 0 && value <= 6, LOAM_ERR(InvalidArgument), "strategy must be 0..6");
       options().inc_strategy = value;
       break;
     case LOAM_OPT_CHECK_SPARSITY: options().check_sparsity = value ? 1 : 0; break;

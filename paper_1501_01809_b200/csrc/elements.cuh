@@ -246,6 +246,77 @@ __host__ __device__ __forceinline__ int p2_mass_kind(int i, int j) {
   return i == j ? 4 : shared == 1 ? 5 : 6;
 }
 
+// Row i (runtime) of the P2 stiffness K_ij = int grad phi_i . grad phi_j / V
+// and mass M_ij = int phi_i phi_j / V tensors for every compile-time j: one
+// vertex/edge branch per row, the dot products g_a . g_m shared by the whole
+// row, and the rational constants selected by index coincidence (same
+// integrals as P2Row::stiff / p2_mass_const, evaluated without per-entry
+// branching).
+template <int D, bool STIFF, bool MASS>
+__device__ __forceinline__ void p2_rows(int i, const Geom<D>& G, double* K, double* M) {
+  constexpr int NV = Simplex<D>::NV, NE = Simplex<D>::NE;
+  constexpr double qs = Simplex<D>::q_same, qd = Simplex<D>::q_diff, l1 = Simplex<D>::l1;
+  constexpr double cs = 16.0 * qs - 8.0 * l1 + 1.0, co = 16.0 * qd - 8.0 * l1 + 1.0;
+  constexpr double es = 4.0 * qs - l1, ed = 4.0 * qd - l1;
+  constexpr double m0 = p2_mass_const<D>(0), m1 = p2_mass_const<D>(1), m2 = p2_mass_const<D>(2),
+                   m3 = p2_mass_const<D>(3), m4 = p2_mass_const<D>(4), m5 = p2_mass_const<D>(5),
+                   m6 = p2_mass_const<D>(6);
+  if (i < NV) {
+    const int v = i;
+    if constexpr (STIFF) {
+      double gv[D], dv[NV];
+      sel<D>(G, v, gv);
+#pragma unroll
+      for (int m = 0; m < NV; ++m) dv[m] = dot<D>(gv, G.g[m]);
+#pragma unroll
+      for (int j = 0; j < NV; ++j) K[j] = (v == j ? cs : co) * dv[j];
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const int a = Simplex<D>::edge_a(e), b = Simplex<D>::edge_b(e);
+        K[NV + e] = 4.0 * ((v == b ? es : ed) * dv[a] + (v == a ? es : ed) * dv[b]);
+      }
+    }
+    if constexpr (MASS) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) M[j] = v == j ? m0 : m1;
+#pragma unroll
+      for (int e = 0; e < NE; ++e)
+        M[NV + e] = (Simplex<D>::edge_a(e) == v || Simplex<D>::edge_b(e) == v) ? m2 : m3;
+    }
+  } else {
+    const int e = i - NV;
+    const int a = Simplex<D>::edge_a(e), b = Simplex<D>::edge_b(e);
+    if constexpr (STIFF) {
+      double ga[D], gb[D], da[NV], db[NV];
+      sel<D>(G, a, ga);
+      sel<D>(G, b, gb);
+#pragma unroll
+      for (int m = 0; m < NV; ++m) {
+        da[m] = dot<D>(ga, G.g[m]);
+        db[m] = dot<D>(gb, G.g[m]);
+      }
+#pragma unroll
+      for (int j = 0; j < NV; ++j) K[j] = 4.0 * ((j == b ? es : ed) * da[j] + (j == a ? es : ed) * db[j]);
+#pragma unroll
+      for (int f = 0; f < NE; ++f) {
+        const int c = Simplex<D>::edge_a(f), d = Simplex<D>::edge_b(f);
+        K[NV + f] = 16.0 * ((b == d ? qs : qd) * da[c] + (b == c ? qs : qd) * da[d] + (a == d ? qs : qd) * db[c] +
+                            (a == c ? qs : qd) * db[d]);
+      }
+    }
+    if constexpr (MASS) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) M[j] = (j == a || j == b) ? m2 : m3;
+#pragma unroll
+      for (int f = 0; f < NE; ++f) {
+        const int c = Simplex<D>::edge_a(f), d = Simplex<D>::edge_b(f);
+        const int shared = (a == c) + (a == d) + (b == c) + (b == d);
+        M[NV + f] = e == f ? m4 : (shared == 1 ? m5 : m6);
+      }
+    }
+  }
+}
+
 template <int D, int P>
 struct Lagrange {
   static constexpr int N = P == 1 ? D + 1 : (D == 2 ? 6 : 10);
@@ -290,13 +361,14 @@ struct ScalarBilinear {
         out[j] = G.V * v;
       }
     } else {
-      const P2Row<D> R(G, i);
+      double K[N], M[N];
+      p2_rows<D, FORM != F_MASS, FORM != F_STIFFNESS>(i, G, K, M);
 #pragma unroll
       for (int j = 0; j < N; ++j) {
         double v;
-        if constexpr (FORM == F_MASS) v = p2_mass_const<D>(p2_mass_kind<D>(i, j));
-        else if constexpr (FORM == F_STIFFNESS) v = R.stiff(G, j);
-        else v = fma(prm.p[0], p2_mass_const<D>(p2_mass_kind<D>(i, j)), R.stiff(G, j));
+        if constexpr (FORM == F_MASS) v = M[j];
+        else if constexpr (FORM == F_STIFFNESS) v = K[j];
+        else v = fma(prm.p[0], M[j], K[j]);
         out[j] = G.V * v;
       }
     }
@@ -342,14 +414,15 @@ struct ScalarAction {
       }
       out[0] = b;
     } else {
-      const P2Row<D> R(G, i);
+      double K[N], M[N];
+      p2_rows<D, FORM != F_MASS_ACTION, FORM != F_STIFFNESS_ACTION>(i, G, K, M);
       double b = 0.0;
 #pragma unroll
       for (int j = 0; j < N; ++j) {
         double a;
-        if constexpr (FORM == F_MASS_ACTION) a = p2_mass_const<D>(p2_mass_kind<D>(i, j));
-        else if constexpr (FORM == F_STIFFNESS_ACTION) a = R.stiff(G, j);
-        else a = fma(prm.p[0], p2_mass_const<D>(p2_mass_kind<D>(i, j)), R.stiff(G, j));
+        if constexpr (FORM == F_MASS_ACTION) a = M[j];
+        else if constexpr (FORM == F_STIFFNESS_ACTION) a = K[j];
+        else a = fma(prm.p[0], M[j], K[j]);
         b = fma(a, C[j], b);
       }
       out[0] = G.V * b;
@@ -425,11 +498,12 @@ struct FormT<F_STOKES_A, 2, 2> {
   static constexpr int NCOEFF = 0;
   __device__ __forceinline__ static void row(int a, const Geom<2>& G, const double*,
                                              const FormParams& prm, double* out) {
-    const P2Row<2> R(G, a);
+    double K[6];
+    p2_rows<2, true, false>(a, G, K, nullptr);
     const double scale = prm.p[0] * G.V;
 #pragma unroll
     for (int b = 0; b < 6; ++b) {
-      const double s = scale * R.stiff(G, b);
+      const double s = scale * K[b];
       out[0 * 12 + b * 2 + 0] = s;
       out[0 * 12 + b * 2 + 1] = 0.0;
       out[1 * 12 + b * 2 + 0] = 0.0;
@@ -438,11 +512,12 @@ struct FormT<F_STOKES_A, 2, 2> {
   }
   __device__ __forceinline__ static void subrow(int a, int d, const Geom<2>& G, const double*,
                                                 const FormParams& prm, double* out) {
-    const P2Row<2> R(G, a);
+    double K[6];
+    p2_rows<2, true, false>(a, G, K, nullptr);
     const double scale = prm.p[0] * G.V;
 #pragma unroll
     for (int b = 0; b < 6; ++b) {
-      const double s = scale * R.stiff(G, b);
+      const double s = scale * K[b];
       out[b * 2 + 0] = d == 0 ? s : 0.0;
       out[b * 2 + 1] = d == 1 ? s : 0.0;
     }

@@ -27,6 +27,8 @@
 #include "async.cuh"
 #include "elements.cuh"
 #include "engine.cuh"
+#include "patch.cuh"
+#include "patch_kernels.cuh"
 #include "plan.cuh"
 #include "test_kernels.cuh"
 
@@ -417,12 +419,10 @@ __global__ void __launch_bounds__(128) k_cell_vec(const __grid_constant__ CellAr
   cell_gather<F>(a, e, X, C, rows);
   Geom<F::GD> G;
   geometry<F::GD>(X, G);
+  double y[F::NRN];
+  ElemVec<F>::all(G, C, a.prm, y); // whole element vector (P2: through grad u_h)
 #pragma unroll
-  for (int i = 0; i < F::NRN; ++i) {
-    double v;
-    F::row(i, G, C, a.prm, &v);
-    red_add<AGG>(a.out, rows[i], v, valid);
-  }
+  for (int i = 0; i < F::NRN; ++i) red_add<AGG>(a.out, rows[i], y[i], valid);
 }
 
 template <class F, bool AGG>
@@ -1255,6 +1255,7 @@ struct PTileArgs {
   int accumulate;
   int off_seg, off_buf, buf_bytes;
   int b_pptr, b_nptr, b_recs, b_win, b_winc;
+  int cas; // concurrent G-lane adds by shared-memory CAS instead of serialised sub-steps
 };
 
 template <class F>
@@ -1431,6 +1432,20 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
           if constexpr (!F::BILINEAR) acc += blk[0];
         }
         if constexpr (F::BILINEAR) {
+          if (a.cas) { // the G lanes of a row add concurrently (fp64 CAS in shared memory)
+            if (has) {
+#pragma unroll
+              for (int j = 0; j < F::NCN; ++j) {
+                const int rk = rec[RL::OFF_RK + j];
+#pragma unroll
+                for (int d = 0; d < F::RD; ++d)
+#pragma unroll
+                  for (int c = 0; c < F::CD; ++c)
+                    if (!diag_block<F>::value || d == c)
+                      atomicAdd(&seg[a0 * W + d * L * F::CD + rk * F::CD + c], blk[d * F::NC + j * F::CD + c]);
+              }
+            }
+          } else
           for (int st = 0; st < G; ++st) {
             if (has && st == sub) {
 #pragma unroll
@@ -1493,6 +1508,7 @@ using NbrFn = void (*)(const TileArgs&, int rec_bytes, size_t smem, cudaStream_t
 using RingFn = void (*)(const RingArgs&, size_t smem, cudaStream_t);
 using PTileFn = void (*)(const PTileArgs&, size_t smem, cudaStream_t);
 using CellFn = void (*)(const CellArgs&, bool agg, cudaStream_t);
+using PatchFn = void (*)(const PatchArgs&, size_t smem, cudaStream_t);
 
 struct Entry {
   KernelInfo info;
@@ -1506,6 +1522,7 @@ struct Entry {
   RingFn ring = nullptr; // scalar P1 triangle forms only
   PTileFn ptile = nullptr;
   CellFn cell = nullptr;
+  PatchFn patch = nullptr; // square Mats and actions whose coordinate map is the row map's vertex prefix
 };
 
 template <class K>
@@ -1567,6 +1584,33 @@ void launch_nbr(const TileArgs& a, int rec_bytes, size_t smem, cudaStream_t s) {
   LG_LAUNCH_CHECK();
 }
 
+constexpr int kPatchThreads = 256;
+
+template <class F>
+void launch_patch(const PatchArgs& a, size_t smem, cudaStream_t s) {
+  if (a.npatches == 0) return;
+  auto go = [&](auto kern) {
+    static size_t attr = 0;
+    if (attr < smem) {
+      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    int blocks = 1;
+    LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kPatchThreads, smem));
+    require(blocks > 0, LOAM_GPU_ERR_CUDA, "patch kernel does not fit on an SM");
+    static const bool one_per_cta = std::getenv("LOAM_GPU_PATCH_GRID") != nullptr;
+    const int grid = one_per_cta ? a.npatches : std::min(a.npatches, blocks * kNumSMs);
+    kern<<<grid, kPatchThreads, smem, s>>>(a);
+  };
+  if constexpr (F::BILINEAR) {
+    if constexpr (F::NRN == F::NCN) go(k_patch_mat<F, kPatchThreads>);
+  } else {
+    go(k_patch_vec<F, kPatchThreads>);
+  }
+  count_launch();
+  LG_LAUNCH_CHECK();
+}
+
 template <class K>
 Entry plain_entry(const char* name, std::vector<std::string> names, std::vector<std::vector<int>> ext) {
   Entry e;
@@ -1602,6 +1646,7 @@ Entry form_entry(const std::string& name) {
   e.owner = &launch_owner<F>;
   e.ptile = &launch_ptile<F>;
   e.cell = &launch_cell<F>;
+  if constexpr (!F::BILINEAR ? F::NCOEFF == F::NRN : F::NRN == F::NCN) e.patch = &launch_patch<F>;
   if constexpr (P == 1 && F::NRN == D + 1 && (!F::BILINEAR || F::NCN == F::NRN)) e.nbr = &launch_nbr<F>;
   if constexpr (P == 1 && D == 2 && F::RD == 1 && F::CD == 1) e.ring = &launch_ring<F>;
   return e;
@@ -1765,6 +1810,8 @@ struct FastPlan {
   NbrPlan nb;
   bool use_ptile = false;
   PTilePlan pt;
+  bool use_patch = false;  // cell-patch row-owner kernels (patch.cuh)
+  PatchPlan patch;
   bool use_cell = false;   // cell-centric atomic scatter
   SortedMap crows;         // (cell mode) sorted row map
   DevBuf<uint8_t> cranks;  // (cell mode, matrices) per-cell in-row ranks
@@ -1810,11 +1857,85 @@ constexpr int kTileSeg = 4096;   // matrix values per neighbour-list tile (32 KB
 constexpr int kTileSlots = 1024; // vertices in a tile's window
 constexpr int kTileRuns = 32;    // contiguous runs per window
 
+// Strategy 6 selects the patch kernels; auto uses them for the forms they
+// win on (profiles/r01/strategies_patch*).
+bool patch_wanted(const Entry& k) {
+  const int strat = options().inc_strategy;
+  if (strat == 6) return true;
+  if (strat != 0 || std::getenv("LOAM_GPU_NO_PATCH")) return false;
+  return std::getenv("LOAM_GPU_PATCH_AUTO") != nullptr && (k.nrn > k.gd + 1 || k.rd > 1);
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+size_t patch_smem_bytes(const Entry& k, const PatchPlan& pp) {
+  if (!k.bilinear) {
+    int ow, orc, op, of, ox;
+    return (size_t)patch_vec_smem(pp.max_win, pp.max_cells, k.nrn, k.gd, &ow, &orc, &op, &of, &ox);
+  }
+  const int gs = k.gd * k.gd + 1; // (Dats size their element vectors from nrn)
+  return (size_t)patch_smem(gs, k.nrn, k.bilinear, pp.max_win, pp.max_cells, pp.max_own, pp.max_pairs,
+                            (int)pp.max_seg, (pp.max_win + 31) / 32).total;
+}
+
+// Cell-patch plan (patch.cuh) when the loop has the shape the patch kernels
+// serve: the coordinate map is the row map's vertex prefix, actions read their
+// coefficient through the row map, Mats are square with exactly the (map, map)
+// pattern (the in-kernel ranks are derived from the maps, not read from
+// col_idx).  Returns false (caller uses another plan) otherwise.
+bool try_build_patch(const Entry& k, int n, const loam_arg_desc* args, FastPlan& P, cudaStream_t s) {
+  if (!k.patch) return false;
+  const NodeMap R = node_view(args[0].map);
+  if ((reinterpret_cast<uintptr_t>(args[1].data) & 15) != 0) return false;
+  auto same_as_rows = [&](const MapView& m) {
+    return m.arity == R.v.arity && m.target == R.v.target &&
+           (m.v == R.v.v || prefix_equal(m.v, m.arity, R.v.v, R.v.arity, m.arity, n, s));
+  };
+  const loam_sparsity_desc* sp = nullptr;
+  if (k.has_coeff) {
+    const loam_map_desc* Cm = args[2].map;
+    if (!same_as_rows(MapView{Cm->values, n, Cm->arity, Cm->target_size})) return false;
+  }
+  if (k.bilinear) {
+    const NodeMap Cn = node_view(args[0].col_map);
+    if (Cn.dim != k.cd || R.dim != k.rd || !same_as_rows(Cn.v)) return false;
+    sp = args[0].sparsity;
+    if (!pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, R.dim, Cn.dim, sp->row_ptr, sp->col_idx, sp->nnz, s))
+      return false;
+  }
+  PatchSpec spec;
+  spec.gd = k.gd;
+  spec.nrn = k.nrn;
+  spec.rd = k.rd;
+  spec.cd = k.cd;
+  spec.bilinear = k.bilinear;
+  spec.budget = env_int("LOAM_GPU_PATCH_BUDGET", 3072);
+  spec.max_cells = env_int("LOAM_GPU_PATCH_CELLS", k.bilinear ? 1024 : 512);
+  spec.halo = k.bilinear; // Dats: cell-owned patches, shared nodes by fp64 RED
+  const loam_map_desc* X = args[1].map;
+  for (int attempt = 0; attempt < 6; ++attempt) {
+    if (!build_patch(P.patch, spec, n, R.v.target, R.v.v, X->values, X->arity, args[1].data,
+                     sp ? sp->row_ptr : nullptr, s))
+      return false;
+    if (patch_smem_bytes(k, P.patch) <= 200 * 1024) return true;
+    spec.budget = spec.budget * 2 / 3;
+    spec.max_cells = spec.max_cells * 2 / 3;
+  }
+  return false;
+}
+
 std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_desc* args, bool cell_mode,
                                           cudaStream_t s) {
   auto P = std::make_shared<FastPlan>();
   P->counter.alloc(4, s);
   LG_CUDA(cudaMemsetAsync(P->counter.get(), 0, 4 * sizeof(int), s));
+  if (!cell_mode && patch_wanted(k) && try_build_patch(k, n, args, *P, s)) {
+    P->use_patch = true;
+    return P;
+  }
   const NodeMap R = node_view(args[0].map);
   const loam_map_desc* X = args[1].map;
   const loam_map_desc* Cm = k.has_coeff ? args[2].map : nullptr;
@@ -1929,10 +2050,6 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     spec.ncoeff = k.has_coeff ? k.ncoeff : 0;
     spec.rd = k.rd;
     spec.cd = k.cd;
-    auto env_int = [](const char* name, int dflt) {
-      const char* v = std::getenv(name);
-      return v ? std::atoi(v) : dflt;
-    };
     spec.tile_rows = kPTileThreads;
     spec.tile_seg = env_int("LOAM_GPU_PT_SEG", 4096);
     spec.tile_pairs = env_int("LOAM_GPU_PT_PAIRS", 768);
@@ -2034,6 +2151,33 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
       std::lock_guard<std::mutex> g(g_cache_mutex);
       g_fast_cache[key] = P;
     }
+  }
+  if (P->use_patch) {
+    const PatchPlan& pp = P->patch;
+    PatchArgs t{};
+    t.hdr = pp.hdr.get();
+    t.npatches = pp.npatches;
+    t.win = pp.win.get();
+    t.recs = pp.recs.get();
+    t.own = pp.own.get();
+    t.orp = pp.orp.get();
+    t.oseg = pp.oseg.get();
+    t.coords = args[1].data;
+    t.coeff = k.has_coeff ? args[2].data : nullptr;
+    t.prm = prm;
+    t.out = args[0].data;
+    t.accumulate = (args[0].flags & LOAM_ARG_ZERO) ? 0 : 1;
+    t.max_win = pp.max_win;
+    t.max_cells = pp.max_cells;
+    t.max_own = pp.max_own;
+    t.max_pairs = pp.max_pairs;
+    t.max_seg = (int)pp.max_seg;
+    t.bw = (pp.max_win + 31) / 32;
+    t.nverts = args[1].map->target_size;
+    if (!k.bilinear && !t.accumulate) // shared nodes are RED-accumulated; nodes in no cell stay zero
+      LG_CUDA(cudaMemsetAsync(args[0].data, 0, sizeof(double) * (size_t)args[0].set_size * args[0].dim, s));
+    k.patch(t, patch_smem_bytes(k, pp), s);
+    return;
   }
   if (P->use_cell) {
     CellArgs c{};
@@ -2148,6 +2292,7 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     t.prm = prm;
     t.out = args[0].data;
     t.accumulate = (args[0].flags & LOAM_ARG_ZERO) ? 0 : 1;
+    t.cas = env_int("LOAM_GPU_PTILE_CAS", 0);
     auto up16 = [](int x) { return (x + 15) & ~15; };
     int off = 128;
     t.off_seg = off;
@@ -2434,7 +2579,7 @@ void execute(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_de
       if (e.code() != LOAM_ERR(ShapeMismatch)) throw; // unblocked pattern: generic engine
     }
   }
-  if (n > 0 && !atomic_auto && (strat == 0 || strat == 2 || strat == 4) && fast_pattern(k, args, nargs)) {
+  if (n > 0 && !atomic_auto && (strat == 0 || strat == 2 || strat == 4 || strat == 6) && fast_pattern(k, args, nargs)) {
     try {
       run_fast(k, n, args, nargs, prm, s);
       return;

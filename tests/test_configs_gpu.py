@@ -14,7 +14,7 @@ from paper_1501_01809_b200 import capi, configs
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
-STRATS = ["auto", "owner", "atomic", "warpagg", "color"]
+STRATS = ["auto", "owner", "atomic", "warpagg", "color", "patch"]
 
 
 def rel(a, b):
