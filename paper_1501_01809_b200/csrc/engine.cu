@@ -941,6 +941,159 @@ struct RingCell {
   }
 };
 
+// Vertex-star kernel for P1 triangle ACTIONS (config 1 shape): one thread per
+// row vertex s.  Its star -- the link vertices v_0..v_{m-1} of the cells
+// around s, in ring / fan order -- is one 32-byte record {m | closed << 4,
+// v_0..v_6}; the cells are (s, v_k, v_{k+1}) (and (s, v_{m-1}, v_0) when the
+// ring is closed).  Two dependent gathers per row (record, then the
+// neighbours' coordinates and coefficients), the action in closed form
+// (RingCell::action), one store: no plan tiles, no shared memory, no
+// atomics -- the short latency chain a 15 MB loop needs.
+struct StarArgs {
+  const int4* star; // 2 per row
+  int nrows;
+  const double* coords;
+  const double* coeff;
+  FormParams prm;
+  double* out;
+  int accumulate;
+};
+
+template <class F>
+__device__ __forceinline__ double star_row(const StarArgs& a, int r, int4 h, int4 t) {
+  const int m = h.x & 15;
+  const bool closed = (h.x >> 4) & 1;
+  const int v[7] = {h.y, h.z, h.w, t.x, t.y, t.z, t.w};
+  const double2 xs = __ldg(reinterpret_cast<const double2*>(a.coords) + r);
+  const double us = __ldg(a.coeff + r);
+  double px = 0, py = 0, up = 0, p0x = 0, p0y = 0, u0 = 0, aa = 0;
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    if (k < m) {
+      const double2 x = __ldg(reinterpret_cast<const double2*>(a.coords) + v[k]);
+      const double u = __ldg(a.coeff + v[k]);
+      const double nx = x.x - xs.x, ny = x.y - xs.y, nn = nx * nx + ny * ny;
+      if (k == 0) {
+        p0x = nx;
+        p0y = ny;
+        u0 = u;
+      } else { // cell (s, v_{k-1}, v_k)
+        const double ab = px * nx + py * ny, ad = fabs(px * ny - py * nx);
+        acc += RingCell<F>::action(aa, ab, nn, ad, a.prm.p[0], us, up, u);
+      }
+      px = nx;
+      py = ny;
+      up = u;
+      aa = nn;
+    }
+  }
+  if (closed && m > 2) { // closing cell (s, v_{m-1}, v_0)
+    const double nn = p0x * p0x + p0y * p0y;
+    const double ab = px * p0x + py * p0y, ad = fabs(px * p0y - py * p0x);
+    acc += RingCell<F>::action(aa, ab, nn, ad, a.prm.p[0], us, up, u0);
+  }
+  return acc;
+}
+
+template <class F>
+__global__ void __launch_bounds__(256) k_star_vec(const __grid_constant__ StarArgs a) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.nrows) return;
+  const double y = star_row<F>(a, r, __ldg(a.star + 2 * r), __ldg(a.star + 2 * r + 1));
+  a.out[r] = a.accumulate ? a.out[r] + y : y;
+}
+
+template <class F>
+void launch_star(const StarArgs& a, cudaStream_t s) {
+  if (a.nrows == 0) return;
+  k_star_vec<F><<<ceil_div(a.nrows, 256), 256, 0, s>>>(a);
+  count_launch();
+  LG_LAUNCH_CHECK();
+}
+
+// Star records of the node map (host build; false if a star is not a single
+// ring or fan of <= 7 link vertices).
+bool build_stars(const int32_t* dmap, int ncells, int nverts, DevBuf<int4>& out, cudaStream_t s) {
+  std::vector<int32_t> cv((size_t)ncells * 3);
+  LG_CUDA(cudaMemcpyAsync(cv.data(), dmap, sizeof(int32_t) * cv.size(), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  // link edges {p, q} of every vertex, CSR by vertex
+  std::vector<int32_t> cnt(nverts + 1, 0);
+  for (size_t e = 0; e < (size_t)ncells; ++e)
+    for (int i = 0; i < 3; ++i) ++cnt[cv[e * 3 + i] + 1];
+  for (int v = 0; v < nverts; ++v) cnt[v + 1] += cnt[v];
+  std::vector<int2> link(cnt[nverts]);
+  {
+    std::vector<int32_t> f(cnt.begin(), cnt.end() - 1);
+    for (size_t e = 0; e < (size_t)ncells; ++e)
+      for (int i = 0; i < 3; ++i) {
+        const int r = cv[e * 3 + i];
+        link[f[r]++] = make_int2(cv[e * 3 + (i + 1) % 3], cv[e * 3 + (i + 2) % 3]);
+      }
+  }
+  std::vector<int4> rec(2 * (size_t)nverts);
+  for (int r = 0; r < nverts; ++r) {
+    const int b = cnt[r], e = cnt[r + 1], nl = e - b;
+    int chain[8], m = 0;
+    bool closed = false;
+    if (nl > 0) {
+      if (nl > 7) return false;
+      // link-graph degrees; start at a degree-1 end (fan) or anywhere (ring)
+      auto deg = [&](int x) {
+        int d = 0;
+        for (int k = b; k < e; ++k) d += (link[k].x == x) + (link[k].y == x);
+        return d;
+      };
+      int start = link[b].x, ends = 0;
+      for (int k = b; k < e; ++k)
+        for (int x : {link[k].x, link[k].y}) {
+          const int d = deg(x);
+          if (d > 2 || x == r) return false;
+          if (d == 1) ++ends;
+        }
+      if (ends != 0 && ends != 2) return false;
+      if (ends == 2) { // the smaller end id, deterministic
+        start = INT32_MAX;
+        for (int k = b; k < e; ++k)
+          for (int x : {link[k].x, link[k].y})
+            if (deg(x) == 1) start = std::min(start, x);
+      }
+      closed = ends == 0;
+      uint32_t used = 0;
+      int cur = start;
+      chain[m++] = cur;
+      for (int step = 0; step < nl; ++step) {
+        int nxt = -1;
+        for (int k = b; k < e; ++k) {
+          if (used >> (k - b) & 1u) continue;
+          if (link[k].x == cur) nxt = link[k].y;
+          else if (link[k].y == cur) nxt = link[k].x;
+          else continue;
+          used |= 1u << (k - b);
+          break;
+        }
+        if (nxt < 0) return false; // several components
+        if (closed && step == nl - 1) {
+          if (nxt != start) return false;
+          break;
+        }
+        chain[m++] = nxt;
+        cur = nxt;
+      }
+      if (m > 7 || (closed ? m != nl : m != nl + 1)) return false;
+    }
+    int v[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int k = 0; k < m; ++k) v[k] = chain[k];
+    rec[2 * r] = make_int4(m | (closed ? 16 : 0), v[0], v[1], v[2]);
+    rec[2 * r + 1] = make_int4(v[3], v[4], v[5], v[6]);
+  }
+  out.alloc(rec.size(), s);
+  LG_CUDA(cudaMemcpyAsync(out.get(), rec.data(), sizeof(int4) * rec.size(), cudaMemcpyHostToDevice, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  return true;
+}
+
 template <class F, bool ACC>
 __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ RingArgs a) {
   static_assert(F::GD == 2 && F::NRN == 3, "ring kernel: P1 triangles");
@@ -1509,6 +1662,7 @@ using RingFn = void (*)(const RingArgs&, size_t smem, cudaStream_t);
 using PTileFn = void (*)(const PTileArgs&, size_t smem, cudaStream_t);
 using CellFn = void (*)(const CellArgs&, bool agg, cudaStream_t);
 using PatchFn = void (*)(const PatchArgs&, size_t smem, cudaStream_t);
+using StarFn = void (*)(const StarArgs&, cudaStream_t);
 
 struct Entry {
   KernelInfo info;
@@ -1523,6 +1677,7 @@ struct Entry {
   PTileFn ptile = nullptr;
   CellFn cell = nullptr;
   PatchFn patch = nullptr; // square Mats and actions whose coordinate map is the row map's vertex prefix
+  StarFn star = nullptr;   // P1 triangle actions
 };
 
 template <class K>
@@ -1649,6 +1804,7 @@ Entry form_entry(const std::string& name) {
   if constexpr (!F::BILINEAR ? F::NCOEFF == F::NRN : F::NRN == F::NCN) e.patch = &launch_patch<F>;
   if constexpr (P == 1 && F::NRN == D + 1 && (!F::BILINEAR || F::NCN == F::NRN)) e.nbr = &launch_nbr<F>;
   if constexpr (P == 1 && D == 2 && F::RD == 1 && F::CD == 1) e.ring = &launch_ring<F>;
+  if constexpr (P == 1 && D == 2 && !F::BILINEAR) e.star = &launch_star<F>;
   return e;
 }
 
@@ -1810,6 +1966,8 @@ struct FastPlan {
   NbrPlan nb;
   bool use_ptile = false;
   PTilePlan pt;
+  bool use_star = false;   // vertex-star kernel (P1 triangle actions)
+  DevBuf<int4> star;
   bool use_patch = false;  // cell-patch row-owner kernels (patch.cuh)
   PatchPlan patch;
   bool use_cell = false;   // cell-centric atomic scatter
@@ -2013,6 +2171,11 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     // the window TMA needs 16-byte aligned coordinate / coefficient arrays
     ok = ok && (reinterpret_cast<uintptr_t>(args[1].data) & 15) == 0 &&
          (!Cm || (reinterpret_cast<uintptr_t>(args[2].data) & 15) == 0);
+    if (ok && k.star && strat == 0 && !std::getenv("LOAM_GPU_NO_STAR") &&
+        build_stars(R.v.v, n, R.v.target, P->star, s)) {
+      P->use_star = true;
+      return P;
+    }
     if (ok && build_nbr(P->nb, srows.v.get(), n, R.v.arity, R.v.target, csr, kTileThreads / R.dim,
                         k.bilinear ? kTileSeg : (1 << 30), kTileSlots, kTileRuns, s)) {
       P->use_nbr = true;
@@ -2151,6 +2314,18 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
       std::lock_guard<std::mutex> g(g_cache_mutex);
       g_fast_cache[key] = P;
     }
+  }
+  if (P->use_star) {
+    StarArgs t{};
+    t.star = P->star.get();
+    t.nrows = args[0].set_size;
+    t.coords = args[1].data;
+    t.coeff = args[2].data;
+    t.prm = prm;
+    t.out = args[0].data;
+    t.accumulate = (args[0].flags & LOAM_ARG_ZERO) ? 0 : 1;
+    k.star(t, s);
+    return;
   }
   if (P->use_patch) {
     const PatchPlan& pp = P->patch;
