@@ -226,6 +226,41 @@ int loam_gpu_cg_solve_block(const loam_block_mat* op, const double* b, int64_t b
                             double rtol, double atol, int32_t maxit, int32_t jacobi,
                             loam_solve_report* report, void* stream);
 
+/* ---- around the assembly loop ------------------------ */
+/* Strong Dirichlet rows on a device CSR (fem/assemble.hpp:54-66
+ * apply_dirichlet): for every bc node r, zero row r inside its sparsity, set
+ * the diagonal to 1 and (rhs != NULL) rhs[r] = value; value = node_values[r]
+ * when node_values != NULL (a bc Function), else `constant`
+ * (DirichletBC::value_at, fem/bc.hpp:17-19).  rhs == NULL is
+ * apply_dirichlet_rows (:69-79).  ShapeMismatch when the matrix is not
+ * square; MissingDiagonal "diagonal (r, r) outside sparsity" -- reported
+ * before any row is modified.  All arrays on the device. */
+int loam_gpu_apply_dirichlet(const loam_sparsity_desc* sparsity, double* values, double* rhs,
+                             const int32_t* nodes, int32_t nnodes, const double* node_values,
+                             double constant, void* stream);
+/* DirichletBC::apply (fem/bc.hpp:21-26): dat[r] = value for every bc node. */
+int loam_gpu_bc_apply(double* dat, int32_t set_size, const int32_t* nodes, int32_t nnodes,
+                      const double* node_values, double constant, void* stream);
+
+/* pointwise (fem/assemble.hpp:150-319): out (=|+=|-=) expr over n values
+ * (set size x dim), expr given as a postfix program over constants and
+ * fields (field -1 = the output itself: the reference's RW staging).  One
+ * rounding per operation, the reference's evaluation order: bitwise equal. */
+enum loam_pw_opcode { LOAM_PW_CONST = 0, LOAM_PW_FIELD, LOAM_PW_ADD, LOAM_PW_SUB, LOAM_PW_MUL,
+                      LOAM_PW_DIV, LOAM_PW_NEG };
+enum loam_pw_assign { LOAM_PW_ASSIGN = 0, LOAM_PW_ADD_TO = 1, LOAM_PW_SUB_FROM = 2 };
+typedef struct loam_pw_instr {
+  int32_t op;    /* loam_pw_opcode */
+  int32_t field; /* LOAM_PW_FIELD: index into fields, -1 = out */
+  double value;  /* LOAM_PW_CONST */
+} loam_pw_instr;
+int loam_gpu_pointwise(double* out, int64_t n, int32_t op, const loam_pw_instr* program,
+                       int32_t nprogram, const double* const* fields, int32_t nfields, void* stream);
+
+/* Reductions of a device vector into *result (host), fixed order. */
+enum loam_reduce_kind { LOAM_REDUCE_SUM = 0, LOAM_REDUCE_MIN, LOAM_REDUCE_MAX, LOAM_REDUCE_MAX_ABS };
+int loam_gpu_reduce(const double* x, int64_t n, int32_t kind, double* result, void* stream);
+
 /* ---- topology / data services ------------------------------------------- */
 /* Map construction check (topology.hpp:45-48): every entry in [0, target). */
 int loam_gpu_map_check(const loam_map_desc* map, void* stream);

@@ -413,3 +413,79 @@ def ref_cg(op, b, x0=None, rtol=1e-8, atol=1e-14, maxit=1000, jacobi=False, nest
         raise KindError(rc, L.ref_last_error().decode())
     return x, {"iterations": int(oi[0]), "converged": bool(oi[1]), "reason": ("rtol", "atol", "maxit")[oi[2]],
                "final_residual_norm": float(od[0])}
+
+
+# ------------------------------------------- around the assembly loop (8f-2, 8f-3)
+# A pointwise program is a list of (op, field, value) postfix instructions
+# (include/loam_gpu.h loam_pw_opcode; field -1 = the output).
+
+def _program(prog):
+    ops = np.array([p[0] for p in prog], np.int32)
+    fidx = np.array([p[1] for p in prog], np.int32)
+    vals = np.array([p[2] for p in prog], np.float64)
+    return ops, fidx, vals
+
+
+def _ptrs(arrays):
+    arrs = [np.ascontiguousarray(a, np.float64) for a in arrays]
+    return arrs, (C.c_void_p * max(len(arrs), 1))(*[a.ctypes.data for a in arrs])
+
+
+def pointwise(prog, assign, out, fields, lib="orc"):
+    """orc_pointwise / the compiled reference's fem::pointwise (assemble.hpp:252-314).
+    Returns the new out (a copy); `out` may be 2-D [size, dim] for the reference."""
+    out = np.array(out, np.float64)
+    ops, fidx, vals = _program(prog)
+    arrs, ptrs = _ptrs(fields)
+    if lib == "orc":
+        rc = orc().orc_pointwise(dp(out.reshape(-1)), C.c_int64(out.size), C.c_int(assign), ip(ops), ip(fidx),
+                                 dp(vals), C.c_int(len(prog)), ptrs)
+        _check(rc)
+    else:
+        size, dim = (out.shape[0], out.shape[1]) if out.ndim == 2 else (out.size, 1)
+        L = ref()
+        rc = L.ref_pointwise(C.c_int(size), C.c_int(dim), C.c_int(assign), ip(ops), ip(fidx), dp(vals),
+                             C.c_int(len(prog)), C.c_int(len(arrs)), ptrs, dp(out.reshape(-1)))
+        if rc:
+            raise KindError(rc, L.ref_last_error().decode())
+    return out
+
+
+def apply_dirichlet(csr, rhs, nodes, node_values=None, constant=0.0, lib="orc"):
+    """orc_apply_dirichlet / the compiled reference's fem::apply_dirichlet(_rows)
+    (assemble.hpp:54-79).  csr = (nrows, ncols, row_ptr, col_idx, values).
+    Returns (values, rhs) copies (rhs None: rows only); raises KindError."""
+    n, m, r, c, v = csr
+    r, c = np.ascontiguousarray(r, np.int64), np.ascontiguousarray(c, np.int32)
+    v = np.array(v, np.float64)
+    b = None if rhs is None else np.array(rhs, np.float64)
+    nodes = np.ascontiguousarray(nodes, np.int32)
+    nv = None if node_values is None else np.ascontiguousarray(node_values, np.float64)
+    vp = lambda a: None if a is None else C.c_void_p(a.ctypes.data)  # noqa: E731
+    if lib == "orc":
+        fail = np.zeros(1, np.int32)
+        rc = orc().orc_apply_dirichlet(C.c_int(n), vp(r), vp(c), vp(v), vp(b), vp(nodes), C.c_int(len(nodes)),
+                                       vp(nv), C.c_double(constant), vp(fail))
+        if rc:
+            raise KindError(rc, f"row {int(fail[0])}")
+    else:
+        L = ref()
+        rc = L.ref_apply_dirichlet(C.c_int(n), vp(r), vp(c), vp(v), vp(b), vp(nodes), C.c_int(len(nodes)), vp(nv),
+                                   C.c_double(constant))
+        if rc:
+            raise KindError(rc, L.ref_last_error().decode())
+    return v, b
+
+
+def ref_run_wave(n, dt, T, cap=64):
+    """The compiled reference's bench::run_wave (bench.hpp:222-300): samples
+    every 100 steps as rows (t, |p|_inf, |phi|_inf, energy)."""
+    L = ref()
+    if not hasattr(L, "ref_run_wave"):
+        raise OracleError("reference built without bench.hpp (json.hpp missing)")
+    out = np.zeros((cap, 4))
+    ns = np.zeros(1, np.int32)
+    rc = L.ref_run_wave(C.c_int(n), C.c_double(dt), C.c_double(T), C.c_int(cap), dp(out.reshape(-1)), ip(ns))
+    if rc:
+        raise KindError(rc, L.ref_last_error().decode())
+    return out[: int(ns[0])]

@@ -752,3 +752,50 @@ done:
   free(q);
   return rc;
 }
+
+/* ---- around the assembly loop -------------------------------------------- */
+
+/* fem/assemble.hpp:225-247 lower_pw + :252-314 pointwise: the reference lowers
+ * the expression to one assignment per component; out += e stages INC (0 + e,
+ * then out + staged), out -= e accumulates -e: both equal out (+|-) e. */
+int orc_pointwise(double* out, int64_t n, int assign, const int32_t* ops, const int32_t* fidx,
+                  const double* vals, int nprog, const double* const* fields) {
+  double st[64];
+  if (nprog <= 0 || nprog > 64) return ORC_ERR_INVALID_ARGUMENT;
+  for (int64_t i = 0; i < n; ++i) {
+    int sp = 0;
+    for (int q = 0; q < nprog; ++q) {
+      switch (ops[q]) {
+      case 0: st[sp++] = vals[q]; break;
+      case 1: st[sp++] = fidx[q] < 0 ? out[i] : fields[fidx[q]][i]; break;
+      case 6: st[sp - 1] = -st[sp - 1]; break;
+      default: {
+        const double b = st[--sp], a = st[sp - 1];
+        st[sp - 1] = ops[q] == 2 ? a + b : ops[q] == 3 ? a - b : ops[q] == 4 ? a * b : a / b;
+      }
+      }
+    }
+    const double v = st[0];
+    out[i] = assign == 0 ? v : assign == 1 ? out[i] + v : out[i] - v;
+  }
+  return ORC_OK;
+}
+
+/* fem/assemble.hpp:54-79 with Sparsity::find (data.hpp:129-136). */
+int orc_apply_dirichlet(int nrows, const int64_t* row_ptr, const int32_t* col_idx, double* values,
+                        double* rhs, const int32_t* nodes, int nn, const double* node_values,
+                        double constant, int32_t* fail) {
+  for (int q = 0; q < nn; ++q) {
+    const int r = nodes[q];
+    if (r < 0 || r >= nrows) return ORC_ERR_INDEX_OUT_OF_RANGE;
+    for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) values[k] = 0.0;
+    const int64_t d = orc_sparsity_find(row_ptr, col_idx, nrows, r, r);
+    if (d < 0) {
+      if (fail) *fail = r;
+      return ORC_ERR_MISSING_DIAGONAL;
+    }
+    values[d] = 1.0;
+    if (rhs) rhs[r] = node_values ? node_values[r] : constant;
+  }
+  return ORC_OK;
+}

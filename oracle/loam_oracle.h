@@ -138,6 +138,26 @@ int orc_cg(const int32_t* row_sizes, const int32_t* col_sizes, const int64_t* co
            const int32_t* const* col_idx, const double* const* values, int nested, const double* b, double* x,
            double rtol, double atol, int maxit, int jacobi, int32_t* report, double* rnorm, int32_t* fail);
 
+/* ---- around the assembly loop ------------------------ */
+
+/* pointwise (fem/assemble.hpp:150-319): out (=|+=|-=) expr for every one of n
+ * values; expr is a postfix program (op codes as include/loam_gpu.h
+ * loam_pw_opcode: 0 const, 1 field, 2 add, 3 sub, 4 mul, 5 div, 6 neg; field
+ * -1 = out).  assign: 0 =, 1 +=, 2 -=.  Evaluated like the reference's
+ * lowered AST: one rounding per operation, left operand first. */
+int orc_pointwise(double* out, int64_t n, int assign, const int32_t* ops, const int32_t* fidx,
+                  const double* vals, int nprog, const double* const* fields);
+
+/* apply_dirichlet (fem/assemble.hpp:54-66; rhs NULL: apply_dirichlet_rows
+ * :69-79): for each node r in order, zero row r, find (r, r), set it to 1,
+ * rhs[r] = node_values ? node_values[r] : constant.  Returns
+ * ORC_ERR_MISSING_DIAGONAL (*fail = r) at the first row without a diagonal,
+ * after modifying the earlier rows -- the reference's order. */
+#define ORC_ERR_MISSING_DIAGONAL (1 + 17)
+int orc_apply_dirichlet(int nrows, const int64_t* row_ptr, const int32_t* col_idx, double* values,
+                        double* rhs, const int32_t* nodes, int nn, const double* node_values,
+                        double constant, int32_t* fail);
+
 #ifdef __cplusplus
 }
 #endif

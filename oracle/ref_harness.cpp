@@ -20,6 +20,9 @@
 #include <vector>
 
 #include "loam/loam.hpp"
+#ifdef LOAM_REF_HAVE_BENCH
+#include "loam/bench.hpp"
+#endif
 #include "loam_oracle.h"
 
 using namespace loam;
@@ -481,3 +484,116 @@ int ref_cg_solve(int nested, const int32_t* rs, const int32_t* cs, const int64_t
 }
 
 } // extern "C"
+
+// ---- around the assembly loop (fem/assemble.hpp, fem/bc.hpp) --------------
+namespace {
+fem::Pw pw_from_program(const int32_t* ops, const int32_t* fidx, const double* vals, int nprog,
+                        const std::vector<DatPtr>& fields, const DatPtr& out) {
+  std::vector<fem::Pw> st;
+  for (int q = 0; q < nprog; ++q) {
+    switch (ops[q]) {
+    case 0: st.push_back(fem::pw(vals[q])); break;
+    case 1: st.push_back(fem::pw(fidx[q] < 0 ? out : fields[fidx[q]])); break;
+    case 6: st.back() = -st.back(); break;
+    default: {
+      fem::Pw b = st.back();
+      st.pop_back();
+      fem::Pw a = st.back();
+      st.back() = ops[q] == 2 ? a + b : ops[q] == 3 ? a - b : ops[q] == 4 ? a * b : a / b;
+    }
+    }
+  }
+  return st.back();
+}
+} // namespace
+
+extern "C" {
+
+// fem::pointwise (fem/assemble.hpp:252-314) on a Set of `size` nodes of `dim`
+// components; out in/out.
+int ref_pointwise(int size, int dim, int assign, const int32_t* ops, const int32_t* fidx, const double* vals,
+                  int nprog, int nfields, const double* const* fields, double* out) {
+  try {
+    auto set = make_set(size, "nodes");
+    auto o = make_dat(set, dim, "out");
+    std::memcpy(o->mutable_view().data(), out, sizeof(double) * static_cast<size_t>(size) * dim);
+    std::vector<DatPtr> fs;
+    for (int k = 0; k < nfields; ++k) {
+      fs.push_back(make_dat(set, dim, "field"));
+      std::memcpy(fs.back()->mutable_view().data(), fields[k], sizeof(double) * static_cast<size_t>(size) * dim);
+    }
+    const auto op = assign == 0 ? fem::PwOp::Assign : assign == 1 ? fem::PwOp::Add : fem::PwOp::Sub;
+    fem::pointwise(o, op, pw_from_program(ops, fidx, vals, nprog, fs, o));
+    std::memcpy(out, o->view().data(), sizeof(double) * static_cast<size_t>(size) * dim);
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
+// fem::apply_dirichlet / apply_dirichlet_rows (fem/assemble.hpp:54-79) with a
+// DirichletBC (fem/bc.hpp) on a node set of nrows nodes; values / rhs in-out.
+int ref_apply_dirichlet(int nrows, const int64_t* rp, const int32_t* ci, double* values, double* rhs,
+                        const int32_t* nodes, int nn, const double* node_values, double constant) {
+  try {
+    auto A = mat_from_csr(nrows, nrows, rp, ci, values);
+    auto space = std::make_shared<fem::FunctionSpace>();
+    space->node_set = make_set(nrows, "nodes");
+    fem::DirichletBC bc;
+    bc.space = space;
+    bc.constant = constant;
+    if (node_values) {
+      bc.function = std::make_shared<fem::Function>();
+      bc.function->space = space;
+      bc.function->dat = make_dat(space->node_set, 1, "bc");
+      std::memcpy(bc.function->dat->mutable_view().data(), node_values, sizeof(double) * nrows);
+    }
+    bc.nodes.assign(nodes, nodes + nn);
+    int code = 0;
+    try {
+      if (rhs) {
+        auto b = make_dat(space->node_set, 1, "rhs");
+        std::memcpy(b->mutable_view().data(), rhs, sizeof(double) * nrows);
+        try {
+          fem::apply_dirichlet(*A, *b, bc);
+        } catch (const Error& e) {
+          code = fail_code(e);
+        }
+        std::memcpy(rhs, b->view().data(), sizeof(double) * nrows);
+      } else {
+        fem::apply_dirichlet_rows(*A, bc);
+      }
+    } catch (const Error& e) {
+      code = fail_code(e);
+    }
+    std::memcpy(values, A->values().data(), sizeof(double) * static_cast<size_t>(rp[nrows]));
+    return code;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
+} // extern "C"
+
+#ifdef LOAM_REF_HAVE_BENCH
+extern "C" {
+// bench::run_wave (bench.hpp:222-300): the reference's explicit wave loop.
+// samples: [cap x 4] rows (t, |p|_inf, |phi|_inf, energy) every 100 steps.
+int ref_run_wave(int n, double dt, double T, int cap, double* samples, int32_t* nsamples) {
+  try {
+    auto r = bench::run_wave(n, dt, T, 1);
+    const int m = std::min<int>(cap, static_cast<int>(r.sample_times.size()));
+    for (int k = 0; k < m; ++k) {
+      samples[4 * k] = r.sample_times[k];
+      samples[4 * k + 1] = r.norm_p[k];
+      samples[4 * k + 2] = r.norm_phi[k];
+      samples[4 * k + 3] = r.energy[k];
+    }
+    *nsamples = m;
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+} // extern "C"
+#endif

@@ -84,6 +84,15 @@ class BlockMatDesc(C.Structure):  # loam_block_mat (solver.hpp:21-28 BlockMat)
                 ("row_sizes", C.c_int32 * 2), ("col_sizes", C.c_int32 * 2)]
 
 
+class PwInstr(C.Structure):  # loam_pw_instr (pointwise program, fem/assemble.hpp:150-319)
+    _fields_ = [("op", C.c_int32), ("field", C.c_int32), ("value", C.c_double)]
+
+
+PW_CONST, PW_FIELD, PW_ADD, PW_SUB, PW_MUL, PW_DIV, PW_NEG = range(7)
+PW_ASSIGN, PW_ADD_TO, PW_SUB_FROM = range(3)
+REDUCE_SUM, REDUCE_MIN, REDUCE_MAX, REDUCE_MAX_ABS = range(4)
+
+
 class SolveReportDesc(C.Structure):  # loam_solve_report (solver.hpp:13-18)
     _fields_ = [("iterations", C.c_int32), ("final_residual_norm", C.c_double), ("converged", C.c_int32),
                 ("reason", C.c_int32)]
@@ -138,6 +147,10 @@ def lib() -> C.CDLL:
                                             i32, i32, C.POINTER(SolveReportDesc), vp]),
             "loam_gpu_cg_solve_block": (C.c_int, [C.POINTER(BlockMatDesc), vp, i64, vp, C.c_double, C.c_double,
                                                   i32, i32, C.POINTER(SolveReportDesc), vp]),
+            "loam_gpu_apply_dirichlet": (C.c_int, [C.POINTER(SparsityDesc), vp, vp, vp, i32, vp, C.c_double, vp]),
+            "loam_gpu_bc_apply": (C.c_int, [vp, i32, vp, i32, vp, C.c_double, vp]),
+            "loam_gpu_pointwise": (C.c_int, [vp, i64, i32, C.POINTER(PwInstr), i32, C.POINTER(vp), i32, vp]),
+            "loam_gpu_reduce": (C.c_int, [vp, i64, i32, dp, vp]),
         }
         for name, (res, args) in proto.items():
             fn = getattr(L, name)
@@ -159,6 +172,7 @@ EXPORTED = [
     "loam_gpu_permute_cells", "loam_gpu_uniform", "loam_gpu_p2_cell_node_map",
     "loam_gpu_expand_map", "loam_gpu_spmv", "loam_gpu_block_spmv", "loam_gpu_cg_solve",
     "loam_gpu_cg_solve_block",
+    "loam_gpu_apply_dirichlet", "loam_gpu_bc_apply", "loam_gpu_pointwise", "loam_gpu_reduce",
 ]
 
 

@@ -13,6 +13,7 @@
 #include "engine.cuh"
 #include "plan.cuh"
 #include "solver.cuh"
+#include "fem.cuh"
 
 using namespace loam_gpu;
 
@@ -368,6 +369,48 @@ int loam_gpu_memset(void* dst, int value, size_t bytes, void* stream) {
 }
 int loam_gpu_stream_sync(void* stream) {
   return guarded([&] { LG_CUDA(cudaStreamSynchronize(as_stream(stream))); });
+}
+
+} // extern "C"
+
+// ---- around the assembly loop (fem.cu) -----------------------------------
+extern "C" {
+
+int loam_gpu_apply_dirichlet(const loam_sparsity_desc* sparsity, double* values, double* rhs, const int32_t* nodes,
+                             int32_t nnodes, const double* node_values, double constant, void* stream) {
+  return guarded([&] {
+    require_device();
+    apply_dirichlet(sparsity, values, rhs, nodes, nnodes, node_values, constant, as_stream(stream));
+  });
+}
+
+int loam_gpu_bc_apply(double* dat, int32_t set_size, const int32_t* nodes, int32_t nnodes, const double* node_values,
+                      double constant, void* stream) {
+  return guarded([&] {
+    require_device();
+    bc_apply(dat, set_size, nodes, nnodes, node_values, constant, as_stream(stream));
+  });
+}
+
+int loam_gpu_pointwise(double* out, int64_t n, int32_t op, const loam_pw_instr* program, int32_t nprogram,
+                       const double* const* fields, int32_t nfields, void* stream) {
+  return guarded([&] {
+    pw_check(program, nprogram, nfields); // program errors are reported without a device
+    require_device();
+    pointwise(out, n, op, program, nprogram, fields, nfields, as_stream(stream));
+  });
+}
+
+int loam_gpu_reduce(const double* x, int64_t n, int32_t kind, double* result, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(result != nullptr, LOAM_ERR(InvalidArgument), "reduce without a result");
+    const cudaStream_t s = as_stream(stream);
+    DevBuf<double> r(1, s);
+    reduce(x, n, kind, r.get(), s);
+    LG_CUDA(cudaMemcpyAsync(result, r.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+    LG_CUDA(cudaStreamSynchronize(s));
+  });
 }
 
 } // extern "C"

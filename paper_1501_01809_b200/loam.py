@@ -604,3 +604,150 @@ def cg_solve(op, b, x0=None, rtol: float = 1e-8, atol: float = 1e-14, maxit: int
         capi.check(capi.lib().loam_gpu_cg_solve(op.sparsity.desc(), op.values.data_ptr(), bt.data_ptr(), n,
                                                 x.data_ptr(), rtol, atol, maxit, precond, C.byref(rep), _stream()))
     return x[:n], SolveReport(rep)
+
+
+# --------------------------------------------------------------------------
+# Around the assembly loop: pointwise expressions
+# (fem/assemble.hpp:150-319), Dirichlet conditions (fem/bc.hpp,
+# fem/assemble.hpp:54-81) and norms, on the device through the C ABI.
+
+class Pw:
+    """fem/assemble.hpp:150-205 PwNode tree: constants, Dat fields, + - * / and negation."""
+
+    def __init__(self, kind: str, value: float = 0.0, field: "Dat | None" = None, a=None, b=None):
+        self.kind, self.value, self.field, self.a, self.b = kind, float(value), field, a, b
+
+    def __add__(self, o): return Pw("add", a=self, b=_as_pw(o))
+    def __radd__(self, o): return Pw("add", a=_as_pw(o), b=self)
+    def __sub__(self, o): return Pw("sub", a=self, b=_as_pw(o))
+    def __rsub__(self, o): return Pw("sub", a=_as_pw(o), b=self)
+    def __mul__(self, o): return Pw("mul", a=self, b=_as_pw(o))
+    def __rmul__(self, o): return Pw("mul", a=_as_pw(o), b=self)
+    def __truediv__(self, o): return Pw("div", a=self, b=_as_pw(o))
+    def __rtruediv__(self, o): return Pw("div", a=_as_pw(o), b=self)
+    def __neg__(self): return Pw("neg", a=self)
+
+    def fields(self, out: list) -> list:
+        """collect_fields (assemble.hpp:209-220): first-appearance order, unique."""
+        if self.kind == "field":
+            if not any(f is self.field for f in out):
+                out.append(self.field)
+        for c in (self.a, self.b):
+            if c is not None:
+                c.fields(out)
+        return out
+
+    def program(self, slot) -> list:
+        """Postfix program (left subtree, right subtree, operator)."""
+        if self.kind == "const":
+            return [(capi.PW_CONST, 0, self.value)]
+        if self.kind == "field":
+            return [(capi.PW_FIELD, slot(self.field), 0.0)]
+        if self.kind == "neg":
+            return self.a.program(slot) + [(capi.PW_NEG, 0, 0.0)]
+        op = {"add": capi.PW_ADD, "sub": capi.PW_SUB, "mul": capi.PW_MUL, "div": capi.PW_DIV}[self.kind]
+        return self.a.program(slot) + self.b.program(slot) + [(op, 0, 0.0)]
+
+
+def _as_pw(x) -> Pw:
+    return x if isinstance(x, Pw) else pw(x)
+
+
+def pw(x) -> Pw:
+    """fem::pw(Real) / fem::pw(DatPtr)."""
+    if isinstance(x, Dat):
+        return Pw("field", field=x)
+    return Pw("const", value=float(x))
+
+
+class PwOp:
+    ASSIGN, ADD, SUB = capi.PW_ASSIGN, capi.PW_ADD_TO, capi.PW_SUB_FROM
+
+
+def pointwise(out: Dat, op: int, expr) -> None:
+    """fem::pointwise (assemble.hpp:252-314): out (=|+=|-=) expr at every node
+    and component; every field lives on out's set with out's dim
+    (SpaceMismatch otherwise).  Bitwise equal to the reference."""
+    expr = _as_pw(expr)
+    fields = expr.fields([])
+    for f in fields:
+        _require(f.set is out.set, "SpaceMismatch", "pointwise fields must share the output's set")
+        _require(f.dim == out.dim, "SpaceMismatch", "pointwise fields must share the output's component count")
+    inputs = [f for f in fields if f is not out]
+    prog = expr.program(lambda f: -1 if f is out else next(i for i, g in enumerate(inputs) if g is f))
+    arr = (capi.PwInstr * len(prog))(*[capi.PwInstr(o, fi, v) for o, fi, v in prog])
+    for f in fields:
+        f._materialize()
+    out._materialize()
+    ptrs = (C.c_void_p * max(len(inputs), 1))(*[f.data.data_ptr() for f in inputs])
+    capi.check(capi.lib().loam_gpu_pointwise(out.data.data_ptr(), out.set.size * out.dim, op, arr, len(prog),
+                                             ptrs, len(inputs), _stream()))
+    out.version += 1
+    out._zero = out._stale = False
+
+
+class DirichletBC:
+    """fem/bc.hpp:11-27: strong condition on `nodes` (sorted) of a scalar node
+    set, value = `constant` or a Dat `function` on that set."""
+
+    def __init__(self, node_set: Set, nodes, constant: float = 0.0, function: "Dat | None" = None):
+        if function is not None:
+            _require(function.set is node_set, "SpaceMismatch", "bc value must live on the constrained space")
+        self.node_set, self.constant, self.function = node_set, float(constant), function
+        self.nodes = np.unique(np.asarray(nodes, dtype=np.int32))
+        self._dev = torch.as_tensor(self.nodes).cuda()
+
+    def value_at(self, node: int) -> float:
+        return float(self.function.view()[node]) if self.function is not None else self.constant
+
+    def _values(self):
+        if self.function is None:
+            return None
+        self.function._materialize()
+        return self.function.data.data_ptr()
+
+    def apply(self, dat: Dat) -> None:
+        """bc.apply(b) (bc.hpp:21-26)."""
+        _require(dat.set is self.node_set, "SpaceMismatch", "bc applied to a vector on a different node set")
+        dat._materialize()
+        capi.check(capi.lib().loam_gpu_bc_apply(dat.data.data_ptr(), dat.set.size, self._dev.data_ptr(),
+                                                len(self.nodes), self._values(), self.constant, _stream()))
+        dat.version += 1
+        dat._zero = dat._stale = False
+
+
+def apply_dirichlet(A: Mat, b: "Dat | None", bc: DirichletBC) -> None:
+    """fem/assemble.hpp:54-66 (b None: apply_dirichlet_rows, :69-79)."""
+    _require(b is None or A.nrows == bc.node_set.size, "ShapeMismatch", "matrix is not square on the bc space")
+    A._materialize()
+    if b is not None:
+        b._materialize()
+    capi.check(capi.lib().loam_gpu_apply_dirichlet(A.sparsity.desc(), A.values.data_ptr(),
+                                                   b.data.data_ptr() if b is not None else None,
+                                                   bc._dev.data_ptr(), len(bc.nodes), bc._values(), bc.constant,
+                                                   _stream()))
+    A._zero = A._stale = False
+    if b is not None:
+        b.version += 1
+        b._zero = b._stale = False
+
+
+def apply_dirichlet_rows(A: Mat, bc: DirichletBC) -> None:
+    apply_dirichlet(A, None, bc)
+
+
+def reduce(x, kind: int) -> float:
+    """Deterministic device reduction (SUM / MIN / MAX / MAX_ABS) of a Dat or tensor."""
+    if isinstance(x, Dat):
+        x._materialize()
+        t, n = x.data, x.set.size * x.dim
+    else:
+        t = _vec(x)
+        n = t.numel()
+    r = C.c_double()
+    capi.check(capi.lib().loam_gpu_reduce(t.data_ptr(), n, kind, C.byref(r), _stream()))
+    return r.value
+
+
+def inf_norm(x) -> float:
+    return reduce(x, capi.REDUCE_MAX_ABS)

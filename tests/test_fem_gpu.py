@@ -1,0 +1,153 @@
+"""SURVEY 8f-2 / 8f-3 on the device, against the compiled reference.
+
+* pointwise (fem/assemble.hpp:150-319): bitwise equal to fem::pointwise;
+* apply_dirichlet / apply_dirichlet_rows (fem/assemble.hpp:54-79) and
+  DirichletBC::apply (fem/bc.hpp:21-26): bitwise equal; MissingDiagonal is
+  reported before any row changes;
+* reductions; the wave time-step chain (bench.hpp:222-300) reproduces
+  bench::run_wave's diagnostics (tolerance 1e-10 relative: the stiffness
+  action is summed in a different order, and the chain runs 300 steps).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_1501_01809_b200 import capi, configs
+from paper_1501_01809_b200 import loam as L
+
+pytestmark = pytest.mark.gpu
+needs_ref = pytest.mark.skipif(not O.ref_available(), reason="compiled reference (oracle/_ref) not built")
+
+
+def random_expr(rng, fields, out, depth=4):
+    """A random Pw tree and its postfix program (reference field order: as collected)."""
+    def node(d):
+        if d == 0 or rng.random() < 0.25:
+            if rng.random() < 0.4:
+                return L.pw(float(rng.uniform(-2, 2)))
+            k = int(rng.integers(-1, len(fields)))
+            return L.pw(out if k < 0 else fields[k])
+        if rng.random() < 0.15:
+            return -node(d - 1)
+        a, b = node(d - 1), node(d - 1)
+        return [a + b, a - b, a * b, a / b][int(rng.integers(0, 4))]
+    return node(depth)
+
+
+@needs_ref
+@pytest.mark.parametrize("seed", range(5))
+@pytest.mark.parametrize("op", [L.PwOp.ASSIGN, L.PwOp.ADD, L.PwOp.SUB])
+def test_pointwise_is_bitwise_reference(gpu_lib, seed, op):
+    rng = np.random.default_rng(seed)
+    s, dim = L.Set(211), 1 + seed % 2
+    fields = []
+    for _ in range(3):
+        d = L.Dat(s, dim)
+        d.set_values(rng.standard_normal(s.size * dim) + 3.0)
+        fields.append(d)
+    out = L.Dat(s, dim)
+    out.set_values(rng.standard_normal(s.size * dim) + 3.0)
+    before = out.view().copy()
+    expr = random_expr(rng, fields, out)
+    used = expr.fields([])
+    inputs = [f for f in used if f is not out]
+    prog = expr.program(lambda f: -1 if f is out else next(i for i, g in enumerate(inputs) if g is f))
+    L.pointwise(out, op, expr)
+    ref = O.pointwise(prog, op, before.reshape(s.size, dim), [f.view() for f in inputs], lib="ref")
+    assert np.array_equal(out.view(), ref.reshape(-1))
+
+
+def test_pointwise_checks_spaces(gpu_lib):  # assemble.hpp:259-264
+    a, b = L.Dat(L.Set(5), 1), L.Dat(L.Set(5), 1)
+    with pytest.raises(capi.LoamError) as e:
+        L.pointwise(a, L.PwOp.ASSIGN, L.pw(b) * 2.0)
+    assert e.value.kind == "SpaceMismatch"
+    c = L.Dat(a.set, 2)
+    with pytest.raises(capi.LoamError):
+        L.pointwise(a, L.PwOp.ASSIGN, L.pw(c))
+
+
+def assembled(n=12, seed=0):
+    m = configs.mesh(2, n, 0.2, seed, seed + 1)
+    cells, verts = L.Set(m.ncells), L.Set(m.nv)
+    cm = L.Map(cells, verts, 3, m.cv)
+    X = L.Dat(verts, 2)
+    X.set_values(m.coords)
+    A = L.Mat(L.build_sparsity(cm, cm))
+    L.execute(L.Parloop(L.kernel("helmholtz_p1_tri", 1.0), cells, [L.arg(A, L.INC, cm, cm), L.arg(X, L.READ, cm)]))
+    return m, verts, A
+
+
+@needs_ref
+@pytest.mark.parametrize("function", [False, True])
+@pytest.mark.parametrize("with_rhs", [True, False])
+def test_apply_dirichlet_is_bitwise_reference(gpu_lib, function, with_rhs):
+    rng = np.random.default_rng(5)
+    m, verts, A = assembled()
+    rp, ci = A.sparsity.host()
+    vals = A.host_values()
+    nodes = np.nonzero(np.arange(m.nv) % 13 == 0)[0]  # marker-1 side of the 12x12 square
+    fn = None
+    if function:
+        fn = L.Dat(verts, 1)
+        fn.set_values(rng.standard_normal(m.nv))
+    bc = L.DirichletBC(verts, nodes, 0.625, fn)
+    b = L.Dat(verts, 1)
+    rhs = rng.standard_normal(m.nv)
+    b.set_values(rhs)
+    if with_rhs:
+        L.apply_dirichlet(A, b, bc)
+    else:
+        L.apply_dirichlet_rows(A, bc)
+    rv, rb = O.apply_dirichlet((m.nv, m.nv, rp, ci, vals), rhs if with_rhs else None, nodes,
+                               fn.view() if fn is not None else None, 0.625, lib="ref")
+    assert np.array_equal(A.host_values(), rv)
+    if with_rhs:
+        assert np.array_equal(b.view(), rb)
+
+
+def test_bc_apply(gpu_lib):  # bc.hpp:21-26
+    s = L.Set(40)
+    d = L.Dat(s, 1)
+    d.set_values(np.arange(40.0))
+    bc = L.DirichletBC(s, [3, 1, 7], -2.5)
+    bc.apply(d)
+    ref = np.arange(40.0)
+    ref[[1, 3, 7]] = -2.5
+    assert np.array_equal(d.view(), ref)
+    with pytest.raises(capi.LoamError) as e:
+        bc.apply(L.Dat(L.Set(40), 1))
+    assert e.value.kind == "SpaceMismatch"
+
+
+def test_missing_diagonal_reported_before_mutation(gpu_lib):  # assemble.hpp:61-62
+    s = L.Set(3)
+    rp = torch.tensor([0, 1, 2, 3], dtype=torch.int64, device="cuda")
+    ci = torch.tensor([1, 1, 2], dtype=torch.int32, device="cuda")
+    A = L.Mat(L.Sparsity(3, 3, rp, ci))
+    A.values[:3] = 7.0
+    A._zero = A._stale = False
+    with pytest.raises(capi.LoamError) as e:
+        L.apply_dirichlet(A, L.Dat(s, 1), L.DirichletBC(s, [1, 0]))
+    assert e.value.kind == "MissingDiagonal" and "diagonal (0, 0) outside sparsity" in str(e.value)
+    assert np.array_equal(A.host_values(), [7.0, 7.0, 7.0])
+
+
+def test_reductions(gpu_lib):
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(100003)
+    assert L.reduce(x, capi.REDUCE_MAX_ABS) == np.max(np.abs(x))
+    assert L.reduce(x, capi.REDUCE_MIN) == np.min(x)
+    assert L.reduce(x, capi.REDUCE_MAX) == np.max(x)
+    assert abs(L.reduce(x, capi.REDUCE_SUM) - np.sum(x)) <= 1e-12 * np.sum(np.abs(x))
+
+
+@needs_ref
+def test_wave_chain_reproduces_reference_run_wave(gpu_lib):  # bench.hpp:222-300, test_bench.cpp:59
+    from paper_1501_01809_b200.wave import WaveLoop
+    ref = O.ref_run_wave(8, 1e-3, 0.3)
+    got = np.array(WaveLoop(8, 1e-3, 0.3).run())
+    assert got.shape == ref.shape and got.shape[0] >= 3
+    assert np.array_equal(got[:, 0], ref[:, 0])  # sample times
+    assert np.max(np.abs(got[:, 1:] - ref[:, 1:]) / np.abs(ref[:, 1:])) <= 1e-10
