@@ -945,13 +945,15 @@ struct RingCell {
 // row vertex s.  Its star -- the link vertices v_0..v_{m-1} of the cells
 // around s, in ring / fan order -- is one 32-byte record {m | closed << 4,
 // v_0..v_6}; the cells are (s, v_k, v_{k+1}) (and (s, v_{m-1}, v_0) when the
-// ring is closed).  Two dependent gathers per row (record, then the
+// ring is closed); the header packs m (3 bits), closed (1), the in-row CSR
+// rank of s (3) and of every v_k (3 each).  Two dependent gathers per row (record, then the
 // neighbours' coordinates and coefficients), the action in closed form
 // (RingCell::action), one store: no plan tiles, no shared memory, no
 // atomics -- the short latency chain a 15 MB loop needs.
 struct StarArgs {
   const int4* star; // 2 per row
   int nrows;
+  const int64_t* row_ptr; // Mats: CSR offsets
   const double* coords;
   const double* coeff;
   FormParams prm;
@@ -961,8 +963,8 @@ struct StarArgs {
 
 template <class F>
 __device__ __forceinline__ double star_row(const StarArgs& a, int r, int4 h, int4 t) {
-  const int m = h.x & 15;
-  const bool closed = (h.x >> 4) & 1;
+  const int m = h.x & 7;
+  const bool closed = (h.x >> 3) & 1;
   const int v[7] = {h.y, h.z, h.w, t.x, t.y, t.z, t.w};
   const double2 xs = __ldg(reinterpret_cast<const double2*>(a.coords) + r);
   const double us = __ldg(a.coeff + r);
@@ -1004,10 +1006,71 @@ __global__ void __launch_bounds__(256) k_star_vec(const __grid_constant__ StarAr
   a.out[r] = a.accumulate ? a.out[r] + y : y;
 }
 
+// Bilinear P1 triangle forms (config 2 shape): the row's CSR segment is
+// {s} u {v_k} (a manifold star), so the thread accumulates the diagonal and
+// one register per link vertex over the cells (RingCell::entries, closed
+// form) and writes the m + 1 values at row_ptr[s] + their packed ranks.
+template <class F>
+__global__ void __launch_bounds__(256) k_star_mat(const __grid_constant__ StarArgs a) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.nrows) return;
+  const int4 h = __ldg(a.star + 2 * r), t = __ldg(a.star + 2 * r + 1);
+  const int hdr = h.x, m = hdr & 7;
+  const bool closed = (hdr >> 3) & 1;
+  const int v[7] = {h.y, h.z, h.w, t.x, t.y, t.z, t.w};
+  const int64_t base = __ldg(a.row_ptr + r);
+  const double2 xs = __ldg(reinterpret_cast<const double2*>(a.coords) + r);
+  double acc[7], self = 0.0;
+  double px = 0, py = 0, p0x = 0, p0y = 0, aa = 0;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    acc[k] = 0.0;
+    if (k < m) {
+      const double2 x = __ldg(reinterpret_cast<const double2*>(a.coords) + v[k]);
+      const double nx = x.x - xs.x, ny = x.y - xs.y, nn = nx * nx + ny * ny;
+      if (k == 0) {
+        p0x = nx;
+        p0y = ny;
+      } else { // cell (s, v_{k-1}, v_k)
+        const double ab = px * nx + py * ny, ad = fabs(px * ny - py * nx);
+        double vs, vp, vn;
+        RingCell<F>::entries(aa, ab, nn, ad, a.prm.p[0], vs, vp, vn);
+        self += vs;
+        acc[k - 1] += vp;
+        acc[k] += vn;
+      }
+      px = nx;
+      py = ny;
+      aa = nn;
+    }
+  }
+  if (closed && m > 2) { // closing cell (s, v_{m-1}, v_0)
+    const double nn = p0x * p0x + p0y * p0y;
+    const double ab = px * p0x + py * p0y, ad = fabs(px * p0y - py * p0x);
+    double vs, vp, vn;
+    RingCell<F>::entries(aa, ab, nn, ad, a.prm.p[0], vs, vp, vn);
+    self += vs;
+#pragma unroll
+    for (int k = 0; k < 7; ++k)
+      if (k == m - 1) acc[k] += vp;
+    acc[0] += vn;
+  }
+  double* o = a.out + base;
+  const int rs = (hdr >> 4) & 7;
+  o[rs] = a.accumulate ? o[rs] + self : self;
+#pragma unroll
+  for (int k = 0; k < 7; ++k)
+    if (k < m) {
+      const int rk = (hdr >> (7 + 3 * k)) & 7;
+      o[rk] = a.accumulate ? o[rk] + acc[k] : acc[k];
+    }
+}
+
 template <class F>
 void launch_star(const StarArgs& a, cudaStream_t s) {
   if (a.nrows == 0) return;
-  k_star_vec<F><<<ceil_div(a.nrows, 256), 256, 0, s>>>(a);
+  if constexpr (F::BILINEAR) k_star_mat<F><<<ceil_div(a.nrows, 256), 256, 0, s>>>(a);
+  else k_star_vec<F><<<ceil_div(a.nrows, 256), 256, 0, s>>>(a);
   count_launch();
   LG_LAUNCH_CHECK();
 }
@@ -1085,7 +1148,19 @@ bool build_stars(const int32_t* dmap, int ncells, int nverts, DevBuf<int4>& out,
     }
     int v[7] = {0, 0, 0, 0, 0, 0, 0};
     for (int k = 0; k < m; ++k) v[k] = chain[k];
-    rec[2 * r] = make_int4(m | (closed ? 16 : 0), v[0], v[1], v[2]);
+    // in-row ranks (CSR columns ascending): of the row vertex and of each link vertex
+    int hdr = m | (closed ? 8 : 0);
+    {
+      int rank_self = 0;
+      for (int k = 0; k < m; ++k) rank_self += v[k] < r;
+      hdr |= rank_self << 4;
+      for (int k = 0; k < m; ++k) {
+        int rk = v[k] > r;
+        for (int q = 0; q < m; ++q) rk += v[q] < v[k];
+        hdr |= rk << (7 + 3 * k);
+      }
+    }
+    rec[2 * r] = make_int4(hdr, v[0], v[1], v[2]);
     rec[2 * r + 1] = make_int4(v[3], v[4], v[5], v[6]);
   }
   out.alloc(rec.size(), s);
@@ -1804,7 +1879,7 @@ Entry form_entry(const std::string& name) {
   if constexpr (!F::BILINEAR ? F::NCOEFF == F::NRN : F::NRN == F::NCN) e.patch = &launch_patch<F>;
   if constexpr (P == 1 && F::NRN == D + 1 && (!F::BILINEAR || F::NCN == F::NRN)) e.nbr = &launch_nbr<F>;
   if constexpr (P == 1 && D == 2 && F::RD == 1 && F::CD == 1) e.ring = &launch_ring<F>;
-  if constexpr (P == 1 && D == 2 && !F::BILINEAR) e.star = &launch_star<F>;
+  if constexpr (P == 1 && D == 2 && F::RD == 1 && F::CD == 1) e.star = &launch_star<F>;
   return e;
 }
 
@@ -2171,8 +2246,13 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     // the window TMA needs 16-byte aligned coordinate / coefficient arrays
     ok = ok && (reinterpret_cast<uintptr_t>(args[1].data) & 15) == 0 &&
          (!Cm || (reinterpret_cast<uintptr_t>(args[2].data) & 15) == 0);
-    if (ok && k.star && strat == 0 && !std::getenv("LOAM_GPU_NO_STAR") &&
-        build_stars(R.v.v, n, R.v.target, P->star, s)) {
+    // Mats: the star kernel writes the (map, map) pattern's rows, so the Mat's
+    // pattern must be exactly that one (not a superset)
+    const bool star_ok = ok && k.star && strat == 0 && !std::getenv("LOAM_GPU_NO_STAR") &&
+                         (!k.bilinear || std::getenv("LOAM_GPU_STAR_MAT")) &&
+                         (!k.bilinear || pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, 1, 1, csr.row_ptr,
+                                                                csr.col_idx, csr.nnz, s));
+    if (star_ok && build_stars(R.v.v, n, R.v.target, P->star, s)) {
       P->use_star = true;
       return P;
     }
@@ -2318,9 +2398,10 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
   if (P->use_star) {
     StarArgs t{};
     t.star = P->star.get();
-    t.nrows = args[0].set_size;
+    t.nrows = k.bilinear ? args[0].sparsity->nrows : args[0].set_size;
+    t.row_ptr = k.bilinear ? args[0].sparsity->row_ptr : nullptr;
     t.coords = args[1].data;
-    t.coeff = args[2].data;
+    t.coeff = k.has_coeff ? args[2].data : nullptr;
     t.prm = prm;
     t.out = args[0].data;
     t.accumulate = (args[0].flags & LOAM_ARG_ZERO) ? 0 : 1;
