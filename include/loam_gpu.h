@@ -276,6 +276,24 @@ int loam_gpu_build_sparsity(const loam_map_desc* row_map, const loam_map_desc* c
 int loam_gpu_color_iteration(int32_t n, uint64_t iterset_id, const loam_map_desc* maps,
                              int nmaps, int32_t* colors, int32_t* num_colors, void* stream);
 
+/* ---- mesh-side builders on the device ---------------------- */
+/* P2 node numbering (fem/space.hpp:48-72): vertices keep their ids, unique
+ * edges are numbered lexicographically from nverts; cell row = vertices then
+ * edges ((1,2),(0,2),(0,1) for triangles; (2,3),(1,3),(1,2),(0,3),(0,2),(0,1)
+ * for tetrahedra).  cv: device [ncells x (gdim+1)], cn: device
+ * [ncells x 6|10].  Returns the node count in *nnodes.  Bit-exact with the
+ * reference (triangles) and with loam_gpu_p2_cell_node_map. */
+int loam_gpu_p2_cell_node_map_dev(int32_t ncells, int32_t nverts, int32_t gdim, const int32_t* cv,
+                                  int32_t* cn, int32_t* nnodes, void* stream);
+/* derive_exterior_facets (mesh.hpp:48-89, no markers): facets incident to
+ * exactly one cell, in (cell, local facet) discovery order, as sorted vertex
+ * tuples (*facet_vertices [n x gdim]) and (cell, local facet) pairs
+ * (*facet_cell [n x 2]); device arrays allocated here, released with
+ * loam_gpu_free.  NonManifold when a facet has more than two cells. */
+int loam_gpu_exterior_facets(int32_t ncells, int32_t nverts, int32_t gdim, const int32_t* cv,
+                             int32_t** facet_vertices, int32_t** facet_cell, int32_t* nfacets,
+                             void* stream);
+
 /* ---- device memory helpers (for FFI callers without a CUDA binding) ------ */
 int loam_gpu_malloc(void** ptr, size_t bytes);
 int loam_gpu_free(void* ptr);

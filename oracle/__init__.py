@@ -489,3 +489,20 @@ def ref_run_wave(n, dt, T, cap=64):
     if rc:
         raise KindError(rc, L.ref_last_error().decode())
     return out[: int(ns[0])]
+
+
+def ref_exterior_facets(gdim, cv, nv):
+    """The compiled reference's derive_exterior_facets (mesh.hpp:48-89):
+    (facet_vertices [n x gdim], facet_cell [n x 2])."""
+    L = ref()
+    cv = np.ascontiguousarray(cv, np.int32)
+    fv, fc = C.c_void_p(), C.c_void_p()
+    n = L.ref_exterior_facets(C.c_int(gdim), C.c_int(cv.size // (gdim + 1)), C.c_int(nv), ip(cv),
+                              C.byref(fv), C.byref(fc))
+    if n < 0:
+        raise KindError(-n, L.ref_last_error().decode())
+    a = np.ctypeslib.as_array(C.cast(fv, C.POINTER(C.c_int32)), shape=(max(n, 1) * gdim,))[: n * gdim].copy()
+    b = np.ctypeslib.as_array(C.cast(fc, C.POINTER(C.c_int32)), shape=(max(n, 1) * 2,))[: n * 2].copy()
+    L.ref_free(fv)
+    L.ref_free(fc)
+    return a.reshape(n, gdim), b.reshape(n, 2)

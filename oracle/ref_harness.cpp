@@ -597,3 +597,25 @@ int ref_run_wave(int n, double dt, double T, int cap, double* samples, int32_t* 
 }
 } // extern "C"
 #endif
+
+extern "C" {
+// mesh.hpp:48-89 derive_exterior_facets (markers none): returns the facet
+// count; facet_vertices [n x gdim] and facet_cell [n x 2] malloc'ed (ref_free).
+int ref_exterior_facets(int gdim, int ncells, int nv, const int32_t* cv, int32_t** fverts, int32_t** fcell) {
+  try {
+    std::vector<double> coords(static_cast<size_t>(nv) * gdim, 0.0);
+    auto mesh = mesh_from_arrays(gdim, ncells, nv, cv, coords.data(), true);
+    std::vector<int32_t> fc;
+    for (auto& pr : mesh->facet_cell) {
+      fc.push_back(pr.first);
+      fc.push_back(pr.second);
+    }
+    *fverts = copy_out(std::vector<int32_t>(mesh->facet_vertex_map->values().begin(),
+                                            mesh->facet_vertex_map->values().end()));
+    *fcell = copy_out(fc);
+    return static_cast<int>(mesh->facet_cell.size());
+  } catch (const Error& e) {
+    return -fail_code(e);
+  }
+}
+} // extern "C"

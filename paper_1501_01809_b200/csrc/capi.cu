@@ -14,6 +14,7 @@
 #include "plan.cuh"
 #include "solver.cuh"
 #include "fem.cuh"
+#include "mesh.cuh"
 
 using namespace loam_gpu;
 
@@ -410,6 +411,30 @@ int loam_gpu_reduce(const double* x, int64_t n, int32_t kind, double* result, vo
     reduce(x, n, kind, r.get(), s);
     LG_CUDA(cudaMemcpyAsync(result, r.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
     LG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+} // extern "C"
+
+// ---- mesh-side builders (mesh.cu) ------------------------------------------
+extern "C" {
+
+int loam_gpu_p2_cell_node_map_dev(int32_t ncells, int32_t nverts, int32_t gdim, const int32_t* cv, int32_t* cn,
+                                  int32_t* nnodes, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(nnodes != nullptr, LOAM_ERR(InvalidArgument), "null node count");
+    *nnodes = p2_cell_node_map_dev(cv, ncells, nverts, gdim, cn, as_stream(stream));
+    LG_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  });
+}
+
+int loam_gpu_exterior_facets(int32_t ncells, int32_t nverts, int32_t gdim, const int32_t* cv,
+                             int32_t** facet_vertices, int32_t** facet_cell, int32_t* nfacets, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(facet_vertices && facet_cell && nfacets, LOAM_ERR(InvalidArgument), "null output");
+    *nfacets = exterior_facets_dev(cv, ncells, nverts, gdim, facet_vertices, facet_cell, as_stream(stream));
   });
 }
 

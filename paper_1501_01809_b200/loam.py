@@ -751,3 +751,38 @@ def reduce(x, kind: int) -> float:
 
 def inf_norm(x) -> float:
     return reduce(x, capi.REDUCE_MAX_ABS)
+
+
+# --------------------------------------------------------------------------
+# Mesh-side builders on the device.
+
+def p2_cell_node_map(cell_vertex: Map, gdim: int):
+    """fem/space.hpp:48-72 on the device: (node Set, cell->node Map) of the P2
+    space over a simplex mesh's cell->vertex map."""
+    nc, nv = cell_vertex.source.size, cell_vertex.target.size
+    nn = 6 if gdim == 2 else 10
+    cn = torch.empty(max(nc * nn, 1), dtype=torch.int32, device="cuda")
+    out = C.c_int32()
+    capi.check(capi.lib().loam_gpu_p2_cell_node_map_dev(nc, nv, gdim, cell_vertex.dev.data_ptr(), cn.data_ptr(),
+                                                        C.byref(out), _stream()))
+    nodes = Set(out.value, "p2_nodes")
+    return nodes, Map(cell_vertex.source, nodes, nn, cn[: nc * nn].cpu().numpy(), "cell_node")
+
+
+def exterior_facets(cell_vertex: Map, gdim: int):
+    """mesh.hpp:48-89 derive_exterior_facets (no markers) on the device:
+    (facet_vertices [n x gdim], facet_cell [n x 2]) as numpy arrays."""
+    nc, nv = cell_vertex.source.size, cell_vertex.target.size
+    fv, fc, n = C.c_void_p(), C.c_void_p(), C.c_int32()
+    capi.check(capi.lib().loam_gpu_exterior_facets(nc, nv, gdim, cell_vertex.dev.data_ptr(), C.byref(fv),
+                                                   C.byref(fc), C.byref(n), _stream()))
+    k = n.value
+    a = np.empty(max(k * gdim, 1), np.int32)
+    b = np.empty(max(k * 2, 1), np.int32)
+    try:
+        capi.check(capi.lib().loam_gpu_memcpy(a.ctypes.data, fv, a.nbytes, None))
+        capi.check(capi.lib().loam_gpu_memcpy(b.ctypes.data, fc, b.nbytes, None))
+    finally:
+        capi.lib().loam_gpu_free(fv)
+        capi.lib().loam_gpu_free(fc)
+    return a[: k * gdim].reshape(k, gdim), b[: k * 2].reshape(k, 2)
