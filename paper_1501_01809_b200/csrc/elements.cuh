@@ -438,6 +438,7 @@ template <int D, int P> struct FormT<F_HELMHOLTZ_ACTION, D, P> : ScalarAction<F_
 //   V [ mu d_de (g_a.g_b) + mu g_a[e] g_b[d] + lambda g_a[d] g_b[e] ].
 template <>
 struct FormT<F_ELASTICITY, 3, 1> {
+  static constexpr int ID = F_ELASTICITY;
   static constexpr int NR = 12, NC = 12, NRN = 4, NCN = 4, RD = 3, CD = 3, GD = 3;
   static constexpr bool HAS_COEFF = false, BILINEAR = true;
   static constexpr int NCOEFF = 0;
@@ -492,6 +493,7 @@ struct FormT<F_ELASTICITY, 3, 1> {
 //   BT = B^T                         velocity rows, pressure cols   12 x 3
 template <>
 struct FormT<F_STOKES_A, 2, 2> {
+  static constexpr int ID = F_STOKES_A;
   static constexpr int NR = 12, NC = 12, NRN = 6, NCN = 6, RD = 2, CD = 2, GD = 2;
   static constexpr bool HAS_COEFF = false, BILINEAR = true;
   static constexpr bool DIAG_BLOCK = true; // (d, c) blocks vanish for d != c
@@ -529,6 +531,7 @@ struct FormT<F_STOKES_A, 2, 2> {
 //   edge (x,y): 4 (l_y g_x[e] + l_x g_y[e]) -> 4 (q(p,y) g_x[e] + q(p,x) g_y[e])
 template <>
 struct FormT<F_STOKES_B, 2, 2> {
+  static constexpr int ID = F_STOKES_B;
   static constexpr int NR = 3, NC = 12, NRN = 3, NCN = 6, RD = 1, CD = 2, GD = 2;
   static constexpr bool HAS_COEFF = false, BILINEAR = true;
   static constexpr int NCOEFF = 0;
@@ -552,6 +555,7 @@ struct FormT<F_STOKES_B, 2, 2> {
 
 template <>
 struct FormT<F_STOKES_BT, 2, 2> {
+  static constexpr int ID = F_STOKES_BT;
   static constexpr int NR = 12, NC = 3, NRN = 6, NCN = 3, RD = 2, CD = 1, GD = 2;
   static constexpr bool HAS_COEFF = false, BILINEAR = true;
   static constexpr int NCOEFF = 0;

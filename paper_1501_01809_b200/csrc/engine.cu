@@ -1494,19 +1494,19 @@ struct PRec { // record layout (plan.cu:build_ptile)
   static constexpr int BYTES = (OFF_CI + 1 + 3) & ~3;
 };
 
-template <class F, int NT>
+template <class F, int NT, int kPS>
 __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PTileArgs a) {
   constexpr int GD = F::GD, NV = GD + 1, W = F::RD * F::CD;
   using RL = PRec<F>;
   constexpr int RB = RL::BYTES;
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
-  uint64_t* empty = full + 3;
+  uint64_t* empty = full + kPS;
   int* slot_tile = reinterpret_cast<int*>(full + 6);
   const int tid = threadIdx.x;
   if (blockIdx.x == 0 && tid == 0) *a.reset_tile = 0;
   if (tid == 0) {
-    for (int b = 0; b < 3; ++b) {
+    for (int b = 0; b < kPS; ++b) {
       mbar_init(&full[b], 1);
       mbar_init(&empty[b], NT / 32);
     }
@@ -1519,7 +1519,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
     m[0] = x.x; m[1] = x.y; m[2] = x.z; m[3] = x.w; m[4] = y.x; m[5] = y.y; m[6] = y.z; m[7] = y.w;
     m[8] = z.x; m[9] = z.y; m[10] = z.z; m[11] = z.w;
   };
-  auto ring = [&](int k) { return sm + a.off_buf + (k % 3) * a.buf_bytes; };
+  auto ring = [&](int k) { return sm + a.off_buf + (k % kPS) * a.buf_bytes; };
   if (tid >= NT) { // ---- producer warp (software-pipelined as in k_ring)
     const int lane = tid & 31;
     auto grab = [&]() {
@@ -1543,17 +1543,17 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
 #pragma unroll
       for (int q = 0; q < 12; ++q) m[q] = nm[q];
       const int2 run0 = nrun, crun0 = ncrun;
-      if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
+      if (k >= kPS) mbar_wait(&empty[k % kPS], (k / kPS - 1) & 1);
       if (tile >= a.ntiles) {
         if (lane == 0) {
-          slot_tile[k % 3] = -1;
-          mbar_arrive(&full[k % 3]);
+          slot_tile[k % kPS] = -1;
+          mbar_arrive(&full[k % kPS]);
         }
         break;
       }
-      if (lane == 0) slot_tile[k % 3] = tile;
+      if (lane == 0) slot_tile[k % kPS] = tile;
       unsigned char* buf = ring(k);
-      uint64_t* bar = &full[k % 3];
+      uint64_t* bar = &full[k % kPS];
       auto rb = [](int64_t lo_b, int64_t hi_b, int64_t& s0) {
         s0 = lo_b & ~int64_t(15);
         return (uint32_t)(((hi_b + 15) & ~int64_t(15)) - s0);
@@ -1586,8 +1586,8 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
   // ---- consumers: one thread per node row
   double* seg = reinterpret_cast<double*>(sm + a.off_seg);
   for (int k = 0;; ++k) {
-    mbar_wait(&full[k % 3], (k / 3) & 1);
-    const int tile = slot_tile[k % 3];
+    mbar_wait(&full[k % kPS], (k / kPS) & 1);
+    const int tile = slot_tile[k % kPS];
     if (tile < 0) break;
     int m[12];
     tile_meta(tile, m);
@@ -1697,7 +1697,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
       }
     }
     __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&empty[k % 3]);
+    if ((tid & 31) == 0) mbar_arrive(&empty[k % kPS]);
     if constexpr (F::BILINEAR) {
       named_bar(1, NT);
       const int len = nA * W;
@@ -1709,19 +1709,34 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
 
 constexpr int kPTileThreads = 128;
 
+// pipeline stages (LOAM_GPU_PT_STAGES, 1..3): fewer stages = less shared
+// memory per CTA = more CTAs per SM; the best count depends on the form
+// (profiles/r01/strategies_ptile_stages.txt)
+inline int ptile_stages(int form) {
+  static const int env = std::getenv("LOAM_GPU_PT_STAGES") ? std::atoi(std::getenv("LOAM_GPU_PT_STAGES")) : 0;
+  if (env >= 1 && env <= 3) return env;
+  return form == F_STOKES_A || form == F_STOKES_B || form == F_STOKES_BT ? 2 : 1;
+}
+
 template <class F>
-void launch_ptile(const PTileArgs& a, size_t smem, cudaStream_t s) {
+void launch_ptile(const PTileArgs& a, size_t smem_base, size_t buf, cudaStream_t s) {
   if (a.ntiles == 0) return;
-  static size_t attr = 0;
-  auto kern = k_ptile<F, kPTileThreads>;
-  if (attr < smem) {
-    LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
-  int blocks = 1;
-  LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kPTileThreads + 32, smem));
-  const int grid = std::min(a.ntiles, std::max(blocks, 1) * kNumSMs);
-  kern<<<grid, kPTileThreads + 32, smem, s>>>(a);
+  auto go = [&](auto kern, int stages) {
+    const size_t smem = smem_base + stages * buf;
+    static size_t attr = 0;
+    if (attr < smem) {
+      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    int blocks = 1;
+    LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kPTileThreads + 32, smem));
+    const int grid = std::min(a.ntiles, std::max(blocks, 1) * kNumSMs);
+    kern<<<grid, kPTileThreads + 32, smem, s>>>(a);
+  };
+  const int st = ptile_stages(F::ID);
+  if (st == 1) go(k_ptile<F, kPTileThreads, 1>, 1);
+  else if (st == 2) go(k_ptile<F, kPTileThreads, 2>, 2);
+  else go(k_ptile<F, kPTileThreads, 3>, 3);
   count_launch();
   LG_LAUNCH_CHECK();
 }
@@ -1734,7 +1749,7 @@ using GenericFn = void (*)(const GLaunch&, cudaStream_t);
 using OwnerFn = void (*)(const OwnerArgs&, int grid, size_t smem, cudaStream_t);
 using NbrFn = void (*)(const TileArgs&, int rec_bytes, size_t smem, cudaStream_t);
 using RingFn = void (*)(const RingArgs&, size_t smem, cudaStream_t);
-using PTileFn = void (*)(const PTileArgs&, size_t smem, cudaStream_t);
+using PTileFn = void (*)(const PTileArgs&, size_t smem_base, size_t buf, cudaStream_t);
 using CellFn = void (*)(const CellArgs&, bool agg, cudaStream_t);
 using PatchFn = void (*)(const PatchArgs&, size_t smem, cudaStream_t);
 using StarFn = void (*)(const StarArgs&, cudaStream_t);
@@ -2566,8 +2581,7 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     t.b_winc = b;
     b += up16(k.has_coeff ? pt.max_cslots * 8 + 16 : 0);
     t.buf_bytes = b;
-    off += 3 * b;
-    k.ptile(t, (size_t)off, s);
+    k.ptile(t, (size_t)off, (size_t)b, s);
     return;
   }
   if (P->use_nbr) {
