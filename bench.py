@@ -481,6 +481,41 @@ def solver_bench(args):
         print(json.dumps(line), flush=True)
 
 
+def wave_bench(args):
+    """Developer line for SURVEY 8f-2: the wave time-step chain (bench.hpp:222-300)
+    on the device -- 3 pointwise loops + 1 stiffness-action par_loop + bc +
+    max-norm per step, the host reading |p| every step as the reference does --
+    next to the compiled reference's run_wave on a bounded sample."""
+    import torch
+    torch.cuda.set_device(0)
+    from paper_1501_01809_b200.wave import WaveLoop
+    import oracle as O
+    n = args.size or 512
+    dt = 0.05 / n
+    w = WaveLoop(n, dt, 1e9)
+    for _ in range(10):
+        w.step()
+    torch.cuda.synchronize()
+    steps = max(args.steps, 50)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        w.step()
+    torch.cuda.synchronize()
+    us = (time.perf_counter() - t0) * 1e6 / steps
+    cells = 2 * n * n
+    line = {"chain": "wave (run_wave)", "mesh": f"{n}^2 P1", "cells": cells, "us_per_step": us,
+            "cell_steps_per_s": cells / (us * 1e-6), "launches_per_step": 6}
+    if O.ref_available():
+        rn, rT = 32, 0.1
+        t0 = time.perf_counter()
+        O.ref_run_wave(rn, 1e-3, rT)
+        rs = (time.perf_counter() - t0) / int(rT / 1e-3)
+        line["reference_cpu"] = {"mesh": f"{rn}^2", "s_per_step": rs, "cell_steps_per_s": 2 * rn * rn / rs,
+                                 "kind": "reference", "cores": 1, "sample": f"bench::run_wave({rn}, 1e-3, {rT})"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -494,9 +529,12 @@ def main():
     ap.add_argument("--strategies", default="auto,owner,atomic,warpagg,color,patch")
     ap.add_argument("--size", type=int, default=None)
     ap.add_argument("--solver", action="store_true", help="developer: SpMV roofline and CG per-iteration lines")
+    ap.add_argument("--wave", action="store_true", help="developer: the wave time-step chain (SURVEY 8f-2)")
     args = ap.parse_args()
     if args.solver:
         return solver_bench(args)
+    if args.wave:
+        return wave_bench(args)
     if args.impl == "reference":
         return reference_arm(args)
     if args.all_configs:
