@@ -511,12 +511,16 @@ __global__ void __launch_bounds__(128) k_owner_mat(const __grid_constant__ Owner
         geometry<F::GD>(B.X[u], G);
         double blk[F::NC];
         form_subrow<F>(i, d, G, nullptr, a.prm, blk);
+        // distinct ranks within a pair: all shared loads, then all stores
+        double cur[F::NC];
 #pragma unroll
-        for (int j = 0; j < F::NCN; ++j) {
-          const int pos = rstart + rk[u][j] * F::CD;
+        for (int j = 0; j < F::NCN; ++j)
 #pragma unroll
-          for (int c = 0; c < F::CD; ++c) seg[pos + c] += blk[j * F::CD + c];
-        }
+          for (int c = 0; c < F::CD; ++c) cur[j * F::CD + c] = seg[rstart + rk[u][j] * F::CD + c];
+#pragma unroll
+        for (int j = 0; j < F::NCN; ++j)
+#pragma unroll
+          for (int c = 0; c < F::CD; ++c) seg[rstart + rk[u][j] * F::CD + c] = cur[j * F::CD + c] + blk[j * F::CD + c];
       }
     }
   }
@@ -1676,15 +1680,26 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
           } else
           for (int st = 0; st < G; ++st) {
             if (has && st == sub) {
+              // the column nodes of one pair have distinct ranks: issue every
+              // shared load of the element row first, then the stores (a
+              // load-add-store chain per entry serialises on shared latency)
+              int pos[F::NCN];
 #pragma unroll
-              for (int j = 0; j < F::NCN; ++j) {
-                const int rk = rec[RL::OFF_RK + j];
+              for (int j = 0; j < F::NCN; ++j) pos[j] = a0 * W + rec[RL::OFF_RK + j] * F::CD;
 #pragma unroll
-                for (int d = 0; d < F::RD; ++d)
+              for (int d = 0; d < F::RD; ++d) {
+                double cur[F::NCN * F::CD];
+#pragma unroll
+                for (int j = 0; j < F::NCN; ++j)
+#pragma unroll
+                  for (int c = 0; c < F::CD; ++c)
+                    if (!diag_block<F>::value || d == c) cur[j * F::CD + c] = seg[pos[j] + d * L * F::CD + c];
+#pragma unroll
+                for (int j = 0; j < F::NCN; ++j)
 #pragma unroll
                   for (int c = 0; c < F::CD; ++c)
                     if (!diag_block<F>::value || d == c)
-                      seg[a0 * W + d * L * F::CD + rk * F::CD + c] += blk[d * F::NC + j * F::CD + c];
+                      seg[pos[j] + d * L * F::CD + c] = cur[j * F::CD + c] + blk[d * F::NC + j * F::CD + c];
               }
             }
             if (G > 1) __syncwarp();
