@@ -25,8 +25,10 @@
 #include <unordered_map>
 
 #include "async.cuh"
+#include "stage.cuh"
 #include "elements.cuh"
 #include "engine.cuh"
+#include "etile.cuh"
 #include "patch.cuh"
 #include "patch_kernels.cuh"
 #include "plan.cuh"
@@ -563,59 +565,6 @@ struct TileArgs {
   int off_seg, off_buf, buf_bytes;
   int b_nptr, b_pptr, b_recs, b_widx, b_selfr, b_win, b_winc; // inside one ring stage
 };
-
-__device__ __forceinline__ int skew_of(int lo, int es) { return ((lo * es) & 15) / es; }
-
-// Warp-cooperative staging of a tile's id runs [lo, hi) of an es-doubles-per-id
-// array into consecutive window slots: lane r handles run r (32 at a time),
-// slots from a warp scan.  A run whose byte count is not a multiple of 16 gets
-// its last double stored by the lane itself (bulk copies move 16-byte units;
-// runs start at even ids so the source side is aligned).  prepare() does the
-// tail stores and returns the warp-total bulk bytes; issue() launches copies.
-struct RunSet {
-  const int2* runs;
-  int cnt;
-  const double* src;
-  double* dst;
-  int es;
-};
-// `first`: the lane's run of the first chunk, prefetched by the caller.
-__device__ __forceinline__ int2 first_run(const int2* runs, int cnt, int lane) {
-  return lane < cnt ? __ldg(runs + lane) : make_int2(0, 0);
-}
-template <bool ISSUE>
-__device__ __forceinline__ uint32_t stage_runs(const RunSet& s, int lane, uint64_t* bar, int2 first) {
-  uint32_t tx = 0;
-  int base = 0;
-  for (int r0 = 0; r0 < s.cnt; r0 += 32) {
-    int lo = first.x, hi = first.y;
-    if (r0 > 0) {
-      const int2 p = r0 + lane < s.cnt ? __ldg(s.runs + r0 + lane) : make_int2(0, 0);
-      lo = p.x;
-      hi = p.y;
-    }
-    const int n = hi - lo;
-    int incl = n;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int slot = base + incl - n;
-    const uint32_t nb = (uint32_t)n * s.es * 8;
-    if (ISSUE) {
-      if (nb >= 16) bulk_g2s(s.dst + (int64_t)slot * s.es, s.src + (int64_t)lo * s.es, nb & ~15u, bar);
-    } else {
-      if (nb & 15) s.dst[(int64_t)(slot + n) * s.es - 1] = s.src[(int64_t)hi * s.es - 1];
-      tx += nb & ~15u;
-    }
-    base += __shfl_sync(0xffffffffu, incl, 31);
-  }
-  if (!ISSUE)
-#pragma unroll
-    for (int o = 16; o; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
-  return tx;
-}
 
 constexpr int kTileThreads = 256;                 // consumer threads (8 warps)
 constexpr int kTileBlock = kTileThreads + 32;     // + one TMA producer warp
@@ -2071,6 +2020,8 @@ struct FastPlan {
   NbrPlan nb;
   bool use_ptile = false;
   PTilePlan pt;
+  bool use_etile = false;  // edge tiles (scalar P2 matrices, etile.cuh)
+  EtilePlan et;
   bool use_star = false;   // vertex-star kernel (P1 triangle actions)
   DevBuf<int4> star;
   bool use_patch = false;  // cell-patch row-owner kernels (patch.cuh)
@@ -2305,6 +2256,25 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     CsrView csr{sp->row_ptr, sp->col_idx, sp->nrows, sp->ncols, sp->nnz, R.dim, Cn.dim};
     build_ranks(P->pp, srows.v.get(), sc, Cn.v.arity, csr, s);
     build_chunks(P->pp, csr, kSegMax, 32 / R.dim, s);
+    // edge tiles: scalar P2 mass / stiffness / helmholtz on one (map, map) pattern
+    const bool et_form = (k.form == F_MASS || k.form == F_STIFFNESS || k.form == F_HELMHOLTZ) &&
+                         k.nrn == (k.gd == 2 ? 6 : 10) && k.ncn == k.nrn && k.rd == 1 && k.cd == 1;
+    if (strat == 0 && et_form && !std::getenv("LOAM_GPU_NO_ETILE") && R.dim == 1 && Cn.dim == 1 &&
+        (reinterpret_cast<uintptr_t>(args[1].data) & 15) == 0 && Cn.v.arity == R.v.arity &&
+        (Cn.v.v == R.v.v || prefix_equal(Cn.v.v, Cn.v.arity, R.v.v, R.v.arity, R.v.arity, n, s)) &&
+        pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, 1, 1, sp->row_ptr, sp->col_idx, sp->nnz, s)) {
+      SortedMap sx;
+      gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, sx, s);
+      EtileSpec es;
+      es.tile_rows = env_int("LOAM_GPU_ET_ROWS", es.tile_rows);
+      es.tile_seg = env_int("LOAM_GPU_ET_SEG", es.tile_seg);
+      es.tile_cells = env_int("LOAM_GPU_ET_CELLS", es.tile_cells);
+      if (build_etile(P->et, es, k.gd, n, R.v.target, srows.v.get(), sx.v.get(), X->target_size, P->pp,
+                      sp->row_ptr, sp->nnz, s)) {
+        P->use_etile = true;
+        return P;
+      }
+    }
   }
   // canonical pair tiles: default for the scalar / 2-vector bilinear forms the
   // ring / neighbour paths do not take (P2 matrices, Taylor-Hood blocks).  P2
@@ -2558,6 +2528,12 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
       fprintf(stderr, "[ring timing] CTA starts span %.2f us, CTA ends from %.2f to %.2f us after the first start\n",
               (double)(h[11] - h[8]) * 1e-3, (double)(h[12] - h[8]) * 1e-3, (double)(h[9] - h[8]) * 1e-3);
     }
+    return;
+  }
+  if (P->use_etile) {
+    launch_etile(k.form, P->et, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
+                 P->counter.get() + P->parity, P->counter.get() + (P->parity ^ 1), s);
+    P->parity ^= 1;
     return;
   }
   if (P->use_ptile) {

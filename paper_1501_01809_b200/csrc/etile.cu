@@ -1,0 +1,730 @@
+// etile.cu -- edge-tile assembly of scalar P2 matrices (see etile.cuh).
+//
+// Reference path replaced: assemble_matrix (fem/assemble.hpp:85-104) ->
+// execute (parloop.hpp:191-384) with the P2 mass / stiffness / helmholtz
+// element kernels (fem/form.hpp:201-320) and Mat::addto (data.hpp:205-222).
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "async.cuh"
+#include "etile.cuh"
+#include "stage.cuh"
+
+namespace loam_gpu {
+
+int et_stages();
+
+namespace {
+
+const int kTriE[3][2] = {{1, 2}, {0, 2}, {0, 1}};                          // space.hpp:66-71
+const int kTetE[6][2] = {{2, 3}, {1, 3}, {1, 2}, {0, 3}, {0, 2}, {0, 1}};  // elements.cuh Simplex<3>
+
+int edge_index(int gd, int x, int y) {
+  const int ne = gd == 2 ? 3 : 6;
+  const int (*E)[2] = gd == 2 ? kTriE : kTetE;
+  if (x > y) std::swap(x, y);
+  for (int f = 0; f < ne; ++f)
+    if (E[f][0] == x && E[f][1] == y) return f;
+  return -1;
+}
+
+// packed upper-triangle index of the Gram entry (p, q) of nv vertices
+int gram_index(int nv, int p, int q) {
+  if (p > q) std::swap(p, q);
+  int idx = 0;
+  for (int r = 0; r < p; ++r) idx += nv - r;
+  return idx + (q - p);
+}
+
+// windows of contiguous vertex ids (even-aligned runs, as the ptile plan)
+int make_runs(std::vector<int>& ids, int limit, std::vector<std::pair<int, int>>& rr) {
+  constexpr int kGap = 8;
+  std::sort(ids.begin(), ids.end());
+  ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+  rr.clear();
+  int slots = 0;
+  for (int v : ids) {
+    const int lo = v & ~1, hi = std::min(limit, (v + 2) & ~1);
+    if (!rr.empty() && lo <= rr.back().second + kGap) rr.back().second = std::max(rr.back().second, hi);
+    else rr.emplace_back(lo, hi);
+  }
+  for (auto& x : rr) slots += x.second - x.first;
+  return slots;
+}
+
+inline int up16(int x) { return (x + 15) & ~15; }
+
+} // namespace
+
+bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nrows_node,
+                 const int32_t* sorted_rows, const int32_t* sorted_x, int nverts, const PairPlan& pp,
+                 const int64_t* row_ptr, int64_t nnz, cudaStream_t s) {
+  const int nv = gd + 1, ne = gd == 2 ? 3 : 6, nrn = nv + ne;
+  const int (*E)[2] = gd == 2 ? kTriE : kTetE;
+  if (pp.nrn != nrn || pp.ncn != nrn || nnz >= (int64_t(1) << 31) || ncells == 0 || ncells >= (1 << 30))
+    return false;
+  const int64_t np = pp.npairs;
+  std::vector<int32_t> hrows((size_t)ncells * nrn), hx((size_t)ncells * nv), hpairs(np), hp(nrows_node + 1);
+  std::vector<uint8_t> hrank((size_t)np * nrn);
+  std::vector<int64_t> hrp(nrows_node + 1);
+  LG_CUDA(cudaMemcpyAsync(hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size(), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hx.data(), sorted_x, sizeof(int32_t) * hx.size(), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hpairs.data(), pp.pairs.get(), sizeof(int32_t) * np, cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hp.data(), pp.ptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hrank.data(), pp.ranks.get(), hrank.size(), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hrp.data(), row_ptr, sizeof(int64_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+
+  // ---- node roles: vertex nodes (local 0..gd) numbered before edge nodes
+  std::vector<int8_t> role(nrows_node, 0);
+  for (int c = 0; c < ncells; ++c)
+    for (int i = 0; i < nrn; ++i) {
+      const int node = hrows[(size_t)c * nrn + i];
+      const int8_t r = i < nv ? 1 : 2;
+      if (role[node] && role[node] != r) return false;
+      role[node] = r;
+    }
+  int maxv = -1, mine = INT_MAX;
+  for (int n = 0; n < nrows_node; ++n) {
+    if (role[n] == 1) maxv = n;
+    if (role[n] == 2) mine = std::min(mine, n);
+  }
+  if (mine == INT_MAX || maxv >= mine) return false;
+  const int E0 = mine, nedge = nrows_node - E0;
+  for (int n = E0; n < nrows_node; ++n)
+    if (role[n] != 2) return false;
+  // ---- edge node <-> vertex pair bijection
+  std::vector<int32_t> eA(nedge), eB(nedge);
+  std::vector<uint64_t> keys(nedge);
+  for (int e = 0; e < nedge; ++e) {
+    const int r = E0 + e;
+    for (int p = hp[r]; p < hp[r + 1]; ++p) {
+      const int c = hpairs[p] / nrn, k = hpairs[p] % nrn - nv;
+      int a = hrows[(size_t)c * nrn + E[k][0]], b = hrows[(size_t)c * nrn + E[k][1]];
+      if (a > b) std::swap(a, b);
+      if (p == hp[r]) {
+        eA[e] = a;
+        eB[e] = b;
+      } else if (a != eA[e] || b != eB[e]) {
+        return false;
+      }
+    }
+    keys[e] = (uint64_t)(uint32_t)eA[e] << 32 | (uint32_t)eB[e];
+  }
+  {
+    std::vector<uint64_t> ks(keys);
+    std::sort(ks.begin(), ks.end());
+    if (std::adjacent_find(ks.begin(), ks.end()) != ks.end()) return false;
+  }
+  auto find_pair = [&](int w, int c) -> int64_t {
+    for (int p = hp[w]; p < hp[w + 1]; ++p)
+      if (hpairs[p] / nrn == c) return p;
+    return -1;
+  };
+  // ---- vertex diagonals
+  std::vector<int32_t> dpos(E0, -1), diag;
+  for (int v = 0; v < E0; ++v)
+    if (hp[v + 1] > hp[v]) {
+      const int p = hp[v], i = hpairs[p] % nrn;
+      dpos[v] = (int32_t)(hrp[v] + hrank[(size_t)p * nrn + i]);
+      diag.push_back(dpos[v]);
+    }
+  // diagonal contribution of (cell, local vertex v) is carried by local edge (0,1) for
+  // v = 0 and (0,v) otherwise
+  auto assigned = [&](int v) { return edge_index(gd, 0, v == 0 ? 1 : v); };
+  // ---- index table: per (local edge k, orientation) the Gram entries the canonical row reads
+  const int ca = nv - 2, cb = nv - 1;
+  uint32_t ktab[12] = {};
+  auto sigma_of = [&](int k, int swap, int* sig) {
+    const int la = E[k][swap], lb = E[k][1 - swap];
+    sig[ca] = la;
+    sig[cb] = lb;
+    int q = 0;
+    for (int v = 0; v < nv; ++v)
+      if (v != la && v != lb) sig[q++] = v;
+  };
+  for (int k = 0; k < ne; ++k)
+    for (int sw = 0; sw < 2; ++sw) {
+      int sig[4];
+      sigma_of(k, sw, sig);
+      uint32_t w = 0;
+      int q = 0;
+      for (int m = 0; m < nv; ++m) w |= (uint32_t)gram_index(nv, sig[ca], sig[m]) << (4 * q++);
+      for (int m = 0; m < nv; ++m)
+        if (m != ca) w |= (uint32_t)gram_index(nv, sig[cb], sig[m]) << (4 * q++);
+      ktab[k * 2 + sw] = w;
+    }
+  // ---- per edge row: transposed positions, vertex-pair positions, records
+  const int rb = (2 + nrn + 3) & ~3;
+  const int64_t p0e = hp[E0], npe = hp[nrows_node] - p0e;
+  std::vector<int32_t> tptr(nedge + 1, 0), tpos, cellof(npe);
+  std::vector<int4> xpos(nedge);
+  std::vector<uint8_t> recs((size_t)npe * rb, 0);
+  std::vector<std::pair<int, int>> vc; // (vertex node, cell carrying it)
+  for (int e = 0; e < nedge; ++e) {
+    const int r = E0 + e, A = eA[e], B = eB[e];
+    vc.clear();
+    for (int p = hp[r]; p < hp[r + 1]; ++p) {
+      const int c = hpairs[p] / nrn;
+      for (int v = 0; v < nv; ++v) vc.emplace_back(hrows[(size_t)c * nrn + v], c);
+    }
+    std::sort(vc.begin(), vc.end());
+    int last = -1;
+    for (auto& x : vc) {
+      if (x.first == last) continue;
+      last = x.first;
+      const int c = x.second;
+      const int k = [&] {
+        for (int p = hp[r]; p < hp[r + 1]; ++p)
+          if (hpairs[p] / nrn == c) return hpairs[p] % nrn;
+        return -1;
+      }();
+      const int64_t pw = find_pair(x.first, c);
+      if (pw < 0 || k < 0) return false;
+      tpos.push_back((int32_t)(hrp[x.first] + hrank[(size_t)pw * nrn + k]));
+    }
+    tptr[e + 1] = (int32_t)tpos.size();
+    {
+      const int p = hp[r], c = hpairs[p] / nrn, k = hpairs[p] % nrn - nv;
+      const int la = E[k][0], lb = E[k][1];
+      const int lA = hrows[(size_t)c * nrn + la] == A ? la : lb, lB = lA == la ? lb : la;
+      const int64_t pA = find_pair(A, c), pB = find_pair(B, c);
+      if (pA < 0 || pB < 0) return false;
+      xpos[e] = make_int4((int32_t)(hrp[A] + hrank[(size_t)pA * nrn + lB]),
+                          (int32_t)(hrp[B] + hrank[(size_t)pB * nrn + lA]), dpos[A], dpos[B]);
+    }
+    for (int p = hp[r]; p < hp[r + 1]; ++p) {
+      const int c = hpairs[p] / nrn, k = hpairs[p] % nrn - nv;
+      const int swap = hrows[(size_t)c * nrn + E[k][0]] != A ? 1 : 0;
+      int sig[4];
+      sigma_of(k, swap, sig);
+      const int fA = assigned(sig[ca]) == k, fB = assigned(sig[cb]) == k;
+      uint8_t* rec = &recs[(size_t)(p - p0e) * rb];
+      const uint16_t h = (uint16_t)(((k * 2 + swap) << 10) | (fA << 14) | (fB << 15));
+      memcpy(rec, &h, 2);
+      const uint8_t* rk = &hrank[(size_t)p * nrn];
+      for (int m = 0; m < nv; ++m) rec[2 + m] = rk[sig[m]];
+      for (int f = 0; f < ne; ++f) rec[2 + nv + f] = rk[nv + edge_index(gd, sig[E[f][0]], sig[E[f][1]])];
+      cellof[p - p0e] = c;
+    }
+  }
+  // ---- edge tiles: consecutive edge rows, their distinct cells and coordinate window
+  std::vector<int32_t> tiles, runs;
+  std::vector<uint8_t> blob;
+  std::vector<int> stamp(ncells, -1), local(ncells, 0), vid;
+  std::vector<std::pair<int, int>> rr;
+  int gen = 0, r0 = 0;
+  const int trows = sp.tile_rows <= 64 ? 64 : 128;
+  const int cell_cap = std::min(sp.tile_cells, 1023);
+  while (r0 < nedge) {
+    int r1 = std::min(nedge, r0 + trows);
+    std::vector<int> cells;
+    int slots = 0;
+    auto fits = [&](int a, int b) {
+      if (hrp[E0 + b] - hrp[E0 + a] > sp.tile_seg) return false;
+      if (hp[E0 + b] - hp[E0 + a] > sp.tile_pairs) return false;
+      ++gen;
+      cells.clear();
+      for (int p = hp[E0 + a]; p < hp[E0 + b]; ++p) {
+        const int c = cellof[p - p0e];
+        if (stamp[c] != gen) {
+          stamp[c] = gen;
+          cells.push_back(c);
+        }
+      }
+      if ((int)cells.size() > cell_cap) return false;
+      vid.clear();
+      for (int c : cells)
+        for (int v = 0; v < nv; ++v) vid.push_back(hx[(size_t)c * nv + v]);
+      slots = make_runs(vid, nverts, rr);
+      return slots <= sp.tile_slots && (int)rr.size() <= sp.tile_runs;
+    };
+    while (!fits(r0, r1)) {
+      if (r1 == r0 + 1) return false;
+      r1 = r0 + (r1 - r0) / 2;
+    }
+    std::sort(cells.begin(), cells.end());
+    for (size_t q = 0; q < cells.size(); ++q) local[cells[q]] = (int)q;
+    std::vector<int> base(rr.size());
+    for (size_t q = 0, acc = 0; q < rr.size(); ++q) {
+      base[q] = (int)acc;
+      acc += rr[q].second - rr[q].first;
+    }
+    auto slot_in = [&](int v) {
+      size_t q = std::upper_bound(rr.begin(), rr.end(), std::make_pair(v, INT32_MAX)) - rr.begin() - 1;
+      return base[q] + v - rr[q].first;
+    };
+    const int nrows = r1 - r0, P0 = hp[E0 + r0], npairs = hp[E0 + r1] - P0, ncell = (int)cells.size();
+    const int T0 = tptr[r0], ntp = tptr[r1] - T0;
+    const int off_prow = 0, off_srow = up16((nrows + 1) * 2), off_tptr = off_srow + up16((nrows + 1) * 2),
+              off_xpos = off_tptr + up16((nrows + 1) * 2), off_tpos = off_xpos + nrows * 16,
+              off_recs = off_tpos + up16(ntp * 4), off_cells = off_recs + up16(npairs * rb),
+              bytes = off_cells + up16(ncell * nv * 2);
+    const size_t b0 = blob.size();
+    blob.resize(b0 + bytes, 0);
+    uint8_t* bp = blob.data() + b0;
+    for (int r = 0; r <= nrows; ++r) {
+      const uint16_t pr = (uint16_t)(hp[E0 + r0 + r] - P0);
+      const uint16_t sr = (uint16_t)(hrp[E0 + r0 + r] - hrp[E0 + r0]);
+      const uint16_t tr = (uint16_t)(tptr[r0 + r] - T0);
+      memcpy(bp + off_prow + 2 * r, &pr, 2);
+      memcpy(bp + off_srow + 2 * r, &sr, 2);
+      memcpy(bp + off_tptr + 2 * r, &tr, 2);
+    }
+    memcpy(bp + off_xpos, &xpos[r0], (size_t)nrows * 16);
+    if (ntp) memcpy(bp + off_tpos, &tpos[T0], (size_t)ntp * 4);
+    for (int q = 0; q < npairs; ++q) {
+      const int64_t pe = P0 + q - p0e;
+      uint8_t* rec = bp + off_recs + (size_t)q * rb;
+      memcpy(rec, &recs[(size_t)pe * rb], rb);
+      uint16_t h;
+      memcpy(&h, rec, 2);
+      h = (uint16_t)(h | local[cellof[pe]]);
+      memcpy(rec, &h, 2);
+    }
+    for (int q = 0; q < ncell; ++q)
+      for (int v = 0; v < nv; ++v) {
+        const uint16_t sl = (uint16_t)slot_in(hx[(size_t)cells[q] * nv + v]);
+        memcpy(bp + off_cells + 2 * (q * nv + v), &sl, 2);
+      }
+    const int seg = (int)(hrp[E0 + r1] - hrp[E0 + r0]);
+    tiles.insert(tiles.end(), {(int)(b0 / 16), bytes, r0, nrows, (int)hrp[E0 + r0], seg, npairs, ncell,
+                               (int)runs.size() / 2, (int)rr.size(), off_prow, off_srow, off_recs, off_cells, off_tptr, off_xpos});
+    for (auto& x : rr) runs.insert(runs.end(), {x.first, x.second});
+    out.max_rows = std::max(out.max_rows, nrows);
+    out.max_pairs = std::max(out.max_pairs, npairs);
+    out.max_seg = std::max(out.max_seg, seg);
+    out.max_cells = std::max(out.max_cells, ncell);
+    out.max_slots = std::max(out.max_slots, slots);
+    out.max_blob = std::max(out.max_blob, bytes);
+    r0 = r1;
+  }
+  out.gd = gd;
+  out.tile_threads = trows;
+  out.ntiles = (int)tiles.size() / 16;
+  out.e0 = E0;
+  out.nedge = nedge;
+  out.rec_bytes = rb;
+  out.ndiag = (int64_t)diag.size();
+  memcpy(out.ktab, ktab, sizeof(ktab));
+  auto upload = [&](auto& dst, const auto& src) {
+    using T = typename std::decay_t<decltype(src)>::value_type;
+    dst.alloc(src.size() + 16, s);
+    if (!src.empty())
+      LG_CUDA(cudaMemcpyAsync(dst.get(), src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, s));
+  };
+  upload(out.tiles, tiles);
+  upload(out.blob, blob);
+  upload(out.runs, runs);
+  upload(out.diag, diag);
+  LG_CUDA(cudaStreamSynchronize(s));
+  return true;
+}
+
+// ===========================================================================
+// Device side
+// ===========================================================================
+
+namespace {
+
+struct EtileArgs {
+  const int32_t* tiles;
+  int ntiles;
+  int* next_tile;
+  int* reset_tile;
+  const uint8_t* blob;
+  const int32_t* runs;
+  const double* coords;
+  double* out;
+  FormParams prm;
+  int accumulate, dynamic, dbg;
+  int off_seg, off_geo, off_buf, buf_bytes, b_win;
+  uint32_t ktab[12];
+};
+
+template <int D>
+struct EtT {
+  static constexpr int NV = D + 1, NE = D == 2 ? 3 : 6, N = NV + NE;
+  static constexpr int NG = NV * (NV + 1) / 2 + 1; // Gram entries + V
+  static constexpr int NT = 2 * NV - 1;            // Gram entries a canonical edge row reads
+  static constexpr int RB = (2 + N + 3) & ~3;
+  static constexpr int CA = NV - 2, CB = NV - 1;   // canonical row edge = local edge 0
+};
+
+// Canonical P2 edge row (row node = local edge 0 = (CA, CB)) from the Gram
+// entries G_xy = V g_x.g_y: same integrals as p2_rows (elements.cuh), with the
+// cell measure folded into G.  Also returns the (CA, CB) vertex-vertex entry
+// and the two vertex diagonals of this cell.
+template <int FORM, int D>
+__device__ __forceinline__ void et_row(const double (&t)[EtT<D>::NT], double V, const FormParams& prm,
+                                       double (&o)[EtT<D>::N], double& vab, double& dga, double& dgb) {
+  using T = EtT<D>;
+  using S = Simplex<D>;
+  constexpr int NV = T::NV, NE = T::NE, a = T::CA, b = T::CB;
+  constexpr double qs = S::q_same, qd = S::q_diff, l1 = S::l1;
+  constexpr double cs = 16.0 * qs - 8.0 * l1 + 1.0, co = 16.0 * qd - 8.0 * l1 + 1.0;
+  constexpr double es = 4.0 * qs - l1, ed = 4.0 * qd - l1;
+  double Ga[NV], Gb[NV];
+#pragma unroll
+  for (int m = 0; m < NV; ++m) {
+    Ga[m] = t[m];
+    Gb[m] = m == a ? t[b] : (m < a ? t[NV + m] : t[2 * NV - 2]);
+  }
+  const double kV = prm.p[0] * V;
+  auto comb = [&](double K, double M) {
+    if constexpr (FORM == F_MASS) return V * M;
+    else if constexpr (FORM == F_STIFFNESS) return K;
+    else return fma(kV, M, K);
+  };
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const double K = 4.0 * ((j == b ? es : ed) * Ga[j] + (j == a ? es : ed) * Gb[j]);
+    o[j] = comb(K, (j == a || j == b) ? p2_mass_const<D>(2) : p2_mass_const<D>(3));
+  }
+#pragma unroll
+  for (int f = 0; f < NE; ++f) {
+    const int c = S::edge_a(f), d = S::edge_b(f);
+    const double K = 16.0 * ((b == d ? qs : qd) * Ga[c] + (b == c ? qs : qd) * Ga[d] + (a == d ? qs : qd) * Gb[c] +
+                             (a == c ? qs : qd) * Gb[d]);
+    const int shared = (a == c) + (a == d) + (b == c) + (b == d);
+    const double M = f == 0 ? p2_mass_const<D>(4) : (shared == 1 ? p2_mass_const<D>(5) : p2_mass_const<D>(6));
+    o[NV + f] = comb(K, M);
+  }
+  vab += comb(co * Ga[b], p2_mass_const<D>(1));
+  dga = comb(cs * Ga[a], p2_mass_const<D>(0));
+  dgb = comb(cs * Gb[b], p2_mass_const<D>(0));
+}
+
+// mbarrier wait that lets the warp sleep (up to the hint, ns) instead of
+// spinning on try_wait: waiting consumers leave their issue slots to the
+// other CTAs of the SM
+__device__ __forceinline__ void et_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(20000)
+      : "memory");
+}
+
+// NT consumer threads (= edge rows per tile) + one TMA producer warp.
+template <int FORM, int D, int NT, int STAGES>
+__global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ EtileArgs a) {
+  using T = EtT<D>;
+  constexpr int NV = T::NV, N = T::N, NG = T::NG, RB = T::RB;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + STAGES;
+  int* slot_tile = reinterpret_cast<int*>(sm + 48);
+  uint32_t* ktab = reinterpret_cast<uint32_t*>(sm + 64);
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0 && tid == 0) *a.reset_tile = 0;
+  if (tid < 12) ktab[tid] = a.ktab[tid];
+  if (tid == 0) {
+    for (int q = 0; q < STAGES; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], NT / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto ring = [&](int k) { return sm + a.off_buf + (k % STAGES) * a.buf_bytes; };
+  auto meta = [&](int tile, int (&m)[16]) {
+    const int4* t = reinterpret_cast<const int4*>(a.tiles + 16 * tile);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 x = __ldg(t + q);
+      m[4 * q] = x.x;
+      m[4 * q + 1] = x.y;
+      m[4 * q + 2] = x.z;
+      m[4 * q + 3] = x.w;
+    }
+  };
+  if (tid >= NT) { // ---- producer warp: tile blob + coordinate window by TMA
+    const int lane = tid & 31;
+    // static round-robin schedule (tiles are near-uniform); the dynamic
+    // counter (a.dynamic) costs a dependent global atomic per tile
+    int sched = 0;
+    auto grab = [&]() {
+      if (!a.dynamic) return (int)blockIdx.x + (sched++) * (int)gridDim.x;
+      int t = 0;
+      if (lane == 0) t = atomicAdd(a.next_tile, 1);
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    int nt = grab();
+    int nm[16];
+    int2 nrun = make_int2(0, 0);
+    auto prefetch = [&]() {
+      if (nt < a.ntiles) {
+        meta(nt, nm);
+        nrun = first_run(reinterpret_cast<const int2*>(a.runs) + nm[8], nm[9], lane);
+      }
+    };
+    prefetch();
+    for (int k = 0;; ++k) {
+      const int tile = nt;
+      int m[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) m[q] = nm[q];
+      const int2 run0 = nrun;
+      if (k >= STAGES) mbar_wait(&empty[k % STAGES], (k / STAGES - 1) & 1);
+      if (tile >= a.ntiles) {
+        if (lane == 0) {
+          slot_tile[k % STAGES] = -1;
+          mbar_arrive(&full[k % STAGES]);
+        }
+        break;
+      }
+      if (lane == 0) slot_tile[k % STAGES] = tile;
+      unsigned char* buf = ring(k);
+      uint64_t* bar = &full[k % STAGES];
+      const RunSet rc{reinterpret_cast<const int2*>(a.runs) + m[8], m[9], a.coords,
+                      reinterpret_cast<double*>(buf + a.b_win), D};
+      const uint32_t tx = (uint32_t)m[1] + stage_runs<false>(rc, lane, bar, run0);
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(bar, tx);
+        bulk_g2s(buf, a.blob + (int64_t)m[0] * 16, (uint32_t)m[1], bar);
+      }
+      __syncwarp();
+      stage_runs<true>(rc, lane, bar, run0);
+      nt = grab();
+      prefetch();
+    }
+    return;
+  }
+  // ---- consumers
+  double* seg0 = reinterpret_cast<double*>(sm + a.off_seg);
+  double* geo = reinterpret_cast<double*>(sm + a.off_geo);
+  for (int k = 0;; ++k) {
+    et_wait(&full[k % STAGES], (k / STAGES) & 1);
+    const int tile = slot_tile[k % STAGES];
+    if (tile < 0) break;
+    int m[16];
+    meta(tile, m);
+    const int nrows = m[3], E0 = m[4], len = m[5], ncell = m[7];
+    const unsigned char* buf = ring(k);
+    const uint16_t* prow = reinterpret_cast<const uint16_t*>(buf + m[10]);
+    const uint16_t* srow = reinterpret_cast<const uint16_t*>(buf + m[11]);
+    const unsigned char* recs = buf + m[12];
+    const uint16_t* cslot = reinterpret_cast<const uint16_t*>(buf + m[13]);
+    const uint16_t* trow = reinterpret_cast<const uint16_t*>(buf + m[14]);
+    const int4* xpos = reinterpret_cast<const int4*>(buf + m[15]);
+    const int32_t* tpos = reinterpret_cast<const int32_t*>(buf + m[15] + 16 * nrows);
+    const double* win = reinterpret_cast<const double*>(buf + a.b_win);
+    // the segment shares the 16-byte parity of its global destination (bulk store)
+    double* seg = seg0 + (E0 & 1);
+    // phase 1: the Gram matrix of every cell of the tile, once
+    for (int c = tid; c < ((a.dbg & 2) ? 0 : ncell); c += NT) {
+      double X[NV][D];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int sl = cslot[c * NV + v];
+#pragma unroll
+        for (int q = 0; q < D; ++q) X[v][q] = win[sl * D + q];
+      }
+      Geom<D> Gm;
+      geometry<D>(X, Gm);
+      double* g = geo + c * NG;
+      if constexpr (FORM != F_MASS) {
+        int idx = 0;
+#pragma unroll
+        for (int p = 0; p < NV; ++p) {
+          double vg[D];
+#pragma unroll
+          for (int q = 0; q < D; ++q) vg[q] = Gm.V * Gm.g[p][q];
+#pragma unroll
+          for (int q = p; q < NV; ++q) g[idx++] = dot<D>(vg, Gm.g[q]);
+        }
+      }
+      g[NG - 1] = Gm.V;
+    }
+    // the previous tile's bulk store must have read the segment
+    if (tid == 0) bulk_wait_read<0>();
+    named_bar(1, NT);
+    {
+      double2* z = reinterpret_cast<double2*>(seg0);
+      const int n2 = (len + 2) >> 1;
+      for (int t = tid; t < n2; t += NT) z[t] = make_double2(0.0, 0.0); // this loop's contributions only
+    }
+    named_bar(1, NT);
+    // phase 2: one thread per edge row
+    if (tid < nrows) {
+      const int p0 = prow[tid], p1 = prow[tid + 1], s0 = srow[tid];
+      double vab = 0.0, dA = 0.0, dB = 0.0;
+      bool hA = false, hB = false;
+      // software pipeline: the next pair's record and Gram entries are loaded
+      // before this pair's arithmetic and segment updates
+      uint32_t w[RB / 4];
+      double t[T::NT], V = 0.0;
+      auto fetch = [&](int p, uint32_t (&wq)[RB / 4], double (&tq)[T::NT], double& Vq) {
+#pragma unroll
+        for (int q = 0; q < RB / 4; ++q) wq[q] = reinterpret_cast<const uint32_t*>(recs + p * RB)[q];
+        const uint32_t h = wq[0] & 0xffffu;
+        const double* g = geo + (h & 1023u) * NG;
+        const uint32_t gi = ktab[(h >> 10) & 15u];
+#pragma unroll
+        for (int q = 0; q < T::NT; ++q) tq[q] = g[(gi >> (4 * q)) & 15u];
+        Vq = g[NG - 1];
+      };
+      const int pe = (a.dbg & 1) ? p0 : p1;
+      if (p0 < pe) fetch(p0, w, t, V);
+      for (int p = p0; p < pe; ++p) {
+        uint32_t wn[RB / 4];
+        double tn[T::NT], Vn = 0.0;
+        if (p + 1 < pe) fetch(p + 1, wn, tn, Vn);
+        const uint32_t h = w[0] & 0xffffu;
+        double o[N], dga, dgb;
+        et_row<FORM, D>(t, V, a.prm, o, vab, dga, dgb);
+        int pos[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) pos[j] = s0 + (int)((w[(2 + j) >> 2] >> (8 * ((2 + j) & 3))) & 0xffu);
+        double cur[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) cur[j] = seg[pos[j]];
+#pragma unroll
+        for (int j = 0; j < N; ++j) seg[pos[j]] = cur[j] + o[j];
+        if (h & 0x4000u) {
+          dA += dga;
+          hA = true;
+        }
+        if (h & 0x8000u) {
+          dB += dgb;
+          hB = true;
+        }
+#pragma unroll
+        for (int q = 0; q < RB / 4; ++q) w[q] = wn[q];
+#pragma unroll
+        for (int q = 0; q < T::NT; ++q) t[q] = tn[q];
+        V = Vn;
+      }
+      // vertex rows: transposed vertex-column entries, the vertex pair, diagonals
+      const int t0 = trow[tid], t1 = (a.dbg & 4) ? t0 : trow[tid + 1];
+      for (int t = t0; t < t1; ++t) {
+        double* dst = a.out + tpos[t];
+        const double v = seg[s0 + t - t0];
+        *dst = a.accumulate ? *dst + v : v;
+      }
+      const int4 xp = xpos[tid];
+      double* dab = a.out + xp.x;
+      double* dba = a.out + xp.y;
+      *dab = a.accumulate ? *dab + vab : vab;
+      *dba = a.accumulate ? *dba + vab : vab;
+      if (hA) atomicAdd(a.out + xp.z, dA);
+      if (hB) atomicAdd(a.out + xp.w, dB);
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[k % STAGES]);
+    if (a.accumulate) {
+      named_bar(1, NT);
+      for (int t = tid; t < len; t += NT) a.out[(int64_t)E0 + t] += seg[t];
+    } else {
+      // segment complete -> one TMA bulk store (doubles off the 16-byte grid stored directly)
+      fence_async_shared();
+      named_bar(1, NT);
+      if (tid == 0) {
+        double* dst = a.out + E0;
+        const int h = E0 & 1, t1 = len - ((E0 + len) & 1);
+        if (h && len > 0) dst[0] = seg[0];
+        if (t1 > h) {
+          bulk_s2g(dst + h, seg + h, (uint32_t)(t1 - h) * 8);
+          bulk_commit();
+        }
+        if (t1 < len && t1 >= h) dst[t1] = seg[t1];
+      }
+    }
+  }
+  if (tid == 0) bulk_wait_read<0>();
+}
+
+__global__ void k_et_zero(const int32_t* __restrict__ pos, int64_t n, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[pos[i]] = 0.0;
+}
+
+template <int FORM, int D>
+void go_etile(const EtilePlan& p, const EtileArgs& a, size_t smem_base, size_t buf, cudaStream_t s) {
+  auto go = [&](auto kern, int threads, int stages) {
+    const size_t smem = smem_base + stages * buf;
+    static size_t attr = 0;
+    if (attr < smem) {
+      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    int blocks = 1;
+    LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, threads, smem));
+    require(blocks > 0, LOAM_GPU_ERR_CUDA, "edge-tile kernel does not fit on an SM");
+    const int grid = std::min(p.ntiles, blocks * kNumSMs);
+    kern<<<grid, threads, smem, s>>>(a);
+  };
+  const int st = et_stages();
+  if (p.tile_threads == 64) {
+    if (st >= 2) go(k_etile<FORM, D, 64, 2>, 96, 2);
+    else go(k_etile<FORM, D, 64, 1>, 96, 1);
+  } else {
+    if (st >= 2) go(k_etile<FORM, D, 128, 2>, 160, 2);
+    else go(k_etile<FORM, D, 128, 1>, 160, 1);
+  }
+}
+
+} // namespace
+
+int et_stages() {
+  // two stages: the next tile's blob and window land while this one computes
+  static const int st = std::getenv("LOAM_GPU_ET_STAGES") ? std::atoi(std::getenv("LOAM_GPU_ET_STAGES")) : 2;
+  return st;
+}
+
+void launch_etile(int form, const EtilePlan& p, const double* coords, double* out, const FormParams& prm,
+                  bool accumulate, int* next_tile, int* reset_tile, cudaStream_t s) {
+  if (!accumulate && p.ndiag) {
+    k_et_zero<<<ceil_div(p.ndiag, 256), 256, 0, s>>>(p.diag.get(), p.ndiag, out);
+    count_launch();
+    LG_LAUNCH_CHECK();
+  }
+  if (p.ntiles == 0) return;
+  EtileArgs a{};
+  a.tiles = p.tiles.get();
+  a.ntiles = p.ntiles;
+  a.next_tile = next_tile;
+  a.reset_tile = reset_tile;
+  a.blob = p.blob.get();
+  a.runs = p.runs.get();
+  a.coords = coords;
+  a.out = out;
+  a.prm = prm;
+  a.accumulate = accumulate ? 1 : 0;
+  a.dynamic = std::getenv("LOAM_GPU_ET_STATIC") ? 0 : 1;
+  a.dbg = std::getenv("LOAM_GPU_ET_DBG") ? std::atoi(std::getenv("LOAM_GPU_ET_DBG")) : 0; // developer: skip phases
+  memcpy(a.ktab, p.ktab, sizeof(a.ktab));
+  const int nv = p.gd + 1, ng = nv * (nv + 1) / 2 + 1;
+  int off = 128;
+  a.off_seg = off;
+  off += up16((p.max_seg + 2) * 8);
+  a.off_geo = off;
+  off += up16(p.max_cells * ng * 8);
+  a.off_buf = off;
+  a.b_win = up16(p.max_blob);
+  a.buf_bytes = a.b_win + up16(p.max_slots * p.gd * 8 + 16);
+  const size_t base = (size_t)off, buf = (size_t)a.buf_bytes;
+  if (p.gd == 3) {
+    if (form == F_MASS) go_etile<F_MASS, 3>(p, a, base, buf, s);
+    else if (form == F_STIFFNESS) go_etile<F_STIFFNESS, 3>(p, a, base, buf, s);
+    else go_etile<F_HELMHOLTZ, 3>(p, a, base, buf, s);
+  } else {
+    if (form == F_MASS) go_etile<F_MASS, 2>(p, a, base, buf, s);
+    else if (form == F_STIFFNESS) go_etile<F_STIFFNESS, 2>(p, a, base, buf, s);
+    else go_etile<F_HELMHOLTZ, 2>(p, a, base, buf, s);
+  }
+  count_launch();
+  LG_LAUNCH_CHECK();
+}
+
+} // namespace loam_gpu

@@ -1,0 +1,66 @@
+// stage.cuh -- warp-cooperative TMA staging of id-run windows (sm_100a).
+//
+// A tile's vertex (or coefficient) window is the union of a few contiguous id
+// runs of an AoS fp64 array; the producer warp copies every run into
+// consecutive shared-memory slots with cp.async.bulk (async.cuh).
+#pragma once
+#include <cstdint>
+
+#include "async.cuh"
+
+namespace loam_gpu {
+
+__device__ __forceinline__ int skew_of(int lo, int es) { return ((lo * es) & 15) / es; }
+
+// Warp-cooperative staging of a tile's id runs [lo, hi) of an es-doubles-per-id
+// array into consecutive window slots: lane r handles run r (32 at a time),
+// slots from a warp scan.  A run whose byte count is not a multiple of 16 gets
+// its last double stored by the lane itself (bulk copies move 16-byte units;
+// runs start at even ids so the source side is aligned).  prepare() does the
+// tail stores and returns the warp-total bulk bytes; issue() launches copies.
+struct RunSet {
+  const int2* runs;
+  int cnt;
+  const double* src;
+  double* dst;
+  int es;
+};
+// `first`: the lane's run of the first chunk, prefetched by the caller.
+__device__ __forceinline__ int2 first_run(const int2* runs, int cnt, int lane) {
+  return lane < cnt ? __ldg(runs + lane) : make_int2(0, 0);
+}
+template <bool ISSUE>
+__device__ __forceinline__ uint32_t stage_runs(const RunSet& s, int lane, uint64_t* bar, int2 first) {
+  uint32_t tx = 0;
+  int base = 0;
+  for (int r0 = 0; r0 < s.cnt; r0 += 32) {
+    int lo = first.x, hi = first.y;
+    if (r0 > 0) {
+      const int2 p = r0 + lane < s.cnt ? __ldg(s.runs + r0 + lane) : make_int2(0, 0);
+      lo = p.x;
+      hi = p.y;
+    }
+    const int n = hi - lo;
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int slot = base + incl - n;
+    const uint32_t nb = (uint32_t)n * s.es * 8;
+    if (ISSUE) {
+      if (nb >= 16) bulk_g2s(s.dst + (int64_t)slot * s.es, s.src + (int64_t)lo * s.es, nb & ~15u, bar);
+    } else {
+      if (nb & 15) s.dst[(int64_t)(slot + n) * s.es - 1] = s.src[(int64_t)hi * s.es - 1];
+      tx += nb & ~15u;
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (!ISSUE)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
+  return tx;
+}
+
+} // namespace loam_gpu
