@@ -146,15 +146,12 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
     for (int v = 0; v < nv; ++v)
       if (v != la && v != lb) sig[q++] = v;
   };
-  for (int k = 0; k < ne; ++k)
+  for (int k = 0; k < ne; ++k) // canonical vertex m <- original local vertex sigma(m), 4 bits each
     for (int sw = 0; sw < 2; ++sw) {
       int sig[4];
       sigma_of(k, sw, sig);
       uint32_t w = 0;
-      int q = 0;
-      for (int m = 0; m < nv; ++m) w |= (uint32_t)gram_index(nv, sig[ca], sig[m]) << (4 * q++);
-      for (int m = 0; m < nv; ++m)
-        if (m != ca) w |= (uint32_t)gram_index(nv, sig[cb], sig[m]) << (4 * q++);
+      for (int m = 0; m < nv; ++m) w |= (uint32_t)sig[m] << (4 * m);
       ktab[k * 2 + sw] = w;
     }
   // ---- per edge row: transposed positions, vertex-pair positions, records
@@ -211,21 +208,40 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       cellof[p - p0e] = c;
     }
   }
-  // ---- edge tiles: consecutive edge rows, their distinct cells and coordinate window
+  // ---- edge tiles: consecutive edge rows, their distinct cells and coordinate window.
+  // Per warp of rows the segment is lane-interleaved (entry j of lane r at
+  // base + 32 j + r: conflict-free shared updates) and so are the pair
+  // records (word q of pair p of lane r at base + 32 (p RBW + q) + r).
   std::vector<int32_t> tiles, runs;
   std::vector<uint8_t> blob;
   std::vector<int> stamp(ncells, -1), local(ncells, 0), vid;
   std::vector<std::pair<int, int>> rr;
   int gen = 0, r0 = 0;
-  const int trows = sp.tile_rows <= 64 ? 64 : 128;
+  const int trows = sp.tile_rows <= 64 ? 64 : 128, nwarps = trows / 32, rbw = rb / 4;
   const int cell_cap = std::min(sp.tile_cells, 1023);
+  auto warp_sizes = [&](int a, int b, std::vector<int>& lmax, std::vector<int>& pmax) {
+    lmax.assign(nwarps, 0);
+    pmax.assign(nwarps, 0);
+    for (int r = a; r < b; ++r) {
+      const int w = (r - a) / 32;
+      lmax[w] = std::max<int>(lmax[w], (int)(hrp[E0 + r + 1] - hrp[E0 + r]));
+      pmax[w] = std::max(pmax[w], hp[E0 + r + 1] - hp[E0 + r]);
+    }
+    int st = 0;
+    for (int w = 0; w < nwarps; ++w) st += 32 * lmax[w];
+    return st;
+  };
+  std::vector<int> lmax, pmax;
   while (r0 < nedge) {
     int r1 = std::min(nedge, r0 + trows);
     std::vector<int> cells;
     int slots = 0;
     auto fits = [&](int a, int b) {
       if (hrp[E0 + b] - hrp[E0 + a] > sp.tile_seg) return false;
+      if (warp_sizes(a, b, lmax, pmax) > sp.tile_seg) return false;
       if (hp[E0 + b] - hp[E0 + a] > sp.tile_pairs) return false;
+      for (int r = a; r < b; ++r)
+        if (hp[E0 + r + 1] - hp[E0 + r] > 255) return false;
       ++gen;
       cells.clear();
       for (int p = hp[E0 + a]; p < hp[E0 + b]; ++p) {
@@ -246,6 +262,7 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       if (r1 == r0 + 1) return false;
       r1 = r0 + (r1 - r0) / 2;
     }
+    const int segT = warp_sizes(r0, r1, lmax, pmax);
     std::sort(cells.begin(), cells.end());
     for (size_t q = 0; q < cells.size(); ++q) local[cells[q]] = (int)q;
     std::vector<int> base(rr.size());
@@ -257,45 +274,63 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       size_t q = std::upper_bound(rr.begin(), rr.end(), std::make_pair(v, INT32_MAX)) - rr.begin() - 1;
       return base[q] + v - rr[q].first;
     };
-    const int nrows = r1 - r0, P0 = hp[E0 + r0], npairs = hp[E0 + r1] - P0, ncell = (int)cells.size();
+    const int nrows = r1 - r0, ncell = (int)cells.size();
     const int T0 = tptr[r0], ntp = tptr[r1] - T0;
-    const int off_prow = 0, off_srow = up16((nrows + 1) * 2), off_tptr = off_srow + up16((nrows + 1) * 2),
-              off_xpos = off_tptr + up16((nrows + 1) * 2), off_tpos = off_xpos + nrows * 16,
-              off_recs = off_tpos + up16(ntp * 4), off_cells = off_recs + up16(npairs * rb),
+    int rwords = 0;
+    for (int w = 0; w < nwarps; ++w) rwords += pmax[w] * rbw * 32;
+    const int off_srow = 0, off_trow = up16((nrows + 1) * 2), off_np = off_trow + up16((nrows + 1) * 2),
+              off_xpos = off_np + up16(trows + 4 * nwarps), off_tpos = off_xpos + nrows * 16,
+              off_recs = off_tpos + up16(ntp * 4), off_cells = off_recs + up16(rwords * 4),
               bytes = off_cells + up16(ncell * nv * 2);
     const size_t b0 = blob.size();
     blob.resize(b0 + bytes, 0);
     uint8_t* bp = blob.data() + b0;
     for (int r = 0; r <= nrows; ++r) {
-      const uint16_t pr = (uint16_t)(hp[E0 + r0 + r] - P0);
       const uint16_t sr = (uint16_t)(hrp[E0 + r0 + r] - hrp[E0 + r0]);
       const uint16_t tr = (uint16_t)(tptr[r0 + r] - T0);
-      memcpy(bp + off_prow + 2 * r, &pr, 2);
       memcpy(bp + off_srow + 2 * r, &sr, 2);
-      memcpy(bp + off_tptr + 2 * r, &tr, 2);
+      memcpy(bp + off_trow + 2 * r, &tr, 2);
+    }
+    for (int r = 0; r < nrows; ++r) bp[off_np + r] = (uint8_t)(hp[E0 + r0 + r + 1] - hp[E0 + r0 + r]);
+    {
+      int sb = 0, wb = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        const uint16_t s16 = (uint16_t)sb, w16 = (uint16_t)wb;
+        memcpy(bp + off_np + trows + 4 * w, &s16, 2);
+        memcpy(bp + off_np + trows + 4 * w + 2, &w16, 2);
+        for (int l = 0; l < 32 && 32 * w + l < nrows; ++l) {
+          const int r = r0 + 32 * w + l;
+          for (int p = hp[E0 + r]; p < hp[E0 + r + 1]; ++p) {
+            const int64_t pe = p - p0e;
+            uint8_t rec[16];
+            memcpy(rec, &recs[(size_t)pe * rb], rb);
+            uint16_t h;
+            memcpy(&h, rec, 2);
+            h = (uint16_t)(h | local[cellof[pe]]);
+            memcpy(rec, &h, 2);
+            const int pi = p - hp[E0 + r];
+            for (int q = 0; q < rbw; ++q)
+              memcpy(bp + off_recs + 4 * ((size_t)wb + (pi * rbw + q) * 32 + l), rec + 4 * q, 4);
+          }
+        }
+        sb += 32 * lmax[w];
+        wb += pmax[w] * rbw * 32;
+      }
     }
     memcpy(bp + off_xpos, &xpos[r0], (size_t)nrows * 16);
     if (ntp) memcpy(bp + off_tpos, &tpos[T0], (size_t)ntp * 4);
-    for (int q = 0; q < npairs; ++q) {
-      const int64_t pe = P0 + q - p0e;
-      uint8_t* rec = bp + off_recs + (size_t)q * rb;
-      memcpy(rec, &recs[(size_t)pe * rb], rb);
-      uint16_t h;
-      memcpy(&h, rec, 2);
-      h = (uint16_t)(h | local[cellof[pe]]);
-      memcpy(rec, &h, 2);
-    }
     for (int q = 0; q < ncell; ++q)
       for (int v = 0; v < nv; ++v) {
         const uint16_t sl = (uint16_t)slot_in(hx[(size_t)cells[q] * nv + v]);
         memcpy(bp + off_cells + 2 * (q * nv + v), &sl, 2);
       }
     const int seg = (int)(hrp[E0 + r1] - hrp[E0 + r0]);
-    tiles.insert(tiles.end(), {(int)(b0 / 16), bytes, r0, nrows, (int)hrp[E0 + r0], seg, npairs, ncell,
-                               (int)runs.size() / 2, (int)rr.size(), off_prow, off_srow, off_recs, off_cells, off_tptr, off_xpos});
+    tiles.insert(tiles.end(), {(int)(b0 / 16), bytes, r0, nrows, (int)hrp[E0 + r0], seg, segT, ncell,
+                               (int)runs.size() / 2, (int)rr.size(), off_srow, off_np, off_recs, off_cells, off_trow,
+                               off_xpos});
+    out.max_segT = std::max(out.max_segT, segT);
     for (auto& x : rr) runs.insert(runs.end(), {x.first, x.second});
     out.max_rows = std::max(out.max_rows, nrows);
-    out.max_pairs = std::max(out.max_pairs, npairs);
     out.max_seg = std::max(out.max_seg, seg);
     out.max_cells = std::max(out.max_cells, ncell);
     out.max_slots = std::max(out.max_slots, slots);
@@ -348,9 +383,10 @@ struct EtileArgs {
 template <int D>
 struct EtT {
   static constexpr int NV = D + 1, NE = D == 2 ? 3 : 6, N = NV + NE;
-  static constexpr int NG = NV * (NV + 1) / 2 + 1; // Gram entries + V
-  static constexpr int NT = 2 * NV - 1;            // Gram entries a canonical edge row reads
-  static constexpr int RB = (2 + N + 3) & ~3;
+  // per cell in shared memory: the Gram matrix G_xy = V g_x.g_y as NV rows of
+  // 4 doubles (two 16-byte loads per row), then V; stride odd in 16-byte units
+  static constexpr int GV = 4 * NV, GS = D == 2 ? 14 : 18;
+  static constexpr int RB = (2 + N + 3) & ~3, RBW = RB / 4;
   static constexpr int CA = NV - 2, CB = NV - 1;   // canonical row edge = local edge 0
 };
 
@@ -359,20 +395,15 @@ struct EtT {
 // cell measure folded into G.  Also returns the (CA, CB) vertex-vertex entry
 // and the two vertex diagonals of this cell.
 template <int FORM, int D>
-__device__ __forceinline__ void et_row(const double (&t)[EtT<D>::NT], double V, const FormParams& prm,
-                                       double (&o)[EtT<D>::N], double& vab, double& dga, double& dgb) {
+__device__ __forceinline__ void et_row(const double (&Ga)[D + 1], const double (&Gb)[D + 1], double V,
+                                       const FormParams& prm, double (&o)[EtT<D>::N], double& vab, double& dga,
+                                       double& dgb) {
   using T = EtT<D>;
   using S = Simplex<D>;
   constexpr int NV = T::NV, NE = T::NE, a = T::CA, b = T::CB;
   constexpr double qs = S::q_same, qd = S::q_diff, l1 = S::l1;
   constexpr double cs = 16.0 * qs - 8.0 * l1 + 1.0, co = 16.0 * qd - 8.0 * l1 + 1.0;
   constexpr double es = 4.0 * qs - l1, ed = 4.0 * qd - l1;
-  double Ga[NV], Gb[NV];
-#pragma unroll
-  for (int m = 0; m < NV; ++m) {
-    Ga[m] = t[m];
-    Gb[m] = m == a ? t[b] : (m < a ? t[NV + m] : t[2 * NV - 2]);
-  }
   const double kV = prm.p[0] * V;
   auto comb = [&](double K, double M) {
     if constexpr (FORM == F_MASS) return V * M;
@@ -413,11 +444,31 @@ __device__ __forceinline__ void et_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// v[i] for a runtime i in 0..3 without local memory or branches (selp.f64)
+__device__ __forceinline__ double sel4(const double (&v)[4], int i) {
+  double r;
+  asm("{\n"
+      ".reg .pred p0, p1;\n"
+      ".reg .f64 lo, hi;\n"
+      ".reg .b32 t;\n"
+      "and.b32 t, %5, 1;\n"
+      "setp.ne.s32 p0, t, 0;\n"
+      "and.b32 t, %5, 2;\n"
+      "setp.ne.s32 p1, t, 0;\n"
+      "selp.f64 lo, %2, %1, p0;\n"
+      "selp.f64 hi, %4, %3, p0;\n"
+      "selp.f64 %0, hi, lo, p1;\n"
+      "}\n"
+      : "=d"(r)
+      : "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]), "r"(i));
+  return r;
+}
+
 // NT consumer threads (= edge rows per tile) + one TMA producer warp.
 template <int FORM, int D, int NT, int STAGES>
 __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ EtileArgs a) {
   using T = EtT<D>;
-  constexpr int NV = T::NV, N = T::N, NG = T::NG, RB = T::RB;
+  constexpr int NV = T::NV, N = T::N;
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + STAGES;
@@ -501,26 +552,30 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
     return;
   }
   // ---- consumers
-  double* seg0 = reinterpret_cast<double*>(sm + a.off_seg);
-  double* geo = reinterpret_cast<double*>(sm + a.off_geo);
+  constexpr int GS = T::GS, RBW = T::RBW;
+  double* segT = reinterpret_cast<double*>(sm + a.off_seg); // lane-interleaved row segments
+  double* geo = reinterpret_cast<double*>(sm + a.off_geo);  // cell Gram matrices; then the contiguous segment
+  const int lane = tid & 31, warp = tid >> 5;
   for (int k = 0;; ++k) {
     et_wait(&full[k % STAGES], (k / STAGES) & 1);
     const int tile = slot_tile[k % STAGES];
     if (tile < 0) break;
     int m[16];
     meta(tile, m);
-    const int nrows = m[3], E0 = m[4], len = m[5], ncell = m[7];
+    const int nrows = m[3], E0 = m[4], len = m[5], lenT = m[6], ncell = m[7];
     const unsigned char* buf = ring(k);
-    const uint16_t* prow = reinterpret_cast<const uint16_t*>(buf + m[10]);
-    const uint16_t* srow = reinterpret_cast<const uint16_t*>(buf + m[11]);
-    const unsigned char* recs = buf + m[12];
+    const uint16_t* srow = reinterpret_cast<const uint16_t*>(buf + m[10]);
+    const uint8_t* npair = buf + m[11];
+    const uint16_t* wmeta = reinterpret_cast<const uint16_t*>(buf + m[11] + NT);
+    const uint32_t* recs = reinterpret_cast<const uint32_t*>(buf + m[12]);
     const uint16_t* cslot = reinterpret_cast<const uint16_t*>(buf + m[13]);
     const uint16_t* trow = reinterpret_cast<const uint16_t*>(buf + m[14]);
     const int4* xpos = reinterpret_cast<const int4*>(buf + m[15]);
     const int32_t* tpos = reinterpret_cast<const int32_t*>(buf + m[15] + 16 * nrows);
     const double* win = reinterpret_cast<const double*>(buf + a.b_win);
-    // the segment shares the 16-byte parity of its global destination (bulk store)
-    double* seg = seg0 + (E0 & 1);
+    // the previous tile's bulk store reads the contiguous segment (in geo)
+    if (tid == 0) bulk_wait_read<0>();
+    named_bar(1, NT);
     // phase 1: the Gram matrix of every cell of the tile, once
     for (int c = tid; c < ((a.dbg & 2) ? 0 : ncell); c += NT) {
       double X[NV][D];
@@ -532,65 +587,81 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
       }
       Geom<D> Gm;
       geometry<D>(X, Gm);
-      double* g = geo + c * NG;
+      double* g = geo + c * GS;
       if constexpr (FORM != F_MASS) {
-        int idx = 0;
+        double vg[NV][D];
+#pragma unroll
+        for (int p = 0; p < NV; ++p)
+#pragma unroll
+          for (int q = 0; q < D; ++q) vg[p][q] = Gm.V * Gm.g[p][q];
+        double Gr[NV][4];
+#pragma unroll
+        for (int p = 0; p < NV; ++p)
+#pragma unroll
+          for (int q = p; q < NV; ++q) {
+            Gr[p][q] = dot<D>(vg[p], Gm.g[q]);
+            Gr[q][p] = Gr[p][q];
+          }
 #pragma unroll
         for (int p = 0; p < NV; ++p) {
-          double vg[D];
-#pragma unroll
-          for (int q = 0; q < D; ++q) vg[q] = Gm.V * Gm.g[p][q];
-#pragma unroll
-          for (int q = p; q < NV; ++q) g[idx++] = dot<D>(vg, Gm.g[q]);
+          if constexpr (NV < 4) Gr[p][3] = 0.0;
+          reinterpret_cast<double2*>(g + 4 * p)[0] = make_double2(Gr[p][0], Gr[p][1]);
+          reinterpret_cast<double2*>(g + 4 * p)[1] = make_double2(Gr[p][2], Gr[p][3]);
         }
       }
-      g[NG - 1] = Gm.V;
+      g[T::GV] = Gm.V;
     }
-    // the previous tile's bulk store must have read the segment
-    if (tid == 0) bulk_wait_read<0>();
-    named_bar(1, NT);
     {
-      double2* z = reinterpret_cast<double2*>(seg0);
-      const int n2 = (len + 2) >> 1;
-      for (int t = tid; t < n2; t += NT) z[t] = make_double2(0.0, 0.0); // this loop's contributions only
+      double2* z = reinterpret_cast<double2*>(segT);
+      for (int t = tid; t < (lenT >> 1); t += NT) z[t] = make_double2(0.0, 0.0); // this loop's contributions only
     }
     named_bar(1, NT);
     // phase 2: one thread per edge row
+    int s0 = 0, L = 0;
+    const int sb = wmeta[2 * warp], rbase = wmeta[2 * warp + 1];
+    double* my = segT + sb + lane; // entry j of this row at my[32 j]
     if (tid < nrows) {
-      const int p0 = prow[tid], p1 = prow[tid + 1], s0 = srow[tid];
+      s0 = srow[tid];
+      L = srow[tid + 1] - s0;
+      const int np = (a.dbg & 1) ? 0 : npair[tid];
       double vab = 0.0, dA = 0.0, dB = 0.0;
       bool hA = false, hB = false;
-      // software pipeline: the next pair's record and Gram entries are loaded
-      // before this pair's arithmetic and segment updates
-      uint32_t w[RB / 4];
-      double t[T::NT], V = 0.0;
-      auto fetch = [&](int p, uint32_t (&wq)[RB / 4], double (&tq)[T::NT], double& Vq) {
+      const uint32_t* rq = recs + rbase + lane;
+      for (int p = 0; p < np; ++p) {
+        uint32_t w[RBW];
 #pragma unroll
-        for (int q = 0; q < RB / 4; ++q) wq[q] = reinterpret_cast<const uint32_t*>(recs + p * RB)[q];
-        const uint32_t h = wq[0] & 0xffffu;
-        const double* g = geo + (h & 1023u) * NG;
-        const uint32_t gi = ktab[(h >> 10) & 15u];
-#pragma unroll
-        for (int q = 0; q < T::NT; ++q) tq[q] = g[(gi >> (4 * q)) & 15u];
-        Vq = g[NG - 1];
-      };
-      const int pe = (a.dbg & 1) ? p0 : p1;
-      if (p0 < pe) fetch(p0, w, t, V);
-      for (int p = p0; p < pe; ++p) {
-        uint32_t wn[RB / 4];
-        double tn[T::NT], Vn = 0.0;
-        if (p + 1 < pe) fetch(p + 1, wn, tn, Vn);
+        for (int q = 0; q < RBW; ++q) w[q] = rq[(p * RBW + q) * 32];
         const uint32_t h = w[0] & 0xffffu;
+        const uint32_t sg = ktab[(h >> 10) & 15u];
+        const double* g = geo + (h & 1023u) * GS;
+        const int la = (sg >> (4 * T::CA)) & 15, lb = (sg >> (4 * T::CB)) & 15;
+        double GA[4], GB[4];
+        {
+          const double2* ra = reinterpret_cast<const double2*>(g + 4 * la);
+          const double2* rb2 = reinterpret_cast<const double2*>(g + 4 * lb);
+          const double2 a0 = ra[0], a1 = ra[1], b0 = rb2[0], b1 = rb2[1];
+          GA[0] = a0.x; GA[1] = a0.y; GA[2] = a1.x; GA[3] = a1.y;
+          GB[0] = b0.x; GB[1] = b0.y; GB[2] = b1.x; GB[3] = b1.y;
+        }
+        const double V = g[T::GV];
+        // canonical order: canonical vertex mm is original local vertex sigma(mm)
+        double Ga[NV], Gb[NV];
+#pragma unroll
+        for (int mm = 0; mm < NV; ++mm) {
+          const int sv = (sg >> (4 * mm)) & 15;
+          Ga[mm] = sel4(GA, sv);
+          Gb[mm] = sel4(GB, sv);
+        }
         double o[N], dga, dgb;
-        et_row<FORM, D>(t, V, a.prm, o, vab, dga, dgb);
+        et_row<FORM, D>(Ga, Gb, V, a.prm, o, vab, dga, dgb);
         int pos[N];
 #pragma unroll
-        for (int j = 0; j < N; ++j) pos[j] = s0 + (int)((w[(2 + j) >> 2] >> (8 * ((2 + j) & 3))) & 0xffu);
+        for (int j = 0; j < N; ++j) pos[j] = 32 * (int)((w[(2 + j) >> 2] >> (8 * ((2 + j) & 3))) & 0xffu);
         double cur[N];
 #pragma unroll
-        for (int j = 0; j < N; ++j) cur[j] = seg[pos[j]];
+        for (int j = 0; j < N; ++j) cur[j] = my[pos[j]];
 #pragma unroll
-        for (int j = 0; j < N; ++j) seg[pos[j]] = cur[j] + o[j];
+        for (int j = 0; j < N; ++j) my[pos[j]] = cur[j] + o[j];
         if (h & 0x4000u) {
           dA += dga;
           hA = true;
@@ -599,17 +670,12 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
           dB += dgb;
           hB = true;
         }
-#pragma unroll
-        for (int q = 0; q < RB / 4; ++q) w[q] = wn[q];
-#pragma unroll
-        for (int q = 0; q < T::NT; ++q) t[q] = tn[q];
-        V = Vn;
       }
       // vertex rows: transposed vertex-column entries, the vertex pair, diagonals
       const int t0 = trow[tid], t1 = (a.dbg & 4) ? t0 : trow[tid + 1];
       for (int t = t0; t < t1; ++t) {
         double* dst = a.out + tpos[t];
-        const double v = seg[s0 + t - t0];
+        const double v = my[32 * (t - t0)];
         *dst = a.accumulate ? *dst + v : v;
       }
       const int4 xp = xpos[tid];
@@ -622,6 +688,9 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[k % STAGES]);
+    named_bar(1, NT); // every Gram read done: geo becomes the contiguous segment
+    double* seg = geo + (E0 & 1); // shares the 16-byte parity of its global destination
+    for (int j = 0; j < L; ++j) seg[s0 + j] = my[32 * j];
     if (a.accumulate) {
       named_bar(1, NT);
       for (int t = tid; t < len; t += NT) a.out[(int64_t)E0 + t] += seg[t];
@@ -704,12 +773,11 @@ void launch_etile(int form, const EtilePlan& p, const double* coords, double* ou
   a.dynamic = std::getenv("LOAM_GPU_ET_STATIC") ? 0 : 1;
   a.dbg = std::getenv("LOAM_GPU_ET_DBG") ? std::atoi(std::getenv("LOAM_GPU_ET_DBG")) : 0; // developer: skip phases
   memcpy(a.ktab, p.ktab, sizeof(a.ktab));
-  const int nv = p.gd + 1, ng = nv * (nv + 1) / 2 + 1;
   int off = 128;
   a.off_seg = off;
-  off += up16((p.max_seg + 2) * 8);
+  off += up16(p.max_segT * 8);
   a.off_geo = off;
-  off += up16(p.max_cells * ng * 8);
+  off += up16(std::max(p.max_cells * (p.gd == 2 ? 14 : 18), p.max_seg + 2) * 8);
   a.off_buf = off;
   a.b_win = up16(p.max_blob);
   a.buf_bytes = a.b_win + up16(p.max_slots * p.gd * 8 + 16);

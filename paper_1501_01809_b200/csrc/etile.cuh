@@ -31,13 +31,14 @@ namespace loam_gpu {
 
 struct EtilePlan {
   int gd = 3, ntiles = 0, e0 = 0, nedge = 0, rec_bytes = 0, tile_threads = 128;
-  int max_rows = 0, max_pairs = 0, max_seg = 0, max_cells = 0, max_slots = 0, max_blob = 0;
+  int max_rows = 0, max_seg = 0, max_segT = 0, max_cells = 0, max_slots = 0, max_blob = 0;
   int64_t ndiag = 0;
   DevBuf<int32_t> tiles; // 16 ints per tile (etile.cu)
-  // per tile, 16-byte aligned sections (one TMA copy): pair offsets u16, segment
-  // offsets u16, transposed-entry offsets u16, per row pos(A,B) / pos(B,A) /
-  // diag(A) / diag(B) (int4), the value positions (in vertex rows) of the rows'
-  // vertex columns (int32), pair records, cell vertex slots (u16)
+  // per tile, 16-byte aligned sections (one TMA copy): segment offsets u16,
+  // transposed-entry offsets u16, pair counts u8 + per-warp (segment base,
+  // record base) u16, per row pos(A,B) / pos(B,A) / diag(A) / diag(B) (int4),
+  // the value positions (in vertex rows) of the rows' vertex columns (int32),
+  // lane-interleaved pair records, cell vertex slots (u16)
   DevBuf<uint8_t> blob;
   DevBuf<int32_t> runs;  // coordinate-window runs [lo, hi)
   DevBuf<int32_t> diag;  // diagonal positions of the vertex rows (zeroed before the REDs)
@@ -45,7 +46,7 @@ struct EtilePlan {
 };
 
 struct EtileSpec {
-  int tile_rows = 64; // 64 or 128: consumer threads per CTA, one edge row each
+  int tile_rows = 128; // 64 or 128: consumer threads per CTA, one edge row each
   int tile_seg = 4096, tile_pairs = 1024, tile_cells = 512, tile_slots = 768, tile_runs = 32;
 };
 
