@@ -2257,12 +2257,13 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     build_ranks(P->pp, srows.v.get(), sc, Cn.v.arity, csr, s);
     build_chunks(P->pp, csr, kSegMax, 32 / R.dim, s);
     // edge tiles: scalar P2 mass / stiffness / helmholtz on one (map, map) pattern
-    const bool et_form = (k.form == F_MASS || k.form == F_STIFFNESS || k.form == F_HELMHOLTZ) &&
-                         k.nrn == (k.gd == 2 ? 6 : 10) && k.ncn == k.nrn && k.rd == 1 && k.cd == 1;
-    if (strat == 0 && et_form && !std::getenv("LOAM_GPU_NO_ETILE") && R.dim == 1 && Cn.dim == 1 &&
+    const bool et_form = ((k.form == F_MASS || k.form == F_STIFFNESS || k.form == F_HELMHOLTZ) &&
+                          k.nrn == (k.gd == 2 ? 6 : 10) && k.ncn == k.nrn && k.rd == 1 && k.cd == 1) ||
+                         (k.form == F_STOKES_A && k.rd == 2 && k.cd == 2);
+    if (strat == 0 && et_form && !std::getenv("LOAM_GPU_NO_ETILE") && R.dim == k.rd && Cn.dim == k.cd &&
         (reinterpret_cast<uintptr_t>(args[1].data) & 15) == 0 && Cn.v.arity == R.v.arity &&
         (Cn.v.v == R.v.v || prefix_equal(Cn.v.v, Cn.v.arity, R.v.v, R.v.arity, R.v.arity, n, s)) &&
-        pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, 1, 1, sp->row_ptr, sp->col_idx, sp->nnz, s)) {
+        pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, k.rd, k.cd, sp->row_ptr, sp->col_idx, sp->nnz, s)) {
       SortedMap sx;
       gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, sx, s);
       EtileSpec es;
@@ -2270,7 +2271,7 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       es.tile_seg = env_int("LOAM_GPU_ET_SEG", es.tile_seg);
       es.tile_cells = env_int("LOAM_GPU_ET_CELLS", es.tile_cells);
       if (build_etile(P->et, es, k.gd, n, R.v.target, srows.v.get(), sx.v.get(), X->target_size, P->pp,
-                      sp->row_ptr, sp->nnz, s)) {
+                      sp->row_ptr, sp->nnz, k.rd, s)) {
         P->use_etile = true;
         return P;
       }

@@ -61,23 +61,32 @@ inline int up16(int x) { return (x + 15) & ~15; }
 
 bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nrows_node,
                  const int32_t* sorted_rows, const int32_t* sorted_x, int nverts, const PairPlan& pp,
-                 const int64_t* row_ptr, int64_t nnz, cudaStream_t s) {
+                 const int64_t* row_ptr, int64_t nnz, int cd, cudaStream_t s) {
   const int nv = gd + 1, ne = gd == 2 ? 3 : 6, nrn = nv + ne;
+  if (cd != 1 && cd != 2) return false;
   const int (*E)[2] = gd == 2 ? kTriE : kTetE;
   if (pp.nrn != nrn || pp.ncn != nrn || nnz >= (int64_t(1) << 31) || ncells == 0 || ncells >= (1 << 30))
     return false;
   const int64_t np = pp.npairs;
   std::vector<int32_t> hrows((size_t)ncells * nrn), hx((size_t)ncells * nv), hpairs(np), hp(nrows_node + 1);
   std::vector<uint8_t> hrank((size_t)np * nrn);
-  std::vector<int64_t> hrp(nrows_node + 1);
+  std::vector<int64_t> hrp((size_t)nrows_node * cd + 1);
   LG_CUDA(cudaMemcpyAsync(hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size(), cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaMemcpyAsync(hx.data(), sorted_x, sizeof(int32_t) * hx.size(), cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaMemcpyAsync(hpairs.data(), pp.pairs.get(), sizeof(int32_t) * np, cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaMemcpyAsync(hp.data(), pp.ptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaMemcpyAsync(hrank.data(), pp.ranks.get(), hrank.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hrp.data(), row_ptr, sizeof(int64_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hrp.data(), row_ptr, sizeof(int64_t) * hrp.size(), cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaStreamSynchronize(s));
-
+  // node-level pattern offsets (a cd x cd component-blocked CSR: node row i owns
+  // dof rows cd*i .. cd*i+cd-1, each cd * L_i long)
+  if (cd > 1) {
+    for (int i = 0; i <= nrows_node; ++i) hrp[i] = hrp[(size_t)i * cd] / (cd * cd);
+    hrp.resize(nrows_node + 1);
+  }
+  // value position of node entry (row node v, in-row rank): the (cd*v, cd*w) dof entry
+  auto vpos = [&](int v, int rank) { return (int32_t)(cd * cd * hrp[v] + cd * rank); };
+  auto vlen = [&](int v) { return (int32_t)(cd * (hrp[v + 1] - hrp[v])); }; // dof row length
   // ---- node roles: vertex nodes (local 0..gd) numbered before edge nodes
   std::vector<int8_t> role(nrows_node, 0);
   for (int c = 0; c < ncells; ++c)
@@ -129,8 +138,9 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
   for (int v = 0; v < E0; ++v)
     if (hp[v + 1] > hp[v]) {
       const int p = hp[v], i = hpairs[p] % nrn;
-      dpos[v] = (int32_t)(hrp[v] + hrank[(size_t)p * nrn + i]);
+      dpos[v] = vpos(v, hrank[(size_t)p * nrn + i]);
       diag.push_back(dpos[v]);
+      if (cd == 2) diag.push_back(vlen(v));
     }
   // diagonal contribution of (cell, local vertex v) is carried by local edge (0,1) for
   // v = 0 and (0,v) otherwise
@@ -157,8 +167,9 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
   // ---- per edge row: transposed positions, vertex-pair positions, records
   const int rb = (2 + nrn + 3) & ~3;
   const int64_t p0e = hp[E0], npe = hp[nrows_node] - p0e;
-  std::vector<int32_t> tptr(nedge + 1, 0), tpos, cellof(npe);
+  std::vector<int32_t> tptr(nedge + 1, 0), tpos, tlen, cellof(npe);
   std::vector<int4> xpos(nedge);
+  std::vector<int2> xlen(cd == 2 ? nedge : 0);
   std::vector<uint8_t> recs((size_t)npe * rb, 0);
   std::vector<std::pair<int, int>> vc; // (vertex node, cell carrying it)
   for (int e = 0; e < nedge; ++e) {
@@ -181,7 +192,8 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       }();
       const int64_t pw = find_pair(x.first, c);
       if (pw < 0 || k < 0) return false;
-      tpos.push_back((int32_t)(hrp[x.first] + hrank[(size_t)pw * nrn + k]));
+      tpos.push_back(vpos(x.first, hrank[(size_t)pw * nrn + k]));
+      if (cd == 2) tlen.push_back(vlen(x.first));
     }
     tptr[e + 1] = (int32_t)tpos.size();
     {
@@ -190,8 +202,9 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       const int lA = hrows[(size_t)c * nrn + la] == A ? la : lb, lB = lA == la ? lb : la;
       const int64_t pA = find_pair(A, c), pB = find_pair(B, c);
       if (pA < 0 || pB < 0) return false;
-      xpos[e] = make_int4((int32_t)(hrp[A] + hrank[(size_t)pA * nrn + lB]),
-                          (int32_t)(hrp[B] + hrank[(size_t)pB * nrn + lA]), dpos[A], dpos[B]);
+      xpos[e] = make_int4(vpos(A, hrank[(size_t)pA * nrn + lB]), vpos(B, hrank[(size_t)pB * nrn + lA]), dpos[A],
+                          dpos[B]);
+      if (cd == 2) xlen[e] = make_int2(vlen(A), vlen(B));
     }
     for (int p = hp[r]; p < hp[r + 1]; ++p) {
       const int c = hpairs[p] / nrn, k = hpairs[p] % nrn - nv;
@@ -280,7 +293,8 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
     for (int w = 0; w < nwarps; ++w) rwords += pmax[w] * rbw * 32;
     const int off_srow = 0, off_trow = up16((nrows + 1) * 2), off_np = off_trow + up16((nrows + 1) * 2),
               off_xpos = off_np + up16(trows + 4 * nwarps), off_tpos = off_xpos + nrows * 16,
-              off_recs = off_tpos + up16(ntp * 4), off_cells = off_recs + up16(rwords * 4),
+              off_tlen = off_tpos + up16(ntp * 4), off_xlen = off_tlen + (cd == 2 ? up16(ntp * 4) : 0),
+              off_recs = off_xlen + (cd == 2 ? up16(nrows * 8) : 0), off_cells = off_recs + up16(rwords * 4),
               bytes = off_cells + up16(ncell * nv * 2);
     const size_t b0 = blob.size();
     blob.resize(b0 + bytes, 0);
@@ -319,13 +333,17 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
     }
     memcpy(bp + off_xpos, &xpos[r0], (size_t)nrows * 16);
     if (ntp) memcpy(bp + off_tpos, &tpos[T0], (size_t)ntp * 4);
+    if (cd == 2) {
+      if (ntp) memcpy(bp + off_tlen, &tlen[T0], (size_t)ntp * 4);
+      memcpy(bp + off_xlen, &xlen[r0], (size_t)nrows * 8);
+    }
     for (int q = 0; q < ncell; ++q)
       for (int v = 0; v < nv; ++v) {
         const uint16_t sl = (uint16_t)slot_in(hx[(size_t)cells[q] * nv + v]);
         memcpy(bp + off_cells + 2 * (q * nv + v), &sl, 2);
       }
     const int seg = (int)(hrp[E0 + r1] - hrp[E0 + r0]);
-    tiles.insert(tiles.end(), {(int)(b0 / 16), bytes, r0, nrows, (int)hrp[E0 + r0], seg, segT, ncell,
+    tiles.insert(tiles.end(), {(int)(b0 / 16), bytes, r0, nrows, (int)(cd * cd * hrp[E0 + r0]), seg, segT, ncell,
                                (int)runs.size() / 2, (int)rr.size(), off_srow, off_np, off_recs, off_cells, off_trow,
                                off_xpos});
     out.max_segT = std::max(out.max_segT, segT);
@@ -338,12 +356,13 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
     r0 = r1;
   }
   out.gd = gd;
+  out.cd = cd;
   out.tile_threads = trows;
   out.ntiles = (int)tiles.size() / 16;
   out.e0 = E0;
   out.nedge = nedge;
   out.rec_bytes = rb;
-  out.ndiag = (int64_t)diag.size();
+  out.ndiag = (int64_t)diag.size() / cd;
   memcpy(out.ktab, ktab, sizeof(ktab));
   auto upload = [&](auto& dst, const auto& src) {
     using T = typename std::decay_t<decltype(src)>::value_type;
@@ -408,6 +427,7 @@ __device__ __forceinline__ void et_row(const double (&Ga)[D + 1], const double (
   auto comb = [&](double K, double M) {
     if constexpr (FORM == F_MASS) return V * M;
     else if constexpr (FORM == F_STIFFNESS) return K;
+    else if constexpr (FORM == F_STOKES_A) return prm.p[0] * K; // nu grad u : grad v, per component
     else return fma(kV, M, K);
   };
 #pragma unroll
@@ -465,7 +485,7 @@ __device__ __forceinline__ double sel4(const double (&v)[4], int i) {
 }
 
 // NT consumer threads (= edge rows per tile) + one TMA producer warp.
-template <int FORM, int D, int NT, int STAGES>
+template <int FORM, int D, int CD, int NT, int STAGES>
 __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ EtileArgs a) {
   using T = EtT<D>;
   constexpr int NV = T::NV, N = T::N;
@@ -562,7 +582,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
     if (tile < 0) break;
     int m[16];
     meta(tile, m);
-    const int nrows = m[3], E0 = m[4], len = m[5], lenT = m[6], ncell = m[7];
+    const int nrows = m[3], E0 = m[4], len = CD * CD * m[5], lenT = m[6], ncell = m[7];
     const unsigned char* buf = ring(k);
     const uint16_t* srow = reinterpret_cast<const uint16_t*>(buf + m[10]);
     const uint8_t* npair = buf + m[11];
@@ -673,24 +693,56 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
       }
       // vertex rows: transposed vertex-column entries, the vertex pair, diagonals
       const int t0 = trow[tid], t1 = (a.dbg & 4) ? t0 : trow[tid + 1];
-      for (int t = t0; t < t1; ++t) {
-        double* dst = a.out + tpos[t];
-        const double v = my[32 * (t - t0)];
-        *dst = a.accumulate ? *dst + v : v;
-      }
+      const int ntp = trow[nrows];
+      // CD = 2: the 2x2 block (v, v) / (v, w) is (x, 0; 0, x) at rows pos, pos + rowlen
+      const int32_t* tlen = tpos + ((ntp + 3) & ~3);
+      const int2* xlen = reinterpret_cast<const int2*>(tlen + ((ntp + 3) & ~3));
+      auto put = [&](int pos, int rl, double v) {
+        if constexpr (CD == 1) {
+          a.out[pos] = a.accumulate ? a.out[pos] + v : v;
+        } else {
+          double2* r0 = reinterpret_cast<double2*>(a.out + pos);
+          double2* r1 = reinterpret_cast<double2*>(a.out + pos + rl);
+          if (a.accumulate) {
+            double2 x0 = *r0, x1 = *r1;
+            x0.x += v;
+            x1.y += v;
+            *r0 = x0;
+            *r1 = x1;
+          } else {
+            *r0 = make_double2(v, 0.0);
+            *r1 = make_double2(0.0, v);
+          }
+        }
+      };
+      for (int t = t0; t < t1; ++t) put(tpos[t], CD == 2 ? tlen[t] : 0, my[32 * (t - t0)]);
       const int4 xp = xpos[tid];
-      double* dab = a.out + xp.x;
-      double* dba = a.out + xp.y;
-      *dab = a.accumulate ? *dab + vab : vab;
-      *dba = a.accumulate ? *dba + vab : vab;
-      if (hA) atomicAdd(a.out + xp.z, dA);
-      if (hB) atomicAdd(a.out + xp.w, dB);
+      const int2 xl = CD == 2 ? xlen[tid] : make_int2(0, 0);
+      put(xp.x, xl.x, vab);
+      put(xp.y, xl.y, vab);
+      if (hA) {
+        atomicAdd(a.out + xp.z, dA);
+        if constexpr (CD == 2) atomicAdd(a.out + xp.z + xl.x + 1, dA);
+      }
+      if (hB) {
+        atomicAdd(a.out + xp.w, dB);
+        if constexpr (CD == 2) atomicAdd(a.out + xp.w + xl.y + 1, dB);
+      }
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[k % STAGES]);
     named_bar(1, NT); // every Gram read done: geo becomes the contiguous segment
     double* seg = geo + (E0 & 1); // shares the 16-byte parity of its global destination
-    for (int j = 0; j < L; ++j) seg[s0 + j] = my[32 * j];
+    if constexpr (CD == 1) {
+      for (int j = 0; j < L; ++j) seg[s0 + j] = my[32 * j];
+    } else { // node row -> dof rows 2r (x, 0, ...) and 2r+1 (0, x, ...); E0 is a multiple of 4
+      double2* r0 = reinterpret_cast<double2*>(seg + 4 * s0);
+      for (int j = 0; j < L; ++j) {
+        const double v = my[32 * j];
+        r0[j] = make_double2(v, 0.0);
+        r0[L + j] = make_double2(0.0, v);
+      }
+    }
     if (a.accumulate) {
       named_bar(1, NT);
       for (int t = tid; t < len; t += NT) a.out[(int64_t)E0 + t] += seg[t];
@@ -713,12 +765,19 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
   if (tid == 0) bulk_wait_read<0>();
 }
 
-__global__ void k_et_zero(const int32_t* __restrict__ pos, int64_t n, double* __restrict__ out) {
+__global__ void k_et_zero(const int32_t* __restrict__ pos, int64_t n, int cd, double* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[pos[i]] = 0.0;
+  if (i >= n) return;
+  if (cd == 1) {
+    out[pos[i]] = 0.0;
+  } else { // the 2x2 diagonal block
+    const int p = pos[2 * i], rl = pos[2 * i + 1];
+    *reinterpret_cast<double2*>(out + p) = make_double2(0.0, 0.0);
+    *reinterpret_cast<double2*>(out + p + rl) = make_double2(0.0, 0.0);
+  }
 }
 
-template <int FORM, int D>
+template <int FORM, int D, int CD>
 void go_etile(const EtilePlan& p, const EtileArgs& a, size_t smem_base, size_t buf, cudaStream_t s) {
   auto go = [&](auto kern, int threads, int stages) {
     const size_t smem = smem_base + stages * buf;
@@ -735,11 +794,11 @@ void go_etile(const EtilePlan& p, const EtileArgs& a, size_t smem_base, size_t b
   };
   const int st = et_stages();
   if (p.tile_threads == 64) {
-    if (st >= 2) go(k_etile<FORM, D, 64, 2>, 96, 2);
-    else go(k_etile<FORM, D, 64, 1>, 96, 1);
+    if (st >= 2) go(k_etile<FORM, D, CD, 64, 2>, 96, 2);
+    else go(k_etile<FORM, D, CD, 64, 1>, 96, 1);
   } else {
-    if (st >= 2) go(k_etile<FORM, D, 128, 2>, 160, 2);
-    else go(k_etile<FORM, D, 128, 1>, 160, 1);
+    if (st >= 2) go(k_etile<FORM, D, CD, 128, 2>, 160, 2);
+    else go(k_etile<FORM, D, CD, 128, 1>, 160, 1);
   }
 }
 
@@ -754,7 +813,7 @@ int et_stages() {
 void launch_etile(int form, const EtilePlan& p, const double* coords, double* out, const FormParams& prm,
                   bool accumulate, int* next_tile, int* reset_tile, cudaStream_t s) {
   if (!accumulate && p.ndiag) {
-    k_et_zero<<<ceil_div(p.ndiag, 256), 256, 0, s>>>(p.diag.get(), p.ndiag, out);
+    k_et_zero<<<ceil_div(p.ndiag, 256), 256, 0, s>>>(p.diag.get(), p.ndiag, p.cd, out);
     count_launch();
     LG_LAUNCH_CHECK();
   }
@@ -777,19 +836,22 @@ void launch_etile(int form, const EtilePlan& p, const double* coords, double* ou
   a.off_seg = off;
   off += up16(p.max_segT * 8);
   a.off_geo = off;
-  off += up16(std::max(p.max_cells * (p.gd == 2 ? 14 : 18), p.max_seg + 2) * 8);
+  off += up16(std::max(p.max_cells * (p.gd == 2 ? 14 : 18), p.cd * p.cd * p.max_seg + 2) * 8);
   a.off_buf = off;
   a.b_win = up16(p.max_blob);
   a.buf_bytes = a.b_win + up16(p.max_slots * p.gd * 8 + 16);
   const size_t base = (size_t)off, buf = (size_t)a.buf_bytes;
-  if (p.gd == 3) {
-    if (form == F_MASS) go_etile<F_MASS, 3>(p, a, base, buf, s);
-    else if (form == F_STIFFNESS) go_etile<F_STIFFNESS, 3>(p, a, base, buf, s);
-    else go_etile<F_HELMHOLTZ, 3>(p, a, base, buf, s);
+  if (p.cd == 2) {
+    require(p.gd == 2 && form == F_STOKES_A, LOAM_ERR(InvalidArgument), "edge tiles: cd = 2 is the Stokes A block");
+    go_etile<F_STOKES_A, 2, 2>(p, a, base, buf, s);
+  } else if (p.gd == 3) {
+    if (form == F_MASS) go_etile<F_MASS, 3, 1>(p, a, base, buf, s);
+    else if (form == F_STIFFNESS) go_etile<F_STIFFNESS, 3, 1>(p, a, base, buf, s);
+    else go_etile<F_HELMHOLTZ, 3, 1>(p, a, base, buf, s);
   } else {
-    if (form == F_MASS) go_etile<F_MASS, 2>(p, a, base, buf, s);
-    else if (form == F_STIFFNESS) go_etile<F_STIFFNESS, 2>(p, a, base, buf, s);
-    else go_etile<F_HELMHOLTZ, 2>(p, a, base, buf, s);
+    if (form == F_MASS) go_etile<F_MASS, 2, 1>(p, a, base, buf, s);
+    else if (form == F_STIFFNESS) go_etile<F_STIFFNESS, 2, 1>(p, a, base, buf, s);
+    else go_etile<F_HELMHOLTZ, 2, 1>(p, a, base, buf, s);
   }
   count_launch();
   LG_LAUNCH_CHECK();

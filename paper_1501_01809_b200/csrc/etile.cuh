@@ -30,7 +30,7 @@
 namespace loam_gpu {
 
 struct EtilePlan {
-  int gd = 3, ntiles = 0, e0 = 0, nedge = 0, rec_bytes = 0, tile_threads = 128;
+  int gd = 3, cd = 1, ntiles = 0, e0 = 0, nedge = 0, rec_bytes = 0, tile_threads = 128;
   int max_rows = 0, max_seg = 0, max_segT = 0, max_cells = 0, max_slots = 0, max_blob = 0;
   int64_t ndiag = 0;
   DevBuf<int32_t> tiles; // 16 ints per tile (etile.cu)
@@ -41,7 +41,7 @@ struct EtilePlan {
   // lane-interleaved pair records, cell vertex slots (u16)
   DevBuf<uint8_t> blob;
   DevBuf<int32_t> runs;  // coordinate-window runs [lo, hi)
-  DevBuf<int32_t> diag;  // diagonal positions of the vertex rows (zeroed before the REDs)
+  DevBuf<int32_t> diag;  // diagonal positions of the vertex rows (+ dof row length when cd = 2)
   uint32_t ktab[12] = {};
 };
 
@@ -57,9 +57,14 @@ struct EtileSpec {
 // nnz < 2^31) or a tile limit cannot be met; the caller then uses another plan.
 bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nrows_node,
                  const int32_t* sorted_rows, const int32_t* sorted_x, int nverts, const PairPlan& pp,
-                 const int64_t* row_ptr, int64_t nnz, cudaStream_t s);
+                 const int64_t* row_ptr, int64_t nnz, int cd, cudaStream_t s);
 
-// One assembly through the plan (form: F_MASS / F_STIFFNESS / F_HELMHOLTZ).
+// cd = 2: the Mat is the component-diagonal 2-vector expansion of the scalar
+// form (Taylor-Hood velocity block nu grad u : grad v, elements.cuh F_STOKES_A):
+// dof entry (2i+d, 2j+c) = delta_dc K_ij on a 2x2-blocked pattern.
+//
+// One assembly through the plan (form: F_MASS / F_STIFFNESS / F_HELMHOLTZ /
+// F_STOKES_A).
 void launch_etile(int form, const EtilePlan& p, const double* coords, double* out, const FormParams& prm,
                   bool accumulate, int* next_tile, int* reset_tile, cudaStream_t s);
 

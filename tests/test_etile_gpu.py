@@ -89,3 +89,25 @@ def test_renumbered_nodes_fall_back(gpu_lib, gdim, n):
     A.zero()
     assert launches(L, loop) == 1
     assert rel(A.host_values(), ref) <= TOL
+
+
+@pytest.mark.parametrize("n", [1, 3, 8])
+def test_stokes_velocity_block_edge_tiles(gpu_lib, n):
+    """Config 5's A block (nu grad u : grad v on vector P2, 2x2 component-diagonal
+    blocks) through the edge tiles: values and the explicit structural zeros."""
+    capi.set_strategy("auto")
+    w = configs.Workload(5, n)
+    w.reset()
+    w.run()
+    w.reset()
+    l0 = capi.launch_count()
+    w.L.execute(w.loops[0])
+    assert capi.launch_count() - l0 == 2, "edge-tile path not taken for the Stokes A block"
+    m = w.inputs
+    dm = w.vdm.values
+    A = w.outputs[0]
+    rp, ci = A.sparsity.host()
+    ref = O.assemble_matrix(O.STOKES_A, 2, 2, m.ncells, dm, 12, dm, 12, m.cv, m.coords, rp, ci, params=(configs.NU,))
+    assert rel(A.host_values(), ref) <= TOL
+    w.L.execute(w.loops[0])  # accumulate
+    assert rel(A.host_values(), 2 * ref) <= TOL
