@@ -179,6 +179,31 @@ def time_steps(torch, w, steps, flush, stream):
     return times
 
 
+def protocol_floor(torch, flush, stream, reps=10):
+    """What the per-step protocol (flush, event, launch, event) charges a
+    trivial kernel and a 100 MB streaming read (torch.sum) on this box: the
+    fixed event + launch cost inside every timed step, and the streaming
+    floor C2's 100.7 algorithmic MB compare against."""
+    o = torch.zeros(1, dtype=torch.float64, device="cuda")
+    a = torch.ones(100_000_000 // 8, dtype=torch.float64, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def t(fn):
+        ts = []
+        for _ in range(reps):
+            flush()
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts[2:]))
+    out = {"empty_kernel_ms": t(lambda: o.fill_(1.0)),
+           "stream_read_100MB_ms": t(lambda: torch.sum(a, dim=0, out=o[0]))}
+    del a
+    return out
+
+
 def e2e_host(torch, w, steps, warmup):
     """The same assembly through loam_gpu_execute_host (loam.HostLoop) with
     pinned host buffers: every step copies the Dats the loop reads host->device
@@ -322,6 +347,7 @@ def gpu_arm(args):
     if os.environ.get("LOAM_BENCH_DEBUG"):
         print("e2e step ms:", [round(t, 3) for t in e2e_times], file=sys.stderr)
     e2e_ms = max_over_ranks(float(np.mean(e2e_times)), "cuda")
+    floor = protocol_floor(torch, flush, stream)
     # correctness spot check of this very run against the reference pattern size
     line = None
     if rank == 0:
@@ -348,7 +374,8 @@ def gpu_arm(args):
                     "d2h_bytes_per_step": d2h},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic("c2_matrix"),
-                         "algorithmic_bytes": abytes, "kernel_ms": kernel_ms, "peak_kind": peak_kind},
+                         "algorithmic_bytes": abytes, "kernel_ms": kernel_ms, "peak_kind": peak_kind,
+                         "protocol_floor": floor},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),

@@ -29,6 +29,7 @@
 #include "elements.cuh"
 #include "engine.cuh"
 #include "etile.cuh"
+#include "ntile.cuh"
 #include "patch.cuh"
 #include "patch_kernels.cuh"
 #include "plan.cuh"
@@ -951,12 +952,30 @@ __device__ __forceinline__ double star_row(const StarArgs& a, int r, int4 h, int
   return acc;
 }
 
-template <class F>
+// RPT rows per thread (r, r + stride, ...): their independent record ->
+// neighbour gather chains overlap, and the grid fits in one wave (one wave of
+// 256-thread blocks at 48 registers holds 740 blocks; C1 has 263,169 rows).
+template <class F, int RPT>
 __global__ void __launch_bounds__(256) k_star_vec(const __grid_constant__ StarArgs a) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= a.nrows) return;
-  const double y = star_row<F>(a, r, __ldg(a.star + 2 * r), __ldg(a.star + 2 * r + 1));
-  a.out[r] = a.accumulate ? a.out[r] + y : y;
+  const int r0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride = gridDim.x * blockDim.x;
+  int4 h[RPT], t[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int r = r0 + q * stride;
+    if (r < a.nrows) {
+      h[q] = __ldg(a.star + 2 * r);
+      t[q] = __ldg(a.star + 2 * r + 1);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int r = r0 + q * stride;
+    if (r < a.nrows) {
+      const double y = star_row<F>(a, r, h[q], t[q]);
+      a.out[r] = a.accumulate ? a.out[r] + y : y;
+    }
+  }
 }
 
 // Bilinear P1 triangle forms (config 2 shape): the row's CSR segment is
@@ -1023,7 +1042,12 @@ template <class F>
 void launch_star(const StarArgs& a, cudaStream_t s) {
   if (a.nrows == 0) return;
   if constexpr (F::BILINEAR) k_star_mat<F><<<ceil_div(a.nrows, 256), 256, 0, s>>>(a);
-  else k_star_vec<F><<<ceil_div(a.nrows, 256), 256, 0, s>>>(a);
+  else {
+    static const int rpt = std::getenv("LOAM_GPU_STAR_RPT") ? std::atoi(std::getenv("LOAM_GPU_STAR_RPT")) : 1;
+    if (rpt >= 4) k_star_vec<F, 4><<<ceil_div(a.nrows, 256 * 4), 256, 0, s>>>(a);
+    else if (rpt == 2) k_star_vec<F, 2><<<ceil_div(a.nrows, 256 * 2), 256, 0, s>>>(a);
+    else k_star_vec<F, 1><<<ceil_div(a.nrows, 256), 256, 0, s>>>(a);
+  }
   count_launch();
   LG_LAUNCH_CHECK();
 }
@@ -2022,6 +2046,8 @@ struct FastPlan {
   PTilePlan pt;
   bool use_etile = false;  // edge tiles (scalar P2 matrices, etile.cuh)
   EtilePlan et;
+  bool use_ntile = false;  // node-block tiles (vector P1 elasticity, ntile.cuh)
+  NtilePlan nt;
   bool use_star = false;   // vertex-star kernel (P1 triangle actions)
   DevBuf<int4> star;
   bool use_patch = false;  // cell-patch row-owner kernels (patch.cuh)
@@ -2273,6 +2299,21 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       if (build_etile(P->et, es, k.gd, n, R.v.target, srows.v.get(), sx.v.get(), X->target_size, P->pp,
                       sp->row_ptr, sp->nnz, k.rd, s)) {
         P->use_etile = true;
+        return P;
+      }
+    }
+    // node-block tiles: vector P1 elasticity on its (map, map) 3x3-blocked pattern
+    if (strat == 0 && k.form == F_ELASTICITY && !std::getenv("LOAM_GPU_NO_NTILE") && R.dim == 3 && Cn.dim == 3 &&
+        (reinterpret_cast<uintptr_t>(args[1].data) & 15) == 0 && Cn.v.arity == R.v.arity &&
+        (Cn.v.v == R.v.v || prefix_equal(Cn.v.v, Cn.v.arity, R.v.v, R.v.arity, R.v.arity, n, s))) {
+      SortedMap sx;
+      gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, sx, s);
+      NtileSpec ns;
+      ns.tile_nodes = env_int("LOAM_GPU_NT_NODES", ns.tile_nodes);
+      ns.tile_items = env_int("LOAM_GPU_NT_ITEMS", ns.tile_items);
+      if (build_ntile(P->nt, ns, n, R.v.target, srows.v.get(), sx.v.get(), X->target_size, P->pp, sp->row_ptr,
+                      sp->nnz, s)) {
+        P->use_ntile = true;
         return P;
       }
     }
@@ -2529,6 +2570,12 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
       fprintf(stderr, "[ring timing] CTA starts span %.2f us, CTA ends from %.2f to %.2f us after the first start\n",
               (double)(h[11] - h[8]) * 1e-3, (double)(h[12] - h[8]) * 1e-3, (double)(h[9] - h[8]) * 1e-3);
     }
+    return;
+  }
+  if (P->use_ntile) {
+    launch_ntile(P->nt, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
+                 P->counter.get() + P->parity, P->counter.get() + (P->parity ^ 1), s);
+    P->parity ^= 1;
     return;
   }
   if (P->use_etile) {

@@ -1,0 +1,494 @@
+// ntile.cu -- node-block tiles for vector P1 matrices (see ntile.cuh).
+//
+// Reference path replaced: assemble_matrix (fem/assemble.hpp:85-104) ->
+// execute (parloop.hpp:191-384) with a dof-expanded map and the
+// linear-elasticity element kernel (restated in elements.cuh FormT<F_ELASTICITY>),
+// Mat::addto (data.hpp:205-222) on the 3x3-blocked pattern of
+// build_sparsity(map, map, 3, 3) (data.hpp:149-179).
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "async.cuh"
+#include "ntile.cuh"
+#include "stage.cuh"
+
+namespace loam_gpu {
+
+namespace {
+
+inline int up16(int x) { return (x + 15) & ~15; }
+
+int make_runs(std::vector<int>& ids, int limit, std::vector<std::pair<int, int>>& rr) {
+  constexpr int kGap = 8;
+  std::sort(ids.begin(), ids.end());
+  ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+  rr.clear();
+  int slots = 0;
+  for (int v : ids) {
+    const int lo = v & ~1, hi = std::min(limit, (v + 2) & ~1);
+    if (!rr.empty() && lo <= rr.back().second + kGap) rr.back().second = std::max(rr.back().second, hi);
+    else rr.emplace_back(lo, hi);
+  }
+  for (auto& x : rr) slots += x.second - x.first;
+  return slots;
+}
+
+constexpr int kNV = 4;        // P1 tet
+#ifndef LOAM_GPU_NT_SPLIT
+#define LOAM_GPU_NT_SPLIT 4
+#endif
+constexpr int kDiagSplit = LOAM_GPU_NT_SPLIT; // threads per diagonal block (its 24 cells in chunks)
+
+} // namespace
+
+bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, const int32_t* sorted_rows,
+                 const int32_t* sorted_x, int nverts, const PairPlan& pp, const int64_t* row_ptr, int64_t nnz,
+                 cudaStream_t s) {
+  if (pp.nrn != kNV || pp.ncn != kNV || nnz >= (int64_t(1) << 31) || ncells == 0) return false;
+  const int64_t np = pp.npairs;
+  std::vector<int32_t> hrows((size_t)ncells * kNV), hx((size_t)ncells * kNV), hpairs(np), hp(nnodes + 1);
+  std::vector<uint8_t> hrank((size_t)np * kNV);
+  std::vector<int64_t> hrp((size_t)nnodes * 3 + 1);
+  LG_CUDA(cudaMemcpyAsync(hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size(), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hx.data(), sorted_x, sizeof(int32_t) * hx.size(), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hpairs.data(), pp.pairs.get(), sizeof(int32_t) * np, cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hp.data(), pp.ptr.get(), sizeof(int32_t) * (nnodes + 1), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hrank.data(), pp.ranks.get(), hrank.size(), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(hrp.data(), row_ptr, sizeof(int64_t) * hrp.size(), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int64_t> nptr(nnodes + 1); // node-level pattern offsets of the 3x3-blocked CSR
+  for (int i = 0; i <= nnodes; ++i) nptr[i] = hrp[(size_t)3 * i] / 9;
+  // every pattern block of every row must be reached by some cell (exact (map, map) pattern)
+  {
+    std::vector<uint8_t> seen;
+    for (int v = 0; v < nnodes; ++v) {
+      const int L = (int)(nptr[v + 1] - nptr[v]);
+      seen.assign(L, 0);
+      for (int p = hp[v]; p < hp[v + 1]; ++p)
+        for (int j = 0; j < kNV; ++j) {
+          const int r = hrank[(size_t)p * kNV + j];
+          if (r >= L) return false;
+          seen[r] = 1;
+        }
+      for (int r = 0; r < L; ++r)
+        if (!seen[r]) return false;
+    }
+  }
+  struct ItemRec { // 8 bytes
+    uint16_t poff;
+    uint8_t np, kind;
+    uint16_t base, stride;
+  };
+  static_assert(sizeof(ItemRec) == 8, "item record");
+  std::vector<int32_t> tiles, runs;
+  std::vector<uint8_t> blob;
+  std::vector<int> stamp(ncells, -1), local(ncells, 0), vid;
+  std::vector<std::pair<int, int>> rr;
+  std::vector<std::vector<uint32_t>> lists; // per rank of a row: (cell << 4 | lv << 2 | lw)
+  std::vector<ItemRec> items;
+  std::vector<uint16_t> prec, diaginfo;
+  int gen = 0, v0 = 0;
+  while (v0 < nnodes) {
+    int v1 = std::min(nnodes, v0 + sp.tile_nodes);
+    std::vector<int> cells;
+    int slots = 0;
+    auto fits = [&](int a, int b) {
+      if (9 * (nptr[b] - nptr[a]) > 60000) return false;
+      int nit = 0, npr = 0;
+      for (int v = a; v < b; ++v) {
+        nit += (int)(nptr[v + 1] - nptr[v]) - 1 + kDiagSplit;
+        npr += 4 * (hp[v + 1] - hp[v]);
+      }
+      if (nit > sp.tile_items || npr > sp.tile_pairs) return false;
+      ++gen;
+      cells.clear();
+      for (int p = hp[a]; p < hp[b]; ++p) {
+        const int c = hpairs[p] / kNV;
+        if (stamp[c] != gen) {
+          stamp[c] = gen;
+          cells.push_back(c);
+        }
+      }
+      if ((int)cells.size() > std::min(sp.tile_cells, 1023)) return false;
+      vid.clear();
+      for (int c : cells)
+        for (int v = 0; v < kNV; ++v) vid.push_back(hx[(size_t)c * kNV + v]);
+      slots = make_runs(vid, nverts, rr);
+      return slots <= sp.tile_slots && (int)rr.size() <= sp.tile_runs;
+    };
+    while (!fits(v0, v1)) {
+      if (v1 == v0 + 1) return false;
+      v1 = v0 + (v1 - v0) / 2;
+    }
+    std::sort(cells.begin(), cells.end());
+    for (size_t q = 0; q < cells.size(); ++q) local[cells[q]] = (int)q;
+    std::vector<int> base(rr.size());
+    for (size_t q = 0, acc = 0; q < rr.size(); ++q) {
+      base[q] = (int)acc;
+      acc += rr[q].second - rr[q].first;
+    }
+    auto slot_in = [&](int v) {
+      size_t q = std::upper_bound(rr.begin(), rr.end(), std::make_pair(v, INT32_MAX)) - rr.begin() - 1;
+      return base[q] + v - rr[q].first;
+    };
+    // items: off-diagonal blocks of every row first, then the diagonal blocks in kDiagSplit parts
+    items.clear();
+    prec.clear();
+    diaginfo.clear();
+    std::vector<ItemRec> ditems;
+    std::vector<uint16_t> dprec;
+    const int64_t S0 = nptr[v0];
+    for (int v = v0; v < v1; ++v) {
+      const int L = (int)(nptr[v + 1] - nptr[v]);
+      lists.assign(L, {});
+      int self = -1;
+      for (int p = hp[v]; p < hp[v + 1]; ++p) {
+        const int c = hpairs[p] / kNV, lv = hpairs[p] % kNV;
+        for (int lw = 0; lw < kNV; ++lw) {
+          const int r = hrank[(size_t)p * kNV + lw];
+          lists[r].push_back((uint32_t)local[c] << 4 | (uint32_t)lv << 2 | (uint32_t)lw);
+          if (lw == lv) self = r;
+        }
+      }
+      const uint16_t rowb = (uint16_t)(9 * (nptr[v] - S0)), stride = (uint16_t)(3 * L);
+      for (int r = 0; r < L; ++r) {
+        if (r == self) continue;
+        items.push_back(ItemRec{(uint16_t)prec.size(), (uint8_t)lists[r].size(), 0, (uint16_t)(rowb + 3 * r), stride});
+        for (uint32_t x : lists[r]) prec.push_back((uint16_t)x);
+        if (lists[r].size() > 255) return false;
+      }
+      const int di = (int)diaginfo.size() / 2;
+      diaginfo.push_back((uint16_t)(rowb + 3 * self));
+      diaginfo.push_back(stride);
+      const auto& dl = lists[self];
+      const int n = (int)dl.size();
+      for (int part = 0; part < kDiagSplit; ++part) {
+        const int a = n * part / kDiagSplit, b = n * (part + 1) / kDiagSplit;
+        ditems.push_back(ItemRec{(uint16_t)dprec.size(), (uint8_t)(b - a), 1, (uint16_t)(di * kDiagSplit + part), 0});
+        for (int q = a; q < b; ++q) dprec.push_back((uint16_t)dl[q]);
+      }
+    }
+    for (auto it : ditems) {
+      it.poff = (uint16_t)(it.poff + prec.size());
+      items.push_back(it);
+    }
+    prec.insert(prec.end(), dprec.begin(), dprec.end());
+    const int nitems = (int)items.size(), npairs = (int)prec.size(), ncell = (int)cells.size(),
+              ndiag = (int)diaginfo.size() / 2;
+    const int off_items = 0, off_pairs = up16(nitems * 8), off_diag = off_pairs + up16(npairs * 2),
+              off_cells = off_diag + up16(ndiag * 4), bytes = off_cells + up16(ncell * kNV * 2);
+    const size_t b0 = blob.size();
+    blob.resize(b0 + bytes, 0);
+    uint8_t* bp = blob.data() + b0;
+    memcpy(bp + off_items, items.data(), (size_t)nitems * 8);
+    memcpy(bp + off_pairs, prec.data(), (size_t)npairs * 2);
+    memcpy(bp + off_diag, diaginfo.data(), (size_t)ndiag * 4);
+    for (int q = 0; q < ncell; ++q)
+      for (int v = 0; v < kNV; ++v) {
+        const uint16_t sl = (uint16_t)slot_in(hx[(size_t)cells[q] * kNV + v]);
+        memcpy(bp + off_cells + 2 * (q * kNV + v), &sl, 2);
+      }
+    const int seg = (int)(9 * (nptr[v1] - nptr[v0]));
+    tiles.insert(tiles.end(), {(int)(b0 / 16), bytes, v0, v1 - v0, (int)(9 * nptr[v0]), seg, nitems, ncell,
+                               (int)runs.size() / 2, (int)rr.size(), off_items, off_pairs, off_cells, off_diag, ndiag,
+                               0});
+    for (auto& x : rr) runs.insert(runs.end(), {x.first, x.second});
+    out.max_seg = std::max(out.max_seg, seg);
+    out.max_cells = std::max(out.max_cells, ncell);
+    out.max_slots = std::max(out.max_slots, slots);
+    out.max_blob = std::max(out.max_blob, bytes);
+    out.max_diag = std::max(out.max_diag, ndiag);
+    v0 = v1;
+  }
+  out.ntiles = (int)tiles.size() / 16;
+  auto upload = [&](auto& dst, const auto& src) {
+    using T = typename std::decay_t<decltype(src)>::value_type;
+    dst.alloc(src.size() + 16, s);
+    if (!src.empty())
+      LG_CUDA(cudaMemcpyAsync(dst.get(), src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, s));
+  };
+  upload(out.tiles, tiles);
+  upload(out.blob, blob);
+  upload(out.runs, runs);
+  LG_CUDA(cudaStreamSynchronize(s));
+  return true;
+}
+
+// ===========================================================================
+// Device side
+// ===========================================================================
+
+namespace {
+
+struct NtileArgs {
+  const int32_t* tiles;
+  int ntiles;
+  int* next_tile;
+  int* reset_tile;
+  const uint8_t* blob;
+  const int32_t* runs;
+  const double* coords;
+  double* out;
+  FormParams prm;
+  int accumulate;
+  int off_seg, off_geo, off_part, off_buf, buf_bytes, b_win;
+};
+
+__device__ __forceinline__ void nt_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(20000)
+      : "memory");
+}
+
+constexpr int kNtThreads = 128;
+constexpr int kGS = 18; // doubles per cell: 4 x (g_k, V) + 2 pad (odd stride in 16-byte units)
+
+template <int STAGES>
+__global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_constant__ NtileArgs a) {
+  constexpr int NT = kNtThreads;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + STAGES;
+  int* slot_tile = reinterpret_cast<int*>(sm + 48);
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0 && tid == 0) *a.reset_tile = 0;
+  if (tid == 0) {
+    for (int q = 0; q < STAGES; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], NT / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto ring = [&](int k) { return sm + a.off_buf + (k % STAGES) * a.buf_bytes; };
+  auto meta = [&](int tile, int (&m)[16]) {
+    const int4* t = reinterpret_cast<const int4*>(a.tiles + 16 * tile);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 x = __ldg(t + q);
+      m[4 * q] = x.x;
+      m[4 * q + 1] = x.y;
+      m[4 * q + 2] = x.z;
+      m[4 * q + 3] = x.w;
+    }
+  };
+  if (tid >= NT) { // ---- producer warp
+    const int lane = tid & 31;
+    auto grab = [&]() {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(a.next_tile, 1);
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    int nt = grab();
+    int nm[16];
+    int2 nrun = make_int2(0, 0);
+    auto prefetch = [&]() {
+      if (nt < a.ntiles) {
+        meta(nt, nm);
+        nrun = first_run(reinterpret_cast<const int2*>(a.runs) + nm[8], nm[9], lane);
+      }
+    };
+    prefetch();
+    for (int k = 0;; ++k) {
+      const int tile = nt;
+      int m[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) m[q] = nm[q];
+      const int2 run0 = nrun;
+      if (k >= STAGES) mbar_wait(&empty[k % STAGES], (k / STAGES - 1) & 1);
+      if (tile >= a.ntiles) {
+        if (lane == 0) {
+          slot_tile[k % STAGES] = -1;
+          mbar_arrive(&full[k % STAGES]);
+        }
+        break;
+      }
+      if (lane == 0) slot_tile[k % STAGES] = tile;
+      unsigned char* buf = ring(k);
+      uint64_t* bar = &full[k % STAGES];
+      const RunSet rc{reinterpret_cast<const int2*>(a.runs) + m[8], m[9], a.coords,
+                      reinterpret_cast<double*>(buf + a.b_win), 3};
+      const uint32_t tx = (uint32_t)m[1] + stage_runs<false>(rc, lane, bar, run0);
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(bar, tx);
+        bulk_g2s(buf, a.blob + (int64_t)m[0] * 16, (uint32_t)m[1], bar);
+      }
+      __syncwarp();
+      stage_runs<true>(rc, lane, bar, run0);
+      nt = grab();
+      prefetch();
+    }
+    return;
+  }
+  // ---- consumers
+  double* seg0 = reinterpret_cast<double*>(sm + a.off_seg);
+  double* geo = reinterpret_cast<double*>(sm + a.off_geo);
+  double* part = reinterpret_cast<double*>(sm + a.off_part);
+  const double lam = a.prm.p[0], mu = a.prm.p[1];
+  for (int k = 0;; ++k) {
+    nt_wait(&full[k % STAGES], (k / STAGES) & 1);
+    const int tile = slot_tile[k % STAGES];
+    if (tile < 0) break;
+    int m[16];
+    meta(tile, m);
+    const int E0 = m[4], len = m[5], nitems = m[6], ncell = m[7], ndiag = m[14];
+    const unsigned char* buf = ring(k);
+    const uint2* items = reinterpret_cast<const uint2*>(buf + m[10]);
+    const uint16_t* prec = reinterpret_cast<const uint16_t*>(buf + m[11]);
+    const uint16_t* cslot = reinterpret_cast<const uint16_t*>(buf + m[12]);
+    const uint16_t* dinfo = reinterpret_cast<const uint16_t*>(buf + m[13]);
+    const double* win = reinterpret_cast<const double*>(buf + a.b_win);
+    double* seg = seg0 + (E0 & 1); // 16-byte parity of the global destination (bulk store)
+    if (tid == 0) bulk_wait_read<0>(); // the previous tile's store has read the segment
+    // phase 1: barycentric gradients and measure of every cell of the tile, once
+    for (int c = tid; c < ncell; c += NT) {
+      double X[4][3];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int sl = cslot[c * 4 + v];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) X[v][q] = win[sl * 3 + q];
+      }
+      Geom<3> Gm;
+      geometry<3>(X, Gm);
+      double2* g = reinterpret_cast<double2*>(geo + c * kGS);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        g[2 * v] = make_double2(Gm.g[v][0], Gm.g[v][1]);
+        g[2 * v + 1] = make_double2(Gm.g[v][2], Gm.V);
+      }
+    }
+    named_bar(1, NT);
+    // phase 2: one thread per 3x3 node block (diagonal blocks: kDiagSplit threads)
+    for (int it = tid; it < nitems; it += NT) {
+      const uint2 ir = items[it];
+      const int poff = ir.x & 0xffff, np = (ir.x >> 16) & 0xff, kind = ir.x >> 24;
+      const int base = ir.y & 0xffff, stride = ir.y >> 16;
+      double acc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+      for (int q = 0; q < np; ++q) {
+        const uint32_t x = prec[poff + q];
+        const double2* g = reinterpret_cast<const double2*>(geo + (x >> 4) * kGS);
+        const int lv = (x >> 2) & 3, lw = x & 3;
+        const double2 a0 = g[2 * lv], a1 = g[2 * lv + 1], b0 = g[2 * lw], b1 = g[2 * lw + 1];
+        const double ga[3] = {a0.x, a0.y, a1.x}, gb[3] = {b0.x, b0.y, b1.x};
+        const double V = a1.y;
+        // FormT<F_ELASTICITY>::row: V (mu g_a[e] g_b[d] + lam g_a[d] g_b[e] + d_de mu g_a.g_b)
+        double mga[3], lga[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          mga[d] = mu * ga[d];
+          lga[d] = lam * ga[d];
+        }
+        const double gg = mu * (ga[0] * gb[0] + ga[1] * gb[1] + ga[2] * gb[2]);
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int e = 0; e < 3; ++e) {
+            double v = fma(mga[e], gb[d], lga[d] * gb[e]);
+            if (d == e) v += gg;
+            acc[d][e] = fma(V, v, acc[d][e]);
+          }
+      }
+      if (kind == 0) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int e = 0; e < 3; ++e) seg[base + d * stride + e] = acc[d][e];
+      } else {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int e = 0; e < 3; ++e) part[base * 9 + d * 3 + e] = acc[d][e];
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[k % STAGES]);
+    named_bar(1, NT);
+    // diagonal blocks: the kDiagSplit partial sums, in a fixed order
+    for (int t = tid; t < ndiag * 9; t += NT) {
+      const int di = t / 9, q = t - 9 * di;
+      double v = part[(di * kDiagSplit) * 9 + q];
+#pragma unroll
+      for (int s = 1; s < kDiagSplit; ++s) v += part[(di * kDiagSplit + s) * 9 + q];
+      const int b = dinfo[2 * di], stride = dinfo[2 * di + 1];
+      seg[b + (q / 3) * stride + q % 3] = v;
+    }
+    if (a.accumulate) {
+      named_bar(1, NT);
+      for (int t = tid; t < len; t += NT) a.out[(int64_t)E0 + t] += seg[t];
+      named_bar(1, NT);
+    } else {
+      fence_async_shared();
+      named_bar(1, NT);
+      if (tid == 0) {
+        double* dst = a.out + E0;
+        const int h = E0 & 1, t1 = len - ((E0 + len) & 1);
+        if (h && len > 0) dst[0] = seg[0];
+        if (t1 > h) {
+          bulk_s2g(dst + h, seg + h, (uint32_t)(t1 - h) * 8);
+          bulk_commit();
+        }
+        if (t1 < len && t1 >= h) dst[t1] = seg[t1];
+      }
+    }
+  }
+  if (tid == 0) bulk_wait_read<0>();
+}
+
+} // namespace
+
+void launch_ntile(const NtilePlan& p, const double* coords, double* out, const FormParams& prm, bool accumulate,
+                  int* next_tile, int* reset_tile, cudaStream_t s) {
+  if (p.ntiles == 0) return;
+  NtileArgs a{};
+  a.tiles = p.tiles.get();
+  a.ntiles = p.ntiles;
+  a.next_tile = next_tile;
+  a.reset_tile = reset_tile;
+  a.blob = p.blob.get();
+  a.runs = p.runs.get();
+  a.coords = coords;
+  a.out = out;
+  a.prm = prm;
+  a.accumulate = accumulate ? 1 : 0;
+  int off = 128;
+  a.off_seg = off;
+  off += up16((p.max_seg + 2) * 8);
+  a.off_geo = off;
+  off += up16(p.max_cells * kGS * 8);
+  a.off_part = off;
+  off += up16(p.max_diag * kDiagSplit * 9 * 8);
+  a.off_buf = off;
+  a.b_win = up16(p.max_blob);
+  a.buf_bytes = a.b_win + up16(p.max_slots * 3 * 8 + 16);
+  static const int st = std::getenv("LOAM_GPU_NT_STAGES") ? std::atoi(std::getenv("LOAM_GPU_NT_STAGES")) : 2;
+  auto go = [&](auto kern, int stages) {
+    const size_t smem = (size_t)off + stages * (size_t)a.buf_bytes;
+    static size_t attr = 0;
+    if (attr < smem) {
+      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    int blocks = 1;
+    LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kNtThreads + 32, smem));
+    require(blocks > 0, LOAM_GPU_ERR_CUDA, "node-tile kernel does not fit on an SM");
+    kern<<<std::min(p.ntiles, blocks * kNumSMs), kNtThreads + 32, smem, s>>>(a);
+  };
+  if (st >= 2) go(k_ntile<2>, 2);
+  else go(k_ntile<1>, 1);
+  count_launch();
+  LG_LAUNCH_CHECK();
+}
+
+} // namespace loam_gpu

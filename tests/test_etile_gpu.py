@@ -111,3 +111,25 @@ def test_stokes_velocity_block_edge_tiles(gpu_lib, n):
     assert rel(A.host_values(), ref) <= TOL
     w.L.execute(w.loops[0])  # accumulate
     assert rel(A.host_values(), 2 * ref) <= TOL
+
+
+@pytest.mark.parametrize("n", [1, 3, 6])
+def test_elasticity_node_block_tiles(gpu_lib, n):
+    """Config 4 (vector P1 elasticity, 3x3-blocked CSR) through the node-block
+    tiles (csrc/ntile.cu): one launch, values vs the oracle, accumulation."""
+    capi.set_strategy("auto")
+    w = configs.Workload(4, n)
+    w.reset()
+    w.run()
+    w.reset()
+    l0 = capi.launch_count()
+    w.run()
+    assert capi.launch_count() - l0 == 1, "node-block tile path not taken"
+    m = w.inputs
+    dm = w.dof_map.values
+    A = w.outputs[0]
+    rp, ci = A.sparsity.host()
+    ref = O.assemble_matrix(O.ELASTICITY, 1, 3, m.ncells, dm, 12, dm, 12, m.cv, m.coords, rp, ci, params=configs.LAME)
+    assert rel(A.host_values(), ref) <= TOL
+    w.run()  # accumulate
+    assert rel(A.host_values(), 2 * ref) <= TOL
