@@ -233,7 +233,7 @@ struct NtileArgs {
   const double* coords;
   double* out;
   FormParams prm;
-  int accumulate;
+  int accumulate, dynamic;
   int off_seg, off_geo, off_part, off_buf, buf_bytes, b_win;
 };
 
@@ -283,7 +283,9 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
   };
   if (tid >= NT) { // ---- producer warp
     const int lane = tid & 31;
+    int sched = 0; // static round-robin (uniform tiles) unless a.dynamic
     auto grab = [&]() {
+      if (!a.dynamic) return (int)blockIdx.x + (sched++) * (int)gridDim.x;
       int t = 0;
       if (lane == 0) t = atomicAdd(a.next_tile, 1);
       return __shfl_sync(0xffffffffu, t, 0);
@@ -362,11 +364,13 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
       }
       Geom<3> Gm;
       geometry<3>(X, Gm);
+      // sqrt(V) g_k: a node block sums V g_a g_b^T = (sqrt(V) g_a)(sqrt(V) g_b)^T over its cells
+      const double sv = sqrt(Gm.V);
       double2* g = reinterpret_cast<double2*>(geo + c * kGS);
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        g[2 * v] = make_double2(Gm.g[v][0], Gm.g[v][1]);
-        g[2 * v + 1] = make_double2(Gm.g[v][2], Gm.V);
+        g[2 * v] = make_double2(sv * Gm.g[v][0], sv * Gm.g[v][1]);
+        g[2 * v + 1] = make_double2(sv * Gm.g[v][2], 0.0);
       }
     }
     named_bar(1, NT);
@@ -375,36 +379,32 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
       const uint2 ir = items[it];
       const int poff = ir.x & 0xffff, np = (ir.x >> 16) & 0xff, kind = ir.x >> 24;
       const int base = ir.y & 0xffff, stride = ir.y >> 16;
+      // S = sum over the block's cells of V g_a g_b^T (9 FMAs per cell); the
+      // element block of FormT<F_ELASTICITY>::row is linear in it:
+      //   A_de = mu S_ed + lam S_de + d_de mu tr(S)
       double acc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
       for (int q = 0; q < np; ++q) {
         const uint32_t x = prec[poff + q];
-        const double2* g = reinterpret_cast<const double2*>(geo + (x >> 4) * kGS);
+        const double* g = geo + (x >> 4) * kGS;
         const int lv = (x >> 2) & 3, lw = x & 3;
-        const double2 a0 = g[2 * lv], a1 = g[2 * lv + 1], b0 = g[2 * lw], b1 = g[2 * lw + 1];
-        const double ga[3] = {a0.x, a0.y, a1.x}, gb[3] = {b0.x, b0.y, b1.x};
-        const double V = a1.y;
-        // FormT<F_ELASTICITY>::row: V (mu g_a[e] g_b[d] + lam g_a[d] g_b[e] + d_de mu g_a.g_b)
-        double mga[3], lga[3];
+        const double2 a0 = reinterpret_cast<const double2*>(g + 4 * lv)[0], b0 = reinterpret_cast<const double2*>(g + 4 * lw)[0];
+        const double a2 = g[4 * lv + 2], b2 = g[4 * lw + 2];
+        const double ga[3] = {a0.x, a0.y, a2}, gb[3] = {b0.x, b0.y, b2};
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          mga[d] = mu * ga[d];
-          lga[d] = lam * ga[d];
-        }
-        const double gg = mu * (ga[0] * gb[0] + ga[1] * gb[1] + ga[2] * gb[2]);
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int e = 0; e < 3; ++e) acc[d][e] = fma(ga[d], gb[e], acc[d][e]);
+      }
+      if (kind == 0) {
+        const double tr = mu * (acc[0][0] + acc[1][1] + acc[2][2]);
 #pragma unroll
         for (int d = 0; d < 3; ++d)
 #pragma unroll
           for (int e = 0; e < 3; ++e) {
-            double v = fma(mga[e], gb[d], lga[d] * gb[e]);
-            if (d == e) v += gg;
-            acc[d][e] = fma(V, v, acc[d][e]);
+            double v = fma(mu, acc[e][d], lam * acc[d][e]);
+            if (d == e) v += tr;
+            seg[base + d * stride + e] = v;
           }
-      }
-      if (kind == 0) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-#pragma unroll
-          for (int e = 0; e < 3; ++e) seg[base + d * stride + e] = acc[d][e];
       } else {
 #pragma unroll
         for (int d = 0; d < 3; ++d)
@@ -417,12 +417,17 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
     named_bar(1, NT);
     // diagonal blocks: the kDiagSplit partial sums, in a fixed order
     for (int t = tid; t < ndiag * 9; t += NT) {
-      const int di = t / 9, q = t - 9 * di;
-      double v = part[(di * kDiagSplit) * 9 + q];
+      const int di = t / 9, q = t - 9 * di, d = q / 3, e = q - 3 * d;
+      auto S = [&](int x, int y) {
+        double v = part[(di * kDiagSplit) * 9 + 3 * x + y];
 #pragma unroll
-      for (int s = 1; s < kDiagSplit; ++s) v += part[(di * kDiagSplit + s) * 9 + q];
+        for (int s = 1; s < kDiagSplit; ++s) v += part[(di * kDiagSplit + s) * 9 + 3 * x + y];
+        return v;
+      };
+      double v = fma(mu, S(e, d), lam * S(d, e));
+      if (d == e) v += mu * (S(0, 0) + S(1, 1) + S(2, 2));
       const int b = dinfo[2 * di], stride = dinfo[2 * di + 1];
-      seg[b + (q / 3) * stride + q % 3] = v;
+      seg[b + d * stride + e] = v;
     }
     if (a.accumulate) {
       named_bar(1, NT);
@@ -485,7 +490,9 @@ void launch_ntile(const NtilePlan& p, const double* coords, double* out, const F
     require(blocks > 0, LOAM_GPU_ERR_CUDA, "node-tile kernel does not fit on an SM");
     kern<<<std::min(p.ntiles, blocks * kNumSMs), kNtThreads + 32, smem, s>>>(a);
   };
-  if (st >= 2) go(k_ntile<2>, 2);
+  a.dynamic = std::getenv("LOAM_GPU_NT_STATIC") ? 0 : 1;
+  if (st >= 3) go(k_ntile<3>, 3);
+  else if (st == 2) go(k_ntile<2>, 2);
   else go(k_ntile<1>, 1);
   count_launch();
   LG_LAUNCH_CHECK();

@@ -28,7 +28,7 @@ struct NtilePlan {
 };
 
 struct NtileSpec {
-  int tile_nodes = 8, tile_items = 512, tile_pairs = 4096, tile_cells = 1023, tile_slots = 1024, tile_runs = 32;
+  int tile_nodes = 12, tile_items = 512, tile_pairs = 4096, tile_cells = 1023, tile_slots = 1024, tile_runs = 32;
 };
 
 // From the locality-sorted node map (ncells x 4), the sorted coordinate map,
