@@ -922,13 +922,23 @@ __device__ __forceinline__ double star_row(const StarArgs& a, int r, int4 h, int
   const int v[7] = {h.y, h.z, h.w, t.x, t.y, t.z, t.w};
   const double2 xs = __ldg(reinterpret_cast<const double2*>(a.coords) + r);
   const double us = __ldg(a.coeff + r);
+  // every neighbour gather is issued before the first use: one dependent
+  // round trip after the star record instead of one per link vertex
+  double2 X[7];
+  double U[7];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    const int vk = k < m ? v[k] : r;
+    X[k] = __ldg(reinterpret_cast<const double2*>(a.coords) + vk);
+    U[k] = __ldg(a.coeff + vk);
+  }
   double px = 0, py = 0, up = 0, p0x = 0, p0y = 0, u0 = 0, aa = 0;
   double acc = 0.0;
 #pragma unroll
   for (int k = 0; k < 7; ++k) {
     if (k < m) {
-      const double2 x = __ldg(reinterpret_cast<const double2*>(a.coords) + v[k]);
-      const double u = __ldg(a.coeff + v[k]);
+      const double2 x = X[k];
+      const double u = U[k];
       const double nx = x.x - xs.x, ny = x.y - xs.y, nn = nx * nx + ny * ny;
       if (k == 0) {
         p0x = nx;
