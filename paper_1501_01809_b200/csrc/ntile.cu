@@ -233,7 +233,7 @@ struct NtileArgs {
   const double* coords;
   double* out;
   FormParams prm;
-  int accumulate, dynamic;
+  int accumulate, dynamic, dbg;
   int off_seg, off_geo, off_part, off_buf, buf_bytes, b_win;
 };
 
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
     double* seg = seg0 + (E0 & 1); // 16-byte parity of the global destination (bulk store)
     if (tid == 0) bulk_wait_read<0>(); // the previous tile's store has read the segment
     // phase 1: barycentric gradients and measure of every cell of the tile, once
-    for (int c = tid; c < ncell; c += NT) {
+    for (int c = tid; c < ((a.dbg & 2) ? 0 : ncell); c += NT) {
       double X[4][3];
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
@@ -377,23 +377,40 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
     // phase 2: one thread per 3x3 node block (diagonal blocks: kDiagSplit threads)
     for (int it = tid; it < nitems; it += NT) {
       const uint2 ir = items[it];
-      const int poff = ir.x & 0xffff, np = (ir.x >> 16) & 0xff, kind = ir.x >> 24;
+      const int poff = ir.x & 0xffff, np = (a.dbg & 1) ? 0 : (ir.x >> 16) & 0xff, kind = ir.x >> 24;
       const int base = ir.y & 0xffff, stride = ir.y >> 16;
       // S = sum over the block's cells of V g_a g_b^T (9 FMAs per cell); the
       // element block of FormT<F_ELASTICITY>::row is linear in it:
       //   A_de = mu S_ed + lam S_de + d_de mu tr(S)
       double acc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-      for (int q = 0; q < np; ++q) {
+      // software pipeline: pair q+1's record and gradients load during pair q's FMAs
+      auto fetch = [&](int q, double (&ga)[3], double (&gb)[3]) {
         const uint32_t x = prec[poff + q];
         const double* g = geo + (x >> 4) * kGS;
         const int lv = (x >> 2) & 3, lw = x & 3;
-        const double2 a0 = reinterpret_cast<const double2*>(g + 4 * lv)[0], b0 = reinterpret_cast<const double2*>(g + 4 * lw)[0];
-        const double a2 = g[4 * lv + 2], b2 = g[4 * lw + 2];
-        const double ga[3] = {a0.x, a0.y, a2}, gb[3] = {b0.x, b0.y, b2};
+        const double2 a0 = reinterpret_cast<const double2*>(g + 4 * lv)[0];
+        const double2 b0 = reinterpret_cast<const double2*>(g + 4 * lw)[0];
+        ga[0] = a0.x;
+        ga[1] = a0.y;
+        ga[2] = g[4 * lv + 2];
+        gb[0] = b0.x;
+        gb[1] = b0.y;
+        gb[2] = g[4 * lw + 2];
+      };
+      double ga[3] = {0, 0, 0}, gb[3] = {0, 0, 0};
+      if (np > 0) fetch(0, ga, gb);
+      for (int q = 0; q < np; ++q) {
+        double na[3] = {0, 0, 0}, nb[3] = {0, 0, 0};
+        if (q + 1 < np) fetch(q + 1, na, nb);
 #pragma unroll
         for (int d = 0; d < 3; ++d)
 #pragma unroll
           for (int e = 0; e < 3; ++e) acc[d][e] = fma(ga[d], gb[e], acc[d][e]);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          ga[d] = na[d];
+          gb[d] = nb[d];
+        }
       }
       if (kind == 0) {
         const double tr = mu * (acc[0][0] + acc[1][1] + acc[2][2]);
@@ -491,6 +508,7 @@ void launch_ntile(const NtilePlan& p, const double* coords, double* out, const F
     kern<<<std::min(p.ntiles, blocks * kNumSMs), kNtThreads + 32, smem, s>>>(a);
   };
   a.dynamic = std::getenv("LOAM_GPU_NT_STATIC") ? 0 : 1;
+  a.dbg = std::getenv("LOAM_GPU_NT_DBG") ? std::atoi(std::getenv("LOAM_GPU_NT_DBG")) : 0; // developer: skip phases
   if (st >= 3) go(k_ntile<3>, 3);
   else if (st == 2) go(k_ntile<2>, 2);
   else go(k_ntile<1>, 1);
