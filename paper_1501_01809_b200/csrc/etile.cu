@@ -7,6 +7,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "async.cuh"
@@ -221,22 +222,58 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       cellof[p - p0e] = c;
     }
   }
+  // ---- compact records: with every edge row at most 32 entries long, a rank
+  // fits in 5 bits; the ranks of the row's own edge and of its two endpoint
+  // vertices (canonical columns ca, cb, nv) are the same for every pair of the
+  // row and move to a per-row word; the others pack with the header into 8
+  // bytes (tets) / 4 bytes (triangles)
+  bool compact = !std::getenv("LOAM_GPU_ET_WIDE");
+  for (int e = 0; e < nedge && compact; ++e) compact = hrp[E0 + e + 1] - hrp[E0 + e] <= 32;
+  std::vector<int> ncj; // canonical columns whose rank varies per pair
+  for (int j = 0; j < nrn; ++j)
+    if (j != ca && j != cb && j != nv) ncj.push_back(j);
+  std::vector<uint32_t> rconst(nedge, 0);
+  for (int e = 0; e < nedge && compact; ++e)
+    for (int p = hp[E0 + e]; p < hp[E0 + e + 1]; ++p) {
+      const uint8_t* rec = &recs[(size_t)(p - p0e) * rb];
+      const uint32_t rcv = (uint32_t)rec[2 + ca] | (uint32_t)rec[2 + cb] << 8 | (uint32_t)rec[2 + nv] << 16;
+      if (p == hp[E0 + e]) rconst[e] = rcv;
+      else if (rcv != rconst[e]) compact = false;
+    }
+  const int rbx = compact ? (gd == 3 ? 8 : 4) : rb; // record bytes in the blob
+  auto pack = [&](const uint8_t* rec, uint8_t* dst) { // full record -> blob record
+    if (!compact) {
+      memcpy(dst, rec, rb);
+      return;
+    }
+    uint64_t w = (uint64_t)rec[0] | (uint64_t)rec[1] << 8;
+    for (size_t q = 0; q < ncj.size(); ++q) w |= (uint64_t)(rec[2 + ncj[q]] & 31) << (q < 3 ? 16 + 5 * q : 32 + 5 * (q - 3));
+    memcpy(dst, &w, rbx);
+  };
   // ---- edge tiles: consecutive edge rows, their distinct cells and coordinate window.
   // Per warp of rows the segment is lane-interleaved (entry j of lane r at
   // base + 32 j + r: conflict-free shared updates) and so are the pair
-  // records (word q of pair p of lane r at base + 32 (p RBW + q) + r).
+  // records (word q of pair p of lane r at base + 32 (p RBW + q) + r).  Lanes
+  // take the tile's rows in order of their pair count, so a warp's rows have
+  // equal loop lengths and record padding.
   std::vector<int32_t> tiles, runs;
   std::vector<uint8_t> blob;
   std::vector<int> stamp(ncells, -1), local(ncells, 0), vid;
   std::vector<std::pair<int, int>> rr;
   int gen = 0, r0 = 0;
-  const int trows = sp.tile_rows <= 64 ? 64 : 128, nwarps = trows / 32, rbw = rb / 4;
+  const int trows = sp.tile_rows <= 64 ? 64 : 128, nwarps = trows / 32, rbw = rbx / 4;
+  std::vector<int> lrow; // lane -> tile row
   const int cell_cap = std::min(sp.tile_cells, 1023);
   auto warp_sizes = [&](int a, int b, std::vector<int>& lmax, std::vector<int>& pmax) {
     lmax.assign(nwarps, 0);
     pmax.assign(nwarps, 0);
-    for (int r = a; r < b; ++r) {
-      const int w = (r - a) / 32;
+    lrow.resize(b - a);
+    for (int r = a; r < b; ++r) lrow[r - a] = r - a;
+    std::stable_sort(lrow.begin(), lrow.end(), [&](int x, int y) {
+      return hp[E0 + a + x + 1] - hp[E0 + a + x] < hp[E0 + a + y + 1] - hp[E0 + a + y];
+    });
+    for (int l = 0; l < b - a; ++l) {
+      const int w = l / 32, r = a + lrow[l];
       lmax[w] = std::max<int>(lmax[w], (int)(hrp[E0 + r + 1] - hrp[E0 + r]));
       pmax[w] = std::max(pmax[w], hp[E0 + r + 1] - hp[E0 + r]);
     }
@@ -292,7 +329,7 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
     int rwords = 0;
     for (int w = 0; w < nwarps; ++w) rwords += pmax[w] * rbw * 32;
     const int off_srow = 0, off_trow = up16((nrows + 1) * 2), off_np = off_trow + up16((nrows + 1) * 2),
-              off_xpos = off_np + up16(trows + 4 * nwarps), off_tpos = off_xpos + nrows * 16,
+              off_xpos = off_np + up16(6 * trows + 4 * nwarps), off_tpos = off_xpos + nrows * 16,
               off_tlen = off_tpos + up16(ntp * 4), off_xlen = off_tlen + (cd == 2 ? up16(ntp * 4) : 0),
               off_recs = off_xlen + (cd == 2 ? up16(nrows * 8) : 0), off_cells = off_recs + up16(rwords * 4),
               bytes = off_cells + up16(ncell * nv * 2);
@@ -306,6 +343,8 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       memcpy(bp + off_trow + 2 * r, &tr, 2);
     }
     for (int r = 0; r < nrows; ++r) bp[off_np + r] = (uint8_t)(hp[E0 + r0 + r + 1] - hp[E0 + r0 + r]);
+    for (int l = 0; l < nrows; ++l) bp[off_np + trows + 4 * nwarps + l] = (uint8_t)lrow[l];
+    if (compact) memcpy(bp + off_np + 2 * trows + 4 * nwarps, &rconst[r0], (size_t)nrows * 4);
     {
       int sb = 0, wb = 0;
       for (int w = 0; w < nwarps; ++w) {
@@ -313,15 +352,16 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
         memcpy(bp + off_np + trows + 4 * w, &s16, 2);
         memcpy(bp + off_np + trows + 4 * w + 2, &w16, 2);
         for (int l = 0; l < 32 && 32 * w + l < nrows; ++l) {
-          const int r = r0 + 32 * w + l;
+          const int r = r0 + lrow[32 * w + l];
           for (int p = hp[E0 + r]; p < hp[E0 + r + 1]; ++p) {
             const int64_t pe = p - p0e;
-            uint8_t rec[16];
-            memcpy(rec, &recs[(size_t)pe * rb], rb);
+            uint8_t full_rec[16], rec[16];
+            memcpy(full_rec, &recs[(size_t)pe * rb], rb);
             uint16_t h;
-            memcpy(&h, rec, 2);
+            memcpy(&h, full_rec, 2);
             h = (uint16_t)(h | local[cellof[pe]]);
-            memcpy(rec, &h, 2);
+            memcpy(full_rec, &h, 2);
+            pack(full_rec, rec);
             const int pi = p - hp[E0 + r];
             for (int q = 0; q < rbw; ++q)
               memcpy(bp + off_recs + 4 * ((size_t)wb + (pi * rbw + q) * 32 + l), rec + 4 * q, 4);
@@ -358,6 +398,7 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
   out.gd = gd;
   out.cd = cd;
   out.tile_threads = trows;
+  out.compact = compact;
   out.ntiles = (int)tiles.size() / 16;
   out.e0 = E0;
   out.nedge = nedge;
@@ -485,7 +526,7 @@ __device__ __forceinline__ double sel4(const double (&v)[4], int i) {
 }
 
 // NT consumer threads (= edge rows per tile) + one TMA producer warp.
-template <int FORM, int D, int CD, int NT, int STAGES>
+template <int FORM, int D, int CD, int NT, int STAGES, bool COMPACT>
 __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ EtileArgs a) {
   using T = EtT<D>;
   constexpr int NV = T::NV, N = T::N;
@@ -572,7 +613,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
     return;
   }
   // ---- consumers
-  constexpr int GS = T::GS, RBW = T::RBW;
+  constexpr int GS = T::GS, RBW = COMPACT ? (D == 3 ? 2 : 1) : T::RBW;
   double* segT = reinterpret_cast<double*>(sm + a.off_seg); // lane-interleaved row segments
   double* geo = reinterpret_cast<double*>(sm + a.off_geo);  // cell Gram matrices; then the contiguous segment
   const int lane = tid & 31, warp = tid >> 5;
@@ -587,6 +628,8 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
     const uint16_t* srow = reinterpret_cast<const uint16_t*>(buf + m[10]);
     const uint8_t* npair = buf + m[11];
     const uint16_t* wmeta = reinterpret_cast<const uint16_t*>(buf + m[11] + NT);
+    const uint8_t* lrow = buf + m[11] + NT + 4 * (NT / 32);                        // lane -> row
+    const uint32_t* rconst = reinterpret_cast<const uint32_t*>(buf + m[11] + 2 * NT + 4 * (NT / 32));
     const uint32_t* recs = reinterpret_cast<const uint32_t*>(buf + m[12]);
     const uint16_t* cslot = reinterpret_cast<const uint16_t*>(buf + m[13]);
     const uint16_t* trow = reinterpret_cast<const uint16_t*>(buf + m[14]);
@@ -640,10 +683,18 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
     int s0 = 0, L = 0;
     const int sb = wmeta[2 * warp], rbase = wmeta[2 * warp + 1];
     double* my = segT + sb + lane; // entry j of this row at my[32 j]
+    const int row = tid < nrows ? lrow[tid] : 0;
     if (tid < nrows) {
-      s0 = srow[tid];
-      L = srow[tid + 1] - s0;
-      const int np = (a.dbg & 1) ? 0 : npair[tid];
+      s0 = srow[row];
+      L = srow[row + 1] - s0;
+      const int np = (a.dbg & 1) ? 0 : npair[row];
+      int pconst[3] = {0, 0, 0}; // compact: ranks of canonical columns CA, CB, NV (the row's own)
+      if constexpr (COMPACT) {
+        const uint32_t rc = rconst[row];
+        pconst[0] = 32 * (int)(rc & 0xffu);
+        pconst[1] = 32 * (int)((rc >> 8) & 0xffu);
+        pconst[2] = 32 * (int)((rc >> 16) & 0xffu);
+      }
       double vab = 0.0, dA = 0.0, dB = 0.0;
       bool hA = false, hB = false;
       const uint32_t* rq = recs + rbase + lane;
@@ -675,8 +726,23 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
         double o[N], dga, dgb;
         et_row<FORM, D>(Ga, Gb, V, a.prm, o, vab, dga, dgb);
         int pos[N];
+        if constexpr (COMPACT) {
+          int q = 0;
 #pragma unroll
-        for (int j = 0; j < N; ++j) pos[j] = 32 * (int)((w[(2 + j) >> 2] >> (8 * ((2 + j) & 3))) & 0xffu);
+          for (int j = 0; j < N; ++j) {
+            if (j == T::CA) pos[j] = pconst[0];
+            else if (j == T::CB) pos[j] = pconst[1];
+            else if (j == NV) pos[j] = pconst[2];
+            else {
+              const int bit = q < 3 ? 16 + 5 * q : 5 * (q - 3);
+              pos[j] = 32 * (int)((w[q < 3 ? 0 : 1] >> bit) & 31u);
+              ++q;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < N; ++j) pos[j] = 32 * (int)((w[(2 + j) >> 2] >> (8 * ((2 + j) & 3))) & 0xffu);
+        }
         double cur[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) cur[j] = my[pos[j]];
@@ -692,7 +758,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
         }
       }
       // vertex rows: transposed vertex-column entries, the vertex pair, diagonals
-      const int t0 = trow[tid], t1 = (a.dbg & 4) ? t0 : trow[tid + 1];
+      const int t0 = trow[row], t1 = (a.dbg & 4) ? t0 : trow[row + 1];
       const int ntp = trow[nrows];
       // CD = 2: the 2x2 block (v, v) / (v, w) is (x, 0; 0, x) at rows pos, pos + rowlen
       const int32_t* tlen = tpos + ((ntp + 3) & ~3);
@@ -716,8 +782,8 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
         }
       };
       for (int t = t0; t < t1; ++t) put(tpos[t], CD == 2 ? tlen[t] : 0, my[32 * (t - t0)]);
-      const int4 xp = xpos[tid];
-      const int2 xl = CD == 2 ? xlen[tid] : make_int2(0, 0);
+      const int4 xp = xpos[row];
+      const int2 xl = CD == 2 ? xlen[row] : make_int2(0, 0);
       put(xp.x, xl.x, vab);
       put(xp.y, xl.y, vab);
       if (hA) {
@@ -793,13 +859,18 @@ void go_etile(const EtilePlan& p, const EtileArgs& a, size_t smem_base, size_t b
     kern<<<grid, threads, smem, s>>>(a);
   };
   const int st = et_stages();
-  if (p.tile_threads == 64) {
-    if (st >= 2) go(k_etile<FORM, D, CD, 64, 2>, 96, 2);
-    else go(k_etile<FORM, D, CD, 64, 1>, 96, 1);
-  } else {
-    if (st >= 2) go(k_etile<FORM, D, CD, 128, 2>, 160, 2);
-    else go(k_etile<FORM, D, CD, 128, 1>, 160, 1);
-  }
+  auto pick = [&](auto compact) {
+    constexpr bool C = decltype(compact)::value;
+    if (p.tile_threads == 64) {
+      if (st >= 2) go(k_etile<FORM, D, CD, 64, 2, C>, 96, 2);
+      else go(k_etile<FORM, D, CD, 64, 1, C>, 96, 1);
+    } else {
+      if (st >= 2) go(k_etile<FORM, D, CD, 128, 2, C>, 160, 2);
+      else go(k_etile<FORM, D, CD, 128, 1, C>, 160, 1);
+    }
+  };
+  if (p.compact) pick(std::true_type{});
+  else pick(std::false_type{});
 }
 
 } // namespace

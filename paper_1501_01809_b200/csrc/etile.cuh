@@ -31,6 +31,7 @@ namespace loam_gpu {
 
 struct EtilePlan {
   int gd = 3, cd = 1, ntiles = 0, e0 = 0, nedge = 0, rec_bytes = 0, tile_threads = 128;
+  bool compact = false; // 5-bit ranks, per-row constant ranks (rows <= 32 entries)
   int max_rows = 0, max_seg = 0, max_segT = 0, max_cells = 0, max_slots = 0, max_blob = 0;
   int64_t ndiag = 0;
   DevBuf<int32_t> tiles; // 16 ints per tile (etile.cu)
