@@ -181,6 +181,20 @@ int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t iterset_size,
                           uint64_t iterset_id, const loam_arg_desc* args, int nargs,
                           void* stream);
 
+/* nsteps independent executions of one loop (same kernel, iteration set,
+ * maps and sparsity; args[k] is step k's argument array over its own host
+ * Dat / Mat buffers).  Same per-step semantics and transfers as
+ * loam_gpu_execute_host -- every step uploads what it reads and downloads
+ * what it writes -- but the steps are pipelined: step k+1's host->device
+ * copies run on one copy engine while step k's device->host copies run on
+ * the other (two device buffer sets), kernels in order on `stream`.
+ * Returns when every step's results are in host memory.  An extension (the
+ * reference executes one loop per call); a time-stepping or multi-RHS caller
+ * uses it to keep both PCIe directions busy. */
+int loam_gpu_execute_host_batch(const loam_kernel_desc* kernel, int32_t iterset_size,
+                                uint64_t iterset_id, const loam_arg_desc* const* args, int nargs,
+                                int nsteps, void* stream);
+
 /* ---- consumers of the assembled matrix --------------------- */
 /* y = A x by CSR traversal (data.hpp:236-250 mat_spmv): rows ascending, each
  * row folded in column order with a separate multiply and add -- bitwise

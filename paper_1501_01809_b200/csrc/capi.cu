@@ -259,6 +259,121 @@ int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t n, uint64_t it
   });
 }
 
+namespace {
+// Copy engines of the batched host calling convention (created once).
+struct CopyStreams {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  CopyStreams() {
+    LG_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    LG_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+  }
+};
+CopyStreams& copy_streams() {
+  static CopyStreams c;
+  return c;
+}
+size_t arg_count(const loam_arg_desc& a) {
+  return a.kind == LOAM_ARG_MAT ? (size_t)a.sparsity->nnz
+         : a.kind == LOAM_ARG_DAT ? (size_t)a.set_size * a.dim : (size_t)a.dim;
+}
+bool arg_needs_old(const loam_arg_desc& a) {
+  return a.access == LOAM_READ || a.access == LOAM_RW || (a.access == LOAM_INC && !(a.flags & LOAM_ARG_ZERO)) ||
+         (a.access == LOAM_WRITE && (a.kind != LOAM_ARG_DAT || a.map));
+}
+} // namespace
+
+int loam_gpu_execute_host_batch(const loam_kernel_desc* kernel, int32_t n, uint64_t iter,
+                                const loam_arg_desc* const* args, int nargs, int nsteps, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(nsteps >= 0 && (nsteps == 0 || args != nullptr), LOAM_ERR(InvalidArgument), "batch without steps");
+    for (int k = 0; k < nsteps; ++k) validate(kernel, n, iter, args[k], nargs); // nothing copied if illegal
+    if (nsteps == 0) return;
+    cudaStream_t s = as_stream(stream);
+    CopyStreams& cs = copy_streams();
+    // device copies of the immutable objects (resident by id, as execute_host)
+    const loam_arg_desc* a0 = args[0];
+    std::vector<loam_map_desc> dmaps(2 * nargs);
+    std::vector<loam_sparsity_desc> dsp(nargs);
+    auto keep = [&](int kind, uint64_t id, const void* host, size_t bytes) -> void* {
+      require(id != 0, LOAM_ERR(InvalidArgument), "batched host execution needs id'd maps and sparsities");
+      return resident_copy(kind, id, host, bytes, s);
+    };
+    auto map_up = [&](const loam_map_desc* m, loam_map_desc& d) {
+      d = *m;
+      d.values = static_cast<const int32_t*>(
+          keep(0, m->id, m->values, sizeof(int32_t) * (size_t)m->source_size * m->arity));
+      if (m->expand_dim > 1 && m->node_values)
+        d.node_values = static_cast<const int32_t*>(
+            keep(1, m->id, m->node_values, sizeof(int32_t) * (size_t)m->source_size * m->node_arity));
+    };
+    for (int q = 0; q < nargs; ++q) {
+      const loam_arg_desc& a = a0[q];
+      if (a.map) map_up(a.map, dmaps[2 * q]);
+      if (a.col_map) map_up(a.col_map, dmaps[2 * q + 1]);
+      if (a.kind == LOAM_ARG_MAT) {
+        dsp[q] = *a.sparsity;
+        dsp[q].row_ptr = static_cast<const int64_t*>(
+            keep(2, a.sparsity->id, a.sparsity->row_ptr, sizeof(int64_t) * ((size_t)a.sparsity->nrows + 1)));
+        dsp[q].col_idx = static_cast<const int32_t*>(
+            keep(3, a.sparsity->id, a.sparsity->col_idx, sizeof(int32_t) * (size_t)a.sparsity->nnz));
+      }
+    }
+    for (int k = 1; k < nsteps; ++k) // one loop shape: the same objects in every step
+      for (int q = 0; q < nargs; ++q)
+        require(args[k][q].kind == a0[q].kind && args[k][q].access == a0[q].access &&
+                    (!a0[q].map || (args[k][q].map && args[k][q].map->id == a0[q].map->id)) &&
+                    (a0[q].kind != LOAM_ARG_MAT || args[k][q].sparsity->id == a0[q].sparsity->id) &&
+                    arg_count(args[k][q]) == arg_count(a0[q]),
+                LOAM_ERR(InvalidArgument), "batched steps must share the loop shape");
+    // two device buffer sets; a set is reused once its previous step's downloads finished
+    std::vector<DevBuf<double>> bufs[2];
+    cudaEvent_t in_ready[2], done[2], freed[2];
+    for (int b = 0; b < 2; ++b) {
+      for (int q = 0; q < nargs; ++q) bufs[b].emplace_back(std::max<size_t>(arg_count(a0[q]), 1), s);
+      LG_CUDA(cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming));
+      LG_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+      LG_CUDA(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
+    }
+    LG_CUDA(cudaEventRecord(freed[0], s)); // buffers allocated on s
+    LG_CUDA(cudaEventRecord(freed[1], s));
+    std::vector<loam_arg_desc> dargs(nargs);
+    for (int k = 0; k < nsteps; ++k) {
+      const int b = k & 1;
+      const loam_arg_desc* a = args[k];
+      LG_CUDA(cudaStreamWaitEvent(cs.h2d, freed[b], 0));
+      for (int q = 0; q < nargs; ++q)
+        if (arg_needs_old(a[q]) && arg_count(a[q]))
+          LG_CUDA(cudaMemcpyAsync(bufs[b][q].get(), a[q].data, sizeof(double) * arg_count(a[q]),
+                                  cudaMemcpyHostToDevice, cs.h2d));
+      LG_CUDA(cudaEventRecord(in_ready[b], cs.h2d));
+      LG_CUDA(cudaStreamWaitEvent(s, in_ready[b], 0));
+      for (int q = 0; q < nargs; ++q) {
+        dargs[q] = a[q];
+        dargs[q].data = bufs[b][q].get();
+        if (a[q].map) dargs[q].map = &dmaps[2 * q];
+        if (a[q].col_map) dargs[q].col_map = &dmaps[2 * q + 1];
+        if (a[q].kind == LOAM_ARG_MAT) dargs[q].sparsity = &dsp[q];
+      }
+      execute(kernel, n, iter, dargs.data(), nargs, s);
+      LG_CUDA(cudaEventRecord(done[b], s));
+      LG_CUDA(cudaStreamWaitEvent(cs.d2h, done[b], 0));
+      for (int q = 0; q < nargs; ++q)
+        if (a[q].access != LOAM_READ && arg_count(a[q]))
+          LG_CUDA(cudaMemcpyAsync(a[q].data, bufs[b][q].get(), sizeof(double) * arg_count(a[q]),
+                                  cudaMemcpyDeviceToHost, cs.d2h));
+      LG_CUDA(cudaEventRecord(freed[b], cs.d2h));
+    }
+    LG_CUDA(cudaStreamSynchronize(cs.d2h));
+    LG_CUDA(cudaStreamSynchronize(s));
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(in_ready[b]);
+      cudaEventDestroy(done[b]);
+      cudaEventDestroy(freed[b]);
+    }
+  });
+}
+
 int loam_gpu_spmv(const loam_sparsity_desc* sparsity, const double* values, const double* x, int64_t x_len,
                   double* y, void* stream) {
   return guarded([&] {

@@ -488,6 +488,44 @@ class HostLoop:
                                                     self.loop.iterset.id, self.descs, len(self.loop.args),
                                                     _stream() if stream is None else stream))
 
+    def step_buffers(self):
+        """A second argument array for loam_gpu_execute_host_batch: the same
+        maps and sparsity host mirrors, its own pinned Dat / Mat / Global
+        buffers (copies of this loop's).  Returns (descs, outputs)."""
+        n = len(self.loop.args)
+        descs = (capi.ArgDesc * max(n, 1))()
+        outs = []
+        for k in range(n):
+            d = capi.ArgDesc()
+            C.memmove(C.byref(d), C.byref(self.descs[k]), C.sizeof(d))
+            nbytes = self._arg_bytes(k)
+            h = torch.empty(max(nbytes // 8, 1), dtype=torch.float64).pin_memory()
+            C.memmove(h.data_ptr(), d.data, nbytes)
+            self._keep.append(h)
+            d.data = h.data_ptr()
+            if self.loop.args[k].access != READ:
+                outs.append(h)
+            descs[k] = d
+        self._keep.append(descs)
+        return descs, outs
+
+    def _arg_bytes(self, k: int) -> int:
+        a = self.loop.args[k]
+        if a.dat is not None:
+            return a.dat.set.size * a.dat.dim * 8
+        if a.mat is not None:
+            return a.mat.sparsity.nnz * 8
+        return a.glob.data.numel() * 8
+
+    def run_batch(self, step_descs, stream: Optional[int] = None) -> None:
+        """loam_gpu_execute_host_batch over the argument arrays `step_descs`
+        (this loop's own and/or step_buffers() ones), pipelined copies."""
+        arr = (C.POINTER(capi.ArgDesc) * len(step_descs))(
+            *[C.cast(d, C.POINTER(capi.ArgDesc)) for d in step_descs])
+        capi.check(capi.lib().loam_gpu_execute_host_batch(
+            C.byref(self.kd), self.loop.iterset.size, self.loop.iterset.id, arr, len(self.loop.args),
+            len(step_descs), _stream() if stream is None else stream))
+
 
 def validate(loop: Parloop) -> None:
     """parloop.hpp:89-146: descriptor checks only, no state change."""

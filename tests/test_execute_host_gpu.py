@@ -87,3 +87,38 @@ def test_host_byte_accounting_is_per_step_dats_only(gpu_lib):
     m = configs.config_inputs(2, 16)
     assert h.h2d_bytes == m.coords.size * 8                       # coordinates (READ Dat)
     assert h.d2h_bytes == w.outputs[0].sparsity.nnz * 8          # the assembled values
+
+
+@pytest.mark.parametrize("cfg,n", [(1, 24), (2, 24), (3, 4), (4, 4), (5, 6)])
+def test_batched_host_convention(gpu_lib, cfg, n):
+    """loam_gpu_execute_host_batch: K steps over two alternating host buffer
+    sets, copies pipelined across steps; both sets end with the
+    device-convention result."""
+    w = configs.Workload(cfg, n)
+    dev = dict(zip(map(id, w.outputs), device_outputs(w)))
+    w.reset()
+    hls = [L.HostLoop(lp) for lp in w.loops]
+    for h in hls:
+        alt, outs = h.step_buffers()
+        h.run_batch([h.descs, alt, h.descs, alt, h.descs])
+        d = dev[id(loop_output(h.loop))]
+        assert rel(h.outputs[0].numpy()[: len(d)], d) <= TOL
+        assert rel(outs[0].numpy()[: len(d)], d) <= TOL
+
+
+def test_batched_steps_upload_their_own_inputs(gpu_lib):
+    w = configs.Workload(1, 20)  # P1 Helmholtz residual: linear in the coefficient u
+    ref = device_outputs(w)[0]
+    w.reset()
+    h = L.HostLoop(w.loops[0])
+    alt, outs = h.step_buffers()
+    # the alternate set's coefficient is 3u: its residual is 3x (the action is linear in u)
+    u_idx = 2
+    k = w.loops[0].args[u_idx].dat
+    nbytes = k.set.size * 8
+    host_u = np.ctypeslib.as_array(C.cast(alt[u_idx].data, C.POINTER(C.c_double)), shape=(k.set.size,))
+    host_u *= 3.0
+    h.run_batch([h.descs, alt, h.descs, alt])
+    assert rel(h.outputs[0].numpy()[: len(ref)], ref) <= TOL
+    assert rel(outs[0].numpy()[: len(ref)], 3.0 * ref) <= TOL
+    assert nbytes > 0
