@@ -30,6 +30,7 @@
 #include "engine.cuh"
 #include "etile.cuh"
 #include "ntile.cuh"
+#include "rtile.cuh"
 #include "patch.cuh"
 #include "patch_kernels.cuh"
 #include "plan.cuh"
@@ -2058,6 +2059,8 @@ struct FastPlan {
   EtilePlan et;
   bool use_ntile = false;  // node-block tiles (vector P1 elasticity, ntile.cuh)
   NtilePlan nt;
+  bool use_rtile = false;  // row tiles with shared cell geometry (Taylor-Hood B / B^T, rtile.cuh)
+  RtilePlan rt;
   bool use_star = false;   // vertex-star kernel (P1 triangle actions)
   DevBuf<int4> star;
   bool use_patch = false;  // cell-patch row-owner kernels (patch.cuh)
@@ -2327,6 +2330,19 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
         return P;
       }
     }
+    // row tiles: the Taylor-Hood coupling blocks
+    if (strat == 0 && rtile_form(k.form) && !std::getenv("LOAM_GPU_NO_RTILE") && R.dim == k.rd && Cn.dim == k.cd &&
+        (reinterpret_cast<uintptr_t>(args[1].data) & 15) == 0) {
+      SortedMap sx;
+      gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, sx, s);
+      RtileSpec rs;
+      rs.tile_rows = env_int("LOAM_GPU_RT_ROWS", rs.tile_rows);
+      if (build_rtile(P->rt, rs, k.form, k.gd, k.nrn, k.ncn, k.rd, k.cd, n, R.v.target, srows.v.get(), sx.v.get(),
+                      X->target_size, P->pp, sp->row_ptr, sp->nnz, s)) {
+        P->use_rtile = true;
+        return P;
+      }
+    }
   }
   // canonical pair tiles: default for the scalar / 2-vector bilinear forms the
   // ring / neighbour paths do not take (P2 matrices, Taylor-Hood blocks).  P2
@@ -2580,6 +2596,12 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
       fprintf(stderr, "[ring timing] CTA starts span %.2f us, CTA ends from %.2f to %.2f us after the first start\n",
               (double)(h[11] - h[8]) * 1e-3, (double)(h[12] - h[8]) * 1e-3, (double)(h[9] - h[8]) * 1e-3);
     }
+    return;
+  }
+  if (P->use_rtile) {
+    launch_rtile(P->rt, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
+                 P->counter.get() + P->parity, P->counter.get() + (P->parity ^ 1), s);
+    P->parity ^= 1;
     return;
   }
   if (P->use_ntile) {

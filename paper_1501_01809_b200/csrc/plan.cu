@@ -520,12 +520,13 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
   return true;
 }
 
-namespace {
 // Local node permutation induced by a vertex permutation sigma (new vertex
 // index of old vertex v is sigma[v]) on Lagrange P1 / P2 simplices; returns
 // newpos[old local node].  P2 local edges follow elements.cuh / space.hpp.
+namespace {
 const int kTriEdge[3][2] = {{1, 2}, {0, 2}, {0, 1}};
 const int kTetEdge[6][2] = {{2, 3}, {1, 3}, {1, 2}, {0, 3}, {0, 2}, {0, 1}};
+} // namespace
 void induced(int gd, int nloc, const int* sigma, int* newpos) {
   const int nv = gd + 1;
   for (int v = 0; v < nv && v < nloc; ++v) newpos[v] = sigma[v];
@@ -557,7 +558,6 @@ int canonical_sigma(int gd, int nrn, int i, int* sigma) {
   (void)nrn;
   return nv;
 }
-} // namespace
 
 bool build_ptile(PTilePlan& out, const PTileSpec& sp, int ncells, int nrows_node, const int32_t* sorted_rows,
                  const int32_t* sorted_cols, const int32_t* sorted_x, int nverts, const int32_t* sorted_coeff,

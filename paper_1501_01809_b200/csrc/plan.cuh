@@ -142,6 +142,13 @@ struct PTileSpec {
 // sorted_* are node-level maps in the locality order; pp holds the pairs and
 // (for matrices) the ranks of the column nodes; csr the Mat pattern (matrices).
 // Returns false when a tile limit cannot be met (caller falls back).
+// Canonical local numbering of a pair (plan.cu): sigma[old vertex] = new vertex
+// making row-space local node i canonical (vertex rows: local vertex 0; P2
+// edge rows: the first local edge); returns the canonical local index (0 or
+// gd+1).  induced() maps old local nodes (nloc of them, P1 or P2) to new.
+int canonical_sigma(int gd, int nrn, int i, int* sigma);
+void induced(int gd, int nloc, const int* sigma, int* newpos);
+
 bool build_ptile(PTilePlan& out, const PTileSpec& sp, int ncells, int nrows_node, const int32_t* sorted_rows,
                  const int32_t* sorted_cols, const int32_t* sorted_x, int nverts, const int32_t* sorted_coeff,
                  int ncoeff_nodes, const PairPlan& pp, const CsrView& csr, cudaStream_t s);

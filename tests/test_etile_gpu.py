@@ -133,3 +133,28 @@ def test_elasticity_node_block_tiles(gpu_lib, n):
     assert rel(A.host_values(), ref) <= TOL
     w.run()  # accumulate
     assert rel(A.host_values(), 2 * ref) <= TOL
+
+
+@pytest.mark.parametrize("n", [1, 4, 9])
+def test_stokes_coupling_blocks_row_tiles(gpu_lib, n):
+    """Config 5's B (pressure rows) and B^T (velocity rows) blocks through the
+    row tiles with shared cell geometry (csrc/rtile.cu): one launch each,
+    values vs the oracle, accumulation."""
+    capi.set_strategy("auto")
+    w = configs.Workload(5, n)
+    w.reset()
+    w.run()
+    m = w.inputs
+    dm = w.vdm.values
+    A, BT, B = w.outputs
+    for lp, out, form, rmap, ar, cmap, ac in ((w.loops[1], B, O.STOKES_B, m.cv, 3, dm, 12),
+                                              (w.loops[2], BT, O.STOKES_BT, dm, 12, m.cv, 3)):
+        out.zero()
+        l0 = capi.launch_count()
+        w.L.execute(lp)
+        assert capi.launch_count() - l0 == 1
+        rp, ci = out.sparsity.host()
+        ref = O.assemble_matrix(form, 2, 2, m.ncells, rmap, ar, cmap, ac, m.cv, m.coords, rp, ci)
+        assert rel(out.host_values(), ref) <= TOL
+        w.L.execute(lp)  # accumulate
+        assert rel(out.host_values(), 2 * ref) <= TOL
