@@ -1,12 +1,14 @@
 """Update profiles/ncu_summary.json with one kernel's ncu numbers.
 
-usage: python tools/ncu_json.py TAG REPORT.ncu-rep ALGORITHMIC_BYTES "source label"
+usage: python tools/ncu_json.py TAG REPORT.ncu-rep|RAW.csv ALGORITHMIC_BYTES "source label"
+(RAW.csv = `ncu -i REPORT --page raw --csv` output)
 Per-launch DRAM traffic (dram__bytes_read + write) and duration of the first
 kernel in the report; bench.py reads the traffic back as roofline.traffic."""
 import csv, io, json, os, subprocess, sys
 
 tag, rep, alg, label = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = open(rep).read() if rep.endswith(".csv") else \
+    subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
 
