@@ -275,6 +275,22 @@ int loam_gpu_pointwise(double* out, int64_t n, int32_t op, const loam_pw_instr* 
 enum loam_reduce_kind { LOAM_REDUCE_SUM = 0, LOAM_REDUCE_MIN, LOAM_REDUCE_MAX, LOAM_REDUCE_MAX_ABS };
 int loam_gpu_reduce(const double* x, int64_t n, int32_t kind, double* result, void* stream);
 
+/* ---- device-resident variants for CUDA-graph capture (extension) ---------
+ * No host synchronisation, scalars in device memory: a time-stepping loop
+ * built from them can be captured once and replayed (bench::run_wave,
+ * bench.hpp:222-300, in wave.py). */
+/* *result_dev = reduction of x (same order as loam_gpu_reduce). */
+int loam_gpu_reduce_dev(const double* x, int64_t n, int32_t kind, double* result_dev, void* stream);
+/* DirichletBC::apply with the constant read from device memory. */
+int loam_gpu_bc_apply_dev(double* dat, int32_t set_size, const int32_t* nodes, int32_t nnodes,
+                          const double* value_dev, void* stream);
+/* The run_wave clock on device state s[6] = {t, bc value, |p|, max |p| over
+ * t <= first_period, blow-up step (0 = none), steps}.  phase 0: s[1] =
+ * sin(10 pi t) (the marker-1 forcing, bench.hpp:237); phase 1 (after |p| is
+ * in s[2]): t += dt, steps += 1, the first-period maximum and the blow-up
+ * test |p| > 1e3 * max (bench.hpp:262-266) record the first failing step. */
+int loam_gpu_wave_clock(double* state_dev, double dt, double first_period, int32_t phase, void* stream);
+
 /* ---- topology / data services ------------------------------------------- */
 /* Map construction check (topology.hpp:45-48): every entry in [0, target). */
 int loam_gpu_map_check(const loam_map_desc* map, void* stream);

@@ -153,6 +153,9 @@ def lib() -> C.CDLL:
             "loam_gpu_bc_apply": (C.c_int, [vp, i32, vp, i32, vp, C.c_double, vp]),
             "loam_gpu_pointwise": (C.c_int, [vp, i64, i32, C.POINTER(PwInstr), i32, C.POINTER(vp), i32, vp]),
             "loam_gpu_reduce": (C.c_int, [vp, i64, i32, dp, vp]),
+            "loam_gpu_reduce_dev": (C.c_int, [vp, i64, i32, vp, vp]),
+            "loam_gpu_bc_apply_dev": (C.c_int, [vp, i32, vp, i32, vp, vp]),
+            "loam_gpu_wave_clock": (C.c_int, [vp, C.c_double, C.c_double, i32, vp]),
             "loam_gpu_p2_cell_node_map_dev": (C.c_int, [i32, i32, i32, vp, vp, ip, vp]),
             "loam_gpu_exterior_facets": (C.c_int, [i32, i32, i32, vp, C.POINTER(vp), C.POINTER(vp), ip, vp]),
         }
@@ -178,6 +181,7 @@ EXPORTED = [
     "loam_gpu_cg_solve_block",
     "loam_gpu_apply_dirichlet", "loam_gpu_bc_apply", "loam_gpu_pointwise", "loam_gpu_reduce",
     "loam_gpu_p2_cell_node_map_dev", "loam_gpu_exterior_facets",
+    "loam_gpu_reduce_dev", "loam_gpu_bc_apply_dev", "loam_gpu_wave_clock",
 ]
 
 

@@ -517,6 +517,30 @@ int loam_gpu_pointwise(double* out, int64_t n, int32_t op, const loam_pw_instr* 
   });
 }
 
+int loam_gpu_reduce_dev(const double* x, int64_t n, int32_t kind, double* result_dev, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(result_dev != nullptr, LOAM_ERR(InvalidArgument), "reduce without a result");
+    reduce(x, n, kind, result_dev, as_stream(stream));
+  });
+}
+
+int loam_gpu_bc_apply_dev(double* dat, int32_t set_size, const int32_t* nodes, int32_t nnodes,
+                          const double* value_dev, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(value_dev != nullptr, LOAM_ERR(InvalidArgument), "bc apply without a device value");
+    bc_apply(dat, set_size, nodes, nnodes, nullptr, 0.0, as_stream(stream), value_dev);
+  });
+}
+
+int loam_gpu_wave_clock(double* state_dev, double dt, double first_period, int32_t phase, void* stream) {
+  return guarded([&] {
+    require_device();
+    wave_clock(state_dev, dt, first_period, phase, as_stream(stream));
+  });
+}
+
 int loam_gpu_reduce(const double* x, int64_t n, int32_t kind, double* result, void* stream) {
   return guarded([&] {
     require_device();

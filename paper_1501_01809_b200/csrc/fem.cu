@@ -60,11 +60,27 @@ __global__ void k_dirichlet(const int64_t* __restrict__ rp, const int32_t* __res
 }
 
 __global__ void k_bc_apply(double* __restrict__ dat, const int32_t* __restrict__ nodes, int nn,
-                           const double* __restrict__ node_values, double constant) {
+                           const double* __restrict__ node_values, double constant,
+                           const double* __restrict__ constant_dev) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nn) return;
   const int r = nodes[i];
-  dat[r] = node_values ? node_values[r] : constant;
+  dat[r] = node_values ? node_values[r] : (constant_dev ? *constant_dev : constant);
+}
+
+// bench::run_wave's clock (bench.hpp:222-300) on device state
+// {t, bc value, |p|, first-period max, blow-up step, steps}
+__global__ void k_wave_clock(double* s, double dt, double first_period, int phase) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (phase == 0) {
+    s[1] = sin(10.0 * M_PI * s[0]);
+    return;
+  }
+  s[0] += dt;
+  s[5] += 1.0;
+  const double pn = s[2];
+  if (s[0] <= first_period) s[3] = fmax(s[3], pn);
+  if (s[4] == 0.0 && s[3] > 0.0 && pn > 1e3 * s[3]) s[4] = s[5];
 }
 
 // ---- pointwise: postfix program in shared memory, register stack ---------
@@ -190,12 +206,12 @@ void apply_dirichlet(const loam_sparsity_desc* sp, double* values, double* rhs, 
 }
 
 void bc_apply(double* dat, int set_size, const int32_t* nodes, int nn, const double* node_values, double constant,
-              cudaStream_t s) {
+              cudaStream_t s, const double* constant_dev) {
   require(nn >= 0 && (nn == 0 || (nodes != nullptr && dat != nullptr)), LOAM_ERR(InvalidArgument),
           "bc apply without data or nodes");
   (void)set_size;
   if (nn == 0) return;
-  k_bc_apply<<<ceil_div(nn, kThreads), kThreads, 0, s>>>(dat, nodes, nn, node_values, constant);
+  k_bc_apply<<<ceil_div(nn, kThreads), kThreads, 0, s>>>(dat, nodes, nn, node_values, constant, constant_dev);
   count_launch();
   LG_LAUNCH_CHECK();
 }
@@ -257,6 +273,13 @@ void reduce(const double* x, int64_t n, int kind, double* result_dev, cudaStream
   k_reduce1<<<nb, kThreads, 0, s>>>(x, n, kind, part.get());
   k_reduce2<<<1, 32, 0, s>>>(part.get(), nb, kind, result_dev);
   count_launch(2);
+  LG_LAUNCH_CHECK();
+}
+
+void wave_clock(double* state, double dt, double first_period, int phase, cudaStream_t s) {
+  require(state != nullptr && (phase == 0 || phase == 1), LOAM_ERR(InvalidArgument), "wave clock: bad arguments");
+  k_wave_clock<<<1, 32, 0, s>>>(state, dt, first_period, phase);
+  count_launch();
   LG_LAUNCH_CHECK();
 }
 

@@ -90,3 +90,61 @@ class WaveLoop:
             self.step()
         torch.cuda.synchronize()
         return self.samples
+
+    # ---- the same chain as one CUDA graph per batch of steps -----------------
+    # The per-step host work (|p| read-back, the forcing value, ctypes calls)
+    # dominates a 512^2 step; with the forcing, |p|, the first-period maximum
+    # and the blow-up test kept in device state (loam_gpu_wave_clock) a batch
+    # of steps is captured once and replayed, and the host reads the state
+    # once per batch.  Blow-up is reported at the first failing step of the
+    # batch (the fields of the later steps of that batch are then discarded
+    # with the error, as the reference discards them when it throws).
+
+    def _device_step(self, state):
+        lib, sh = capi.lib(), torch.cuda.current_stream().cuda_stream
+        sp = state.data_ptr()
+        capi.check(lib.loam_gpu_wave_clock(sp, self.dt, 0.2, 0, sh))
+        L.pointwise(self.phi, L.PwOp.SUB, self.half)
+        self.b.zero()
+        L.execute(self.action)
+        L.pointwise(self.p, L.PwOp.ADD, self.kick)
+        capi.check(lib.loam_gpu_bc_apply_dev(self.p.data.data_ptr(), self.p.set.size, self.bc._dev.data_ptr(),
+                                             len(self.bc.nodes), sp + 8, sh))
+        L.pointwise(self.phi, L.PwOp.SUB, self.half)
+        capi.check(lib.loam_gpu_reduce_dev(self.p.data.data_ptr(), self.p.set.size, capi.REDUCE_MAX_ABS, sp + 16, sh))
+        capi.check(lib.loam_gpu_wave_clock(sp, self.dt, 0.2, 1, sh))
+
+    def run_graph(self, batch: int = 100, max_steps: int | None = None):
+        """run() through CUDA graphs of `batch` steps (`batch` divides 100, so the
+        every-100-steps diagnostics fall on batch boundaries); the steps after
+        the last full batch run one by one as in run()."""
+        assert batch >= 1 and 100 % batch == 0
+        t, remaining = self.t, 0  # the step count run() would take (same double arithmetic)
+        while t <= self.T and (max_steps is None or remaining < max_steps):
+            t += self.dt
+            remaining += 1
+        self.b.zero()
+        L.execute(self.action)  # the par_loop's plan is built and cached outside the capture
+        state = torch.tensor([self.t, 0.0, 0.0, self.first_period_max, 0.0, float(self.steps)],
+                             dtype=torch.float64, device="cuda")
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(batch):
+                self._device_step(state)
+        torch.cuda.current_stream().wait_stream(side)
+        while remaining >= batch and self.steps % batch == 0:
+            g.replay()
+            remaining -= batch
+            h = state.cpu().numpy()
+            self.t, pnorm, self.first_period_max, self.steps = float(h[0]), float(h[2]), float(h[3]), int(h[5])
+            if h[4] != 0.0:
+                raise capi.LoamError(1 + capi.ERROR_KINDS.index("InstabilityDetected"),
+                                     f"wave field blew up at step {int(h[4])}")
+            if self.steps % 100 == 0:
+                self.samples.append((self.t, pnorm, L.inf_norm(self.phi), self.energy()))
+        for _ in range(remaining):
+            self.step()
+        torch.cuda.synchronize()
+        return self.samples

@@ -151,3 +151,16 @@ def test_wave_chain_reproduces_reference_run_wave(gpu_lib):  # bench.hpp:222-300
     assert got.shape == ref.shape and got.shape[0] >= 3
     assert np.array_equal(got[:, 0], ref[:, 0])  # sample times
     assert np.max(np.abs(got[:, 1:] - ref[:, 1:]) / np.abs(ref[:, 1:])) <= 1e-10
+
+
+@pytest.mark.parametrize("batch", [1, 10, 50])
+def test_wave_chain_in_cuda_graphs(gpu_lib, batch):
+    """The run_wave chain captured once per batch of steps (device-resident
+    forcing, |p|, blow-up test) and replayed: the samples equal the
+    reference's to 1e-10 and the host-driven chain's sample times exactly."""
+    from paper_1501_01809_b200.wave import WaveLoop
+    ref = O.ref_run_wave(8, 1e-3, 0.3)
+    got = np.array(WaveLoop(8, 1e-3, 0.3).run_graph(batch))
+    assert got.shape == ref.shape and got.shape[0] >= 3
+    assert np.array_equal(got[:, 0], ref[:, 0])
+    assert np.max(np.abs(got[:, 1:] - ref[:, 1:]) / np.abs(ref[:, 1:])) <= 1e-10
