@@ -1224,7 +1224,6 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
   uint64_t* empty = full + 3;
   int* slot_tile = reinterpret_cast<int*>(full + 6); // [3] tile id carried by each ring stage (-1: done)
   const int tid = threadIdx.x;
-  if (blockIdx.x == 0 && tid == 0) *a.reset_tile = 0;
   if (tid == 0) {
     for (int b = 0; b < 3; ++b) {
       mbar_init(&full[b], 1);
@@ -1452,6 +1451,7 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
   // the segment must outlive its bulk store's shared-memory reads; the global
   // writes themselves complete with the grid
   if (F::BILINEAR && tid == 0) bulk_wait_read<0>();
+  tile_counter_release(a.next_tile, a.reset_tile, kTileThreads, tid);
   if (a.timing && (tid & 31) == 0) {
     atomicAdd(a.timing, (unsigned long long)t_first);
     atomicAdd(a.timing + 1, (unsigned long long)t_wait);
@@ -1551,7 +1551,6 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
   uint64_t* empty = full + kPS;
   int* slot_tile = reinterpret_cast<int*>(full + 6);
   const int tid = threadIdx.x;
-  if (blockIdx.x == 0 && tid == 0) *a.reset_tile = 0;
   if (tid == 0) {
     for (int b = 0; b < kPS; ++b) {
       mbar_init(&full[b], 1);
@@ -1763,6 +1762,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
       named_bar(1, NT);
     }
   }
+  tile_counter_release(a.next_tile, a.reset_tile, NT, tid);
 }
 
 constexpr int kPTileThreads = 128;
@@ -2652,9 +2652,8 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     RingArgs t{};
     t.tiles = nb.rtiles.get();
     t.ntiles = nb.ntiles;
-    t.next_tile = P->counter.get() + P->parity;
-    t.reset_tile = P->counter.get() + (P->parity ^ 1);
-    P->parity ^= 1;
+    t.next_tile = P->counter.get();      // tile counter
+    t.reset_tile = P->counter.get() + 1; // exit count (tile_counter_release)
     t.nptr = nb.nptr.get();
     t.rptr = nb.rptr.get();
     t.recs = nb.rrecs.get();
@@ -2723,20 +2722,17 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
   }
   if (P->use_rtile) {
     launch_rtile(P->rt, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
-                 P->counter.get() + P->parity, P->counter.get() + (P->parity ^ 1), s);
-    P->parity ^= 1;
+                 P->counter.get(), P->counter.get() + 1, s);
     return;
   }
   if (P->use_ntile) {
     launch_ntile(P->nt, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
-                 P->counter.get() + P->parity, P->counter.get() + (P->parity ^ 1), s);
-    P->parity ^= 1;
+                 P->counter.get(), P->counter.get() + 1, s);
     return;
   }
   if (P->use_etile) {
     launch_etile(k.form, P->et, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
-                 P->counter.get() + P->parity, P->counter.get() + (P->parity ^ 1), s);
-    P->parity ^= 1;
+                 P->counter.get(), P->counter.get() + 1, s);
     return;
   }
   if (P->use_ptile) {
@@ -2744,9 +2740,8 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     PTileArgs t{};
     t.tiles = pt.tiles.get();
     t.ntiles = pt.ntiles;
-    t.next_tile = P->counter.get() + P->parity;
-    t.reset_tile = P->counter.get() + (P->parity ^ 1);
-    P->parity ^= 1;
+    t.next_tile = P->counter.get();      // tile counter
+    t.reset_tile = P->counter.get() + 1; // exit count (tile_counter_release)
     t.pptr = pt.pptr.get();
     t.nptr = pt.nptr.get();
     t.recs = pt.recs.get();

@@ -536,7 +536,6 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
   int* slot_tile = reinterpret_cast<int*>(sm + 48);
   uint32_t* ktab = reinterpret_cast<uint32_t*>(sm + 64);
   const int tid = threadIdx.x;
-  if (blockIdx.x == 0 && tid == 0) *a.reset_tile = 0;
   if (tid < 12) ktab[tid] = a.ktab[tid];
   if (tid == 0) {
     for (int q = 0; q < STAGES; ++q) {
@@ -829,6 +828,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
     }
   }
   if (tid == 0) bulk_wait_read<0>();
+  tile_counter_release(a.next_tile, a.reset_tile, NT, tid);
 }
 
 __global__ void k_et_zero(const int32_t* __restrict__ pos, int64_t n, int cd, double* __restrict__ out) {

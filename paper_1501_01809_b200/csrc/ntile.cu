@@ -260,7 +260,6 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
   uint64_t* empty = full + STAGES;
   int* slot_tile = reinterpret_cast<int*>(sm + 48);
   const int tid = threadIdx.x;
-  if (blockIdx.x == 0 && tid == 0) *a.reset_tile = 0;
   if (tid == 0) {
     for (int q = 0; q < STAGES; ++q) {
       mbar_init(&full[q], 1);
@@ -466,6 +465,7 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
     }
   }
   if (tid == 0) bulk_wait_read<0>();
+  tile_counter_release(a.next_tile, a.reset_tile, NT, tid);
 }
 
 } // namespace

@@ -270,7 +270,6 @@ __global__ void __launch_bounds__(NT + 32, 1) k_rtile(const __grid_constant__ Rt
   uint64_t* empty = full + STAGES;
   int* slot_tile = reinterpret_cast<int*>(sm + 48);
   const int tid = threadIdx.x;
-  if (blockIdx.x == 0 && tid == 0) *a.reset_tile = 0;
   if (tid == 0) {
     for (int q = 0; q < STAGES; ++q) {
       mbar_init(&full[q], 1);
@@ -472,6 +471,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_rtile(const __grid_constant__ Rt
     }
   }
   if (tid == 0) bulk_wait_read<0>();
+  tile_counter_release(a.next_tile, a.reset_tile, NT, tid);
 }
 
 template <class F>

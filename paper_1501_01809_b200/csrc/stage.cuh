@@ -63,4 +63,18 @@ __device__ __forceinline__ uint32_t stage_runs(const RunSet& s, int lane, uint64
   return tx;
 }
 
+// Persistent tile kernels grab tiles from a global counter.  The last CTA to
+// finish puts the counter (and the exit count) back to zero, so every launch
+// -- including a replay of a captured CUDA graph with frozen arguments --
+// starts from tile 0.  Called by all `nconsumers` consumer threads after their
+// last tile (the producer warp has grabbed its last tile before the consumers
+// see the end marker).
+__device__ __forceinline__ void tile_counter_release(int* next_tile, int* done, int nconsumers, int tid) {
+  named_bar(1, nconsumers);
+  if (tid == 0 && atomicAdd(done, 1) == (int)gridDim.x - 1) { // the launch boundary orders these for the next launch
+    *next_tile = 0;
+    *done = 0;
+  }
+}
+
 } // namespace loam_gpu
