@@ -10,6 +10,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <memory>
+#include <mutex>
+#include <unordered_map>
 #include <stdexcept>
 #include <string>
 
@@ -85,6 +87,20 @@ private:
 };
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+// Raise a kernel's dynamic shared-memory limit to at least `smem`, once per
+// kernel (keyed by the kernel's address: instantiations that share a function
+// type must not share the cache).
+inline void ensure_dynamic_smem(const void* kern, size_t smem) {
+  static std::mutex m;
+  static std::unordered_map<const void*, size_t> done;
+  std::lock_guard<std::mutex> g(m);
+  size_t& cur = done[kern];
+  if (cur < smem) {
+    LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+}
 
 constexpr int kNumSMs = 148; // B200
 

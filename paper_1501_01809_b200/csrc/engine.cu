@@ -1781,11 +1781,7 @@ void launch_ptile(const PTileArgs& a, size_t smem_base, size_t buf, cudaStream_t
   if (a.ntiles == 0) return;
   auto go = [&](auto kern, int stages) {
     const size_t smem = smem_base + stages * buf;
-    static size_t attr = 0;
-    if (attr < smem) {
-      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int blocks = 1;
     LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kPTileThreads + 32, smem));
     const int grid = std::min(a.ntiles, std::max(blocks, 1) * kNumSMs);
@@ -1859,16 +1855,10 @@ template <class F>
 void launch_nbr(const TileArgs& a, int rec_bytes, size_t smem, cudaStream_t s) {
   if (a.ntiles == 0) return;
   auto go = [&](auto kern) {
-    static int per_sm = -1;
-    static size_t attr_smem = 0;
-    if (attr_smem < smem) {
-      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_smem = smem;
-      per_sm = -1;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int blocks = 1;
     LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kTileBlock, smem));
-    per_sm = blocks > 0 ? blocks : 1;
+    const int per_sm = blocks > 0 ? blocks : 1;
     const int grid = std::min(a.ntiles, per_sm * kNumSMs);
     kern<<<grid, kTileBlock, smem, s>>>(a);
   };
@@ -1895,11 +1885,7 @@ template <class F>
 void launch_patch(const PatchArgs& a, size_t smem, cudaStream_t s) {
   if (a.npatches == 0) return;
   auto go = [&](auto kern) {
-    static size_t attr = 0;
-    if (attr < smem) {
-      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int blocks = 1;
     LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kPatchThreads, smem));
     require(blocks > 0, LOAM_GPU_ERR_CUDA, "patch kernel does not fit on an SM");

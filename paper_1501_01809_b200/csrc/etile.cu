@@ -688,6 +688,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
       L = srow[row + 1] - s0;
       const int np = (a.dbg & 1) ? 0 : npair[row];
       int pconst[3] = {0, 0, 0}; // compact: ranks of canonical columns CA, CB, NV (the row's own)
+      double creg[3] = {0.0, 0.0, 0.0};
       if constexpr (COMPACT) {
         const uint32_t rc = rconst[row];
         pconst[0] = 32 * (int)(rc & 0xffu);
@@ -742,11 +743,27 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
 #pragma unroll
           for (int j = 0; j < N; ++j) pos[j] = 32 * (int)((w[(2 + j) >> 2] >> (8 * ((2 + j) & 3))) & 0xffu);
         }
-        double cur[N];
+        if constexpr (COMPACT) {
+          // the row's own edge and its two endpoint vertices: same entry for
+          // every pair of the row -> register sums (same order), stored once
+          // after the loop; the other columns by read-modify-write
+          creg[0] += o[T::CA];
+          creg[1] += o[T::CB];
+          creg[2] += o[NV];
+          double cur[N];
 #pragma unroll
-        for (int j = 0; j < N; ++j) cur[j] = my[pos[j]];
+          for (int j = 0; j < N; ++j)
+            if (j != T::CA && j != T::CB && j != NV) cur[j] = my[pos[j]];
 #pragma unroll
-        for (int j = 0; j < N; ++j) my[pos[j]] = cur[j] + o[j];
+          for (int j = 0; j < N; ++j)
+            if (j != T::CA && j != T::CB && j != NV) my[pos[j]] = cur[j] + o[j];
+        } else {
+          double cur[N];
+#pragma unroll
+          for (int j = 0; j < N; ++j) cur[j] = my[pos[j]];
+#pragma unroll
+          for (int j = 0; j < N; ++j) my[pos[j]] = cur[j] + o[j];
+        }
         if (h & 0x4000u) {
           dA += dga;
           hA = true;
@@ -754,6 +771,13 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
         if (h & 0x8000u) {
           dB += dgb;
           hB = true;
+        }
+      }
+      if constexpr (COMPACT) {
+        if (np > 0) {
+          my[pconst[0]] = creg[0];
+          my[pconst[1]] = creg[1];
+          my[pconst[2]] = creg[2];
         }
       }
       // vertex rows: transposed vertex-column entries, the vertex pair, diagonals
@@ -847,11 +871,7 @@ template <int FORM, int D, int CD>
 void go_etile(const EtilePlan& p, const EtileArgs& a, size_t smem_base, size_t buf, cudaStream_t s) {
   auto go = [&](auto kern, int threads, int stages) {
     const size_t smem = smem_base + stages * buf;
-    static size_t attr = 0;
-    if (attr < smem) {
-      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int blocks = 1;
     LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, threads, smem));
     require(blocks > 0, LOAM_GPU_ERR_CUDA, "edge-tile kernel does not fit on an SM");

@@ -497,11 +497,7 @@ void launch_ntile(const NtilePlan& p, const double* coords, double* out, const F
   static const int st = std::getenv("LOAM_GPU_NT_STAGES") ? std::atoi(std::getenv("LOAM_GPU_NT_STAGES")) : 2;
   auto go = [&](auto kern, int stages) {
     const size_t smem = (size_t)off + stages * (size_t)a.buf_bytes;
-    static size_t attr = 0;
-    if (attr < smem) {
-      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int blocks = 1;
     LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kNtThreads + 32, smem));
     require(blocks > 0, LOAM_GPU_ERR_CUDA, "node-tile kernel does not fit on an SM");

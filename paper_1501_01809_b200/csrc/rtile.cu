@@ -478,11 +478,7 @@ template <class F>
 void go_rtile(const RtilePlan& p, const RtileArgs& a, size_t base, size_t buf, cudaStream_t s) {
   auto go = [&](auto kern, int threads, int stages) {
     const size_t smem = base + stages * buf;
-    static size_t attr = 0;
-    if (attr < smem) {
-      LG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
+    ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
     int blocks = 1;
     LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, threads, smem));
     require(blocks > 0, LOAM_GPU_ERR_CUDA, "row-tile kernel does not fit on an SM");
