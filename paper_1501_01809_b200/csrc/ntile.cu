@@ -449,6 +449,10 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
       named_bar(1, NT);
       for (int t = tid; t < len; t += NT) a.out[(int64_t)E0 + t] += seg[t];
       named_bar(1, NT);
+    } else if (a.dbg & 4) { // developer: coalesced thread stores instead of the bulk store
+      named_bar(1, NT);
+      for (int t = tid; t < len; t += NT) a.out[(int64_t)E0 + t] = seg[t];
+      named_bar(1, NT);
     } else {
       fence_async_shared();
       named_bar(1, NT);
