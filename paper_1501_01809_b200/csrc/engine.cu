@@ -415,6 +415,50 @@ __device__ __forceinline__ void cell_gather(const CellArgs& a, int e, double (&X
 #ifndef LOAM_GPU_CELL_MINB
 #define LOAM_GPU_CELL_MINB 1
 #endif
+// The same with the warp's 32 map rows staged through shared memory by
+// coalesced 16-byte loads: used when the row, coefficient and coordinate maps
+// are one sorted map whose first gdim+1 entries are the vertices (P2 actions,
+// config 3).  One thread's 10-entry row is 40 scattered bytes per lane
+// otherwise -- 10 load instructions touching ~40 sectors each per warp.
+template <class F>
+__global__ void __launch_bounds__(128) k_cell_vec_rows(const __grid_constant__ CellArgs a) {
+  constexpr int NRN = F::NRN, GD = F::GD, NV = GD + 1;
+  static_assert((32 * NRN) % 4 == 0, "row block of a warp must be a whole number of int4");
+  __shared__ __align__(16) int32_t rows_s[4][32 * NRN];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t c0 = ((int64_t)blockIdx.x * 4 + wl) * 32;
+  if (c0 >= a.n) return;
+  const int ncell = a.n - c0 < 32 ? (int)(a.n - c0) : 32;
+  const int nint = ncell * NRN;
+  const int32_t* src = a.rmap + c0 * NRN;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    for (int q = lane; q < nint / 4; q += 32)
+      reinterpret_cast<int4*>(rows_s[wl])[q] = __ldg(reinterpret_cast<const int4*>(src) + q);
+    for (int q = (nint / 4) * 4 + lane; q < nint; q += 32) rows_s[wl][q] = __ldg(src + q);
+  } else {
+    for (int q = lane; q < nint; q += 32) rows_s[wl][q] = __ldg(src + q);
+  }
+  __syncwarp();
+  if (lane >= ncell) return;
+  const int32_t* row = rows_s[wl] + lane * NRN;
+  int nodes[NRN];
+#pragma unroll
+  for (int i = 0; i < NRN; ++i) nodes[i] = row[i];
+  double X[NV][GD], C[F::NCOEFF];
+#pragma unroll
+  for (int q = 0; q < F::NCOEFF; ++q) C[q] = __ldg(a.coeff + nodes[q]);
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int c = 0; c < GD; ++c) X[v][c] = __ldg(a.coords + (int64_t)nodes[v] * GD + c);
+  Geom<GD> G;
+  geometry<GD>(X, G);
+  double y[NRN];
+  ElemVec<F>::all(G, C, a.prm, y);
+#pragma unroll
+  for (int i = 0; i < NRN; ++i) atomicAdd(a.out + nodes[i], y[i]);
+}
+
 template <class F, bool AGG>
 __global__ void __launch_bounds__(128, LOAM_GPU_CELL_MINB) k_cell_vec(const __grid_constant__ CellArgs a) {
   const int e0 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -470,6 +514,17 @@ void launch_cell(const CellArgs& a, bool agg, cudaStream_t s) {
     if (agg) k_cell_mat<F, true><<<grid, 128, 0, s>>>(a);
     else k_cell_mat<F, false><<<grid, 128, 0, s>>>(a);
   } else {
+    // one sorted map for rows, coefficients and (its vertex prefix) coordinates
+    const bool one_map = F::HAS_COEFF && F::NCOEFF == F::NRN && a.rmap == a.cmap && a.xmap == a.cmap &&
+                         a.cstride == F::NRN && a.xstride == F::NRN && !std::getenv("LOAM_GPU_NO_CELL_ROWS");
+    if constexpr (F::HAS_COEFF && F::NCOEFF == F::NRN) {
+      if (!agg && one_map) {
+        k_cell_vec_rows<F><<<ceil_div(a.n, 128), 128, 0, s>>>(a);
+        count_launch();
+        LG_LAUNCH_CHECK();
+        return;
+      }
+    }
     if (agg) k_cell_vec<F, true><<<grid, 128, 0, s>>>(a);
     else k_cell_vec<F, false><<<grid, 128, 0, s>>>(a);
   }
@@ -2333,6 +2388,13 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
         P->cptr = P->cmap.v.get();
       }
       P->cstride = Cm->arity;
+      // vertex ids = the coefficient map's first gdim+1 entries (P2 vertices
+      // first): one sorted map serves rows, coefficients and coordinates
+      if (P->cptr == P->crows.v.get() && prefix_equal(Cm->values, Cm->arity, X->values, X->arity, X->arity, n, s)) {
+        P->xptr = P->cptr;
+        P->xstride = P->cstride;
+        P->xmap.v.release();
+      }
     }
     return P;
   }
