@@ -2152,8 +2152,8 @@ NodeMap node_view(const loam_map_desc* m) {
 }
 
 struct FastPlan {
-  DevBuf<int> counter; // dynamic tile scheduler: two ping-pong counters
-  int parity = 0;
+  DevBuf<int> counter; // dynamic tile scheduler: [0] next tile, [1] exit count (stage.cuh:tile_counter_release)
+
   bool use_nbr = false;
   NbrPlan nb;
   bool use_ptile = false;
