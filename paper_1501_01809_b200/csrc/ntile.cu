@@ -37,6 +37,7 @@ int make_runs(std::vector<int>& ids, int limit, std::vector<std::pair<int, int>>
 }
 
 constexpr int kNV = 4;        // P1 tet
+constexpr int kNtConsumers = 128; // consumer threads per CTA (= k_ntile's NT)
 #ifndef LOAM_GPU_NT_SPLIT
 #define LOAM_GPU_NT_SPLIT 4
 #endif
@@ -176,6 +177,27 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
       items.push_back(it);
     }
     prec.insert(prec.end(), dprec.begin(), dprec.end());
+    // lane-interleaved records: the items run in rounds of kNtConsumers
+    // threads; pair q of the item on lane l of round r sits at
+    // block(r) + q * kNtConsumers + l (the lanes of a warp read consecutive
+    // half-words: no shared-memory bank conflicts)
+    {
+      std::vector<uint16_t> inter;
+      for (size_t r0i = 0; r0i < items.size(); r0i += kNtConsumers) {
+        const size_t r1i = std::min(items.size(), r0i + kNtConsumers);
+        int pm = 0;
+        for (size_t i = r0i; i < r1i; ++i) pm = std::max<int>(pm, items[i].np);
+        const size_t blk = inter.size();
+        inter.resize(blk + (size_t)pm * kNtConsumers, 0);
+        for (size_t i = r0i; i < r1i; ++i) {
+          const int l = (int)(i - r0i);
+          for (int q = 0; q < items[i].np; ++q) inter[blk + (size_t)q * kNtConsumers + l] = prec[items[i].poff + q];
+          if (blk + l > 65535) return false;
+          items[i].poff = (uint16_t)(blk + l);
+        }
+      }
+      prec.swap(inter);
+    }
     const int nitems = (int)items.size(), npairs = (int)prec.size(), ncell = (int)cells.size(),
               ndiag = (int)diaginfo.size() / 2;
     const int off_items = 0, off_pairs = up16(nitems * 8), off_diag = off_pairs + up16(npairs * 2),
@@ -384,7 +406,7 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
       double acc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
       // software pipeline: pair q+1's record and gradients load during pair q's FMAs
       auto fetch = [&](int q, double (&ga)[3], double (&gb)[3]) {
-        const uint32_t x = prec[poff + q];
+        const uint32_t x = prec[poff + q * NT];
         const double* g = geo + (x >> 4) * kGS;
         const int lv = (x >> 2) & 3, lw = x & 3;
         const double2 a0 = reinterpret_cast<const double2*>(g + 4 * lv)[0];
