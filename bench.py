@@ -204,6 +204,35 @@ def protocol_floor(torch, flush, stream, reps=10):
     return out
 
 
+def config_table(torch, flush, stream, steps=5):
+    """Every BASELINE config at full size through `auto` (the same flushed
+    per-step protocol as the headline, median of `steps`): cells/s and the
+    fraction of the measured HBM peak, so the contract line carries the whole
+    table measured on the same box."""
+    from paper_1501_01809_b200 import capi, configs
+    peak, _ = peaks()
+    names = {(1, None): "C1 P1 Helmholtz residual 512^2", (2, None): "C2 P1 Laplace CSR 1024^2",
+             (3, "residual"): "C3 P2 Helmholtz residual 64^3", (3, "matrix"): "C3 P2 Helmholtz CSR 64^3",
+             (4, None): "C4 vector-P1 elasticity 96^3", (5, None): "C5 Taylor-Hood blocks 768^2"}
+    rows = []
+    capi.set_strategy("auto")
+    for (cfg, part), name in names.items():
+        w = configs.Workload(cfg, None, part)
+        w.reset()
+        w.run()
+        for _ in range(2):
+            w.reset()
+            flush()
+            w.run()
+        ms = float(np.median(time_steps(torch, w, steps, flush, stream)))
+        ab = algorithmic_bytes(w)
+        rows.append({"config": name, "ms": round(ms, 4), "cells_per_s": w.inputs.ncells / (ms * 1e-3),
+                     "frac": round(ab / (ms * 1e-3) / 1e9 / peak, 3)})
+        del w
+        torch.cuda.empty_cache()
+    return rows
+
+
 def e2e_host(torch, w, steps, warmup):
     """The same assembly through the host-memory C ABI with pinned host
     buffers: every step copies the Dats the loop reads host->device and the
@@ -369,6 +398,7 @@ def gpu_arm(args):
         print("e2e step ms:", [round(t, 3) for t in e2e_times], file=sys.stderr)
     e2e_ms = max_over_ranks(float(np.mean(e2e_times)), "cuda")
     floor = protocol_floor(torch, flush, stream)
+    table = config_table(torch, flush, stream) if rank == 0 and not args.no_config_table else None
     # correctness spot check of this very run against the reference pattern size
     line = None
     if rank == 0:
@@ -401,6 +431,7 @@ def gpu_arm(args):
                          "algorithmic_bytes": abytes, "kernel_ms": kernel_ms, "peak_kind": peak_kind,
                          "protocol_floor": floor},
             "cpu_baseline": cpu,
+            "all_configs": table,
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }
@@ -586,6 +617,7 @@ def main():
     ap.add_argument("--impl", default="loam_gpu", choices=["loam_gpu", "reference"])
     ap.add_argument("--strategy", default="auto", choices=["auto", "owner", "atomic", "color", "nbr", "warpagg", "patch"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config-table", action="store_true", help="skip the per-config table in the line")
     ap.add_argument("--all-configs", action="store_true")
     ap.add_argument("--configs", default="")
     ap.add_argument("--strategies", default="auto,owner,atomic,warpagg,color,patch")

@@ -8,7 +8,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref
 timeout 1500 python bench.py --all-configs --steps 10 ${STRATS:+--strategies $STRATS} > $O/strategies_all_configs.jsonl 2> $O/all.err; echo all_rc=$?
 python tools/table.py $O/strategies_all_configs.jsonl > $O/strategies_all_configs.txt
 python tools/c5_split.py > $O/c5_split.txt 2>&1
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 80 --csv --log-file $O/launches_c2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1; echo launch_rc=$?
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 80 --csv --log-file $O/launches_c2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config-table > $O/ncu_launch.log 2>&1; echo launch_rc=$?
 summ() { python tools/ncu_summary.py $1.ncu-rep 20 > $1.txt 2>&1; python tools/ncu_lines.py $1.ncu-rep 25 >> $1.txt 2>&1; ncu -i $1.ncu-rep --page raw --csv > $1_raw.csv 2>/dev/null; rm -f $1.ncu-rep; }
 ncu --set full --clock-control none --import-source on -k regex:k_etile -s 2 -c 1 -o $O/cfg3m python bench.py --all-configs --configs 3m --strategies auto --steps 3 > $O/ncu_cfg3m.log 2>&1; echo ncu_3m_rc=$?
 summ $O/cfg3m
@@ -20,7 +20,7 @@ ncu --set full --clock-control none --import-source on -k regex:k_rtile -s 1 -c 
 summ $O/cfg5b
 ncu --set full --clock-control none --import-source on -k regex:k_star -s 2 -c 1 -o $O/cfg1 python bench.py --all-configs --configs 1 --strategies auto --steps 3 > $O/ncu_cfg1.log 2>&1; echo ncu_1_rc=$?
 summ $O/cfg1
-ncu --set full --clock-control none --import-source on -k regex:k_ring -s 5 -c 1 -o $O/c2_ring python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_c2.log 2>&1; echo ncu_c2_rc=$?
+ncu --set full --clock-control none --import-source on -k regex:k_ring -s 5 -c 1 -o $O/c2_ring python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config-table > $O/ncu_c2.log 2>&1; echo ncu_c2_rc=$?
 summ $O/c2_ring
 ncu --set full --clock-control none --import-source on -k regex:k_cell -s 2 -c 1 -o $O/cfg3r python bench.py --all-configs --configs 3r --strategies auto --steps 3 > $O/ncu_cfg3r.log 2>&1; echo ncu_3r_rc=$?
 summ $O/cfg3r
