@@ -2459,7 +2459,8 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     const bool et_form = ((k.form == F_MASS || k.form == F_STIFFNESS || k.form == F_HELMHOLTZ) &&
                           k.nrn == (k.gd == 2 ? 6 : 10) && k.ncn == k.nrn && k.rd == 1 && k.cd == 1) ||
                          (k.form == F_STOKES_A && k.rd == 2 && k.cd == 2);
-    if (strat == 0 && et_form && !std::getenv("LOAM_GPU_NO_ETILE") && R.dim == k.rd && Cn.dim == k.cd &&
+    if (strat == 0 && et_form && !std::getenv("LOAM_GPU_NO_ETILE") && !(k.form == F_STOKES_A && rtile_form(k.form)) &&
+        R.dim == k.rd && Cn.dim == k.cd &&
         (reinterpret_cast<uintptr_t>(args[1].data) & 15) == 0 && Cn.v.arity == R.v.arity &&
         (Cn.v.v == R.v.v || prefix_equal(Cn.v.v, Cn.v.arity, R.v.v, R.v.arity, R.v.arity, n, s)) &&
         pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, k.rd, k.cd, sp->row_ptr, sp->col_idx, sp->nnz, s)) {

@@ -43,7 +43,8 @@ int make_runs(std::vector<int>& ids, int limit, std::vector<std::pair<int, int>>
 // selects the row tiles for B^T as well.
 bool rtile_form(int form) {
   static const bool bt = std::getenv("LOAM_GPU_RTILE_BT") != nullptr;
-  return form == F_STOKES_B || (bt && form == F_STOKES_BT);
+  static const bool av = std::getenv("LOAM_GPU_RTILE_A") != nullptr;
+  return form == F_STOKES_B || (bt && form == F_STOKES_BT) || (av && form == F_STOKES_A);
 }
 
 bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn, int ncn, int rd, int cd,
@@ -434,12 +435,14 @@ __global__ void __launch_bounds__(NT + 32, 1) k_rtile(const __grid_constant__ Rt
 #pragma unroll
           for (int j = 0; j < NCN; ++j)
 #pragma unroll
-            for (int c = 0; c < CD; ++c) cur[j * CD + c] = my[32 * (d * CD * Lm + pos[j] * CD + c)];
+            for (int c = 0; c < CD; ++c)
+              if (!diag_block<F>::value || d == c) cur[j * CD + c] = my[32 * (d * CD * Lm + pos[j] * CD + c)];
 #pragma unroll
           for (int j = 0; j < NCN; ++j)
 #pragma unroll
             for (int c = 0; c < CD; ++c)
-              my[32 * (d * CD * Lm + pos[j] * CD + c)] = cur[j * CD + c] + blk[d * NC + j * CD + c];
+              if (!diag_block<F>::value || d == c) // structurally zero blocks (Stokes A) keep the zero-fill
+                my[32 * (d * CD * Lm + pos[j] * CD + c)] = cur[j * CD + c] + blk[d * NC + j * CD + c];
         }
       }
     }
@@ -519,6 +522,7 @@ void launch_rtile(const RtilePlan& p, const double* coords, double* out, const F
   a.b_win = up16(p.max_blob);
   a.buf_bytes = a.b_win + up16(p.max_slots * 2 * 8 + 16);
   if (p.form == F_STOKES_B) go_rtile<FormT<F_STOKES_B, 2, 2>>(p, a, off, a.buf_bytes, s);
+  else if (p.form == F_STOKES_A) go_rtile<FormT<F_STOKES_A, 2, 2>>(p, a, off, a.buf_bytes, s);
   else if (p.form == F_STOKES_BT) go_rtile<FormT<F_STOKES_BT, 2, 2>>(p, a, off, a.buf_bytes, s);
   else fail(LOAM_ERR(InvalidArgument), "row tiles: unsupported form");
   count_launch();
