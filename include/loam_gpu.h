@@ -323,6 +323,25 @@ int loam_gpu_p2_cell_node_map_dev(int32_t ncells, int32_t nverts, int32_t gdim, 
 int loam_gpu_exterior_facets(int32_t ncells, int32_t nverts, int32_t gdim, const int32_t* cv,
                              int32_t** facet_vertices, int32_t** facet_cell, int32_t* nfacets,
                              void* stream);
+/* rcm_order (topology.hpp:131-178): reverse Cuthill-McKee over adjacency
+ * lists given as CSR (row_ptr device [n+1], col_idx device), bit-exact with
+ * the reference: seeds of minimum degree (lowest index) per component,
+ * neighbours in (degree, index) order, reversed.  degree = list length.
+ * order: device [n], order[new] = old.  IndexOutOfRange / AsymmetricAdjacency
+ * at the first offending entry in list order, as the reference scans. */
+int loam_gpu_rcm_order(int32_t n, const int64_t* row_ptr, const int32_t* col_idx, int32_t* order,
+                       void* stream);
+/* vertex_adjacency (mesh.hpp:350-362): per vertex the sorted other vertices
+ * sharing a cell, as CSR (device arrays allocated here, loam_gpu_free). */
+int loam_gpu_vertex_adjacency(int32_t ncells, int32_t nverts, int32_t gdim, const int32_t* cv,
+                              int64_t** row_ptr, int32_t** col_idx, int64_t* nnz, void* stream);
+/* The renumbering half of reorder (mesh.hpp:369-386) for a given perm
+ * (perm[new] = old, device [nverts]): coords_out[new] = coords[perm[new]]
+ * (may be null), cv_out[k] = new_of[cv[k]].  InvalidArgument when perm is not
+ * a permutation. */
+int loam_gpu_renumber_vertices(int32_t nverts, int32_t gdim, const double* coords, int32_t ncells,
+                               const int32_t* cv, const int32_t* perm, double* coords_out, int32_t* cv_out,
+                               void* stream);
 
 /* ---- device memory helpers (for FFI callers without a CUDA binding) ------ */
 int loam_gpu_malloc(void** ptr, size_t bytes);

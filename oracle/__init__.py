@@ -506,3 +506,60 @@ def ref_exterior_facets(gdim, cv, nv):
     L.ref_free(fv)
     L.ref_free(fc)
     return a.reshape(n, gdim), b.reshape(n, 2)
+
+
+# ------------------------------------------- vertex renumbering (8f-4: RCM)
+def _csr_of_lists(adj):
+    rp = np.zeros(len(adj) + 1, np.int64)
+    rp[1:] = np.cumsum([len(a) for a in adj])
+    ci = np.array([v for a in adj for v in a], np.int32) if rp[-1] else np.zeros(0, np.int32)
+    return rp, ci
+
+
+def rcm_order(adj, lib="orc"):
+    """rcm_order (topology.hpp:131-178).  adj: list of neighbour lists or a CSR
+    (row_ptr, col_idx).  lib="orc": the C restatement; "ref": the compiled
+    reference.  Raises KindError(1 + ErrorKind) like the reference."""
+    rp, ci = adj if isinstance(adj, tuple) else _csr_of_lists(adj)
+    rp = np.ascontiguousarray(rp, np.int64)
+    ci = np.ascontiguousarray(ci, np.int32)
+    n = rp.size - 1
+    out = np.zeros(max(n, 1), np.int32)
+    if lib == "orc":
+        L = orc()
+        fail = np.zeros(1, np.int64)
+        rc = L.orc_rcm_order(C.c_int(n), rp.ctypes.data_as(I64P), ip(ci), ip(out), fail.ctypes.data_as(I64P))
+        if rc:
+            raise KindError(rc, f"entry {int(fail[0])}")
+    else:
+        L = ref()
+        rc = L.ref_rcm_order(C.c_int(n), rp.ctypes.data_as(I64P), ip(ci), ip(out))
+        if rc:
+            raise KindError(-rc, L.ref_last_error().decode())
+    return out[:n]
+
+
+def vertex_adjacency(cv, nv, gdim):
+    """mesh.hpp:350-362: sorted other vertices sharing a cell, as CSR."""
+    cv = np.asarray(cv, np.int32).reshape(-1, gdim + 1)
+    nb = [set() for _ in range(nv)]
+    for row in cv:
+        for a in row:
+            nb[a].update(int(b) for b in row if b != a)
+    return _csr_of_lists([sorted(s) for s in nb])
+
+
+def ref_reorder(gdim, cv, coords):
+    """The compiled reference's reorder (mesh.hpp:364-396): (perm, coords, cv)."""
+    L = ref()
+    cv = np.ascontiguousarray(cv, np.int32)
+    coords = np.ascontiguousarray(coords, np.float64)
+    nv = coords.size // gdim
+    perm = np.zeros(max(nv, 1), np.int32)
+    xo = np.zeros(max(coords.size, 1))
+    co = np.zeros(max(cv.size, 1), np.int32)
+    rc = L.ref_reorder(C.c_int(gdim), C.c_int(cv.size // (gdim + 1)), C.c_int(nv), ip(cv), dp(coords),
+                       ip(perm), dp(xo), ip(co))
+    if rc:
+        raise KindError(-rc, L.ref_last_error().decode())
+    return perm[:nv], xo[: coords.size], co[: cv.size]

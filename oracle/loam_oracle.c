@@ -799,3 +799,61 @@ int orc_apply_dirichlet(int nrows, const int64_t* row_ptr, const int32_t* col_id
   }
   return ORC_OK;
 }
+
+/* topology.hpp:131-178.  The queue is order[] itself (head chases tail);
+ * a dequeued vertex's new neighbours are insertion-sorted by (degree, index)
+ * in place at the tail before they are enqueued. */
+int orc_rcm_order(int n, const int64_t* row_ptr, const int32_t* col_idx, int32_t* order, int64_t* fail) {
+  for (int u = 0; u < n; ++u)
+    for (int64_t k = row_ptr[u]; k < row_ptr[u + 1]; ++k) {
+      const int v = col_idx[k];
+      if (v < 0 || v >= n) {
+        if (fail) *fail = k;
+        return ORC_ERR_INDEX_OUT_OF_RANGE;
+      }
+      int64_t q = row_ptr[v];
+      while (q < row_ptr[v + 1] && col_idx[q] != u) ++q;
+      if (q == row_ptr[v + 1]) {
+        if (fail) *fail = k;
+        return ORC_ERR_ASYMMETRIC_ADJACENCY;
+      }
+    }
+  char* seen = (char*)calloc(n ? (size_t)n : 1, 1);
+  if (!seen) return ORC_ERR_INVALID_ARGUMENT;
+#define DEG(x) (row_ptr[(x) + 1] - row_ptr[(x)])
+#define BEFORE(a, b) (DEG(a) != DEG(b) ? DEG(a) < DEG(b) : (a) < (b))
+  int tail = 0;
+  for (;;) {
+    int seed = -1;
+    for (int u = 0; u < n; ++u)
+      if (!seen[u] && (seed < 0 || DEG(u) < DEG(seed))) seed = u;
+    if (seed < 0) break;
+    seen[seed] = 1;
+    int head = tail;
+    order[tail++] = seed;
+    while (head < tail) {
+      const int u = order[head++];
+      const int first = tail;
+      for (int64_t k = row_ptr[u]; k < row_ptr[u + 1]; ++k) {
+        const int v = col_idx[k];
+        if (seen[v]) continue;
+        seen[v] = 1;
+        int j = tail++;
+        while (j > first && BEFORE(v, order[j - 1])) {
+          order[j] = order[j - 1];
+          --j;
+        }
+        order[j] = v;
+      }
+    }
+  }
+#undef BEFORE
+#undef DEG
+  free(seen);
+  for (int i = 0, j = n - 1; i < j; ++i, --j) {
+    const int32_t t = order[i];
+    order[i] = order[j];
+    order[j] = t;
+  }
+  return ORC_OK;
+}

@@ -55,6 +55,15 @@ enum orc_form {
 int orc_color_iteration(int n, int nmaps, const int32_t* const* maps, const int32_t* arity,
                         const int32_t* target_size, int32_t* colors);
 
+/* Reverse Cuthill-McKee (topology.hpp:131-178) over adjacency lists given as
+ * CSR (row_ptr [n+1], col_idx): checks every entry in list order (out of
+ * range -> ORC_ERR_INDEX_OUT_OF_RANGE, no back entry ->
+ * ORC_ERR_ASYMMETRIC_ADJACENCY, *fail = entry position), then BFS from the
+ * minimum-(degree, index) unvisited vertex, unvisited neighbours appended in
+ * (degree, index) order, reversed.  order[new] = old. */
+#define ORC_ERR_ASYMMETRIC_ADJACENCY (1 + 3)
+int orc_rcm_order(int n, const int64_t* row_ptr, const int32_t* col_idx, int32_t* order, int64_t* fail);
+
 /* ---- sparsity (data.hpp:149-179) -------------------------------------- */
 
 /* Builds the CSR union pattern.  Returns nnz (>=0) or -error.  The arrays are

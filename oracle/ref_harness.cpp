@@ -619,3 +619,36 @@ int ref_exterior_facets(int gdim, int ncells, int nv, const int32_t* cv, int32_t
   }
 }
 } // extern "C"
+
+extern "C" {
+// topology.hpp:131-178 rcm_order over CSR adjacency lists; 0 or -err.
+int ref_rcm_order(int n, const int64_t* rp, const int32_t* ci, int32_t* order) {
+  try {
+    std::vector<std::vector<int>> adj(n);
+    for (int u = 0; u < n; ++u) adj[u].assign(ci + rp[u], ci + rp[u + 1]);
+    const auto r = rcm_order(n, adj);
+    std::copy(r.begin(), r.end(), order);
+    return 0;
+  } catch (const Error& e) {
+    return -fail_code(e);
+  }
+}
+
+// mesh.hpp:350-362 vertex_adjacency + 364-396 reorder on a mesh built from
+// arrays: writes perm [nv], the renumbered coords [nv x gdim] and cv.
+int ref_reorder(int gdim, int ncells, int nv, const int32_t* cv, const double* coords, int32_t* perm,
+                double* coords_out, int32_t* cv_out) {
+  try {
+    auto mesh = mesh_from_arrays(gdim, ncells, nv, cv, coords, true);
+    auto [out, p] = reorder(*mesh);
+    std::copy(p.begin(), p.end(), perm);
+    auto x = out->coordinates->view();
+    std::copy(x.begin(), x.end(), coords_out);
+    const auto& m = out->cell_vertex_map->values();
+    std::copy(m.begin(), m.end(), cv_out);
+    return 0;
+  } catch (const Error& e) {
+    return -fail_code(e);
+  }
+}
+} // extern "C"

@@ -577,4 +577,31 @@ int loam_gpu_exterior_facets(int32_t ncells, int32_t nverts, int32_t gdim, const
   });
 }
 
+int loam_gpu_rcm_order(int32_t n, const int64_t* row_ptr, const int32_t* col_idx, int32_t* order, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(n == 0 || (row_ptr && col_idx && order), LOAM_ERR(InvalidArgument), "null adjacency or output");
+    rcm_order_dev(n, row_ptr, col_idx, order, as_stream(stream));
+  });
+}
+
+int loam_gpu_vertex_adjacency(int32_t ncells, int32_t nverts, int32_t gdim, const int32_t* cv, int64_t** row_ptr,
+                              int32_t** col_idx, int64_t* nnz, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(row_ptr && col_idx && nnz, LOAM_ERR(InvalidArgument), "null output");
+    require(gdim == 2 || gdim == 3, LOAM_ERR(InvalidArgument), "gdim must be 2 or 3");
+    *nnz = vertex_adjacency_dev(cv, ncells, nverts, gdim, row_ptr, col_idx, as_stream(stream));
+  });
+}
+
+int loam_gpu_renumber_vertices(int32_t nverts, int32_t gdim, const double* coords, int32_t ncells, const int32_t* cv,
+                               const int32_t* perm, double* coords_out, int32_t* cv_out, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(gdim == 2 || gdim == 3, LOAM_ERR(InvalidArgument), "gdim must be 2 or 3");
+    renumber_vertices_dev(nverts, gdim, coords, ncells, cv, perm, coords_out, cv_out, as_stream(stream));
+  });
+}
+
 } // extern "C"

@@ -824,3 +824,66 @@ def exterior_facets(cell_vertex: Map, gdim: int):
         capi.lib().loam_gpu_free(fv)
         capi.lib().loam_gpu_free(fc)
     return a[: k * gdim].reshape(k, gdim), b[: k * 2].reshape(k, 2)
+
+
+def vertex_adjacency(cell_vertex: Map, gdim: int):
+    """mesh.hpp:350-362 on the device: (row_ptr int64, col_idx int32) device
+    tensors, per vertex the sorted other vertices that share a cell."""
+    nc, nv = cell_vertex.source.size, cell_vertex.target.size
+    rp, ci, nnz = C.c_void_p(), C.c_void_p(), C.c_int64()
+    capi.check(capi.lib().loam_gpu_vertex_adjacency(nc, nv, gdim, cell_vertex.dev.data_ptr(), C.byref(rp),
+                                                    C.byref(ci), C.byref(nnz), _stream()))
+    try:
+        trp = torch.empty(nv + 1, dtype=torch.int64, device="cuda")
+        tci = torch.empty(max(nnz.value, 1), dtype=torch.int32, device="cuda")
+        capi.check(capi.lib().loam_gpu_memcpy(trp.data_ptr(), rp, 8 * (nv + 1), _stream()))
+        capi.check(capi.lib().loam_gpu_memcpy(tci.data_ptr(), ci, 4 * nnz.value, _stream()))
+        capi.check(capi.lib().loam_gpu_stream_sync(_stream()))
+    finally:
+        capi.lib().loam_gpu_free(rp)
+        capi.lib().loam_gpu_free(ci)
+    return trp, tci[: nnz.value]
+
+
+def rcm_order(n: int, row_ptr, col_idx) -> torch.Tensor:
+    """topology.hpp:131-178 rcm_order on the device over CSR adjacency lists
+    (numpy or device tensors); returns perm (int32 device tensor),
+    perm[new] = old.  Raises LoamError(IndexOutOfRange / AsymmetricAdjacency)
+    like the reference."""
+    rp = torch.as_tensor(np.asarray(row_ptr, np.int64) if isinstance(row_ptr, (list, np.ndarray)) else row_ptr)
+    ci = torch.as_tensor(np.asarray(col_idx, np.int32) if isinstance(col_idx, (list, np.ndarray)) else col_idx)
+    rp = rp.to(device="cuda", dtype=torch.int64).contiguous()
+    ci = ci.to(device="cuda", dtype=torch.int32).contiguous()
+    if ci.numel() == 0:
+        ci = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    capi.check(capi.lib().loam_gpu_rcm_order(n, rp.data_ptr(), ci.data_ptr(), out.data_ptr(), _stream()))
+    return out[:n]
+
+
+def reorder(cell_vertex: Map, coordinates: Dat):
+    """mesh.hpp:364-396 reorder on the device: RCM over the vertex adjacency,
+    then coordinates and the cell->vertex map renumbered consistently.
+    Returns (new cell_vertex Map, new coordinates Dat, perm) with
+    perm[new] = old (numpy).  Exterior facets keep their (cell, local facet)
+    order under the renumbering (cells are not permuted), as the reference
+    requires; re-derive them with exterior_facets(new_map, gdim)."""
+    gdim = coordinates.dim
+    nv, nc = cell_vertex.target.size, cell_vertex.source.size
+    _require(cell_vertex.arity == gdim + 1, "ArityMismatch", "cell_vertex arity must be gdim + 1")
+    _require(coordinates.set.size == nv, "DimensionMismatch",
+             "coordinates must live on the map's target set")
+    rp, ci = vertex_adjacency(cell_vertex, gdim)
+    perm = rcm_order(nv, rp, ci)
+    coordinates._materialize()
+    verts = Set(nv, cell_vertex.target.name)
+    X = Dat(verts, gdim, coordinates.name)
+    cv_out = torch.empty(max(nc * (gdim + 1), 1), dtype=torch.int32, device="cuda")
+    capi.check(capi.lib().loam_gpu_renumber_vertices(nv, gdim, coordinates.data.data_ptr(), nc,
+                                                     cell_vertex.dev.data_ptr(), perm.data_ptr(),
+                                                     X.data.data_ptr(), cv_out.data_ptr(), _stream()))
+    X.version += 1
+    X._zero = X._stale = False
+    cvals = cv_out[: nc * (gdim + 1)].cpu().numpy()
+    m = Map(cell_vertex.source, verts, gdim + 1, cvals, cell_vertex.name)
+    return m, X, perm.cpu().numpy()

@@ -75,7 +75,35 @@ def main():
         ker[f"tri_p2_{kind}"] = O.ref_local_kernel(kind, 2, 2, X2, C6, kappa=2.5)
         ker[f"tet_p1_{kind}"] = O.ref_local_kernel(kind, 1, 3, X3, np.append(C3, 0.4), kappa=2.5)
     np.savez_compressed(os.path.join(OUT, "local_kernels.npz"), X2=X2, X3=X3, C3=C3, C6=C6, **ker)
+    rcm_fixture()
     print("golden fixtures written to", OUT)
+
+
+def random_graph(n, m, seed):
+    """Seeded symmetric adjacency lists (no self loops), unsorted rows."""
+    rng = np.random.default_rng(seed)
+    adj = [[] for _ in range(n)]
+    for _ in range(m):
+        a, b = (int(x) for x in rng.integers(0, n, 2))
+        if a != b and b not in adj[a]:
+            adj[a].append(b)
+            adj[b].append(a)
+    return adj
+
+
+def rcm_fixture():
+    """rcm_order (topology.hpp:131-178) and reorder (mesh.hpp:364-396) of the
+    reference on cell-permuted meshes and seeded random graphs."""
+    out = {}
+    for tag, gdim, n in (("sq", 2, 6), ("cube", 3, 3)):
+        m = configs.mesh(gdim, n, 0.1, 7, 8)
+        perm, xo, co = O.ref_reorder(gdim, m.cv, m.coords)
+        out.update({f"{tag}_cv": m.cv, f"{tag}_coords": m.coords, f"{tag}_perm": perm, f"{tag}_coords_out": xo,
+                    f"{tag}_cv_out": co})
+    for k, (n, m_, seed) in enumerate(((40, 50, 1), (200, 300, 2), (64, 20, 3))):
+        rp, ci = O._csr_of_lists(random_graph(n, m_, seed))
+        out.update({f"g{k}_row_ptr": rp, f"g{k}_col_idx": ci, f"g{k}_order": O.rcm_order((rp, ci), lib="ref")})
+    np.savez_compressed(os.path.join(OUT, "rcm.npz"), **out)
 
 
 if __name__ == "__main__":
