@@ -2485,6 +2485,9 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       NtileSpec ns;
       ns.tile_nodes = env_int("LOAM_GPU_NT_NODES", ns.tile_nodes);
       ns.tile_items = env_int("LOAM_GPU_NT_ITEMS", ns.tile_items);
+      ns.tile_pairs = env_int("LOAM_GPU_NT_PAIRS", ns.tile_pairs);
+      ns.tile_cells = env_int("LOAM_GPU_NT_CELLS", ns.tile_cells);
+      ns.tile_slots = env_int("LOAM_GPU_NT_SLOTS", ns.tile_slots);
       if (build_ntile(P->nt, ns, n, R.v.target, srows.v.get(), sx.v.get(), X->target_size, P->pp, sp->row_ptr,
                       sp->nnz, s)) {
         P->use_ntile = true;

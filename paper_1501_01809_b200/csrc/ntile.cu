@@ -7,6 +7,7 @@
 // build_sparsity(map, map, 3, 3) (data.hpp:149-179).
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -42,6 +43,8 @@ constexpr int kNtConsumers = 128; // consumer threads per CTA (= k_ntile's NT)
 #define LOAM_GPU_NT_SPLIT 4
 #endif
 constexpr int kDiagSplit = LOAM_GPU_NT_SPLIT; // threads per diagonal block (its 24 cells in chunks)
+static_assert(kDiagSplit >= 1 && kDiagSplit <= 32 && (kDiagSplit & (kDiagSplit - 1)) == 0,
+              "diagonal parts are combined within a power-of-two lane group");
 
 } // namespace
 
@@ -172,6 +175,9 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
         for (int q = a; q < b; ++q) dprec.push_back((uint16_t)dl[q]);
       }
     }
+    // the kDiagSplit parts of a diagonal block sit on consecutive lanes of one
+    // aligned lane group (combined by shuffles): pad with no-op items
+    while (items.size() % kDiagSplit) items.push_back(ItemRec{0, 0, 2, 0, 0});
     for (auto it : ditems) {
       it.poff = (uint16_t)(it.poff + prec.size());
       items.push_back(it);
@@ -272,7 +278,14 @@ __device__ __forceinline__ void nt_wait(uint64_t* bar, uint32_t parity) {
 }
 
 constexpr int kNtThreads = 128;
-constexpr int kGS = 18; // doubles per cell: 4 x (g_k, V) + 2 pad (odd stride in 16-byte units)
+#ifndef LOAM_GPU_NT_GS
+#define LOAM_GPU_NT_GS 12
+#endif
+// doubles per cell: sqrt(V) g_k as 4 x (x, y) then 4 x z (12: the smallest
+// record; phase 2 reads random cells, so an odd 16-byte stride buys little
+// and the smaller footprint fits 4 CTAs per SM)
+constexpr int kGS = LOAM_GPU_NT_GS;
+static_assert(kGS >= 12 && kGS % 2 == 0, "cell record");
 
 template <int STAGES>
 __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_constant__ NtileArgs a) {
@@ -357,7 +370,6 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
   // ---- consumers
   double* seg0 = reinterpret_cast<double*>(sm + a.off_seg);
   double* geo = reinterpret_cast<double*>(sm + a.off_geo);
-  double* part = reinterpret_cast<double*>(sm + a.off_part);
   const double lam = a.prm.p[0], mu = a.prm.p[1];
   for (int k = 0;; ++k) {
     nt_wait(&full[k % STAGES], (k / STAGES) & 1);
@@ -387,11 +399,12 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
       geometry<3>(X, Gm);
       // sqrt(V) g_k: a node block sums V g_a g_b^T = (sqrt(V) g_a)(sqrt(V) g_b)^T over its cells
       const double sv = sqrt(Gm.V);
-      double2* g = reinterpret_cast<double2*>(geo + c * kGS);
+      double* gc = geo + c * kGS;
+      double2* g = reinterpret_cast<double2*>(gc);
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        g[2 * v] = make_double2(sv * Gm.g[v][0], sv * Gm.g[v][1]);
-        g[2 * v + 1] = make_double2(sv * Gm.g[v][2], 0.0);
+        g[v] = make_double2(sv * Gm.g[v][0], sv * Gm.g[v][1]);
+        gc[8 + v] = sv * Gm.g[v][2];
       }
     }
     named_bar(1, NT);
@@ -409,14 +422,14 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
         const uint32_t x = prec[poff + q * NT];
         const double* g = geo + (x >> 4) * kGS;
         const int lv = (x >> 2) & 3, lw = x & 3;
-        const double2 a0 = reinterpret_cast<const double2*>(g + 4 * lv)[0];
-        const double2 b0 = reinterpret_cast<const double2*>(g + 4 * lw)[0];
+        const double2 a0 = reinterpret_cast<const double2*>(g)[lv];
+        const double2 b0 = reinterpret_cast<const double2*>(g)[lw];
         ga[0] = a0.x;
         ga[1] = a0.y;
-        ga[2] = g[4 * lv + 2];
+        ga[2] = g[8 + lv];
         gb[0] = b0.x;
         gb[1] = b0.y;
-        gb[2] = g[4 * lw + 2];
+        gb[2] = g[8 + lw];
       };
       double ga[3] = {0, 0, 0}, gb[3] = {0, 0, 0};
       if (np > 0) fetch(0, ga, gb);
@@ -433,40 +446,43 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
           gb[d] = nb[d];
         }
       }
-      if (kind == 0) {
-        const double tr = mu * (acc[0][0] + acc[1][1] + acc[2][2]);
+      if (kind == 2) continue; // padding before the diagonal groups
+      int wb = base, ws = stride;
+      if (kind == 1) {
+        // diagonal block: its kDiagSplit parts are on the consecutive lanes
+        // of one aligned group; the first lane sums them in part order
+        // ((p0 + p1) + p2) + p3 -- the same bits on every run
+        const int lane = tid & 31, g0 = lane & ~(kDiagSplit - 1);
+        const unsigned gmask = ((1u << kDiagSplit) - 1u) << g0;
 #pragma unroll
         for (int d = 0; d < 3; ++d)
 #pragma unroll
           for (int e = 0; e < 3; ++e) {
-            double v = fma(mu, acc[e][d], lam * acc[d][e]);
-            if (d == e) v += tr;
-            seg[base + d * stride + e] = v;
+            double v = acc[d][e];
+#pragma unroll
+            for (int s = 1; s < kDiagSplit; ++s) {
+              const double o = __shfl_sync(gmask, acc[d][e], s, kDiagSplit);
+              v += o;
+            }
+            acc[d][e] = v;
           }
-      } else {
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-#pragma unroll
-          for (int e = 0; e < 3; ++e) part[base * 9 + d * 3 + e] = acc[d][e];
+        if (lane != g0) continue;
+        const int di = base / kDiagSplit;
+        wb = dinfo[2 * di];
+        ws = dinfo[2 * di + 1];
       }
+      const double tr = mu * (acc[0][0] + acc[1][1] + acc[2][2]);
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          double v = fma(mu, acc[e][d], lam * acc[d][e]);
+          if (d == e) v += tr;
+          seg[wb + d * ws + e] = v;
+        }
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[k % STAGES]);
-    named_bar(1, NT);
-    // diagonal blocks: the kDiagSplit partial sums, in a fixed order
-    for (int t = tid; t < ndiag * 9; t += NT) {
-      const int di = t / 9, q = t - 9 * di, d = q / 3, e = q - 3 * d;
-      auto S = [&](int x, int y) {
-        double v = part[(di * kDiagSplit) * 9 + 3 * x + y];
-#pragma unroll
-        for (int s = 1; s < kDiagSplit; ++s) v += part[(di * kDiagSplit + s) * 9 + 3 * x + y];
-        return v;
-      };
-      double v = fma(mu, S(e, d), lam * S(d, e));
-      if (d == e) v += mu * (S(0, 0) + S(1, 1) + S(2, 2));
-      const int b = dinfo[2 * di], stride = dinfo[2 * di + 1];
-      seg[b + d * stride + e] = v;
-    }
     if (a.accumulate) {
       named_bar(1, NT);
       for (int t = tid; t < len; t += NT) a.out[(int64_t)E0 + t] += seg[t];
@@ -515,8 +531,6 @@ void launch_ntile(const NtilePlan& p, const double* coords, double* out, const F
   off += up16((p.max_seg + 2) * 8);
   a.off_geo = off;
   off += up16(p.max_cells * kGS * 8);
-  a.off_part = off;
-  off += up16(p.max_diag * kDiagSplit * 9 * 8);
   a.off_buf = off;
   a.b_win = up16(p.max_blob);
   a.buf_bytes = a.b_win + up16(p.max_slots * 3 * 8 + 16);
@@ -529,6 +543,9 @@ void launch_ntile(const NtilePlan& p, const double* coords, double* out, const F
     require(blocks > 0, LOAM_GPU_ERR_CUDA, "node-tile kernel does not fit on an SM");
     kern<<<std::min(p.ntiles, blocks * kNumSMs), kNtThreads + 32, smem, s>>>(a);
   };
+  if (std::getenv("LOAM_GPU_NT_INFO")) // developer: plan maxima behind the shared-memory footprint
+    fprintf(stderr, "ntile: tiles %d max_seg %d max_cells %d max_blob %d max_slots %d max_diag %d smem/stage %d fixed %d\n",
+            p.ntiles, p.max_seg, p.max_cells, p.max_blob, p.max_slots, p.max_diag, a.buf_bytes, off);
   a.dynamic = std::getenv("LOAM_GPU_NT_STATIC") ? 0 : 1;
   a.dbg = std::getenv("LOAM_GPU_NT_DBG") ? std::atoi(std::getenv("LOAM_GPU_NT_DBG")) : 0; // developer: skip phases
   if (st >= 3) go(k_ntile<3>, 3);
