@@ -597,6 +597,25 @@ inline std::vector<Real> block_spmv(const BlockMat& op, std::span<const Real> x)
   return detail::to_host(y, op.nrows());
 }
 
+/// Reverse Cuthill-McKee (topology.hpp:131-178) on the device: r[new] = old,
+/// bit-identical to the reference; IndexOutOfRange / AsymmetricAdjacency at
+/// the first offending entry in list order.
+inline std::vector<int> rcm_order(int n, const std::vector<std::vector<int>>& adjacency) {
+  require(static_cast<int>(adjacency.size()) == n, ErrorKind::InvalidArgument, "adjacency list count != n");
+  std::vector<int64_t> rp(static_cast<size_t>(n) + 1, 0);
+  for (int u = 0; u < n; ++u) rp[u + 1] = rp[u] + static_cast<int64_t>(adjacency[u].size());
+  std::vector<int32_t> ci;
+  ci.reserve(static_cast<size_t>(rp[n]));
+  for (const auto& a : adjacency) ci.insert(ci.end(), a.begin(), a.end());
+  detail::DeviceArray<int64_t> drp(rp.size(), false);
+  detail::DeviceArray<int32_t> dci(ci.size(), false), dout(static_cast<size_t>(n), false);
+  drp.upload(rp.data());
+  if (!ci.empty()) dci.upload(ci.data());
+  check(loam_gpu_rcm_order(n, drp.dev, dci.dev, dout.dev, nullptr));
+  const auto& h = dout.download();
+  return std::vector<int>(h.begin(), h.begin() + n);
+}
+
 struct SolveReport { // solver.hpp:13-18
   int iterations = 0;
   Real final_residual_norm = 0.0;

@@ -309,6 +309,14 @@ static void test_cg() { // test_solver.cpp:24-123
   CHECK(std::sqrt(rn) <= 1e-10 * std::sqrt(bn) + 1e-12);
 }
 
+static void test_rcm() { // test_topology.cpp rcm_order cases
+  CHECK(rcm_order(3, {{1}, {0, 2}, {1}}) == (std::vector<int>{2, 1, 0}));
+  CHECK(rcm_order(1, {{}}) == (std::vector<int>{0}));
+  CHECK(rcm_order(4, {{1, 2, 3}, {0}, {0}, {0}}) == (std::vector<int>{3, 2, 0, 1}));
+  expect_error(ErrorKind::AsymmetricAdjacency, [] { rcm_order(2, {{1}, {}}); });
+  expect_error(ErrorKind::IndexOutOfRange, [] { rcm_order(2, {{3}, {0}}); });
+}
+
 int main() {
   const std::vector<std::pair<const char*, void (*)()>> cases = {
       {"direct loop doubles a field", test_direct_loop},
@@ -325,6 +333,7 @@ int main() {
       {"spmv by CSR traversal", test_spmv},
       {"block spmv skips zero blocks and swaps components", test_block_spmv},
       {"cg known answers, breakdown, maxit, block operator", test_cg},
+      {"rcm_order known answers and errors", test_rcm},
   };
   for (auto& [name, fn] : cases) {
     const int before = g_fail;
