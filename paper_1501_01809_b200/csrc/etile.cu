@@ -5,6 +5,7 @@
 // element kernels (fem/form.hpp:201-320) and Mat::addto (data.hpp:205-222).
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -932,6 +933,9 @@ void launch_etile(int form, const EtilePlan& p, const double* coords, double* ou
   a.b_win = up16(p.max_blob);
   a.buf_bytes = a.b_win + up16(p.max_slots * p.gd * 8 + 16);
   const size_t base = (size_t)off, buf = (size_t)a.buf_bytes;
+  if (std::getenv("LOAM_GPU_ET_INFO")) // developer: plan maxima behind the shared-memory footprint
+    fprintf(stderr, "etile: tiles %d max_segT %d max_seg %d max_cells %d max_blob %d max_slots %d stage %d fixed %d\n",
+            p.ntiles, p.max_segT, p.max_seg, p.max_cells, p.max_blob, p.max_slots, a.buf_bytes, off);
   if (p.cd == 2) {
     require(p.gd == 2 && form == F_STOKES_A, LOAM_ERR(InvalidArgument), "edge tiles: cd = 2 is the Stokes A block");
     go_etile<F_STOKES_A, 2, 2>(p, a, base, buf, s);
