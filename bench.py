@@ -588,16 +588,20 @@ def wave_bench(args):
     line = {"chain": "wave (run_wave)", "mesh": f"{n}^2 P1", "cells": cells, "us_per_step": us,
             "cell_steps_per_s": cells / (us * 1e-6), "launches_per_step": 6}
     # the same chain replayed as CUDA graphs of 100 steps (device-resident forcing / |p| / blow-up test)
-    wg = WaveLoop(n, dt, 1e9)
-    wg.run_graph(100, max_steps=200)  # capture + warm-up
-    torch.cuda.synchronize()
     gsteps = max(steps, 2000) // 100 * 100
-    t0 = time.perf_counter()
-    wg.run_graph(100, max_steps=gsteps)
-    torch.cuda.synchronize()
-    gus = (time.perf_counter() - t0) * 1e6 / gsteps
-    line["graph"] = {"us_per_step": gus, "cell_steps_per_s": cells / (gus * 1e-6), "steps_per_graph": 100,
-                     "note": "wall clock per step including one capture per run_graph call"}
+    for key, fused in (("graph", False), ("graph_fused", True)):
+        wg = WaveLoop(n, dt, 1e9)
+        wg.run_graph(100, max_steps=200, fused=fused)  # capture + warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        wg.run_graph(100, max_steps=gsteps, fused=fused)
+        torch.cuda.synchronize()
+        gus = (time.perf_counter() - t0) * 1e6 / gsteps
+        line[key] = {"us_per_step": gus, "cell_steps_per_s": cells / (gus * 1e-6), "steps_per_graph": 100,
+                     "launches_per_step": 3 if fused else 8,
+                     "note": ("one fused kernel per step (loam_gpu_wave_step) + 2 clock kernels; " if fused else
+                              "execute + 3 pointwise + bc + |p| + 2 clock kernels; ") +
+                             "wall clock per step including one capture per run_graph call"}
     if O.ref_available():
         rn, rT = 32, 0.1
         t0 = time.perf_counter()

@@ -284,6 +284,19 @@ int loam_gpu_reduce_dev(const double* x, int64_t n, int32_t kind, double* result
 /* DirichletBC::apply with the constant read from device memory. */
 int loam_gpu_bc_apply_dev(double* dat, int32_t set_size, const int32_t* nodes, int32_t nnodes,
                           const double* value_dev, void* stream);
+/* One bench::run_wave step (bench.hpp:267-289) fused into the vertex-star
+ * stiffness action: `args` describe the action loop (b INC, X READ, phi READ
+ * over the cell->vertex map, kernel stiffness_action_p1_tri); the kernel
+ * reads p_in / phi_in (device [n_vertices]) and writes p_out / phi_out
+ * (distinct buffers): phi_h = phi - half_dt p; b = K phi_h; p += b pc;
+ * p[bc != 0] = state[1]; phi = phi_h - half_dt p; state[2] = max(state[2],
+ * |p|_inf).  Bitwise equal to the unfused chain (execute + pointwise +
+ * bc_apply + reduce).  UnsupportedForm when the loop has no vertex-star plan
+ * (the caller then runs the unfused chain). */
+int loam_gpu_wave_step(const loam_kernel_desc* kernel, int32_t n, uint64_t iter, const loam_arg_desc* args,
+                       int nargs, const double* p_in, const double* phi_in, double* p_out, double* phi_out,
+                       const double* p_constant, const uint8_t* bc_mask, double half_dt, double* state,
+                       void* stream);
 /* The run_wave clock on device state s[6] = {t, bc value, |p|, max |p| over
  * t <= first_period, blow-up step (0 = none), steps}.  phase 0: s[1] =
  * sin(10 pi t) (the marker-1 forcing, bench.hpp:237); phase 1 (after |p| is

@@ -159,6 +159,7 @@ def lib() -> C.CDLL:
             "loam_gpu_p2_cell_node_map_dev": (C.c_int, [i32, i32, i32, vp, vp, ip, vp]),
             "loam_gpu_exterior_facets": (C.c_int, [i32, i32, i32, vp, C.POINTER(vp), C.POINTER(vp), ip, vp]),
             "loam_gpu_rcm_order": (C.c_int, [i32, vp, vp, vp, vp]),
+            "loam_gpu_wave_step": (C.c_int, [C.POINTER(KernelDesc), i32, u64, C.POINTER(ArgDesc), C.c_int, vp, vp, vp, vp, vp, vp, C.c_double, vp, vp]),
             "loam_gpu_vertex_adjacency": (C.c_int, [i32, i32, i32, vp, C.POINTER(vp), C.POINTER(vp),
                                                     C.POINTER(C.c_int64), vp]),
             "loam_gpu_renumber_vertices": (C.c_int, [i32, i32, vp, i32, vp, vp, vp, vp, vp]),
@@ -186,7 +187,7 @@ EXPORTED = [
     "loam_gpu_apply_dirichlet", "loam_gpu_bc_apply", "loam_gpu_pointwise", "loam_gpu_reduce",
     "loam_gpu_p2_cell_node_map_dev", "loam_gpu_exterior_facets",
     "loam_gpu_reduce_dev", "loam_gpu_bc_apply_dev", "loam_gpu_wave_clock",
-    "loam_gpu_rcm_order", "loam_gpu_vertex_adjacency", "loam_gpu_renumber_vertices",
+    "loam_gpu_rcm_order", "loam_gpu_vertex_adjacency", "loam_gpu_renumber_vertices", "loam_gpu_wave_step",
 ]
 
 

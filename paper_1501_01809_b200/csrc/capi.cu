@@ -577,6 +577,21 @@ int loam_gpu_exterior_facets(int32_t ncells, int32_t nverts, int32_t gdim, const
   });
 }
 
+int loam_gpu_wave_step(const loam_kernel_desc* kernel, int32_t n, uint64_t iter, const loam_arg_desc* args,
+                       int nargs, const double* p_in, const double* phi_in, double* p_out, double* phi_out,
+                       const double* p_constant, const uint8_t* bc_mask, double half_dt, double* state,
+                       void* stream) {
+  return guarded([&] {
+    require_device();
+    require(p_in && phi_in && p_out && phi_out && p_constant && bc_mask && state, LOAM_ERR(InvalidArgument),
+            "null field");
+    require(p_out != p_in && phi_out != phi_in && p_out != phi_in && phi_out != p_in, LOAM_ERR(InvalidArgument),
+            "wave step: outputs must not alias the inputs");
+    wave_step(kernel, n, iter, args, nargs, p_in, phi_in, p_out, phi_out, p_constant, bc_mask, half_dt, state,
+              as_stream(stream));
+  });
+}
+
 int loam_gpu_rcm_order(int32_t n, const int64_t* row_ptr, const int32_t* col_idx, int32_t* order, void* stream) {
   return guarded([&] {
     require_device();

@@ -22,6 +22,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 #include <unordered_map>
 
 #include "async.cuh"
@@ -1030,13 +1031,19 @@ struct StarArgs {
   int accumulate;
 };
 
-template <class F>
-__device__ __forceinline__ double star_row(const StarArgs& a, int r, int4 h, int4 t) {
+struct CoeffLoad {
+  const double* c;
+  __device__ __forceinline__ double operator()(int v) const { return __ldg(c + v); }
+};
+
+template <class F, class Coef = CoeffLoad>
+__device__ __forceinline__ double star_row(const StarArgs& a, int r, int4 h, int4 t, Coef coef = Coef{nullptr}) {
+  if constexpr (std::is_same_v<Coef, CoeffLoad>) coef.c = a.coeff;
   const int m = h.x & 7;
   const bool closed = (h.x >> 3) & 1;
   const int v[7] = {h.y, h.z, h.w, t.x, t.y, t.z, t.w};
   const double2 xs = __ldg(reinterpret_cast<const double2*>(a.coords) + r);
-  const double us = __ldg(a.coeff + r);
+  const double us = coef(r);
   // every neighbour gather is issued before the first use: one dependent
   // round trip after the star record instead of one per link vertex
   double2 X[7];
@@ -1045,7 +1052,7 @@ __device__ __forceinline__ double star_row(const StarArgs& a, int r, int4 h, int
   for (int k = 0; k < 7; ++k) {
     const int vk = k < m ? v[k] : r;
     X[k] = __ldg(reinterpret_cast<const double2*>(a.coords) + vk);
-    U[k] = __ldg(a.coeff + vk);
+    U[k] = coef(vk);
   }
   double px = 0, py = 0, up = 0, p0x = 0, p0y = 0, u0 = 0, aa = 0;
   double acc = 0.0;
@@ -1175,6 +1182,63 @@ void launch_star(const StarArgs& a, cudaStream_t s) {
   }
   count_launch();
   LG_LAUNCH_CHECK();
+}
+
+// ---- the run_wave time step fused into the vertex-star action -------------
+// bench::run_wave (bench.hpp:267-289) per step:
+//   phi -= dt/2 p;  b = K phi;  p += b * pc;  p[bc] = forcing;  phi -= dt/2 p;  |p|_inf
+// Every update but the action is pointwise and the star kernel owns its
+// vertex row, so one kernel does the step: the half-kick phi - (dt/2) p of
+// every gathered neighbour is formed on the fly from the previous step's
+// fields (ping-pong buffers: no thread reads what another writes), then the
+// owner applies the kick, the Dirichlet forcing and the second half-kick to
+// its vertex and folds |p| into the step's maximum.  The arithmetic is the
+// pointwise engine's (__dmul_rn / __dsub_rn / __dadd_rn, no contraction)
+// and the star kernel's, so the fields equal the unfused chain bitwise.
+struct WaveFields {
+  const double* p_in;
+  const double* phi_in;
+  double* p_out;
+  double* phi_out;
+  const double* pc;
+  const uint8_t* bc;  // 1 on the Dirichlet vertices
+  double half_dt;
+  double* state;      // [1] forcing value, [2] |p|_inf (max-folded; zeroed by the clock)
+};
+
+struct HalfKick {
+  const double* phi;
+  const double* p;
+  double h;
+  __device__ __forceinline__ double operator()(int v) const {
+    return __dsub_rn(__ldg(phi + v), __dmul_rn(h, __ldg(p + v)));
+  }
+};
+
+template <class F>
+__global__ void __launch_bounds__(256) k_wave_step(const __grid_constant__ StarArgs a, const __grid_constant__ WaveFields w) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  double m = 0.0;
+  if (r < a.nrows) {
+    const int4 h = __ldg(a.star + 2 * r), t = __ldg(a.star + 2 * r + 1);
+    const HalfKick hk{w.phi_in, w.p_in, w.half_dt};
+    const double b = star_row<F>(a, r, h, t, hk);
+    double p = __dadd_rn(__ldg(w.p_in + r), __dmul_rn(b, __ldg(w.pc + r)));
+    if (w.bc[r]) p = w.state[1];
+    w.p_out[r] = p;
+    w.phi_out[r] = __dsub_rn(hk(r), __dmul_rn(w.half_dt, p));
+    m = fabs(p);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q) m = fmax(m, wm[q]);
+    // non-negative doubles order like their bit patterns
+    atomicMax(reinterpret_cast<unsigned long long*>(w.state + 2), (unsigned long long)__double_as_longlong(m));
+  }
 }
 
 // Star records of the node map (host build; false if a star is not a single
@@ -2597,6 +2661,9 @@ bool fast_pattern(const Entry& k, const loam_arg_desc* args, int nargs) {
   return true;
 }
 
+// set while wave_step() asks run_fast for the loop's plan instead of a launch
+thread_local std::shared_ptr<FastPlan>* g_plan_probe = nullptr;
+
 void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const FormParams& prm,
               cudaStream_t s, bool cell_mode = false) {
   std::vector<uint64_t> key{(uint64_t)k.form, (uint64_t)k.gd, (uint64_t)k.nrn, (uint64_t)k.ncn,
@@ -2626,6 +2693,10 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
       std::lock_guard<std::mutex> g(g_cache_mutex);
       g_fast_cache[key] = P;
     }
+  }
+  if (g_plan_probe) {
+    *g_plan_probe = P;
+    return;
   }
   if (P->use_star) {
     StarArgs t{};
@@ -3101,6 +3172,39 @@ void execute(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_de
     }
   }
   run_generic(k, n, iter, args, nargs, prm, s);
+}
+
+void wave_step(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_desc* args, int nargs,
+               const double* p_in, const double* phi_in, double* p_out, double* phi_out, const double* pc,
+               const uint8_t* bc, double half_dt, double* state, cudaStream_t s) {
+  require(kd != nullptr, LOAM_ERR(InvalidArgument), "parloop without kernel");
+  const Entry& k = lookup(kd->name);
+  validate_args(k, n, iter, args, nargs);
+  require(k.form == F_STIFFNESS_ACTION && k.gd == 2 && k.nrn == 3 && !k.bilinear && nargs == 3,
+          LOAM_ERR(UnsupportedForm), "wave step: the action must be stiffness_action_p1_tri");
+  require(options().inc_strategy == 0 && fast_pattern(k, args, nargs), LOAM_ERR(UnsupportedForm),
+          "wave step: needs the auto strategy's vertex-star plan");
+  std::shared_ptr<FastPlan> P;
+  g_plan_probe = &P;
+  try {
+    run_fast(k, n, args, nargs, FormParams{{0, 0, 0, 0}}, s);
+  } catch (...) {
+    g_plan_probe = nullptr;
+    throw;
+  }
+  g_plan_probe = nullptr;
+  require(P && P->use_star, LOAM_ERR(UnsupportedForm), "wave step: the mesh has no vertex-star plan");
+  StarArgs t{};
+  t.star = P->star.get();
+  t.nrows = args[0].set_size;
+  t.coords = args[1].data;
+  t.coeff = nullptr;
+  t.out = nullptr;
+  WaveFields w{p_in, phi_in, p_out, phi_out, pc, bc, half_dt, state};
+  if (t.nrows == 0) return;
+  k_wave_step<FormT<F_STIFFNESS_ACTION, 2, 1>><<<ceil_div(t.nrows, 256), 256, 0, s>>>(t, w);
+  count_launch();
+  LG_LAUNCH_CHECK();
 }
 
 void plan_cache_clear() {

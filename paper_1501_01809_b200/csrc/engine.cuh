@@ -27,6 +27,11 @@ void validate(const loam_kernel_desc* k, int n, uint64_t iter_id, const loam_arg
 void execute(const loam_kernel_desc* k, int n, uint64_t iter_id, const loam_arg_desc* args,
              int nargs, cudaStream_t s);
 void plan_cache_clear();
+// bench::run_wave's step (bench.hpp:267-289) fused into the vertex-star
+// stiffness action of `args` (b INC, X READ, phi READ; engine.cu k_wave_step).
+void wave_step(const loam_kernel_desc* k, int n, uint64_t iter_id, const loam_arg_desc* args, int nargs,
+               const double* p_in, const double* phi_in, double* p_out, double* phi_out, const double* pc,
+               const uint8_t* bc, double half_dt, double* state, cudaStream_t s);
 
 // Services.
 void map_check(const loam_map_desc* m, cudaStream_t s);

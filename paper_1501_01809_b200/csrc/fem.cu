@@ -74,6 +74,7 @@ __global__ void k_wave_clock(double* s, double dt, double first_period, int phas
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (phase == 0) {
     s[1] = sin(10.0 * M_PI * s[0]);
+    s[2] = 0.0; // |p| of this step: written by the reduction, or max-folded by the fused step
     return;
   }
   s[0] += dt;

@@ -18,6 +18,7 @@ sequential sums as in the reference) match bench::run_wave's samples.
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
 
 import numpy as np
@@ -114,10 +115,55 @@ class WaveLoop:
         capi.check(lib.loam_gpu_reduce_dev(self.p.data.data_ptr(), self.p.set.size, capi.REDUCE_MAX_ABS, sp + 16, sh))
         capi.check(lib.loam_gpu_wave_clock(sp, self.dt, 0.2, 1, sh))
 
-    def run_graph(self, batch: int = 100, max_steps: int | None = None):
+    # ---- the step fused into the vertex-star action (loam_gpu_wave_step) ----
+    # One kernel per step instead of six (pointwise x3, action, bc, |p|): the
+    # half-kick of every gathered neighbour is formed on the fly and the owner
+    # of each vertex applies kick, forcing and half-kick; p and phi ping-pong
+    # between the Dats and a second buffer pair.  Bitwise equal to the
+    # unfused chain (tests/test_fem_gpu.py).
+
+    def _fused_setup(self) -> bool:
+        if getattr(self, "_fz", None) is not None:
+            return self._fz is not False
+        nv = self.verts.size
+        mask = torch.zeros(max(nv, 1), dtype=torch.uint8, device="cuda")
+        mask[self.bc._dev.long()] = 1
+        pb, phib = torch.empty_like(self.p.data), torch.empty_like(self.phi.data)
+        kd, descs, keep = L._build(self.action)
+        probe = torch.zeros(6, dtype=torch.float64, device="cuda")
+        try:  # also builds the loop's plan outside any capture
+            self._fused_call(kd, descs, self.p.data, self.phi.data, pb, phib, mask, probe)
+        except capi.LoamError as e:
+            if e.kind != "UnsupportedForm":
+                raise
+            self._fz = False
+            return False
+        self._fz = (kd, descs, keep, mask, pb, phib)
+        for d in (self.p, self.phi):  # written behind the Dat's back from here on
+            d._materialize()
+            d._zero = d._stale = False
+        return True
+
+    def _fused_call(self, kd, descs, p_in, phi_in, p_out, phi_out, mask, state):
+        capi.check(capi.lib().loam_gpu_wave_step(
+            C.byref(kd), self.cells.size, self.cells.id, descs, len(self.action.args), p_in.data_ptr(),
+            phi_in.data_ptr(), p_out.data_ptr(), phi_out.data_ptr(), self.p_constant.data.data_ptr(),
+            mask.data_ptr(), self.dt / 2, state.data_ptr(), torch.cuda.current_stream().cuda_stream))
+
+    def _fused_step(self, state, parity: int):
+        kd, descs, keep, mask, pb, phib = self._fz
+        lib, sh = capi.lib(), torch.cuda.current_stream().cuda_stream
+        A, B = (self.p.data, self.phi.data), (pb, phib)
+        src, dst = (A, B) if parity == 0 else (B, A)
+        capi.check(lib.loam_gpu_wave_clock(state.data_ptr(), self.dt, 0.2, 0, sh))
+        self._fused_call(kd, descs, src[0], src[1], dst[0], dst[1], mask, state)
+        capi.check(lib.loam_gpu_wave_clock(state.data_ptr(), self.dt, 0.2, 1, sh))
+
+    def run_graph(self, batch: int = 100, max_steps: int | None = None, fused: bool = True):
         """run() through CUDA graphs of `batch` steps (`batch` divides 100, so the
         every-100-steps diagnostics fall on batch boundaries); the steps after
-        the last full batch run one by one as in run()."""
+        the last full batch run one by one as in run().  `fused`: one kernel per
+        step (loam_gpu_wave_step) when the action runs on vertex stars."""
         assert batch >= 1 and 100 % batch == 0
         t, remaining = self.t, 0  # the step count run() would take (same double arithmetic)
         while t <= self.T and (max_steps is None or remaining < max_steps):
@@ -130,9 +176,16 @@ class WaveLoop:
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
+        fused = fused and self._fused_setup()
         with torch.cuda.graph(g, stream=side):
-            for _ in range(batch):
-                self._device_step(state)
+            for i in range(batch):
+                if fused:
+                    self._fused_step(state, i & 1)
+                else:
+                    self._device_step(state)
+            if fused and batch & 1:  # the fields end in the second buffers
+                self.p.data.copy_(self._fz[4])
+                self.phi.data.copy_(self._fz[5])
         torch.cuda.current_stream().wait_stream(side)
         while remaining >= batch and self.steps % batch == 0:
             g.replay()

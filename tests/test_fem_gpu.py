@@ -164,3 +164,16 @@ def test_wave_chain_in_cuda_graphs(gpu_lib, batch):
     assert got.shape == ref.shape and got.shape[0] >= 3
     assert np.array_equal(got[:, 0], ref[:, 0])
     assert np.max(np.abs(got[:, 1:] - ref[:, 1:]) / np.abs(ref[:, 1:])) <= 1e-10
+
+
+@pytest.mark.parametrize("batch", [1, 10])
+def test_fused_wave_step_equals_unfused_chain_bitwise(gpu_lib, batch):
+    """loam_gpu_wave_step (one kernel per step: half-kick gathered on the fly,
+    kick, forcing, half-kick and |p| in the vertex-star owner) against the
+    six-kernel chain: identical samples and identical p / phi bits."""
+    from paper_1501_01809_b200.wave import WaveLoop
+    a, b = WaveLoop(16, 1e-3, 0.25), WaveLoop(16, 1e-3, 0.25)
+    sa, sb = np.array(a.run_graph(batch, fused=True)), np.array(b.run_graph(batch, fused=False))
+    assert a._fz and b.__dict__.get("_fz") is None  # the fused path really ran
+    assert np.array_equal(sa, sb)
+    assert np.array_equal(a.p.view(), b.p.view()) and np.array_equal(a.phi.view(), b.phi.view())
