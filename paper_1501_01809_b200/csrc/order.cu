@@ -28,6 +28,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
 #include <string>
 
 #include "mesh.cuh"
@@ -146,6 +147,90 @@ __global__ void k_rcm_emit(int base, int m, const unsigned long long* __restrict
   }
 }
 
+// Consecutive BFS levels in ONE block while a level's candidates fit a
+// shared-memory sort (kLevelCap keys): expand -> keys -> bitonic sort -> emit
+// per level with block barriers instead of ~8 launches and a host read.
+// Reads of data other threads of this launch wrote go around L1 (ld.cg).
+// Stops when the component is exhausted (cur[2] = 0) or a level overflows
+// the cap (cur[3] = its candidate count: cand / parent / touched are set,
+// the host sorts and emits that level).  cur = {pos, base, m, overflow}.
+constexpr int kLevelCap = 4096, kLevelThreads = 1024;
+
+__global__ void __launch_bounds__(kLevelThreads) k_rcm_levels(const int64_t* __restrict__ rp,
+                                                              const int32_t* __restrict__ ci, int32_t* order,
+                                                              uint8_t* visited, int32_t* parent, int32_t* touched,
+                                                              int32_t* cand, const int32_t* __restrict__ rank,
+                                                              const int32_t* __restrict__ byrank, int* cur) {
+  __shared__ unsigned long long sk[kLevelCap];
+  __shared__ int s_cnt;
+  const int tid = threadIdx.x;
+  int pos = cur[0], base = cur[1], m = cur[2];
+  while (m > 0 && m <= kLevelCap / 2) { // wide frontiers go back to the grid-wide path
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    for (int w = tid; w < m; w += kLevelThreads) { // a thread per frontier vertex: one latency chain per level
+      const int p = base + w, u = __ldcg(order + p);
+      for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {
+        const int v = ci[k];
+        if (__ldcg(visited + v)) continue;
+        atomicMin(&parent[v], p);
+        if (atomicExch(&touched[v], 1) == 0) cand[atomicAdd(&s_cnt, 1)] = v;
+      }
+    }
+    __syncthreads();
+    const int cnt = s_cnt;
+    if (cnt == 0 || cnt > kLevelCap) {
+      if (tid == 0) {
+        cur[0] = pos;
+        cur[1] = base;
+        cur[2] = cnt == 0 ? 0 : m;
+        cur[3] = cnt;
+      }
+      return;
+    }
+    int P = 1;
+    while (P < cnt) P <<= 1;
+    for (int i = tid; i < P; i += kLevelThreads) {
+      if (i < cnt) {
+        const int v = __ldcg(cand + i);
+        sk[i] = ((unsigned long long)(unsigned)__ldcg(parent + v) << 32) | (unsigned)rank[v];
+      } else {
+        sk[i] = ~0ull;
+      }
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = tid; i < P; i += kLevelThreads) {
+          const int x = i ^ j;
+          if (x > i) {
+            const unsigned long long a = sk[i], b = sk[x];
+            if ((a > b) == ((i & k) == 0)) {
+              sk[i] = b;
+              sk[x] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int i = tid; i < cnt; i += kLevelThreads) {
+      const int v = byrank[(unsigned)sk[i]];
+      order[pos + i] = v;
+      visited[v] = 1;
+    }
+    __syncthreads();
+    base = pos;
+    m = cnt;
+    pos += cnt;
+  }
+  if (tid == 0) { // exhausted (m == 0) or a wide frontier (m > cap / 2): no level pending
+    cur[0] = pos;
+    cur[1] = base;
+    cur[2] = m;
+    cur[3] = -1;
+  }
+}
+
 __global__ void k_reverse(int n, const int32_t* __restrict__ in, int32_t* __restrict__ out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[n - 1 - i] = in[i];
 }
@@ -258,6 +343,8 @@ void rcm_order_dev(int n, const int64_t* rp, const int32_t* ci, int32_t* out, cu
   LG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, keys.get(), skeys.get(), n, 0, 64, s));
   DevBuf<uint8_t> sort_tmp(sort_bytes ? sort_bytes : 1, s);
   int pos = nz, cursor = nz;
+  static const bool use_levels = !std::getenv("LOAM_GPU_RCM_NO_BLOCK");
+  DevBuf<int> lcur(4, s);
   int hc[2];
   while (pos < n) {
     // next seed: the first unvisited vertex of the (degree, index) order
@@ -277,6 +364,32 @@ void rcm_order_dev(int n, const int64_t* rp, const int32_t* ci, int32_t* out, cu
     int base = pos, m = 1;
     ++pos;
     while (m > 0) {
+      if (use_levels && m <= kLevelCap / 2) { // as many levels as fit one block's sort, in one launch
+        int hcur[4] = {pos, base, m, 0};
+        LG_CUDA(cudaMemcpyAsync(lcur.get(), hcur, sizeof(hcur), cudaMemcpyHostToDevice, s));
+        k_rcm_levels<<<1, kLevelThreads, 0, s>>>(rp, ci, order.get(), visited.get(), parent.get(), touched.get(),
+                                                cand.get(), rank.get(), byrank.get(), lcur.get());
+        count_launch();
+        LG_CUDA(cudaMemcpyAsync(hcur, lcur.get(), sizeof(hcur), cudaMemcpyDeviceToHost, s));
+        LG_CUDA(cudaStreamSynchronize(s));
+        pos = hcur[0];
+        base = hcur[1];
+        m = hcur[2];
+        if (m == 0) break;
+        if (hcur[3] < 0) continue; // frontier too wide for the block: the grid-wide path takes the next level
+        // this level overflowed the block sort: its candidates are listed
+        const int mc = hcur[3];
+        k_rcm_keys<<<grid_for(mc), kThreads, 0, s>>>(mc, cand.get(), parent.get(), rank.get(), keys.get());
+        count_launch();
+        size_t b = sort_bytes;
+        LG_CUDA(cub::DeviceRadixSort::SortKeys(sort_tmp.get(), b, keys.get(), skeys.get(), mc, 0, 32 + rank_bits, s));
+        k_rcm_emit<<<grid_for(mc), kThreads, 0, s>>>(pos, mc, skeys.get(), byrank.get(), order.get(), visited.get());
+        count_launch();
+        base = pos;
+        m = mc;
+        pos += mc;
+        continue;
+      }
       LG_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int), s));
       k_rcm_expand<<<grid_for((int64_t)m * 32), kThreads, 0, s>>>(base, m, order.get(), rp, ci, visited.get(),
                                                                   parent.get(), touched.get(), cand.get(),
