@@ -14,16 +14,25 @@ CUDA events on the launching stream; N>1 runs N independent replicas (one
 rank per GPU, weak scaling) and takes the max over ranks.
 
   value      assembled cells/s (whole job)
-  e2e        same metric through loam_gpu_execute_host (the reference calling
-             convention, host buffers): H2D of maps/pattern/coordinates and
-             D2H of the values inside the timed region
+  e2e        same metric through loam_gpu_execute_host_batch (the reference
+             calling convention, host buffers): H2D of the coordinates and D2H
+             of the values inside the timed region; cold_one_shot = a whole
+             assemble_matrix with nothing cached (uploads, build_sparsity,
+             plan, execute, download)
   roofline   minimal algorithmic bytes (map int32 + coords fp64 + values fp64
-             written once) / kernel time vs MEASURED_PEAKS.json hbm_gbs
+             written once) / mean kernel time vs MEASURED_PEAKS.json hbm_gbs
+  sparsity_build  C2's build_sparsity on the device vs its roofline (C2-sp)
   cpu_baseline  the reference's own par_loop (oracle/_ref: loam::execute with
-             the reference's optimised AST kernel, all host threads) on a
-             bounded sample of the same workload (256^2 mesh, same generator)
+             the reference's optimised AST kernel) on the full C2 mesh at all
+             host threads, plus 1-thread and compiled-host-kernel lines and
+             the CPU model
+  all_configs   the six BASELINE workloads: GPU ms, cells/s, HBM fraction,
+             first-call plan build, and the reference engine's cells/s on a
+             bounded sample of each
 
---impl reference runs only the reference CPU arm (rank 0) and prints its line.
+--impl reference runs only the reference CPU arm (rank 0) on the SAME workload
+(full C2 mesh, inputs from the oracle's restated generator, so the product
+library is never loaded there), --steps / --warmup as given.
 --all-configs (developer) prints one line per config/strategy for profiles/.
 """
 from __future__ import annotations
@@ -45,7 +54,6 @@ sys.path.insert(0, ROOT)
 METRIC = "assembled cells/s + achieved HBM GB/s vs peak for P1/P2 residual & CSR matrix"
 UNIT = "cells/s"
 WORKLOAD = "C2: P1 Laplace stiffness CSR assembly, unit square 1024x1024 (2,097,152 cells)"
-REF_SAMPLE_N = 256  # reference CPU arm: 131,072-cell mesh of the same generator
 
 
 def peaks():
@@ -204,11 +212,13 @@ def protocol_floor(torch, flush, stream, reps=10):
     return out
 
 
-def config_table(torch, flush, stream, steps=5):
+def config_table(torch, flush, stream, steps=5, cpu=True):
     """Every BASELINE config at full size through `auto` (the same flushed
     per-step protocol as the headline, median of `steps`): cells/s and the
     fraction of the measured HBM peak, so the contract line carries the whole
-    table measured on the same box."""
+    table measured on the same box.  plan_build_s = the first execute (plan
+    construction + the assembly); cpu_* = the compiled reference engine with
+    the restated host kernel on a bounded sample of the same workload."""
     from paper_1501_01809_b200 import capi, configs
     peak, _ = peaks()
     names = {(1, None): "C1 P1 Helmholtz residual 512^2", (2, None): "C2 P1 Laplace CSR 1024^2",
@@ -218,19 +228,72 @@ def config_table(torch, flush, stream, steps=5):
     capi.set_strategy("auto")
     for (cfg, part), name in names.items():
         w = configs.Workload(cfg, None, part)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         w.reset()
         w.run()
+        torch.cuda.synchronize()
+        plan_s = time.perf_counter() - t0
         for _ in range(2):
             w.reset()
             flush()
             w.run()
         ms = float(np.median(time_steps(torch, w, steps, flush, stream)))
         ab = algorithmic_bytes(w)
-        rows.append({"config": name, "ms": round(ms, 4), "cells_per_s": w.inputs.ncells / (ms * 1e-3),
-                     "frac": round(ab / (ms * 1e-3) / 1e9 / peak, 3)})
+        row = {"config": name, "ms": round(ms, 4), "cells_per_s": w.inputs.ncells / (ms * 1e-3),
+               "frac": round(ab / (ms * 1e-3) / 1e9 / peak, 3), "plan_build_s": round(plan_s, 4)}
+        if cpu:
+            try:
+                row.update(reference_config_cpu(cfg, part, os.cpu_count() or 1))
+            except Exception as exc:  # noqa: BLE001
+                row["cpu_error"] = str(exc)
+        rows.append(row)
         del w
         torch.cuda.empty_cache()
     return rows
+
+
+def sparsity_build(torch, w, reps=5):
+    """C2-sp: build_sparsity of the C2 cell->vertex map on the
+    device (keys, radix sort, unique, row offsets) against its 62,955,540-byte
+    roofline (map read + row_ptr + col_idx written once)."""
+    from paper_1501_01809_b200 import loam as L
+    peak, _ = peaks()
+    ts = []
+    for _ in range(reps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sp = L.build_sparsity(w.cvm, w.cvm)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+        del sp
+    ms = 1e3 * float(np.median(ts[1:]))
+    m = w.inputs
+    ab = m.ncells * 3 * 4 + (m.nv + 1) * 8 + w.outputs[0].sparsity.nnz * 4
+    return {"ms": ms, "algorithmic_bytes": ab, "frac": ab / (ms * 1e-3) / 1e9 / peak,
+            "note": "host wall clock around loam_gpu_build_sparsity (one call, synchronous)"}
+
+
+def cold_one_shot(torch, m):
+    """A reference user's one-shot fem::assemble_matrix (assemble.hpp:85-104) on
+    the C2 inputs through the device API with nothing cached: upload the map
+    and coordinates, build_sparsity, plan + assemble, download the values."""
+    from paper_1501_01809_b200 import loam as L
+    out = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cells, verts = L.Set(m.ncells), L.Set(m.nv)
+        cv = L.Map(cells, verts, 3, m.cv)
+        X = L.Dat(verts, 2)
+        X.set_values(m.coords)
+        A = L.Mat(L.build_sparsity(cv, cv))
+        L.execute(L.Parloop(L.kernel("stiffness_p1_tri"), cells, [L.arg(A, L.INC, cv, cv), L.arg(X, L.READ, cv)]))
+        vals = A.host_values()
+        torch.cuda.synchronize()
+        out.append(time.perf_counter() - t0)
+        del cells, verts, cv, X, A, vals
+    return {"s": min(out), "includes": "H2D map + coordinates, build_sparsity, plan build, execute, D2H values"}
 
 
 def e2e_host(torch, w, steps, warmup):
@@ -285,14 +348,102 @@ def e2e_host(torch, w, steps, warmup):
     return times, h2d, d2h, float(np.mean(seq))
 
 
-def reference_sample(threads, warmup, steps, n=REF_SAMPLE_N):
-    """The reference's own par_loop on the host cores (oracle/_ref)."""
+def cpu_model() -> str:
+    """The host CPU model (lscpu's "Model name"), from /proc/cpuinfo."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_c2(threads, warmup, steps, n=None, as_shipped=True):
+    """The reference's own par_loop (oracle/_ref: loam::execute, parloop.hpp:191)
+    on the C2 workload, inputs from the oracle's restatement of the generator
+    (bit-identical to the GPU arm's, tests/test_oracle_cpu.py) -- the product
+    library is never loaded here.  as_shipped: the reference's optimised AST
+    kernel (assemble.hpp:16-19); else the restated compiled host kernel
+    (kernel.hpp:523-529).  Returns (cells, per-step seconds)."""
     import oracle as O
-    from paper_1501_01809_b200 import configs
-    m = configs.config_inputs(2, n)
-    times = O.ref_time_execute(O.STIFFNESS, 1, 2, m.cv, m.coords, as_shipped=True, threads=threads,
+    m = O.inputs(2, n)
+    times = O.ref_time_execute(O.STIFFNESS, 1, 2, m.cv, m.coords, as_shipped=as_shipped, threads=threads,
                                warmup=warmup, steps=steps)
     return m.ncells, times
+
+
+# per-config CPU figures: the compiled reference ENGINE (build_sparsity + execute +
+# Mat::addto) with the restated host kernel, on bounded samples of each workload
+CPU_SAMPLES = {(1, None): 512, (2, None): 1024, (3, "residual"): 32, (3, "matrix"): 16, (4, None): 32,
+               (5, None): 256}
+
+
+def reference_config_cpu(cfg, part, threads):
+    import oracle as O
+    n = CPU_SAMPLES[(cfg, part)]
+    m = O.inputs(cfg, n)
+    run = []
+    if cfg == 1:
+        run.append(dict(form=O.HELMHOLTZ_ACTION, degree=1, gdim=2, row_map=m.cv, ar_r=3, nrt=m.nv, col_map=None,
+                        ar_c=0, nct=0, coeff=m.extra["u"], params=(1.0,)))
+    elif cfg == 2:
+        run.append(dict(form=O.STIFFNESS, degree=1, gdim=2, row_map=m.cv, ar_r=3, nrt=m.nv, col_map=m.cv, ar_c=3,
+                        nct=m.nv, params=()))
+    elif cfg == 3:
+        cn, nn = m.extra["p2"], m.extra["nn"]
+        if part == "residual":
+            run.append(dict(form=O.HELMHOLTZ_ACTION, degree=2, gdim=3, row_map=cn, ar_r=10, nrt=nn, col_map=None,
+                            ar_c=0, nct=0, coeff=m.extra["u"], params=(1.0,)))
+        else:
+            run.append(dict(form=O.HELMHOLTZ, degree=2, gdim=3, row_map=cn, ar_r=10, nrt=nn, col_map=cn, ar_c=10,
+                            nct=nn, params=(1.0,)))
+    elif cfg == 4:
+        dm = O.dof_map(m.cv, 4, 3)
+        run.append(dict(form=O.ELASTICITY, degree=1, gdim=3, row_map=dm, ar_r=12, nrt=3 * m.nv, col_map=dm, ar_c=12,
+                        nct=3 * m.nv, params=(1.0, 0.5)))
+    else:
+        cn, nn = m.extra["p2"], m.extra["nn"]
+        vd = O.dof_map(cn, 6, 2)
+        run += [dict(form=O.STOKES_A, degree=2, gdim=2, row_map=vd, ar_r=12, nrt=2 * nn, col_map=vd, ar_c=12,
+                     nct=2 * nn, params=(1.0,)),
+                dict(form=O.STOKES_B, degree=2, gdim=2, row_map=m.cv, ar_r=3, nrt=m.nv, col_map=vd, ar_c=12,
+                     nct=2 * nn, params=()),
+                dict(form=O.STOKES_BT, degree=2, gdim=2, row_map=vd, ar_r=12, nrt=2 * nn, col_map=m.cv, ar_c=3,
+                     nct=m.nv, params=())]
+    step, sp = 0.0, 0.0
+    for r in run:
+        t, s_ = O.ref_time_engine(r["form"], r["degree"], r["gdim"], m.ncells, r["row_map"], r["ar_r"], r["nrt"],
+                                  r["col_map"], r["ar_c"], r["nct"], m.cv, m.coords, coeff=r.get("coeff"),
+                                  params=r["params"], threads=threads, warmup=0, steps=1)
+        step += float(t.min())
+        sp += s_
+    return {"cpu_cells_per_s": m.ncells / step, "cpu_sample_cells": m.ncells, "cpu_threads": threads,
+            "cpu_build_sparsity_s": sp if sp else None}
+
+
+def cpu_baseline_block(threads):
+    """SURVEY 8d CPU lines on the GPU box's host cores: the as-shipped reference
+    (optimised AST kernel) and the compiled-host-kernel engine, at 1 thread and
+    at all threads, next to the CPU model."""
+    lines = []
+
+    def line(as_shipped, th, n, warmup, steps):
+        cells, t = reference_c2(th, warmup, steps, n, as_shipped)
+        lines.append({"kernel": "as-shipped AST (assemble.hpp:16-19)" if as_shipped else
+                      "compiled host kernel (kernel.hpp:523-529)", "threads": th, "cells": cells,
+                      "cells_per_s": cells / float(np.mean(t)), "steps": steps, "warmup": warmup})
+        return lines[-1]
+
+    main = line(True, threads, None, 1, 2)
+    line(True, 1, 128, 0, 2)
+    line(False, threads, None, 1, 2)
+    line(False, 1, None, 0, 1)
+    return {"value": main["cells_per_s"], "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": "oracle/_ref loam::execute with the reference's optimised AST stiffness_p1_tri on the full C2 "
+                      f"mesh ({main['cells']} cells), {threads} threads, mean of 2 after 1 warm-up",
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(), "lines": lines}
 
 
 # --------------------------------------------------------------------------- arms
@@ -321,25 +472,34 @@ def weak_value(cells_per_rank: int, world: int, ms: float) -> float:
 
 
 def reference_arm(args):
+    """The reference's own CPU par_loop on THIS arm's workload (full C2 mesh),
+    all host threads, honouring --steps / --warmup; rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    steps = max(1, min(args.steps, 3))
-    ncells, times = reference_sample(threads, min(args.warmup, 1), steps)
-    value = ncells / min(times)
+    ncells, times = reference_c2(threads, args.warmup, args.steps)
+    ms = 1e3 * float(np.mean(times))
+    value = ncells / (ms * 1e-3)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * float(np.mean(times)),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "sample_cells": ncells},
+        "data": "synthetic", "config": config_of(ncells),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"loam::execute(optimised AST stiffness_p1_tri) on the {REF_SAMPLE_N}^2 "
-                                   f"mesh ({ncells} cells) of the same generator, min of {steps}"},
+                         "sample": f"the whole workload: loam::execute (optimised AST stiffness_p1_tri) on the "
+                                   f"{ncells}-cell C2 mesh, {threads} threads, mean of {args.steps} steps after "
+                                   f"{args.warmup} warm-up", "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def config_of(cells):
+    """The workload both arms report (same dict: the driver compares them)."""
+    return {"workload": WORKLOAD, "cells": cells, "mesh": "unit square 1024^2, jitter 0.2h seed 2, "
+            "cell permutation seed 3 (splitmix64, SURVEY 8d)"}
 
 
 def gpu_arm(args):
@@ -390,7 +550,7 @@ def gpu_arm(args):
     value = weak_value(cells, world, ms)
     abytes = algorithmic_bytes(w)
     peak, peak_kind = peaks()
-    kernel_ms = float(np.median(times))
+    kernel_ms = float(np.mean(times))  # average launch duration (events on the launching stream)
     achieved = abytes / (kernel_ms * 1e-3) / 1e9
     # end to end through the C ABI with host buffers
     e2e_times, h2d, d2h, e2e_seq_ms = e2e_host(torch, w, max(4, args.steps), 2)
@@ -398,18 +558,16 @@ def gpu_arm(args):
         print("e2e step ms:", [round(t, 3) for t in e2e_times], file=sys.stderr)
     e2e_ms = max_over_ranks(float(np.mean(e2e_times)), "cuda")
     floor = protocol_floor(torch, flush, stream)
-    table = config_table(torch, flush, stream) if rank == 0 and not args.no_config_table else None
-    # correctness spot check of this very run against the reference pattern size
+    sp_build = sparsity_build(torch, w) if rank == 0 else None
+    cold = cold_one_shot(torch, w.inputs) if rank == 0 else None
+    table = (config_table(torch, flush, stream, cpu=not args.no_cpu_baseline)
+             if rank == 0 and not args.no_config_table else None)
     line = None
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
             try:
-                threads = os.cpu_count() or 1
-                ncells_s, ct = reference_sample(threads, 1, 2)
-                cpu = {"value": ncells_s / min(ct), "unit": UNIT, "cores": threads, "kind": "reference",
-                       "sample": f"oracle/_ref loam::execute (optimised AST stiffness_p1_tri) on the "
-                                 f"{REF_SAMPLE_N}^2 mesh of the same generator ({ncells_s} cells), min of 2"}
+                cpu = cpu_baseline_block(os.cpu_count() or 1)
             except Exception as exc:  # noqa: BLE001
                 cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                        "sample": f"unavailable: {exc}"}
@@ -417,15 +575,18 @@ def gpu_arm(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "cells": cells, "vertices": w.inputs.nv,
-                       "nnz": w.outputs[0].sparsity.nnz, "l2": "flushed before every step: 512 MiB write + 256 MiB read (cold, clean)",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "strategy": args.strategy, "plan_build_s": round(plan_s, 4)},
+            "config": config_of(cells),
+            "protocol": {"vertices": w.inputs.nv, "nnz": w.outputs[0].sparsity.nnz,
+                         "l2": "flushed before every step: 512 MiB write + 256 MiB read (cold, clean)",
+                         "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                         "strategy": args.strategy, "plan_build_s": round(plan_s, 4),
+                         "step": "one loam::execute into a fresh Mat whose sparsity was built beforehand"},
             "e2e": {"value": weak_value(cells, world, e2e_ms), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                     "path": "loam_gpu_execute_host_batch: per step H2D of the read Dats + kernel + D2H of the "
                             "values, uploads overlapping the previous step's downloads",
-                    "sequential_ms_per_step": e2e_seq_ms},
+                    "sequential_ms_per_step": e2e_seq_ms, "cold_one_shot": cold},
+            "sparsity_build": sp_build,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic("c2_matrix"),
                          "algorithmic_bytes": abytes, "kernel_ms": kernel_ms, "peak_kind": peak_kind,

@@ -88,6 +88,7 @@ typedef struct loam_map_desc {
   int32_t expand_dim; /* 0 or 1: plain map */
   const int32_t* node_values;
   int32_t node_arity, node_target_size;
+  uint64_t node_id;   /* identity of the declared node map (0 = unknown) */
 } loam_map_desc;
 
 /* loam::Sparsity (data.hpp:116-142): CSR, int64 row offsets, int32 columns. */
@@ -98,6 +99,17 @@ typedef struct loam_sparsity_desc {
   int64_t nnz;
   int32_t row_dim, col_dim; /* dof expansion the pattern was built with (>=1) */
   uint64_t id;
+  /* Provenance: the NODE-level maps the pattern was built from (the ids of
+   * build_sparsity's row / column maps, or of the node maps a dof-expanded map
+   * declares) and the dof dims at that level; 0 = unknown.  A loop whose
+   * (row, column) maps are exactly these has exactly this pattern, so an
+   * owner-computes kernel may write a fresh Mat's rows without zero-filling
+   * them first.  Any other loop -- a sub-mesh loop into a whole-mesh pattern
+   * (legal: parloop.hpp:119-121 compares shapes only) -- may touch only part
+   * of the pattern: the library then zero-fills a fresh Mat before the loop
+   * (data.hpp:185-187: untouched entries stay zero). */
+  uint64_t pattern_row_map, pattern_col_map;
+  int32_t pattern_row_dim, pattern_col_dim;
 } loam_sparsity_desc;
 
 /* loam::Arg (parloop.hpp:17-52) over a Dat, Mat or Global. */
@@ -151,6 +163,14 @@ enum loam_option { LOAM_OPT_INC_STRATEGY = 0, LOAM_OPT_CHECK_SPARSITY = 1, LOAM_
 int loam_gpu_set_option(int option, int value);
 int loam_gpu_get_option(int option);
 int loam_gpu_plan_cache_clear(void);
+/* Object identities.  Plans (colourings, pair lists, tiles) and the resident
+ * host-call copies are cached by the ids in the descriptors, so ids must be
+ * unique per process across every client (C++ facade, Python mirror, FFI
+ * bindings): take them from loam_gpu_new_id().  loam_gpu_release_id(id)
+ * evicts every cached plan and resident copy keyed by `id` (call it when a
+ * Map or Sparsity is destroyed). */
+uint64_t loam_gpu_new_id(void);
+int loam_gpu_release_id(uint64_t id);
 /* Number of kernels this library launched since load (bench gpu_launches). */
 int64_t loam_gpu_launch_count(void);
 

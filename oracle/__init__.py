@@ -563,3 +563,99 @@ def ref_reorder(gdim, cv, coords):
     if rc:
         raise KindError(-rc, L.ref_last_error().decode())
     return perm[:nv], xo[: coords.size], co[: cv.size]
+
+
+# ------------------------------------------- seeded synthetic inputs (bench --impl reference)
+# BASELINE.json configs[0..4]; the same constants as paper_1501_01809_b200/configs.py
+# (tests/test_oracle_cpu.py checks both generators produce identical bits), kept
+# here so the reference arm never loads the product library.
+FULL = {1: 512, 2: 1024, 3: 64, 4: 96, 5: 768}
+JITTER = {1: (0.2, 0), 2: (0.2, 2), 3: (0.15, 4), 4: (0.1, 6), 5: (0.2, 7)}
+PERM_SEED = {1: 1, 2: 3, 3: 5, 4: None, 5: 8}
+
+
+class Inputs:
+    def __init__(self, gdim, n, coords, cv):
+        self.gdim, self.n, self.coords, self.cv, self.extra = gdim, n, coords, cv, {}
+
+    @property
+    def nv(self):
+        return self.coords.size // self.gdim
+
+    @property
+    def ncells(self):
+        return self.cv.size // (self.gdim + 1)
+
+
+def _gen_protos():
+    L = orc()
+    if not getattr(L, "_gen", False):
+        L.orc_unit_square_mesh.argtypes = [C.c_int, DP, IP]
+        L.orc_unit_cube_mesh.argtypes = [C.c_int, DP, IP]
+        L.orc_jitter.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint64, DP]
+        L.orc_permute_cells.argtypes = [C.c_int, C.c_int, C.c_uint64, IP]
+        L.orc_uniform.argtypes = [C.c_int64, C.c_uint64, C.c_double, C.c_double, DP]
+        L._gen = True
+    return L
+
+
+def mesh(gdim, n, amp=0.0, jitter_seed=None, perm_seed=None):
+    L = _gen_protos()
+    if gdim == 2:
+        coords, cv = np.empty((n + 1) ** 2 * 2), np.empty(2 * n * n * 3, dtype=np.int32)
+        _check(L.orc_unit_square_mesh(n, dp(coords), ip(cv)))
+    else:
+        coords, cv = np.empty((n + 1) ** 3 * 3), np.empty(6 * n ** 3 * 4, dtype=np.int32)
+        _check(L.orc_unit_cube_mesh(n, dp(coords), ip(cv)))
+    if jitter_seed is not None and amp:
+        _check(L.orc_jitter(gdim, n, amp, jitter_seed, dp(coords)))
+    if perm_seed is not None:
+        _check(L.orc_permute_cells(cv.size // (gdim + 1), gdim + 1, perm_seed, ip(cv)))
+    return Inputs(gdim, n, coords, cv)
+
+
+def uniform(count, seed, lo, hi):
+    out = np.empty(count)
+    _check(_gen_protos().orc_uniform(count, seed, lo, hi, dp(out)))
+    return out
+
+
+def inputs(cfg, n=None):
+    """BASELINE config `cfg` (1..5) at size n (default full), generated by the restatement."""
+    n = FULL[cfg] if n is None else n
+    gdim = 3 if cfg in (3, 4) else 2
+    amp, js = JITTER[cfg]
+    m = mesh(gdim, n, amp, js, PERM_SEED[cfg])
+    if cfg == 1:
+        m.extra["u"] = uniform(m.nv, 1000, 0.0, 1.0)
+    if cfg in (3, 5):
+        m.extra["p2"], m.extra["nn"] = p2_cell_node_map(m.cv, m.nv, gdim)
+    if cfg == 3:
+        m.extra["u"] = uniform(m.extra["nn"], 1002, -1.0, 1.0)
+    return m
+
+
+def dof_map(nodes, arity, dim):
+    v = np.asarray(nodes, np.int64).reshape(-1, arity)
+    return (v[:, :, None] * dim + np.arange(dim)).reshape(-1).astype(np.int32)
+
+
+def ref_time_engine(form, degree, gdim, ncells, row_map, ar_r, nrt, col_map, ar_c, nct, coord_map, coords,
+                    coeff=None, params=(), threads=1, warmup=1, steps=3):
+    """The compiled reference ENGINE (build_sparsity + execute + addto) with the
+    restated host kernel (kernel.hpp:523-529) on arbitrary maps: per-step
+    seconds of zero + execute, and the build_sparsity seconds (matrices)."""
+    L = ref()
+    L.ref_time_engine.argtypes = [C.c_int, C.c_int, C.c_int, DP, C.c_int, IP, C.c_int, C.c_int, IP, C.c_int,
+                                  C.c_int, IP, C.c_int, DP, DP, C.c_int, C.c_int, C.c_int, DP, DP]
+    rm = np.ascontiguousarray(row_map, dtype=np.int32)
+    cm = rm if col_map is None else np.ascontiguousarray(col_map, dtype=np.int32)
+    xm = np.ascontiguousarray(coord_map, dtype=np.int32)
+    times = np.zeros(steps)
+    sp = np.zeros(1)
+    _check(L.ref_time_engine(form, degree, gdim, dp(_params(params)), ncells, ip(rm), ar_r, nrt,
+                             None if col_map is None else ip(cm), ar_c, nct, ip(xm), coords.size // gdim,
+                             dp(np.ascontiguousarray(coords)),
+                             None if coeff is None else dp(np.ascontiguousarray(coeff)),
+                             threads, warmup, steps, dp(times), dp(sp)), L)
+    return times, float(sp[0])

@@ -857,3 +857,109 @@ int orc_rcm_order(int n, const int64_t* row_ptr, const int32_t* col_idx, int32_t
   }
   return ORC_OK;
 }
+
+/* ---- seeded synthetic inputs (bench --impl reference) -------- */
+/* The reference has no jitter / permutation / coefficient generator; the
+ * meshes themselves restate unit_square_mesh (mesh.hpp:96-143: vertices
+ * row-major, cells (a,b,c),(a,c,d) per square, a=SW b=SE c=NE d=NW) and
+ * unit_cube_mesh (mesh.hpp:148-214: six Kuhn tets per cube, one per axis
+ * permutation, odd permutations re-oriented).  The stream is splitmix64 with
+ * u = (x >> 11) * 2^-53.  tests/test_oracle_cpu.py checks these
+ * against the compiled reference's meshes and against the product's own
+ * generator bit-for-bit. */
+static uint64_t orc_sm64(uint64_t* st) {
+  uint64_t z = (*st += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static double orc_sm64_u(uint64_t* st) { return (double)(orc_sm64(st) >> 11) * 0x1.0p-53; }
+
+int orc_unit_square_mesh(int n, double* coords, int32_t* cv) {
+  if (n < 1) return ORC_ERR_INVALID_ARGUMENT;
+  for (int j = 0; j <= n; ++j)
+    for (int i = 0; i <= n; ++i) {
+      const int64_t v = (int64_t)j * (n + 1) + i;
+      coords[2 * v] = (double)i / n;
+      coords[2 * v + 1] = (double)j / n;
+    }
+  int64_t w = 0;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      const int32_t a = j * (n + 1) + i, b = a + 1, c = a + n + 2, d = a + n + 1;
+      const int32_t t[6] = {a, b, c, a, c, d};
+      for (int q = 0; q < 6; ++q) cv[w++] = t[q];
+    }
+  return ORC_OK;
+}
+
+int orc_unit_cube_mesh(int n, double* coords, int32_t* cv) {
+  static const int axes[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  if (n < 1) return ORC_ERR_INVALID_ARGUMENT;
+  const int64_t s = n + 1;
+  for (int k = 0; k <= n; ++k)
+    for (int j = 0; j <= n; ++j)
+      for (int i = 0; i <= n; ++i) {
+        const int64_t v = ((int64_t)k * s + j) * s + i;
+        coords[3 * v] = (double)i / n;
+        coords[3 * v + 1] = (double)j / n;
+        coords[3 * v + 2] = (double)k / n;
+      }
+  int64_t w = 0;
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i)
+        for (int p = 0; p < 6; ++p) {
+          int x[3] = {i, j, k};
+          int32_t t[4];
+          t[0] = (int32_t)(((int64_t)x[2] * s + x[1]) * s + x[0]);
+          for (int q = 0; q < 3; ++q) {
+            x[axes[p][q]]++;
+            t[q + 1] = (int32_t)(((int64_t)x[2] * s + x[1]) * s + x[0]);
+          }
+          /* the odd axis permutations (one transposition from identity) give
+             negatively oriented tets: swap the last two vertices */
+          const int odd = (p == 1 || p == 2 || p == 5);
+          if (odd) {
+            const int32_t tmp = t[2];
+            t[2] = t[3];
+            t[3] = tmp;
+          }
+          for (int q = 0; q < 4; ++q) cv[w++] = t[q];
+        }
+  return ORC_OK;
+}
+
+int orc_jitter(int gdim, int n, double amp, uint64_t seed, double* coords) {
+  if ((gdim != 2 && gdim != 3) || n < 1) return ORC_ERR_INVALID_ARGUMENT;
+  const int64_t s = n + 1, nv = gdim == 2 ? s * s : s * s * s;
+  const double h = 1.0 / n;
+  uint64_t st = seed;
+  for (int64_t v = 0; v < nv; ++v) {
+    const int64_t i = v % s, j = (v / s) % s, k = gdim == 3 ? v / (s * s) : 1;
+    if (!(i > 0 && i < n && j > 0 && j < n && (gdim == 2 || (k > 0 && k < n)))) continue;
+    for (int d = 0; d < gdim; ++d) coords[v * gdim + d] += (2.0 * orc_sm64_u(&st) - 1.0) * amp * h;
+  }
+  return ORC_OK;
+}
+
+int orc_permute_cells(int ncells, int arity, uint64_t seed, int32_t* cv) {
+  if (ncells < 0 || arity < 1) return ORC_ERR_INVALID_ARGUMENT;
+  uint64_t st = seed;
+  for (int64_t i = (int64_t)ncells - 1; i >= 1; --i) {
+    const int64_t j = (int64_t)(orc_sm64(&st) % (uint64_t)(i + 1));
+    if (j == i) continue;
+    for (int a = 0; a < arity; ++a) {
+      const int32_t tmp = cv[i * arity + a];
+      cv[i * arity + a] = cv[j * arity + a];
+      cv[j * arity + a] = tmp;
+    }
+  }
+  return ORC_OK;
+}
+
+int orc_uniform(int64_t count, uint64_t seed, double lo, double hi, double* out) {
+  uint64_t st = seed;
+  for (int64_t k = 0; k < count; ++k) out[k] = lo + (hi - lo) * orc_sm64_u(&st);
+  return ORC_OK;
+}

@@ -167,6 +167,13 @@ int orc_apply_dirichlet(int nrows, const int64_t* row_ptr, const int32_t* col_id
                         double* rhs, const int32_t* nodes, int nn, const double* node_values,
                         double constant, int32_t* fail);
 
+/* ---- seeded synthetic inputs (SURVEY 8d generator; bench --impl reference) */
+int orc_unit_square_mesh(int n, double* coords, int32_t* cv);  /* mesh.hpp:96-143 */
+int orc_unit_cube_mesh(int n, double* coords, int32_t* cv);    /* mesh.hpp:148-214 */
+int orc_jitter(int gdim, int n, double amp, uint64_t seed, double* coords);
+int orc_permute_cells(int ncells, int arity, uint64_t seed, int32_t* cv);
+int orc_uniform(int64_t count, uint64_t seed, double lo, double hi, double* out);
+
 #ifdef __cplusplus
 }
 #endif

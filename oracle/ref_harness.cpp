@@ -320,6 +320,71 @@ int ref_engine_vector(int form, int degree, int gdim, const double* params, int 
   }
 }
 
+// Timed reference ENGINE on arbitrary maps (bench per-config CPU figures):
+// the reference's build_sparsity (timed once into *sparsity_s), then `steps`
+// timed rounds of Mat::zero / Dat reset + loam::execute with `threads`
+// workers and the restated host kernel (kernel.hpp:523-529).  col_map NULL =
+// a residual: Dat INC through row_map, coefficient `coeff` READ through it.
+int ref_time_engine(int form, int degree, int gdim, const double* params, int ncells, const int32_t* row_map,
+                    int ar_r, int nrt, const int32_t* col_map, int ar_c, int nct, const int32_t* coord_map,
+                    int nv, const double* coords, const double* coeff, int threads, int warmup, int steps,
+                    double* times, double* sparsity_s) {
+  try {
+    auto cells = make_set(ncells, "cells");
+    auto rt = make_set(nrt, "rows");
+    auto verts = make_set(nv, "vertices");
+    auto rm = make_map(cells, rt, ar_r, std::vector<int>(row_map, row_map + static_cast<size_t>(ncells) * ar_r));
+    auto xm = make_map(cells, verts, gdim + 1,
+                       std::vector<int>(coord_map, coord_map + static_cast<size_t>(ncells) * (gdim + 1)));
+    auto X = make_dat(verts, gdim, "coordinates");
+    std::memcpy(X->mutable_view().data(), coords, sizeof(double) * static_cast<size_t>(nv) * gdim);
+    std::vector<double> p(params, params + 4);
+    MatPtr mat;
+    DatPtr vec, u;
+    Parloop loop;
+    *sparsity_s = 0.0;
+    if (col_map) {
+      auto ct = nct == nrt && col_map == row_map ? rt : make_set(nct, "cols");
+      auto cm = col_map == row_map
+                    ? rm
+                    : make_map(cells, ct, ar_c, std::vector<int>(col_map, col_map + static_cast<size_t>(ncells) * ar_c));
+      const double t0 = now();
+      auto sp = build_sparsity(rm, cm);
+      *sparsity_s = now() - t0;
+      mat = make_mat(sp, "assembled");
+      auto kernel = ir::make_host_kernel(
+          "host_form_" + std::to_string(form), {{"A", {ar_r, ar_c}}, {"X", {gdim + 1, gdim}}},
+          [=](Real* const* a) { orc_element(form, degree, gdim, p.data(), a[1], nullptr, a[0]); });
+      loop = Parloop{kernel, cells, {arg(mat, Access::INC, rm, cm), arg(X, Access::READ, xm)}};
+    } else {
+      vec = make_dat(rt, 1, "assembled");
+      u = make_dat(rt, 1, "u");
+      std::memcpy(u->mutable_view().data(), coeff, sizeof(double) * static_cast<size_t>(nrt));
+      auto kernel = ir::make_host_kernel(
+          "host_form_" + std::to_string(form), {{"A", {ar_r}}, {"X", {gdim + 1, gdim}}, {"C", {ar_r}}},
+          [=](Real* const* a) { orc_element(form, degree, gdim, p.data(), a[1], a[2], a[0]); });
+      loop = Parloop{kernel, cells, {arg(vec, Access::INC, rm), arg(X, Access::READ, xm), arg(u, Access::READ, rm)}};
+    }
+    auto run = [&]() {
+      if (mat) mat->zero();
+      if (vec) {
+        auto w = vec->mutable_view();
+        std::fill(w.begin(), w.end(), 0.0);
+      }
+      execute(loop, threads);
+    };
+    for (int i = 0; i < warmup; ++i) run();
+    for (int i = 0; i < steps; ++i) {
+      const double t0 = now();
+      run();
+      times[i] = now() - t0;
+    }
+    return 0;
+  } catch (const Error& e) {
+    return fail_code(e);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Timing entry for bench.py (--impl reference and the cpu_baseline leg).
 // Builds the reference objects once, runs `warmup` untimed executes, then

@@ -54,7 +54,7 @@ class MapDesc(C.Structure):
         ("values", C.c_void_p), ("source_size", C.c_int32), ("target_size", C.c_int32),
         ("arity", C.c_int32), ("source_id", C.c_uint64), ("target_id", C.c_uint64),
         ("id", C.c_uint64), ("expand_dim", C.c_int32), ("node_values", C.c_void_p),
-        ("node_arity", C.c_int32), ("node_target_size", C.c_int32),
+        ("node_arity", C.c_int32), ("node_target_size", C.c_int32), ("node_id", C.c_uint64),
     ]
 
 
@@ -62,7 +62,8 @@ class SparsityDesc(C.Structure):
     _fields_ = [
         ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("nrows", C.c_int32),
         ("ncols", C.c_int32), ("nnz", C.c_int64), ("row_dim", C.c_int32), ("col_dim", C.c_int32),
-        ("id", C.c_uint64),
+        ("id", C.c_uint64), ("pattern_row_map", C.c_uint64), ("pattern_col_map", C.c_uint64),
+        ("pattern_row_dim", C.c_int32), ("pattern_col_dim", C.c_int32),
     ]
 
 
@@ -117,6 +118,8 @@ def lib() -> C.CDLL:
             "loam_gpu_set_option": (C.c_int, [C.c_int, C.c_int]),
             "loam_gpu_get_option": (C.c_int, [C.c_int]),
             "loam_gpu_plan_cache_clear": (C.c_int, []),
+            "loam_gpu_new_id": (u64, []),
+            "loam_gpu_release_id": (C.c_int, [u64]),
             "loam_gpu_launch_count": (i64, []),
             "loam_gpu_kernel_signature": (C.c_int, [C.c_char_p, ip, C.c_int]),
             "loam_gpu_kernel_names": (C.c_char_p, []),
@@ -175,7 +178,8 @@ def lib() -> C.CDLL:
 # Every symbol include/loam_gpu.h declares (checked by tests/test_capi_cpu.py).
 EXPORTED = [
     "loam_gpu_last_error", "loam_gpu_version", "loam_gpu_device_ok", "loam_gpu_set_option",
-    "loam_gpu_get_option", "loam_gpu_plan_cache_clear", "loam_gpu_launch_count",
+    "loam_gpu_get_option", "loam_gpu_plan_cache_clear", "loam_gpu_new_id", "loam_gpu_release_id",
+    "loam_gpu_launch_count",
     "loam_gpu_kernel_signature", "loam_gpu_kernel_names", "loam_gpu_validate", "loam_gpu_execute",
     "loam_gpu_execute_host", "loam_gpu_execute_host_batch", "loam_gpu_map_check", "loam_gpu_build_sparsity",
     "loam_gpu_color_iteration", "loam_gpu_malloc", "loam_gpu_free", "loam_gpu_host_alloc",
@@ -189,6 +193,18 @@ EXPORTED = [
     "loam_gpu_reduce_dev", "loam_gpu_bc_apply_dev", "loam_gpu_wave_clock",
     "loam_gpu_rcm_order", "loam_gpu_vertex_adjacency", "loam_gpu_renumber_vertices", "loam_gpu_wave_step",
 ]
+
+
+def new_id() -> int:
+    """A process-unique object identity (shared with every other client of the library)."""
+    return int(lib().loam_gpu_new_id())
+
+
+def release_id(obj_id: int) -> None:
+    """Evict the plans / resident copies keyed by obj_id (object destroyed)."""
+    global _lib
+    if _lib is not None:
+        _lib.loam_gpu_release_id(obj_id)
 
 
 def check(code: int) -> None:

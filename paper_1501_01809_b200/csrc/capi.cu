@@ -4,6 +4,7 @@
 // with a thread-local message; CUDA failures -> LOAM_GPU_ERR_CUDA.  No CPU
 // fallback: compute entry points fail with LOAM_GPU_ERR_NO_DEVICE when no
 // sm_100 device is usable.
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <cstring>
@@ -101,6 +102,21 @@ void* resident_copy(int kind, uint64_t id, const void* host, size_t bytes, cudaS
   return r.dev;
 }
 
+void resident_release(uint64_t id) {
+  std::lock_guard<std::mutex> g(g_res_mutex);
+  for (auto it = g_resident.begin(); it != g_resident.end();) {
+    if (it->first.second == id) {
+      if (it->second.dev) {
+        cudaDeviceSynchronize(); // a queued call may still read it
+        cudaFree(it->second.dev);
+      }
+      it = g_resident.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
 void resident_clear() {
   std::lock_guard<std::mutex> g(g_res_mutex);
   for (auto& [k, r] : g_resident)
@@ -143,6 +159,19 @@ int loam_gpu_plan_cache_clear(void) {
   return guarded([] {
     plan_cache_clear();
     resident_clear();
+  });
+}
+
+uint64_t loam_gpu_new_id(void) {
+  static std::atomic<uint64_t> next{1};
+  return next++;
+}
+
+int loam_gpu_release_id(uint64_t id) {
+  if (id == 0) return 0;
+  return guarded([&] {
+    plan_cache_release(id);
+    resident_release(id);
   });
 }
 

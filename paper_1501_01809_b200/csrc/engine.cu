@@ -2209,14 +2209,126 @@ NodeMap node_view(const loam_map_desc* m) {
   if (m->expand_dim > 1 && m->node_values) {
     r.v = MapView{m->node_values, m->source_size, m->node_arity, m->node_target_size};
     r.dim = m->expand_dim;
+    r.id = m->node_id; // the node map's identity (0 = unknown)
   } else {
     r.v = MapView{m->values, m->source_size, m->arity, m->target_size};
   }
   return r;
 }
 
+// A Mat argument whose (row, col) maps are, at node level, the maps its
+// sparsity was built from (loam_sparsity_desc provenance) has exactly that
+// pattern: every entry is reached by some cell of the loop.
+bool pattern_provenance_exact(const loam_arg_desc& a) {
+  if (a.kind != LOAM_ARG_MAT || !a.sparsity || !a.map || !a.col_map) return false;
+  const loam_sparsity_desc* sp = a.sparsity;
+  if (!sp->pattern_row_map || !sp->pattern_col_map) return false;
+  const NodeMap R = node_view(a.map), C = node_view(a.col_map);
+  return R.id == sp->pattern_row_map && C.id == sp->pattern_col_map && R.dim == sp->pattern_row_dim &&
+         C.dim == sp->pattern_col_dim;
+}
+
+// Tile counters of the persistent tile kernels, one pair per launch in
+// flight.  A kernel takes tiles from counter [0] and the last CTA puts [0] and
+// the exit count [1] back to zero (stage.cuh:tile_counter_release), so a pair
+// may be reused by the next launch that is ORDERED after it: a launch on the
+// same stream, or any launch once the recorded event of the previous user has
+// completed.  Two launches of one cached plan that may overlap (two streams, a
+// graph replay beside a direct execute) therefore never share a pair.  A launch
+// captured into a CUDA graph keeps its pair for good (its pointer is frozen in
+// the graph; replays of one graph are ordered among themselves).
+struct TileCounters {
+  static constexpr int kSlots = 32;
+  struct Slot {
+    cudaEvent_t done = nullptr;
+    cudaStream_t stream = nullptr;
+    int state = 0; // 0 unused, 1 direct launches, 2 owned by a captured graph
+  };
+  DevBuf<int> mem;
+  Slot slot[kSlots];
+  std::mutex mu;
+
+  void init(cudaStream_t s) {
+    mem.alloc(2 * kSlots, s);
+    LG_CUDA(cudaMemsetAsync(mem.get(), 0, mem.bytes(), s));
+  }
+  ~TileCounters() {
+    for (Slot& q : slot)
+      if (q.done) cudaEventDestroy(q.done);
+  }
+  // index of a pair this launch may use on stream s
+  int acquire(cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    LG_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone) {
+      for (int i = 0; i < kSlots; ++i)
+        if (slot[i].state == 0) {
+          slot[i].state = 2;
+          return i;
+        }
+      fail(LOAM_ERR(InvalidArgument), "more than 32 CUDA-graph captures of one par_loop plan");
+    }
+    for (int i = 0; i < kSlots; ++i) {
+      Slot& q = slot[i];
+      if (q.state == 0 || (q.state == 1 && (q.stream == s || cudaEventQuery(q.done) == cudaSuccess))) return i;
+    }
+    // every pair is in flight on other streams: order after the first one
+    for (int i = 0; i < kSlots; ++i)
+      if (slot[i].state == 1) {
+        LG_CUDA(cudaStreamWaitEvent(s, slot[i].done, 0));
+        return i;
+      }
+    fail(LOAM_ERR(InvalidArgument), "no tile counter available");
+    return -1;
+  }
+  // after the launch that used pair i (no-op for captured pairs)
+  void commit(int i, cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu);
+    Slot& q = slot[i];
+    if (q.state == 2) return;
+    if (!q.done) LG_CUDA(cudaEventCreateWithFlags(&q.done, cudaEventDisableTiming));
+    LG_CUDA(cudaEventRecord(q.done, s));
+    q.stream = s;
+    q.state = 1;
+  }
+  int* next(int i) const { return mem.get() + 2 * i; }
+  int* exits(int i) const { return mem.get() + 2 * i + 1; }
+};
+
+__global__ void k_mark_nodes(const int32_t* __restrict__ m, int64_t len, uint8_t* __restrict__ mark) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+    mark[m[i]] = 1;
+}
+__global__ void k_count_unmarked(const uint8_t* __restrict__ mark, int n, int* __restrict__ cnt) {
+  int c = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) c += mark[i] == 0;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
+// Does every target node appear in the map?  (A Dat INC through it then
+// reaches every entry of the Dat.)
+bool map_covers_target(const MapView& m, cudaStream_t s) {
+  if (m.target == 0) return true;
+  DevBuf<uint8_t> mark((size_t)m.target, s);
+  DevBuf<int> cnt(1, s);
+  LG_CUDA(cudaMemsetAsync(mark.get(), 0, (size_t)m.target, s));
+  LG_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int), s));
+  const int64_t len = (int64_t)m.n * m.arity;
+  if (len) k_mark_nodes<<<kNumSMs * 4, 256, 0, s>>>(m.v, len, mark.get());
+  k_count_unmarked<<<kNumSMs * 4, 256, 0, s>>>(mark.get(), m.target, cnt.get());
+  count_launch(len ? 2 : 1);
+  LG_LAUNCH_CHECK();
+  int h = 0;
+  LG_CUDA(cudaMemcpyAsync(&h, cnt.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  return h == 0;
+}
+
 struct FastPlan {
-  DevBuf<int> counter; // dynamic tile scheduler: [0] next tile, [1] exit count (stage.cuh:tile_counter_release)
+  TileCounters counter; // dynamic tile scheduler of the persistent tile kernels
+  bool exact = false;   // the loop's (row, col) pattern IS the Mat's pattern (provenance / checked)
 
   bool use_nbr = false;
   NbrPlan nb;
@@ -2327,8 +2439,10 @@ bool try_build_patch(const Entry& k, int n, const loam_arg_desc* args, FastPlan&
     const NodeMap Cn = node_view(args[0].col_map);
     if (Cn.dim != k.cd || R.dim != k.rd || !same_as_rows(Cn.v)) return false;
     sp = args[0].sparsity;
-    if (!pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, R.dim, Cn.dim, sp->row_ptr, sp->col_idx, sp->nnz, s))
+    if (!P.exact &&
+        !pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, R.dim, Cn.dim, sp->row_ptr, sp->col_idx, sp->nnz, s))
       return false;
+    P.exact = true;
   }
   PatchSpec spec;
   spec.gd = k.gd;
@@ -2396,8 +2510,8 @@ void build_cell_segments(const int32_t* sorted_rows, int n, int arity, FastPlan&
 std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_desc* args, bool cell_mode,
                                           cudaStream_t s) {
   auto P = std::make_shared<FastPlan>();
-  P->counter.alloc(4, s);
-  LG_CUDA(cudaMemsetAsync(P->counter.get(), 0, 4 * sizeof(int), s));
+  P->counter.init(s);
+  P->exact = k.bilinear ? pattern_provenance_exact(args[0]) : map_covers_target(node_view(args[0].map).v, s);
   if (!cell_mode && patch_wanted(k) && try_build_patch(k, n, args, *P, s)) {
     P->use_patch = true;
     return P;
@@ -2494,9 +2608,11 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     // pattern must be exactly that one (not a superset)
     const bool star_ok = ok && k.star && strat == 0 && !std::getenv("LOAM_GPU_NO_STAR") &&
                          (!k.bilinear || std::getenv("LOAM_GPU_STAR_MAT")) &&
-                         (!k.bilinear || pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, 1, 1, csr.row_ptr,
-                                                                csr.col_idx, csr.nnz, s));
+                         (!k.bilinear || P->exact ||
+                          pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, 1, 1, csr.row_ptr, csr.col_idx,
+                                                 csr.nnz, s));
     if (star_ok && build_stars(R.v.v, n, R.v.target, P->star, s)) {
+      if (k.bilinear) P->exact = true;
       P->use_star = true;
       return P;
     }
@@ -2527,7 +2643,9 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
         R.dim == k.rd && Cn.dim == k.cd &&
         (reinterpret_cast<uintptr_t>(args[1].data) & 15) == 0 && Cn.v.arity == R.v.arity &&
         (Cn.v.v == R.v.v || prefix_equal(Cn.v.v, Cn.v.arity, R.v.v, R.v.arity, R.v.arity, n, s)) &&
-        pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, k.rd, k.cd, sp->row_ptr, sp->col_idx, sp->nnz, s)) {
+        (P->exact ||
+         pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, k.rd, k.cd, sp->row_ptr, sp->col_idx, sp->nnz, s))) {
+      P->exact = true;
       SortedMap sx;
       gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, sx, s);
       EtileSpec es;
@@ -2698,6 +2816,18 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     *g_plan_probe = P;
     return;
   }
+  // A fresh output the loop may not reach entirely (a sub-mesh loop into a
+  // whole-mesh Mat or Dat): zero it here and let the owner-computes kernels
+  // accumulate, so untouched entries stay zero as in the reference
+  // (data.hpp:37-39,185-187).  The cell-centric path zero-fills on its own.
+  std::vector<loam_arg_desc> local;
+  if ((args[0].flags & LOAM_ARG_ZERO) && !P->exact && !P->use_cell) {
+    const size_t len = k.bilinear ? (size_t)args[0].sparsity->nnz : (size_t)args[0].set_size * args[0].dim;
+    LG_CUDA(cudaMemsetAsync(args[0].data, 0, sizeof(double) * len, s));
+    local.assign(args, args + nargs);
+    local[0].flags &= ~LOAM_ARG_ZERO;
+    args = local.data();
+  }
   if (P->use_star) {
     StarArgs t{};
     t.star = P->star.get();
@@ -2775,8 +2905,9 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     RingArgs t{};
     t.tiles = nb.rtiles.get();
     t.ntiles = nb.ntiles;
-    t.next_tile = P->counter.get();      // tile counter
-    t.reset_tile = P->counter.get() + 1; // exit count (tile_counter_release)
+    const int ctr = P->counter.acquire(s);
+    t.next_tile = P->counter.next(ctr);   // tile counter
+    t.reset_tile = P->counter.exits(ctr); // exit count (tile_counter_release)
     t.nptr = nb.nptr.get();
     t.rptr = nb.rptr.get();
     t.recs = nb.rrecs.get();
@@ -2818,6 +2949,7 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
       t.timing = tbuf.get();
     }
     k.ring(t, (size_t)off, s);
+    P->counter.commit(ctr, s);
     if (timing) {
       std::vector<unsigned long long> hv(16 + 4 * 2048 + 2 * 16384);
       unsigned long long* h = hv.data();
@@ -2844,18 +2976,24 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     return;
   }
   if (P->use_rtile) {
+    const int ctr = P->counter.acquire(s);
     launch_rtile(P->rt, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
-                 P->counter.get(), P->counter.get() + 1, s);
+                 P->counter.next(ctr), P->counter.exits(ctr), s);
+    P->counter.commit(ctr, s);
     return;
   }
   if (P->use_ntile) {
+    const int ctr = P->counter.acquire(s);
     launch_ntile(P->nt, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
-                 P->counter.get(), P->counter.get() + 1, s);
+                 P->counter.next(ctr), P->counter.exits(ctr), s);
+    P->counter.commit(ctr, s);
     return;
   }
   if (P->use_etile) {
+    const int ctr = P->counter.acquire(s);
     launch_etile(k.form, P->et, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
-                 P->counter.get(), P->counter.get() + 1, s);
+                 P->counter.next(ctr), P->counter.exits(ctr), s);
+    P->counter.commit(ctr, s);
     return;
   }
   if (P->use_ptile) {
@@ -2863,8 +3001,9 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     PTileArgs t{};
     t.tiles = pt.tiles.get();
     t.ntiles = pt.ntiles;
-    t.next_tile = P->counter.get();      // tile counter
-    t.reset_tile = P->counter.get() + 1; // exit count (tile_counter_release)
+    const int ctr = P->counter.acquire(s);
+    t.next_tile = P->counter.next(ctr);   // tile counter
+    t.reset_tile = P->counter.exits(ctr); // exit count (tile_counter_release)
     t.pptr = pt.pptr.get();
     t.nptr = pt.nptr.get();
     t.recs = pt.recs.get();
@@ -2894,6 +3033,7 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     b += up16(k.has_coeff ? pt.max_cslots * 8 + 16 : 0);
     t.buf_bytes = b;
     k.ptile(t, (size_t)off, (size_t)b, s);
+    P->counter.commit(ctr, s);
     return;
   }
   if (P->use_nbr) {
@@ -3211,6 +3351,38 @@ void plan_cache_clear() {
   std::lock_guard<std::mutex> g(g_cache_mutex);
   g_fast_cache.clear();
   g_color_cache.clear();
+}
+
+void plan_cache_release(uint64_t id) {
+  // key layouts: fast plans = 7 shape words, then object ids; colourings =
+  // {iteration set id, n, map ids...}
+  auto holds = [id](const std::vector<uint64_t>& k, size_t from, size_t skip) {
+    for (size_t i = from; i < k.size(); ++i)
+      if (i != skip && k[i] == id) return true;
+    return false;
+  };
+  std::vector<std::shared_ptr<FastPlan>> dead_fast;
+  std::vector<std::shared_ptr<ColorCacheEntry>> dead_color;
+  {
+    std::lock_guard<std::mutex> g(g_cache_mutex);
+    for (auto it = g_fast_cache.begin(); it != g_fast_cache.end();) {
+      if (holds(it->first, 7, (size_t)-1)) {
+        dead_fast.push_back(std::move(it->second));
+        it = g_fast_cache.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    for (auto it = g_color_cache.begin(); it != g_color_cache.end();) {
+      if (holds(it->first, 0, 1)) {
+        dead_color.push_back(std::move(it->second));
+        it = g_color_cache.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  if (!dead_fast.empty() || !dead_color.empty()) LG_CUDA(cudaDeviceSynchronize()); // queued launches may use them
 }
 
 namespace {

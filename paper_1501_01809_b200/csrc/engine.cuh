@@ -27,6 +27,8 @@ void validate(const loam_kernel_desc* k, int n, uint64_t iter_id, const loam_arg
 void execute(const loam_kernel_desc* k, int n, uint64_t iter_id, const loam_arg_desc* args,
              int nargs, cudaStream_t s);
 void plan_cache_clear();
+// evict every cached plan keyed by an object id (Map / Sparsity destroyed)
+void plan_cache_release(uint64_t id);
 // bench::run_wave's step (bench.hpp:267-289) fused into the vertex-star
 // stiffness action of `args` (b INC, X READ, phi READ; engine.cu k_wave_step).
 void wave_step(const loam_kernel_desc* k, int n, uint64_t iter_id, const loam_arg_desc* args, int nargs,

@@ -60,10 +60,9 @@ inline void require(bool c, ErrorKind k, const std::string& m) {
 }
 
 namespace detail {
-inline uint64_t next_id() {
-  static std::atomic<uint64_t> id{1};
-  return id++;
-}
+// Identities come from the library so they are unique across every client
+// of it in the process (plans and resident copies are cached by id).
+inline uint64_t next_id() { return loam_gpu_new_id(); }
 template <class T>
 struct DeviceArray { // owned device buffer + lazily synchronised host mirror
   T* dev = nullptr;
@@ -135,6 +134,10 @@ public:
   const SetPtr& target() const { return target_; }
   int arity() const { return arity_; }
   const std::string& name() const { return name_; }
+  ~Map() { loam_gpu_release_id(id_); } // evict the plans cached for this map
+  uint64_t id() const { return id_; }
+  Map(const Map&) = delete;
+  Map& operator=(const Map&) = delete;
   const int* row(int e) const { return values_.data() + static_cast<long>(e) * arity_; }
   const std::vector<int>& values() const { return values_; }
   loam_map_desc desc() const {
@@ -261,9 +264,12 @@ inline GlobalPtr make_global(int dim, std::string name = "global") { return std:
 
 class Sparsity { // data.hpp:116-142 (device CSR)
 public:
-  Sparsity(int nrows, int ncols, int64_t* row_ptr, int32_t* col_idx, int64_t nnz, int rd, int cd)
-      : nrows_(nrows), ncols_(ncols), rp_(row_ptr), ci_(col_idx), nnz_(nnz), rd_(rd), cd_(cd) {}
+  Sparsity(int nrows, int ncols, int64_t* row_ptr, int32_t* col_idx, int64_t nnz, int rd, int cd,
+           uint64_t row_map_id = 0, uint64_t col_map_id = 0)
+      : nrows_(nrows), ncols_(ncols), rp_(row_ptr), ci_(col_idx), nnz_(nnz), rd_(rd), cd_(cd),
+        row_map_id_(row_map_id), col_map_id_(col_map_id) {}
   ~Sparsity() {
+    loam_gpu_release_id(id_);
     loam_gpu_free(rp_);
     loam_gpu_free(ci_);
   }
@@ -288,7 +294,8 @@ public:
     return (it == last || *it != col) ? -1 : it - hci_.begin();
   }
   loam_sparsity_desc desc() const {
-    return loam_sparsity_desc{rp_, ci_, nrows_, ncols_, nnz_, rd_, cd_, id_};
+    // provenance: the maps build_sparsity was given (loam_gpu.h)
+    return loam_sparsity_desc{rp_, ci_, nrows_, ncols_, nnz_, rd_, cd_, id_, row_map_id_, col_map_id_, rd_, cd_};
   }
 
 private:
@@ -307,6 +314,7 @@ private:
   int32_t* ci_;
   int64_t nnz_;
   int rd_, cd_;
+  uint64_t row_map_id_, col_map_id_;
   uint64_t id_ = detail::next_id();
   mutable bool synced_ = false;
   mutable std::vector<long> hrp_;
@@ -324,7 +332,7 @@ inline SparsityPtr build_sparsity(const MapPtr& row_map, const MapPtr& col_map, 
   int64_t nnz = 0;
   check(loam_gpu_build_sparsity(&r, &c, row_dim, col_dim, &rp, &ci, &nnz, nullptr));
   return std::make_shared<const Sparsity>(row_map->target()->size() * row_dim, col_map->target()->size() * col_dim, rp,
-                                          ci, nnz, row_dim, col_dim);
+                                          ci, nnz, row_dim, col_dim, row_map->id(), col_map->id());
 }
 
 class Mat { // data.hpp:183-228

@@ -11,7 +11,6 @@ Errors raise capi.LoamError whose `.kind` is the reference ErrorKind name.
 from __future__ import annotations
 
 import ctypes as C
-import itertools
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -21,7 +20,15 @@ import torch
 from . import capi
 from .capi import INC, MAX, MIN, READ, RW, SUM, WRITE, LoamError
 
-_ids = itertools.count(1)
+class _Ids:
+    """Object identities come from the library (loam_gpu_new_id), unique across
+    every client in the process (C++ facade, FFI bindings, this mirror)."""
+
+    def __next__(self) -> int:
+        return capi.new_id()
+
+
+_ids = _Ids()
 
 
 def _fail(kind: str, msg: str):
@@ -92,6 +99,15 @@ class Map:
     def row(self, e: int) -> np.ndarray:
         return self.values[e * self.arity:(e + 1) * self.arity]
 
+    def node_level(self, dim: int = 1):
+        """(identity, dof dim) at node level: a dof-expanded map stands for its node map."""
+        if self.node_map is not None and self.expand_dim > 1:
+            return self.node_map.id, dim * self.expand_dim
+        return self.id, dim
+
+    def __del__(self):
+        capi.release_id(getattr(self, "id", 0))
+
     def desc(self) -> capi.MapDesc:
         if self._desc is None:
             d = capi.MapDesc()
@@ -103,6 +119,7 @@ class Map:
                 d.node_values = self.node_map.dev.data_ptr()
                 d.node_arity = self.node_map.arity
                 d.node_target_size = self.node_map.target.size
+                d.node_id = self.node_map.id
             self._desc = d
         return self._desc
 
@@ -206,10 +223,12 @@ class Sparsity:
     """data.hpp:116-142: CSR with int64 row offsets and int32 columns (device)."""
 
     def __init__(self, nrows: int, ncols: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
-                 row_dim: int = 1, col_dim: int = 1):
+                 row_dim: int = 1, col_dim: int = 1, built_from=None):
         self.nrows, self.ncols = int(nrows), int(ncols)
         self.row_ptr, self.col_idx = row_ptr, col_idx
         self.row_dim, self.col_dim = row_dim, col_dim
+        # node-level (row map id, row dim, col map id, col dim) it was built from
+        self.built_from = built_from
         self.id = next(_ids)
         self._host = None
         self._desc = None
@@ -238,8 +257,13 @@ class Sparsity:
             d.row_ptr, d.col_idx = self.row_ptr.data_ptr(), self.col_idx.data_ptr()
             d.nrows, d.ncols, d.nnz = self.nrows, self.ncols, self.nnz
             d.row_dim, d.col_dim, d.id = self.row_dim, self.col_dim, self.id
+            if self.built_from is not None:
+                d.pattern_row_map, d.pattern_row_dim, d.pattern_col_map, d.pattern_col_dim = self.built_from
             self._desc = d
         return self._desc
+
+    def __del__(self):
+        capi.release_id(getattr(self, "id", 0))
 
 
 def build_sparsity(row_map: Map, col_map: Map, row_dim: int = 1, col_dim: int = 1) -> Sparsity:
@@ -258,7 +282,8 @@ def build_sparsity(row_map: Map, col_map: Map, row_dim: int = 1, col_dim: int = 
     finally:
         capi.lib().loam_gpu_free(rp)
         capi.lib().loam_gpu_free(ci)
-    return Sparsity(nrows, ncols, row_ptr, col_idx, row_dim, col_dim)
+    return Sparsity(nrows, ncols, row_ptr, col_idx, row_dim, col_dim,
+                    built_from=(*row_map.node_level(row_dim), *col_map.node_level(col_dim)))
 
 
 class Mat:

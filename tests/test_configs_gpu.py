@@ -167,3 +167,45 @@ def test_ring_and_general_paths_agree():
     finally:
         del os.environ["LOAM_GPU_NO_RING"]
     assert rel(a, b) <= TOL
+
+
+needs_ref = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+
+
+def dof_map(nodes, arity, dim):
+    v = np.asarray(nodes, np.int64).reshape(-1, arity)
+    return (v[:, :, None] * dim + np.arange(dim)).reshape(-1).astype(np.int32)
+
+
+@needs_ref
+@pytest.mark.parametrize("strat", ["auto", "owner", "atomic"])
+def test_c4_elasticity_equals_compiled_reference_engine(strat):
+    """The device Mat against the compiled reference's own build_sparsity +
+    execute + Mat::addto (restated host kernel, kernel.hpp:523-529), n=8."""
+    w = run_cfg(4, 8, strat)
+    m = w.inputs
+    dm = dof_map(m.cv, 4, 3)
+    rp, ci, rv = O.ref_engine_matrix(O.ELASTICITY, 1, 3, m.ncells, dm, 12, 3 * m.nv, dm, 12, 3 * m.nv, m.cv,
+                                     m.coords, params=configs.LAME)
+    grp, gci = w.outputs[0].sparsity.host()
+    assert np.array_equal(grp, rp) and np.array_equal(gci, ci)
+    assert rel(w.outputs[0].host_values(), rv) <= TOL
+
+
+@needs_ref
+@pytest.mark.parametrize("strat", ["auto", "owner", "atomic"])
+def test_c5_blocks_equal_compiled_reference_engine(strat):
+    w = run_cfg(5, 8, strat)
+    m = w.inputs
+    cn, nn = m.extra["p2"], m.extra["nn"]
+    vd = dof_map(cn, 6, 2)
+    A, BT, B = w.outputs
+    for M, form, rmap, ar_r, nrt, cmap, ar_c, nct, prm in (
+            (A, O.STOKES_A, vd, 12, 2 * nn, vd, 12, 2 * nn, (configs.NU,)),
+            (B, O.STOKES_B, m.cv, 3, m.nv, vd, 12, 2 * nn, ()),
+            (BT, O.STOKES_BT, vd, 12, 2 * nn, m.cv, 3, m.nv, ())):
+        rp, ci, rv = O.ref_engine_matrix(form, 2, 2, m.ncells, rmap, ar_r, nrt, cmap, ar_c, nct, m.cv, m.coords,
+                                         params=prm)
+        grp, gci = M.sparsity.host()
+        assert np.array_equal(grp, rp) and np.array_equal(gci, ci), M.name
+        assert rel(M.host_values(), rv) <= TOL, M.name

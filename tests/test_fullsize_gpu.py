@@ -1,10 +1,11 @@
 """BASELINE full sizes (configs C1-C5 exactly as bench.py runs them, `auto`
-path): parity where the oracle finishes in seconds, size-independent
-properties of the assembled operators everywhere else.
+path): every output against the C restatement at full size -- sparsity
+row_ptr / col_idx bit-exact against orc_build_sparsity (data.hpp:149-179),
+values within relative max norm 1e-12 (north_star tolerance) of
+orc_assemble_matrix / orc_assemble_vector (the reference's par_loop + addto,
+data.hpp:205-222) -- plus size-independent properties of the assembled
+operators (which would also catch an error shared by kernel and oracle):
 
-* C1 512^2 residual, C2 1024^2 CSR (sparsity bit-exact) and the C3 64^3
-  P2 residual: against the C restatement at full size, relative max norm
-  1e-12 (north_star tolerance).
 * C3 matrix (60.9 M nnz): A u = b(u) -- the matrix (edge tiles) and the
   residual (cell kernel) are the same bilinear form through two unrelated
   kernels, and b(u) is itself checked against the oracle above; A = A^T;
@@ -90,6 +91,21 @@ def test_c2_full_csr_equals_oracle():
     assert symmetric(K) <= TOL
 
 
+def oracle_csr(mat, ncells, rmap, ar_r, nrt, cmap, ar_c, nct, rd, cd):
+    """row_ptr / col_idx of the Mat, checked bit-exact against the restatement."""
+    rp, ci = mat.sparsity.host()
+    orp, oci = O.build_sparsity(ncells, rmap, ar_r, nrt, cmap, ar_c, nct, rd, cd)
+    assert np.array_equal(rp, orp), "row_ptr differs from orc_build_sparsity"
+    assert np.array_equal(ci, oci), "col_idx differs from orc_build_sparsity"
+    del orp, oci
+    return rp, ci
+
+
+def dof_map(nodes, arity, dim):
+    v = np.asarray(nodes, np.int64).reshape(-1, arity)
+    return (v[:, :, None] * dim + np.arange(dim)).reshape(-1).astype(np.int32)
+
+
 def test_c3_full_residual_equals_oracle_and_matrix_action():
     w = run(3)
     m = w.inputs
@@ -99,6 +115,12 @@ def test_c3_full_residual_equals_oracle_and_matrix_action():
     ref = O.assemble_vector(O.HELMHOLTZ_ACTION, 2, 3, m.ncells, cn, 10, m.cv, m.coords, cn, 10,
                             m.extra["u"], nn, params=(configs.KAPPA,))
     assert rel(b, ref) <= TOL
+    # the matrix value for value: sparsity bit-exact, values 1e-12
+    rp, ci = oracle_csr(w.outputs[1], m.ncells, cn, 10, nn, cn, 10, nn, 1, 1)
+    refA = O.assemble_matrix(O.HELMHOLTZ, 2, 3, m.ncells, cn, 10, cn, 10, m.cv, m.coords, rp, ci,
+                             params=(configs.KAPPA,))
+    assert rel(w.outputs[1].host_values(), refA) <= TOL
+    del refA
     A = csr(w.outputs[1], nn)
     assert A.nnz == 60859905
     assert small_against(A, m.extra["u"], b) <= TOL  # A u = b(u): two kernels, one form
@@ -115,10 +137,16 @@ def rigid_modes(X):
     return [np.stack(f, axis=1).ravel() for f in fields]  # dof = 3 * vertex + component
 
 
-def test_c4_full_elasticity_annihilates_rigid_motions():
+def test_c4_full_elasticity_equals_oracle_and_annihilates_rigid_motions():
     w = run(4)
     m = w.inputs
     assert m.ncells == 5308416
+    rp, ci = oracle_csr(w.outputs[0], m.ncells, m.cv, 4, m.nv, m.cv, 4, m.nv, 3, 3)
+    dm = dof_map(m.cv, 4, 3)
+    ref = O.assemble_matrix(O.ELASTICITY, 1, 3, m.ncells, dm, 12, dm, 12, m.cv, m.coords, rp, ci,
+                            params=configs.LAME)
+    assert rel(w.outputs[0].host_values(), ref) <= TOL
+    del ref, dm
     A = csr(w.outputs[0], 3 * m.nv)
     assert A.nnz == 121188969
     X = m.coords.reshape(-1, 3)
@@ -140,12 +168,22 @@ def p2_node_coords(m):
     return P
 
 
-def test_c5_full_blocks_properties():
+def test_c5_full_blocks_equal_oracle_and_properties():
     w = run(5)
     m = w.inputs
     nn = m.extra["nn"]
     assert m.ncells == 1179648 and nn == 2362369
     Am, BTm, Bm = w.outputs
+    cn = m.extra["p2"]
+    vd = dof_map(cn, 6, 2)
+    for M, form, rmap, ar_r, cmap, ar_c, prm, rsp, csp in (
+            (Am, O.STOKES_A, vd, 12, vd, 12, (configs.NU,), (cn, 6, nn, 2), (cn, 6, nn, 2)),
+            (Bm, O.STOKES_B, m.cv, 3, vd, 12, (), (m.cv, 3, m.nv, 1), (cn, 6, nn, 2)),
+            (BTm, O.STOKES_BT, vd, 12, m.cv, 3, (), (cn, 6, nn, 2), (m.cv, 3, m.nv, 1))):
+        rp, ci = oracle_csr(M, m.ncells, rsp[0], rsp[1], rsp[2], csp[0], csp[1], csp[2], rsp[3], csp[3])
+        ref = O.assemble_matrix(form, 2, 2, m.ncells, rmap, ar_r, cmap, ar_c, m.cv, m.coords, rp, ci, params=prm)
+        assert rel(M.host_values(), ref) <= TOL, M.name
+        del ref
     A, B, BT = csr(Am, 2 * nn), csr(Bm, 2 * nn), csr(BTm, m.nv)
     assert (A.nnz, B.nnz, BT.nnz) == (108576772, 22428674, 22428674)
     P = p2_node_coords(m)

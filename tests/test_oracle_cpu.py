@@ -228,3 +228,81 @@ def test_reference_threads_bitwise_identical():  # test_parloop.cpp:273-315 on t
     a = O.ref_assemble_matrix(O.STIFFNESS, 1, 2, m.cv, m.coords, threads=1)[2]
     b = O.ref_assemble_matrix(O.STIFFNESS, 1, 2, m.cv, m.coords, threads=4)[2]
     assert np.array_equal(a, b)
+
+
+def _dof_map(nodes, arity, dim):
+    v = np.asarray(nodes, np.int64).reshape(-1, arity)
+    return (v[:, :, None] * dim + np.arange(dim)).reshape(-1).astype(np.int32)
+
+
+@needs_ref
+def test_reference_engine_agrees_with_restatement_on_elasticity():
+    """C4 through the compiled reference ENGINE (build_sparsity + execute + Mat::addto,
+    data.hpp:149-222, parloop.hpp:191-384) with dof-expanded maps:
+    sparsity bit-exact and values equal to the restatement's assembly."""
+    from paper_1501_01809_b200 import configs
+    m = configs.config_inputs(4, 8)
+    dm = _dof_map(m.cv, 4, 3)
+    rp, ci, rv = O.ref_engine_matrix(O.ELASTICITY, 1, 3, m.ncells, dm, 12, 3 * m.nv, dm, 12, 3 * m.nv, m.cv,
+                                     m.coords, params=configs.LAME)
+    orp, oci = O.build_sparsity(m.ncells, m.cv, 4, m.nv, m.cv, 4, m.nv, 3, 3)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    ov = O.assemble_matrix(O.ELASTICITY, 1, 3, m.ncells, dm, 12, dm, 12, m.cv, m.coords, rp, ci, params=configs.LAME)
+    assert rel(ov, rv) <= 1e-13
+
+
+@needs_ref
+def test_reference_engine_agrees_with_restatement_on_taylor_hood_blocks():
+    """C5's A, B and B^T through the compiled reference engine with separate
+    velocity (dof-expanded P2) and pressure (P1) maps."""
+    from paper_1501_01809_b200 import configs
+    m = configs.config_inputs(5, 8)
+    cn, nn = m.extra["p2"], m.extra["nn"]
+    vd = _dof_map(cn, 6, 2)
+    for form, rmap, ar_r, nrt, cmap, ar_c, nct, prm, rdim, cdim in (
+            (O.STOKES_A, vd, 12, 2 * nn, vd, 12, 2 * nn, (configs.NU,), (cn, 6, nn, 2), (cn, 6, nn, 2)),
+            (O.STOKES_B, m.cv, 3, m.nv, vd, 12, 2 * nn, (), (m.cv, 3, m.nv, 1), (cn, 6, nn, 2)),
+            (O.STOKES_BT, vd, 12, 2 * nn, m.cv, 3, m.nv, (), (cn, 6, nn, 2), (m.cv, 3, m.nv, 1))):
+        rp, ci, rv = O.ref_engine_matrix(form, 2, 2, m.ncells, rmap, ar_r, nrt, cmap, ar_c, nct, m.cv, m.coords,
+                                         params=prm)
+        orp, oci = O.build_sparsity(m.ncells, rdim[0], rdim[1], rdim[2], cdim[0], cdim[1], cdim[2], rdim[3], cdim[3])
+        assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+        ov = O.assemble_matrix(form, 2, 2, m.ncells, rmap, ar_r, cmap, ar_c, m.cv, m.coords, rp, ci, params=prm)
+        assert rel(ov, rv) <= 1e-13
+
+
+# ------------------------------------------------------------------ 6. the oracle-side input generator
+@pytest.mark.parametrize("cfg,n", [(1, 7), (2, 16), (3, 3), (4, 4), (5, 6), (2, 1024)])
+def test_oracle_generator_equals_product_generator(cfg, n):
+    """bench --impl reference builds its inputs with the restatement (no product
+    library in that process): they must be the very bits the GPU arm assembles."""
+    from paper_1501_01809_b200 import configs
+    a, b = O.inputs(cfg, n), configs.config_inputs(cfg, n)
+    assert np.array_equal(a.cv, b.cv)
+    assert np.array_equal(a.coords.view(np.uint64), b.coords.view(np.uint64))
+    for k in b.extra:
+        va, vb = np.asarray(a.extra[k]), np.asarray(b.extra[k])
+        assert np.array_equal(va.view(np.uint64) if va.dtype == np.float64 else va,
+                              vb.view(np.uint64) if vb.dtype == np.float64 else vb), k
+    assert (O.FULL, O.JITTER, O.PERM_SEED) == (configs.FULL, configs.JITTER, configs.PERM_SEED)
+
+
+@needs_ref
+@pytest.mark.parametrize("gdim,n", [(2, 5), (3, 3)])
+def test_oracle_meshes_equal_reference_generators(gdim, n):
+    coords, cv = O.ref_unit_mesh(gdim, n)
+    m = O.mesh(gdim, n)
+    assert np.array_equal(m.cv, cv) and np.array_equal(m.coords, coords)
+
+
+@needs_ref
+def test_timed_reference_engine_runs():
+    m = O.inputs(4, 3)
+    dm = O.dof_map(m.cv, 4, 3)
+    t, sp = O.ref_time_engine(O.ELASTICITY, 1, 3, m.ncells, dm, 12, 3 * m.nv, dm, 12, 3 * m.nv, m.cv, m.coords,
+                              params=(1.0, 0.5), threads=2, warmup=1, steps=2)
+    assert t.size == 2 and np.all(t > 0) and sp > 0
+    m = O.inputs(3, 2)
+    t, sp = O.ref_time_engine(O.HELMHOLTZ_ACTION, 2, 3, m.ncells, m.extra["p2"], 10, m.extra["nn"], None, 0, 0,
+                              m.cv, m.coords, coeff=m.extra["u"], params=(1.0,), threads=1, warmup=0, steps=1)
+    assert t[0] > 0 and sp == 0.0
