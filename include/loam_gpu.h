@@ -158,8 +158,17 @@ int loam_gpu_device_ok(void); /* 1 when an sm_100 device is usable */
  * LOAM_OPT_CHECK_SPARSITY: 1 (default) = a Mat INC/WRITE synchronises once to
  *   report OutsideSparsity like Mat::addto (data.hpp:214-216); 0 = the check
  *   is done only when the slot plan is built (plans prove the pattern).
- * LOAM_OPT_LOCALITY: 1 (default) = renumber cells internally for locality. */
-enum loam_option { LOAM_OPT_INC_STRATEGY = 0, LOAM_OPT_CHECK_SPARSITY = 1, LOAM_OPT_LOCALITY = 2 };
+ * LOAM_OPT_LOCALITY: 1 (default) = renumber cells internally for locality.
+ * LOAM_OPT_TEST_KERNELS: 1 = also register the kernels the reference's own
+ *   test suite builds (add_one, ones_block, double_direct, ...: test_parloop.cpp,
+ *   test_data.cpp); 0 (default) = the product registry only.
+ * LOAM_OPT_DETERMINISTIC: 1 = every scatter path is bitwise reproducible run
+ *   to run (no fp64 atomics whose order varies: the reference's guarantee,
+ *   parloop.hpp:182-190); 0 (default) = the fastest path per form, which may
+ *   sum some entries with fp64 REDs (results differ in the last bits between
+ *   runs, within 1e-12 of the reference).  Changing it clears the plan cache. */
+enum loam_option { LOAM_OPT_INC_STRATEGY = 0, LOAM_OPT_CHECK_SPARSITY = 1, LOAM_OPT_LOCALITY = 2,
+                   LOAM_OPT_TEST_KERNELS = 3, LOAM_OPT_DETERMINISTIC = 4 };
 int loam_gpu_set_option(int option, int value);
 int loam_gpu_get_option(int option);
 int loam_gpu_plan_cache_clear(void);

@@ -27,7 +27,7 @@ ERR_NO_DEVICE = 101
 READ, WRITE, RW, INC, SUM, MIN, MAX = range(7)  # loam::Access (data.hpp:17)
 ARG_DAT, ARG_MAT, ARG_GLOBAL = range(3)
 ARG_ZERO = 1
-OPT_INC_STRATEGY, OPT_CHECK_SPARSITY, OPT_LOCALITY = range(3)
+OPT_INC_STRATEGY, OPT_CHECK_SPARSITY, OPT_LOCALITY, OPT_TEST_KERNELS, OPT_DETERMINISTIC = range(5)
 STRATEGY = {"auto": 0, "atomic": 1, "owner": 2, "color": 3, "nbr": 4, "warpagg": 5, "patch": 6}
 
 

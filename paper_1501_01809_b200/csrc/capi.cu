@@ -141,6 +141,11 @@ int loam_gpu_set_option(int option, int value) {
       break;
     case LOAM_OPT_CHECK_SPARSITY: options().check_sparsity = value ? 1 : 0; break;
     case LOAM_OPT_LOCALITY: options().locality = value ? 1 : 0; break;
+    case LOAM_OPT_TEST_KERNELS: options().test_kernels = value ? 1 : 0; break;
+    case LOAM_OPT_DETERMINISTIC:
+      if (options().deterministic != (value ? 1 : 0)) plan_cache_clear(); // plans depend on it
+      options().deterministic = value ? 1 : 0;
+      break;
     default: fail(LOAM_ERR(InvalidArgument), "unknown option");
     }
   });
@@ -151,6 +156,8 @@ int loam_gpu_get_option(int option) {
   case LOAM_OPT_INC_STRATEGY: return options().inc_strategy;
   case LOAM_OPT_CHECK_SPARSITY: return options().check_sparsity;
   case LOAM_OPT_LOCALITY: return options().locality;
+  case LOAM_OPT_TEST_KERNELS: return options().test_kernels;
+  case LOAM_OPT_DETERMINISTIC: return options().deterministic;
   default: return -1;
   }
 }

@@ -4,6 +4,9 @@
 // becomes an int code 1 + kind with a thread-local message.  Internally the
 // engine throws loam_gpu::Error and the C ABI (capi.cu) converts.
 #pragma once
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -103,5 +106,17 @@ inline void ensure_dynamic_smem(const void* kern, size_t smem) {
 }
 
 constexpr int kNumSMs = 148; // B200
+
+// Developer phase timing of plan construction (LOAM_GPU_PLAN_TIMING=1):
+// synchronises `s` and prints the host wall clock since the previous tick.
+inline void plan_tick(const char* label, cudaStream_t s) {
+  static const bool on = std::getenv("LOAM_GPU_PLAN_TIMING") != nullptr;
+  if (!on) return;
+  static auto last = std::chrono::steady_clock::now();
+  cudaStreamSynchronize(s);
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[plan] %-28s %9.3f ms\n", label, std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
 
 } // namespace loam_gpu

@@ -1,3 +1,4 @@
+#include <chrono>
 // engine.cu -- the B200 par_loop engine: registry, validate, execute.
 //
 // Replaces loam::execute (parloop.hpp:191-384).  Two device paths:
@@ -829,7 +830,7 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
         }
       };
       double X0[GD];
-      vertex(self, X0);
+      if (L > 0) vertex(self, X0); // L == 0: a row no cell of the loop touches (no pairs)
       for (int p = pptr_s[node] - P0; p < p1; p += 2) { // two pairs per iteration (ILP)
         constexpr int N = F::NRN;
         const bool two = p + 1 < p1;
@@ -902,8 +903,9 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
       }
       if constexpr (!F::BILINEAR) a.out[R0 + node] = a.accumulate ? a.out[R0 + node] + acc : acc;
       if constexpr (F::BILINEAR && !REG)
+        if (L > 0)
 #pragma unroll
-        for (int c = 0; c < F::CD; ++c) seg[rstart + self * F::CD + c] += dblk[c];
+          for (int c = 0; c < F::CD; ++c) seg[rstart + self * F::CD + c] += dblk[c];
       if constexpr (REG) { // the row straight from registers (scalar rows: W == 1)
         double* o = a.out + E0 + a0;
 #pragma unroll
@@ -2088,6 +2090,17 @@ const std::map<std::string, Entry>& registry() {
     m["stokes_a_p2_tri"] = form_entry<F_STOKES_A, 2, 2>("stokes_a_p2_tri");
     m["stokes_b_p2_tri"] = form_entry<F_STOKES_B, 2, 2>("stokes_b_p2_tri");
     m["stokes_bt_p2_tri"] = form_entry<F_STOKES_BT, 2, 2>("stokes_bt_p2_tri");
+    return m;
+  }();
+  return r;
+}
+
+// The kernels the reference's own test suite builds (test_parloop.cpp,
+// test_data.cpp: add_one, ones_block, ...): a separate registry, visible only
+// when LOAM_OPT_TEST_KERNELS is set (the parity tests), not product kernels.
+const std::map<std::string, Entry>& test_registry() {
+  static const std::map<std::string, Entry> r = [] {
+    std::map<std::string, Entry> m;
     using namespace testk;
     m["double_direct"] = plain_entry<DoubleDirect>("double_direct", {"A", "B"}, {{1}, {1}});
     m["add_one"] = plain_entry<AddOne>("add_one", {"V"}, {{3}});
@@ -2111,12 +2124,22 @@ const std::map<std::string, Entry>& registry() {
   return r;
 }
 
+const Entry* find_entry(const std::string& name) {
+  auto it = registry().find(name);
+  if (it != registry().end()) return &it->second;
+  if (options().test_kernels) {
+    auto jt = test_registry().find(name);
+    if (jt != test_registry().end()) return &jt->second;
+  }
+  return nullptr;
+}
+
 const Entry& lookup(const char* name) {
   require(name != nullptr, LOAM_ERR(InvalidArgument), "parloop without kernel");
-  auto it = registry().find(name);
-  require(it != registry().end(), LOAM_ERR(InvalidArgument),
+  const Entry* e = find_entry(name);
+  require(e != nullptr, LOAM_ERR(InvalidArgument),
           std::string("kernel ") + name + " has no device implementation (no CPU fallback)");
-  return it->second;
+  return *e;
 }
 
 // ===========================================================================
@@ -2509,6 +2532,7 @@ void build_cell_segments(const int32_t* sorted_rows, int n, int arity, FastPlan&
 
 std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_desc* args, bool cell_mode,
                                           cudaStream_t s) {
+  plan_tick("plan start", s);
   auto P = std::make_shared<FastPlan>();
   P->counter.init(s);
   P->exact = k.bilinear ? pattern_provenance_exact(args[0]) : map_covers_target(node_view(args[0].map).v, s);
@@ -2530,9 +2554,11 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     LG_CUDA(cudaMemcpyAsync(P->loc.perm.get(), id.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
     LG_CUDA(cudaStreamSynchronize(s));
   }
+  plan_tick("locality order", s);
   const int32_t* perm = P->loc.perm.get();
   SortedMap srows;
   gather_rows(R.v, perm, srows, s);
+  plan_tick("gather rows", s);
   if (cell_mode) { // sorted row / coordinate / coefficient maps (+ per-cell slot ranks)
     P->use_cell = true;
     if (k.bilinear) {
@@ -2611,13 +2637,16 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
                          (!k.bilinear || P->exact ||
                           pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, 1, 1, csr.row_ptr, csr.col_idx,
                                                  csr.nnz, s));
+    plan_tick("nbr checks", s);
     if (star_ok && build_stars(R.v.v, n, R.v.target, P->star, s)) {
+      plan_tick("stars", s);
       if (k.bilinear) P->exact = true;
       P->use_star = true;
       return P;
     }
     if (ok && build_nbr(P->nb, srows.v.get(), n, R.v.arity, R.v.target, csr, kTileThreads / R.dim,
                         k.bilinear ? kTileSeg : (1 << 30), kTileSlots, kTileRuns, s)) {
+      plan_tick("nbr / ring tiles", s);
       P->use_nbr = true;
       return P;
     }
@@ -2633,8 +2662,11 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     }
     const loam_sparsity_desc* sp = args[0].sparsity;
     CsrView csr{sp->row_ptr, sp->col_idx, sp->nrows, sp->ncols, sp->nnz, R.dim, Cn.dim};
+    plan_tick("pairs", s);
     build_ranks(P->pp, srows.v.get(), sc, Cn.v.arity, csr, s);
+    plan_tick("ranks", s);
     build_chunks(P->pp, csr, kSegMax, 32 / R.dim, s);
+    plan_tick("chunks", s);
     // edge tiles: scalar P2 mass / stiffness / helmholtz on one (map, map) pattern
     const bool et_form = ((k.form == F_MASS || k.form == F_STIFFNESS || k.form == F_HELMHOLTZ) &&
                           k.nrn == (k.gd == 2 ? 6 : 10) && k.ncn == k.nrn && k.rd == 1 && k.cd == 1) ||
@@ -2654,6 +2686,7 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       es.tile_cells = env_int("LOAM_GPU_ET_CELLS", es.tile_cells);
       if (build_etile(P->et, es, k.gd, n, R.v.target, srows.v.get(), sx.v.get(), X->target_size, P->pp,
                       sp->row_ptr, sp->nnz, k.rd, s)) {
+        plan_tick("edge tiles", s);
         P->use_etile = true;
         return P;
       }
@@ -2672,6 +2705,7 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       ns.tile_slots = env_int("LOAM_GPU_NT_SLOTS", ns.tile_slots);
       if (build_ntile(P->nt, ns, n, R.v.target, srows.v.get(), sx.v.get(), X->target_size, P->pp, sp->row_ptr,
                       sp->nnz, s)) {
+        plan_tick("node tiles", s);
         P->use_ntile = true;
         return P;
       }
@@ -2685,6 +2719,7 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       rs.tile_rows = env_int("LOAM_GPU_RT_ROWS", rs.tile_rows);
       if (build_rtile(P->rt, rs, k.form, k.gd, k.nrn, k.ncn, k.rd, k.cd, n, R.v.target, srows.v.get(), sx.v.get(),
                       X->target_size, P->pp, sp->row_ptr, sp->nnz, s)) {
+        plan_tick("row tiles", s);
         P->use_rtile = true;
         return P;
       }
@@ -2719,6 +2754,7 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     }
     if (build_ptile(P->pt, spec, n, R.v.target, srows.v.get(), nullptr, sx.v.get(), X->target_size,
                     Cm ? scf.v.get() : nullptr, Cm ? Cm->target_size : 0, P->pp, csr, s)) {
+      plan_tick("pair tiles", s);
       P->use_ptile = true;
       return P;
     }
@@ -3261,17 +3297,22 @@ void run_generic(const Entry& k, int n, uint64_t iter, const loam_arg_desc* args
 // ===========================================================================
 
 const KernelInfo* find_kernel(const std::string& name) {
-  auto it = registry().find(name);
-  return it == registry().end() ? nullptr : &it->second.info;
+  const Entry* e = find_entry(name);
+  return e ? &e->info : nullptr;
 }
 
 const std::string& kernel_names() {
-  static const std::string s = [] {
+  static const std::string prod = [] {
     std::string r;
     for (auto& [name, e] : registry()) r += name + "\n";
     return r;
   }();
-  return s;
+  static const std::string all = [] {
+    std::string r = prod;
+    for (auto& [name, e] : test_registry()) r += name + "\n";
+    return r;
+  }();
+  return options().test_kernels ? all : prod;
 }
 
 void validate(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_desc* args, int nargs) {

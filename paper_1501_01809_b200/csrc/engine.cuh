@@ -11,6 +11,8 @@ struct Options {
   int inc_strategy = 0;   // 0 auto, 1 atomics, 2 owner-computes, 3 colouring
   int check_sparsity = 1;
   int locality = 1;
+  int test_kernels = 0;   // expose the reference test-suite kernels (add_one, ...)
+  int deterministic = 0;  // bitwise-reproducible scatter paths only
 };
 Options& options();
 

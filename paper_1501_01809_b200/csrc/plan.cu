@@ -289,8 +289,10 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
     LG_CUDA(cudaFreeAsync(built_ci, s));
   }
   // ---- pairs grouped by row, packed records
+  plan_tick("nbr: node pattern", s);
   PairPlan pp;
   build_pairs(sorted_rows, ncells, nrn, nrows_node, pp, s);
+  plan_tick("nbr: pairs", s);
   std::vector<int32_t> h(nrows_node + 1), hp(nrows_node + 1);
   LG_CUDA(cudaMemcpyAsync(h.data(), np.nptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaMemcpyAsync(hp.data(), pp.ptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
@@ -336,6 +338,7 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
     }
     if (herr >> 62) return false;
   }
+  plan_tick("nbr: records", s);
   np.pptr.alloc(nrows_node + 1 + 4, s);
   LG_CUDA(cudaMemsetAsync(np.pptr.get(), 0, np.pptr.bytes(), s));
   LG_CUDA(cudaMemcpyAsync(np.pptr.get(), pp.ptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToDevice, s));
@@ -352,6 +355,7 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
   std::vector<int32_t> verts;
   std::vector<std::pair<int, int>> rr;
   std::vector<std::pair<int, int>> tile_of_rows;
+  bool has_empty_row = false;
   auto make_runs = [&](int r0, int r1) { // runs of the tile's vertices; returns slot count
     verts.assign(hadj.begin() + h[r0], hadj.begin() + h[r1]);
     std::sort(verts.begin(), verts.end());
@@ -393,7 +397,11 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
     for (int r = r0; r < r1; ++r) {
       int q = 0;
       while (h[r] + q < h[r + 1] && hadj[h[r] + q] != r) ++q;
-      require(h[r] + q < h[r + 1], LOAM_ERR(InvalidArgument), "row node missing from its own pattern row");
+      // a row node no cell of the loop touches (a sub-mesh loop) has an empty
+      // pattern row and no pairs: its owner writes nothing but its zero
+      require(h[r] + q < h[r + 1] || (h[r] == h[r + 1] && hp[r] == hp[r + 1]), LOAM_ERR(InvalidArgument),
+              "row node missing from its own pattern row");
+      if (h[r] == h[r + 1]) has_empty_row = true;
       hs[r] = (uint8_t)q;
     }
     tiles.insert(tiles.end(), {r0, r1, h[r0], h[r1], hp[r0], hp[r1], (int)runs.size() / 2, (int)rr.size()});
@@ -406,6 +414,7 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
     np.max_runs = std::max(np.max_runs, (int)rr.size());
     r0 = r1;
   }
+  plan_tick("nbr: host tiles", s);
   np.ntiles = (int)tiles.size() / 8;
   np.tiles.alloc(tiles.size() ? tiles.size() : 8, s);
   np.runs.alloc(runs.size() ? runs.size() : 2, s);
@@ -415,7 +424,7 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
   // vertex ring / fan so a kernel fetches one new vertex per cell and completes
   // every off-diagonal entry after two consecutive cells (no read-modify-write)
   np.ring = false;
-  if (nrn == 3 && maxlen <= 8 && np.max_slots <= 8191 && pp.npairs) {
+  if (nrn == 3 && maxlen <= 8 && np.max_slots <= 8191 && pp.npairs && !has_empty_row) {
     std::vector<int32_t> hpairs(pp.npairs), hrows((size_t)ncells * nrn);
     // pp.ptr was moved into np.pptr above; pair codes are still in pp.pairs
     LG_CUDA(cudaMemcpyAsync(hpairs.data(), pp.pairs.get(), sizeof(int32_t) * pp.npairs, cudaMemcpyDeviceToHost, s));

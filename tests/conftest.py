@@ -32,6 +32,12 @@ def _ensure_built():
 
 _ensure_built()
 
+# The reference test-suite kernels (add_one, ones_block, ...) are a separate,
+# opt-in registry (LOAM_OPT_TEST_KERNELS): the parity tests use them.
+from paper_1501_01809_b200 import capi as _capi  # noqa: E402
+
+_capi.set_option(_capi.OPT_TEST_KERNELS, 1)
+
 
 @pytest.fixture(scope="session")
 def gpu_lib():

@@ -318,6 +318,7 @@ static void test_rcm() { // test_topology.cpp rcm_order cases
 }
 
 int main() {
+  loam_gpu_set_option(LOAM_OPT_TEST_KERNELS, 1); // the reference test-suite kernels
   const std::vector<std::pair<const char*, void (*)()>> cases = {
       {"direct loop doubles a field", test_direct_loop},
       {"indirect INC accumulates cell incidence", test_indirect_inc},

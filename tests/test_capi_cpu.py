@@ -71,6 +71,21 @@ def test_registry_staged_shapes(name, ext):
     assert out == ext
 
 
+def test_reference_test_kernels_are_opt_in():
+    """add_one & co. (the reference test suite's kernels) are not product
+    kernels: visible only with LOAM_OPT_TEST_KERNELS (conftest sets it)."""
+    L = capi.lib()
+    buf = (C.c_int32 * 8)()
+    try:
+        capi.set_option(capi.OPT_TEST_KERNELS, 0)
+        assert L.loam_gpu_kernel_signature(b"add_one", buf, 8) < 0
+        assert b"add_one" not in L.loam_gpu_kernel_names()
+        assert L.loam_gpu_kernel_signature(b"stiffness_p1_tri", buf, 8) == 2
+    finally:
+        capi.set_option(capi.OPT_TEST_KERNELS, 1)
+    assert L.loam_gpu_kernel_signature(b"add_one", buf, 8) == 1
+
+
 def test_unregistered_kernel_signature_is_an_error():
     buf = (C.c_int32 * 8)()
     n = capi.lib().loam_gpu_kernel_signature(b"no_such_kernel", buf, 8)
