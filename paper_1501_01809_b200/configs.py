@@ -107,10 +107,10 @@ def config_inputs(cfg: int, n: int | None = None) -> MeshInputs:
 class Workload:
     """One config's par_loop(s) built on the loam mirror (device-resident)."""
 
-    def __init__(self, cfg: int, n: int | None = None, part: str | None = None):
+    def __init__(self, cfg: int, n: int | None = None, part: str | None = None, inputs: MeshInputs | None = None):
         from . import loam as L  # torch import deferred
         self.cfg, self.part = cfg, part
-        m = self.inputs = config_inputs(cfg, n)
+        m = self.inputs = config_inputs(cfg, n) if inputs is None else inputs
         self.L = L
         cells = L.Set(m.ncells, "cells")
         verts = L.Set(m.nv, "vertices")

@@ -981,7 +981,7 @@ struct RingCell {
                                                  double& vs, double& vp, double& vn) {
     double kp = 0.0, kn = 0.0;
     if constexpr (K) {
-      const double r = 0.5 * fast_rcp(ad);
+      const double r = fast_half_rcp(ad);
       kp = (ab - bb) * r;
       kn = (ab - aa) * r;
     }
@@ -1002,7 +1002,7 @@ struct RingCell {
                                                   double us, double up, double un) {
     double v = 0.0;
     if constexpr (K) {
-      const double r = 0.5 * fast_rcp(ad);
+      const double r = fast_half_rcp(ad);
       v = ((ab - bb) * (up - us) + (ab - aa) * (un - us)) * r;
     }
     if constexpr (M) {
@@ -1353,42 +1353,48 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
     fence_mbar_init();
   }
   __syncthreads();
-  auto tile_meta = [&](int tile, int (&m)[8]) {
-    const int4* t = reinterpret_cast<const int4*>(a.tiles + 16 * tile);
-    const int4 x = __ldg(t), y = __ldg(t + 1);
-    m[0] = x.x; m[1] = x.y; m[2] = x.z; m[3] = x.w; m[4] = y.x; m[5] = y.y; m[6] = y.z; m[7] = y.w;
-  };
   auto ring = [&](int k) { return sm + a.off_buf + (k % 3) * a.buf_bytes; };
+  // tile records of this CTA, 8 tiles per batch, double-buffered (cp.async);
+  // the meta of the tile in each ring stage, handed to the consumers with it
+  __shared__ __align__(16) int meta_s[2][8 * 16];
+  __shared__ int stage_meta[3][8];
   if (tid >= kTileThreads) { // ---- producer warp
-    // Tiles: the first three of each CTA are static (blockIdx + k * grid), the
-    // rest come from the dynamic counter.  A tile's meta and its first window
-    // runs share one 64-byte record (plan.cu, kRingInlineRuns), and the next
-    // tile is fetched while the current stage drains, so a freed stage waits
-    // only for its bulk copies.
+    // Static schedule: tile k of this CTA is blockIdx + k * grid (tiles cost
+    // about the same).  The 64-byte tile records (meta + the first window
+    // runs) arrive 8 tiles at a time by cp.async, one batch ahead, so the
+    // producer's per-tile chain holds no dependent global round trip (the
+    // former dynamic counter cost an atomic, a record load and a run load
+    // per tile, ~3 round trips -- the consumers waited ~1k cycles per tile).
     const int lane = tid & 31;
-    auto grab = [&](int k) {
-      if (k < 3) return (int)(blockIdx.x + k * gridDim.x);
-      int t = 0;
-      if (lane == 0) t = 3 * gridDim.x + atomicAdd(a.next_tile, 1);
-      return __shfl_sync(0xffffffffu, t, 0);
+    auto load_batch = [&](int b) { // tiles 8b..8b+7 -> meta_s[b & 1]; lane = (tile in batch, 16-byte part)
+      const int kk = 8 * b + (lane >> 2), part = lane & 3;
+      const int tile = blockIdx.x + kk * gridDim.x;
+      if (tile < a.ntiles) cp_async16(&meta_s[b & 1][(lane >> 2) * 16 + part * 4], a.tiles + 16 * tile + part * 4);
+      cp_async_commit();
     };
-    auto fetch = [&](int tile, int (&mm)[8], int2& run) {
-      tile_meta(tile, mm);
-      int2 inl = make_int2(0, 0);
-      if (lane < kRingInlineRuns) inl = __ldg(reinterpret_cast<const int2*>(a.tiles + 16 * tile + 8) + lane);
-      const int cnt = mm[7];
-      run = lane < cnt ? (lane < kRingInlineRuns ? inl : __ldg(reinterpret_cast<const int2*>(a.runs) + mm[6] + lane))
-                       : make_int2(0, 0);
-    };
-    int nt = grab(0), nm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int2 nrun = make_int2(0, 0);
-    if (nt < a.ntiles) fetch(nt, nm, nrun);
+    load_batch(0);
+    load_batch(1);
     for (int k = 0;; ++k) {
-      const int tile = nt;
-      int m[8];
+      const int tile = blockIdx.x + k * gridDim.x;
+      if (k % 8 == 0) {
+        cp_async_wait<1>(); // batch k / 8 has landed (the next one may still be in flight)
+        __syncwarp();
+      }
+      const int* rec = &meta_s[(k / 8) & 1][(k % 8) * 16];
+      int m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int2 run0 = make_int2(0, 0);
+      if (tile < a.ntiles) { // (past the end the batch slot was never filled)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) m[q] = nm[q];
-      const int2 run0 = nrun;
+        for (int q = 0; q < 8; ++q) m[q] = rec[q];
+        const int cnt = m[7];
+        if (lane < cnt)
+          run0 = lane < kRingInlineRuns ? reinterpret_cast<const int2*>(rec + 8)[lane]
+                                        : __ldg(reinterpret_cast<const int2*>(a.runs) + m[6] + lane);
+      }
+      if (k % 8 == 7) {
+        __syncwarp(); // every lane has read batch k / 8: refill its buffer
+        load_batch(k / 8 + 2);
+      }
       if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
       if (tile >= a.ntiles) { // publish "no more tiles" through the stage
         if (lane == 0) {
@@ -1397,6 +1403,7 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
         }
         break;
       }
+      if (lane < 8) stage_meta[k % 3][lane] = m[lane];
       if (lane == 0) slot_tile[k % 3] = tile;
       unsigned char* buf = ring(k);
       uint64_t* bar = &full[k % 3];
@@ -1425,9 +1432,8 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
       __syncwarp();
       stage_runs<true>(rc, lane, bar, run0);
       stage_runs<true>(rk, lane, bar, run0);
-      nt = grab(k + 1);
-      if (nt < a.ntiles) fetch(nt, nm, nrun);
     }
+    cp_async_wait<0>();
     return;
   }
   // ---- consumers: one thread per row vertex
@@ -1448,7 +1454,8 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
     }
     if (tile < 0) break;
     int m[8];
-    tile_meta(tile, m);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) m[q] = stage_meta[k % 3][q];
     const int R0 = m[0], nrows = m[1] - m[0], A0 = m[2], nA = m[3] - m[2], P0 = m[4];
     // the segment, skewed so segb[t] and out[A0 + t] agree mod 16 bytes; the
     // previous tile's bulk store must have finished reading it
@@ -1481,55 +1488,91 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
       };
       const double2 xs = win[self_slot];
       const double us = F::HAS_COEFF ? winc[self_slot] : 0.0;
+      // a chain record is (window slot << 4 | in-row rank): the slot's byte
+      // offset in the double2 window is the record with the rank masked off
+      const unsigned char* winb = reinterpret_cast<const unsigned char*>(win);
+      auto wx = [&](uint32_t r) { return *reinterpret_cast<const double2*>(winb + (r & 0xfff0u)); };
+      auto wc = [&](uint32_t r) { return winc[r >> 4]; };
       // chain vertex 0 (a row with no cell has q1 == q0 + 1 and no pair)
       const uint32_t h0 = rec_s[q0];
       const int rk0 = h0 & 7;
       double2 ea;
       {
-        const double2 x = win[h0 >> 3];
+        const double2 x = wx(h0);
         ea = make_double2(x.x - xs.x, x.y - xs.y);
       }
       double aa = ea.x * ea.x + ea.y * ea.y;
-      double up = F::HAS_COEFF ? winc[h0 >> 3] : 0.0;
+      double up = F::HAS_COEFF ? wc(h0) : 0.0;
+      // pure stiffness: the diagonal is minus the sum of the row's
+      // off-diagonal entries (the same cell terms, summed per entry)
+      constexpr bool kDiagBySum = F::BILINEAR && RingCell<F>::K && !RingCell<F>::M;
       double diag = 0.0, first = 0.0, carry = 0.0, acc = 0.0;
       int rkp = rk0;
-      // one cell: (s, previous chain vertex, chain vertex q)
-      auto cell = [&](uint32_t r, double& vp, double& vn) {
-        const double2 x = win[r >> 3];
-        const double2 eb = make_double2(x.x - xs.x, x.y - xs.y);
-        const double bb = eb.x * eb.x + eb.y * eb.y;
-        const double ab = ea.x * eb.x + ea.y * eb.y;
-        const double ad = fabs(ea.x * eb.y - ea.y * eb.x);
+      // one cell (s, chain vertex with edge e0 / e0.e0 = a0, chain vertex at x):
+      // returns its edge and |edge|^2 for the next cell
+      auto cell = [&](const double2& e0, double a0, const double2& x, double2& e1, double& b1, double un,
+                      double& vp, double& vn) {
+        e1 = make_double2(x.x - xs.x, x.y - xs.y);
+        b1 = e1.x * e1.x + e1.y * e1.y;
+        const double ab = e0.x * e1.x + e0.y * e1.y;
+        const double ad = fabs(e0.x * e1.y - e0.y * e1.x);
         if constexpr (F::BILINEAR) {
           double vs;
-          RingCell<F>::entries(aa, ab, bb, ad, kappa, vs, vp, vn);
-          diag += vs;
+          RingCell<F>::entries(a0, ab, b1, ad, kappa, vs, vp, vn);
+          if constexpr (!kDiagBySum) diag += vs;
         } else {
-          const double un = winc[r >> 3];
-          acc += RingCell<F>::action(aa, ab, bb, ad, kappa, us, up, un);
+          acc += RingCell<F>::action(a0, ab, b1, ad, kappa, us, up, un);
           up = un;
         }
-        ea = eb;
-        aa = bb;
+      };
+      auto emit = [&](int rank, double v) {
+        if constexpr (F::BILINEAR) {
+          put(rank, v);
+          if constexpr (kDiagBySum) diag -= v;
+        }
       };
       if (q1 - q0 > 1) {
-        double vp, vn;
+        double vp = 0.0, vn = 0.0;
         uint32_t r = rec_s[q0 + 1];
-        cell(r, first, carry);
+        {
+          double2 e1;
+          double b1;
+          cell(ea, aa, wx(r), e1, b1, F::HAS_COEFF ? wc(r) : 0.0, first, carry);
+          ea = e1;
+          aa = b1;
+        }
         rkp = r & 7;
-#pragma unroll 2
-        for (int q = q0 + 2; q < q1; ++q) {
+        int q = q0 + 2;
+        // two cells per iteration; the second writes the loop-carried edge in
+        // place (no register rotation)
+        for (; q + 1 < q1; q += 2) {
+          const uint32_t r1 = rec_s[q], r2 = rec_s[q + 1];
+          const double2 x1 = wx(r1), x2 = wx(r2);
+          const double u1 = F::HAS_COEFF ? wc(r1) : 0.0, u2 = F::HAS_COEFF ? wc(r2) : 0.0;
+          double2 e1;
+          double b1;
+          cell(ea, aa, x1, e1, b1, u1, vp, vn);
+          emit(rkp, carry + vp);
+          carry = vn;
+          cell(e1, b1, x2, ea, aa, u2, vp, vn);
+          emit(r1 & 7, carry + vp);
+          carry = vn;
+          rkp = r2 & 7;
+        }
+        if (q < q1) {
           r = rec_s[q];
-          cell(r, vp, vn);
-          if constexpr (F::BILINEAR) put(rkp, carry + vp);
+          double2 e1;
+          double b1;
+          cell(ea, aa, wx(r), e1, b1, F::HAS_COEFF ? wc(r) : 0.0, vp, vn);
+          emit(rkp, carry + vp);
           carry = vn;
           rkp = r & 7;
         }
         if constexpr (F::BILINEAR) {
-          if (rkp == rk0) put(rk0, first + carry); // closed ring
+          if (rkp == rk0) emit(rk0, first + carry); // closed ring
           else {
-            put(rk0, first);
-            put(rkp, carry);
+            emit(rk0, first);
+            emit(rkp, carry);
           }
         }
       }

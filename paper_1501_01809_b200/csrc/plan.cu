@@ -424,7 +424,7 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
   // vertex ring / fan so a kernel fetches one new vertex per cell and completes
   // every off-diagonal entry after two consecutive cells (no read-modify-write)
   np.ring = false;
-  if (nrn == 3 && maxlen <= 8 && np.max_slots <= 8191 && pp.npairs && !has_empty_row) {
+  if (nrn == 3 && maxlen <= 8 && np.max_slots <= 4095 && pp.npairs && !has_empty_row) {
     std::vector<int32_t> hpairs(pp.npairs), hrows((size_t)ncells * nrn);
     // pp.ptr was moved into np.pptr above; pair codes are still in pp.pairs
     LG_CUDA(cudaMemcpyAsync(hpairs.data(), pp.pairs.get(), sizeof(int32_t) * pp.npairs, cudaMemcpyDeviceToHost, s));
@@ -462,7 +462,7 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
         const int self_slot = slot_of(r), self_rank = rank_of(r);
         rinfo[r] = (uint32_t)self_slot | ((uint32_t)self_rank << 16);
         if (P == 0) {
-          rrec[rptr[r]] = (uint16_t)((self_slot << 3) | self_rank);
+          rrec[rptr[r]] = (uint16_t)((self_slot << 4) | self_rank);
           continue;
         }
         // degree of every neighbour in the star; open fans start at a degree-1 vertex
@@ -477,14 +477,14 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
         if (!ok || (ones != 0 && ones != 2)) { ok = false; break; }
         used.assign(P, 0);
         int v = start;
-        rrec[rptr[r]] = (uint16_t)((slot_of(v) << 3) | rank_of(v));
+        rrec[rptr[r]] = (uint16_t)((slot_of(v) << 4) | rank_of(v));
         for (int k = 0; k < P; ++k) {
           int q = 0;
           while (q < P && (used[q] || (av[q] != v && bv[q] != v))) ++q;
           if (q == P) { ok = false; break; } // star is not a single fan / ring
           used[q] = 1;
           v = av[q] == v ? bv[q] : av[q];
-          rrec[rptr[r] + 1 + k] = (uint16_t)((slot_of(v) << 3) | rank_of(v));
+          rrec[rptr[r] + 1 + k] = (uint16_t)((slot_of(v) << 4) | rank_of(v));
         }
         if (ok && ones == 0 && v != start) ok = false; // a ring must close
       }

@@ -18,6 +18,14 @@ import numpy as np
 import torch
 
 from . import capi
+
+
+def _release(obj_id: int) -> None:
+    """Evict a destroyed Map / Sparsity's cached plans (quietly at interpreter exit)."""
+    try:
+        capi.release_id(obj_id)
+    except Exception:  # noqa: BLE001 -- module teardown: nothing left to evict
+        pass
 from .capi import INC, MAX, MIN, READ, RW, SUM, WRITE, LoamError
 
 class _Ids:
@@ -106,7 +114,7 @@ class Map:
         return self.id, dim
 
     def __del__(self):
-        capi.release_id(getattr(self, "id", 0))
+        _release(getattr(self, "id", 0))
 
     def desc(self) -> capi.MapDesc:
         if self._desc is None:
@@ -263,7 +271,7 @@ class Sparsity:
         return self._desc
 
     def __del__(self):
-        capi.release_id(getattr(self, "id", 0))
+        _release(getattr(self, "id", 0))
 
 
 def build_sparsity(row_map: Map, col_map: Map, row_dim: int = 1, col_dim: int = 1) -> Sparsity:
