@@ -27,6 +27,18 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+// Raise the expected transaction bytes of the current phase without arriving.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+// Programmatic dependent launch (PDL).  wait: block until every prerequisite
+// grid has completed and its memory is visible (a no-op for a kernel launched
+// without the programmatic attribute); launch_dependents: this CTA allows the
+// next PDL-launched kernel in the stream to start its prologue.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifdef LOAM_GPU_MBAR_SUSPEND
   // with a suspend-time hint the waiting warp sleeps instead of spinning,

@@ -1353,6 +1353,9 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
     fence_mbar_init();
   }
   __syncthreads();
+  // PDL: the next PDL-launched kernel may start its prologue (it waits for
+  // this grid's completion before touching anything this grid writes)
+  if (tid == 0) grid_dep_launch();
   auto ring = [&](int k) { return sm + a.off_buf + (k % 3) * a.buf_bytes; };
   // tile records of this CTA, 8 tiles per batch, double-buffered (cp.async);
   // the meta of the tile in each ring stage, handed to the consumers with it
@@ -1418,21 +1421,26 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
                       reinterpret_cast<double*>(buf + a.b_win), 2};
       const RunSet rk{reinterpret_cast<const int2*>(a.runs) + m[6], F::HAS_COEFF ? m[7] : 0, a.coeff,
                       reinterpret_cast<double*>(buf + a.b_winc), 1};
-      const uint32_t tx = n0 + n1 + n2 + n3 + stage_runs<false>(rc, lane, bar, run0) +
-                          stage_runs<false>(rk, lane, bar, run0);
-      fence_async_shared();
-      __syncwarp();
+      // plan ranges (library-owned, immutable: safe before the PDL wait)
       if (lane == 0) {
-        mbar_arrive_expect_tx(bar, tx);
+        mbar_expect_tx(bar, n0 + n1 + n2 + n3);
         if (n0) bulk_g2s(buf + a.b_nptr, reinterpret_cast<const unsigned char*>(a.nptr) + g0, n0, bar);
         bulk_g2s(buf + a.b_rptr, reinterpret_cast<const unsigned char*>(a.rptr) + g1, n1, bar);
         if (n2) bulk_g2s(buf + a.b_recs, reinterpret_cast<const unsigned char*>(a.recs) + g2, n2, bar);
         if (n3) bulk_g2s(buf + a.b_info, reinterpret_cast<const unsigned char*>(a.rowinfo) + g3, n3, bar);
       }
+      // the caller's data (coordinates / coefficients) only after every
+      // prerequisite grid has completed
+      if (k == 0) grid_dep_wait();
+      const uint32_t tx = stage_runs<false>(rc, lane, bar, run0) + stage_runs<false>(rk, lane, bar, run0);
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(bar, tx);
       __syncwarp();
       stage_runs<true>(rc, lane, bar, run0);
       stage_runs<true>(rk, lane, bar, run0);
     }
+    if (a.ntiles <= (int)blockIdx.x) grid_dep_wait(); // (no tile: still order the exit)
     cp_async_wait<0>();
     return;
   }
@@ -1453,6 +1461,7 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
       else t_wait += c1 - c0;
     }
     if (tile < 0) break;
+    if (k == 0) grid_dep_wait(); // (returns at once: the producer has waited)
     int m[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) m[q] = stage_meta[k % 3][q];
@@ -1646,6 +1655,12 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
   }
 }
 
+// PDL for the persistent tile kernels (LOAM_GPU_NO_PDL=1 disables it).
+bool pdl_enabled() {
+  static const bool on = std::getenv("LOAM_GPU_NO_PDL") == nullptr;
+  return on;
+}
+
 template <class F>
 void launch_ring(const RingArgs& a, size_t smem, cudaStream_t s) {
   if constexpr (F::GD == 2 && F::NRN == 3 && F::RD == 1 && F::CD == 1) {
@@ -1660,7 +1675,20 @@ void launch_ring(const RingArgs& a, size_t smem, cudaStream_t s) {
     int blocks = 1;
     LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kTileBlock, smem));
     const int grid = std::min(a.ntiles, std::max(blocks, 1) * kNumSMs);
-    kern<<<grid, kTileBlock, smem, s>>>(a);
+    // programmatic dependent launch: the kernel's prologue (barriers, tile
+    // records, plan ranges) overlaps the previous kernel's tail; it waits
+    // (griddepcontrol.wait) before reading the caller's data or writing
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTileBlock);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr_pdl[1];
+    attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr_pdl[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr_pdl;
+    cfg.numAttrs = 1;
+    LG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
     count_launch();
     LG_LAUNCH_CHECK();
   } else {
