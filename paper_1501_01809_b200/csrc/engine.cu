@@ -770,7 +770,7 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_tile(const __grid_constant__ 
   if (tid >= kTileThreads) { // ---- producer warp: TMA issue only, up to 3 tiles ahead
     if (tid == kTileThreads)
       for (int k = 0; k < K; ++k) {
-        if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
+        if (k >= 3) mbar_wait_sleep(&empty[k % 3], (k / 3 - 1) & 1);
         issue(k);
       }
     return;
@@ -1398,7 +1398,7 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
         __syncwarp(); // every lane has read batch k / 8: refill its buffer
         load_batch(k / 8 + 2);
       }
-      if (k >= 3) mbar_wait(&empty[k % 3], (k / 3 - 1) & 1);
+      if (k >= 3) mbar_wait_sleep(&empty[k % 3], (k / 3 - 1) & 1);
       if (tile >= a.ntiles) { // publish "no more tiles" through the stage
         if (lane == 0) {
           slot_tile[k % 3] = -1;
@@ -1524,7 +1524,10 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
         e1 = make_double2(x.x - xs.x, x.y - xs.y);
         b1 = e1.x * e1.x + e1.y * e1.y;
         const double ab = e0.x * e1.x + e0.y * e1.y;
-        const double ad = fabs(e0.x * e1.y - e0.y * e1.x);
+        // |cross| with the sign bit cleared on the integer pipe (the FP64
+        // pipe is this loop's busiest unit)
+        const double cr = e0.x * e1.y - e0.y * e1.x;
+        const double ad = __hiloint2double(__double2hiint(cr) & 0x7fffffff, __double2loint(cr));
         if constexpr (F::BILINEAR) {
           double vs;
           RingCell<F>::entries(a0, ab, b1, ad, kappa, vs, vp, vn);
@@ -1781,7 +1784,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
 #pragma unroll
       for (int q = 0; q < 12; ++q) m[q] = nm[q];
       const int2 run0 = nrun, crun0 = ncrun;
-      if (k >= kPS) mbar_wait(&empty[k % kPS], (k / kPS - 1) & 1);
+      if (k >= kPS) mbar_wait_sleep(&empty[k % kPS], (k / kPS - 1) & 1);
       if (tile >= a.ntiles) {
         if (lane == 0) {
           slot_tile[k % kPS] = -1;
@@ -2715,7 +2718,16 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       P->use_star = true;
       return P;
     }
-    if (ok && build_nbr(P->nb, srows.v.get(), n, R.v.arity, R.v.target, csr, kTileThreads / R.dim,
+    // tile rows: at most one per consumer thread; for the ring kernel's static
+    // schedule (3 CTAs per SM) the row count is evened out so every CTA gets
+    // the same number of tiles (no tail of CTAs with one tile more)
+    int tile_rows = kTileThreads / R.dim;
+    if (k.ring && R.dim == 1 && k.bilinear) {
+      const int G = 3 * kNumSMs;
+      const int per_cta = ceil_div(ceil_div(R.v.target, tile_rows), G);
+      tile_rows = std::max(32, ceil_div(R.v.target, (int64_t)per_cta * G));
+    }
+    if (ok && build_nbr(P->nb, srows.v.get(), n, R.v.arity, R.v.target, csr, tile_rows,
                         k.bilinear ? kTileSeg : (1 << 30), kTileSlots, kTileRuns, s)) {
       plan_tick("nbr / ring tiles", s);
       P->use_nbr = true;

@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
 #pragma unroll
       for (int q = 0; q < 16; ++q) m[q] = nm[q];
       const int2 run0 = nrun;
-      if (k >= STAGES) mbar_wait(&empty[k % STAGES], (k / STAGES - 1) & 1);
+      if (k >= STAGES) mbar_wait_sleep(&empty[k % STAGES], (k / STAGES - 1) & 1);
       if (tile >= a.ntiles) {
         if (lane == 0) {
           slot_tile[k % STAGES] = -1;

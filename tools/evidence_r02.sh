@@ -1,0 +1,15 @@
+# Round-2 ncu evidence: launch list of the contract bench command (C2) and one
+# --set full capture per config's dominant kernel (each command exits 0
+# without ncu first; see tools/r02_check.sh).  Summaries -> gpurun_out/ev2/.
+O=gpurun_out/ev2; mkdir -p $O
+summ() { python tools/ncu_summary.py $1.ncu-rep 20 > $1.txt 2>&1; python tools/ncu_lines.py $1.ncu-rep 25 >> $1.txt 2>&1; ncu -i $1.ncu-rep --page raw --csv > $1_raw.csv 2>/dev/null; rm -f $1.ncu-rep; }
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config-table > $O/plain_bench.jsonl 2> $O/plain_bench.err; echo plain_rc=$?
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 200 --csv --log-file $O/launches_c2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config-table > $O/ncu_launch.log 2>&1; echo launch_rc=$?
+ncu --set full --clock-control none --import-source on -k regex:k_ring -s 12 -c 1 -o $O/c2_ring python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config-table > $O/ncu_c2.log 2>&1; echo ncu_c2_rc=$?
+summ $O/c2_ring
+for c in 1 3r 3m 4 5; do
+  case $c in 1) k=k_star;; 3r) k=k_cell;; 3m) k=k_etile;; 4) k=k_ntile;; 5) k=k_etile;; esac
+  python bench.py --all-configs --configs $c --strategies auto --steps 3 > $O/plain_cfg$c.log 2>&1; echo plain_$c rc=$?
+  ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o $O/cfg$c python bench.py --all-configs --configs $c --strategies auto --steps 3 > $O/ncu_cfg$c.log 2>&1; echo ncu_$c rc=$?
+  summ $O/cfg$c
+done
