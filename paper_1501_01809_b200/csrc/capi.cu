@@ -364,7 +364,26 @@ int loam_gpu_execute_host_batch(const loam_kernel_desc* kernel, int32_t n, uint6
                 LOAM_ERR(InvalidArgument), "batched steps must share the loop shape");
     // two device buffer sets; a set is reused once its previous step's downloads finished
     std::vector<DevBuf<double>> bufs[2];
-    cudaEvent_t in_ready[2], done[2], freed[2];
+    // Declared after the buffers, so destroyed first -- on success AND when a
+    // step throws: both copy streams and `s` are drained before the buffers
+    // are freed (stream-ordered on s) and before the caller's host buffers
+    // are released, then the events are destroyed.
+    struct Guard {
+      CopyStreams& cs;
+      cudaStream_t s;
+      cudaEvent_t ev[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+      ~Guard() {
+        cudaStreamSynchronize(cs.h2d);
+        cudaStreamSynchronize(cs.d2h);
+        cudaStreamSynchronize(s);
+        for (auto& row : ev)
+          for (auto& e : row)
+            if (e) cudaEventDestroy(e);
+      }
+    } guard{cs, s};
+    cudaEvent_t* in_ready = guard.ev[0];
+    cudaEvent_t* done = guard.ev[1];
+    cudaEvent_t* freed = guard.ev[2];
     for (int b = 0; b < 2; ++b) {
       for (int q = 0; q < nargs; ++q) bufs[b].emplace_back(std::max<size_t>(arg_count(a0[q]), 1), s);
       LG_CUDA(cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming));
@@ -402,11 +421,6 @@ int loam_gpu_execute_host_batch(const loam_kernel_desc* kernel, int32_t n, uint6
     }
     LG_CUDA(cudaStreamSynchronize(cs.d2h));
     LG_CUDA(cudaStreamSynchronize(s));
-    for (int b = 0; b < 2; ++b) {
-      cudaEventDestroy(in_ready[b]);
-      cudaEventDestroy(done[b]);
-      cudaEventDestroy(freed[b]);
-    }
   });
 }
 

@@ -290,9 +290,28 @@ __global__ void k_renumber_map(int64_t len, int n, const int32_t* __restrict__ n
 
 } // namespace
 
+__global__ void k_rcm_rowptr_check(int n, const int64_t* __restrict__ rp, int* bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 && rp[0] != 0) atomicOr(bad, 1);
+  if (i < n && rp[i + 1] < rp[i]) atomicOr(bad, 1);
+}
+
 void rcm_order_dev(int n, const int64_t* rp, const int32_t* ci, int32_t* out, cudaStream_t s) {
   require(n >= 0, LOAM_ERR(InvalidArgument), "negative vertex count");
   if (n == 0) return;
+  // the list structure first: row_ptr must start at 0 and never
+  // decrease, or the validation below would read outside col_idx and fault
+  {
+    DevBuf<int> shape(1, s);
+    LG_CUDA(cudaMemsetAsync(shape.get(), 0, sizeof(int), s));
+    k_rcm_rowptr_check<<<grid_for(n), kThreads, 0, s>>>(n, rp, shape.get());
+    count_launch();
+    LG_CUDA(cudaGetLastError());
+    int hshape = 0;
+    LG_CUDA(cudaMemcpyAsync(&hshape, shape.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    LG_CUDA(cudaStreamSynchronize(s));
+    require(hshape == 0, LOAM_ERR(InvalidArgument), "adjacency list count != n (row offsets not a CSR of n lists)");
+  }
   DevBuf<unsigned long long> bad(1, s);
   LG_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), s));
   k_rcm_validate<<<grid_for(n), kThreads, 0, s>>>(n, rp, ci, bad.get());

@@ -887,6 +887,10 @@ def rcm_order(n: int, row_ptr, col_idx) -> torch.Tensor:
     ci = torch.as_tensor(np.asarray(col_idx, np.int32) if isinstance(col_idx, (list, np.ndarray)) else col_idx)
     rp = rp.to(device="cuda", dtype=torch.int64).contiguous()
     ci = ci.to(device="cuda", dtype=torch.int32).contiguous()
+    # the reference rejects a list count != n (InvalidArgument); here the
+    # offsets must also fit the column array (the device checks monotonicity)
+    if rp.numel() != n + 1 or (n > 0 and int(rp[-1].item()) > ci.numel()):
+        raise capi.LoamError(1 + capi.ERROR_KINDS.index("InvalidArgument"), "adjacency list count != n")
     if ci.numel() == 0:
         ci = torch.zeros(1, dtype=torch.int32, device="cuda")
     out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")

@@ -132,3 +132,19 @@ def test_reorder_config_meshes_equal_restatement(gpu_lib, gdim, n):
     new_of[ref] = np.arange(m.nv, dtype=np.int32)
     assert np.array_equal(cv, new_of[m.cv])
     assert np.array_equal(x, m.coords.reshape(-1, gdim)[ref].ravel())
+
+
+@pytest.mark.parametrize("rp,ci", [
+    ([0, 1], [0, 0]),            # n + 1 offsets expected, n = 2
+    ([0, 2, 1], [1, 0]),         # decreasing offsets
+    ([1, 1, 2], [1, 0]),         # offsets do not start at 0
+    ([0, 1, 5], [1, 0]),         # offsets past the column array
+])
+def test_rcm_rejects_malformed_lists(gpu_lib, rp, ci):
+    """A malformed CSR is InvalidArgument ('adjacency list count != n' in the
+    reference), never an out-of-bounds read."""
+    with pytest.raises(capi.LoamError) as e:
+        L.rcm_order(2, np.asarray(rp, np.int64), np.asarray(ci, np.int32))
+    assert e.value.kind == "InvalidArgument"
+    # the context is still usable
+    assert np.array_equal(dev_rcm([[1], [0]]), O.rcm_order([[1], [0]]))
