@@ -9,7 +9,11 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <exception>
+#include <thread>
+#include <vector>
 #include <cstdint>
 #include <cstdio>
 #include <memory>
@@ -117,6 +121,46 @@ inline void plan_tick(const char* label, cudaStream_t s) {
   const auto now = std::chrono::steady_clock::now();
   std::fprintf(stderr, "[plan] %-28s %9.3f ms\n", label, std::chrono::duration<double, std::milli>(now - last).count());
   last = now;
+}
+
+// Host-side plan construction runs on all host cores: parallel_chunks(n, f)
+// splits [0, n) into contiguous chunks (at most one per thread, `align`-sized
+// multiples) and calls f(chunk, begin, end) concurrently; the first exception
+// is rethrown after every thread joined.  LOAM_GPU_PLAN_THREADS overrides the
+// thread count (1 = serial).
+inline int plan_threads() {
+  static const int t = [] {
+    const char* e = std::getenv("LOAM_GPU_PLAN_THREADS");
+    int v = e ? std::atoi(e) : (int)std::thread::hardware_concurrency();
+    return std::max(1, std::min(v, 64));
+  }();
+  return t;
+}
+template <class F>
+int parallel_chunks(int64_t n, int64_t align, F&& f, int64_t min_chunk = 4096) {
+  const int64_t units = (n + align - 1) / align;
+  int T = (int)std::max<int64_t>(1, std::min<int64_t>(plan_threads(), (n + min_chunk - 1) / min_chunk));
+  T = (int)std::max<int64_t>(1, std::min<int64_t>(T, units));
+  std::vector<int64_t> cut(T + 1);
+  for (int t = 0; t <= T; ++t) cut[t] = std::min<int64_t>(n, (units * t / T) * align);
+  if (T == 1) {
+    f(0, (int64_t)0, n);
+    return 1;
+  }
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(T);
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      try {
+        f(t, cut[t], cut[t + 1]);
+      } catch (...) {
+        err[t] = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+  return T;
 }
 
 } // namespace loam_gpu

@@ -80,6 +80,7 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
   LG_CUDA(cudaMemcpyAsync(hrank.data(), pp.ranks.get(), hrank.size(), cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaMemcpyAsync(hrp.data(), row_ptr, sizeof(int64_t) * hrp.size(), cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaStreamSynchronize(s));
+  plan_tick("etile: D2H", s);
   // node-level pattern offsets (a cd x cd component-blocked CSR: node row i owns
   // dof rows cd*i .. cd*i+cd-1, each cd * L_i long)
   if (cd > 1) {
@@ -135,6 +136,7 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       if (hpairs[p] / nrn == c) return p;
     return -1;
   };
+  plan_tick("etile: roles + edge keys", s);
   // ---- vertex diagonals
   std::vector<int32_t> dpos(E0, -1), diag;
   for (int v = 0; v < E0; ++v)
@@ -167,62 +169,91 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       ktab[k * 2 + sw] = w;
     }
   // ---- per edge row: transposed positions, vertex-pair positions, records
+  // (rows are independent: chunks of rows on all host cores, the variable-
+  // length transposed-position lists concatenated in row order afterwards)
   const int rb = (2 + nrn + 3) & ~3;
   const int64_t p0e = hp[E0], npe = hp[nrows_node] - p0e;
   std::vector<int32_t> tptr(nedge + 1, 0), tpos, tlen, cellof(npe);
   std::vector<int4> xpos(nedge);
   std::vector<int2> xlen(cd == 2 ? nedge : 0);
   std::vector<uint8_t> recs((size_t)npe * rb, 0);
-  std::vector<std::pair<int, int>> vc; // (vertex node, cell carrying it)
-  for (int e = 0; e < nedge; ++e) {
-    const int r = E0 + e, A = eA[e], B = eB[e];
-    vc.clear();
-    for (int p = hp[r]; p < hp[r + 1]; ++p) {
-      const int c = hpairs[p] / nrn;
-      for (int v = 0; v < nv; ++v) vc.emplace_back(hrows[(size_t)c * nrn + v], c);
+  struct RecChunk {
+    int64_t eb = 0, ee = 0;
+    bool ok = true;
+    std::vector<int32_t> tpos, tlen, cnt;
+  };
+  std::vector<RecChunk> rch(plan_threads());
+  const int nrch = parallel_chunks(nedge, 1, [&](int t, int64_t eb, int64_t ee) {
+    RecChunk& C = rch[t];
+    C.eb = eb;
+    C.ee = ee;
+    C.cnt.assign(ee - eb, 0);
+    std::vector<std::pair<int, int>> vc; // (vertex node, cell carrying it)
+    for (int64_t e = eb; e < ee; ++e) {
+      const int r = E0 + (int)e, A = eA[e], B = eB[e];
+      vc.clear();
+      for (int p = hp[r]; p < hp[r + 1]; ++p) {
+        const int c = hpairs[p] / nrn;
+        for (int v = 0; v < nv; ++v) vc.emplace_back(hrows[(size_t)c * nrn + v], c);
+      }
+      std::sort(vc.begin(), vc.end());
+      int last = -1;
+      for (auto& x : vc) {
+        if (x.first == last) continue;
+        last = x.first;
+        const int c = x.second;
+        const int k = [&] {
+          for (int p = hp[r]; p < hp[r + 1]; ++p)
+            if (hpairs[p] / nrn == c) return hpairs[p] % nrn;
+          return -1;
+        }();
+        const int64_t pw = find_pair(x.first, c);
+        if (pw < 0 || k < 0) {
+          C.ok = false;
+          return;
+        }
+        C.tpos.push_back(vpos(x.first, hrank[(size_t)pw * nrn + k]));
+        if (cd == 2) C.tlen.push_back(vlen(x.first));
+        ++C.cnt[e - eb];
+      }
+      {
+        const int p = hp[r], c = hpairs[p] / nrn, k = hpairs[p] % nrn - nv;
+        const int la = E[k][0], lb = E[k][1];
+        const int lA = hrows[(size_t)c * nrn + la] == A ? la : lb, lB = lA == la ? lb : la;
+        const int64_t pA = find_pair(A, c), pB = find_pair(B, c);
+        if (pA < 0 || pB < 0) {
+          C.ok = false;
+          return;
+        }
+        xpos[e] = make_int4(vpos(A, hrank[(size_t)pA * nrn + lB]), vpos(B, hrank[(size_t)pB * nrn + lA]), dpos[A],
+                            dpos[B]);
+        if (cd == 2) xlen[e] = make_int2(vlen(A), vlen(B));
+      }
+      for (int p = hp[r]; p < hp[r + 1]; ++p) {
+        const int c = hpairs[p] / nrn, k = hpairs[p] % nrn - nv;
+        const int swap = hrows[(size_t)c * nrn + E[k][0]] != A ? 1 : 0;
+        int sig[4];
+        sigma_of(k, swap, sig);
+        const int fA = assigned(sig[ca]) == k, fB = assigned(sig[cb]) == k;
+        uint8_t* rec = &recs[(size_t)(p - p0e) * rb];
+        const uint16_t h = (uint16_t)(((k * 2 + swap) << 10) | (fA << 14) | (fB << 15));
+        memcpy(rec, &h, 2);
+        const uint8_t* rk = &hrank[(size_t)p * nrn];
+        for (int m = 0; m < nv; ++m) rec[2 + m] = rk[sig[m]];
+        for (int f = 0; f < ne; ++f) rec[2 + nv + f] = rk[nv + edge_index(gd, sig[E[f][0]], sig[E[f][1]])];
+        cellof[p - p0e] = c;
+      }
     }
-    std::sort(vc.begin(), vc.end());
-    int last = -1;
-    for (auto& x : vc) {
-      if (x.first == last) continue;
-      last = x.first;
-      const int c = x.second;
-      const int k = [&] {
-        for (int p = hp[r]; p < hp[r + 1]; ++p)
-          if (hpairs[p] / nrn == c) return hpairs[p] % nrn;
-        return -1;
-      }();
-      const int64_t pw = find_pair(x.first, c);
-      if (pw < 0 || k < 0) return false;
-      tpos.push_back(vpos(x.first, hrank[(size_t)pw * nrn + k]));
-      if (cd == 2) tlen.push_back(vlen(x.first));
-    }
-    tptr[e + 1] = (int32_t)tpos.size();
-    {
-      const int p = hp[r], c = hpairs[p] / nrn, k = hpairs[p] % nrn - nv;
-      const int la = E[k][0], lb = E[k][1];
-      const int lA = hrows[(size_t)c * nrn + la] == A ? la : lb, lB = lA == la ? lb : la;
-      const int64_t pA = find_pair(A, c), pB = find_pair(B, c);
-      if (pA < 0 || pB < 0) return false;
-      xpos[e] = make_int4(vpos(A, hrank[(size_t)pA * nrn + lB]), vpos(B, hrank[(size_t)pB * nrn + lA]), dpos[A],
-                          dpos[B]);
-      if (cd == 2) xlen[e] = make_int2(vlen(A), vlen(B));
-    }
-    for (int p = hp[r]; p < hp[r + 1]; ++p) {
-      const int c = hpairs[p] / nrn, k = hpairs[p] % nrn - nv;
-      const int swap = hrows[(size_t)c * nrn + E[k][0]] != A ? 1 : 0;
-      int sig[4];
-      sigma_of(k, swap, sig);
-      const int fA = assigned(sig[ca]) == k, fB = assigned(sig[cb]) == k;
-      uint8_t* rec = &recs[(size_t)(p - p0e) * rb];
-      const uint16_t h = (uint16_t)(((k * 2 + swap) << 10) | (fA << 14) | (fB << 15));
-      memcpy(rec, &h, 2);
-      const uint8_t* rk = &hrank[(size_t)p * nrn];
-      for (int m = 0; m < nv; ++m) rec[2 + m] = rk[sig[m]];
-      for (int f = 0; f < ne; ++f) rec[2 + nv + f] = rk[nv + edge_index(gd, sig[E[f][0]], sig[E[f][1]])];
-      cellof[p - p0e] = c;
-    }
+  });
+  for (int t = 0; t < nrch; ++t) {
+    const RecChunk& C = rch[t];
+    if (!C.ok) return false;
+    for (int64_t e = C.eb; e < C.ee; ++e) tptr[e + 1] = tptr[e] + C.cnt[e - C.eb];
+    tpos.insert(tpos.end(), C.tpos.begin(), C.tpos.end());
+    tlen.insert(tlen.end(), C.tlen.begin(), C.tlen.end());
   }
+  rch.clear();
+  plan_tick("etile: per-row records", s);
   // ---- compact records: with every edge row at most 32 entries long, a rank
   // fits in 5 bits; the ranks of the row's own edge and of its two endpoint
   // vertices (canonical columns ca, cb, nv) are the same for every pair of the
@@ -256,15 +287,27 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
   // base + 32 j + r: conflict-free shared updates) and so are the pair
   // records (word q of pair p of lane r at base + 32 (p RBW + q) + r).  Lanes
   // take the tile's rows in order of their pair count, so a warp's rows have
-  // equal loop lengths and record padding.
-  std::vector<int32_t> tiles, runs;
-  std::vector<uint8_t> blob;
-  std::vector<int> stamp(ncells, -1), local(ncells, 0), vid;
-  std::vector<std::pair<int, int>> rr;
-  int gen = 0, r0 = 0;
+  // equal loop lengths and record padding.  Chunks of whole tile-row blocks
+  // are tiled on all host cores and concatenated (blob / run offsets shifted).
   const int trows = sp.tile_rows <= 64 ? 64 : 128, nwarps = trows / 32, rbw = rbx / 4;
-  std::vector<int> lrow; // lane -> tile row
   const int cell_cap = std::min(sp.tile_cells, 1023);
+  struct TileChunk {
+    bool ok = true;
+    std::vector<int32_t> tiles, runs;
+    std::vector<uint8_t> blob;
+    int max_segT = 0, max_rows = 0, max_seg = 0, max_cells = 0, max_slots = 0, max_blob = 0;
+  };
+  std::vector<TileChunk> tch(plan_threads());
+  const int ntch = parallel_chunks(nedge, trows, [&](int t, int64_t cb0, int64_t cb1) {
+  TileChunk& O = tch[t];
+  std::vector<int32_t>& tiles = O.tiles;
+  std::vector<int32_t>& runs = O.runs;
+  std::vector<uint8_t>& blob = O.blob;
+  std::vector<int> vid; // (no per-thread ncells-sized arrays: cell sets are sorted vectors)
+  std::vector<std::pair<int, int>> rr;
+  int r0 = (int)cb0;
+  const int rend = (int)cb1;
+  std::vector<int> lrow; // lane -> tile row
   auto warp_sizes = [&](int a, int b, std::vector<int>& lmax, std::vector<int>& pmax) {
     lmax.assign(nwarps, 0);
     pmax.assign(nwarps, 0);
@@ -283,8 +326,8 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
     return st;
   };
   std::vector<int> lmax, pmax;
-  while (r0 < nedge) {
-    int r1 = std::min(nedge, r0 + trows);
+  while (r0 < rend) {
+    int r1 = std::min(rend, r0 + trows);
     std::vector<int> cells;
     int slots = 0;
     auto fits = [&](int a, int b) {
@@ -293,15 +336,10 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       if (hp[E0 + b] - hp[E0 + a] > sp.tile_pairs) return false;
       for (int r = a; r < b; ++r)
         if (hp[E0 + r + 1] - hp[E0 + r] > 255) return false;
-      ++gen;
       cells.clear();
-      for (int p = hp[E0 + a]; p < hp[E0 + b]; ++p) {
-        const int c = cellof[p - p0e];
-        if (stamp[c] != gen) {
-          stamp[c] = gen;
-          cells.push_back(c);
-        }
-      }
+      for (int p = hp[E0 + a]; p < hp[E0 + b]; ++p) cells.push_back(cellof[p - p0e]);
+      std::sort(cells.begin(), cells.end());
+      cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
       if ((int)cells.size() > cell_cap) return false;
       vid.clear();
       for (int c : cells)
@@ -310,12 +348,15 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       return slots <= sp.tile_slots && (int)rr.size() <= sp.tile_runs;
     };
     while (!fits(r0, r1)) {
-      if (r1 == r0 + 1) return false;
+      if (r1 == r0 + 1) {
+        O.ok = false;
+        return;
+      }
       r1 = r0 + (r1 - r0) / 2;
     }
     const int segT = warp_sizes(r0, r1, lmax, pmax);
     std::sort(cells.begin(), cells.end());
-    for (size_t q = 0; q < cells.size(); ++q) local[cells[q]] = (int)q;
+    auto local_of = [&](int c) { return (int)(std::lower_bound(cells.begin(), cells.end(), c) - cells.begin()); };
     std::vector<int> base(rr.size());
     for (size_t q = 0, acc = 0; q < rr.size(); ++q) {
       base[q] = (int)acc;
@@ -360,7 +401,7 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
             memcpy(full_rec, &recs[(size_t)pe * rb], rb);
             uint16_t h;
             memcpy(&h, full_rec, 2);
-            h = (uint16_t)(h | local[cellof[pe]]);
+            h = (uint16_t)(h | local_of(cellof[pe]));
             memcpy(full_rec, &h, 2);
             pack(full_rec, rec);
             const int pi = p - hp[E0 + r];
@@ -387,15 +428,38 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
     tiles.insert(tiles.end(), {(int)(b0 / 16), bytes, r0, nrows, (int)(cd * cd * hrp[E0 + r0]), seg, segT, ncell,
                                (int)runs.size() / 2, (int)rr.size(), off_srow, off_np, off_recs, off_cells, off_trow,
                                off_xpos});
-    out.max_segT = std::max(out.max_segT, segT);
+    O.max_segT = std::max(O.max_segT, segT);
     for (auto& x : rr) runs.insert(runs.end(), {x.first, x.second});
-    out.max_rows = std::max(out.max_rows, nrows);
-    out.max_seg = std::max(out.max_seg, seg);
-    out.max_cells = std::max(out.max_cells, ncell);
-    out.max_slots = std::max(out.max_slots, slots);
-    out.max_blob = std::max(out.max_blob, bytes);
+    O.max_rows = std::max(O.max_rows, nrows);
+    O.max_seg = std::max(O.max_seg, seg);
+    O.max_cells = std::max(O.max_cells, ncell);
+    O.max_slots = std::max(O.max_slots, slots);
+    O.max_blob = std::max(O.max_blob, bytes);
     r0 = r1;
   }
+  });
+  std::vector<int32_t> tiles, runs;
+  std::vector<uint8_t> blob;
+  for (int t = 0; t < ntch; ++t) {
+    TileChunk& O = tch[t];
+    if (!O.ok) return false;
+    const int bshift = (int)(blob.size() / 16), rshift = (int)(runs.size() / 2);
+    for (size_t q = 0; q < O.tiles.size(); q += 16) {
+      O.tiles[q + 0] += bshift;
+      O.tiles[q + 8] += rshift;
+    }
+    tiles.insert(tiles.end(), O.tiles.begin(), O.tiles.end());
+    runs.insert(runs.end(), O.runs.begin(), O.runs.end());
+    blob.insert(blob.end(), O.blob.begin(), O.blob.end());
+    out.max_segT = std::max(out.max_segT, O.max_segT);
+    out.max_rows = std::max(out.max_rows, O.max_rows);
+    out.max_seg = std::max(out.max_seg, O.max_seg);
+    out.max_cells = std::max(out.max_cells, O.max_cells);
+    out.max_slots = std::max(out.max_slots, O.max_slots);
+    out.max_blob = std::max(out.max_blob, O.max_blob);
+  }
+  tch.clear();
+  plan_tick("etile: tiles", s);
   out.gd = gd;
   out.cd = cd;
   out.tile_threads = trows;

@@ -63,6 +63,7 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
   LG_CUDA(cudaMemcpyAsync(hrank.data(), pp.ranks.get(), hrank.size(), cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaMemcpyAsync(hrp.data(), row_ptr, sizeof(int64_t) * hrp.size(), cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaStreamSynchronize(s));
+  plan_tick("ntile: D2H", s);
   std::vector<int64_t> nptr(nnodes + 1); // node-level pattern offsets of the 3x3-blocked CSR
   for (int i = 0; i <= nnodes; ++i) nptr[i] = hrp[(size_t)3 * i] / 9;
   // every pattern block of every row must be reached by some cell (exact (map, map) pattern)
@@ -81,22 +82,36 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
         if (!seen[r]) return false;
     }
   }
+  plan_tick("ntile: exact-pattern check", s);
   struct ItemRec { // 8 bytes
     uint16_t poff;
     uint8_t np, kind;
     uint16_t base, stride;
   };
   static_assert(sizeof(ItemRec) == 8, "item record");
-  std::vector<int32_t> tiles, runs;
-  std::vector<uint8_t> blob;
-  std::vector<int> stamp(ncells, -1), local(ncells, 0), vid;
+  // tiles of consecutive node rows: chunks of rows tiled on all host cores and
+  // concatenated (blob / run offsets shifted)
+  struct TileChunk {
+    bool ok = true;
+    std::vector<int32_t> tiles, runs;
+    std::vector<uint8_t> blob;
+    int max_seg = 0, max_cells = 0, max_slots = 0, max_blob = 0, max_diag = 0;
+  };
+  std::vector<TileChunk> tch(plan_threads());
+  const int ntch = parallel_chunks(nnodes, sp.tile_nodes, [&](int t, int64_t cb0, int64_t cb1) {
+  TileChunk& O = tch[t];
+  std::vector<int32_t>& tiles = O.tiles;
+  std::vector<int32_t>& runs = O.runs;
+  std::vector<uint8_t>& blob = O.blob;
+  std::vector<int> vid; // (no per-thread ncells-sized arrays: cell sets are sorted vectors)
   std::vector<std::pair<int, int>> rr;
   std::vector<std::vector<uint32_t>> lists; // per rank of a row: (cell << 4 | lv << 2 | lw)
   std::vector<ItemRec> items;
   std::vector<uint16_t> prec, diaginfo;
-  int gen = 0, v0 = 0;
-  while (v0 < nnodes) {
-    int v1 = std::min(nnodes, v0 + sp.tile_nodes);
+  const int vend = (int)cb1;
+  int v0 = (int)cb0;
+  while (v0 < vend) {
+    int v1 = std::min(vend, v0 + sp.tile_nodes);
     std::vector<int> cells;
     int slots = 0;
     auto fits = [&](int a, int b) {
@@ -107,15 +122,10 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
         npr += 4 * (hp[v + 1] - hp[v]);
       }
       if (nit > sp.tile_items || npr > sp.tile_pairs) return false;
-      ++gen;
       cells.clear();
-      for (int p = hp[a]; p < hp[b]; ++p) {
-        const int c = hpairs[p] / kNV;
-        if (stamp[c] != gen) {
-          stamp[c] = gen;
-          cells.push_back(c);
-        }
-      }
+      for (int p = hp[a]; p < hp[b]; ++p) cells.push_back(hpairs[p] / kNV);
+      std::sort(cells.begin(), cells.end());
+      cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
       if ((int)cells.size() > std::min(sp.tile_cells, 1023)) return false;
       vid.clear();
       for (int c : cells)
@@ -124,11 +134,11 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
       return slots <= sp.tile_slots && (int)rr.size() <= sp.tile_runs;
     };
     while (!fits(v0, v1)) {
-      if (v1 == v0 + 1) return false;
+      if (v1 == v0 + 1) { O.ok = false; return; }
       v1 = v0 + (v1 - v0) / 2;
     }
     std::sort(cells.begin(), cells.end());
-    for (size_t q = 0; q < cells.size(); ++q) local[cells[q]] = (int)q;
+    auto local_of = [&](int c) { return (int)(std::lower_bound(cells.begin(), cells.end(), c) - cells.begin()); };
     std::vector<int> base(rr.size());
     for (size_t q = 0, acc = 0; q < rr.size(); ++q) {
       base[q] = (int)acc;
@@ -153,7 +163,7 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
         const int c = hpairs[p] / kNV, lv = hpairs[p] % kNV;
         for (int lw = 0; lw < kNV; ++lw) {
           const int r = hrank[(size_t)p * kNV + lw];
-          lists[r].push_back((uint32_t)local[c] << 4 | (uint32_t)lv << 2 | (uint32_t)lw);
+          lists[r].push_back((uint32_t)local_of(c) << 4 | (uint32_t)lv << 2 | (uint32_t)lw);
           if (lw == lv) self = r;
         }
       }
@@ -162,7 +172,7 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
         if (r == self) continue;
         items.push_back(ItemRec{(uint16_t)prec.size(), (uint8_t)lists[r].size(), 0, (uint16_t)(rowb + 3 * r), stride});
         for (uint32_t x : lists[r]) prec.push_back((uint16_t)x);
-        if (lists[r].size() > 255) return false;
+        if (lists[r].size() > 255) { O.ok = false; return; }
       }
       const int di = (int)diaginfo.size() / 2;
       diaginfo.push_back((uint16_t)(rowb + 3 * self));
@@ -198,7 +208,7 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
         for (size_t i = r0i; i < r1i; ++i) {
           const int l = (int)(i - r0i);
           for (int q = 0; q < items[i].np; ++q) inter[blk + (size_t)q * kNtConsumers + l] = prec[items[i].poff + q];
-          if (blk + l > 65535) return false;
+          if (blk + l > 65535) { O.ok = false; return; }
           items[i].poff = (uint16_t)(blk + l);
         }
       }
@@ -224,13 +234,35 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
                                (int)runs.size() / 2, (int)rr.size(), off_items, off_pairs, off_cells, off_diag, ndiag,
                                0});
     for (auto& x : rr) runs.insert(runs.end(), {x.first, x.second});
-    out.max_seg = std::max(out.max_seg, seg);
-    out.max_cells = std::max(out.max_cells, ncell);
-    out.max_slots = std::max(out.max_slots, slots);
-    out.max_blob = std::max(out.max_blob, bytes);
-    out.max_diag = std::max(out.max_diag, ndiag);
+    O.max_seg = std::max(O.max_seg, seg);
+    O.max_cells = std::max(O.max_cells, ncell);
+    O.max_slots = std::max(O.max_slots, slots);
+    O.max_blob = std::max(O.max_blob, bytes);
+    O.max_diag = std::max(O.max_diag, ndiag);
     v0 = v1;
   }
+  });
+  std::vector<int32_t> tiles, runs;
+  std::vector<uint8_t> blob;
+  for (int t = 0; t < ntch; ++t) {
+    TileChunk& O = tch[t];
+    if (!O.ok) return false;
+    const int bshift = (int)(blob.size() / 16), rshift = (int)(runs.size() / 2);
+    for (size_t q = 0; q < O.tiles.size(); q += 16) {
+      O.tiles[q + 0] += bshift;
+      O.tiles[q + 8] += rshift;
+    }
+    tiles.insert(tiles.end(), O.tiles.begin(), O.tiles.end());
+    runs.insert(runs.end(), O.runs.begin(), O.runs.end());
+    blob.insert(blob.end(), O.blob.begin(), O.blob.end());
+    out.max_seg = std::max(out.max_seg, O.max_seg);
+    out.max_cells = std::max(out.max_cells, O.max_cells);
+    out.max_slots = std::max(out.max_slots, O.max_slots);
+    out.max_blob = std::max(out.max_blob, O.max_blob);
+    out.max_diag = std::max(out.max_diag, O.max_diag);
+  }
+  tch.clear();
+  plan_tick("ntile: tiles", s);
   out.ntiles = (int)tiles.size() / 16;
   auto upload = [&](auto& dst, const auto& src) {
     using T = typename std::decay_t<decltype(src)>::value_type;

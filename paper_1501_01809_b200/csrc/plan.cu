@@ -1,3 +1,4 @@
+#include <atomic>
 // plan.cu -- device-side plan construction (see plan.cuh).
 #include <cub/cub.cuh>
 
@@ -349,13 +350,25 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
   const int64_t w = (int64_t)node.rd * node.cd;
   const int nv = nrows_node; // P1: row nodes are the coordinate vertices
   constexpr int kGap = 8;    // merge runs separated by <= kGap unused vertices
-  std::vector<int32_t> tiles, runs;
   std::vector<uint16_t> hw(nn + 8, 0);
   std::vector<uint8_t> hs(nrows_node + 16, 0);
+  // chunks of whole tile-row blocks tiled on all host cores (window slots and
+  // self ranks written in place; tiles concatenated, run offsets shifted)
+  struct TileChunk {
+    bool ok = true, has_empty_row = false;
+    std::vector<int32_t> tiles, runs;
+    std::vector<std::pair<int, int>> tile_of_rows;
+    int max_rows = 0, max_adj = 0, max_pairs = 0, max_seg = 0, max_slots = 0, max_runs = 0;
+  };
+  std::vector<TileChunk> tch(plan_threads());
+  const int ntch = parallel_chunks(nrows_node, tile_rows, [&](int t, int64_t cb0, int64_t cb1) {
+  TileChunk& O = tch[t];
+  std::vector<int32_t>& tiles = O.tiles;
+  std::vector<int32_t>& runs = O.runs;
+  std::vector<std::pair<int, int>>& tile_of_rows = O.tile_of_rows;
+  bool& has_empty_row = O.has_empty_row;
   std::vector<int32_t> verts;
   std::vector<std::pair<int, int>> rr;
-  std::vector<std::pair<int, int>> tile_of_rows;
-  bool has_empty_row = false;
   auto make_runs = [&](int r0, int r1) { // runs of the tile's vertices; returns slot count
     verts.assign(hadj.begin() + h[r0], hadj.begin() + h[r1]);
     std::sort(verts.begin(), verts.end());
@@ -370,17 +383,20 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
     for (auto& x : rr) slots += x.second - x.first;
     return slots;
   };
-  int r0 = 0;
-  while (r0 < nrows_node) {
-    int r1 = std::min(nrows_node, r0 + tile_rows);
+  int r0 = (int)cb0;
+  const int rend = (int)cb1;
+  while (r0 < rend) {
+    int r1 = std::min(rend, r0 + tile_rows);
     while (r1 > r0 + 1 && (int64_t)(h[r1] - h[r0]) * w > tile_seg) --r1;
     int slots = make_runs(r0, r1);
     while (r1 > r0 + 1 && (slots > tile_slots || (int)rr.size() > tile_runs)) {
       r1 = r0 + (r1 - r0) / 2;
       slots = make_runs(r0, r1);
     }
-    if (slots > tile_slots || (int)rr.size() > tile_runs || (int64_t)(h[r1] - h[r0]) * w > tile_seg)
-      return false; // a single row does not fit: use the pair-list path
+    if (slots > tile_slots || (int)rr.size() > tile_runs || (int64_t)(h[r1] - h[r0]) * w > tile_seg) {
+      O.ok = false; // a single row does not fit: use the pair-list path
+      return;
+    }
     // window slots: run k occupies [base_k, base_k + hi - lo)
     std::vector<int> base(rr.size());
     int acc = 0;
@@ -406,14 +422,35 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
     }
     tiles.insert(tiles.end(), {r0, r1, h[r0], h[r1], hp[r0], hp[r1], (int)runs.size() / 2, (int)rr.size()});
     for (auto& x : rr) runs.insert(runs.end(), {x.first, x.second});
-    np.max_rows = std::max(np.max_rows, r1 - r0);
-    np.max_adj = std::max(np.max_adj, h[r1] - h[r0]);
-    np.max_pairs = std::max(np.max_pairs, hp[r1] - hp[r0]);
-    np.max_seg = std::max<int>(np.max_seg, (int)((h[r1] - h[r0]) * w));
-    np.max_slots = std::max(np.max_slots, slots);
-    np.max_runs = std::max(np.max_runs, (int)rr.size());
+    O.max_rows = std::max(O.max_rows, r1 - r0);
+    O.max_adj = std::max(O.max_adj, h[r1] - h[r0]);
+    O.max_pairs = std::max(O.max_pairs, hp[r1] - hp[r0]);
+    O.max_seg = std::max<int>(O.max_seg, (int)((h[r1] - h[r0]) * w));
+    O.max_slots = std::max(O.max_slots, slots);
+    O.max_runs = std::max(O.max_runs, (int)rr.size());
     r0 = r1;
   }
+  });
+  std::vector<int32_t> tiles, runs;
+  std::vector<std::pair<int, int>> tile_of_rows;
+  bool has_empty_row = false;
+  for (int t = 0; t < ntch; ++t) {
+    TileChunk& O = tch[t];
+    if (!O.ok) return false;
+    const int rshift = (int)(runs.size() / 2);
+    for (size_t q = 0; q < O.tiles.size(); q += 8) O.tiles[q + 6] += rshift;
+    tiles.insert(tiles.end(), O.tiles.begin(), O.tiles.end());
+    runs.insert(runs.end(), O.runs.begin(), O.runs.end());
+    tile_of_rows.insert(tile_of_rows.end(), O.tile_of_rows.begin(), O.tile_of_rows.end());
+    has_empty_row = has_empty_row || O.has_empty_row;
+    np.max_rows = std::max(np.max_rows, O.max_rows);
+    np.max_adj = std::max(np.max_adj, O.max_adj);
+    np.max_pairs = std::max(np.max_pairs, O.max_pairs);
+    np.max_seg = std::max(np.max_seg, O.max_seg);
+    np.max_slots = std::max(np.max_slots, O.max_slots);
+    np.max_runs = std::max(np.max_runs, O.max_runs);
+  }
+  tch.clear();
   plan_tick("nbr: host tiles", s);
   np.ntiles = (int)tiles.size() / 8;
   np.tiles.alloc(tiles.size() ? tiles.size() : 8, s);
@@ -434,12 +471,13 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
     for (int r = 0; r <= nrows_node; ++r) rptr[r] = hp[r] + r;
     std::vector<uint16_t> rrec((size_t)rptr[nrows_node] + 8, 0);
     std::vector<uint32_t> rinfo(nrows_node + 4, 0);
-    bool ok = true;
-    std::vector<int> av, bv;
-    std::vector<char> used;
-    for (size_t t = 0; t < tile_of_rows.size() && ok; ++t) {
-      const int tr0 = tile_of_rows[t].first, tr1 = tile_of_rows[t].second;
-      for (int r = tr0; r < tr1 && ok; ++r) {
+    // rows are independent: chunks of rows on all host cores
+    std::atomic<bool> all_ok{true};
+    parallel_chunks(nrows_node, 1, [&](int, int64_t rb0, int64_t rb1) {
+      bool ok = true;
+      std::vector<int> av, bv;
+      std::vector<char> used;
+      for (int r = (int)rb0; r < (int)rb1 && ok; ++r) {
         auto slot_of = [&](int v) { // window slot of vertex v in this row's tile
           for (int64_t a = h[r]; a < h[r + 1]; ++a)
             if (hadj[a] == v) return (int)hw[a];
@@ -488,8 +526,10 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
         }
         if (ok && ones == 0 && v != start) ok = false; // a ring must close
       }
-    }
-    if (ok) {
+      if (!ok) all_ok = false;
+    });
+    (void)tile_of_rows;
+    if (all_ok) {
       np.ring = true;
       np.rptr.alloc(rptr.size() + 4, s);
       np.rrecs.alloc(rrec.size(), s);
@@ -618,17 +658,30 @@ bool build_ptile(PTilePlan& out, const PTileSpec& sp, int ncells, int nrows_node
     for (auto& x : rr) slots += x.second - x.first;
     return slots;
   };
-  std::vector<int32_t> tiles, runs, cruns;
   std::vector<uint8_t> recs((size_t)np * rb + 64, 0);
-  std::vector<int> vid, cid;
-  std::vector<std::pair<int, int>> rr, cr;
   auto slot_in = [](const std::vector<std::pair<int, int>>& R, const std::vector<int>& base, int v) {
     size_t k = std::upper_bound(R.begin(), R.end(), std::make_pair(v, INT32_MAX)) - R.begin() - 1;
     return base[k] + v - R[k].first;
   };
-  int r0 = 0;
-  while (r0 < nrows_node) {
-    int r1 = std::min(nrows_node, r0 + sp.tile_rows);
+  // chunks of whole tile-row blocks tiled on all host cores (records are
+  // written in place; tiles concatenated with their run offsets shifted)
+  struct TileChunk {
+    bool ok = true;
+    std::vector<int32_t> tiles, runs, cruns;
+    int max_rows = 0, max_pairs = 0, max_seg = 0, max_slots = 0, max_cslots = 0;
+  };
+  std::vector<TileChunk> tch(plan_threads());
+  const int ntch = parallel_chunks(nrows_node, sp.tile_rows, [&](int t, int64_t cb0, int64_t cb1) {
+  TileChunk& O = tch[t];
+  std::vector<int32_t>& tiles = O.tiles;
+  std::vector<int32_t>& runs = O.runs;
+  std::vector<int32_t>& cruns = O.cruns;
+  std::vector<int> vid, cid;
+  std::vector<std::pair<int, int>> rr, cr;
+  int r0 = (int)cb0;
+  const int rend = (int)cb1;
+  while (r0 < rend) {
+    int r1 = std::min(rend, r0 + sp.tile_rows);
     auto fits = [&](int a, int b, int& slots, int& cslots) {
       if (ncn && (hn[b] - hn[a]) * W > sp.tile_seg) return false;
       if (hp[b] - hp[a] > sp.tile_pairs) return false;
@@ -646,7 +699,10 @@ bool build_ptile(PTilePlan& out, const PTileSpec& sp, int ncells, int nrows_node
     };
     int slots = 0, cslots = 0;
     while (!fits(r0, r1, slots, cslots)) {
-      if (r1 == r0 + 1) return false;
+      if (r1 == r0 + 1) {
+        O.ok = false;
+        return;
+      }
       r1 = r0 + (r1 - r0) / 2;
     }
     std::vector<int> base(rr.size()), cbase(cr.size());
@@ -692,13 +748,33 @@ bool build_ptile(PTilePlan& out, const PTileSpec& sp, int ncells, int nrows_node
                                (int)rr.size(), (int)cruns.size() / 2, (int)cr.size(), G, 0});
     for (auto& x : rr) runs.insert(runs.end(), {x.first, x.second});
     for (auto& x : cr) cruns.insert(cruns.end(), {x.first, x.second});
-    out.max_rows = std::max(out.max_rows, r1 - r0);
-    out.max_pairs = std::max(out.max_pairs, hp[r1] - hp[r0]);
-    out.max_seg = std::max<int>(out.max_seg, (int)((hn[r1] - hn[r0]) * W));
-    out.max_slots = std::max(out.max_slots, slots);
-    out.max_cslots = std::max(out.max_cslots, cslots);
+    O.max_rows = std::max(O.max_rows, r1 - r0);
+    O.max_pairs = std::max(O.max_pairs, hp[r1] - hp[r0]);
+    O.max_seg = std::max<int>(O.max_seg, (int)((hn[r1] - hn[r0]) * W));
+    O.max_slots = std::max(O.max_slots, slots);
+    O.max_cslots = std::max(O.max_cslots, cslots);
     r0 = r1;
   }
+  });
+  std::vector<int32_t> tiles, runs, cruns;
+  for (int t = 0; t < ntch; ++t) {
+    TileChunk& O = tch[t];
+    if (!O.ok) return false;
+    const int rshift = (int)(runs.size() / 2), cshift = (int)(cruns.size() / 2);
+    for (size_t q = 0; q < O.tiles.size(); q += 12) {
+      O.tiles[q + 6] += rshift;
+      O.tiles[q + 8] += cshift;
+    }
+    tiles.insert(tiles.end(), O.tiles.begin(), O.tiles.end());
+    runs.insert(runs.end(), O.runs.begin(), O.runs.end());
+    cruns.insert(cruns.end(), O.cruns.begin(), O.cruns.end());
+    out.max_rows = std::max(out.max_rows, O.max_rows);
+    out.max_pairs = std::max(out.max_pairs, O.max_pairs);
+    out.max_seg = std::max(out.max_seg, O.max_seg);
+    out.max_slots = std::max(out.max_slots, O.max_slots);
+    out.max_cslots = std::max(out.max_cslots, O.max_cslots);
+  }
+  tch.clear();
   out.ntiles = (int)tiles.size() / 12;
   std::vector<int32_t> pp32(hp.begin(), hp.end()), nn32(hn.begin(), hn.end());
   pp32.resize(pp32.size() + 8, 0);

@@ -90,11 +90,23 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
       }
     }
   // ---- tiles of consecutive row nodes
-  std::vector<int32_t> tiles, runs;
-  std::vector<uint8_t> blob;
-  std::vector<int> stamp(ncells, -1), local(ncells, 0), vid, lrow;
-  std::vector<std::pair<int, int>> rr;
   const int trows = sp.tile_rows <= 64 ? 64 : 128, nwarps = trows / 32, W = rd * cd;
+  // chunks of whole tile-row blocks tiled on all host cores, concatenated
+  // (blob / run offsets shifted)
+  struct TileChunk {
+    bool ok = true;
+    std::vector<int32_t> tiles, runs;
+    std::vector<uint8_t> blob;
+    int max_seg = 0, max_segT = 0, max_cells = 0, max_slots = 0, max_blob = 0;
+  };
+  std::vector<TileChunk> tch(plan_threads());
+  const int ntch = parallel_chunks(nrows_node, trows, [&](int t, int64_t cb0, int64_t cb1) {
+  TileChunk& O = tch[t];
+  std::vector<int32_t>& tiles = O.tiles;
+  std::vector<int32_t>& runs = O.runs;
+  std::vector<uint8_t>& blob = O.blob;
+  std::vector<int> vid, lrow;
+  std::vector<std::pair<int, int>> rr;
   std::vector<int> lmax, pmax;
   auto warp_sizes = [&](int a, int b) {
     lmax.assign(nwarps, 0);
@@ -112,9 +124,10 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
     for (int w = 0; w < nwarps; ++w) st += 32 * lmax[w] * W;
     return st;
   };
-  int gen = 0, r0 = 0;
-  while (r0 < nrows_node) {
-    int r1 = std::min(nrows_node, r0 + trows);
+  int r0 = (int)cb0;
+  const int rend = (int)cb1;
+  while (r0 < rend) {
+    int r1 = std::min(rend, r0 + trows);
     std::vector<int> cells;
     int slots = 0;
     auto fits = [&](int a, int b) {
@@ -122,15 +135,10 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
       if (hp[b] - hp[a] > sp.tile_pairs) return false;
       for (int r = a; r < b; ++r)
         if (hp[r + 1] - hp[r] > 255) return false;
-      ++gen;
       cells.clear();
-      for (int p = hp[a]; p < hp[b]; ++p) {
-        const int c = hpairs[p] / nrn;
-        if (stamp[c] != gen) {
-          stamp[c] = gen;
-          cells.push_back(c);
-        }
-      }
+      for (int p = hp[a]; p < hp[b]; ++p) cells.push_back(hpairs[p] / nrn);
+      std::sort(cells.begin(), cells.end());
+      cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
       if ((int)cells.size() > std::min(sp.tile_cells, 1023)) return false;
       vid.clear();
       for (int c : cells)
@@ -139,12 +147,15 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
       return slots <= sp.tile_slots && (int)rr.size() <= sp.tile_runs;
     };
     while (!fits(r0, r1)) {
-      if (r1 == r0 + 1) return false;
+      if (r1 == r0 + 1) {
+        O.ok = false;
+        return;
+      }
       r1 = r0 + (r1 - r0) / 2;
     }
     const int segT = warp_sizes(r0, r1);
     std::sort(cells.begin(), cells.end());
-    for (size_t q = 0; q < cells.size(); ++q) local[cells[q]] = (int)q;
+    auto local_of = [&](int c) { return (int)(std::lower_bound(cells.begin(), cells.end(), c) - cells.begin()); };
     std::vector<int> base(rr.size());
     for (size_t q = 0, acc = 0; q < rr.size(); ++q) {
       base[q] = (int)acc;
@@ -157,7 +168,10 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
     const int nrows = r1 - r0, ncell = (int)cells.size();
     int rwords = 0;
     for (int w = 0; w < nwarps; ++w) rwords += pmax[w] * rbw * 32;
-    if (rwords > 65535 || segT > 65535) return false;
+    if (rwords > 65535 || segT > 65535) {
+      O.ok = false;
+      return;
+    }
     const int off_srow = 0, off_np = up16((nrows + 1) * 2), off_recs = off_np + up16(2 * trows + 8 * nwarps),
               off_cells = off_recs + up16(rwords * 4), bytes = off_cells + up16(ncell * nv * 2);
     const size_t b0 = blob.size();
@@ -181,7 +195,7 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
             memcpy(rec, &recs[(size_t)p * rb], rb);
             uint32_t h;
             memcpy(&h, rec, 4);
-            h |= (uint32_t)local[hpairs[p] / nrn];
+            h |= (uint32_t)local_of(hpairs[p] / nrn);
             memcpy(rec, &h, 4);
             const int pi = p - hp[r];
             for (int q = 0; q < rbw; ++q)
@@ -201,13 +215,34 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
     tiles.insert(tiles.end(), {(int)(b0 / 16), bytes, r0, nrows, (int)(W * nptr[r0]), seg, segT, ncell,
                                (int)runs.size() / 2, (int)rr.size(), off_srow, off_np, off_recs, off_cells, 0, 0});
     for (auto& x : rr) runs.insert(runs.end(), {x.first, x.second});
-    out.max_seg = std::max(out.max_seg, seg);
-    out.max_segT = std::max(out.max_segT, segT);
-    out.max_cells = std::max(out.max_cells, ncell);
-    out.max_slots = std::max(out.max_slots, slots);
-    out.max_blob = std::max(out.max_blob, bytes);
+    O.max_seg = std::max(O.max_seg, seg);
+    O.max_segT = std::max(O.max_segT, segT);
+    O.max_cells = std::max(O.max_cells, ncell);
+    O.max_slots = std::max(O.max_slots, slots);
+    O.max_blob = std::max(O.max_blob, bytes);
     r0 = r1;
   }
+  });
+  std::vector<int32_t> tiles, runs;
+  std::vector<uint8_t> blob;
+  for (int t = 0; t < ntch; ++t) {
+    TileChunk& O = tch[t];
+    if (!O.ok) return false;
+    const int bshift = (int)(blob.size() / 16), rshift = (int)(runs.size() / 2);
+    for (size_t q = 0; q < O.tiles.size(); q += 16) {
+      O.tiles[q + 0] += bshift;
+      O.tiles[q + 8] += rshift;
+    }
+    tiles.insert(tiles.end(), O.tiles.begin(), O.tiles.end());
+    runs.insert(runs.end(), O.runs.begin(), O.runs.end());
+    blob.insert(blob.end(), O.blob.begin(), O.blob.end());
+    out.max_seg = std::max(out.max_seg, O.max_seg);
+    out.max_segT = std::max(out.max_segT, O.max_segT);
+    out.max_cells = std::max(out.max_cells, O.max_cells);
+    out.max_slots = std::max(out.max_slots, O.max_slots);
+    out.max_blob = std::max(out.max_blob, O.max_blob);
+  }
+  tch.clear();
   out.form = form;
   out.ntiles = (int)tiles.size() / 16;
   out.tile_threads = trows;
