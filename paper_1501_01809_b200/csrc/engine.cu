@@ -371,6 +371,7 @@ struct CellArgs {
   const int64_t* row_ptr; // (matrices) CSR dof-row offsets
   FormParams prm;
   double* out;
+  double* contrib; // deterministic mode: [n x NRN] element-vector entries, summed per row afterwards
 };
 
 template <bool AGG>
@@ -457,6 +458,12 @@ __global__ void __launch_bounds__(128) k_cell_vec_rows(const __grid_constant__ C
   geometry<GD>(X, G);
   double y[NRN];
   ElemVec<F>::all(G, C, a.prm, y);
+  if (a.contrib) { // deterministic mode: entries in place, summed per row in a fixed order
+    double* dst = a.contrib + (c0 + lane) * NRN;
+#pragma unroll
+    for (int i = 0; i < NRN; ++i) dst[i] = y[i];
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < NRN; ++i) atomicAdd(a.out + nodes[i], y[i]);
 }
@@ -474,8 +481,25 @@ __global__ void __launch_bounds__(128, LOAM_GPU_CELL_MINB) k_cell_vec(const __gr
   geometry<F::GD>(X, G);
   double y[F::NRN];
   ElemVec<F>::all(G, C, a.prm, y); // whole element vector (P2: through grad u_h)
+  if (!AGG && a.contrib) { // deterministic mode (see k_cell_vec_rows)
+#pragma unroll
+    for (int i = 0; i < F::NRN; ++i) a.contrib[(int64_t)e * F::NRN + i] = y[i];
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < F::NRN; ++i) red_add<AGG>(a.out, rows[i], y[i], valid);
+}
+
+// Deterministic mode's second pass: every row sums its (cell, local row)
+// entries in the pair plan's fixed order (cells ascending) -- bitwise the same
+// on every run, unlike fp64 REDs whose order varies.
+__global__ void k_pair_sum(const int32_t* __restrict__ ptr, const int32_t* __restrict__ pairs, int nrows,
+                           const double* __restrict__ contrib, double* __restrict__ out, int accumulate) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  double acc = 0.0;
+  for (int p = ptr[r]; p < ptr[r + 1]; ++p) acc += contrib[pairs[p]];
+  out[r] = accumulate ? out[r] + acc : acc;
 }
 
 template <class F, bool AGG>
@@ -2423,6 +2447,10 @@ bool map_covers_target(const MapView& m, cudaStream_t s) {
   return h == 0;
 }
 
+// The scatter strategy in effect: deterministic mode runs the auto paths only
+// (their RED-based pieces switch to fixed-order variants).
+int strategy() { return options().deterministic ? 0 : options().inc_strategy; }
+
 struct FastPlan {
   TileCounters counter; // dynamic tile scheduler of the persistent tile kernels
   bool exact = false;   // the loop's (row, col) pattern IS the Mat's pattern (provenance / checked)
@@ -2442,6 +2470,7 @@ struct FastPlan {
   bool use_patch = false;  // cell-patch row-owner kernels (patch.cuh)
   PatchPlan patch;
   bool use_cell = false;   // cell-centric atomic scatter
+  bool det_cell = false;   // deterministic mode: cell entries + fixed-order pair sums
   bool use_cseg = false;   // (actions, auto) warp-segmented reduction of the cell scatter
   DevBuf<uint16_t> cs_slots, cs_start;
   DevBuf<int32_t> cs_off, cs_node;
@@ -2493,7 +2522,7 @@ constexpr int kTileRuns = 32;    // contiguous runs per window
 // Strategy 6 selects the patch kernels; auto uses them for the forms they
 // win on (profiles/r01/strategies_patch*).
 bool patch_wanted(const Entry& k) {
-  const int strat = options().inc_strategy;
+  const int strat = strategy();
   if (strat == 6) return true;
   if (strat != 0 || std::getenv("LOAM_GPU_NO_PATCH")) return false;
   return std::getenv("LOAM_GPU_PATCH_AUTO") != nullptr && (k.nrn > k.gd + 1 || k.rd > 1);
@@ -2650,9 +2679,15 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       build_ranks(pp, srows.v.get(), sc, Cn.v.arity, csr, s); // OutsideSparsity / ShapeMismatch here
       cell_major_ranks(pp, P->cranks, s);
     }
+    // deterministic mode: the rows' (cell, local row) pair lists for the
+    // fixed-order second pass (k_pair_sum)
+    if (!k.bilinear && options().deterministic && R.dim == 1) {
+      build_pairs(srows.v.get(), n, R.v.arity, R.v.target, P->pp, s);
+      P->det_cell = true;
+    }
     // (measured slower than one RED per entry on config 3, 0.128 vs 0.081 ms: the
     // plain kernel is bound by its dependent gathers, not by the L2 atomics)
-    if (!k.bilinear && k.cell_seg && options().inc_strategy == 0 && std::getenv("LOAM_GPU_CSEG"))
+    if (!k.bilinear && k.cell_seg && strategy() == 0 && !options().deterministic && std::getenv("LOAM_GPU_CSEG"))
       build_cell_segments(srows.v.get(), n, R.v.arity, *P, s);
     P->crows = std::move(srows);
     gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, P->xmap, s);
@@ -2678,7 +2713,7 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
   }
   // Neighbour-list plan when row, column, coordinate (and coefficient) maps
   // are one node map (P1 forms): no per-pair cell ids or map rows at all.
-  const int strat = options().inc_strategy;
+  const int strat = strategy();
   if (k.nbr && (strat == 0 || strat == 4)) {
     auto same = [&](const MapView& m) {
       return m.arity == R.v.arity && (m.v == R.v.v || prefix_equal(m.v, m.arity, R.v.v, R.v.arity, m.arity, n, s));
@@ -2767,6 +2802,7 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       es.tile_rows = env_int("LOAM_GPU_ET_ROWS", es.tile_rows);
       es.tile_seg = env_int("LOAM_GPU_ET_SEG", es.tile_seg);
       es.tile_cells = env_int("LOAM_GPU_ET_CELLS", es.tile_cells);
+      es.det = options().deterministic != 0;
       if (build_etile(P->et, es, k.gd, n, R.v.target, srows.v.get(), sx.v.get(), X->target_size, P->pp,
                       sp->row_ptr, sp->nnz, k.rd, s)) {
         plan_tick("edge tiles", s);
@@ -2904,7 +2940,8 @@ thread_local std::shared_ptr<FastPlan>* g_plan_probe = nullptr;
 void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const FormParams& prm,
               cudaStream_t s, bool cell_mode = false) {
   std::vector<uint64_t> key{(uint64_t)k.form, (uint64_t)k.gd, (uint64_t)k.nrn, (uint64_t)k.ncn,
-                            (uint64_t)options().locality, (uint64_t)options().inc_strategy, (uint64_t)cell_mode};
+                            (uint64_t)options().locality, (uint64_t)strategy(), (uint64_t)cell_mode,
+                            (uint64_t)options().deterministic};
   bool cacheable = true;
   for (int q = 0; q < nargs; ++q) {
     const loam_arg_desc& a = args[q];
@@ -3001,6 +3038,17 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     c.coeff = k.has_coeff ? args[2].data : nullptr;
     c.prm = prm;
     c.out = args[0].data;
+    if (P->det_cell) { // deterministic: entries in place, then fixed-order row sums
+      DevBuf<double> contrib((size_t)n * k.nrn, s);
+      c.contrib = contrib.get();
+      k.cell(c, false, s);
+      const int nrows = P->pp.nrows_node;
+      k_pair_sum<<<ceil_div(nrows, 256), 256, 0, s>>>(P->pp.ptr.get(), P->pp.pairs.get(), nrows, contrib.get(),
+                                                      args[0].data, (args[0].flags & LOAM_ARG_ZERO) ? 0 : 1);
+      count_launch();
+      LG_LAUNCH_CHECK();
+      return;
+    }
     if (args[0].flags & LOAM_ARG_ZERO) {
       const size_t len = k.bilinear ? (size_t)args[0].sparsity->nnz : (size_t)args[0].set_size * args[0].dim;
       LG_CUDA(cudaMemsetAsync(args[0].data, 0, sizeof(double) * len, s));
@@ -3016,7 +3064,7 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
       k.cell_seg(g, s);
       return;
     }
-    k.cell(c, options().inc_strategy == 5, s);
+    k.cell(c, strategy() == 5, s);
     return;
   }
   if (P->use_nbr && P->nb.ring && k.ring && !std::getenv("LOAM_GPU_NO_RING")) {
@@ -3278,7 +3326,7 @@ void run_generic(const Entry& k, int n, uint64_t iter, const loam_arg_desc* args
   L.nargs = nargs;
   L.prm = prm;
   int off = 0, slot_stride = 0;
-  bool need_color = options().inc_strategy == 3;
+  bool need_color = options().inc_strategy == 3 || options().deterministic; // colouring: the reference's order
   std::vector<const loam_map_desc*> conflict;
   for (int q = 0; q < nargs; ++q) {
     const loam_arg_desc& a = args[q];
@@ -3410,7 +3458,10 @@ void execute(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_de
   validate_args(k, n, iter, args, nargs); // before any mutation (parloop.hpp:193)
   FormParams prm{{0, 0, 0, 0}};
   for (int i = 0; i < kd->nparams && i < 4; ++i) prm.p[i] = kd->params[i];
-  const int strat = options().inc_strategy;
+  // deterministic mode: the auto paths only (the atomic / warp-aggregated /
+  // patch strategies sum in a varying order); the RED-based pieces of auto run
+  // their fixed-order variants (cell entries + pair sums, edge-tile diagonals)
+  const int strat = strategy();
   // auto: P2 tetrahedral actions (C3 residual) are fastest with one fp64 RED
   // per element entry -- 10 rows per cell, each recomputed by its owner would
   // redo the cell geometry 10 times (profiles/r01/strategies_*: 0.34 vs 0.80 ms)
@@ -3446,7 +3497,7 @@ void wave_step(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_
   validate_args(k, n, iter, args, nargs);
   require(k.form == F_STIFFNESS_ACTION && k.gd == 2 && k.nrn == 3 && !k.bilinear && nargs == 3,
           LOAM_ERR(UnsupportedForm), "wave step: the action must be stiffness_action_p1_tri");
-  require(options().inc_strategy == 0 && fast_pattern(k, args, nargs), LOAM_ERR(UnsupportedForm),
+  require(strategy() == 0 && fast_pattern(k, args, nargs), LOAM_ERR(UnsupportedForm),
           "wave step: needs the auto strategy's vertex-star plan");
   std::shared_ptr<FastPlan> P;
   g_plan_probe = &P;

@@ -253,6 +253,35 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
     tlen.insert(tlen.end(), C.tlen.begin(), C.tlen.end());
   }
   rch.clear();
+  // deterministic diagonals: per diagonal (vertex order of `diag`), the slots
+  // 2 e + endpoint of the edge rows that carry a contribution, edge-ascending
+  std::vector<int32_t> dptr, dslots;
+  if (sp.det) {
+    std::vector<int32_t> didx(E0, -1);
+    int nd = 0;
+    for (int v = 0; v < E0; ++v)
+      if (hp[v + 1] > hp[v]) didx[v] = nd++;
+    std::vector<int32_t> cnt(nd + 1, 0);
+    std::vector<uint8_t> has(2 * (size_t)nedge, 0);
+    for (int e = 0; e < nedge; ++e)
+      for (int p = hp[E0 + e]; p < hp[E0 + e + 1]; ++p) {
+        uint16_t h;
+        memcpy(&h, &recs[(size_t)(p - p0e) * rb], 2);
+        has[2 * (size_t)e] |= (h >> 14) & 1;
+        has[2 * (size_t)e + 1] |= (h >> 15) & 1;
+      }
+    for (int e = 0; e < nedge; ++e) {
+      if (has[2 * (size_t)e]) ++cnt[didx[eA[e]] + 1];
+      if (has[2 * (size_t)e + 1]) ++cnt[didx[eB[e]] + 1];
+    }
+    for (int d = 0; d < nd; ++d) cnt[d + 1] += cnt[d];
+    dptr = cnt;
+    dslots.resize(cnt[nd]);
+    for (int e = 0; e < nedge; ++e) {
+      if (has[2 * (size_t)e]) dslots[cnt[didx[eA[e]]]++] = 2 * e;
+      if (has[2 * (size_t)e + 1]) dslots[cnt[didx[eB[e]]]++] = 2 * e + 1;
+    }
+  }
   plan_tick("etile: per-row records", s);
   // ---- compact records: with every edge row at most 32 entries long, a rank
   // fits in 5 bits; the ranks of the row's own edge and of its two endpoint
@@ -480,6 +509,11 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
   upload(out.blob, blob);
   upload(out.runs, runs);
   upload(out.diag, diag);
+  out.det = sp.det;
+  if (sp.det) {
+    upload(out.dptr, dptr);
+    upload(out.dslots, dslots);
+  }
   LG_CUDA(cudaStreamSynchronize(s));
   return true;
 }
@@ -503,6 +537,7 @@ struct EtileArgs {
   int accumulate, dynamic, dbg;
   int off_seg, off_geo, off_buf, buf_bytes, b_win;
   uint32_t ktab[12];
+  double* dsum; // deterministic mode: diagonal partial sums by (edge row, endpoint)
 };
 
 template <int D>
@@ -874,13 +909,19 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
       const int2 xl = CD == 2 ? xlen[row] : make_int2(0, 0);
       put(xp.x, xl.x, vab);
       put(xp.y, xl.y, vab);
-      if (hA) {
-        atomicAdd(a.out + xp.z, dA);
-        if constexpr (CD == 2) atomicAdd(a.out + xp.z + xl.x + 1, dA);
-      }
-      if (hB) {
-        atomicAdd(a.out + xp.w, dB);
-        if constexpr (CD == 2) atomicAdd(a.out + xp.w + xl.y + 1, dB);
+      if (a.dsum) { // deterministic: partial sums in slots, summed in a fixed order (k_et_dsum)
+        const int64_t e = (int64_t)m[2] + row;
+        if (hA) a.dsum[2 * e] = dA;
+        if (hB) a.dsum[2 * e + 1] = dB;
+      } else {
+        if (hA) {
+          atomicAdd(a.out + xp.z, dA);
+          if constexpr (CD == 2) atomicAdd(a.out + xp.z + xl.x + 1, dA);
+        }
+        if (hB) {
+          atomicAdd(a.out + xp.w, dB);
+          if constexpr (CD == 2) atomicAdd(a.out + xp.w + xl.y + 1, dB);
+        }
       }
     }
     __syncwarp();
@@ -932,6 +973,28 @@ __global__ void k_et_zero(const int32_t* __restrict__ pos, int64_t n, int cd, do
   }
 }
 
+// Deterministic diagonals: diagonal d = its slots summed in list order.
+__global__ void k_et_dsum(const int32_t* __restrict__ pos, const int32_t* __restrict__ dptr,
+                          const int32_t* __restrict__ dslots, int64_t n, int cd, const double* __restrict__ dsum,
+                          double* __restrict__ out, int accumulate) {
+  const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  double acc = 0.0;
+  for (int q = dptr[d]; q < dptr[d + 1]; ++q) acc += dsum[dslots[q]];
+  if (cd == 1) {
+    out[pos[d]] = accumulate ? out[pos[d]] + acc : acc;
+  } else { // the 2x2 diagonal block (x, 0; 0, x)
+    const int p = pos[2 * d], rl = pos[2 * d + 1];
+    if (accumulate) {
+      out[p] += acc;
+      out[p + rl + 1] += acc;
+    } else {
+      *reinterpret_cast<double2*>(out + p) = make_double2(acc, 0.0);
+      *reinterpret_cast<double2*>(out + p + rl) = make_double2(0.0, acc);
+    }
+  }
+}
+
 template <int FORM, int D, int CD>
 void go_etile(const EtilePlan& p, const EtileArgs& a, size_t smem_base, size_t buf, cudaStream_t s) {
   auto go = [&](auto kern, int threads, int stages) {
@@ -968,12 +1031,24 @@ int et_stages() {
 
 void launch_etile(int form, const EtilePlan& p, const double* coords, double* out, const FormParams& prm,
                   bool accumulate, int* next_tile, int* reset_tile, cudaStream_t s) {
-  if (!accumulate && p.ndiag) {
+  if (!accumulate && p.ndiag && !p.det) {
     k_et_zero<<<ceil_div(p.ndiag, 256), 256, 0, s>>>(p.diag.get(), p.ndiag, p.cd, out);
     count_launch();
     LG_LAUNCH_CHECK();
   }
-  if (p.ntiles == 0) return;
+  DevBuf<double> dsum;
+  if (p.det) dsum.alloc(2 * (size_t)std::max(p.nedge, 1), s);
+  auto finish = [&] { // deterministic mode: the diagonals in a fixed order
+    if (!p.det || !p.ndiag) return;
+    k_et_dsum<<<ceil_div(p.ndiag, 256), 256, 0, s>>>(p.diag.get(), p.dptr.get(), p.dslots.get(), p.ndiag, p.cd,
+                                                     dsum.get(), out, accumulate ? 1 : 0);
+    count_launch();
+    LG_LAUNCH_CHECK();
+  };
+  if (p.ntiles == 0) {
+    finish();
+    return;
+  }
   EtileArgs a{};
   a.tiles = p.tiles.get();
   a.ntiles = p.ntiles;
@@ -988,6 +1063,7 @@ void launch_etile(int form, const EtilePlan& p, const double* coords, double* ou
   a.dynamic = std::getenv("LOAM_GPU_ET_STATIC") ? 0 : 1;
   a.dbg = std::getenv("LOAM_GPU_ET_DBG") ? std::atoi(std::getenv("LOAM_GPU_ET_DBG")) : 0; // developer: skip phases
   memcpy(a.ktab, p.ktab, sizeof(a.ktab));
+  a.dsum = p.det ? dsum.get() : nullptr;
   int off = 128;
   a.off_seg = off;
   off += up16(p.max_segT * 8);
@@ -1014,6 +1090,7 @@ void launch_etile(int form, const EtilePlan& p, const double* coords, double* ou
   }
   count_launch();
   LG_LAUNCH_CHECK();
+  finish();
 }
 
 } // namespace loam_gpu

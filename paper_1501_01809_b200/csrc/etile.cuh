@@ -44,11 +44,18 @@ struct EtilePlan {
   DevBuf<int32_t> runs;  // coordinate-window runs [lo, hi)
   DevBuf<int32_t> diag;  // diagonal positions of the vertex rows (+ dof row length when cd = 2)
   uint32_t ktab[12] = {};
+  // deterministic mode: the edge rows store their diagonal partial sums in
+  // slots (2 e + endpoint) instead of RED-adding them; diagonal d (in `diag`
+  // order) sums slots dslots[dptr[d] .. dptr[d + 1]) in that (edge-ascending)
+  // order
+  bool det = false;
+  DevBuf<int32_t> dptr, dslots;
 };
 
 struct EtileSpec {
   int tile_rows = 128; // 64 or 128: consumer threads per CTA, one edge row each
   int tile_seg = 4096, tile_pairs = 1024, tile_cells = 512, tile_slots = 768, tile_runs = 32;
+  bool det = false; // deterministic diagonals (EtilePlan::det)
 };
 
 // Builds the plan from the locality-sorted row map (ncells x nrn, P2), the

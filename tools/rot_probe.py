@@ -12,6 +12,8 @@ import bench  # noqa: E402
 from paper_1501_01809_b200 import capi, configs  # noqa: E402
 
 capi.set_strategy("auto")
+if os.environ.get("DET"):
+    capi.set_option(capi.OPT_DETERMINISTIC, 1)
 flush = bench.Flusher(torch)
 stream = torch.cuda.current_stream()
 peak, _ = bench.peaks()
@@ -26,7 +28,7 @@ for c in sys.argv[1:] or ["1", "2", "3r", "3m", "4", "5"]:
     K = max(40, 4 * rot.R)
     ts = [rot.time(K, stream, warmup=K) for _ in range(3)]
     f = lambda ms: ab / (ms * 1e-3) / 1e9 / peak
-    print(f"config {c} pdl={'off' if os.environ.get('LOAM_GPU_NO_PDL') else 'on'}: R={rot.R} K={K} "
+    print(f"config {c} pdl={'off' if os.environ.get('LOAM_GPU_NO_PDL') else 'on'}{' det' if os.environ.get('DET') else ''}: R={rot.R} K={K} "
           f"rotation {min(ts)*1e3:.1f} us ({f(min(ts)):.3f}) [{', '.join(f'{x*1e3:.1f}' for x in ts)}]  "
           f"flushed {fl*1e3:.1f} us ({f(fl):.3f}); launches/step {rot.launches_per_step:.1f}", flush=True)
     del rot, w
