@@ -30,6 +30,7 @@
 #include "stage.cuh"
 #include "elements.cuh"
 #include "engine.cuh"
+#include "ctile.cuh"
 #include "etile.cuh"
 #include "ntile.cuh"
 #include "rtile.cuh"
@@ -2471,6 +2472,8 @@ struct FastPlan {
   PatchPlan patch;
   bool use_cell = false;   // cell-centric atomic scatter
   bool det_cell = false;   // deterministic mode: cell entries + fixed-order pair sums
+  bool use_ctile = false;  // P2 actions: cell tiles (ctile.cu)
+  CtilePlan ct;
   bool use_cseg = false;   // (actions, auto) warp-segmented reduction of the cell scatter
   DevBuf<uint16_t> cs_slots, cs_start;
   DevBuf<int32_t> cs_off, cs_node;
@@ -2709,6 +2712,17 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
         P->xmap.v.release();
       }
     }
+    // P2 actions on one sorted map (rows = coefficients, vertex prefix =
+    // coordinates): cell tiles with TMA-staged windows and one RED per
+    // distinct node of a tile instead of one per element entry.  Opt-in
+    // (LOAM_GPU_CTILE=1): measured slower than the cell kernel on config 3
+    // (83 vs 68 us per step; DESIGN 15) -- the cell kernel's gathers hit L2.
+    const bool action = k.form == F_MASS_ACTION || k.form == F_STIFFNESS_ACTION || k.form == F_HELMHOLTZ_ACTION;
+    if (!k.bilinear && action && !P->det_cell && R.dim == 1 && k.nrn == (k.gd == 3 ? 10 : 6) && Cm &&
+        P->xptr == P->crows.v.get() && P->cptr == P->crows.v.get() && std::getenv("LOAM_GPU_CTILE") &&
+        (reinterpret_cast<uintptr_t>(args[1].data) & 15) == 0 && (reinterpret_cast<uintptr_t>(args[2].data) & 15) == 0 &&
+        build_ctile(P->ct, k.gd, k.nrn, n, P->crows.v.get(), R.v.target, X->target_size, s))
+      P->use_ctile = true;
     return P;
   }
   // Neighbour-list plan when row, column, coordinate (and coefficient) maps
@@ -3022,6 +3036,13 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     if (!k.bilinear && !t.accumulate) // shared nodes are RED-accumulated; nodes in no cell stay zero
       LG_CUDA(cudaMemsetAsync(args[0].data, 0, sizeof(double) * (size_t)args[0].set_size * args[0].dim, s));
     k.patch(t, patch_smem_bytes(k, pp), s);
+    return;
+  }
+  if (P->use_ctile) {
+    const int ctr = P->counter.acquire(s);
+    launch_ctile(k.form, P->ct, args[1].data, args[2].data, args[0].data, (int64_t)args[0].set_size * args[0].dim,
+                 prm, !(args[0].flags & LOAM_ARG_ZERO), P->counter.next(ctr), P->counter.exits(ctr), s);
+    P->counter.commit(ctr, s);
     return;
   }
   if (P->use_cell) {

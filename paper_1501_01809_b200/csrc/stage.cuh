@@ -63,6 +63,48 @@ __device__ __forceinline__ uint32_t stage_runs(const RunSet& s, int lane, uint64
   return tx;
 }
 
+// Static tile schedule with prefetched tile records (RI ints each, RI % 4 ==
+// 0).  Tile k of a CTA is blockIdx + k * grid; the producer warp pulls the
+// records of 8 tiles at a time into shared memory by cp.async (one 16-byte
+// part per lane), one batch ahead in a double buffer, so its per-tile chain
+// holds no dependent global round trip for the tile's meta (a dynamic counter
+// costs an atomic plus a record load per tile).  For tiles of uniform cost.
+// buf: shared int[2][8 * RI], 16-byte aligned.  Per tile: rec = at(k), read
+// it into registers, then done(k).
+template <int RI>
+struct TileFeedT {
+  static_assert(RI % 4 == 0 && RI <= 16, "record of whole 16-byte parts, one per lane");
+  static constexpr int kParts = RI / 4;
+  int* buf;
+  const int32_t* tiles;
+  int ntiles;
+  __device__ __forceinline__ int tile(int k) const { return (int)blockIdx.x + k * (int)gridDim.x; }
+  __device__ __forceinline__ void load(int b, int lane) const { // tiles 8b..8b+7 -> buf[b & 1]
+    const int q = lane / kParts, part = lane - q * kParts;
+    const int t = tile(8 * b + q);
+    if (q < 8 && t < ntiles) cp_async16(buf + (b & 1) * 8 * RI + q * RI + part * 4, tiles + (int64_t)RI * t + part * 4);
+    cp_async_commit();
+  }
+  __device__ __forceinline__ void start(int lane) const {
+    load(0, lane);
+    load(1, lane);
+  }
+  __device__ __forceinline__ const int* at(int k) const {
+    if (k % 8 == 0) {
+      cp_async_wait<1>(); // batch k / 8 has landed
+      __syncwarp();
+    }
+    return buf + ((k / 8) & 1) * 8 * RI + (k % 8) * RI;
+  }
+  __device__ __forceinline__ void done(int k, int lane) const {
+    if (k % 8 == 7) {
+      __syncwarp();
+      load(k / 8 + 2, lane);
+    }
+  }
+  __device__ __forceinline__ void drain() const { cp_async_wait<0>(); }
+};
+
 // Persistent tile kernels grab tiles from a global counter.  The last CTA to
 // finish puts the counter (and the exit count) back to zero, so every launch
 // -- including a replay of a captured CUDA graph with frozen arguments --
