@@ -13,6 +13,7 @@
 #include <atomic>
 #include <exception>
 #include <thread>
+#include <utility>
 #include <vector>
 #include <cstdint>
 #include <cstdio>
@@ -121,6 +122,31 @@ inline void plan_tick(const char* label, cudaStream_t s) {
   const auto now = std::chrono::steady_clock::now();
   std::fprintf(stderr, "[plan] %-28s %9.3f ms\n", label, std::chrono::duration<double, std::milli>(now - last).count());
   last = now;
+}
+
+// Programmatic dependent launch (PDL): a kernel launched this way may start
+// while the previous kernel in the stream drains; it must execute
+// griddepcontrol.wait (async.cuh grid_dep_wait) before it reads anything a
+// previous kernel may write or writes anything at all.  Only kernels written
+// that way are launched through here.  LOAM_GPU_NO_PDL=1 disables it.
+inline bool pdl_on() {
+  static const bool on = std::getenv("LOAM_GPU_NO_PDL") == nullptr;
+  return on;
+}
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) throw Error(LOAM_GPU_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
 }
 
 // Host-side plan construction runs on all host cores: parallel_chunks(n, f)

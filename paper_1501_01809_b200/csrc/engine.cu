@@ -1116,6 +1116,9 @@ __device__ __forceinline__ double star_row(const StarArgs& a, int r, int4 h, int
 // 256-thread blocks at 48 registers holds 740 blocks; C1 has 263,169 rows).
 template <class F, int RPT>
 __global__ void __launch_bounds__(256) k_star_vec(const __grid_constant__ StarArgs a) {
+  // PDL: let the next kernel's prologue start; load this row's star record
+  // (plan data, library-owned) before waiting for the previous kernel
+  if (threadIdx.x == 0) grid_dep_launch();
   const int r0 = blockIdx.x * blockDim.x + threadIdx.x;
   const int stride = gridDim.x * blockDim.x;
   int4 h[RPT], t[RPT];
@@ -1127,6 +1130,7 @@ __global__ void __launch_bounds__(256) k_star_vec(const __grid_constant__ StarAr
       t[q] = __ldg(a.star + 2 * r + 1);
     }
   }
+  grid_dep_wait(); // coordinates, coefficients and the output after the previous kernel
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
     const int r = r0 + q * stride;
@@ -1203,9 +1207,9 @@ void launch_star(const StarArgs& a, cudaStream_t s) {
   if constexpr (F::BILINEAR) k_star_mat<F><<<ceil_div(a.nrows, 256), 256, 0, s>>>(a);
   else {
     static const int rpt = std::getenv("LOAM_GPU_STAR_RPT") ? std::atoi(std::getenv("LOAM_GPU_STAR_RPT")) : 1;
-    if (rpt >= 4) k_star_vec<F, 4><<<ceil_div(a.nrows, 256 * 4), 256, 0, s>>>(a);
-    else if (rpt == 2) k_star_vec<F, 2><<<ceil_div(a.nrows, 256 * 2), 256, 0, s>>>(a);
-    else k_star_vec<F, 1><<<ceil_div(a.nrows, 256), 256, 0, s>>>(a);
+    if (rpt >= 4) launch_pdl(k_star_vec<F, 4>, dim3(ceil_div(a.nrows, 256 * 4)), dim3(256), 0, s, a);
+    else if (rpt == 2) launch_pdl(k_star_vec<F, 2>, dim3(ceil_div(a.nrows, 256 * 2)), dim3(256), 0, s, a);
+    else launch_pdl(k_star_vec<F, 1>, dim3(ceil_div(a.nrows, 256)), dim3(256), 0, s, a);
   }
   count_launch();
   LG_LAUNCH_CHECK();
@@ -1779,6 +1783,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
     fence_mbar_init();
   }
   __syncthreads();
+  if (tid == 0) grid_dep_launch(); // PDL: the next kernel's prologue may start
   auto tile_meta = [&](int tile, int (&m)[12]) {
     const int4* t = reinterpret_cast<const int4*>(a.tiles + 12 * tile);
     const int4 x = __ldg(t), y = __ldg(t + 1), z = __ldg(t + 2);
@@ -1803,6 +1808,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
       }
     };
     prefetch();
+    grid_dep_wait(); // the caller's data only after the previous kernel (PDL)
     for (int k = 0;; ++k) {
       const int tile = nt;
       int m[12];
@@ -1849,6 +1855,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_ptile(const __grid_constant__ PT
     }
     return;
   }
+  grid_dep_wait(); // (PDL) before the consumers read or write anything of the caller's
   // ---- consumers: one thread per node row
   double* seg = reinterpret_cast<double*>(sm + a.off_seg);
   for (int k = 0;; ++k) {
@@ -2005,7 +2012,7 @@ void launch_ptile(const PTileArgs& a, size_t smem_base, size_t buf, cudaStream_t
     int blocks = 1;
     LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kPTileThreads + 32, smem));
     const int grid = std::min(a.ntiles, std::max(blocks, 1) * kNumSMs);
-    kern<<<grid, kPTileThreads + 32, smem, s>>>(a);
+    launch_pdl(kern, dim3(grid), dim3(kPTileThreads + 32), smem, s, a);
   };
   const int st = ptile_stages(F::ID);
   if (st == 1) go(k_ptile<F, kPTileThreads, 1>, 1);
@@ -2977,6 +2984,9 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
   }
   if (!P) {
     P = build_fast_plan(k, n, args, cell_mode, s);
+    // the plan's device arrays are complete before any kernel reads them: the
+    // PDL kernels load plan data before griddepcontrol.wait
+    LG_CUDA(cudaStreamSynchronize(s));
     if (cacheable) {
       std::lock_guard<std::mutex> g(g_cache_mutex);
       g_fast_cache[key] = P;

@@ -645,6 +645,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
     fence_mbar_init();
   }
   __syncthreads();
+  if (tid == 0) grid_dep_launch(); // PDL: the next kernel's prologue may start
   auto ring = [&](int k) { return sm + a.off_buf + (k % STAGES) * a.buf_bytes; };
   auto meta = [&](int tile, int (&m)[16]) {
     const int4* t = reinterpret_cast<const int4*>(a.tiles + 16 * tile);
@@ -678,6 +679,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
       }
     };
     prefetch();
+    grid_dep_wait(); // the caller's data only after the previous kernel (PDL)
     for (int k = 0;; ++k) {
       const int tile = nt;
       int m[16];
@@ -711,6 +713,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_etile(const __grid_constant__ Et
     }
     return;
   }
+  grid_dep_wait(); // (PDL) before the consumers read or write anything of the caller's
   // ---- consumers
   constexpr int GS = T::GS, RBW = COMPACT ? (D == 3 ? 2 : 1) : T::RBW;
   double* segT = reinterpret_cast<double*>(sm + a.off_seg); // lane-interleaved row segments
@@ -1004,7 +1007,7 @@ void go_etile(const EtilePlan& p, const EtileArgs& a, size_t smem_base, size_t b
     LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, threads, smem));
     require(blocks > 0, LOAM_GPU_ERR_CUDA, "edge-tile kernel does not fit on an SM");
     const int grid = std::min(p.ntiles, blocks * kNumSMs);
-    kern<<<grid, threads, smem, s>>>(a);
+    launch_pdl(kern, dim3(grid), dim3(threads), smem, s, a);
   };
   const int st = et_stages();
   auto pick = [&](auto compact) {

@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
     fence_mbar_init();
   }
   __syncthreads();
+  if (tid == 0) grid_dep_launch(); // PDL: the next kernel's prologue may start
   auto ring = [&](int k) { return sm + a.off_buf + (k % STAGES) * a.buf_bytes; };
   auto meta = [&](int tile, int (&m)[16]) {
     const int4* t = reinterpret_cast<const int4*>(a.tiles + 16 * tile);
@@ -366,6 +367,7 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
       }
     };
     prefetch();
+    grid_dep_wait(); // the caller's data only after the previous kernel (PDL)
     for (int k = 0;; ++k) {
       const int tile = nt;
       int m[16];
@@ -399,6 +401,7 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
     }
     return;
   }
+  grid_dep_wait(); // (PDL) before the consumers read or write anything of the caller's
   // ---- consumers
   double* seg0 = reinterpret_cast<double*>(sm + a.off_seg);
   double* geo = reinterpret_cast<double*>(sm + a.off_geo);
@@ -573,7 +576,7 @@ void launch_ntile(const NtilePlan& p, const double* coords, double* out, const F
     int blocks = 1;
     LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kNtThreads + 32, smem));
     require(blocks > 0, LOAM_GPU_ERR_CUDA, "node-tile kernel does not fit on an SM");
-    kern<<<std::min(p.ntiles, blocks * kNumSMs), kNtThreads + 32, smem, s>>>(a);
+    launch_pdl(kern, dim3(std::min(p.ntiles, blocks * kNumSMs)), dim3(kNtThreads + 32), smem, s, a);
   };
   if (std::getenv("LOAM_GPU_NT_INFO")) // developer: plan maxima behind the shared-memory footprint
     fprintf(stderr, "ntile: tiles %d max_seg %d max_cells %d max_blob %d max_slots %d max_diag %d smem/stage %d fixed %d\n",

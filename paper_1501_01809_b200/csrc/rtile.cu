@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_rtile(const __grid_constant__ Rt
     fence_mbar_init();
   }
   __syncthreads();
+  if (tid == 0) grid_dep_launch(); // PDL: the next kernel's prologue may start
   auto ring = [&](int k) { return sm + a.off_buf + (k % STAGES) * a.buf_bytes; };
   auto meta = [&](int tile, int (&m)[16]) {
     const int4* t = reinterpret_cast<const int4*>(a.tiles + 16 * tile);
@@ -343,6 +344,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_rtile(const __grid_constant__ Rt
       }
     };
     prefetch();
+    grid_dep_wait(); // the caller's data only after the previous kernel (PDL)
     for (int k = 0;; ++k) {
       const int tile = nt;
       int m[16];
@@ -376,6 +378,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_rtile(const __grid_constant__ Rt
     }
     return;
   }
+  grid_dep_wait(); // (PDL) before the consumers read or write anything of the caller's
   // ---- consumers
   double* segT = reinterpret_cast<double*>(sm + a.off_seg); // lane-interleaved row segments
   double* geo = reinterpret_cast<double*>(sm + a.off_geo);  // cell geometry; then the contiguous segment
@@ -520,7 +523,7 @@ void go_rtile(const RtilePlan& p, const RtileArgs& a, size_t base, size_t buf, c
     int blocks = 1;
     LG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, threads, smem));
     require(blocks > 0, LOAM_GPU_ERR_CUDA, "row-tile kernel does not fit on an SM");
-    kern<<<std::min(p.ntiles, blocks * kNumSMs), threads, smem, s>>>(a);
+    launch_pdl(kern, dim3(std::min(p.ntiles, blocks * kNumSMs)), dim3(threads), smem, s, a);
   };
   static const int st = std::getenv("LOAM_GPU_RT_STAGES") ? std::atoi(std::getenv("LOAM_GPU_RT_STAGES")) : 2;
   if (p.tile_threads == 64) {
