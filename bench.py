@@ -240,15 +240,26 @@ class Rotation:
             self.graphs[steps] = g
         return self.graphs[steps]
 
+    # a captured launch keeps its plan's tile-counter pair (32 per plan,
+    # engine.cu TileCounters): a graph holds at most 16 steps per replica and
+    # longer runs replay it back to back
+    def chunks(self, steps):
+        L = min(steps, 16 * self.R)
+        return [L] * (steps // L) + ([steps % L] if steps % L else [])
+
+    def replay_steps(self, steps):
+        for c in self.chunks(steps):
+            self.graph(c).replay()
+
     def time(self, steps, stream, warmup=0):
-        """ms per step over `steps` back-to-back steps (one graph launch,
-        events on `stream`)."""
-        g = self.graph(steps)
-        for _ in range(max(1, -(-warmup // steps))):
-            g.replay()
+        """ms per step over EXACTLY `steps` back-to-back steps (graph
+        launches, one pair of events on `stream`)."""
+        for c in self.chunks(steps):
+            self.graph(c)  # captured before the timed region
+        self.replay_steps(max(warmup, 1))
         e0, e1 = self.torch.cuda.Event(enable_timing=True), self.torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        g.replay()
+        self.replay_steps(steps)
         e1.record(stream)
         e1.synchronize()
         return e0.elapsed_time(e1) / steps
@@ -605,14 +616,14 @@ def gpu_arm(args):
         w.run()
     flushed = time_steps(torch, w, max(args.steps, 10), flush, stream)
     rot = Rotation(torch, w)
-    g = rot.graph(args.steps)
-    wg = rot.graph(max(args.warmup, 3))
+    for c in rot.chunks(args.steps) + rot.chunks(max(args.warmup, 3)):
+        rot.graph(c)  # every graph captured before the clocks start
     clocks = ClockSampler(local)
     with clocks:
-        wg.replay()  # W >= 3 untimed warm-up steps
+        rot.replay_steps(max(args.warmup, 3))  # W >= 3 untimed warm-up steps
         soak_end = time.perf_counter() + 0.3  # keep the GPU busy so NVML sees load
         while time.perf_counter() < soak_end:
-            g.replay()
+            rot.replay_steps(args.steps)
             torch.cuda.synchronize()
         torch.cuda.synchronize()
         if world > 1:
