@@ -1366,16 +1366,26 @@ bool build_stars(const int32_t* dmap, int ncells, int nverts, DevBuf<int4>& out,
   return true;
 }
 
+#ifndef LOAM_GPU_RING_STAGES
+#define LOAM_GPU_RING_STAGES 3
+#endif
+#ifndef LOAM_GPU_RING_MINB
+#define LOAM_GPU_RING_MINB 3
+#endif
+constexpr int kRS = LOAM_GPU_RING_STAGES;            // ring pipeline stages
+constexpr int kRingMinBlocks = LOAM_GPU_RING_MINB;   // CTAs per SM the registers are sized for
+static_assert(2 * 8 * kRS + 4 * kRS <= 128, "ring barriers + stage ids fit the 128-byte header");
+
 template <class F, bool ACC>
-__global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ RingArgs a) {
+__global__ void __launch_bounds__(kTileBlock, kRingMinBlocks) k_ring(const __grid_constant__ RingArgs a) {
   static_assert(F::GD == 2 && F::NRN == 3, "ring kernel: P1 triangles");
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
-  uint64_t* empty = full + 3;
-  int* slot_tile = reinterpret_cast<int*>(full + 6); // [3] tile id carried by each ring stage (-1: done)
+  uint64_t* empty = full + kRS;
+  int* slot_tile = reinterpret_cast<int*>(full + 2 * kRS); // [kRS] tile id carried by each ring stage (-1: done)
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int b = 0; b < 3; ++b) {
+    for (int b = 0; b < kRS; ++b) {
       mbar_init(&full[b], 1);
       mbar_init(&empty[b], kTileThreads / 32);
     }
@@ -1385,11 +1395,11 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
   // PDL: the next PDL-launched kernel may start its prologue (it waits for
   // this grid's completion before touching anything this grid writes)
   if (tid == 0) grid_dep_launch();
-  auto ring = [&](int k) { return sm + a.off_buf + (k % 3) * a.buf_bytes; };
+  auto ring = [&](int k) { return sm + a.off_buf + (k % kRS) * a.buf_bytes; };
   // tile records of this CTA, 8 tiles per batch, double-buffered (cp.async);
   // the meta of the tile in each ring stage, handed to the consumers with it
   __shared__ __align__(16) int meta_s[2][8 * 16];
-  __shared__ int stage_meta[3][8];
+  __shared__ int stage_meta[kRS][8];
   if (tid >= kTileThreads) { // ---- producer warp
     // Static schedule: tile k of this CTA is blockIdx + k * grid (tiles cost
     // about the same).  The 64-byte tile records (meta + the first window
@@ -1427,18 +1437,18 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
         __syncwarp(); // every lane has read batch k / 8: refill its buffer
         load_batch(k / 8 + 2);
       }
-      if (k >= 3) mbar_wait_sleep(&empty[k % 3], (k / 3 - 1) & 1);
+      if (k >= kRS) mbar_wait_sleep(&empty[k % kRS], (k / kRS - 1) & 1);
       if (tile >= a.ntiles) { // publish "no more tiles" through the stage
         if (lane == 0) {
-          slot_tile[k % 3] = -1;
-          mbar_arrive(&full[k % 3]);
+          slot_tile[k % kRS] = -1;
+          mbar_arrive(&full[k % kRS]);
         }
         break;
       }
-      if (lane < 8) stage_meta[k % 3][lane] = m[lane];
-      if (lane == 0) slot_tile[k % 3] = tile;
+      if (lane < 8) stage_meta[k % kRS][lane] = m[lane];
+      if (lane == 0) slot_tile[k % kRS] = tile;
       unsigned char* buf = ring(k);
-      uint64_t* bar = &full[k % 3];
+      uint64_t* bar = &full[k % kRS];
       auto rb = [](int lo, int hi, int es, int64_t& s0) {
         s0 = ((int64_t)lo * es) & ~int64_t(15);
         return (uint32_t)((((int64_t)hi * es + 15) & ~int64_t(15)) - s0);
@@ -1480,30 +1490,37 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
   long long t_first = 0, t_wait = 0, t_comp = 0, t_n = 0, t_early = 0, t_last = 0;
   for (int k = 0;; ++k) {
     const long long c0 = a.timing ? clock64() : 0;
-    mbar_wait(&full[k % 3], (k / 3) & 1);
+    mbar_wait(&full[k % kRS], (k / kRS) & 1);
     const long long c1 = a.timing ? clock64() : 0;
-    const int tile = slot_tile[k % 3];
+    const int tile = slot_tile[k % kRS];
     if (a.timing) {
       if (k == 0) t_first += c1 - c0;
       else if (tile < 0) t_last += c1 - c0;
-      else if (k < 3) t_early += c1 - c0;
+      else if (k < kRS) t_early += c1 - c0;
       else t_wait += c1 - c0;
     }
     if (tile < 0) break;
     if (k == 0) grid_dep_wait(); // (returns at once: the producer has waited)
     int m[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) m[q] = stage_meta[k % 3][q];
-    const int R0 = m[0], nrows = m[1] - m[0], A0 = m[2], nA = m[3] - m[2], P0 = m[4];
-    // the segment, skewed so segb[t] and out[A0 + t] agree mod 16 bytes; the
-    // previous tile's bulk store must have finished reading it
-    double* segb = seg + (A0 & 1);
+    for (int q = 0; q < 8; ++q) m[q] = stage_meta[k % kRS][q];
+    const int R0 = m[0], nrows = m[1] - m[0], P0 = m[4];
+    (void)m[3];
+    // every warp owns its 32 rows' CSR values (a contiguous range [W0, W1))
+    // in its own shared slice, skewed so wsegb[t] and out[W0 + t] agree mod
+    // 16 bytes, and stores it with its own bulk copy: no CTA-wide barrier
+    // per tile (the previous store of this warp must have read the slice)
+    const int wl = tid >> 5, lane = tid & 31;
+    const int* nptr_w = reinterpret_cast<const int32_t*>(ring(k) + a.b_nptr) + skew_of(R0, 4);
+    const int W0 = F::BILINEAR ? nptr_w[min(32 * wl, nrows)] : 0;
+    const int W1 = F::BILINEAR ? nptr_w[min(32 * wl + 32, nrows)] : 0;
+    double* segb = seg + wl * a.seg_stride + (W0 & 1) - W0; // indexed by the global CSR offset
     if constexpr (F::BILINEAR) {
-      if (tid == 0) bulk_wait_read<0>();
-      named_bar(1, kTileThreads);
+      if (lane == 0) bulk_wait_read<0>();
+      __syncwarp();
       if constexpr (ACC) {
-        for (int t = tid; t < nA; t += kTileThreads) segb[t] = a.out[(int64_t)A0 + t];
-        named_bar(1, kTileThreads);
+        for (int t = W0 + lane; t < W1; t += 32) segb[t] = a.out[t];
+        __syncwarp();
       }
     }
     const long long c1b = a.timing ? clock64() : 0;
@@ -1517,9 +1534,8 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
     if (tid < nrows) {
       const uint32_t info = info_s[tid];
       const int self_slot = info & 0xffff, self_rank = (info >> 16) & 0xff;
-      const int a0 = F::BILINEAR ? nptr_s[tid] - A0 : 0;
       const int q0 = rptr_s[tid] - P0, q1 = rptr_s[tid + 1] - P0;
-      double* row = segb + a0;
+      double* row = segb + (F::BILINEAR ? nptr_s[tid] : 0);
       auto put = [&](int rank, double v) {
         if constexpr (ACC) row[rank] += v;
         else row[rank] = v;
@@ -1622,21 +1638,22 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
     }
     __syncwarp();
     const long long c1c = a.timing ? clock64() : 0;
-    if ((tid & 31) == 0) mbar_arrive(&empty[k % 3]);
+    if (lane == 0) mbar_arrive(&empty[k % kRS]);
     if constexpr (F::BILINEAR) {
-      // segment complete -> one bulk store (head / tail doubles off the
-      // 16-byte grid stored directly)
+      // the warp's slice complete -> one bulk store by its lane 0 (head /
+      // tail doubles off the 16-byte grid stored directly)
       fence_async_shared();
-      named_bar(1, kTileThreads);
-      if (tid == 0) {
-        double* dst = a.out + A0;
-        const int h = A0 & 1, t1 = nA - ((A0 + nA) & 1);
-        if (h && nA > 0) dst[0] = segb[0];
+      __syncwarp();
+      if (lane == 0 && W1 > W0) {
+        const int nw = W1 - W0, h = W0 & 1, t1 = nw - ((W0 + nw) & 1);
+        double* dst = a.out + W0;
+        const double* src = segb + W0;
+        if (h) dst[0] = src[0];
         if (t1 > h) {
-          bulk_s2g(dst + h, segb + h, (uint32_t)(t1 - h) * 8);
+          bulk_s2g(dst + h, src + h, (uint32_t)(t1 - h) * 8);
           bulk_commit();
         }
-        if (t1 < nA && t1 >= h) dst[t1] = segb[t1];
+        if (t1 < nw && t1 >= h) dst[t1] = src[t1];
       }
     }
     if (a.timing) {
@@ -1655,7 +1672,7 @@ __global__ void __launch_bounds__(kTileBlock, 3) k_ring(const __grid_constant__ 
   }
   // the segment must outlive its bulk store's shared-memory reads; the global
   // writes themselves complete with the grid
-  if (F::BILINEAR && tid == 0) bulk_wait_read<0>();
+  if (F::BILINEAR && (tid & 31) == 0) bulk_wait_read<0>();
   tile_counter_release(a.next_tile, a.reset_tile, kTileThreads, tid);
   if (a.timing && (tid & 31) == 0) {
     atomicAdd(a.timing, (unsigned long long)t_first);
@@ -2779,7 +2796,7 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
     // the same number of tiles (no tail of CTAs with one tile more)
     int tile_rows = kTileThreads / R.dim;
     if (k.ring && R.dim == 1 && k.bilinear) {
-      const int G = 3 * kNumSMs;
+      const int G = kRingMinBlocks * kNumSMs;
       const int per_cta = ceil_div(ceil_div(R.v.target, tile_rows), G);
       tile_rows = std::max(32, ceil_div(R.v.target, (int64_t)per_cta * G));
     }
@@ -3119,8 +3136,9 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     auto up16 = [](int x) { return (x + 15) & ~15; };
     int off = 128; // 6 mbarriers + 3 stage tile ids
     t.off_seg = off;
-    t.seg_stride = k.bilinear ? up16((nb.max_seg + 2) * 8) / 8 : 0;
-    off += t.seg_stride * 8;
+    // one slice per consumer warp: 32 rows of at most max_len entries (+ skew)
+    t.seg_stride = k.bilinear ? up16((32 * nb.max_len + 2) * 8) / 8 : 0;
+    off += (kTileThreads / 32) * t.seg_stride * 8;
     t.off_buf = off;
     int b = 0;
     t.b_nptr = b;
@@ -3136,7 +3154,7 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
     t.b_winc = b;
     b += up16(k.has_coeff ? nb.max_slots * 8 : 0);
     t.buf_bytes = b;
-    off += 3 * b;
+    off += kRS * b;
     static const bool timing = std::getenv("LOAM_GPU_PHASE_TIMING") != nullptr;
     DevBuf<unsigned long long> tbuf;
     if (timing) {
