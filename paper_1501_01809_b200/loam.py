@@ -114,7 +114,10 @@ class Map:
         return self.id, dim
 
     def __del__(self):
-        _release(getattr(self, "id", 0))
+        try:
+            _release(getattr(self, "id", 0))
+        except Exception:  # noqa: BLE001 -- interpreter teardown: module globals already gone
+            pass
 
     def desc(self) -> capi.MapDesc:
         if self._desc is None:
@@ -271,7 +274,10 @@ class Sparsity:
         return self._desc
 
     def __del__(self):
-        _release(getattr(self, "id", 0))
+        try:
+            _release(getattr(self, "id", 0))
+        except Exception:  # noqa: BLE001 -- interpreter teardown: module globals already gone
+            pass
 
 
 def build_sparsity(row_map: Map, col_map: Map, row_dim: int = 1, col_dim: int = 1) -> Sparsity:

@@ -65,3 +65,30 @@ for mode in ("flush", "flush+spin"):
         e0.record(st); step(); e1.record(st); e1.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
     print("C2 step", mode, np.median(ts[3:]))
+
+# back to back from one CUDA graph over rotated buffers (bench.Rotation's
+# protocol): what a 15 MB / 100 MB streaming read and copy cost per step when
+# every step's data is cold but launches are not the gap
+def b2b(nbytes, kind, K=40):
+    R = max(2, int(np.ceil(3 * 126 * 2**20 / nbytes)) + 1)
+    n = nbytes // 8 // (2 if kind == "copy" else 1)
+    src = [torch.ones(n, dtype=torch.float64, device="cuda") for _ in range(R)]
+    dst = [torch.empty_like(x) for x in src] if kind == "copy" else None
+    outs = torch.zeros(R, dtype=torch.float64, device="cuda")
+    g, side = torch.cuda.CUDAGraph(), torch.cuda.Stream()
+    side.wait_stream(st)
+    with torch.cuda.graph(g, stream=side):
+        for k in range(K):
+            if kind == "copy":
+                dst[k % R].copy_(src[k % R])
+            else:
+                torch.sum(src[k % R], dim=0, out=outs[k % R])
+    st.wait_stream(side)
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record(st); g.replay(); e1.record(st); e1.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / K, R
+for nb in (15_000_000, 100_000_000):
+    for kind in ("read", "copy"):
+        us, R = b2b(nb, kind)
+        print(f"back-to-back {kind} {nb/1e6:.0f} MB (R={R}): {us:.2f} us/step = {nb/us/1e3:.0f} GB/s")
