@@ -2800,6 +2800,14 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       const int per_cta = ceil_div(ceil_div(R.v.target, tile_rows), G);
       tile_rows = std::max(32, ceil_div(R.v.target, (int64_t)per_cta * G));
     }
+    // the ring plan on the device (LOAM_GPU_HOST_RING=1: the host builder)
+    if (ok && k.ring && k.bilinear && R.dim == 1 && R.v.arity == 3 && !std::getenv("LOAM_GPU_NO_RING") &&
+        !std::getenv("LOAM_GPU_HOST_RING") &&
+        build_ring_dev(P->nb, srows.v.get(), n, R.v.target, csr, tile_rows, kTileSeg, kTileSlots, s)) {
+      plan_tick("ring tiles (device)", s);
+      P->use_nbr = true;
+      return P;
+    }
     if (ok && build_nbr(P->nb, srows.v.get(), n, R.v.arity, R.v.target, csr, tile_rows,
                         k.bilinear ? kTileSeg : (1 << 30), kTileSlots, kTileRuns, s)) {
       plan_tick("nbr / ring tiles", s);

@@ -1049,4 +1049,244 @@ void color_dev(int n, const std::vector<MapView>& maps, ColorPlan& out, cudaStre
   for (int c = 0; c < out.ncolors; ++c) out.offsets[c + 1] = out.offsets[c] + hc[c];
 }
 
+
+// ===========================================================================
+// Ring plan on the device (the C2 headline's first-call cost).  Same tiles,
+// window runs, slots and chain records as build_nbr's host ring mode for
+// tiles of a fixed row count; any tile or row the fast path cannot handle
+// (a window range over kRdBits, too many runs or slots, a non-manifold star,
+// a row without pairs) sets a flag and the caller falls back to build_nbr.
+// ===========================================================================
+namespace {
+
+constexpr int kRdThreads = 256;      // one CTA per tile, one thread per row
+constexpr int kRdBits = 16384;       // window range bitmap (vertex pairs)
+constexpr int kRdMaxRuns = 32;       // runs per tile (fixed stride in the runs array)
+constexpr int kRdMaxAdj = 8 * kRdThreads;
+
+struct RingDevArgs {
+  const int32_t* rows;    // sorted cell rows [ncells x 3]
+  const int32_t* nptr;    // node pattern offsets
+  const int32_t* nadj;    // node pattern columns
+  const int32_t* pptr;    // pair offsets per row
+  const int32_t* pairs;   // cell * 3 + i
+  int nrows, tile_rows, ntiles, tile_slots;
+  int32_t* rtiles;        // [ntiles x 16]
+  int32_t* runs;          // [ntiles x kRdMaxRuns x 2]
+  int32_t* rptr;          // [nrows + 1]
+  uint16_t* rrecs;
+  uint32_t* rowinfo;
+  int* stat;              // [0] fail flag, [1..] maxima: rows, adj, recs, slots, runs, len
+};
+
+__global__ void __launch_bounds__(kRdThreads) k_ring_plan(const RingDevArgs a) {
+  __shared__ uint32_t bits[kRdBits / 32];
+  __shared__ int run_lo[kRdMaxRuns], run_hi[kRdMaxRuns], run_base[kRdMaxRuns];
+  __shared__ int nruns, vmin_s, vmax_s, fail_s, slots_s;
+  __shared__ uint16_t eslot[kRdMaxAdj];
+  const int t = blockIdx.x, tid = threadIdx.x;
+  const int r0 = t * a.tile_rows, r1 = min(a.nrows, r0 + a.tile_rows);
+  const int a0 = a.nptr[r0], a1 = a.nptr[r1];
+  if (tid == 0) {
+    vmin_s = INT_MAX;
+    vmax_s = -1;
+    fail_s = (a1 - a0 > kRdMaxAdj) ? 1 : 0;
+  }
+  for (int q = tid; q < kRdBits / 32; q += kRdThreads) bits[q] = 0u;
+  __syncthreads();
+  int lmin = INT_MAX, lmax = -1;
+  for (int e = a0 + tid; e < a1; e += kRdThreads) {
+    const int v = a.nadj[e];
+    lmin = min(lmin, v);
+    lmax = max(lmax, v);
+  }
+  atomicMin(&vmin_s, lmin);
+  atomicMax(&vmax_s, lmax);
+  __syncthreads();
+  const int base = vmin_s & ~1;
+  if (tid == 0 && (vmax_s < 0 || (vmax_s - base) / 2 >= kRdBits)) fail_s = 1;
+  __syncthreads();
+  if (fail_s) {
+    if (tid == 0) atomicExch(a.stat, 1);
+    return;
+  }
+  for (int e = a0 + tid; e < a1; e += kRdThreads) {
+    const int p = (a.nadj[e] - base) >> 1; // the even-aligned vertex pair of the id
+    atomicOr(&bits[p >> 5], 1u << (p & 31));
+  }
+  __syncthreads();
+  // runs, in id order, merged across gaps of <= 8 vertices (4 pairs):
+  // build_nbr's make_runs on the sorted unique ids
+  if (tid == 0) {
+    const int npairs = (vmax_s - base) / 2 + 1;
+    int n = 0, slots = 0, lo = -1, hi = -1;
+    for (int p = 0; p < npairs; ++p) {
+      if (!((bits[p >> 5] >> (p & 31)) & 1u)) continue;
+      const int vlo = base + 2 * p, vhi = min(a.nrows, vlo + 2);
+      if (lo >= 0 && vlo <= hi + 8) {
+        hi = max(hi, vhi);
+      } else {
+        if (lo >= 0) {
+          if (n == kRdMaxRuns) { fail_s = 1; break; }
+          run_lo[n] = lo; run_hi[n] = hi; run_base[n] = slots; slots += hi - lo; ++n;
+        }
+        lo = vlo;
+        hi = vhi;
+      }
+    }
+    if (!fail_s && lo >= 0) {
+      if (n == kRdMaxRuns) fail_s = 1;
+      else { run_lo[n] = lo; run_hi[n] = hi; run_base[n] = slots; slots += hi - lo; ++n; }
+    }
+    if (slots > a.tile_slots) fail_s = 1;
+    nruns = n;
+    slots_s = slots;
+  }
+  __syncthreads();
+  if (fail_s) {
+    if (tid == 0) atomicExch(a.stat, 1);
+    return;
+  }
+  // window slot of every pattern entry of the tile
+  for (int e = a0 + tid; e < a1; e += kRdThreads) {
+    const int v = a.nadj[e];
+    int k = 0;
+    while (k + 1 < nruns && run_lo[k + 1] <= v) ++k;
+    eslot[e - a0] = (uint16_t)(run_base[k] + v - run_lo[k]);
+  }
+  __syncthreads();
+  // one thread per row: the star's chain (the host's ring / fan order)
+  const int r = r0 + tid;
+  bool ok = true;
+  if (r < r1) {
+    const int na0 = a.nptr[r], L = a.nptr[r + 1] - na0;
+    const int P = a.pptr[r + 1] - a.pptr[r];
+    const int rp = a.pptr[r] + r;
+    a.rptr[r] = rp;
+    if (r + 1 == a.nrows) a.rptr[r + 1] = a.pptr[r + 1] + r + 1;
+    auto rank_of = [&](int v) {
+      for (int q = 0; q < L; ++q)
+        if (a.nadj[na0 + q] == v) return q;
+      return -1;
+    };
+    auto rec = [&](int v, int& out) {
+      const int q = rank_of(v);
+      if (q < 0 || q > 7) return false;
+      out = (eslot[na0 + q - a0] << 4) | q;
+      return true;
+    };
+    int av[8], bv[8];
+    if (L > 8 || P > 7 || P == 0) ok = false;
+    for (int q = 0; q < P && ok; ++q) {
+      const int code = a.pairs[a.pptr[r] + q];
+      const int c = code / 3, i = code - 3 * c;
+      av[q] = a.rows[(int64_t)c * 3 + (i + 1) % 3];
+      bv[q] = a.rows[(int64_t)c * 3 + (i + 2) % 3];
+    }
+    int self = -1, start = 0, ones = 0;
+    if (ok) ok = rec(r, self);
+    if (ok) {
+      a.rowinfo[r] = (uint32_t)(self >> 4) | ((uint32_t)(self & 15) << 16);
+      start = av[0];
+      for (int q = 0; q < P && ok; ++q)
+        for (int u2 = 0; u2 < 2; ++u2) {
+          const int v = u2 ? bv[q] : av[q];
+          int deg = 0;
+          for (int u = 0; u < P; ++u) deg += (av[u] == v) + (bv[u] == v);
+          if (deg > 2 || v == r) ok = false;
+          if (deg == 1) { ++ones; start = v; }
+        }
+      if (ones != 0 && ones != 2) ok = false;
+    }
+    if (ok) {
+      unsigned used = 0u;
+      int v = start, x = 0;
+      ok = rec(v, x);
+      if (ok) a.rrecs[rp] = (uint16_t)x;
+      for (int k = 0; k < P && ok; ++k) {
+        int q = 0;
+        while (q < P && (((used >> q) & 1u) || (av[q] != v && bv[q] != v))) ++q;
+        if (q == P) { ok = false; break; }
+        used |= 1u << q;
+        v = av[q] == v ? bv[q] : av[q];
+        ok = rec(v, x);
+        if (ok) a.rrecs[rp + 1 + k] = (uint16_t)x;
+      }
+      if (ok && ones == 0 && v != start) ok = false; // a ring must close
+    }
+    if (!ok) atomicExch(a.stat, 1);
+    atomicMax(a.stat + 6, L);
+  }
+  if (tid == 0) {
+    int32_t* rt = a.rtiles + 16 * t;
+    rt[0] = r0; rt[1] = r1; rt[2] = a0; rt[3] = a1;
+    rt[4] = a.pptr[r0] + r0; rt[5] = a.pptr[r1] + r1;
+    rt[6] = t * kRdMaxRuns; rt[7] = nruns;
+    for (int q = 0; q < kRingInlineRuns; ++q) {
+      rt[8 + 2 * q] = q < nruns ? run_lo[q] : 0;
+      rt[9 + 2 * q] = q < nruns ? run_hi[q] : 0;
+    }
+    for (int q = 0; q < nruns; ++q) {
+      a.runs[2 * (t * kRdMaxRuns + q)] = run_lo[q];
+      a.runs[2 * (t * kRdMaxRuns + q) + 1] = run_hi[q];
+    }
+    atomicMax(a.stat + 1, r1 - r0);
+    atomicMax(a.stat + 2, a1 - a0);
+    atomicMax(a.stat + 3, rt[5] - rt[4]);
+    atomicMax(a.stat + 4, slots_s);
+    atomicMax(a.stat + 5, nruns);
+  }
+}
+
+} // namespace
+
+bool build_ring_dev(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrows_node, const CsrView& csr,
+                    int tile_rows, int tile_seg, int tile_slots, cudaStream_t s) {
+  if (csr.rd != 1 || csr.cd != 1 || !csr.row_ptr || nrows_node == 0 || tile_rows > kRdThreads ||
+      csr.nnz >= (int64_t(1) << 31) || (int64_t)tile_rows * 8 > tile_seg)
+    return false;
+  np.nrows_node = nrows_node;
+  np.nrn = 3;
+  np.rd = np.cd = 1;
+  const int64_t nn = csr.nnz;
+  np.nptr.alloc(nrows_node + 1 + 4, s);
+  LG_CUDA(cudaMemsetAsync(np.nptr.get(), 0, np.nptr.bytes(), s));
+  k_i64_to_i32<<<ceil_div(nrows_node + 1, kTPB), kTPB, 0, s>>>(csr.row_ptr, nrows_node + 1, np.nptr.get());
+  count_launch();
+  PairPlan pp;
+  build_pairs(sorted_rows, ncells, 3, nrows_node, pp, s);
+  const int ntiles = ceil_div(nrows_node, tile_rows);
+  const int64_t nrec = pp.npairs + nrows_node;
+  np.rptr.alloc(nrows_node + 1 + 4, s);
+  np.rrecs.alloc(nrec + 8, s);
+  np.rowinfo.alloc(nrows_node + 4, s);
+  np.rtiles.alloc((size_t)ntiles * 16, s);
+  np.runs.alloc((size_t)ntiles * kRdMaxRuns * 2 + 2, s);
+  LG_CUDA(cudaMemsetAsync(np.rptr.get(), 0, np.rptr.bytes(), s));
+  LG_CUDA(cudaMemsetAsync(np.rrecs.get(), 0, np.rrecs.bytes(), s));
+  DevBuf<int> stat(8, s);
+  LG_CUDA(cudaMemsetAsync(stat.get(), 0, stat.bytes(), s));
+  RingDevArgs a{sorted_rows, np.nptr.get(), csr.col_idx, pp.ptr.get(), pp.pairs.get(), nrows_node, tile_rows, ntiles,
+                std::min(tile_slots, 4095), np.rtiles.get(), np.runs.get(), np.rptr.get(), np.rrecs.get(),
+                np.rowinfo.get(), stat.get()};
+  k_ring_plan<<<ntiles, kRdThreads, 0, s>>>(a);
+  count_launch();
+  LG_LAUNCH_CHECK();
+  int h[8];
+  LG_CUDA(cudaMemcpyAsync(h, stat.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  if (h[0]) return false;
+  np.ring = true;
+  np.ntiles = ntiles;
+  np.max_rows = h[1];
+  np.max_adj = h[2];
+  np.max_pairs = h[3]; // ring records per tile (pairs + one head per row)
+  np.max_slots = h[4];
+  np.max_runs = h[5];
+  np.max_len = h[6];
+  np.max_seg = h[2];
+  (void)nn;
+  return true;
+}
+
 } // namespace loam_gpu

@@ -118,6 +118,12 @@ bool build_nbr(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrn, int
                const CsrView& csr, int tile_rows, int tile_seg, int tile_slots, int tile_runs,
                cudaStream_t s);
 
+// The ring mode of the neighbour plan built on the device (scalar P1 triangle
+// Mats, tiles of exactly tile_rows rows): false when a tile or a row needs the
+// host builder (build_nbr), which the caller then runs.
+bool build_ring_dev(NbrPlan& np, const int32_t* sorted_rows, int ncells, int nrows_node, const CsrView& csr,
+                    int tile_rows, int tile_seg, int tile_slots, cudaStream_t s);
+
 // Canonical pair-tile plan (any catalogue form on simplices).  Each pair
 // (row node r, cell e) is stored with the cell's local numbering PERMUTED so
 // that r is a canonical local node (vertex rows: local vertex 0; P2 edge rows:
