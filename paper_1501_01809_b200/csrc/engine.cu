@@ -1,3 +1,4 @@
+#include <climits>
 #include <chrono>
 // engine.cu -- the B200 par_loop engine: registry, validate, execute.
 //
@@ -1274,6 +1275,102 @@ __global__ void __launch_bounds__(256) k_wave_step(const __grid_constant__ StarA
 
 // Star records of the node map (host build; false if a star is not a single
 // ring or fan of <= 7 link vertices).
+// build_stars on the device: one thread per vertex, its link edges from the
+// pair plan (cells ascending, as the host loop meets them), the same chain
+// and header -- bitwise the host's records (tests/test_ring_plan_gpu.py).
+__global__ void k_star_plan(const int32_t* __restrict__ cv, const int32_t* __restrict__ ptr,
+                            const int32_t* __restrict__ pairs, int nverts, int4* __restrict__ rec, int* fail) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nverts) return;
+  const int b = ptr[r], nl = ptr[r + 1] - b;
+  int lx[7], ly[7], chain[8], m = 0;
+  bool closed = false;
+  if (nl > 7) { atomicExch(fail, 1); return; }
+  for (int k = 0; k < nl; ++k) {
+    const int code = pairs[b + k], c = code / 3, i = code - 3 * c;
+    lx[k] = cv[(int64_t)c * 3 + (i + 1) % 3];
+    ly[k] = cv[(int64_t)c * 3 + (i + 2) % 3];
+  }
+  if (nl > 0) {
+    auto deg = [&](int x) {
+      int d = 0;
+      for (int k = 0; k < nl; ++k) d += (lx[k] == x) + (ly[k] == x);
+      return d;
+    };
+    int start = lx[0], ends = 0;
+    for (int k = 0; k < nl; ++k)
+      for (int u = 0; u < 2; ++u) {
+        const int x = u ? ly[k] : lx[k];
+        const int d = deg(x);
+        if (d > 2 || x == r) { atomicExch(fail, 1); return; }
+        if (d == 1) ++ends;
+      }
+    if (ends != 0 && ends != 2) { atomicExch(fail, 1); return; }
+    if (ends == 2) { // the smaller end id, deterministic
+      start = INT_MAX;
+      for (int k = 0; k < nl; ++k)
+        for (int u = 0; u < 2; ++u) {
+          const int x = u ? ly[k] : lx[k];
+          if (deg(x) == 1) start = min(start, x);
+        }
+    }
+    closed = ends == 0;
+    unsigned used = 0u;
+    int cur = start;
+    chain[m++] = cur;
+    for (int step = 0; step < nl; ++step) {
+      int nxt = -1;
+      for (int k = 0; k < nl; ++k) {
+        if (used >> k & 1u) continue;
+        if (lx[k] == cur) nxt = ly[k];
+        else if (ly[k] == cur) nxt = lx[k];
+        else continue;
+        used |= 1u << k;
+        break;
+      }
+      if (nxt < 0) { atomicExch(fail, 1); return; } // several components
+      if (closed && step == nl - 1) {
+        if (nxt != start) { atomicExch(fail, 1); return; }
+        break;
+      }
+      if (m == 8) { atomicExch(fail, 1); return; }
+      chain[m++] = nxt;
+      cur = nxt;
+    }
+    if (m > 7 || (closed ? m != nl : m != nl + 1)) { atomicExch(fail, 1); return; }
+  }
+  int v[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int k = 0; k < m; ++k) v[k] = chain[k];
+  int hdr = m | (closed ? 8 : 0);
+  int rank_self = 0;
+  for (int k = 0; k < m; ++k) rank_self += v[k] < r;
+  hdr |= rank_self << 4;
+  for (int k = 0; k < m; ++k) {
+    int rk = v[k] > r;
+    for (int q = 0; q < m; ++q) rk += v[q] < v[k];
+    hdr |= rk << (7 + 3 * k);
+  }
+  rec[2 * r] = make_int4(hdr, v[0], v[1], v[2]);
+  rec[2 * r + 1] = make_int4(v[3], v[4], v[5], v[6]);
+}
+
+bool build_stars_dev(const int32_t* dmap, int ncells, int nverts, DevBuf<int4>& out, cudaStream_t s) {
+  PairPlan pp;
+  build_pairs(dmap, ncells, 3, nverts, pp, s);
+  out.alloc(2 * (size_t)std::max(nverts, 1), s);
+  DevBuf<int> fail(1, s);
+  LG_CUDA(cudaMemsetAsync(fail.get(), 0, sizeof(int), s));
+  if (nverts) {
+    k_star_plan<<<ceil_div(nverts, 256), 256, 0, s>>>(dmap, pp.ptr.get(), pp.pairs.get(), nverts, out.get(), fail.get());
+    count_launch();
+    LG_LAUNCH_CHECK();
+  }
+  int h = 0;
+  LG_CUDA(cudaMemcpyAsync(&h, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  return h == 0;
+}
+
 bool build_stars(const int32_t* dmap, int ncells, int nverts, DevBuf<int4>& out, cudaStream_t s) {
   std::vector<int32_t> cv((size_t)ncells * 3);
   LG_CUDA(cudaMemcpyAsync(cv.data(), dmap, sizeof(int32_t) * cv.size(), cudaMemcpyDeviceToHost, s));
@@ -2785,7 +2882,8 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
                           pattern_is_map_pattern(R.v.v, n, R.v.arity, R.v.target, 1, 1, csr.row_ptr, csr.col_idx,
                                                  csr.nnz, s));
     plan_tick("nbr checks", s);
-    if (star_ok && build_stars(R.v.v, n, R.v.target, P->star, s)) {
+    if (star_ok && (std::getenv("LOAM_GPU_HOST_RING") ? build_stars(R.v.v, n, R.v.target, P->star, s)
+                                                       : build_stars_dev(R.v.v, n, R.v.target, P->star, s))) {
       plan_tick("stars", s);
       if (k.bilinear) P->exact = true;
       P->use_star = true;
