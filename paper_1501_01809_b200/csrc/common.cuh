@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -147,6 +148,44 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
   if (e != cudaSuccess) throw Error(LOAM_GPU_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
+}
+
+// Uploads the concatenation of host byte vectors (one per plan chunk) into one
+// device buffer without building the concatenation on the host; returns the
+// byte offset of every part.  The copies run from all host cores (the
+// pageable-memory staging is CPU work).
+template <class Parts>
+std::vector<size_t> upload_parts(DevBuf<uint8_t>& dst, const Parts& parts, cudaStream_t s) {
+  std::vector<size_t> off(parts.size() + 1, 0);
+  for (size_t i = 0; i < parts.size(); ++i) off[i + 1] = off[i] + parts[i]->size();
+  dst.alloc(off.back() + 16, s);
+  LG_CUDA(cudaStreamSynchronize(s)); // the buffer exists before other threads copy into it
+  uint8_t* base = dst.get();
+  std::vector<std::thread> th;
+  std::vector<cudaError_t> err(parts.size(), cudaSuccess);
+  for (size_t i = 0; i < parts.size(); ++i)
+    th.emplace_back([&, i] {
+      if (!parts[i]->empty()) err[i] = cudaMemcpy(base + off[i], parts[i]->data(), parts[i]->size(), cudaMemcpyHostToDevice);
+    });
+  for (auto& x : th) x.join();
+  for (auto e : err)
+    if (e != cudaSuccess) throw Error(LOAM_GPU_ERR_CUDA, std::string("plan upload: ") + cudaGetErrorString(e));
+  return off;
+}
+
+// Device -> pageable host copies of a plan builder's inputs.
+struct D2H {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+// (A pinned staging buffer measured slower here: cudaMallocHost of the ~300
+// MB a P2 plan needs costs more than the pageable copies; threads per array
+// did not overlap the pageable staging either.)
+inline void parallel_d2h(const std::vector<D2H>& copies, cudaStream_t s) {
+  for (const D2H& c : copies)
+    if (c.bytes) LG_CUDA(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
 }
 
 // Host-side plan construction runs on all host cores: parallel_chunks(n, f)

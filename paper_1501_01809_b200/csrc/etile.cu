@@ -73,13 +73,13 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
   std::vector<int32_t> hrows((size_t)ncells * nrn), hx((size_t)ncells * nv), hpairs(np), hp(nrows_node + 1);
   std::vector<uint8_t> hrank((size_t)np * nrn);
   std::vector<int64_t> hrp((size_t)nrows_node * cd + 1);
-  LG_CUDA(cudaMemcpyAsync(hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hx.data(), sorted_x, sizeof(int32_t) * hx.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hpairs.data(), pp.pairs.get(), sizeof(int32_t) * np, cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hp.data(), pp.ptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hrank.data(), pp.ranks.get(), hrank.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hrp.data(), row_ptr, sizeof(int64_t) * hrp.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaStreamSynchronize(s));
+  parallel_d2h({{hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size()},
+                {hx.data(), sorted_x, sizeof(int32_t) * hx.size()},
+                {hpairs.data(), pp.pairs.get(), sizeof(int32_t) * (size_t)np},
+                {hp.data(), pp.ptr.get(), sizeof(int32_t) * (size_t)(nrows_node + 1)},
+                {hrank.data(), pp.ranks.get(), hrank.size()},
+                {hrp.data(), row_ptr, sizeof(int64_t) * hrp.size()}},
+               s);
   plan_tick("etile: D2H", s);
   // node-level pattern offsets (a cd x cd component-blocked CSR: node row i owns
   // dof rows cd*i .. cd*i+cd-1, each cd * L_i long)
@@ -468,18 +468,20 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
   }
   });
   std::vector<int32_t> tiles, runs;
-  std::vector<uint8_t> blob;
+  std::vector<const std::vector<uint8_t>*> parts;
+  size_t bytes_so_far = 0;
   for (int t = 0; t < ntch; ++t) {
     TileChunk& O = tch[t];
     if (!O.ok) return false;
-    const int bshift = (int)(blob.size() / 16), rshift = (int)(runs.size() / 2);
+    const int bshift = (int)(bytes_so_far / 16), rshift = (int)(runs.size() / 2);
     for (size_t q = 0; q < O.tiles.size(); q += 16) {
       O.tiles[q + 0] += bshift;
       O.tiles[q + 8] += rshift;
     }
     tiles.insert(tiles.end(), O.tiles.begin(), O.tiles.end());
     runs.insert(runs.end(), O.runs.begin(), O.runs.end());
-    blob.insert(blob.end(), O.blob.begin(), O.blob.end());
+    parts.push_back(&O.blob);
+    bytes_so_far += O.blob.size();
     out.max_segT = std::max(out.max_segT, O.max_segT);
     out.max_rows = std::max(out.max_rows, O.max_rows);
     out.max_seg = std::max(out.max_seg, O.max_seg);
@@ -487,6 +489,7 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
     out.max_slots = std::max(out.max_slots, O.max_slots);
     out.max_blob = std::max(out.max_blob, O.max_blob);
   }
+  upload_parts(out.blob, parts, s); // the chunks' blobs, uploaded in place (no host concatenation)
   tch.clear();
   plan_tick("etile: tiles", s);
   out.gd = gd;
@@ -506,7 +509,6 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       LG_CUDA(cudaMemcpyAsync(dst.get(), src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, s));
   };
   upload(out.tiles, tiles);
-  upload(out.blob, blob);
   upload(out.runs, runs);
   upload(out.diag, diag);
   out.det = sp.det;

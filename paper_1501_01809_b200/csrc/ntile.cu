@@ -1,3 +1,4 @@
+#include <chrono>
 // ntile.cu -- node-block tiles for vector P1 matrices (see ntile.cuh).
 //
 // Reference path replaced: assemble_matrix (fem/assemble.hpp:85-104) ->
@@ -56,13 +57,13 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
   std::vector<int32_t> hrows((size_t)ncells * kNV), hx((size_t)ncells * kNV), hpairs(np), hp(nnodes + 1);
   std::vector<uint8_t> hrank((size_t)np * kNV);
   std::vector<int64_t> hrp((size_t)nnodes * 3 + 1);
-  LG_CUDA(cudaMemcpyAsync(hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hx.data(), sorted_x, sizeof(int32_t) * hx.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hpairs.data(), pp.pairs.get(), sizeof(int32_t) * np, cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hp.data(), pp.ptr.get(), sizeof(int32_t) * (nnodes + 1), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hrank.data(), pp.ranks.get(), hrank.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hrp.data(), row_ptr, sizeof(int64_t) * hrp.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaStreamSynchronize(s));
+  parallel_d2h({{hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size()},
+                {hx.data(), sorted_x, sizeof(int32_t) * hx.size()},
+                {hpairs.data(), pp.pairs.get(), sizeof(int32_t) * (size_t)np},
+                {hp.data(), pp.ptr.get(), sizeof(int32_t) * (size_t)(nnodes + 1)},
+                {hrank.data(), pp.ranks.get(), hrank.size()},
+                {hrp.data(), row_ptr, sizeof(int64_t) * hrp.size()}},
+               s);
   plan_tick("ntile: D2H", s);
   std::vector<int64_t> nptr(nnodes + 1); // node-level pattern offsets of the 3x3-blocked CSR
   for (int i = 0; i <= nnodes; ++i) nptr[i] = hrp[(size_t)3 * i] / 9;
@@ -96,6 +97,8 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
     std::vector<int32_t> tiles, runs;
     std::vector<uint8_t> blob;
     int max_seg = 0, max_cells = 0, max_slots = 0, max_blob = 0, max_diag = 0;
+    double t_fits = 0, t_items = 0, t_blob = 0; // developer timing (LOAM_GPU_PLAN_TIMING)
+    int64_t n_fits = 0, n_tiles = 0;
   };
   std::vector<TileChunk> tch(plan_threads());
   const int ntch = parallel_chunks(nnodes, sp.tile_nodes, [&](int t, int64_t cb0, int64_t cb1) {
@@ -105,14 +108,16 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
   std::vector<uint8_t>& blob = O.blob;
   std::vector<int> vid; // (no per-thread ncells-sized arrays: cell sets are sorted vectors)
   std::vector<std::pair<int, int>> rr;
-  std::vector<std::vector<uint32_t>> lists; // per rank of a row: (cell << 4 | lv << 2 | lw)
-  std::vector<ItemRec> items;
-  std::vector<uint16_t> prec, diaginfo;
+  // per-tile scratch reused across tiles (no allocation in the hot loop)
+  std::vector<uint32_t> flat;   // a row's per-rank lists, flattened: (cell << 4 | lv << 2 | lw)
+  std::vector<int> lcnt, lpos;  // per-rank list offsets / fill cursors
+  std::vector<ItemRec> items, ditems;
+  std::vector<uint16_t> prec, diaginfo, dprec, inter;
+  std::vector<int> cells, base;
   const int vend = (int)cb1;
   int v0 = (int)cb0;
   while (v0 < vend) {
     int v1 = std::min(vend, v0 + sp.tile_nodes);
-    std::vector<int> cells;
     int slots = 0;
     auto fits = [&](int a, int b) {
       if (9 * (nptr[b] - nptr[a]) > 60000) return false;
@@ -133,13 +138,18 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
       slots = make_runs(vid, nverts, rr);
       return slots <= sp.tile_slots && (int)rr.size() <= sp.tile_runs;
     };
+    const auto tp0 = std::chrono::steady_clock::now();
+    int nfits = 1;
     while (!fits(v0, v1)) {
       if (v1 == v0 + 1) { O.ok = false; return; }
       v1 = v0 + (v1 - v0) / 2;
+      ++nfits;
     }
-    std::sort(cells.begin(), cells.end());
+    const auto tp1 = std::chrono::steady_clock::now();
+    O.t_fits += std::chrono::duration<double>(tp1 - tp0).count();
+    O.n_fits += nfits;
     auto local_of = [&](int c) { return (int)(std::lower_bound(cells.begin(), cells.end(), c) - cells.begin()); };
-    std::vector<int> base(rr.size());
+    base.resize(rr.size());
     for (size_t q = 0, acc = 0; q < rr.size(); ++q) {
       base[q] = (int)acc;
       acc += rr[q].second - rr[q].first;
@@ -152,33 +162,41 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
     items.clear();
     prec.clear();
     diaginfo.clear();
-    std::vector<ItemRec> ditems;
-    std::vector<uint16_t> dprec;
+    ditems.clear();
+    dprec.clear();
     const int64_t S0 = nptr[v0];
     for (int v = v0; v < v1; ++v) {
       const int L = (int)(nptr[v + 1] - nptr[v]);
-      lists.assign(L, {});
+      // per-rank lists in (pair, lw) order, flattened by a counting pass
+      lcnt.assign(L + 1, 0);
+      for (int p = hp[v]; p < hp[v + 1]; ++p)
+        for (int lw = 0; lw < kNV; ++lw) ++lcnt[hrank[(size_t)p * kNV + lw] + 1];
+      for (int r = 0; r < L; ++r) lcnt[r + 1] += lcnt[r];
+      lpos.assign(lcnt.begin(), lcnt.end() - 1);
+      flat.resize(lcnt[L]);
       int self = -1;
       for (int p = hp[v]; p < hp[v + 1]; ++p) {
         const int c = hpairs[p] / kNV, lv = hpairs[p] % kNV;
+        const uint32_t loc = (uint32_t)local_of(c) << 4;
         for (int lw = 0; lw < kNV; ++lw) {
           const int r = hrank[(size_t)p * kNV + lw];
-          lists[r].push_back((uint32_t)local_of(c) << 4 | (uint32_t)lv << 2 | (uint32_t)lw);
+          flat[lpos[r]++] = loc | (uint32_t)lv << 2 | (uint32_t)lw;
           if (lw == lv) self = r;
         }
       }
       const uint16_t rowb = (uint16_t)(9 * (nptr[v] - S0)), stride = (uint16_t)(3 * L);
       for (int r = 0; r < L; ++r) {
         if (r == self) continue;
-        items.push_back(ItemRec{(uint16_t)prec.size(), (uint8_t)lists[r].size(), 0, (uint16_t)(rowb + 3 * r), stride});
-        for (uint32_t x : lists[r]) prec.push_back((uint16_t)x);
-        if (lists[r].size() > 255) { O.ok = false; return; }
+        const int len = lcnt[r + 1] - lcnt[r];
+        if (len > 255) { O.ok = false; return; }
+        items.push_back(ItemRec{(uint16_t)prec.size(), (uint8_t)len, 0, (uint16_t)(rowb + 3 * r), stride});
+        for (int q = lcnt[r]; q < lcnt[r + 1]; ++q) prec.push_back((uint16_t)flat[q]);
       }
       const int di = (int)diaginfo.size() / 2;
       diaginfo.push_back((uint16_t)(rowb + 3 * self));
       diaginfo.push_back(stride);
-      const auto& dl = lists[self];
-      const int n = (int)dl.size();
+      const uint32_t* dl = flat.data() + lcnt[self];
+      const int n = lcnt[self + 1] - lcnt[self];
       for (int part = 0; part < kDiagSplit; ++part) {
         const int a = n * part / kDiagSplit, b = n * (part + 1) / kDiagSplit;
         ditems.push_back(ItemRec{(uint16_t)dprec.size(), (uint8_t)(b - a), 1, (uint16_t)(di * kDiagSplit + part), 0});
@@ -198,7 +216,7 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
     // block(r) + q * kNtConsumers + l (the lanes of a warp read consecutive
     // half-words: no shared-memory bank conflicts)
     {
-      std::vector<uint16_t> inter;
+      inter.clear();
       for (size_t r0i = 0; r0i < items.size(); r0i += kNtConsumers) {
         const size_t r1i = std::min(items.size(), r0i + kNtConsumers);
         int pm = 0;
@@ -214,6 +232,8 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
       }
       prec.swap(inter);
     }
+    const auto tp2 = std::chrono::steady_clock::now();
+    O.t_items += std::chrono::duration<double>(tp2 - tp1).count();
     const int nitems = (int)items.size(), npairs = (int)prec.size(), ncell = (int)cells.size(),
               ndiag = (int)diaginfo.size() / 2;
     const int off_items = 0, off_pairs = up16(nitems * 8), off_diag = off_pairs + up16(npairs * 2),
@@ -239,30 +259,44 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
     O.max_slots = std::max(O.max_slots, slots);
     O.max_blob = std::max(O.max_blob, bytes);
     O.max_diag = std::max(O.max_diag, ndiag);
+    O.t_blob += std::chrono::duration<double>(std::chrono::steady_clock::now() - tp2).count();
+    ++O.n_tiles;
     v0 = v1;
   }
   });
   std::vector<int32_t> tiles, runs;
-  std::vector<uint8_t> blob;
+  std::vector<const std::vector<uint8_t>*> parts;
+  size_t bytes_so_far = 0;
   for (int t = 0; t < ntch; ++t) {
     TileChunk& O = tch[t];
     if (!O.ok) return false;
-    const int bshift = (int)(blob.size() / 16), rshift = (int)(runs.size() / 2);
+    const int bshift = (int)(bytes_so_far / 16), rshift = (int)(runs.size() / 2);
     for (size_t q = 0; q < O.tiles.size(); q += 16) {
       O.tiles[q + 0] += bshift;
       O.tiles[q + 8] += rshift;
     }
     tiles.insert(tiles.end(), O.tiles.begin(), O.tiles.end());
     runs.insert(runs.end(), O.runs.begin(), O.runs.end());
-    blob.insert(blob.end(), O.blob.begin(), O.blob.end());
+    parts.push_back(&O.blob);
+    bytes_so_far += O.blob.size();
     out.max_seg = std::max(out.max_seg, O.max_seg);
     out.max_cells = std::max(out.max_cells, O.max_cells);
     out.max_slots = std::max(out.max_slots, O.max_slots);
     out.max_blob = std::max(out.max_blob, O.max_blob);
     out.max_diag = std::max(out.max_diag, O.max_diag);
   }
-  tch.clear();
+  if (std::getenv("LOAM_GPU_PLAN_TIMING")) {
+    double f = 0, it = 0, bl = 0;
+    int64_t nf = 0, nt = 0;
+    for (int t = 0; t < ntch; ++t) {
+      f += tch[t].t_fits; it += tch[t].t_items; bl += tch[t].t_blob; nf += tch[t].n_fits; nt += tch[t].n_tiles;
+    }
+    fprintf(stderr, "[plan] ntile: %d chunks, %lld tiles, %lld fits calls; thread-seconds fits %.3f items %.3f blob %.3f\n",
+            ntch, (long long)nt, (long long)nf, f, it, bl);
+  }
   plan_tick("ntile: tiles", s);
+  upload_parts(out.blob, parts, s); // the chunks' blobs, uploaded in place (no host concatenation)
+  tch.clear();
   out.ntiles = (int)tiles.size() / 16;
   auto upload = [&](auto& dst, const auto& src) {
     using T = typename std::decay_t<decltype(src)>::value_type;
@@ -271,7 +305,6 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
       LG_CUDA(cudaMemcpyAsync(dst.get(), src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, s));
   };
   upload(out.tiles, tiles);
-  upload(out.blob, blob);
   upload(out.runs, runs);
   LG_CUDA(cudaStreamSynchronize(s));
   return true;

@@ -616,26 +616,20 @@ bool build_ptile(PTilePlan& out, const PTileSpec& sp, int ncells, int nrows_node
   // ---- host copies
   std::vector<int32_t> hrows((size_t)ncells * nrn), hx((size_t)ncells * nv), hcols, hcf, hpairs(np), hp(nrows_node + 1);
   std::vector<uint8_t> hrank;
-  LG_CUDA(cudaMemcpyAsync(hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hx.data(), sorted_x, sizeof(int32_t) * hx.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hpairs.data(), pp.pairs.get(), sizeof(int32_t) * np, cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hp.data(), pp.ptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
-  if (ncn) {
-    hrank.resize((size_t)np * ncn);
-    LG_CUDA(cudaMemcpyAsync(hrank.data(), pp.ranks.get(), hrank.size(), cudaMemcpyDeviceToHost, s));
-  }
-  if (ncf) {
-    hcf.resize((size_t)ncells * ncf);
-    LG_CUDA(cudaMemcpyAsync(hcf.data(), sorted_coeff, sizeof(int32_t) * hcf.size(), cudaMemcpyDeviceToHost, s));
-  }
-  std::vector<int64_t> hn(nrows_node + 1, 0);
-  if (ncn) { // node-level pattern offsets from the (blocked) CSR
-    std::vector<int64_t> rp((size_t)nrows_node * csr.rd + 1);
-    LG_CUDA(cudaMemcpyAsync(rp.data(), csr.row_ptr, sizeof(int64_t) * rp.size(), cudaMemcpyDeviceToHost, s));
-    LG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int64_t> hn(nrows_node + 1, 0), rp;
+  if (ncn) hrank.resize((size_t)np * ncn);
+  if (ncf) hcf.resize((size_t)ncells * ncf);
+  if (ncn) rp.resize((size_t)nrows_node * csr.rd + 1);
+  parallel_d2h({{hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size()},
+                {hx.data(), sorted_x, sizeof(int32_t) * hx.size()},
+                {hpairs.data(), pp.pairs.get(), sizeof(int32_t) * (size_t)np},
+                {hp.data(), pp.ptr.get(), sizeof(int32_t) * (size_t)(nrows_node + 1)},
+                {hrank.data(), pp.ranks.get(), hrank.size()},
+                {hcf.data(), sorted_coeff, sizeof(int32_t) * hcf.size()},
+                {rp.data(), csr.row_ptr, sizeof(int64_t) * rp.size()}},
+               s);
+  if (ncn) // node-level pattern offsets from the (blocked) CSR
     for (int r = 0; r <= nrows_node; ++r) hn[r] = rp[(size_t)r * csr.rd] / ((int64_t)csr.rd * csr.cd);
-  }
-  LG_CUDA(cudaStreamSynchronize(s));
   (void)sorted_cols;
   const int W = sp.rd * sp.cd;
   // ---- record layout

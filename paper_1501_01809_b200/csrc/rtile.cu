@@ -57,12 +57,12 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
   std::vector<int32_t> hx((size_t)ncells * nv), hpairs(np), hp(nrows_node + 1);
   std::vector<uint8_t> hrank((size_t)np * ncn);
   std::vector<int64_t> hrp((size_t)nrows_node * rd + 1);
-  LG_CUDA(cudaMemcpyAsync(hx.data(), sorted_x, sizeof(int32_t) * hx.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hpairs.data(), pp.pairs.get(), sizeof(int32_t) * np, cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hp.data(), pp.ptr.get(), sizeof(int32_t) * (nrows_node + 1), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hrank.data(), pp.ranks.get(), hrank.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaMemcpyAsync(hrp.data(), row_ptr, sizeof(int64_t) * hrp.size(), cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaStreamSynchronize(s));
+  parallel_d2h({{hx.data(), sorted_x, sizeof(int32_t) * hx.size()},
+                {hpairs.data(), pp.pairs.get(), sizeof(int32_t) * (size_t)np},
+                {hp.data(), pp.ptr.get(), sizeof(int32_t) * (size_t)(nrows_node + 1)},
+                {hrank.data(), pp.ranks.get(), hrank.size()},
+                {hrp.data(), row_ptr, sizeof(int64_t) * hrp.size()}},
+               s);
   std::vector<int64_t> nptr(nrows_node + 1); // node-level pattern offsets of the rd x cd blocked CSR
   for (int i = 0; i <= nrows_node; ++i) nptr[i] = hrp[(size_t)rd * i] / (rd * cd);
   // ---- canonical pair records: u32 header (tile cell | canonical->original
@@ -224,24 +224,27 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
   }
   });
   std::vector<int32_t> tiles, runs;
-  std::vector<uint8_t> blob;
+  std::vector<const std::vector<uint8_t>*> parts;
+  size_t bytes_so_far = 0;
   for (int t = 0; t < ntch; ++t) {
     TileChunk& O = tch[t];
     if (!O.ok) return false;
-    const int bshift = (int)(blob.size() / 16), rshift = (int)(runs.size() / 2);
+    const int bshift = (int)(bytes_so_far / 16), rshift = (int)(runs.size() / 2);
     for (size_t q = 0; q < O.tiles.size(); q += 16) {
       O.tiles[q + 0] += bshift;
       O.tiles[q + 8] += rshift;
     }
     tiles.insert(tiles.end(), O.tiles.begin(), O.tiles.end());
     runs.insert(runs.end(), O.runs.begin(), O.runs.end());
-    blob.insert(blob.end(), O.blob.begin(), O.blob.end());
+    parts.push_back(&O.blob);
+    bytes_so_far += O.blob.size();
     out.max_seg = std::max(out.max_seg, O.max_seg);
     out.max_segT = std::max(out.max_segT, O.max_segT);
     out.max_cells = std::max(out.max_cells, O.max_cells);
     out.max_slots = std::max(out.max_slots, O.max_slots);
     out.max_blob = std::max(out.max_blob, O.max_blob);
   }
+  upload_parts(out.blob, parts, s); // the chunks' blobs, uploaded in place (no host concatenation)
   tch.clear();
   out.form = form;
   out.ntiles = (int)tiles.size() / 16;
@@ -253,7 +256,6 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
       LG_CUDA(cudaMemcpyAsync(dst.get(), src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, s));
   };
   upload(out.tiles, tiles);
-  upload(out.blob, blob);
   upload(out.runs, runs);
   LG_CUDA(cudaStreamSynchronize(s));
   return true;
