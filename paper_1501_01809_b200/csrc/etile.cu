@@ -70,9 +70,10 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
   if (pp.nrn != nrn || pp.ncn != nrn || nnz >= (int64_t(1) << 31) || ncells == 0 || ncells >= (1 << 30))
     return false;
   const int64_t np = pp.npairs;
-  std::vector<int32_t> hrows((size_t)ncells * nrn), hx((size_t)ncells * nv), hpairs(np), hp(nrows_node + 1);
-  std::vector<uint8_t> hrank((size_t)np * nrn);
-  std::vector<int64_t> hrp((size_t)nrows_node * cd + 1);
+  auto hrows = host_array<int32_t>((size_t)ncells * nrn), hx = host_array<int32_t>((size_t)ncells * nv),
+       hpairs = host_array<int32_t>(np), hp = host_array<int32_t>(nrows_node + 1);
+  auto hrank = host_array<uint8_t>((size_t)np * nrn);
+  auto hrp = host_array<int64_t>((size_t)nrows_node * cd + 1);
   parallel_d2h({{hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size()},
                 {hx.data(), sorted_x, sizeof(int32_t) * hx.size()},
                 {hpairs.data(), pp.pairs.get(), sizeof(int32_t) * (size_t)np},
@@ -127,9 +128,15 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
     keys[e] = (uint64_t)(uint32_t)eA[e] << 32 | (uint32_t)eB[e];
   }
   {
-    std::vector<uint64_t> ks(keys);
-    std::sort(ks.begin(), ks.end());
-    if (std::adjacent_find(ks.begin(), ks.end()) != ks.end()) return false;
+    // strictly increasing keys (the lexicographic edge numbering of
+    // space.hpp:48-57) are distinct without a sort
+    bool increasing = true;
+    for (size_t e = 1; e < keys.size() && increasing; ++e) increasing = keys[e - 1] < keys[e];
+    if (!increasing) {
+      std::vector<uint64_t> ks(keys);
+      std::sort(ks.begin(), ks.end());
+      if (std::adjacent_find(ks.begin(), ks.end()) != ks.end()) return false;
+    }
   }
   auto find_pair = [&](int w, int c) -> int64_t {
     for (int p = hp[w]; p < hp[w + 1]; ++p)
@@ -173,10 +180,11 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
   // length transposed-position lists concatenated in row order afterwards)
   const int rb = (2 + nrn + 3) & ~3;
   const int64_t p0e = hp[E0], npe = hp[nrows_node] - p0e;
-  std::vector<int32_t> tptr(nedge + 1, 0), tpos, tlen, cellof(npe);
+  std::vector<int32_t> tptr(nedge + 1, 0), tpos, tlen;
+  auto cellof = host_array<int32_t>(npe);
   std::vector<int4> xpos(nedge);
   std::vector<int2> xlen(cd == 2 ? nedge : 0);
-  std::vector<uint8_t> recs((size_t)npe * rb, 0);
+  auto recs = host_array<uint8_t>((size_t)npe * rb); // zeroed by the parallel first touch
   struct RecChunk {
     int64_t eb = 0, ee = 0;
     bool ok = true;

@@ -1,3 +1,4 @@
+#include <atomic>
 #include <chrono>
 // ntile.cu -- node-block tiles for vector P1 matrices (see ntile.cuh).
 //
@@ -54,9 +55,10 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
                  cudaStream_t s) {
   if (pp.nrn != kNV || pp.ncn != kNV || nnz >= (int64_t(1) << 31) || ncells == 0) return false;
   const int64_t np = pp.npairs;
-  std::vector<int32_t> hrows((size_t)ncells * kNV), hx((size_t)ncells * kNV), hpairs(np), hp(nnodes + 1);
-  std::vector<uint8_t> hrank((size_t)np * kNV);
-  std::vector<int64_t> hrp((size_t)nnodes * 3 + 1);
+  auto hrows = host_array<int32_t>((size_t)ncells * kNV), hx = host_array<int32_t>((size_t)ncells * kNV),
+       hpairs = host_array<int32_t>(np), hp = host_array<int32_t>(nnodes + 1);
+  auto hrank = host_array<uint8_t>((size_t)np * kNV);
+  auto hrp = host_array<int64_t>((size_t)nnodes * 3 + 1);
   parallel_d2h({{hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size()},
                 {hx.data(), sorted_x, sizeof(int32_t) * hx.size()},
                 {hpairs.data(), pp.pairs.get(), sizeof(int32_t) * (size_t)np},
@@ -69,19 +71,29 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
   for (int i = 0; i <= nnodes; ++i) nptr[i] = hrp[(size_t)3 * i] / 9;
   // every pattern block of every row must be reached by some cell (exact (map, map) pattern)
   {
-    std::vector<uint8_t> seen;
-    for (int v = 0; v < nnodes; ++v) {
-      const int L = (int)(nptr[v + 1] - nptr[v]);
-      seen.assign(L, 0);
-      for (int p = hp[v]; p < hp[v + 1]; ++p)
-        for (int j = 0; j < kNV; ++j) {
-          const int r = hrank[(size_t)p * kNV + j];
-          if (r >= L) return false;
-          seen[r] = 1;
-        }
-      for (int r = 0; r < L; ++r)
-        if (!seen[r]) return false;
-    }
+    std::atomic<bool> exact{true};
+    parallel_chunks(nnodes, 1, [&](int, int64_t v0, int64_t v1) {
+      std::vector<uint8_t> seen;
+      for (int64_t v = v0; v < v1 && exact; ++v) {
+        const int L = (int)(nptr[v + 1] - nptr[v]);
+        seen.assign(L, 0);
+        for (int p = hp[v]; p < hp[v + 1]; ++p)
+          for (int j = 0; j < kNV; ++j) {
+            const int r = hrank[(size_t)p * kNV + j];
+            if (r >= L) {
+              exact = false;
+              return;
+            }
+            seen[r] = 1;
+          }
+        for (int r = 0; r < L; ++r)
+          if (!seen[r]) {
+            exact = false;
+            return;
+          }
+      }
+    });
+    if (!exact) return false;
   }
   plan_tick("ntile: exact-pattern check", s);
   struct ItemRec { // 8 bytes

@@ -614,8 +614,10 @@ bool build_ptile(PTilePlan& out, const PTileSpec& sp, int ncells, int nrows_node
   const int gd = sp.gd, nv = gd + 1, nrn = sp.nrn, ncn = sp.ncn, ncf = sp.ncoeff;
   const int64_t np = pp.npairs;
   // ---- host copies
-  std::vector<int32_t> hrows((size_t)ncells * nrn), hx((size_t)ncells * nv), hcols, hcf, hpairs(np), hp(nrows_node + 1);
-  std::vector<uint8_t> hrank;
+  auto hrows = host_array<int32_t>((size_t)ncells * nrn), hx = host_array<int32_t>((size_t)ncells * nv),
+       hpairs = host_array<int32_t>(np), hp = host_array<int32_t>(nrows_node + 1);
+  std::vector<int32_t> hcols, hcf;
+  hvec<uint8_t> hrank;
   std::vector<int64_t> hn(nrows_node + 1, 0), rp;
   if (ncn) hrank.resize((size_t)np * ncn);
   if (ncf) hcf.resize((size_t)ncells * ncf);

@@ -54,9 +54,10 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
   (void)sorted_rows;
   if (!rtile_form(form) || pp.nrn != nrn || pp.ncn != ncn || nnz >= (int64_t(1) << 31) || ncells == 0) return false;
   const int64_t np = pp.npairs;
-  std::vector<int32_t> hx((size_t)ncells * nv), hpairs(np), hp(nrows_node + 1);
-  std::vector<uint8_t> hrank((size_t)np * ncn);
-  std::vector<int64_t> hrp((size_t)nrows_node * rd + 1);
+  auto hx = host_array<int32_t>((size_t)ncells * nv), hpairs = host_array<int32_t>(np),
+       hp = host_array<int32_t>(nrows_node + 1);
+  auto hrank = host_array<uint8_t>((size_t)np * ncn);
+  auto hrp = host_array<int64_t>((size_t)nrows_node * rd + 1);
   parallel_d2h({{hx.data(), sorted_x, sizeof(int32_t) * hx.size()},
                 {hpairs.data(), pp.pairs.get(), sizeof(int32_t) * (size_t)np},
                 {hp.data(), pp.ptr.get(), sizeof(int32_t) * (size_t)(nrows_node + 1)},
