@@ -341,6 +341,15 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
   std::vector<int32_t>& runs = O.runs;
   std::vector<uint8_t>& blob = O.blob;
   std::vector<int> vid; // (no per-thread ncells-sized arrays: cell sets are sorted vectors)
+  // generation stamps over all cells / vertices (calloc'd: only touched pages map)
+  struct Stamps {
+    int* p;
+    explicit Stamps(size_t n) : p(static_cast<int*>(std::calloc(n + 1, sizeof(int)))) {
+      if (!p) throw std::bad_alloc();
+    }
+    ~Stamps() { std::free(p); }
+  } cstamp(ncells), vstamp(nverts), clocal(ncells);
+  int gen = 0;
   std::vector<std::pair<int, int>> rr;
   int r0 = (int)cb0;
   const int rend = (int)cb1;
@@ -373,14 +382,24 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       if (hp[E0 + b] - hp[E0 + a] > sp.tile_pairs) return false;
       for (int r = a; r < b; ++r)
         if (hp[E0 + r + 1] - hp[E0 + r] > 255) return false;
+      ++gen;
       cells.clear();
-      for (int p = hp[E0 + a]; p < hp[E0 + b]; ++p) cells.push_back(cellof[p - p0e]);
-      std::sort(cells.begin(), cells.end());
-      cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
-      if ((int)cells.size() > cell_cap) return false;
       vid.clear();
-      for (int c : cells)
-        for (int v = 0; v < nv; ++v) vid.push_back(hx[(size_t)c * nv + v]);
+      for (int p = hp[E0 + a]; p < hp[E0 + b]; ++p) { // distinct cells (pair order) and their distinct vertices
+        const int c = cellof[p - p0e];
+        if (cstamp.p[c] == gen) continue;
+        cstamp.p[c] = gen;
+        clocal.p[c] = (int)cells.size();
+        cells.push_back(c);
+        for (int v = 0; v < nv; ++v) {
+          const int x = hx[(size_t)c * nv + v];
+          if (vstamp.p[x] != gen) {
+            vstamp.p[x] = gen;
+            vid.push_back(x);
+          }
+        }
+      }
+      if ((int)cells.size() > cell_cap) return false;
       slots = make_runs(vid, nverts, rr);
       return slots <= sp.tile_slots && (int)rr.size() <= sp.tile_runs;
     };
@@ -392,8 +411,11 @@ bool build_etile(EtilePlan& out, const EtileSpec& sp, int gd, int ncells, int nr
       r1 = r0 + (r1 - r0) / 2;
     }
     const int segT = warp_sizes(r0, r1, lmax, pmax);
+    // cells in id order (the locality order: neighbouring cells share Gram /
+    // gradient rows in shared memory), local ids renumbered to match
     std::sort(cells.begin(), cells.end());
-    auto local_of = [&](int c) { return (int)(std::lower_bound(cells.begin(), cells.end(), c) - cells.begin()); };
+    for (size_t q = 0; q < cells.size(); ++q) clocal.p[cells[q]] = (int)q;
+    auto local_of = [&](int c) { return clocal.p[c]; };
     std::vector<int> base(rr.size());
     for (size_t q = 0, acc = 0; q < rr.size(); ++q) {
       base[q] = (int)acc;

@@ -118,7 +118,7 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
   std::vector<int32_t>& tiles = O.tiles;
   std::vector<int32_t>& runs = O.runs;
   std::vector<uint8_t>& blob = O.blob;
-  std::vector<int> vid; // (no per-thread ncells-sized arrays: cell sets are sorted vectors)
+  std::vector<int> vid;
   std::vector<std::pair<int, int>> rr;
   // per-tile scratch reused across tiles (no allocation in the hot loop)
   std::vector<uint32_t> flat;   // a row's per-rank lists, flattened: (cell << 4 | lv << 2 | lw)
@@ -126,6 +126,16 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
   std::vector<ItemRec> items, ditems;
   std::vector<uint16_t> prec, diaginfo, dprec, inter;
   std::vector<int> cells, base;
+  // generation stamps over all cells / vertices: calloc'd, so only the pages a
+  // chunk touches are ever mapped (a chunk's tiles stay in a narrow id range)
+  struct Stamps {
+    int* p;
+    explicit Stamps(size_t n) : p(static_cast<int*>(std::calloc(n + 1, sizeof(int)))) {
+      if (!p) throw std::bad_alloc();
+    }
+    ~Stamps() { std::free(p); }
+  } cstamp(ncells), vstamp(nverts), clocal(ncells);
+  int gen = 0;
   const int vend = (int)cb1;
   int v0 = (int)cb0;
   while (v0 < vend) {
@@ -139,14 +149,24 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
         npr += 4 * (hp[v + 1] - hp[v]);
       }
       if (nit > sp.tile_items || npr > sp.tile_pairs) return false;
+      ++gen;
       cells.clear();
-      for (int p = hp[a]; p < hp[b]; ++p) cells.push_back(hpairs[p] / kNV);
-      std::sort(cells.begin(), cells.end());
-      cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
-      if ((int)cells.size() > std::min(sp.tile_cells, 1023)) return false;
       vid.clear();
-      for (int c : cells)
-        for (int v = 0; v < kNV; ++v) vid.push_back(hx[(size_t)c * kNV + v]);
+      for (int p = hp[a]; p < hp[b]; ++p) { // distinct cells (pair order) and their distinct vertices
+        const int c = hpairs[p] / kNV;
+        if (cstamp.p[c] == gen) continue;
+        cstamp.p[c] = gen;
+        clocal.p[c] = (int)cells.size();
+        cells.push_back(c);
+        for (int v = 0; v < kNV; ++v) {
+          const int x = hx[(size_t)c * kNV + v];
+          if (vstamp.p[x] != gen) {
+            vstamp.p[x] = gen;
+            vid.push_back(x);
+          }
+        }
+      }
+      if ((int)cells.size() > std::min(sp.tile_cells, 1023)) return false;
       slots = make_runs(vid, nverts, rr);
       return slots <= sp.tile_slots && (int)rr.size() <= sp.tile_runs;
     };
@@ -160,7 +180,11 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
     const auto tp1 = std::chrono::steady_clock::now();
     O.t_fits += std::chrono::duration<double>(tp1 - tp0).count();
     O.n_fits += nfits;
-    auto local_of = [&](int c) { return (int)(std::lower_bound(cells.begin(), cells.end(), c) - cells.begin()); };
+    // cells in id order (the locality order: neighbouring cells share Gram /
+    // gradient rows in shared memory), local ids renumbered to match
+    std::sort(cells.begin(), cells.end());
+    for (size_t q = 0; q < cells.size(); ++q) clocal.p[cells[q]] = (int)q;
+    auto local_of = [&](int c) { return clocal.p[c]; };
     base.resize(rr.size());
     for (size_t q = 0, acc = 0; q < rr.size(); ++q) {
       base[q] = (int)acc;

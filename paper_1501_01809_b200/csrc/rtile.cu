@@ -107,6 +107,15 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
   std::vector<int32_t>& runs = O.runs;
   std::vector<uint8_t>& blob = O.blob;
   std::vector<int> vid, lrow;
+  // generation stamps over all cells / vertices (calloc'd: only touched pages map)
+  struct Stamps {
+    int* p;
+    explicit Stamps(size_t n) : p(static_cast<int*>(std::calloc(n + 1, sizeof(int)))) {
+      if (!p) throw std::bad_alloc();
+    }
+    ~Stamps() { std::free(p); }
+  } cstamp(ncells), vstamp(nverts), clocal(ncells);
+  int gen = 0;
   std::vector<std::pair<int, int>> rr;
   std::vector<int> lmax, pmax;
   auto warp_sizes = [&](int a, int b) {
@@ -136,14 +145,24 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
       if (hp[b] - hp[a] > sp.tile_pairs) return false;
       for (int r = a; r < b; ++r)
         if (hp[r + 1] - hp[r] > 255) return false;
+      ++gen;
       cells.clear();
-      for (int p = hp[a]; p < hp[b]; ++p) cells.push_back(hpairs[p] / nrn);
-      std::sort(cells.begin(), cells.end());
-      cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
-      if ((int)cells.size() > std::min(sp.tile_cells, 1023)) return false;
       vid.clear();
-      for (int c : cells)
-        for (int v = 0; v < nv; ++v) vid.push_back(hx[(size_t)c * nv + v]);
+      for (int p = hp[a]; p < hp[b]; ++p) { // distinct cells (pair order) and their distinct vertices
+        const int c = hpairs[p] / nrn;
+        if (cstamp.p[c] == gen) continue;
+        cstamp.p[c] = gen;
+        clocal.p[c] = (int)cells.size();
+        cells.push_back(c);
+        for (int v = 0; v < nv; ++v) {
+          const int x = hx[(size_t)c * nv + v];
+          if (vstamp.p[x] != gen) {
+            vstamp.p[x] = gen;
+            vid.push_back(x);
+          }
+        }
+      }
+      if ((int)cells.size() > std::min(sp.tile_cells, 1023)) return false;
       slots = make_runs(vid, nverts, rr);
       return slots <= sp.tile_slots && (int)rr.size() <= sp.tile_runs;
     };
@@ -155,8 +174,11 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
       r1 = r0 + (r1 - r0) / 2;
     }
     const int segT = warp_sizes(r0, r1);
+    // cells in id order (the locality order: neighbouring cells share Gram /
+    // gradient rows in shared memory), local ids renumbered to match
     std::sort(cells.begin(), cells.end());
-    auto local_of = [&](int c) { return (int)(std::lower_bound(cells.begin(), cells.end(), c) - cells.begin()); };
+    for (size_t q = 0; q < cells.size(); ++q) clocal.p[cells[q]] = (int)q;
+    auto local_of = [&](int c) { return clocal.p[c]; };
     std::vector<int> base(rr.size());
     for (size_t q = 0, acc = 0; q < rr.size(); ++q) {
       base[q] = (int)acc;
