@@ -674,6 +674,15 @@ bool build_ptile(PTilePlan& out, const PTileSpec& sp, int ncells, int nrows_node
   std::vector<int32_t>& cruns = O.cruns;
   std::vector<int> vid, cid;
   std::vector<std::pair<int, int>> rr, cr;
+  // generation stamps (calloc'd: only the pages a chunk touches map)
+  struct Stamps {
+    int* p;
+    explicit Stamps(size_t n) : p(static_cast<int*>(std::calloc(n + 1, sizeof(int)))) {
+      if (!p) throw std::bad_alloc();
+    }
+    ~Stamps() { std::free(p); }
+  } cstamp(ncells), vstamp(nverts), fstamp(ncf ? ncoeff_nodes : 0);
+  int gen = 0;
   int r0 = (int)cb0;
   const int rend = (int)cb1;
   while (r0 < rend) {
@@ -681,12 +690,27 @@ bool build_ptile(PTilePlan& out, const PTileSpec& sp, int ncells, int nrows_node
     auto fits = [&](int a, int b, int& slots, int& cslots) {
       if (ncn && (hn[b] - hn[a]) * W > sp.tile_seg) return false;
       if (hp[b] - hp[a] > sp.tile_pairs) return false;
+      ++gen;
       vid.clear();
       cid.clear();
-      for (int p = hp[a]; p < hp[b]; ++p) {
+      for (int p = hp[a]; p < hp[b]; ++p) { // distinct cells' distinct vertices / coefficient nodes
         const int c = hpairs[p] / nrn;
-        for (int v = 0; v < nv; ++v) vid.push_back(hx[(size_t)c * nv + v]);
-        for (int q = 0; q < ncf; ++q) cid.push_back(hcf[(size_t)c * ncf + q]);
+        if (cstamp.p[c] == gen) continue;
+        cstamp.p[c] = gen;
+        for (int v = 0; v < nv; ++v) {
+          const int x = hx[(size_t)c * nv + v];
+          if (vstamp.p[x] != gen) {
+            vstamp.p[x] = gen;
+            vid.push_back(x);
+          }
+        }
+        for (int q = 0; q < ncf; ++q) {
+          const int x = hcf[(size_t)c * ncf + q];
+          if (fstamp.p[x] != gen) {
+            fstamp.p[x] = gen;
+            cid.push_back(x);
+          }
+        }
       }
       slots = make_runs(vid, nverts, rr);
       cslots = ncf ? make_runs(cid, ncoeff_nodes, cr) : 0;

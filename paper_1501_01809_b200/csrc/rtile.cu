@@ -1,3 +1,4 @@
+#include <atomic>
 // rtile.cu -- row tiles with shared cell geometry (see rtile.cuh).
 //
 // Reference path replaced: the three par_loops of assemble_blocks for the
@@ -70,8 +71,10 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
   // vertex map, 2 bits each | edge-row flag), then the column ranks in
   // canonical order
   const int rb = (4 + ncn + 3) & ~3, rbw = rb / 4;
-  std::vector<uint8_t> recs((size_t)np * rb, 0);
-  for (int r = 0; r < nrows_node; ++r)
+  auto recs = host_array<uint8_t>((size_t)np * rb); // zeroed by the parallel first touch
+  std::atomic<bool> recs_ok{true};
+  parallel_chunks(nrows_node, 1, [&](int, int64_t rb0, int64_t rb1) {
+  for (int r = (int)rb0; r < (int)rb1; ++r)
     for (int p = hp[r]; p < hp[r + 1]; ++p) {
       const int i = hpairs[p] % nrn;
       int sigma[4], inv[4], colpos[10];
@@ -86,10 +89,15 @@ bool build_rtile(RtilePlan& out, const RtileSpec& sp, int form, int gd, int nrn,
       const int L = (int)(nptr[r + 1] - nptr[r]);
       for (int j = 0; j < ncn; ++j) {
         const int rk = hrank[(size_t)p * ncn + j];
-        if (rk >= L) return false;
+        if (rk >= L) {
+          recs_ok = false;
+          return;
+        }
         rec[4 + colpos[j]] = (uint8_t)rk;
       }
     }
+  });
+  if (!recs_ok) return false;
   // ---- tiles of consecutive row nodes
   const int trows = sp.tile_rows <= 64 ? 64 : 128, nwarps = trows / 32, W = rd * cd;
   // chunks of whole tile-row blocks tiled on all host cores, concatenated
