@@ -33,6 +33,7 @@
 #include "engine.cuh"
 #include "ctile.cuh"
 #include "etile.cuh"
+#include "ltile.cuh"
 #include "ntile.cuh"
 #include "rtile.cuh"
 #include "patch.cuh"
@@ -2596,6 +2597,8 @@ struct FastPlan {
   EtilePlan et;
   bool use_ntile = false;  // node-block tiles (vector P1 elasticity, ntile.cuh)
   NtilePlan nt;
+  bool use_ltile = false;  // edge-link tiles (the same loops on manifold meshes, ltile.cuh)
+  LtilePlan lt;
   bool use_rtile = false;  // row tiles with shared cell geometry (Taylor-Hood B / B^T, rtile.cuh)
   RtilePlan rt;
   bool use_star = false;   // vertex-star kernel (P1 triangle actions)
@@ -2971,6 +2974,17 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
         (Cn.v.v == R.v.v || prefix_equal(Cn.v.v, Cn.v.arity, R.v.v, R.v.arity, R.v.arity, n, s))) {
       SortedMap sx;
       gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, sx, s);
+      if (!std::getenv("LOAM_GPU_NO_LTILE")) { // manifold meshes: a block walks its edge's link
+        LtileSpec ls;
+        ls.tile_nodes = env_int("LOAM_GPU_LT_NODES", ls.tile_nodes);
+        if (build_ltile(P->lt, ls, n, R.v.target, srows.v.get(), sx.v.get(), X->target_size, P->pp, sp->row_ptr,
+                        sp->nnz, s)) {
+          plan_tick("link tiles", s);
+          P->use_ltile = true;
+          return P;
+        }
+        P->lt = LtilePlan{};
+      }
       NtileSpec ns;
       ns.tile_nodes = env_int("LOAM_GPU_NT_NODES", ns.tile_nodes);
       ns.tile_items = env_int("LOAM_GPU_NT_ITEMS", ns.tile_items);
@@ -3311,6 +3325,13 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
   if (P->use_rtile) {
     const int ctr = P->counter.acquire(s);
     launch_rtile(P->rt, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
+                 P->counter.next(ctr), P->counter.exits(ctr), s);
+    P->counter.commit(ctr, s);
+    return;
+  }
+  if (P->use_ltile) {
+    const int ctr = P->counter.acquire(s);
+    launch_ltile(P->lt, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
                  P->counter.next(ctr), P->counter.exits(ctr), s);
     P->counter.commit(ctr, s);
     return;

@@ -241,6 +241,8 @@ bool build_ntile(NtilePlan& out, const NtileSpec& sp, int ncells, int nnodes, co
     }
     // the kDiagSplit parts of a diagonal block sit on consecutive lanes of one
     // aligned lane group (combined by shuffles): pad with no-op items
+    // blocks of equal pair counts share warps (a warp's pair loop runs to its longest item)
+    std::stable_sort(items.begin(), items.end(), [](const ItemRec& x, const ItemRec& y) { return x.np > y.np; });
     while (items.size() % kDiagSplit) items.push_back(ItemRec{0, 0, 2, 0, 0});
     for (auto it : ditems) {
       it.poff = (uint16_t)(it.poff + prec.size());
@@ -395,6 +397,7 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + STAGES;
   int* slot_tile = reinterpret_cast<int*>(sm + 48);
+  int4* slot_meta = reinterpret_cast<int4*>(sm + 128); // the stage's tile record, passed on by the producer
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int q = 0; q < STAGES; ++q) {
@@ -451,7 +454,12 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
         }
         break;
       }
-      if (lane == 0) slot_tile[k % STAGES] = tile;
+      if (lane == 0) {
+        slot_tile[k % STAGES] = tile;
+        int4* sm4 = slot_meta + 4 * (k % STAGES);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sm4[q] = make_int4(m[4 * q], m[4 * q + 1], m[4 * q + 2], m[4 * q + 3]);
+      }
       unsigned char* buf = ring(k);
       uint64_t* bar = &full[k % STAGES];
       const RunSet rc{reinterpret_cast<const int2*>(a.runs) + m[8], m[9], a.coords,
@@ -480,7 +488,17 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
     const int tile = slot_tile[k % STAGES];
     if (tile < 0) break;
     int m[16];
-    meta(tile, m);
+    {
+      const int4* sm4 = slot_meta + 4 * (k % STAGES);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int4 x = sm4[q];
+        m[4 * q] = x.x;
+        m[4 * q + 1] = x.y;
+        m[4 * q + 2] = x.z;
+        m[4 * q + 3] = x.w;
+      }
+    }
     const int E0 = m[4], len = m[5], nitems = m[6], ncell = m[7], ndiag = m[14];
     const unsigned char* buf = ring(k);
     const uint2* items = reinterpret_cast<const uint2*>(buf + m[10]);
@@ -489,7 +507,6 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
     const uint16_t* dinfo = reinterpret_cast<const uint16_t*>(buf + m[13]);
     const double* win = reinterpret_cast<const double*>(buf + a.b_win);
     double* seg = seg0 + (E0 & 1); // 16-byte parity of the global destination (bulk store)
-    if (tid == 0) bulk_wait_read<0>(); // the previous tile's store has read the segment
     // phase 1: barycentric gradients and measure of every cell of the tile, once
     for (int c = tid; c < ((a.dbg & 2) ? 0 : ncell); c += NT) {
       double X[4][3];
@@ -511,6 +528,7 @@ __global__ void __launch_bounds__(kNtThreads + 32, 1) k_ntile(const __grid_const
         gc[8 + v] = sv * Gm.g[v][2];
       }
     }
+    if (tid == 0) bulk_wait_read<0>(); // the previous tile's store has read the segment (overlapped with phase 1)
     named_bar(1, NT);
     // phase 2: one thread per 3x3 node block (diagonal blocks: kDiagSplit threads)
     for (int it = tid; it < nitems; it += NT) {
@@ -630,7 +648,7 @@ void launch_ntile(const NtilePlan& p, const double* coords, double* out, const F
   a.out = out;
   a.prm = prm;
   a.accumulate = accumulate ? 1 : 0;
-  int off = 128;
+  int off = 128 + 3 * 64; // barriers + per-stage tile records
   a.off_seg = off;
   off += up16((p.max_seg + 2) * 8);
   a.off_geo = off;
