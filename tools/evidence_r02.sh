@@ -3,7 +3,7 @@
 # deterministic), plan-build phases, the ncu launch list of the bench command
 # and one --set full capture per config's dominant kernel (every profiled
 # command first exits 0 without ncu).  Outputs under gpurun_out/ev2/.
-O=gpurun_out/ev2; mkdir -p $O
+O=gpurun_out/${EV:-ev2}; mkdir -p $O
 summ() { python tools/ncu_summary.py $1.ncu-rep 20 > $1.txt 2>&1; python tools/ncu_lines.py $1.ncu-rep 25 >> $1.txt 2>&1; ncu -i $1.ncu-rep --page raw --csv > $1_raw.csv 2>/dev/null; rm -f $1.ncu-rep; }
 timeout 1100 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo pytest_rc=$?; tail -1 $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke_rc=$?
@@ -17,7 +17,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ncu --set full --clock-control none --import-source on -k regex:k_ring -s 12 -c 1 -o $O/c2_ring python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config-table > $O/ncu_c2.log 2>&1; echo ncu_c2_rc=$?
 summ $O/c2_ring
 for c in 1 3r 3m 4 5; do
-  case $c in 1) k=k_star;; 3r) k=k_cell;; 3m) k=k_etile;; 4) k=k_ntile;; 5) k=k_etile;; esac
+  case $c in 1) k=k_star;; 3r) k=k_cell;; 3m) k=k_etile;; 4) k=k_ltile;; 5) k=k_etile;; esac
   python bench.py --all-configs --configs $c --strategies auto --steps 3 > $O/plain_cfg$c.log 2>&1; echo plain_$c rc=$?
   ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o $O/cfg$c python bench.py --all-configs --configs $c --strategies auto --steps 3 > $O/ncu_cfg$c.log 2>&1; echo ncu_$c rc=$?
   summ $O/cfg$c
