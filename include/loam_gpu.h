@@ -224,6 +224,24 @@ int loam_gpu_execute_host_batch(const loam_kernel_desc* kernel, int32_t iterset_
                                 uint64_t iterset_id, const loam_arg_desc* const* args, int nargs,
                                 int nsteps, void* stream);
 
+/* fem::assemble_blocks (fem/assemble.hpp:439-448) assembles the blocks of a
+ * nested BlockMat (solver.hpp:21-28) with one par_loop per block.  This entry
+ * takes those loops together (device data, as loam_gpu_execute): every loop is
+ * validated before anything is written, then the loops run in order -- except
+ * that the Taylor-Hood Stokes triple (stokes_a_p2_tri, stokes_b_p2_tri,
+ * stokes_bt_p2_tri over one cell set, velocity map, pressure map and
+ * coordinate Dat) is assembled by ONE launch that forms every cell's geometry
+ * once for the three blocks.  Results are those of the separate loops (values
+ * to rounding; the fused path is deterministic run to run). */
+typedef struct loam_loop_desc {
+  const loam_kernel_desc* kernel;
+  int32_t iterset_size;
+  uint64_t iterset_id;
+  const loam_arg_desc* args;
+  int32_t nargs;
+} loam_loop_desc;
+int loam_gpu_execute_blocks(const loam_loop_desc* loops, int nloops, void* stream);
+
 /* ---- consumers of the assembled matrix --------------------- */
 /* y = A x by CSR traversal (data.hpp:236-250 mat_spmv): rows ascending, each
  * row folded in column order with a separate multiply and add -- bitwise

@@ -181,5 +181,8 @@ class Workload:
             o.zero()
 
     def run(self):
+        if self.cfg == 5:  # fem::assemble_blocks (fem/assemble.hpp:439-448): the three blocks in one call
+            self.L.execute_blocks(self.loops)
+            return
         for lp in self.loops:
             self.L.execute(lp)

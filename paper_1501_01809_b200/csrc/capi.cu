@@ -217,6 +217,16 @@ int loam_gpu_execute(const loam_kernel_desc* kernel, int32_t n, uint64_t iter, c
   });
 }
 
+int loam_gpu_execute_blocks(const loam_loop_desc* loops, int nloops, void* stream) {
+  return guarded([&] {
+    require_device();
+    std::vector<LoopDesc> l((size_t)std::max(nloops, 0));
+    for (int i = 0; i < nloops; ++i)
+      l[i] = LoopDesc{loops[i].kernel, loops[i].iterset_size, loops[i].iterset_id, loops[i].args, loops[i].nargs};
+    execute_blocks(l.data(), nloops, as_stream(stream));
+  });
+}
+
 // Host-memory calling convention of the reference: every pointer is host
 // memory.  Uploads maps, patterns and the data the loop reads, runs, downloads
 // every written object, and returns with the results visible on the host.

@@ -34,6 +34,7 @@
 #include "ctile.cuh"
 #include "etile.cuh"
 #include "ltile.cuh"
+#include "thtile.cuh"
 #include "ntile.cuh"
 #include "rtile.cuh"
 #include "patch.cuh"
@@ -3676,6 +3677,117 @@ void execute(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_de
   run_generic(k, n, iter, args, nargs, prm, s);
 }
 
+// ---------------------------------------------------------------------------
+// fem::assemble_blocks (fem/assemble.hpp:439-448): the loops of a nested block
+// matrix issued together.  The Taylor-Hood triple (stokes_a / stokes_b /
+// stokes_bt over one cell set, velocity map, pressure map and coordinate Dat)
+// runs as ONE launch (thtile.cuh) when its plan builds; any other list -- and
+// the triple on a mesh or pattern the plan declines -- runs loop by loop,
+// exactly as the reference does.
+struct ThFused {
+  TileCounters counter;
+  ThtilePlan plan;
+  bool ok = false;
+};
+std::map<std::vector<uint64_t>, std::shared_ptr<ThFused>> g_th_cache;
+
+bool try_taylor_hood(const LoopDesc* loops, int nloops, cudaStream_t s) {
+  if (nloops != 3 || strategy() != 0 || std::getenv("LOAM_GPU_NO_THTILE")) return false;
+  int ia = -1, ib = -1, it = -1;
+  for (int i = 0; i < 3; ++i) {
+    if (!loops[i].kernel || !loops[i].kernel->name) return false;
+    const Entry& k = lookup(loops[i].kernel->name);
+    if (k.form == F_STOKES_A && ia < 0) ia = i;
+    else if (k.form == F_STOKES_B && ib < 0) ib = i;
+    else if (k.form == F_STOKES_BT && it < 0) it = i;
+    else return false;
+    if (!fast_pattern(k, loops[i].args, loops[i].nargs)) return false;
+  }
+  const int n = loops[ia].n;
+  if (n <= 0 || loops[ib].n != n || loops[it].n != n || loops[ib].iter != loops[ia].iter ||
+      loops[it].iter != loops[ia].iter || loops[ia].kernel->nparams < 1)
+    return false;
+  const loam_arg_desc &A = loops[ia].args[0], &B = loops[ib].args[0], &T = loops[it].args[0], &X = loops[ia].args[1];
+  for (int i : {ib, it}) {
+    const loam_arg_desc& Xi = loops[i].args[1];
+    if (Xi.data != X.data || Xi.map->values != X.map->values || Xi.map->arity != X.map->arity) return false;
+  }
+  const NodeMap RA = node_view(A.map), CA = node_view(A.col_map), RB = node_view(B.map), CB = node_view(B.col_map),
+                RT = node_view(T.map), CT = node_view(T.col_map);
+  auto same = [](const NodeMap& a, const NodeMap& b) {
+    return a.v.v == b.v.v && a.v.arity == b.v.arity && a.v.target == b.v.target && a.dim == b.dim && a.v.n == b.v.n;
+  };
+  if (!same(RA, CA) || !same(RA, CB) || !same(RA, RT) || !same(RB, CT)) return false;
+  if (RA.v.arity != 6 || RA.dim != 2 || RB.v.arity != 3 || RB.dim != 1 || RA.v.n != n || RB.v.n != n) return false;
+  const MapView xm{X.map->values, n, X.map->arity, X.map->target_size};
+  if (xm.arity != 3 || X.map->source_size != n || RB.v.target != xm.target) return false;
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!aligned(X.data) || !aligned(A.data) || !aligned(B.data) || !aligned(T.data)) return false;
+  if (A.data == B.data || A.data == T.data || B.data == T.data) return false;
+  std::vector<uint64_t> key{(uint64_t)n};
+  bool cacheable = true;
+  for (const loam_arg_desc* a : {&A, &B, &T}) {
+    for (uint64_t id : {a->map->id, a->col_map->id, a->sparsity->id}) {
+      key.push_back(id);
+      cacheable &= id != 0;
+    }
+  }
+  key.push_back(X.map->id);
+  cacheable &= X.map->id != 0;
+  std::shared_ptr<ThFused> P;
+  if (cacheable) {
+    std::lock_guard<std::mutex> g(g_cache_mutex);
+    auto f = g_th_cache.find(key);
+    if (f != g_th_cache.end()) P = f->second;
+  }
+  if (!P) {
+    plan_tick("plan start", s);
+    P = std::make_shared<ThFused>();
+    P->counter.init(s);
+    bool ok = RB.v.v == xm.v || prefix_equal(RB.v.v, 3, xm.v, 3, 3, n, s);
+    auto exact = [&](const loam_arg_desc& a, const NodeMap& R, const NodeMap& C) {
+      const loam_sparsity_desc* sp = a.sparsity;
+      return pattern_provenance_exact(a) ||
+             pattern_is_maps_pattern(R.v, C.v, R.dim, C.dim, sp->row_ptr, sp->col_idx, sp->nnz, s);
+    };
+    ok = ok && exact(A, RA, CA) && exact(B, RB, CB) && exact(T, RT, CT);
+    plan_tick("thtile: checks", s);
+    if (ok) {
+      PairPlan pp;
+      build_pairs(RA.v.v, n, 6, RA.v.target, pp, s);
+      ThtileSpec ts;
+      ts.spoke_items = env_int("LOAM_GPU_TH_SPOKES", ts.spoke_items);
+      ts.edge_items = env_int("LOAM_GPU_TH_EDGES", ts.edge_items);
+      ok = build_thtile(P->plan, ts, n, RA.v.target, xm.target, RA.v.v, xm.v, pp, A.sparsity->row_ptr, A.sparsity->nnz,
+                        B.sparsity->row_ptr, B.sparsity->nnz, T.sparsity->row_ptr, T.sparsity->nnz, s);
+      plan_tick("thtile", s);
+    }
+    if (!ok) P->plan = ThtilePlan{};
+    P->ok = ok;
+    LG_CUDA(cudaStreamSynchronize(s)); // plan data complete before a PDL kernel reads it
+    if (cacheable) {
+      std::lock_guard<std::mutex> g(g_cache_mutex);
+      g_th_cache[key] = P;
+    }
+  }
+  if (!P->ok) return false;
+  const int acc = ((A.flags & LOAM_ARG_ZERO) ? 0 : 1) | ((B.flags & LOAM_ARG_ZERO) ? 0 : 2) |
+                  ((T.flags & LOAM_ARG_ZERO) ? 0 : 4);
+  const int ctr = P->counter.acquire(s);
+  launch_thtile(P->plan, X.data, A.data, B.data, T.data, loops[ia].kernel->params[0], acc, P->counter.next(ctr),
+                P->counter.exits(ctr), s);
+  P->counter.commit(ctr, s);
+  return true;
+}
+
+void execute_blocks(const LoopDesc* loops, int nloops, cudaStream_t s) {
+  require(nloops >= 0 && (nloops == 0 || loops != nullptr), LOAM_ERR(InvalidArgument), "block loops without a list");
+  // every loop is validated before anything is written (parloop.hpp:193 per loop)
+  for (int i = 0; i < nloops; ++i) validate(loops[i].kernel, loops[i].n, loops[i].iter, loops[i].args, loops[i].nargs);
+  if (try_taylor_hood(loops, nloops, s)) return;
+  for (int i = 0; i < nloops; ++i) execute(loops[i].kernel, loops[i].n, loops[i].iter, loops[i].args, loops[i].nargs, s);
+}
+
 void wave_step(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_desc* args, int nargs,
                const double* p_in, const double* phi_in, double* p_out, double* phi_out, const double* pc,
                const uint8_t* bc, double half_dt, double* state, cudaStream_t s) {
@@ -3713,6 +3825,7 @@ void plan_cache_clear() {
   std::lock_guard<std::mutex> g(g_cache_mutex);
   g_fast_cache.clear();
   g_color_cache.clear();
+  g_th_cache.clear();
 }
 
 void plan_cache_release(uint64_t id) {
@@ -3744,7 +3857,20 @@ void plan_cache_release(uint64_t id) {
       }
     }
   }
-  if (!dead_fast.empty() || !dead_color.empty()) LG_CUDA(cudaDeviceSynchronize()); // queued launches may use them
+  std::vector<std::shared_ptr<ThFused>> dead_th;
+  {
+    std::lock_guard<std::mutex> g(g_cache_mutex);
+    for (auto it = g_th_cache.begin(); it != g_th_cache.end();) {
+      if (holds(it->first, 1, (size_t)-1)) {
+        dead_th.push_back(std::move(it->second));
+        it = g_th_cache.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  if (!dead_fast.empty() || !dead_color.empty() || !dead_th.empty())
+    LG_CUDA(cudaDeviceSynchronize()); // queued launches may use them
 }
 
 namespace {

@@ -28,6 +28,16 @@ void validate(const loam_kernel_desc* k, int n, uint64_t iter_id, const loam_arg
               int nargs);
 void execute(const loam_kernel_desc* k, int n, uint64_t iter_id, const loam_arg_desc* args,
              int nargs, cudaStream_t s);
+// fem::assemble_blocks (fem/assemble.hpp:439-448): the loops of a nested block
+// matrix in one call; the Taylor-Hood triple runs as one launch (thtile.cuh).
+struct LoopDesc {
+  const loam_kernel_desc* kernel;
+  int n;
+  uint64_t iter;
+  const loam_arg_desc* args;
+  int nargs;
+};
+void execute_blocks(const LoopDesc* loops, int nloops, cudaStream_t s);
 void plan_cache_clear();
 // evict every cached plan keyed by an object id (Map / Sparsity destroyed)
 void plan_cache_release(uint64_t id);

@@ -22,6 +22,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "plan.cuh"
 
 namespace loam_gpu {
 
@@ -63,5 +64,8 @@ bool build_patch(PatchPlan& out, const PatchSpec& sp, int ncells, int nnodes, co
 // True when the CSR (row_ptr, col_idx) equals build_sparsity(m, m, rd, cd).
 bool pattern_is_map_pattern(const int32_t* m, int n, int arity, int target, int rd, int cd,
                             const int64_t* row_ptr, const int32_t* col_idx, int64_t nnz, cudaStream_t s);
+// The same test for a rectangular pattern: build_sparsity(rows, cols, rd, cd).
+bool pattern_is_maps_pattern(const MapView& rows, const MapView& cols, int rd, int cd, const int64_t* row_ptr,
+                             const int32_t* col_idx, int64_t nnz, cudaStream_t s);
 
 } // namespace loam_gpu

@@ -66,11 +66,17 @@ __global__ void k_count_ne64(const int64_t* __restrict__ a, const int64_t* __res
 
 bool pattern_is_map_pattern(const int32_t* m, int n, int arity, int target, int rd, int cd,
                             const int64_t* row_ptr, const int32_t* col_idx, int64_t nnz, cudaStream_t s) {
+  const MapView mv{m, n, arity, target};
+  return pattern_is_maps_pattern(mv, mv, rd, cd, row_ptr, col_idx, nnz, s);
+}
+
+bool pattern_is_maps_pattern(const MapView& rows, const MapView& cols, int rd, int cd, const int64_t* row_ptr,
+                             const int32_t* col_idx, int64_t nnz, cudaStream_t s) {
   int64_t* rp = nullptr;
   int32_t* ci = nullptr;
   int64_t bn = 0;
-  const MapView mv{m, n, arity, target};
-  build_sparsity_dev(mv, mv, rd, cd, &rp, &ci, &bn, s);
+  const int target = rows.target;
+  build_sparsity_dev(rows, cols, rd, cd, &rp, &ci, &bn, s);
   bool same = bn == nnz;
   if (same) {
     DevBuf<unsigned long long> bad(1, s);

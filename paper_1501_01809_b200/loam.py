@@ -588,6 +588,30 @@ def execute(loop: Parloop, threads: int = 1) -> None:
                 a.mat._zero = a.mat._stale = False
 
 
+def execute_blocks(loops) -> None:
+    """The par_loops of fem::assemble_blocks (fem/assemble.hpp:439-448) in one
+    call: every loop validated first, then run in order -- the Taylor-Hood
+    Stokes triple as one fused launch (loam_gpu_execute_blocks)."""
+    loops = list(loops)
+    built = [_build(lp) for lp in loops]
+    arr = (capi.LoopDesc * max(len(loops), 1))()
+    for i, (lp, (kd, descs, keep)) in enumerate(zip(loops, built)):
+        arr[i].kernel = C.pointer(kd)
+        arr[i].iterset_size = lp.iterset.size
+        arr[i].iterset_id = lp.iterset.id
+        arr[i].args = C.cast(descs, C.POINTER(capi.ArgDesc))
+        arr[i].nargs = len(lp.args)
+    capi.check(capi.lib().loam_gpu_execute_blocks(arr, len(loops), _stream()))
+    for lp in loops:
+        for a in lp.args:
+            if a.access != READ:
+                if a.dat is not None:
+                    a.dat.version += 1
+                    a.dat._zero = a.dat._stale = False
+                if a.mat is not None:
+                    a.mat._zero = a.mat._stale = False
+
+
 # --------------------------------------------------------------------------
 # Consumers of the assembled matrix (SURVEY 8f-1): data.hpp:236-250,
 # solver.hpp:13-207, on the device through the C ABI.
