@@ -3684,8 +3684,7 @@ void execute(const loam_kernel_desc* kd, int n, uint64_t iter, const loam_arg_de
 // runs as ONE launch (thtile.cuh) when its plan builds; any other list -- and
 // the triple on a mesh or pattern the plan declines -- runs loop by loop,
 // exactly as the reference does.
-struct ThFused {
-  TileCounters counter;
+struct ThFused { // (static tile schedule: no counters, any number of launches in flight)
   ThtilePlan plan;
   bool ok = false;
 };
@@ -3743,7 +3742,6 @@ bool try_taylor_hood(const LoopDesc* loops, int nloops, cudaStream_t s) {
   if (!P) {
     plan_tick("plan start", s);
     P = std::make_shared<ThFused>();
-    P->counter.init(s);
     bool ok = RB.v.v == xm.v || prefix_equal(RB.v.v, 3, xm.v, 3, 3, n, s);
     auto exact = [&](const loam_arg_desc& a, const NodeMap& R, const NodeMap& C) {
       const loam_sparsity_desc* sp = a.sparsity;
@@ -3773,10 +3771,7 @@ bool try_taylor_hood(const LoopDesc* loops, int nloops, cudaStream_t s) {
   if (!P->ok) return false;
   const int acc = ((A.flags & LOAM_ARG_ZERO) ? 0 : 1) | ((B.flags & LOAM_ARG_ZERO) ? 0 : 2) |
                   ((T.flags & LOAM_ARG_ZERO) ? 0 : 4);
-  const int ctr = P->counter.acquire(s);
-  launch_thtile(P->plan, X.data, A.data, B.data, T.data, loops[ia].kernel->params[0], acc, P->counter.next(ctr),
-                P->counter.exits(ctr), s);
-  P->counter.commit(ctr, s);
+  launch_thtile(P->plan, X.data, A.data, B.data, T.data, loops[ia].kernel->params[0], acc, s);
   return true;
 }
 

@@ -69,7 +69,7 @@ bool build_thtile(ThtilePlan& out, const ThtileSpec& sp, int ncells, int nnodes,
   }
   struct TileChunk {
     bool ok = true;
-    std::vector<int32_t> tiles, runs;
+    std::vector<int32_t> tiles, runs, roff;
     std::vector<uint8_t> blob;
     int max_seg = 0, max_slots = 0, max_blob = 0;
   };
@@ -142,9 +142,21 @@ bool build_thtile(ThtilePlan& out, const ThtileSpec& sp, int ncells, int nnodes,
       // 16-byte aligned, even-length segments (bulk stores)
       if ((A0 | A1 | B0 | B1 | T0 | T1) & 1) return false;
       const int seg = (int)((A1 - A0) + (B1 - B0) + (T1 - T0));
-      O.tiles.insert(O.tiles.end(), {(int)(b0 / 16), bytes, kind, nitems, nv, (int)A0, (int)(A1 - A0), (int)B0,
-                                     (int)(B1 - B0), (int)T0, (int)(T1 - T0), (int)O.runs.size() / 2, (int)rr.size(),
-                                     off_rec, off_d, slots});
+      if (bytes >= (1 << 16) || A1 - A0 >= (1 << 16) || B1 - B0 >= (1 << 16) || T1 - T0 >= (1 << 16) ||
+          (int)rr.size() >= (1 << 15))
+        return false;
+      // 8 meta ints + the first 4 window runs (the producer's chain holds no dependent load for them):
+      // blob offset / 16 | bytes, kind << 16, nv << 20 | nitems, run offset << 8 (packed at merge) |
+      // A, B, B^T value offsets | lenA, lenB << 16 | lenT, run count << 16
+      int rec[16] = {(int)(b0 / 16), bytes | kind << 16 | nv << 20, nitems, (int)A0, (int)B0, (int)T0,
+                     (int)(A1 - A0) | (int)(B1 - B0) << 16, (int)(T1 - T0) | (int)rr.size() << 16,
+                     0, 0, 0, 0, 0, 0, 0, 0};
+      for (size_t q = 0; q < rr.size() && q < 4; ++q) {
+        rec[8 + 2 * q] = rr[q].first;
+        rec[9 + 2 * q] = rr[q].second;
+      }
+      O.tiles.insert(O.tiles.end(), rec, rec + 16);
+      O.roff.push_back((int)O.runs.size() / 2);
       for (auto& x : rr) O.runs.insert(O.runs.end(), {x.first, x.second});
       O.max_seg = std::max(O.max_seg, seg);
       O.max_slots = std::max(O.max_slots, slots);
@@ -342,7 +354,9 @@ bool build_thtile(ThtilePlan& out, const ThtileSpec& sp, int ncells, int nnodes,
     const int bshift = (int)(bytes_so_far / 16), rshift = (int)(runs.size() / 2);
     for (size_t q = 0; q < O.tiles.size(); q += 16) {
       O.tiles[q + 0] += bshift;
-      O.tiles[q + 11] += rshift;
+      const int64_t ro = (int64_t)O.roff[q / 16] + rshift;
+      if (ro >= (1 << 23)) return false;
+      O.tiles[q + 2] |= (int)ro << 8;
     }
     tiles.insert(tiles.end(), O.tiles.begin(), O.tiles.end());
     runs.insert(runs.end(), O.runs.begin(), O.runs.end());
@@ -378,8 +392,6 @@ namespace {
 struct ThtileArgs {
   const int32_t* tiles;
   int ntiles;
-  int* next_tile;
-  int* reset_tile;
   const uint8_t* blob;
   const int32_t* runs;
   const double* coords;
@@ -412,7 +424,10 @@ __global__ void __launch_bounds__(kThConsumers + 32, LOAM_GPU_TH_MINB) k_thtile(
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + STAGES;
   int* slot_tile = reinterpret_cast<int*>(sm + 48);
-  int4* slot_meta = reinterpret_cast<int4*>(sm + 128); // the stage's tile record, passed on by the producer
+  // tile records of this CTA, 8 tiles per batch, double-buffered (cp.async);
+  // the meta of the tile in each stage, handed to the consumers with it
+  __shared__ __align__(16) int meta_s[2][8 * 16];
+  __shared__ int stage_meta[STAGES][8];
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int q = 0; q < STAGES; ++q) {
@@ -425,61 +440,72 @@ __global__ void __launch_bounds__(kThConsumers + 32, LOAM_GPU_TH_MINB) k_thtile(
   if (tid == 0) grid_dep_launch(); // PDL: the next kernel's prologue may start
   auto ring = [&](int k) { return sm + a.off_buf + (k % STAGES) * a.buf_bytes; };
   if (tid >= NT) { // ---- producer warp: tile blob + coordinate window by TMA
+    // Static schedule (tile k of this CTA = blockIdx + k * grid; spoke tiles
+    // first, edge tiles after, so every CTA gets the same mix).  The 64-byte
+    // records (meta + the first window runs) arrive 8 tiles at a time by
+    // cp.async, one batch ahead: no dependent global round trip per tile (a
+    // dynamic counter cost an atomic, a record load and a run load per tile,
+    // and the consumers spent 39 % of their stall samples waiting for data).
     const int lane = tid & 31;
-    auto grab = [&]() {
-      int t = 0;
-      if (lane == 0) t = atomicAdd(a.next_tile, 1);
-      return __shfl_sync(0xffffffffu, t, 0);
+    auto load_batch = [&](int b) { // tiles 8b..8b+7 -> meta_s[b & 1]; lane = (tile in batch, 16-byte part)
+      const int kk = 8 * b + (lane >> 2), part = lane & 3;
+      const int tile = blockIdx.x + kk * gridDim.x;
+      if (tile < a.ntiles) cp_async16(&meta_s[b & 1][(lane >> 2) * 16 + part * 4], a.tiles + 16 * tile + part * 4);
+      cp_async_commit();
     };
-    int nt = grab();
-    int4 nm[4];
-    int2 nrun = make_int2(0, 0);
-    auto prefetch = [&]() {
-      if (nt < a.ntiles) {
-        const int4* t = reinterpret_cast<const int4*>(a.tiles + 16 * nt);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) nm[q] = __ldg(t + q);
-        nrun = first_run(reinterpret_cast<const int2*>(a.runs) + nm[2].w, nm[3].x, lane);
-      }
-    };
-    prefetch();
-    grid_dep_wait(); // the caller's data only after the previous kernel (PDL)
+    load_batch(0);
+    load_batch(1);
     for (int k = 0;; ++k) {
-      const int tile = nt;
-      const int4 m0 = nm[0], m1 = nm[1], m2 = nm[2], m3 = nm[3];
-      const int2 run0 = nrun;
+      const int tile = blockIdx.x + k * gridDim.x;
+      if (k % 8 == 0) {
+        cp_async_wait<1>(); // batch k / 8 has landed (the next one may still be in flight)
+        __syncwarp();
+      }
+      const int* rec = &meta_s[(k / 8) & 1][(k % 8) * 16];
+      int2 run0 = make_int2(0, 0);
+      int cnt = 0, run_off = 0, m0 = 0, m1 = 0, mine = 0;
+      if (tile < a.ntiles) { // (past the end the batch slot was never filled)
+        m0 = rec[0];
+        m1 = rec[1];
+        mine = rec[lane & 7];
+        cnt = rec[7] >> 16;
+        run_off = (int)((unsigned)rec[2] >> 8);
+        if (lane < cnt)
+          run0 = lane < 4 ? reinterpret_cast<const int2*>(rec + 8)[lane]
+                          : __ldg(reinterpret_cast<const int2*>(a.runs) + run_off + lane);
+      }
+      if (k % 8 == 7) {
+        __syncwarp(); // every lane has read batch k / 8: refill its buffer
+        load_batch(k / 8 + 2);
+      }
       if (k >= STAGES) mbar_wait_sleep(&empty[k % STAGES], (k / STAGES - 1) & 1);
-      if (tile >= a.ntiles) {
+      if (tile >= a.ntiles) { // publish "no more tiles" through the stage
         if (lane == 0) {
           slot_tile[k % STAGES] = -1;
           mbar_arrive(&full[k % STAGES]);
         }
         break;
       }
-      if (lane == 0) {
-        slot_tile[k % STAGES] = tile;
-        int4* sm4 = slot_meta + 4 * (k % STAGES);
-        sm4[0] = m0;
-        sm4[1] = m1;
-        sm4[2] = m2;
-        sm4[3] = m3;
-      }
+      if (lane < 8) stage_meta[k % STAGES][lane] = mine;
+      if (lane == 0) slot_tile[k % STAGES] = tile;
       unsigned char* buf = ring(k);
       uint64_t* bar = &full[k % STAGES];
-      const RunSet rc{reinterpret_cast<const int2*>(a.runs) + m2.w, m3.x, a.coords,
+      const uint32_t bytes = (uint32_t)m1 & 0xffffu;
+      const RunSet rc{reinterpret_cast<const int2*>(a.runs) + run_off, cnt, a.coords,
                       reinterpret_cast<double*>(buf + a.b_win), 2};
-      const uint32_t tx = (uint32_t)m0.y + stage_runs<false>(rc, lane, bar, run0);
+      if (lane == 0) { // the plan's records (library-owned, immutable: safe before the PDL wait)
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(buf, a.blob + (int64_t)m0 * 16, bytes, bar);
+      }
+      if (k == 0) grid_dep_wait(); // the caller's coordinates only after the previous kernel (PDL)
+      const uint32_t tx = stage_runs<false>(rc, lane, bar, run0);
       fence_async_shared();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_expect_tx(bar, tx);
-        bulk_g2s(buf, a.blob + (int64_t)m0.x * 16, (uint32_t)m0.y, bar);
-      }
+      if (lane == 0) mbar_arrive_expect_tx(bar, tx);
       __syncwarp();
       stage_runs<true>(rc, lane, bar, run0);
-      nt = grab();
-      prefetch();
     }
+    cp_async_wait<0>();
     return;
   }
   grid_dep_wait(); // (PDL) before the consumers read or write anything of the caller's
@@ -491,10 +517,11 @@ __global__ void __launch_bounds__(kThConsumers + 32, LOAM_GPU_TH_MINB) k_thtile(
     mbar_wait_sleep(&full[k % STAGES], (k / STAGES) & 1);
     const int tile = slot_tile[k % STAGES];
     if (tile < 0) break;
-    const int4* sm4 = slot_meta + 4 * (k % STAGES);
-    const int4 m0 = sm4[0], m1 = sm4[1], m2 = sm4[2], m3 = sm4[3];
-    const int kind = m0.z, nitems = m0.w, nv = m1.x, E0A = m1.y, lenA = m1.z, E0B = m1.w, lenB = m2.x, E0T = m2.y,
-              lenT = m2.z, off_rec = m3.y, off_d = m3.z;
+    const int* sm8 = stage_meta[k % STAGES];
+    const int m1 = sm8[1], m2 = sm8[2], m6 = sm8[6], m7 = sm8[7];
+    const int kind = (m1 >> 16) & 0xf, nv = (m1 >> 20) & 0xff, nitems = m2 & 0xff, E0A = sm8[3], E0B = sm8[4],
+              E0T = sm8[5], lenA = m6 & 0xffff, lenB = (int)((unsigned)m6 >> 16), lenT = m7 & 0xffff;
+    const int off_rec = 8 * ((nitems + 1) & ~1), off_d = off_rec + (((kind == 0 ? 8 : 16) * nitems + 15) & ~15);
     const unsigned char* buf = ring(k);
     const double* win = reinterpret_cast<const double*>(buf + a.b_win);
     double* sA = seg0;
@@ -705,19 +732,16 @@ __global__ void __launch_bounds__(kThConsumers + 32, LOAM_GPU_TH_MINB) k_thtile(
     }
   }
   if (tid == 0) bulk_wait_read<0>();
-  tile_counter_release(a.next_tile, a.reset_tile, NT, tid);
 }
 
 } // namespace
 
 void launch_thtile(const ThtilePlan& p, const double* coords, double* A, double* B, double* BT, double nu, int acc,
-                   int* next_tile, int* reset_tile, cudaStream_t s) {
+                   cudaStream_t s) {
   if (p.ntiles == 0) return;
   ThtileArgs a{};
   a.tiles = p.tiles.get();
   a.ntiles = p.ntiles;
-  a.next_tile = next_tile;
-  a.reset_tile = reset_tile;
   a.blob = p.blob.get();
   a.runs = p.runs.get();
   a.coords = coords;
@@ -726,7 +750,7 @@ void launch_thtile(const ThtilePlan& p, const double* coords, double* A, double*
   a.outT = BT;
   a.nu = nu;
   a.acc = acc;
-  int off = 128 + 3 * 64; // barriers + per-stage tile records
+  int off = 128; // barriers, stage tiles
   a.off_seg = off;
   off += up16(p.max_seg * 8 + 16);
   a.off_scr = off;

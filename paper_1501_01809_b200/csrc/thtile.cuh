@@ -43,13 +43,13 @@ namespace loam_gpu {
 
 struct ThtilePlan {
   int ntiles = 0, max_seg = 0, max_slots = 0, max_blob = 0;
-  DevBuf<int32_t> tiles; // 16 ints per tile (thtile.cu)
+  DevBuf<int32_t> tiles; // 16 ints per tile: 8 meta + the first 4 window runs (thtile.cu)
   DevBuf<uint8_t> blob;  // per tile: item window slots, item records, vertex records
   DevBuf<int32_t> runs;  // coordinate-window runs [lo, hi)
 };
 
 struct ThtileSpec {
-  int spoke_items = 128, edge_items = 128, tile_slots = 1024, tile_runs = 32;
+  int spoke_items = 128, edge_items = 64, tile_slots = 1024, tile_runs = 32;
 };
 
 // vnm: the velocity cell->node map (ncells x 6, device), xmap: the cell->vertex
@@ -61,6 +61,6 @@ bool build_thtile(ThtilePlan& out, const ThtileSpec& sp, int ncells, int nnodes,
 
 // acc: bit 0 / 1 / 2 = add to the existing values of A / B / B^T instead of overwriting
 void launch_thtile(const ThtilePlan& p, const double* coords, double* A, double* B, double* BT, double nu, int acc,
-                   int* next_tile, int* reset_tile, cudaStream_t s);
+                   cudaStream_t s);
 
 } // namespace loam_gpu
