@@ -241,6 +241,10 @@ typedef struct loam_loop_desc {
   int32_t nargs;
 } loam_loop_desc;
 int loam_gpu_execute_blocks(const loam_loop_desc* loops, int nloops, void* stream);
+/* The same over HOST data (the calling convention of loam_gpu_execute_host:
+ * uploads what the loops read -- one copy per host array across the loops --
+ * runs them, downloads what they wrote, synchronously). */
+int loam_gpu_execute_blocks_host(const loam_loop_desc* loops, int nloops, void* stream);
 
 /* ---- consumers of the assembled matrix --------------------- */
 /* y = A x by CSR traversal (data.hpp:236-250 mat_spmv): rows ascending, each

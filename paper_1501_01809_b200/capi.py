@@ -134,6 +134,7 @@ def lib() -> C.CDLL:
             "loam_gpu_execute_host_batch": (C.c_int, [C.POINTER(KernelDesc), i32, u64,
                                                       C.POINTER(C.POINTER(ArgDesc)), C.c_int, C.c_int, vp]),
             "loam_gpu_execute_blocks": (C.c_int, [C.POINTER(LoopDesc), C.c_int, vp]),
+            "loam_gpu_execute_blocks_host": (C.c_int, [C.POINTER(LoopDesc), C.c_int, vp]),
             "loam_gpu_map_check": (C.c_int, [C.POINTER(MapDesc), vp]),
             "loam_gpu_build_sparsity": (C.c_int, [C.POINTER(MapDesc), C.POINTER(MapDesc), C.c_int, C.c_int,
                                                   C.POINTER(vp), C.POINTER(vp), C.POINTER(i64), vp]),
@@ -187,7 +188,7 @@ EXPORTED = [
     "loam_gpu_get_option", "loam_gpu_plan_cache_clear", "loam_gpu_new_id", "loam_gpu_release_id",
     "loam_gpu_launch_count",
     "loam_gpu_kernel_signature", "loam_gpu_kernel_names", "loam_gpu_validate", "loam_gpu_execute",
-    "loam_gpu_execute_host", "loam_gpu_execute_host_batch", "loam_gpu_execute_blocks", "loam_gpu_map_check", "loam_gpu_build_sparsity",
+    "loam_gpu_execute_host", "loam_gpu_execute_host_batch", "loam_gpu_execute_blocks", "loam_gpu_execute_blocks_host", "loam_gpu_map_check", "loam_gpu_build_sparsity",
     "loam_gpu_color_iteration", "loam_gpu_malloc", "loam_gpu_free", "loam_gpu_host_alloc",
     "loam_gpu_host_free", "loam_gpu_memcpy", "loam_gpu_memset", "loam_gpu_stream_sync",
     "loam_gpu_unit_square_mesh", "loam_gpu_unit_cube_mesh", "loam_gpu_jitter",

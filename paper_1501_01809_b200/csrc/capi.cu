@@ -230,54 +230,63 @@ int loam_gpu_execute_blocks(const loam_loop_desc* loops, int nloops, void* strea
 // Host-memory calling convention of the reference: every pointer is host
 // memory.  Uploads maps, patterns and the data the loop reads, runs, downloads
 // every written object, and returns with the results visible on the host.
-int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t n, uint64_t iter,
-                          const loam_arg_desc* args, int nargs, void* stream) {
-  return guarded([&] {
-    require_device();
-    validate(kernel, n, iter, args, nargs); // nothing is copied for an illegal loop
-    cudaStream_t s = as_stream(stream);
-    std::vector<DevBuf<char>> bufs;
-    std::vector<std::pair<const void*, void*>> uploaded; // one copy per host array
-    auto up = [&](const void* host, size_t bytes) -> void* {
-      for (auto& [h, d] : uploaded)
-        if (h == host) return d;
-      bufs.emplace_back(bytes ? bytes : 1, s);
-      if (bytes) LG_CUDA(cudaMemcpyAsync(bufs.back().get(), host, bytes, cudaMemcpyHostToDevice, s));
-      uploaded.emplace_back(host, bufs.back().get());
-      return bufs.back().get();
-    };
-    auto alloc = [&](size_t bytes) -> void* {
-      bufs.emplace_back(bytes ? bytes : 1, s);
-      return bufs.back().get();
-    };
-    std::vector<loam_arg_desc> dargs(args, args + nargs);
-    std::vector<loam_map_desc> dmaps(2 * nargs);
-    std::vector<loam_sparsity_desc> dsp(nargs);
-    // immutable objects with an id stay resident; anonymous ones (id 0) are copied per call
-    auto keep = [&](int kind, uint64_t id, const void* host, size_t bytes) -> void* {
-      return id ? resident_copy(kind, id, host, bytes, s) : up(host, bytes);
-    };
-    auto map_up = [&](const loam_map_desc* m, loam_map_desc& d) {
-      d = *m;
-      d.values = static_cast<const int32_t*>(
-          keep(0, m->id, m->values, sizeof(int32_t) * (size_t)m->source_size * m->arity));
-      if (m->expand_dim > 1 && m->node_values)
-        d.node_values = static_cast<const int32_t*>(
-            keep(1, m->id, m->node_values, sizeof(int32_t) * (size_t)m->source_size * m->node_arity));
-    };
+namespace {
+// The loops of one host-convention call: every loop validated first (nothing
+// is copied for an illegal loop), one device copy per host array across the
+// loops, the loops run (one loop: execute; several: execute_blocks), every
+// written object downloaded.
+void run_host_loops(const loam_loop_desc* loops, int nloops, cudaStream_t s) {
+  for (int l = 0; l < nloops; ++l)
+    validate(loops[l].kernel, loops[l].iterset_size, loops[l].iterset_id, loops[l].args, loops[l].nargs);
+  std::vector<DevBuf<char>> bufs;
+  std::vector<std::pair<const void*, void*>> uploaded; // one copy per host array
+  auto up = [&](const void* host, size_t bytes) -> void* {
+    for (auto& [h, d] : uploaded)
+      if (h == host) return d;
+    bufs.emplace_back(bytes ? bytes : 1, s);
+    if (bytes) LG_CUDA(cudaMemcpyAsync(bufs.back().get(), host, bytes, cudaMemcpyHostToDevice, s));
+    uploaded.emplace_back(host, bufs.back().get());
+    return bufs.back().get();
+  };
+  // immutable objects with an id stay resident; anonymous ones (id 0) are copied per call
+  auto keep = [&](int kind, uint64_t id, const void* host, size_t bytes) -> void* {
+    return id ? resident_copy(kind, id, host, bytes, s) : up(host, bytes);
+  };
+  auto map_up = [&](const loam_map_desc* m, loam_map_desc& d) {
+    d = *m;
+    d.values = static_cast<const int32_t*>(
+        keep(0, m->id, m->values, sizeof(int32_t) * (size_t)m->source_size * m->arity));
+    if (m->expand_dim > 1 && m->node_values)
+      d.node_values = static_cast<const int32_t*>(
+          keep(1, m->id, m->node_values, sizeof(int32_t) * (size_t)m->source_size * m->node_arity));
+  };
+  struct DevLoop {
+    std::vector<loam_arg_desc> dargs;
+    std::vector<loam_map_desc> dmaps;
+    std::vector<loam_sparsity_desc> dsp;
+  };
+  std::vector<DevLoop> dl((size_t)nloops);
+  std::vector<std::pair<const void*, void*>> written; // host object -> its device copy (one per object)
+  for (int l = 0; l < nloops; ++l) {
+    const loam_arg_desc* args = loops[l].args;
+    const int nargs = loops[l].nargs;
+    DevLoop& D = dl[l];
+    D.dargs.assign(args, args + nargs);
+    D.dmaps.resize(2 * (size_t)nargs);
+    D.dsp.resize((size_t)nargs);
     for (int q = 0; q < nargs; ++q) {
       const loam_arg_desc& a = args[q];
-      loam_arg_desc& d = dargs[q];
-      if (a.map) { map_up(a.map, dmaps[2 * q]); d.map = &dmaps[2 * q]; }
-      if (a.col_map) { map_up(a.col_map, dmaps[2 * q + 1]); d.col_map = &dmaps[2 * q + 1]; }
+      loam_arg_desc& d = D.dargs[q];
+      if (a.map) { map_up(a.map, D.dmaps[2 * q]); d.map = &D.dmaps[2 * q]; }
+      if (a.col_map) { map_up(a.col_map, D.dmaps[2 * q + 1]); d.col_map = &D.dmaps[2 * q + 1]; }
       size_t count;
       if (a.kind == LOAM_ARG_MAT) {
         const loam_sparsity_desc* sp = a.sparsity;
-        dsp[q] = *sp;
-        dsp[q].row_ptr = static_cast<const int64_t*>(
+        D.dsp[q] = *sp;
+        D.dsp[q].row_ptr = static_cast<const int64_t*>(
             keep(2, sp->id, sp->row_ptr, sizeof(int64_t) * ((size_t)sp->nrows + 1)));
-        dsp[q].col_idx = static_cast<const int32_t*>(keep(3, sp->id, sp->col_idx, sizeof(int32_t) * (size_t)sp->nnz));
-        d.sparsity = &dsp[q];
+        D.dsp[q].col_idx = static_cast<const int32_t*>(keep(3, sp->id, sp->col_idx, sizeof(int32_t) * (size_t)sp->nnz));
+        d.sparsity = &D.dsp[q];
         count = (size_t)sp->nnz;
       } else if (a.kind == LOAM_ARG_DAT) {
         count = (size_t)a.set_size * a.dim;
@@ -287,21 +296,63 @@ int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t n, uint64_t it
       const bool needs_old = a.access == LOAM_READ || a.access == LOAM_RW ||
                              (a.access == LOAM_INC && !(a.flags & LOAM_ARG_ZERO)) ||
                              (a.kind != LOAM_ARG_DAT && a.access == LOAM_WRITE);
-      d.data = static_cast<double*>(needs_old ? up(a.data, sizeof(double) * count) : alloc(sizeof(double) * count));
-      if (!needs_old && a.kind == LOAM_ARG_DAT && a.access == LOAM_WRITE && a.map) {
-        // indirect WRITE leaves untouched entries as they were (test_parloop.cpp:182-200)
-        LG_CUDA(cudaMemcpyAsync(d.data, a.data, sizeof(double) * count, cudaMemcpyHostToDevice, s));
+      void* prior = nullptr; // an object an earlier loop of the call wrote: keep working on that copy
+      for (auto& [h, dv] : written)
+        if (h == a.data) prior = dv;
+      if (prior) {
+        d.data = static_cast<double*>(prior);
+        if (!needs_old) d.flags &= ~LOAM_ARG_ZERO;
+      } else if (needs_old) {
+        d.data = static_cast<double*>(up(a.data, sizeof(double) * count));
+      } else {
+        bufs.emplace_back(count ? sizeof(double) * count : 1, s);
+        d.data = reinterpret_cast<double*>(bufs.back().get());
+        if (a.kind == LOAM_ARG_DAT && a.access == LOAM_WRITE && a.map) {
+          // indirect WRITE leaves untouched entries as they were (test_parloop.cpp:182-200)
+          LG_CUDA(cudaMemcpyAsync(d.data, a.data, sizeof(double) * count, cudaMemcpyHostToDevice, s));
+        }
       }
+      if (a.access != LOAM_READ && !prior) written.emplace_back(a.data, d.data);
     }
-    execute(kernel, n, iter, dargs.data(), nargs, s);
-    for (int q = 0; q < nargs; ++q) {
-      const loam_arg_desc& a = args[q];
+  }
+  if (nloops == 1) {
+    execute(loops[0].kernel, loops[0].iterset_size, loops[0].iterset_id, dl[0].dargs.data(), loops[0].nargs, s);
+  } else {
+    std::vector<LoopDesc> ld((size_t)nloops);
+    for (int l = 0; l < nloops; ++l)
+      ld[l] = LoopDesc{loops[l].kernel, loops[l].iterset_size, loops[l].iterset_id, dl[l].dargs.data(), loops[l].nargs};
+    execute_blocks(ld.data(), nloops, s);
+  }
+  for (int l = 0; l < nloops; ++l)
+    for (int q = 0; q < loops[l].nargs; ++q) {
+      const loam_arg_desc& a = loops[l].args[q];
       if (a.access == LOAM_READ) continue;
-      size_t count = a.kind == LOAM_ARG_MAT ? (size_t)a.sparsity->nnz
-                     : a.kind == LOAM_ARG_DAT ? (size_t)a.set_size * a.dim : (size_t)a.dim;
-      if (count) LG_CUDA(cudaMemcpyAsync(a.data, dargs[q].data, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+      const size_t count = a.kind == LOAM_ARG_MAT ? (size_t)a.sparsity->nnz
+                           : a.kind == LOAM_ARG_DAT ? (size_t)a.set_size * a.dim : (size_t)a.dim;
+      if (count)
+        LG_CUDA(cudaMemcpyAsync(a.data, dl[l].dargs[q].data, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
     }
-    LG_CUDA(cudaStreamSynchronize(s));
+  LG_CUDA(cudaStreamSynchronize(s));
+}
+} // namespace
+
+int loam_gpu_execute_host(const loam_kernel_desc* kernel, int32_t n, uint64_t iter,
+                          const loam_arg_desc* args, int nargs, void* stream) {
+  return guarded([&] {
+    require_device();
+    const loam_loop_desc one{kernel, n, iter, args, nargs};
+    run_host_loops(&one, 1, as_stream(stream));
+  });
+}
+
+// fem::assemble_blocks (fem/assemble.hpp:439-448) under the host-memory
+// calling convention: the loops of loam_gpu_execute_blocks over host data.
+int loam_gpu_execute_blocks_host(const loam_loop_desc* loops, int nloops, void* stream) {
+  return guarded([&] {
+    require_device();
+    require(nloops >= 0 && (nloops == 0 || loops != nullptr), LOAM_ERR(InvalidArgument), "block loops without a list");
+    if (nloops == 0) return;
+    run_host_loops(loops, nloops, as_stream(stream));
   });
 }
 

@@ -149,8 +149,23 @@ public:
     d.source_id = source_->id();
     d.target_id = target_->id();
     d.id = id_;
+    if (node_) { // a dof-expanded map declares the node map it expands
+      const loam_map_desc n = node_->desc();
+      d.expand_dim = expand_dim_;
+      d.node_values = n.values;
+      d.node_arity = n.arity;
+      d.node_target_size = n.target_size;
+      d.node_id = n.id;
+    }
     return d;
   }
+  /// (make_expanded_map) the node map this map expands by `dim` dofs per node
+  void declare_node_map(std::shared_ptr<const Map> node, int dim) const {
+    node_ = std::move(node);
+    expand_dim_ = dim;
+  }
+  const std::shared_ptr<const Map>& node_map() const { return node_; }
+  int expand_dim() const { return expand_dim_; }
 
 private:
   SetPtr source_, target_;
@@ -159,10 +174,27 @@ private:
   std::string name_;
   detail::DeviceArray<int32_t> dev_;
   uint64_t id_ = detail::next_id();
+  mutable std::shared_ptr<const Map> node_;
+  mutable int expand_dim_ = 0;
 };
 using MapPtr = std::shared_ptr<const Map>;
 inline MapPtr make_map(SetPtr source, SetPtr target, int arity, std::vector<int> values, std::string name = "map") {
   return std::make_shared<const Map>(std::move(source), std::move(target), arity, std::move(values), std::move(name));
+}
+
+/// The dof-expanded map a vector-valued Mat needs (entries dim * node + d, the
+/// layout fem spaces with value_dim > 1 use), declaring its node map
+/// so the device works on the 1/dim-size node map.
+inline MapPtr make_expanded_map(const MapPtr& node_map, int dim, SetPtr dofs = nullptr, std::string name = "dof_map") {
+  require(dim >= 1, ErrorKind::InvalidArgument, "dof expansion must be positive");
+  if (!dofs) dofs = make_set(node_map->target()->size() * dim, name + "_dofs");
+  const std::vector<int>& v = node_map->values();
+  std::vector<int> exp(v.size() * (size_t)dim);
+  for (size_t i = 0; i < v.size(); ++i)
+    for (int d = 0; d < dim; ++d) exp[i * dim + d] = v[i] * dim + d;
+  auto m = make_map(node_map->source(), std::move(dofs), node_map->arity() * dim, std::move(exp), std::move(name));
+  m->declare_node_map(node_map, dim);
+  return m;
 }
 
 struct Coloring { // topology.hpp:78-81
@@ -540,6 +572,31 @@ inline void execute(const Parloop& loop, int threads = 1) {
     if (a.mat) a.mat->touched_by_device();
     if (a.global) a.global->touched_by_device();
   }
+}
+
+// fem::assemble_blocks (fem/assemble.hpp:439-448) issues one par_loop per block
+// of a nested BlockMat; execute_blocks takes those loops together: all are
+// validated before anything is written, then they run in order -- the
+// Taylor-Hood Stokes triple (stokes_a / stokes_b / stokes_bt over one cell set
+// and one pair of maps) as ONE launch.  Results visible on return.
+inline void execute_blocks(const std::vector<Parloop>& loops, int threads = 1) {
+  require(threads >= 1, ErrorKind::InvalidArgument, "thread count must be positive");
+  std::vector<detail::Descs> D(loops.size());
+  std::vector<loam_loop_desc> L(loops.size());
+  for (size_t i = 0; i < loops.size(); ++i) {
+    detail::build(loops[i], D[i], true);
+    L[i] = loam_loop_desc{&D[i].kd, loops[i].iterset->size(), loops[i].iterset->id(), D[i].args.data(),
+                          (int32_t)D[i].args.size()};
+  }
+  check(loam_gpu_execute_blocks(L.data(), (int)L.size(), nullptr));
+  check(loam_gpu_stream_sync(nullptr));
+  for (const Parloop& loop : loops)
+    for (const Arg& a : loop.args) {
+      if (a.access == Access::READ) continue;
+      if (a.dat) a.dat->touched_by_device();
+      if (a.mat) a.mat->touched_by_device();
+      if (a.global) a.global->touched_by_device();
+    }
 }
 
 // ---------------------------------------------------------------- matrix consumers

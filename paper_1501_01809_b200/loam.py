@@ -445,7 +445,7 @@ class HostLoop:
     writes; ``h2d_bytes`` / ``d2h_bytes`` count the per-call Dat transfers.
     """
 
-    def __init__(self, loop: Parloop, pin: bool = True):
+    def __init__(self, loop: Parloop, pin: bool = True, mirrors: Optional[dict] = None):
         self.loop = loop
         self._keep, self.outputs = [], []
         self.h2d_bytes = self.d2h_bytes = 0
@@ -454,7 +454,10 @@ class HostLoop:
         self.kd = kd
         self.descs = (capi.ArgDesc * max(len(loop.args), 1))()
 
-        mirrors = {}  # one host mirror per object: an id must name one host buffer
+        # one host mirror per object: an id must name one host buffer.  Loops
+        # that run in one call (run_host_blocks) share `mirrors`, so an object
+        # they all read (the coordinates) is one host array, uploaded once.
+        mirrors = {} if mirrors is None else mirrors
 
         def host(t) -> torch.Tensor:
             key = (id(t), t.data_ptr() if isinstance(t, torch.Tensor) else t.ctypes.data)
@@ -564,6 +567,21 @@ class HostLoop:
         capi.check(capi.lib().loam_gpu_execute_host_batch(
             C.byref(self.kd), self.loop.iterset.size, self.loop.iterset.id, arr, len(self.loop.args),
             len(step_descs), _stream() if stream is None else stream))
+
+
+def run_host_blocks(host_loops, stream: Optional[int] = None) -> None:
+    """fem::assemble_blocks (fem/assemble.hpp:439-448) under the host-memory
+    calling convention: the HostLoops' par_loops in one
+    loam_gpu_execute_blocks_host call (build them with a shared `mirrors`)."""
+    hl = list(host_loops)
+    arr = (capi.LoopDesc * max(len(hl), 1))()
+    for i, h in enumerate(hl):
+        arr[i].kernel = C.pointer(h.kd)
+        arr[i].iterset_size = h.loop.iterset.size
+        arr[i].iterset_id = h.loop.iterset.id
+        arr[i].args = C.cast(h.descs, C.POINTER(capi.ArgDesc))
+        arr[i].nargs = len(h.loop.args)
+    capi.check(capi.lib().loam_gpu_execute_blocks_host(arr, len(hl), _stream() if stream is None else stream))
 
 
 def validate(loop: Parloop) -> None:

@@ -317,6 +317,64 @@ static void test_rcm() { // test_topology.cpp rcm_order cases
   expect_error(ErrorKind::IndexOutOfRange, [] { rcm_order(2, {{3}, {0}}); });
 }
 
+// fem::assemble_blocks (fem/assemble.hpp:439-448): the Taylor-Hood triple through
+// execute_blocks (one launch) equals the three loops run one by one.
+static void test_execute_blocks_taylor_hood() {
+  const int n = 9, nv = (n + 1) * (n + 1), nc = 2 * n * n;
+  std::vector<Real> xy(2 * (size_t)nv);
+  std::vector<int> cv(3 * (size_t)nc), cn(6 * (size_t)nc);
+  CHECK(loam_gpu_unit_square_mesh(n, xy.data(), cv.data()) == 0);
+  CHECK(loam_gpu_jitter(2, n, 0.2, 7, xy.data()) == 0);
+  CHECK(loam_gpu_p2_cell_node_map(nc, nv, 2, cv.data(), cn.data()) > 0); // (returns the node count)
+  int nn = 0;
+  for (int x : cn) nn = std::max(nn, x + 1);
+  auto cells = make_set(nc), verts = make_set(nv), nodes = make_set(nn);
+  auto pm = make_map(cells, verts, 3, cv), vnm = make_map(cells, nodes, 6, cn);
+  auto vdm = make_expanded_map(vnm, 2);
+  auto X = make_dat(verts, 2, "coordinates");
+  {
+    auto w = X->mutable_view();
+    for (size_t i = 0; i < xy.size(); ++i) w[i] = xy[i];
+  }
+  auto spA = build_sparsity(vnm, vnm, 2, 2), spB = build_sparsity(pm, vnm, 1, 2), spT = build_sparsity(vnm, pm, 2, 1);
+  auto loops = [&](const MatPtr& A, const MatPtr& B, const MatPtr& T) {
+    return std::vector<Parloop>{
+        {kernel("stokes_a_p2_tri", {1.0}), cells, {arg(A, Access::INC, vdm, vdm), arg(X, Access::READ, pm)}},
+        {kernel("stokes_b_p2_tri"), cells, {arg(B, Access::INC, pm, vdm), arg(X, Access::READ, pm)}},
+        {kernel("stokes_bt_p2_tri"), cells, {arg(T, Access::INC, vdm, pm), arg(X, Access::READ, pm)}}};
+  };
+  auto A1 = make_mat(spA), B1 = make_mat(spB), T1 = make_mat(spT);
+  for (const Parloop& lp : loops(A1, B1, T1)) execute(lp);
+  auto A2 = make_mat(spA), B2 = make_mat(spB), T2 = make_mat(spT);
+  execute_blocks(loops(A2, B2, T2)); // plan
+  A2->zero();
+  B2->zero();
+  T2->zero();
+  const int64_t before = loam_gpu_launch_count();
+  execute_blocks(loops(A2, B2, T2));
+  CHECK(loam_gpu_launch_count() - before == 1);
+  auto close = [](const std::vector<Real>& a, const std::vector<Real>& b) {
+    Real num = 0, den = 0;
+    for (size_t i = 0; i < a.size(); ++i) {
+      num = std::max(num, std::abs(a[i] - b[i]));
+      den = std::max(den, std::abs(b[i]));
+    }
+    return a.size() == b.size() && num <= 1e-12 * den;
+  };
+  CHECK(close(A2->values(), A1->values()));
+  CHECK(close(B2->values(), B1->values()));
+  CHECK(close(T2->values(), T1->values()));
+  // B^T really is the transpose of B (to rounding: rows of B and of B^T are owned by different items)
+  for (int v = 0; v < nv; v += 7)
+    for (int d = 0; d < 2 * nn; d += 11) CHECK(std::abs(B2->at(v, d) - T2->at(d, v)) <= 1e-15);
+  // an illegal loop in the list: nothing is written
+  auto A3 = make_mat(spA), B3 = make_mat(spB), T3 = make_mat(spT);
+  auto bad = loops(A3, B3, T3);
+  bad[2].args[0] = arg(T3, Access::INC, vdm, vdm);
+  expect_error(ErrorKind::ShapeMismatch, [&] { execute_blocks(bad); });
+  for (Real x : A3->values()) CHECK(x == 0.0);
+}
+
 int main() {
   loam_gpu_set_option(LOAM_OPT_TEST_KERNELS, 1); // the reference test-suite kernels
   const std::vector<std::pair<const char*, void (*)()>> cases = {
@@ -335,6 +393,7 @@ int main() {
       {"block spmv skips zero blocks and swaps components", test_block_spmv},
       {"cg known answers, breakdown, maxit, block operator", test_cg},
       {"rcm_order known answers and errors", test_rcm},
+      {"execute_blocks: Taylor-Hood triple in one launch", test_execute_blocks_taylor_hood},
   };
   for (auto& [name, fn] : cases) {
     const int before = g_fail;

@@ -226,3 +226,26 @@ def test_validation_errors_come_before_any_write():
         L.execute_blocks([w.loops[0], w.loops[1], bad])
     for o, k in zip(w.outputs, keep):
         assert np.array_equal(o.host_values(), k)
+
+
+def test_host_convention_blocks_run_fused_and_match():
+    """loam_gpu_execute_blocks_host: host buffers in, host buffers out, the
+    triple still one launch (the loops share the coordinates' host array)."""
+    w = configs.Workload(5, 11)
+    refs = dict(zip(map(id, w.outputs), oracle_blocks(w.inputs)))
+    w.reset()
+    shared = {}
+    hls = [L.HostLoop(lp, mirrors=shared) for lp in w.loops]
+    L.run_host_blocks(hls)  # plan
+    before = capi.launch_count()
+    L.run_host_blocks(hls)
+    assert capi.launch_count() - before == 1
+    for h in hls:
+        ref = refs[id(h.loop.args[0].mat)]
+        assert rel(h.outputs[0].numpy()[: len(ref)], ref) <= TOL
+    # separate mirrors: the loops no longer share the coordinate array -> loop by loop, same values
+    hl2 = [L.HostLoop(lp) for lp in w.loops]
+    L.run_host_blocks(hl2)
+    for h in hl2:
+        ref = refs[id(h.loop.args[0].mat)]
+        assert rel(h.outputs[0].numpy()[: len(ref)], ref) <= TOL
