@@ -427,8 +427,15 @@ __device__ __forceinline__ void cell_gather(const CellArgs& a, int e, double (&X
 // are one sorted map whose first gdim+1 entries are the vertices (P2 actions,
 // config 3).  One thread's 10-entry row is 40 scattered bytes per lane
 // otherwise -- 10 load instructions touching ~40 sectors each per warp.
+// (build option: a register cap through min blocks per SM; the default leaves the
+// allocation to ptxas -- 96 registers, 5 CTAs / SM.  A bound of 1 makes it take 122.)
+#ifdef LOAM_GPU_CELLROWS_MINB
+#define LOAM_GPU_CELLROWS_BOUNDS __launch_bounds__(128, LOAM_GPU_CELLROWS_MINB)
+#else
+#define LOAM_GPU_CELLROWS_BOUNDS __launch_bounds__(128)
+#endif
 template <class F>
-__global__ void __launch_bounds__(128) k_cell_vec_rows(const __grid_constant__ CellArgs a) {
+__global__ void LOAM_GPU_CELLROWS_BOUNDS k_cell_vec_rows(const __grid_constant__ CellArgs a) {
   constexpr int NRN = F::NRN, GD = F::GD, NV = GD + 1;
   static_assert((32 * NRN) % 4 == 0, "row block of a warp must be a whole number of int4");
   __shared__ __align__(16) int32_t rows_s[4][32 * NRN];

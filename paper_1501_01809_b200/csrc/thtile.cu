@@ -404,7 +404,7 @@ struct ThtileArgs {
 };
 
 #ifndef LOAM_GPU_TH_MINB
-#define LOAM_GPU_TH_MINB 3
+#define LOAM_GPU_TH_MINB 4
 #endif
 
 __device__ __forceinline__ void th_load(const double* win, int slot, double (&x)[2]) {
