@@ -256,7 +256,10 @@ class Rotation:
         launches, one pair of events on `stream`)."""
         for c in self.chunks(steps):
             self.graph(c)  # captured before the timed region
-        self.replay_steps(max(warmup, 1))
+        # warm-up: >= `warmup` untimed steps through the SAME graph(s) the timed
+        # region replays (a graph's first launch also uploads it to the device)
+        for _ in range(max(1, -(-max(warmup, 1) // steps))):
+            self.replay_steps(steps)
         e0, e1 = self.torch.cuda.Event(enable_timing=True), self.torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         self.replay_steps(steps)

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -953,11 +954,121 @@ void build_chunks(PairPlan& pp, const CsrView& csr, int smax, int max_rows, cuda
   LG_CUDA(cudaStreamSynchronize(s)); // host vector goes out of scope
 }
 
+// Row-owner sparsity build: one thread per row node merges the column nodes
+// of the cells around it (the node -> cell inverse of the row map) into a
+// sorted, duplicate-free list -- pass 1 counts, pass 2 (after the scan) writes
+// the dof-expanded columns.  No 64-bit key per (cell, i, j) is materialised or
+// sorted (the radix path below sorts ncells * arity_r * arity_c keys); rows
+// with more than kRowCap distinct column nodes send the whole build there.
+constexpr int kRowCap = 192;
+
+template <bool FILL>
+__global__ void __launch_bounds__(128) k_row_cols(const int32_t* __restrict__ ptr, const int32_t* __restrict__ pairs,
+                                                  int ar_r, const int32_t* __restrict__ cm, int ar_c, int nr,
+                                                  int32_t* __restrict__ counts, int* overflow,
+                                                  const int64_t* __restrict__ rp, int rd, int cd,
+                                                  int32_t* __restrict__ ci) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nr) return;
+  int list[kRowCap];
+  int len = 0;
+  bool over = false;
+  for (int p = ptr[r]; p < ptr[r + 1] && !over; ++p) {
+    const int64_t c = pairs[p] / ar_r;
+    for (int j = 0; j < ar_c; ++j) {
+      const int x = __ldg(cm + c * ar_c + j);
+      int lo = 0, hi = len;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (list[mid] < x) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < len && list[lo] == x) continue;
+      if (len == kRowCap) {
+        over = true;
+        break;
+      }
+      for (int q = len; q > lo; --q) list[q] = list[q - 1];
+      list[lo] = x;
+      ++len;
+    }
+  }
+  if constexpr (!FILL) {
+    counts[r] = len;
+    if (over) *overflow = 1;
+  } else {
+    for (int d = 0; d < rd; ++d) {
+      int32_t* dst = ci + rp[(int64_t)r * rd + d];
+      for (int i = 0; i < len; ++i)
+        for (int x = 0; x < cd; ++x) dst[(int64_t)i * cd + x] = list[i] * cd + x;
+    }
+  }
+}
+
+// node -> cells inverse of a map by counting + atomic cursors (the order of a
+// node's cells is arbitrary: k_row_cols sorts what it merges)
+__global__ void k_inv_fill(const int32_t* __restrict__ m, int64_t np, int arity, const int32_t* __restrict__ ptr,
+                           int32_t* __restrict__ cursor, int32_t* __restrict__ cells) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= np) return;
+  const int r = m[t];
+  cells[ptr[r] + atomicAdd(cursor + r, 1)] = (int32_t)t; // the pair code cell * arity + i, as build_pairs
+}
+
+bool build_sparsity_rows(const MapView& rows, const MapView& cols, int rd, int cd, int64_t** row_ptr,
+                         int32_t** col_idx, int64_t* nnz, cudaStream_t s) {
+  const int n = rows.n, nr = rows.target;
+  if (n == 0 || nr == 0 || (int64_t)n * rows.arity >= (int64_t(1) << 31)) return false;
+  const int64_t np = (int64_t)n * rows.arity;
+  DevBuf<int32_t> pptr(nr + 1, s), pcells(np, s), cursor(nr + 1, s);
+  LG_CUDA(cudaMemsetAsync(cursor.get(), 0, sizeof(int32_t) * (nr + 1), s));
+  k_count<<<ceil_div(np, kTPB), kTPB, 0, s>>>(rows.v, np, cursor.get());
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, cursor.get(), pptr.get(), nr + 1, s);
+  }, s);
+  LG_CUDA(cudaMemsetAsync(cursor.get(), 0, sizeof(int32_t) * (nr + 1), s));
+  k_inv_fill<<<ceil_div(np, kTPB), kTPB, 0, s>>>(rows.v, np, rows.arity, pptr.get(), cursor.get(), pcells.get());
+  count_launch(2);
+  LG_LAUNCH_CHECK();
+  DevBuf<int32_t> counts(nr + 1, s);
+  DevBuf<int64_t> node_off(nr + 1, s);
+  DevBuf<int> over(1, s);
+  LG_CUDA(cudaMemsetAsync(counts.get(), 0, sizeof(int32_t) * (nr + 1), s));
+  LG_CUDA(cudaMemsetAsync(over.get(), 0, sizeof(int), s));
+  k_row_cols<false><<<ceil_div(nr, 128), 128, 0, s>>>(pptr.get(), pcells.get(), rows.arity, cols.v, cols.arity, nr,
+                                                      counts.get(), over.get(), nullptr, rd, cd, nullptr);
+  count_launch();
+  LG_LAUNCH_CHECK();
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, counts.get(), node_off.get(), nr + 1, s);
+  }, s);
+  int hover = 0;
+  int64_t nu = 0;
+  LG_CUDA(cudaMemcpyAsync(&hover, over.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(&nu, node_off.get() + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  if (hover) return false;
+  const int64_t nrows = (int64_t)nr * rd;
+  const int64_t total = nu * rd * cd;
+  require(total < (int64_t(1) << 40), LOAM_ERR(InvalidArgument), "sparsity too large");
+  LG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(row_ptr), sizeof(int64_t) * (nrows + 1), s));
+  LG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(col_idx), sizeof(int32_t) * (total ? total : 1), s));
+  k_expand_rowptr<<<ceil_div(nrows + 1, kTPB), kTPB, 0, s>>>(node_off.get(), nr, rd, cd, *row_ptr);
+  k_row_cols<true><<<ceil_div(nr, 128), 128, 0, s>>>(pptr.get(), pcells.get(), rows.arity, cols.v, cols.arity, nr,
+                                                     nullptr, nullptr, *row_ptr, rd, cd, *col_idx);
+  count_launch(2);
+  LG_LAUNCH_CHECK();
+  *nnz = total;
+  return true;
+}
+
 void build_sparsity_dev(const MapView& rows, const MapView& cols, int rd, int cd,
                         int64_t** row_ptr, int32_t** col_idx, int64_t* nnz, cudaStream_t s) {
   require(rows.n == cols.n, LOAM_ERR(SourceMismatch),
           "row and column maps must share their source set");
   const int n = rows.n;
+  static const bool sort_only = std::getenv("LOAM_GPU_SPARSITY_SORT") != nullptr; // developer: the radix path
+  if (!sort_only && build_sparsity_rows(rows, cols, rd, cd, row_ptr, col_idx, nnz, s)) return;
   const int64_t nk = (int64_t)n * rows.arity * cols.arity;
   require(nk < (int64_t(1) << 31), LOAM_ERR(InvalidArgument), "sparsity key count exceeds 2^31");
   DevBuf<unsigned long long> keys(nk, s), sorted(nk, s);
