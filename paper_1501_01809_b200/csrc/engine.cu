@@ -35,6 +35,7 @@
 #include "etile.cuh"
 #include "ltile.cuh"
 #include "thtile.cuh"
+#include "wtile.cuh"
 #include "ntile.cuh"
 #include "rtile.cuh"
 #include "patch.cuh"
@@ -2603,6 +2604,8 @@ struct FastPlan {
   PTilePlan pt;
   bool use_etile = false;  // edge tiles (scalar P2 matrices, etile.cuh)
   EtilePlan et;
+  bool use_wtile = false;  // link-walk tiles (scalar P2 tetrahedra on manifold meshes, wtile.cuh)
+  WtilePlan wt;
   bool use_ntile = false;  // node-block tiles (vector P1 elasticity, ntile.cuh)
   NtilePlan nt;
   bool use_ltile = false;  // edge-link tiles (the same loops on manifold meshes, ltile.cuh)
@@ -2964,6 +2967,23 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       P->exact = true;
       SortedMap sx;
       gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, sx, s);
+      // scalar P2 tetrahedra: the edge rows walk their links (wtile.cuh); the
+      // edge tiles stay for triangles, the Stokes A block, non-manifold
+      // meshes and deterministic mode (fixed-order diagonal sums)
+      if (k.gd == 3 && k.rd == 1 && k.cd == 1 && k.nrn == 10 && !options().deterministic &&
+          !std::getenv("LOAM_GPU_NO_WTILE")) {
+        WtileSpec ws;
+        ws.tile_rows = env_int("LOAM_GPU_WT_ROWS", ws.tile_rows);
+        if (build_wtile(P->wt, ws, n, R.v.target, X->target_size, srows.v.get(), sx.v.get(), P->pp, sp->row_ptr,
+                        sp->col_idx, sp->nnz, s)) {
+          plan_tick("walk tiles", s);
+          P->use_wtile = true;
+          return P;
+        }
+        require(!std::getenv("LOAM_GPU_WT_REQUIRE"), LOAM_ERR(UnsupportedForm),
+                "walk-tile plan declined (LOAM_GPU_WT_REQUIRE is set: tests of that path)");
+        P->wt = WtilePlan{};
+      }
       EtileSpec es;
       es.tile_rows = env_int("LOAM_GPU_ET_ROWS", es.tile_rows);
       es.tile_seg = env_int("LOAM_GPU_ET_SEG", es.tile_seg);
@@ -3333,6 +3353,13 @@ void run_fast(const Entry& k, int n, const loam_arg_desc* args, int nargs, const
   if (P->use_rtile) {
     const int ctr = P->counter.acquire(s);
     launch_rtile(P->rt, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
+                 P->counter.next(ctr), P->counter.exits(ctr), s);
+    P->counter.commit(ctr, s);
+    return;
+  }
+  if (P->use_wtile) {
+    const int ctr = P->counter.acquire(s);
+    launch_wtile(P->wt, k.form, args[1].data, args[0].data, prm, !(args[0].flags & LOAM_ARG_ZERO),
                  P->counter.next(ctr), P->counter.exits(ctr), s);
     P->counter.commit(ctr, s);
     return;

@@ -309,17 +309,15 @@ bool build_thtile(ThtilePlan& out, const ThtileSpec& sp, int ncells, int nnodes,
         nwo[q] = hv[(size_t)c * 6 + 3 + la];            // edge node (w, opposite)
       }
       if (nce == 2 && xo[0] == xo[1]) return fail();
-      cols = {xv, xw, e, xo[0], nwo[0], nvo[0]};
-      pcols = {xv, xw, xo[0]};
-      if (nce == 2) {
-        cols.insert(cols.end(), {xo[1], nwo[1], nvo[1]});
-        pcols.push_back(xo[1]);
-      }
-      const std::vector<int> order = cols, porder = pcols; // device order: v, w, e, p, (w,p), (v,p), q, (w,q), (v,q)
+      // device order: v, w, e, p, (w,p), (v,p), q, (w,q), (v,q) | v, w, p, q
+      const int order[9] = {xv, xw, e, xo[0], nwo[0], nvo[0], xo[1], nwo[1], nvo[1]};
+      const int porder[4] = {xv, xw, xo[0], xo[1]};
+      const int L = nce == 2 ? 9 : 6, Lp = nce == 2 ? 4 : 3;
+      cols.assign(order, order + L);
+      pcols.assign(porder, porder + Lp);
       std::sort(cols.begin(), cols.end());
       std::sort(pcols.begin(), pcols.end());
       if (std::adjacent_find(cols.begin(), cols.end()) != cols.end()) return fail();
-      const int L = (int)cols.size(), Lp = (int)pcols.size();
       const int64_t a0 = hA[(size_t)2 * e], a1 = hA[(size_t)2 * e + 1], a2 = hA[(size_t)2 * e + 2];
       const int64_t t0 = hT[(size_t)2 * e], t1 = hT[(size_t)2 * e + 1], t2 = hT[(size_t)2 * e + 2];
       if (a1 - a0 != 2 * L || a2 - a1 != 2 * L || t1 - t0 != Lp || t2 - t1 != Lp) return fail();
@@ -337,9 +335,9 @@ bool build_thtile(ThtilePlan& out, const ThtileSpec& sp, int ncells, int nnodes,
       put16(it.rec + 2, (int)(t0 - hT[(size_t)2 * e0]));
       it.rec[4] = (uint8_t)(L | (nce == 2 ? 0x80 : 0));
       it.rec[5] = (uint8_t)Lp;
-      for (size_t j = 0; j < order.size(); ++j) it.rec[6 + j] = (uint8_t)rank_in(cols, order[j]);
+      for (int j = 0; j < L; ++j) it.rec[6 + j] = (uint8_t)rank_in(cols, order[j]);
       int packed = 0;
-      for (size_t j = 0; j < porder.size(); ++j) packed |= rank_in(pcols, porder[j]) << (2 * j);
+      for (int j = 0; j < Lp; ++j) packed |= rank_in(pcols, porder[j]) << (2 * j);
       it.rec[15] = (uint8_t)packed;
       items.push_back(it);
     }
