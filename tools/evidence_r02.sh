@@ -17,7 +17,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ncu --set full --clock-control none --import-source on -k regex:k_ring -s 12 -c 1 -o $O/c2_ring python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-config-table > $O/ncu_c2.log 2>&1; echo ncu_c2_rc=$?
 summ $O/c2_ring
 for c in 1 3r 3m 4 5; do
-  case $c in 1) k=k_star;; 3r) k=k_cell;; 3m) k=k_etile;; 4) k=k_ltile;; 5) k=k_thtile;; esac
+  case $c in 1) k=k_star;; 3r) k=k_cell;; 3m) k=k_wtile;; 4) k=k_ltile;; 5) k=k_thtile;; esac
   python bench.py --all-configs --configs $c --strategies auto --steps 3 > $O/plain_cfg$c.log 2>&1; echo plain_$c rc=$?
   ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o $O/cfg$c python bench.py --all-configs --configs $c --strategies auto --steps 3 > $O/ncu_cfg$c.log 2>&1; echo ncu_$c rc=$?
   summ $O/cfg$c
