@@ -25,7 +25,10 @@ namespace {
 inline int up16(int x) { return (x + 15) & ~15; }
 
 constexpr int kNV = 4;            // P1 tet
-constexpr int kLtConsumers = 128; // consumer threads per CTA = blocks per tile at most
+#ifndef LOAM_GPU_LT_NT
+#define LOAM_GPU_LT_NT 128
+#endif
+constexpr int kLtConsumers = LOAM_GPU_LT_NT; // consumer threads per CTA = blocks per tile at most
 
 } // namespace
 
