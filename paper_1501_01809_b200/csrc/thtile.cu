@@ -184,9 +184,15 @@ bool build_thtile(ThtilePlan& out, const ThtileSpec& sp, int ncells, int nnodes,
         if (!lw.add(a, a, b, b)) return fail();
       }
       const int nc = (int)sc.size();
-      if (nc < 1 || nc + 1 > LinkWalk::kMax || !lw.walk(nc, seq)) return fail();
-      const bool ring = seq.front() == seq.back();
-      const int k = ring ? nc : nc + 1; // spokes
+      if (nc == 0) { // a vertex of no cell (sub-mesh loops): its rows must be empty, nothing to compute
+        if (hA[(size_t)2 * v + 2] != hA[(size_t)2 * v] || hB[v + 1] != hB[v] || hT[(size_t)2 * v + 2] != hT[(size_t)2 * v])
+          return fail();
+        seq.assign(1, -1);
+      } else if (nc + 1 > LinkWalk::kMax || !lw.walk(nc, seq)) {
+        return fail();
+      }
+      const bool ring = nc > 0 && seq.front() == seq.back();
+      const int k = nc == 0 ? 0 : ring ? nc : nc + 1; // spokes
       if (k > spoke_items) return fail();
       // cell i of the walk = (v, seq[i], seq[i + 1])
       auto cell_of = [&](int a, int b) -> const StarCell* {
@@ -234,6 +240,10 @@ bool build_thtile(ThtilePlan& out, const ThtileSpec& sp, int ncells, int nnodes,
         cols.push_back(S.nvw);
         pcols.push_back(S.w);
       }
+      if (nc == 0) { // empty rows
+        cols.clear();
+        pcols.clear();
+      }
       std::sort(cols.begin(), cols.end());
       std::sort(pcols.begin(), pcols.end());
       if (std::adjacent_find(cols.begin(), cols.end()) != cols.end()) return fail();
@@ -245,11 +255,11 @@ bool build_thtile(ThtilePlan& out, const ThtileSpec& sp, int ncells, int nnodes,
         return fail();
       // close the tile before this vertex when it no longer fits
       auto fits = [&] {
-        return (int)items.size() + k <= spoke_items && v - v0 < 255 && hA[(size_t)2 * v + 2] - hA[(size_t)2 * v0] < 60000 &&
+        return (int)items.size() + k <= spoke_items && v - v0 < NT && hA[(size_t)2 * v + 2] - hA[(size_t)2 * v0] < 60000 &&
                hT[(size_t)2 * v + 2] - hT[(size_t)2 * v0] < 60000;
       };
-      if (!items.empty() && !fits()) {
-        if (!emit(0, v0, v)) return fail();
+      if (v > v0 && !fits()) {
+        if (!items.empty() && !emit(0, v0, v)) return fail();
         items.clear();
         dinfo.clear();
         v0 = v;
@@ -289,7 +299,11 @@ bool build_thtile(ThtilePlan& out, const ThtileSpec& sp, int ncells, int nnodes,
     int e0 = e_begin;
     for (int e = e_begin; e < eend; ++e) {
       const int nce = hp[e + 1] - hp[e];
-      if (nce < 1 || nce > 2) return fail();
+      if (nce == 0) { // a node of no cell: empty rows
+        if (hA[(size_t)2 * e + 2] != hA[(size_t)2 * e] || hT[(size_t)2 * e + 2] != hT[(size_t)2 * e]) return fail();
+        continue;
+      }
+      if (nce > 2) return fail();
       int xv = -1, xw = -1, xo[2] = {-1, -1}, nvo[2] = {-1, -1}, nwo[2] = {-1, -1};
       for (int q = 0; q < nce; ++q) {
         const int c = hpairs[hp[e] + q] / 6, l = hpairs[hp[e] + q] % 6;
@@ -701,12 +715,14 @@ __global__ void __launch_bounds__(kThConsumers + 32, LOAM_GPU_TH_MINB) k_thtile(
           s1 += scr[3 * (first + i) + 1];
           s2 += scr[3 * (first + i) + 2];
         }
-        double* r0 = sA + baseA + 2 * selfA;
-        *reinterpret_cast<double2*>(r0) = make_double2(s0, 0.0);
-        *reinterpret_cast<double2*>(r0 + 2 * L) = make_double2(0.0, s0);
-        *reinterpret_cast<double2*>(sB + baseB + 2 * selfA) = make_double2(s1, s2);
-        sT[baseT + selfT] = s1;
-        sT[baseT + Lp + selfT] = s2;
+        if (ns) { // (a vertex of no cell has empty rows)
+          double* r0 = sA + baseA + 2 * selfA;
+          *reinterpret_cast<double2*>(r0) = make_double2(s0, 0.0);
+          *reinterpret_cast<double2*>(r0 + 2 * L) = make_double2(0.0, s0);
+          *reinterpret_cast<double2*>(sB + baseB + 2 * selfA) = make_double2(s1, s2);
+          sT[baseT + selfT] = s1;
+          sT[baseT + Lp + selfT] = s2;
+        }
       }
     }
     __syncwarp();

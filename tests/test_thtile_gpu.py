@@ -210,9 +210,8 @@ def test_submesh_with_its_own_patterns_runs_fused():
         refs.append(O.assemble_matrix(kind, 2, 2, sel.size, rm, ra, cm, ca, cv, m.coords, rp, ci, params=prm))
     for o, r in zip(outs, refs):
         assert rel(o.host_values(), r) <= TOL
-    # unused vertices / nodes of the whole mesh have empty rows: the fused plan
-    # either serves them (one launch) or declines (three or more)
-    assert launches == 1 or launches >= 3
+    # unused vertices / nodes of the whole mesh have empty rows: still one launch
+    assert launches == 1
 
 
 def test_validation_errors_come_before_any_write():
