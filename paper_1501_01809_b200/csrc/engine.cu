@@ -2968,12 +2968,11 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       SortedMap sx;
       gather_rows(MapView{X->values, n, X->arity, X->target_size}, perm, sx, s);
       // scalar P2 tetrahedra: the edge rows walk their links (wtile.cuh); the
-      // edge tiles stay for triangles, the Stokes A block, non-manifold
-      // meshes and deterministic mode (fixed-order diagonal sums)
-      if (k.gd == 3 && k.rd == 1 && k.cd == 1 && k.nrn == 10 && !options().deterministic &&
-          !std::getenv("LOAM_GPU_NO_WTILE")) {
+      // edge tiles stay for triangles, the Stokes A block and non-manifold meshes
+      if (k.gd == 3 && k.rd == 1 && k.cd == 1 && k.nrn == 10 && !std::getenv("LOAM_GPU_NO_WTILE")) {
         WtileSpec ws;
         ws.tile_rows = env_int("LOAM_GPU_WT_ROWS", ws.tile_rows);
+        ws.det = options().deterministic != 0;
         if (build_wtile(P->wt, ws, n, R.v.target, X->target_size, srows.v.get(), sx.v.get(), P->pp, sp->row_ptr,
                         sp->col_idx, sp->nnz, s)) {
           plan_tick("walk tiles", s);

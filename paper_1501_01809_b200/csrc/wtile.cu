@@ -97,6 +97,7 @@ bool build_wtile(WtilePlan& out, const WtileSpec& sp, int ncells, int nnodes, in
   };
   std::vector<TileChunk> tch(plan_threads());
   const int nedges = nnodes - nverts;
+  std::vector<int32_t> ev(sp.det ? nedges : 0), ew(sp.det ? nedges : 0); // deterministic mode: the rows' endpoints
   const int ntch = parallel_chunks(nedges, 1, [&](int t, int64_t cb0, int64_t cb1) {
     TileChunk& O = tch[t];
     struct Stamps {
@@ -295,7 +296,11 @@ bool build_wtile(WtilePlan& out, const WtileSpec& sp, int ncells, int nnodes, in
         if (xw < seq[i] && xw < seq[i + 1]) ownv |= 1u << i; // (v, w) is v's edge to its smallest other vertex of the cell
         if (xv < seq[i] && xv < seq[i + 1]) ownw |= 1u << i;
       }
-      it.own = ownv | ownw << 16;
+      it.own = ownv | ownw << 12 | (uint32_t)(e - e0) << 24; // + the row's index in its tile
+      if (sp.det) {
+        ev[e - nverts] = xv;
+        ew[e - nverts] = xw;
+      }
       it.hdr = (uint32_t)(hrp[e] - hrp[e0]) | (uint32_t)L << 16 | (uint32_t)nce << 24 | (ring ? 1u << 28 : 0u);
       items.push_back(it);
     }
@@ -335,6 +340,23 @@ bool build_wtile(WtilePlan& out, const WtileSpec& sp, int ncells, int nnodes, in
   upload(out.tiles, tiles);
   upload(out.runs, runs);
   upload(out.dpos, dpos);
+  out.det = sp.det;
+  out.nedges = nedges;
+  if (sp.det) { // per vertex: the diagonal-share slots (2 (e - nverts) + endpoint) of its edges, ascending
+    std::vector<int32_t> dptr(nverts + 1, 0), dslots(2 * (size_t)nedges);
+    for (int e = 0; e < nedges; ++e) {
+      ++dptr[ev[e] + 1];
+      ++dptr[ew[e] + 1];
+    }
+    for (int v = 0; v < nverts; ++v) dptr[v + 1] += dptr[v];
+    std::vector<int32_t> cur(dptr.begin(), dptr.end() - 1);
+    for (int e = 0; e < nedges; ++e) {
+      dslots[cur[ev[e]]++] = 2 * e;
+      dslots[cur[ew[e]]++] = 2 * e + 1;
+    }
+    upload(out.dptr, dptr);
+    upload(out.dslots, dslots);
+  }
   LG_CUDA(cudaStreamSynchronize(s));
   return true;
 }
@@ -357,7 +379,20 @@ struct WtileArgs {
   FormParams prm;
   int accumulate;
   int off_seg, off_buf, buf_bytes, b_win;
+  double* dsum; // deterministic mode: the rows' diagonal shares by (edge, endpoint), summed by k_wt_dsum
+  int nverts;
 };
+
+// Deterministic diagonals: vertex v = its edges' shares in edge order.
+__global__ void k_wt_dsum(const int32_t* __restrict__ dpos, const int32_t* __restrict__ dptr,
+                          const int32_t* __restrict__ dslots, int n, const double* __restrict__ dsum,
+                          double* __restrict__ out, int accumulate) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  double acc = 0.0;
+  for (int q = dptr[v]; q < dptr[v + 1]; ++q) acc += dsum[dslots[q]];
+  out[dpos[v]] = accumulate ? out[dpos[v]] + acc : acc;
+}
 
 __global__ void k_wt_zero(double* __restrict__ out, const int32_t* __restrict__ dpos, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -473,6 +508,7 @@ __global__ void __launch_bounds__(kWtConsumers + 32, LOAM_GPU_WT_MINB) k_wtile(c
     if (tile < 0) break;
     const int4* sm4 = slot_meta + 4 * (k % STAGES);
     const int4 m1 = sm4[1], m2 = sm4[2], m3 = sm4[3];
+    const int n0 = sm4[0].z; // the tile's first row
     const int E0 = m1.x, len = m1.y, nitems = m1.z, off_s = m2.z, off_r = m2.w, off_p = m3.x, maxlv = m3.y;
     const unsigned char* buf = ring(k);
     const uint32_t* H = reinterpret_cast<const uint32_t*>(buf);
@@ -527,7 +563,7 @@ __global__ void __launch_bounds__(kWtConsumers + 32, LOAM_GPU_WT_MINB) k_wtile(c
         row[R[(3 + 3 * maxlv + i) * NT + tid]] = o[4];
         avw += wt_vv<FORM>(G, 0, 1, a.prm);
         if ((own >> i) & 1u) dv += wt_vv<FORM>(G, 0, 0, a.prm);
-        if ((own >> (16 + i)) & 1u) dw += wt_vv<FORM>(G, 1, 1, a.prm);
+        if ((own >> (12 + i)) & 1u) dw += wt_vv<FORM>(G, 1, 1, a.prm);
 #pragma unroll
         for (int d = 0; d < 3; ++d) X[2][d] = X[3][d];
       }
@@ -547,8 +583,14 @@ __global__ void __launch_bounds__(kWtConsumers + 32, LOAM_GPU_WT_MINB) k_wtile(c
       put(P[NT + tid], aw);
       put(P[2 * NT + tid], avw);
       put(P[3 * NT + tid], avw);
-      if (dv != 0.0) atomicAdd(a.out + P[4 * NT + tid], dv);
-      if (dw != 0.0) atomicAdd(a.out + P[5 * NT + tid], dw);
+      if (a.dsum) { // deterministic: the shares in slots, summed per vertex in edge order (k_wt_dsum)
+        const int64_t ei = (int64_t)(n0 - a.nverts) + (own >> 24);
+        a.dsum[2 * ei] = dv;
+        a.dsum[2 * ei + 1] = dw;
+      } else {
+        if (dv != 0.0) atomicAdd(a.out + P[4 * NT + tid], dv);
+        if (dw != 0.0) atomicAdd(a.out + P[5 * NT + tid], dw);
+      }
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&empty[k % STAGES]); // the stage's records and window are read
@@ -597,11 +639,16 @@ void go_wtile(const WtilePlan& p, WtileArgs& a, int off, cudaStream_t s) {
 void launch_wtile(const WtilePlan& p, int form, const double* coords, double* out, const FormParams& prm,
                   bool accumulate, int* next_tile, int* reset_tile, cudaStream_t s) {
   if (p.ntiles == 0) return;
-  if (!accumulate) { // the vertex diagonals are RED-summed: start from zero
+  DevBuf<double> dsum;
+  if (p.det) {
+    dsum.alloc(2 * (size_t)std::max(p.nedges, 1), s);
+  } else if (!accumulate) { // the vertex diagonals are RED-summed: start from zero
     k_wt_zero<<<ceil_div(p.nverts, 256), 256, 0, s>>>(out, p.dpos.get(), p.nverts);
     count_launch();
   }
   WtileArgs a{};
+  a.dsum = p.det ? dsum.get() : nullptr;
+  a.nverts = p.nverts;
   a.tiles = p.tiles.get();
   a.ntiles = p.ntiles;
   a.next_tile = next_tile;
@@ -622,6 +669,11 @@ void launch_wtile(const WtilePlan& p, int form, const double* coords, double* ou
   else if (form == F_STIFFNESS) go_wtile<F_STIFFNESS>(p, a, off, s);
   else go_wtile<F_HELMHOLTZ>(p, a, off, s);
   count_launch();
+  if (p.det) {
+    k_wt_dsum<<<ceil_div(p.nverts, 256), 256, 0, s>>>(p.dpos.get(), p.dptr.get(), p.dslots.get(), p.nverts, dsum.get(), out,
+                                                      accumulate ? 1 : 0);
+    count_launch();
+  }
   LG_LAUNCH_CHECK();
 }
 

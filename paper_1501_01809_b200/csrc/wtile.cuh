@@ -20,8 +20,9 @@
 // to rebuild.
 //
 // The plan declines -- the edge tiles run instead -- unless the structure of
-// etile.cuh holds and every edge's link is one ring or fan.  Deterministic
-// mode keeps the edge tiles (their fixed-order diagonal sums).
+// etile.cuh holds and every edge's link is one ring or fan.  In deterministic
+// mode the diagonal shares go to per-(edge, endpoint) slots that a second
+// kernel sums per vertex in edge order instead of by RED.
 #pragma once
 #include <cstdint>
 
@@ -37,10 +38,16 @@ struct WtilePlan {
   DevBuf<uint8_t> blob;  // per tile: row headers, link slots, in-row ranks, transposed positions
   DevBuf<int32_t> runs;  // coordinate-window runs [lo, hi)
   DevBuf<int32_t> dpos;  // position of every vertex diagonal (zeroed before a fresh assembly)
+  // deterministic mode: the edge rows store their diagonal shares in slots
+  // 2 (e - nverts) + endpoint and k_wt_dsum sums vertex v over dslots[dptr[v] .. dptr[v + 1])
+  bool det = false;
+  int nedges = 0;
+  DevBuf<int32_t> dptr, dslots;
 };
 
 struct WtileSpec {
   int tile_rows = 128, tile_slots = 1024, tile_runs = 32, max_link = 12;
+  bool det = false; // deterministic diagonals (WtilePlan::det)
 };
 
 // rows / xmap: the (locality-sorted) P2 cell->node map (ncells x 10) and
