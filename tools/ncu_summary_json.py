@@ -1,5 +1,5 @@
 """Rebuild profiles/ncu_summary.json from the round's `ncu --set full` raw CSV
-exports (profiles/r02/s5_*_raw.csv, the last evidence pass of the round): per config the dominant kernel's
+exports (profiles/r02/s6_*_raw.csv, the last evidence pass of the round): per config the dominant kernel's
 duration and DRAM bytes next to its algorithmic bytes (bench.py reads the
 C2 entry's traffic for roofline.traffic)."""
 import csv
@@ -9,8 +9,8 @@ import os
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ALG = {"c2_matrix": 100745240, "c1_residual": 14712864, "c3_residual": 103852584, "c3_matrix": 556384800,
        "c4_elasticity": 1076350560, "c5_blocks": 1279402064}
-SRC = {"c2_matrix": "s5_c2_ring", "c1_residual": "s5_cfg1", "c3_residual": "s5_cfg3r", "c3_matrix": "s5_cfg3m",
-       "c4_elasticity": "s5_cfg4", "c5_blocks": "s5_cfg5"}
+SRC = {"c2_matrix": "s6_c2_ring", "c1_residual": "s6_cfg1", "c3_residual": "s6_cfg3r", "c3_matrix": "s6_cfg3m",
+       "c4_elasticity": "s6_cfg4", "c5_blocks": "s6_cfg5"}
 out = {}
 for tag, stem in SRC.items():
     path = os.path.join(ROOT, "profiles", "r02", stem + "_raw.csv")
