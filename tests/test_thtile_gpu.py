@@ -248,3 +248,25 @@ def test_host_convention_blocks_run_fused_and_match():
     for h in hl2:
         ref = refs[id(h.loop.args[0].mat)]
         assert rel(h.outputs[0].numpy()[: len(ref)], ref) <= TOL
+
+
+@pytest.mark.parametrize("K", [3, 7, 40, 70])
+def test_high_valence_star_meshes(K):
+    """A star of K triangles around one vertex plus an outer ring (the meshes of
+    test_irregular_gpu): the centre vertex has K spokes -- one vertex fills a
+    tile at K = 40, and at K = 70 the star exceeds the walk's capacity, the
+    plan declines and the separate loops run.  All against the oracle."""
+    from tests.test_irregular_gpu import star2d
+    m = star2d(K)
+    cn, nn = configs.p2_map(m)
+    m.extra["p2"], m.extra["nn"] = cn, nn
+    loops, outs = _blocks(m, m.cv, cn, m.ncells)
+    L.execute_blocks(loops)
+    for o in outs:
+        o.zero()
+    before = capi.launch_count()
+    L.execute_blocks(loops)
+    launches = capi.launch_count() - before
+    assert launches == 1 if K <= 40 else launches >= 3
+    for o, r in zip(outs, oracle_blocks(m, m.cv, cn, m.ncells)):
+        assert rel(o.host_values(), r) <= TOL

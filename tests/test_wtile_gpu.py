@@ -97,3 +97,30 @@ def test_config3_matrix_takes_the_walk_tiles():
     cn = m.extra["p2"]
     ref = O.assemble_matrix(O.HELMHOLTZ, 2, 3, m.ncells, cn, 10, cn, 10, m.cv, m.coords, rp, ci, params=(configs.KAPPA,))
     assert rel(A.host_values(), ref) <= TOL
+
+
+@pytest.mark.parametrize("K", [3, 5, 12, 13, 40])
+@pytest.mark.parametrize("form", ["mass", "helmholtz"])
+def test_fans_around_one_edge(K, form):
+    """K tetrahedra around one edge (the meshes of test_irregular_gpu): the
+    centre edge's link is a ring of K vertices, every other edge has a fan of
+    one or two cells.  Up to 12 cells per link the walk tiles run; beyond, the
+    plan declines and the edge tiles take over.  All against the oracle."""
+    from tests.test_irregular_gpu import fan3d
+    m = fan3d(K)
+    cn, nn = configs.p2_map(m)
+    cells, verts, nodes = L.Set(m.ncells), L.Set(m.nv), L.Set(nn)
+    cvm, cnm = L.Map(cells, verts, 4, m.cv), L.Map(cells, nodes, 10, cn)
+    X = L.Dat(verts, 3)
+    X.set_values(m.coords)
+    A = L.Mat(L.build_sparsity(cnm, cnm))
+    params = (1.7,) if form == "helmholtz" else ()
+    loop = L.Parloop(L.kernel(f"{form}_p2_tet", *params), cells, [L.arg(A, L.INC, cnm, cnm), L.arg(X, L.READ, cvm)])
+    if K <= 12:
+        os.environ["LOAM_GPU_WT_REQUIRE"] = "1"
+    L.execute(loop)
+    rp, ci = A.sparsity.host()
+    ref = O.assemble_matrix(KINDS[form], 2, 3, m.ncells, cn, 10, cn, 10, m.cv, m.coords, rp, ci, params=params)
+    assert rel(A.host_values(), ref) <= TOL
+    L.execute(loop)
+    assert rel(A.host_values(), 2 * ref) <= TOL
