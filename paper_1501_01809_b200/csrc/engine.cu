@@ -3004,7 +3004,9 @@ std::shared_ptr<FastPlan> build_fast_plan(const Entry& k, int n, const loam_arg_
       if (!std::getenv("LOAM_GPU_NO_LTILE")) { // manifold meshes: a block walks its edge's link
         LtileSpec ls;
         ls.tile_nodes = env_int("LOAM_GPU_LT_NODES", ls.tile_nodes);
-        if (build_ltile(P->lt, ls, n, R.v.target, srows.v.get(), sx.v.get(), X->target_size, P->pp, sp->row_ptr,
+        // (the coordinate map IS the node map for vector P1: one sorted copy serves both)
+        const int32_t* lx = (X->values == R.v.v && X->arity == R.v.arity) ? srows.v.get() : sx.v.get();
+        if (build_ltile(P->lt, ls, n, R.v.target, srows.v.get(), lx, X->target_size, P->pp, sp->row_ptr,
                         sp->nnz, s)) {
           plan_tick("link tiles", s);
           P->use_ltile = true;

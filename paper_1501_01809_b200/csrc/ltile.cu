@@ -38,17 +38,20 @@ bool build_ltile(LtilePlan& out, const LtileSpec& sp, int ncells, int nnodes, co
   if (pp.nrn != kNV || pp.ncn != kNV || nnz >= (int64_t(1) << 31) || ncells == 0) return false;
   constexpr int NT = kLtConsumers;
   const int64_t np = pp.npairs;
-  auto hrows = host_array<int32_t>((size_t)ncells * kNV), hx = host_array<int32_t>((size_t)ncells * kNV),
+  // (sorted_x == sorted_rows: the coordinate map is the node map -- one download serves both)
+  const bool same_x = sorted_x == sorted_rows;
+  auto hrows = host_array<int32_t>((size_t)ncells * kNV), hx_own = host_array<int32_t>(same_x ? 0 : (size_t)ncells * kNV),
        hpairs = host_array<int32_t>(np), hp = host_array<int32_t>(nnodes + 1);
   auto hrank = host_array<uint8_t>((size_t)np * kNV);
   auto hrp = host_array<int64_t>((size_t)nnodes * 3 + 1);
   parallel_d2h({{hrows.data(), sorted_rows, sizeof(int32_t) * hrows.size()},
-                {hx.data(), sorted_x, sizeof(int32_t) * hx.size()},
+                {hx_own.data(), sorted_x, sizeof(int32_t) * hx_own.size()},
                 {hpairs.data(), pp.pairs.get(), sizeof(int32_t) * (size_t)np},
                 {hp.data(), pp.ptr.get(), sizeof(int32_t) * (size_t)(nnodes + 1)},
                 {hrank.data(), pp.ranks.get(), hrank.size()},
                 {hrp.data(), row_ptr, sizeof(int64_t) * hrp.size()}},
                s);
+  const int32_t* hx = same_x ? hrows.data() : hx_own.data();
   plan_tick("ltile: D2H", s);
   std::vector<int64_t> nptr(nnodes + 1); // node-level pattern offsets of the 3x3-blocked CSR
   for (int i = 0; i <= nnodes; ++i) nptr[i] = hrp[(size_t)3 * i] / 9;
