@@ -1020,6 +1020,7 @@ bool build_sparsity_rows(const MapView& rows, const MapView& cols, int rd, int c
   const int n = rows.n, nr = rows.target;
   if (n == 0 || nr == 0 || (int64_t)n * rows.arity >= (int64_t(1) << 31)) return false;
   const int64_t np = (int64_t)n * rows.arity;
+  plan_tick("sparsity: start", s);
   DevBuf<int32_t> pptr(nr + 1, s), pcells(np, s), cursor(nr + 1, s);
   LG_CUDA(cudaMemsetAsync(cursor.get(), 0, sizeof(int32_t) * (nr + 1), s));
   k_count<<<ceil_div(np, kTPB), kTPB, 0, s>>>(rows.v, np, cursor.get());
@@ -1030,6 +1031,7 @@ bool build_sparsity_rows(const MapView& rows, const MapView& cols, int rd, int c
   k_inv_fill<<<ceil_div(np, kTPB), kTPB, 0, s>>>(rows.v, np, rows.arity, pptr.get(), cursor.get(), pcells.get());
   count_launch(2);
   LG_LAUNCH_CHECK();
+  plan_tick("sparsity: node -> cell inverse", s);
   DevBuf<int32_t> counts(nr + 1, s);
   DevBuf<int64_t> node_off(nr + 1, s);
   DevBuf<int> over(1, s);
@@ -1047,6 +1049,7 @@ bool build_sparsity_rows(const MapView& rows, const MapView& cols, int rd, int c
   LG_CUDA(cudaMemcpyAsync(&hover, over.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaMemcpyAsync(&nu, node_off.get() + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaStreamSynchronize(s));
+  plan_tick("sparsity: row counts + scan", s);
   if (hover) return false;
   const int64_t nrows = (int64_t)nr * rd;
   const int64_t total = nu * rd * cd;
@@ -1058,6 +1061,7 @@ bool build_sparsity_rows(const MapView& rows, const MapView& cols, int rd, int c
                                                      nullptr, nullptr, *row_ptr, rd, cd, *col_idx);
   count_launch(2);
   LG_LAUNCH_CHECK();
+  plan_tick("sparsity: columns", s);
   *nnz = total;
   return true;
 }
